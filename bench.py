@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""SVLF B200 benchmark (BASELINE.json metric: rendered rays/s at 1600x1600).
+
+One step = render one full 1600x1600 frame of the C2 workload (RTMV-shaped
+4-object scene, octree depth 8 from 100 back-projected 400^2 hemisphere depth
+maps, init_model seed 1) per GPU. N GPUs = one process per GPU (torchrun),
+octree and model replicated, each rank renders its own frame: weak scaling,
+no data-path collective. Timing: CUDA events on the
+library's stream around each step, L2 flushed (256 MiB write) between steps
+(the model is L2-sized), max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--precision bf16|fp32] [--objects 4|20]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+FLOP_PER_HIT = 110_848  # f_T 17,408 MAC + f_C 38,016 MAC, x2
+BYTES_PER_RAY_OUT = 20  # rgb 12 + alpha 4 + depth 4
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def workload(objects: int):
+    import paper_2205_07058_b200.synthetic as S
+
+    sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=objects, n_views=100, view_res=400, res=256,
+                                                   dilation=1, width=1600)
+    return pts, res, dil, cam, W, H
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if os.environ.get("SVLF_BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+    return world, rank, local, dist
+
+
+def max_over_ranks(x: float, dist, device):
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1):
+    """Reference render_frame (oracle/_ref, reference flags, all host threads) on
+    the same octree/model/camera; falls back to the C restatement."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    if O.reference_available():
+        R = O.Reference()
+        kind = "reference"
+        tree = R.tree_build(pts, res, dil)
+        model = R.init_model(tree, 1)
+        hm = R._with_model(tree, model)
+        secs = []
+        for _ in range(frames):
+            s, st = R.time_render(hm, cam, W, H, parallel=True)
+            secs.append(s)
+        R.lib.ref_model_free(hm)
+        cores = R.thread_count()
+    else:
+        R = O.Oracle()
+        kind = "port"
+        tree = R.tree_build(pts, res, dil)
+        model = R.init_model(tree, 1)
+        secs = []
+        for _ in range(frames):
+            t0 = time.perf_counter()
+            R.render_frame(tree, model, cam, W, H)
+            secs.append(time.perf_counter() - t0)
+        cores = os.cpu_count()
+    s = min(secs)
+    return {"value": round(W * H / s / 1e6, 4), "unit": "Mrays/s", "cores": cores, "kind": kind,
+            "sample": f"{frames} full {W}x{H} frame(s) of the same workload, render_frame, best of {frames}",
+            "seconds_per_frame": round(s, 3)}
+
+
+def run_reference(args):
+    world, rank, local, dist = dist_init()
+    if rank != 0:
+        return
+    pts, res, dil, cam, W, H = workload(args.objects)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    if O.reference_available():
+        R = O.Reference()
+        kind = "reference"
+        tree = R.tree_build(pts, res, dil)
+        model = R.init_model(tree, 1)
+        hm = R._with_model(tree, model)
+
+        def step():
+            return R.time_render(hm, cam, W, H, parallel=True)[0]
+        cores = R.thread_count()
+    else:
+        R = O.Oracle()
+        kind = "port"
+        tree = R.tree_build(pts, res, dil)
+        model = R.init_model(tree, 1)
+
+        def step():
+            t0 = time.perf_counter()
+            R.render_frame(tree, model, cam, W, H)
+            return time.perf_counter() - t0
+        cores = os.cpu_count()
+    for _ in range(args.warmup):
+        step()
+    secs = [step() for _ in range(args.steps)]
+    total = sum(secs)
+    value = args.steps * W * H / total / 1e6
+    line = {"impl": "reference", "metric": "rendered rays/s at 1600x1600 (C2)", "value": round(value, 4),
+            "unit": "Mrays/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 decoders / f64 geometry", "data": "synthetic",
+            "config": {"workload": f"C2: RTMV-shaped {args.objects}-object scene, octree depth 8, one {W}x{H} frame",
+                       "frames_per_step": 1},
+            "cpu_baseline": {"value": round(value, 4), "unit": "Mrays/s", "cores": cores, "kind": kind,
+                             "sample": f"{args.steps} full {W}x{H} frames (render_frame, all host threads)"},
+            "e2e": {"value": round(value, 4), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default=os.environ.get("SVLF_BENCH_PRECISION", "auto"),
+                    choices=["auto", "bf16", "fp32"])
+    ap.add_argument("--objects", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    world, rank, local, dist = dist_init()
+    import torch
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    import paper_2205_07058_b200 as P
+
+    t_gen = time.perf_counter()
+    pts, res, dil, cam, W, H = workload(args.objects)
+    t_gen = time.perf_counter() - t_gen
+    ctx = P.Context(local)
+    stream = torch.cuda.Stream(device)
+    ctx.set_stream(stream.cuda_stream)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    camera = P.Camera.from_record(cam, W, H)
+
+    precision = args.precision
+    if precision == "auto":
+        try:
+            P.render_frame(model, P.Camera.from_record(cam, 64, 64), precision="bf16")
+            precision = "bf16"
+        except RuntimeError:
+            precision = "fp32"
+
+    n = W * H
+    d_rgb = torch.empty(n * 3, dtype=torch.float32, device=device)
+    d_alpha = torch.empty(n, dtype=torch.float32, device=device)
+    d_depth = torch.empty(n, dtype=torch.float32, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    def step(stats=None):
+        P.render_frame_device(model, camera, d_rgb.data_ptr(), d_alpha.data_ptr(), d_depth.data_ptr(),
+                              stats=stats, precision=precision)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        stats = P.RenderStats()
+        launches0 = P.Context.kernel_launches()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        decode_ms = []
+        barrier(dist)
+        torch.cuda.synchronize(device)
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                step(stats)
+                ev[i][1].record(stream)
+                decode_ms.append(ctx.last_timings())
+            stream.synchronize()
+        torch.cuda.synchronize(device)
+        barrier(dist)
+        launches = P.Context.kernel_launches() - launches0
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = max_over_ranks(sum(step_ms), dist, device)
+    ms_per_step = total_ms / args.steps
+    value = world * n / (ms_per_step * 1e-3) / 1e6
+
+    # ---- e2e: public host-buffer API (D2H of the frame inside the timed region)
+    camera_bytes = 20 * 8 + 8
+    e2e_ms = []
+    for i in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        torch.cuda.synchronize(device)
+        barrier(dist)
+        t0 = time.perf_counter()
+        P.render_frame(model, camera, precision=precision)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step = max_over_ranks(statistics.median(e2e_ms), dist, device)
+    e2e_value = world * n / (e2e_step * 1e-3) / 1e6
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_kind = load_peaks()
+    hits = stats.traversal_hits / args.steps
+    dec = [t["decode_ms"] for t in decode_ms]
+    dec_ms = statistics.median(dec)
+    flops = hits * FLOP_PER_HIT
+    achieved_tflops = flops / (dec_ms * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
+    stage = {k: round(statistics.median(t[k] for t in decode_ms), 4)
+             for k in ("traverse_ms", "emit_ms", "decode_ms", "composite_ms")}
+    line = {
+        "metric": "rendered rays/s at 1600x1600 (C2)",
+        "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": f"{precision} decoders (fp32 accumulate) / f64 geometry", "data": "synthetic",
+        "config": {"workload": f"C2: RTMV-shaped {args.objects}-object scene (make_random_scene(7,{args.objects})), "
+                               f"octree depth 8 (res 256, dilation 1) from 100 hemisphere 400^2 depth maps, "
+                               f"one {W}x{H} frame per GPU per step, init_model seed 1",
+                   "leaves": int(tree.leaf_count), "vertices": int(tree.vertex_count),
+                   "hits_per_ray": round(hits / n, 4),
+                   "foreground_fraction": round(stats.rays_with_hits / args.steps / n, 4),
+                   "precision": precision, "parallelism": f"replicated octree, {world} rank(s), one frame each",
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "input_gen_seconds": round(t_gen, 1)},
+        "stages_ms": stage,
+        "roofline": {"bound": "tensor", "kernel": f"decode_{precision}", "achieved": round(achieved_tflops, 3),
+                     "peak": peak, "unit": "TFLOP/s", "frac": round(achieved_tflops / peak, 5),
+                     "traffic": None, "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)",
+                     "algorithmic": f"{FLOP_PER_HIT} FLOP/hit x {int(hits)} hits per launch"},
+        "e2e": {"value": round(e2e_value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": camera_bytes,
+                "d2h_bytes_per_step": n * BYTES_PER_RAY_OUT,
+                "api": "paper_2205_07058_b200.render_frame (C ABI svlf_render_frame, host buffers)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1)
+        except Exception as e:  # reported, never silently dropped
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

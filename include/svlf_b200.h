@@ -1,0 +1,210 @@
+/*
+ * svlf_b200.h -- C ABI of the B200-native SVLF render/train path.
+ *
+ * This is the drop-in boundary. The reference (/root/reference/proj) is a C++
+ * static library (svlf_core, src/CMakeLists.txt:1-18) with no FFI; every entry
+ * point below replaces one reference interface, cited per function. The C++
+ * API in include/svlf/ headers (same names and signatures as the reference
+ * headers) is a thin shim over these calls, and the Python package
+ * paper_2205_07058_b200 binds them with ctypes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no exceptions cross the ABI. Every call returns
+ *    an svlf_status; on failure svlf_last_error() (thread-local) holds the
+ *    reference's exception message, e.g. "empty occupancy", "tangent ray",
+ *    "point not in voxel", "surface point outside voxel". The C++ shim
+ *    rethrows the same exception type with the same message
+ *    (SVLF_ERR_INVALID_ARGUMENT -> std::invalid_argument, SVLF_ERR_RUNTIME ->
+ *    std::runtime_error, SVLF_ERR_OUT_OF_RANGE -> std::out_of_range).
+ *  - Geometry is fp64, features/decoders fp32 (reference geometry.hpp:8).
+ *  - Host-pointer calls are synchronous: results are in the caller's buffers
+ *    on return. *_device calls take device pointers and are asynchronous on
+ *    the context stream (svlf_ctx_synchronize to wait).
+ *  - Flat decoder layout: per layer l, W_l row-major [out][in] then b_l
+ *    (reference include/svlf/mlp.hpp:50-53). f_T 134->128->2 (17,538 floats),
+ *    f_C 38->128->128->128->3 (38,403 floats).
+ *  - There is no CPU fallback: a missing or failing CUDA device is an error.
+ */
+#ifndef SVLF_B200_H
+#define SVLF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVLF_ABI_VERSION 1
+#define SVLF_FEAT_T_DIM 64   /* model.hpp:13 kThicknessFeatDim */
+#define SVLF_FEAT_C_DIM 32   /* model.hpp:14 kColorFeatDim */
+#define SVLF_DEC_T_SIZE 17538
+#define SVLF_DEC_C_SIZE 38403
+
+typedef enum svlf_status {
+    SVLF_OK = 0,
+    SVLF_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    SVLF_ERR_RUNTIME = 2,          /* std::runtime_error */
+    SVLF_ERR_OUT_OF_RANGE = 3,     /* std::out_of_range */
+    SVLF_ERR_CUDA = 4,             /* device failure (no reference analogue) */
+    SVLF_ERR_CAPACITY = 5          /* caller buffer too small; required size reported */
+} svlf_status;
+
+/* Decoder arithmetic for render: FP32 = CUDA-core fp32 in the reference's
+ * accumulation order (parity: max-abs <= 1e-3); BF16 = tcgen05 tensor cores,
+ * bf16 operands with fp32 accumulation in TMEM (parity: PSNR delta <= 0.05 dB). */
+typedef enum svlf_precision { SVLF_PRECISION_FP32 = 0, SVLF_PRECISION_BF16 = 1 } svlf_precision;
+
+/* reference LossMode (src/train.cpp:37): stage 1 = SURFACE, stages 2-3 = VOLUMETRIC */
+typedef enum svlf_loss_mode { SVLF_LOSS_SURFACE = 0, SVLF_LOSS_VOLUMETRIC = 1 } svlf_loss_mode;
+
+typedef struct svlf_ctx svlf_ctx;
+typedef struct svlf_octree svlf_octree;
+typedef struct svlf_model svlf_model;
+
+/* GridConfig, include/svlf/octree.hpp:13-19 */
+typedef struct svlf_grid {
+    uint32_t resolution;
+    uint32_t dilation;
+    double lo[3];
+    double hi[3];
+} svlf_grid;
+
+/* Camera, include/svlf/camera.hpp:12-33 (row-major camera_to_world) */
+typedef struct svlf_camera {
+    double fx, fy, cx, cy;
+    double camera_to_world[16];
+    uint32_t width, height;
+} svlf_camera;
+
+/* RenderStats, include/svlf/render.hpp:94-100 (additive counters) */
+typedef struct svlf_render_stats {
+    long long rays, rays_with_hits, traversal_hits, thickness_queries, color_queries;
+} svlf_render_stats;
+
+/* LossWeights, include/svlf/train.hpp:43-48 */
+typedef struct svlf_loss_weights {
+    double eta, tau, empty, alpha;
+} svlf_loss_weights;
+
+/* LossStats, include/svlf/train.hpp:50-54 (additive counters) */
+typedef struct svlf_loss_stats {
+    long long rays, skipped_rays, eta_skipped;
+} svlf_loss_stats;
+
+typedef struct svlf_octree_info {
+    int leaf_level;
+    uint32_t vertex_count;
+    size_t leaf_count;
+    size_t dropped_points;
+    double cell_size;
+    size_t level_size[22];
+} svlf_octree_info;
+
+/* Per-launch device timings of the last render/train call (CUDA events on the
+ * context stream), milliseconds. */
+typedef struct svlf_timings {
+    float traverse_ms, emit_ms, decode_ms, composite_ms, backward_ms, adam_ms, total_ms;
+    long long hits;
+} svlf_timings;
+
+/* ---- context -------------------------------------------------------- */
+const char* svlf_last_error(void);
+int svlf_abi_version(void);
+svlf_status svlf_ctx_create(int device, svlf_ctx** out);
+svlf_status svlf_ctx_destroy(svlf_ctx* ctx);
+svlf_status svlf_ctx_synchronize(svlf_ctx* ctx);
+/* Run the context's work on an external cudaStream_t (e.g. a framework's
+ * current stream, so its CUDA events time this library); NULL restores the
+ * context's own stream. */
+svlf_status svlf_ctx_set_stream(svlf_ctx* ctx, void* cuda_stream);
+svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out);
+/* Count of this library's kernel launches on the context since creation. */
+long long svlf_ctx_kernel_launches(const svlf_ctx* ctx);
+
+/* ---- octree: SparseOctree::build / from_leaves (octree.hpp:47,82; src/octree.cpp:30-142)
+ * ctx may be NULL: the octree is then host-only and is uploaded to the device
+ * of the first context that renders/traverses with it. */
+svlf_status svlf_octree_build(svlf_ctx* ctx, const svlf_grid* grid, const double* points_xyz,
+                              size_t n_points, svlf_octree** out);
+svlf_status svlf_octree_from_leaves(svlf_ctx* ctx, const svlf_grid* grid, const uint64_t* leaf_codes,
+                                    size_t n_leaves, svlf_octree** out);
+svlf_status svlf_octree_destroy(svlf_octree* tree);
+svlf_status svlf_octree_get_info(const svlf_octree* tree, svlf_octree_info* out);
+svlf_status svlf_octree_level_codes(const svlf_octree* tree, int level, uint64_t* out);
+/* corner_vertices for every leaf, leaf-code order, 8 ids per leaf (octree.hpp:69-71) */
+svlf_status svlf_octree_corner_ids(const svlf_octree* tree, uint32_t* out);
+
+/* ---- traversal: SparseOctree::traverse (octree.hpp:75-78; src/octree.cpp:185-235)
+ * Batched: rays are n x (origin xyz, unit dir xyz). offsets[n+1] is the CSR
+ * row pointer. Hits (voxel_id = leaf Morton code, t_in, t_out, and x1/x2 as
+ * 6 doubles when x12 is non-null) are written only if the total fits
+ * `capacity`; *total always receives the required count (SVLF_ERR_CAPACITY
+ * otherwise). Bit-exact with the reference built without FMA contraction. */
+svlf_status svlf_traverse(svlf_ctx* ctx, const svlf_octree* tree, const double* rays, size_t n,
+                          uint64_t* offsets, size_t capacity, uint64_t* voxel_ids, double* t_in,
+                          double* t_out, double* x12, size_t* total);
+
+/* ---- model: SvlfModel + ModelAdam (model.hpp:16-34,80-90) ----------- */
+svlf_status svlf_model_create(svlf_ctx* ctx, const svlf_octree* tree, svlf_model** out);
+svlf_status svlf_model_destroy(svlf_model* model);
+/* init_model(octree, seed), src/model.cpp:15-28 (bit-identical parameters) */
+svlf_status svlf_model_init(svlf_model* model, uint64_t seed);
+svlf_status svlf_model_set_params(svlf_model* model, const float* feat_t, const float* feat_c,
+                                  const float* dec_t, const float* dec_c);
+svlf_status svlf_model_get_params(svlf_model* model, float* feat_t, float* feat_c, float* dec_t,
+                                  float* dec_c);
+/* Gradients of the last svlf_loss_grads / svlf_train_step call (sums over rays). */
+svlf_status svlf_model_get_grads(svlf_model* model, float* feat_t, float* feat_c, float* dec_t,
+                                 float* dec_c);
+/* Adam state, tensor order: feat_t, feat_c, then per layer W,b of f_T, then
+ * per layer W,b of f_C (ModelAdam, model.hpp:83-90). steps[] has 14 entries. */
+svlf_status svlf_model_get_adam(svlf_model* model, float* m_all, float* v_all, uint64_t* steps);
+svlf_status svlf_model_set_adam(svlf_model* model, const float* m_all, const float* v_all,
+                                const uint64_t* steps);
+size_t svlf_model_param_count(const svlf_model* model);
+
+/* ---- render: render_frame(model, camera, out, stats, background) (render.hpp:104-105;
+ * src/render.cpp:209-247). Host buffers: rgb W*H*3 interleaved, alpha W*H,
+ * depth W*H (0 where alpha <= 1e-4). background may be NULL (black). stats may
+ * be NULL; counters are added to it. */
+svlf_status svlf_render_frame(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
+                              const float* background, svlf_precision precision, float* rgb,
+                              float* alpha, float* depth, svlf_render_stats* stats);
+/* Same with DEVICE output buffers, asynchronous (inputs resident in HBM). */
+svlf_status svlf_render_frame_device(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
+                                     const float* background, svlf_precision precision,
+                                     float* d_rgb, float* d_alpha, float* d_depth,
+                                     svlf_render_stats* stats);
+/* Sub-rectangle of rows [row0, row0+rows) of the camera's image (tile
+ * sharding across ranks); output buffers hold W*rows pixels. Device buffers. */
+svlf_status svlf_render_rows_device(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
+                                    uint32_t row0, uint32_t rows, const float* background,
+                                    svlf_precision precision, float* d_rgb, float* d_alpha,
+                                    float* d_depth, svlf_render_stats* stats);
+/* Arbitrary rays (render_ray per ray, render.hpp:75), host buffers. */
+svlf_status svlf_render_rays(svlf_ctx* ctx, svlf_model* model, const double* rays, size_t n,
+                             const float* background, svlf_precision precision, float* rgb,
+                             float* alpha, float* depth, svlf_render_stats* stats);
+
+/* ---- train: one optimizer step over a ray batch (src/train.cpp:443-479 body:
+ * loss_chunk over the batch, gradient sum, adam_model_step). Rays n x 6,
+ * c_gt n x 3, depth_gt n (Euclidean, 0 = background), alpha_gt n (0/1).
+ * Surface mode drops rays with no resolved surface voxel (counted as skipped).
+ * loss_sum = sum of per-ray losses (the reference logs loss_sum / n). */
+svlf_status svlf_train_step(svlf_ctx* ctx, svlf_model* model, const double* rays,
+                            const float* c_gt, const double* depth_gt, const uint8_t* alpha_gt,
+                            size_t n, svlf_loss_mode mode, int color_frozen, float lr,
+                            const svlf_loss_weights* lw, svlf_loss_stats* stats,
+                            double* loss_sum);
+/* Loss and summed gradients only (no Adam), the gradient oracle entry for
+ * surface_loss / volumetric_loss summed over rays (train.hpp:60-71). */
+svlf_status svlf_loss_grads(svlf_ctx* ctx, svlf_model* model, const double* rays,
+                            const float* c_gt, const double* depth_gt, const uint8_t* alpha_gt,
+                            size_t n, svlf_loss_mode mode, int color_frozen,
+                            const svlf_loss_weights* lw, svlf_loss_stats* stats, double* loss_sum);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVLF_B200_H */

@@ -1,0 +1,554 @@
+"""B200-native SVLF per-ray render + train path (arXiv 2205.07058).
+
+Python mirror of the reference's C++ interface for this path, over the C ABI
+in include/svlf_b200.h (libsvlf_b200.so, built in-tree for sm_100a):
+
+    SparseOctree.build(points, GridConfig) / SparseOctree.from_leaves(...)
+        -> reference SparseOctree::build / from_leaves (include/svlf/octree.hpp:47,82)
+    octree.traverse(rays)                  -> SparseOctree::traverse (octree.hpp:75-78), batched
+    Model(octree).init(seed)               -> init_model (include/svlf/model.hpp:80)
+    render_frame(model, camera, ...)       -> render_frame (include/svlf/render.hpp:104-105)
+    train_step(model, batch, ...)          -> the per-frame body of train() (src/train.cpp:443-479)
+    loss_grads(model, batch, ...)          -> surface_loss / volumetric_loss summed (train.hpp:60-71)
+
+Errors re-raise the reference's exception type and message (ValueError for
+std::invalid_argument, RuntimeError for std::runtime_error, IndexError for
+std::out_of_range). There is no CPU fallback: without the built library or a
+CUDA device every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "GridConfig", "Camera", "LossWeights", "RenderStats", "LossStats", "Context", "SparseOctree",
+    "Model", "render_frame", "render_rays", "train_step", "loss_grads", "library_path", "load_library",
+    "DEC_T_SIZE", "DEC_C_SIZE", "SvlfCudaError",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+DEC_T_SIZE = 17538
+DEC_C_SIZE = 38403
+FEAT_T_DIM = 64
+FEAT_C_DIM = 32
+
+
+class SvlfCudaError(RuntimeError):
+    """Device failure (no reference analogue)."""
+
+
+class SvlfCapacityError(RuntimeError):
+    pass
+
+
+# ---- ABI structs -----------------------------------------------------------
+class _Grid(C.Structure):
+    _fields_ = [("resolution", C.c_uint32), ("dilation", C.c_uint32), ("lo", C.c_double * 3),
+                ("hi", C.c_double * 3)]
+
+
+class _Camera(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("camera_to_world", C.c_double * 16), ("width", C.c_uint32), ("height", C.c_uint32)]
+
+
+class _RenderStats(C.Structure):
+    _fields_ = [(n, C.c_longlong) for n in
+                ("rays", "rays_with_hits", "traversal_hits", "thickness_queries", "color_queries")]
+
+
+class _LossWeights(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("eta", "tau", "empty", "alpha")]
+
+
+class _LossStats(C.Structure):
+    _fields_ = [(n, C.c_longlong) for n in ("rays", "skipped_rays", "eta_skipped")]
+
+
+class _OctreeInfo(C.Structure):
+    _fields_ = [("leaf_level", C.c_int), ("vertex_count", C.c_uint32), ("leaf_count", C.c_size_t),
+                ("dropped_points", C.c_size_t), ("cell_size", C.c_double), ("level_size", C.c_size_t * 22)]
+
+
+class _Timings(C.Structure):
+    _fields_ = [(n, C.c_float) for n in
+                ("traverse_ms", "emit_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms", "total_ms")] + \
+               [("hits", C.c_longlong)]
+
+
+# ---- public value types (reference structs) ----------------------------------
+@dataclass
+class GridConfig:
+    """include/svlf/octree.hpp:13-19."""
+    resolution: int = 128
+    lo: tuple = (0.0, 0.0, 0.0)
+    hi: tuple = (1.0, 1.0, 1.0)
+    dilation: int = 1
+
+    def _c(self):
+        return _Grid(self.resolution, self.dilation, (C.c_double * 3)(*self.lo), (C.c_double * 3)(*self.hi))
+
+
+@dataclass
+class Camera:
+    """include/svlf/camera.hpp:12-33; camera_to_world row-major 4x4."""
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    camera_to_world: tuple
+    width: int
+    height: int
+
+    @staticmethod
+    def from_record(rec, width, height):
+        """rec = (fx, fy, cx, cy, c2w[16]) as produced by synthetic/oracle helpers."""
+        rec = [float(x) for x in rec]
+        return Camera(rec[0], rec[1], rec[2], rec[3], tuple(rec[4:20]), int(width), int(height))
+
+    def record(self):
+        return np.array([self.fx, self.fy, self.cx, self.cy, *self.camera_to_world], dtype=np.float64)
+
+    def _c(self):
+        return _Camera(self.fx, self.fy, self.cx, self.cy, (C.c_double * 16)(*self.camera_to_world),
+                       self.width, self.height)
+
+
+@dataclass
+class LossWeights:
+    """include/svlf/train.hpp:43-48."""
+    eta: float = 1.0
+    tau: float = 0.01
+    empty: float = 0.01
+    alpha: float = 0.1
+
+    def _c(self):
+        return _LossWeights(self.eta, self.tau, self.empty, self.alpha)
+
+
+@dataclass
+class RenderStats:
+    """include/svlf/render.hpp:94-100."""
+    rays: int = 0
+    rays_with_hits: int = 0
+    traversal_hits: int = 0
+    thickness_queries: int = 0
+    color_queries: int = 0
+
+
+@dataclass
+class LossStats:
+    """include/svlf/train.hpp:50-54."""
+    rays: int = 0
+    skipped_rays: int = 0
+    eta_skipped: int = 0
+
+
+# ---- library loading -----------------------------------------------------------
+_LIB = None
+
+
+def library_path() -> str:
+    return os.path.join(HERE, "libsvlf_b200.so")
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def load_library():
+    """Load libsvlf_b200.so (fails loudly when it is missing: no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = library_path()
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run __graft_entry__.build() (make -C paper_2205_07058_b200/csrc)")
+    L = C.CDLL(path)
+    vp, sz, st = C.c_void_p, C.c_size_t, C.c_int
+    sigs = {
+        "svlf_last_error": ([], C.c_char_p),
+        "svlf_abi_version": ([], C.c_int),
+        "svlf_ctx_create": ([C.c_int, C.POINTER(vp)], st),
+        "svlf_ctx_destroy": ([vp], st),
+        "svlf_ctx_synchronize": ([vp], st),
+        "svlf_ctx_set_stream": ([vp, vp], st),
+        "svlf_ctx_last_timings": ([vp, C.POINTER(_Timings)], st),
+        "svlf_ctx_kernel_launches": ([vp], C.c_longlong),
+        "svlf_octree_build": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
+        "svlf_octree_from_leaves": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
+        "svlf_octree_destroy": ([vp], st),
+        "svlf_octree_get_info": ([vp, C.POINTER(_OctreeInfo)], st),
+        "svlf_octree_level_codes": ([vp, C.c_int, vp], st),
+        "svlf_octree_corner_ids": ([vp, vp], st),
+        "svlf_traverse": ([vp, vp, vp, sz, vp, sz, vp, vp, vp, vp, C.POINTER(sz)], st),
+        "svlf_model_create": ([vp, vp, C.POINTER(vp)], st),
+        "svlf_model_destroy": ([vp], st),
+        "svlf_model_init": ([vp, C.c_uint64], st),
+        "svlf_model_set_params": ([vp, vp, vp, vp, vp], st),
+        "svlf_model_get_params": ([vp, vp, vp, vp, vp], st),
+        "svlf_model_get_grads": ([vp, vp, vp, vp, vp], st),
+        "svlf_model_get_adam": ([vp, vp, vp, vp], st),
+        "svlf_model_set_adam": ([vp, vp, vp, vp], st),
+        "svlf_model_param_count": ([vp], sz),
+        "svlf_render_frame": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
+        "svlf_render_frame_device": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp,
+                                      C.POINTER(_RenderStats)], st),
+        "svlf_render_rows_device": ([vp, vp, C.POINTER(_Camera), C.c_uint32, C.c_uint32, vp, C.c_int, vp, vp, vp,
+                                     C.POINTER(_RenderStats)], st),
+        "svlf_render_rays": ([vp, vp, vp, sz, vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
+        "svlf_train_step": ([vp, vp, vp, vp, vp, vp, sz, C.c_int, C.c_int, C.c_float, C.POINTER(_LossWeights),
+                             C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
+        "svlf_loss_grads": ([vp, vp, vp, vp, vp, vp, sz, C.c_int, C.c_int, C.POINTER(_LossWeights),
+                             C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _LIB = L
+    return L
+
+
+def _check(status):
+    if status == 0:
+        return
+    msg = _LIB.svlf_last_error().decode()
+    if status == 1:
+        raise ValueError(msg)
+    if status == 3:
+        raise IndexError(msg)
+    if status == 4:
+        raise SvlfCudaError(msg)
+    if status == 5:
+        raise SvlfCapacityError(msg)
+    raise RuntimeError(msg)
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.reshape(shape) if shape is not None else a
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# ---- objects ------------------------------------------------------------------
+class Context:
+    """One CUDA device + stream + scratch arenas (svlf_ctx)."""
+
+    def __init__(self, device: int = 0):
+        L = load_library()
+        h = C.c_void_p()
+        _check(L.svlf_ctx_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _LIB.svlf_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(_LIB.svlf_ctx_synchronize(self._h))
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(_LIB.svlf_ctx_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def last_timings(self) -> dict:
+        t = _Timings()
+        _check(_LIB.svlf_ctx_last_timings(self._h, C.byref(t)))
+        return {n: getattr(t, n) for n, _ in _Timings._fields_}
+
+    @staticmethod
+    def kernel_launches() -> int:
+        return int(load_library().svlf_ctx_kernel_launches(None))
+
+
+_DEFAULT_CTX = None
+
+
+def default_context() -> Context:
+    global _DEFAULT_CTX
+    if _DEFAULT_CTX is None:
+        _DEFAULT_CTX = Context(0)
+    return _DEFAULT_CTX
+
+
+class SparseOctree:
+    """Host-built octree with a device mirror (reference SparseOctree)."""
+
+    def __init__(self, handle, ctx: Context, grid: GridConfig):
+        self._h = handle
+        self.ctx = ctx
+        self.config = grid
+        info = _OctreeInfo()
+        _check(_LIB.svlf_octree_get_info(self._h, C.byref(info)))
+        self.leaf_level = info.leaf_level
+        self.vertex_count = info.vertex_count
+        self.leaf_count = info.leaf_count
+        self.dropped_points = info.dropped_points
+        self.cell_size = info.cell_size
+        self._level_sizes = [info.level_size[i] for i in range(self.leaf_level + 1)]
+
+    @staticmethod
+    def build(points, grid: GridConfig, ctx: Context | None = None) -> "SparseOctree":
+        """Host build (no device needed); uploaded on first use by a context."""
+        load_library()
+        pts = _f64(points).reshape(-1, 3)
+        h = C.c_void_p()
+        g = grid._c()
+        _check(_LIB.svlf_octree_build(ctx.handle if ctx else None, C.byref(g), _dp(pts), pts.shape[0],
+                                      C.byref(h)))
+        return SparseOctree(h, ctx, grid)
+
+    @staticmethod
+    def from_leaves(codes, grid: GridConfig, ctx: Context | None = None) -> "SparseOctree":
+        load_library()
+        c = np.ascontiguousarray(codes, dtype=np.uint64)
+        h = C.c_void_p()
+        g = grid._c()
+        _check(_LIB.svlf_octree_from_leaves(ctx.handle if ctx else None, C.byref(g), _dp(c), c.size,
+                                            C.byref(h)))
+        return SparseOctree(h, ctx, grid)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.svlf_octree_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def level_codes(self, level: int) -> np.ndarray:
+        out = np.zeros(self._level_sizes[level], np.uint64)
+        _check(_LIB.svlf_octree_level_codes(self._h, level, _dp(out)))
+        return out
+
+    @property
+    def leaf_codes(self) -> np.ndarray:
+        return self.level_codes(self.leaf_level)
+
+    def corner_ids(self) -> np.ndarray:
+        out = np.zeros(self.leaf_count * 8, np.uint32)
+        _check(_LIB.svlf_octree_corner_ids(self._h, _dp(out)))
+        return out
+
+    def corner_vertices(self, voxel_id: int) -> np.ndarray:
+        leaves = self.leaf_codes
+        i = int(np.searchsorted(leaves, np.uint64(voxel_id)))
+        if i >= leaves.size or leaves[i] != np.uint64(voxel_id):
+            raise IndexError("unknown voxel id")
+        return self.corner_ids()[8 * i: 8 * i + 8]
+
+    def traverse(self, rays, with_points: bool = False):
+        """Batched traversal on the GPU: rays n x 6 -> (offsets[n+1], voxel_ids,
+        t_in, t_out[, x12 (n_hits x 6)]), each ray's hits sorted by (t_in, id)."""
+        r = _f64(rays).reshape(-1, 6)
+        n = r.shape[0]
+        off = np.zeros(n + 1, np.uint64)
+        total = C.c_size_t(0)
+        cap = max(8 * n, 1024)
+        while True:
+            ids = np.zeros(cap, np.uint64)
+            tin = np.zeros(cap)
+            tout = np.zeros(cap)
+            x12 = np.zeros((cap, 6)) if with_points else None
+            ctx = self.ctx or default_context()
+            st = _LIB.svlf_traverse(ctx.handle, self._h, _dp(r), n, _dp(off), cap, _dp(ids), _dp(tin),
+                                    _dp(tout), _dp(x12) if with_points else None, C.byref(total))
+            if st == 5:
+                cap = int(total.value)
+                continue
+            _check(st)
+            break
+        t = int(total.value)
+        out = (off.astype(np.int64), ids[:t], tin[:t], tout[:t])
+        return out + (x12[:t],) if with_points else out
+
+
+class Model:
+    """SvlfModel + gradients + ModelAdam, resident on the device."""
+
+    def __init__(self, octree: SparseOctree, seed: int | None = None, ctx: Context | None = None):
+        self.octree = octree
+        self.ctx = ctx or octree.ctx or default_context()
+        h = C.c_void_p()
+        _check(_LIB.svlf_model_create(self.ctx.handle, octree.handle, C.byref(h)))
+        self._h = h
+        self.V = octree.vertex_count
+        if seed is not None:
+            self.init(seed)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.svlf_model_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def init(self, seed: int):
+        _check(_LIB.svlf_model_init(self._h, seed))
+        return self
+
+    def _bufs(self):
+        return (np.zeros(self.V * FEAT_T_DIM, np.float32), np.zeros(self.V * FEAT_C_DIM, np.float32),
+                np.zeros(DEC_T_SIZE, np.float32), np.zeros(DEC_C_SIZE, np.float32))
+
+    def set_params(self, ft=None, fc=None, mt=None, mc=None):
+        arrs = [None if a is None else _f32(a).reshape(-1) for a in (ft, fc, mt, mc)]
+        sizes = (self.V * FEAT_T_DIM, self.V * FEAT_C_DIM, DEC_T_SIZE, DEC_C_SIZE)
+        for a, s in zip(arrs, sizes):
+            if a is not None and a.size != s:
+                raise ValueError("parameter size mismatch")
+        _check(_LIB.svlf_model_set_params(self._h, *[None if a is None else _dp(a) for a in arrs]))
+
+    def get_params(self):
+        b = self._bufs()
+        _check(_LIB.svlf_model_get_params(self._h, *[_dp(a) for a in b]))
+        return b
+
+    def get_grads(self):
+        b = self._bufs()
+        _check(_LIB.svlf_model_get_grads(self._h, *[_dp(a) for a in b]))
+        return b
+
+    def param_count(self) -> int:
+        return int(_LIB.svlf_model_param_count(self._h))
+
+    def get_adam(self):
+        n = self.param_count()
+        m, v = np.zeros(n, np.float32), np.zeros(n, np.float32)
+        steps = np.zeros(14, np.uint64)
+        _check(_LIB.svlf_model_get_adam(self._h, _dp(m), _dp(v), _dp(steps)))
+        return m, v, steps
+
+    def set_adam(self, m, v, steps):
+        m, v = _f32(m), _f32(v)
+        steps = np.ascontiguousarray(steps, dtype=np.uint64)
+        _check(_LIB.svlf_model_set_adam(self._h, _dp(m), _dp(v), _dp(steps)))
+
+
+_PREC = {"fp32": 0, "bf16": 1}
+
+
+def _bg(background):
+    if background is None:
+        return None, None
+    b = _f32(background).reshape(3)
+    return b, _dp(b)
+
+
+def render_frame(model: Model, camera: Camera, stats: RenderStats | None = None, background=None,
+                 precision: str = "fp32"):
+    """render_frame (include/svlf/render.hpp:104): returns (rgb HxWx3, alpha HxW, depth HxW)."""
+    n = camera.width * camera.height
+    rgb = np.zeros(n * 3, np.float32)
+    alpha = np.zeros(n, np.float32)
+    depth = np.zeros(n, np.float32)
+    st = _RenderStats()
+    keep, bgp = _bg(background)
+    cam = camera._c()
+    _check(_LIB.svlf_render_frame(model.ctx.handle, model.handle, C.byref(cam), bgp, _PREC[precision],
+                                  _dp(rgb), _dp(alpha), _dp(depth), C.byref(st)))
+    _add_stats(stats, st)
+    return (rgb.reshape(camera.height, camera.width, 3), alpha.reshape(camera.height, camera.width),
+            depth.reshape(camera.height, camera.width))
+
+
+def render_frame_device(model: Model, camera: Camera, d_rgb: int, d_alpha: int, d_depth: int,
+                        stats: RenderStats | None = None, background=None, precision: str = "fp32",
+                        row0: int = 0, rows: int | None = None):
+    """Device-buffer variant (pointers as ints); rows sub-range for tile sharding."""
+    st = _RenderStats()
+    keep, bgp = _bg(background)
+    cam = camera._c()
+    rows = camera.height - row0 if rows is None else rows
+    _check(_LIB.svlf_render_rows_device(model.ctx.handle, model.handle, C.byref(cam), row0, rows, bgp,
+                                        _PREC[precision], C.c_void_p(d_rgb), C.c_void_p(d_alpha),
+                                        C.c_void_p(d_depth), C.byref(st)))
+    _add_stats(stats, st)
+
+
+def render_rays(model: Model, rays, stats: RenderStats | None = None, background=None, precision="fp32"):
+    """render_ray per ray (render.hpp:75), batched: returns (rgb n x 3, alpha n, depth n)."""
+    r = _f64(rays).reshape(-1, 6)
+    n = r.shape[0]
+    rgb = np.zeros(n * 3, np.float32)
+    alpha = np.zeros(n, np.float32)
+    depth = np.zeros(n, np.float32)
+    st = _RenderStats()
+    keep, bgp = _bg(background)
+    _check(_LIB.svlf_render_rays(model.ctx.handle, model.handle, _dp(r), n, bgp, _PREC[precision], _dp(rgb),
+                                 _dp(alpha), _dp(depth), C.byref(st)))
+    _add_stats(stats, st)
+    return rgb.reshape(n, 3), alpha, depth
+
+
+def _add_stats(stats, st):
+    if stats is not None:
+        for f, _ in _RenderStats._fields_:
+            setattr(stats, f, getattr(stats, f) + getattr(st, f))
+
+
+def _batch(rays, c_gt, depth_gt, alpha_gt):
+    r = _f64(rays).reshape(-1, 6)
+    n = r.shape[0]
+    c = _f32(c_gt).reshape(n * 3)
+    d = _f64(depth_gt).reshape(n)
+    a = np.ascontiguousarray(np.asarray(alpha_gt).reshape(n) != 0, dtype=np.uint8)
+    return r, c, d, a, n
+
+
+def train_step(model: Model, rays, c_gt, depth_gt, alpha_gt, mode: str = "volumetric",
+               color_frozen: bool = False, lr: float = 1e-3, weights: LossWeights | None = None,
+               stats: LossStats | None = None) -> float:
+    """One optimizer step over a ray batch (src/train.cpp:443-479). Returns the loss sum."""
+    r, c, d, a, n = _batch(rays, c_gt, depth_gt, alpha_gt)
+    lw = (weights or LossWeights())._c()
+    st = _LossStats()
+    loss = C.c_double()
+    _check(_LIB.svlf_train_step(model.ctx.handle, model.handle, _dp(r), _dp(c), _dp(d), _dp(a), n,
+                                0 if mode == "surface" else 1, int(color_frozen), C.c_float(lr), C.byref(lw),
+                                C.byref(st), C.byref(loss)))
+    _add_loss_stats(stats, st)
+    return loss.value
+
+
+def loss_grads(model: Model, rays, c_gt, depth_gt, alpha_gt, mode: str = "volumetric",
+               color_frozen: bool = False, weights: LossWeights | None = None,
+               stats: LossStats | None = None) -> float:
+    """Loss sum and summed gradients (read with model.get_grads()), no optimizer step."""
+    r, c, d, a, n = _batch(rays, c_gt, depth_gt, alpha_gt)
+    lw = (weights or LossWeights())._c()
+    st = _LossStats()
+    loss = C.c_double()
+    _check(_LIB.svlf_loss_grads(model.ctx.handle, model.handle, _dp(r), _dp(c), _dp(d), _dp(a), n,
+                                0 if mode == "surface" else 1, int(color_frozen), C.byref(lw), C.byref(st),
+                                C.byref(loss)))
+    _add_loss_stats(stats, st)
+    return loss.value
+
+
+def _add_loss_stats(stats, st):
+    if stats is not None:
+        for f, _ in _LossStats._fields_:
+            setattr(stats, f, getattr(stats, f) + getattr(st, f))

@@ -1,0 +1,735 @@
+// C ABI implementation (include/svlf_b200.h): contexts, device mirrors of
+// octrees and models, and the render / traversal / train pipelines.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "host_octree.hpp"
+#include "host_rng.hpp"
+#include "train.cuh"
+
+namespace svlfb {
+
+std::atomic<long long> g_kernel_launches{0};
+size_t pack_f32_floats();
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+svlf_status guard(F&& f) {
+    try {
+        f();
+        return SVLF_OK;
+    } catch (const SvlfError& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return SVLF_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SVLF_ERR_RUNTIME;
+    }
+}
+
+void require(bool cond, const char* msg) {
+    if (!cond) fail(SVLF_ERR_INVALID_ARGUMENT, msg);
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        SVLF_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) SVLF_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+const char* dev_error_message(int code) {
+    switch (code) {
+        case kErrTangentRay: return "tangent ray";
+        case kErrPointNotInVoxel: return "point not in voxel";
+        case kErrSurfaceOutside: return "surface point outside voxel";
+        case kErrNegativeTau: return "negative optical thickness";
+        default: return "device error";
+    }
+}
+
+}  // namespace
+}  // namespace svlfb
+
+using namespace svlfb;
+
+enum EvIdx { EV_START, EV_COUNT, EV_EMIT, EV_DECODE, EV_COMPOSITE, EV_BACKWARD, EV_ADAM, EV_N };
+
+struct svlf_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;      // active stream
+    cudaStream_t own_stream = nullptr;  // created with the context
+    DevBuf rays, counts, offsets, scan_tmp, hit_leaf, hit_tin, hit_tout, hit_ray;
+    DevBuf h_tau, h_eta, h_rgb, out_rgb, out_alpha, out_depth, misc, tmp64, tmpx12;
+    TrainScratch train;
+    int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
+    cudaEvent_t ev[EV_N] = {};
+    svlf_timings last{};
+    std::mutex mu;  // one pipeline at a time per context
+};
+
+// Host octree; its device mirror is uploaded lazily to the device of the
+// first context that uses it (an octree built with ctx == NULL is host-only
+// until then, which keeps build/load usable without a GPU).
+struct svlf_octree {
+    HostOctree host;
+    mutable int device = -1;
+    mutable DevBuf first_child, mask, corners, leaf_codes;
+    mutable DevOctree view{};
+};
+
+struct svlf_model {
+    svlf_ctx* ctx = nullptr;
+    const svlf_octree* tree = nullptr;
+    uint32_t V = 0;
+    size_t n_ft = 0, n_fc = 0, n_total = 0;
+    DevBuf params, grads, adam_m, adam_v, pack_f32, pack_bf16;
+    uint64_t steps[14] = {};
+    uint64_t version = 1, pack_f32_version = 0, pack_bf16_version = 0;
+
+    float* p() const { return params.as<float>(); }
+    DevModel view() const {
+        return DevModel{p(), p() + n_ft, p() + n_ft + n_fc, p() + n_ft + n_fc + SVLF_DEC_T_SIZE, V};
+    }
+};
+
+namespace svlfb {
+namespace {
+
+// Device mirror of `t` on the current device (uploaded on first use).
+const DevOctree& dev_view(const svlf_octree* t) {
+    int dev = -1;
+    SVLF_CUDA(cudaGetDevice(&dev));
+    if (t->device == dev) return t->view;
+    for (DevBuf* b : {&t->first_child, &t->mask, &t->corners, &t->leaf_codes}) {
+        if (b->p) SVLF_CUDA(cudaFree(b->p));
+        b->p = nullptr;
+        b->cap = 0;
+    }
+    const HostOctree& h = t->host;
+    const size_t internal = h.node_first_child.size();
+    uint32_t* fc = t->first_child.ensure<uint32_t>(internal);
+    uint8_t* mk = t->mask.ensure<uint8_t>(internal);
+    uint32_t* cr = t->corners.ensure<uint32_t>(h.corner_ids.size());
+    uint64_t* lc = t->leaf_codes.ensure<uint64_t>(h.leaves().size());
+    SVLF_CUDA(cudaMemcpy(fc, h.node_first_child.data(), internal * 4, cudaMemcpyHostToDevice));
+    SVLF_CUDA(cudaMemcpy(mk, h.node_mask.data(), internal, cudaMemcpyHostToDevice));
+    SVLF_CUDA(cudaMemcpy(cr, h.corner_ids.data(), h.corner_ids.size() * 4, cudaMemcpyHostToDevice));
+    SVLF_CUDA(cudaMemcpy(lc, h.leaves().data(), h.leaves().size() * 8, cudaMemcpyHostToDevice));
+    DevOctree& v = t->view;
+    v = DevOctree{};
+    v.first_child = fc;
+    v.mask = mk;
+    v.corners = cr;
+    v.leaf_codes = lc;
+    for (int l = 0; l <= h.leaf_level + 1 && l < kMaxLevelsDev + 2; ++l) v.level_off[l] = h.level_off[l];
+    const double extent = h.grid.hi[0] - h.grid.lo[0];
+    for (int l = 0; l <= h.leaf_level; ++l) v.cell[l] = extent / (1u << l);  // src/octree.cpp:205
+    for (int a = 0; a < 3; ++a) {
+        v.lo[a] = h.grid.lo[a];
+        v.hi[a] = h.grid.hi[a];
+    }
+    v.cell_size = h.cell_size;
+    v.L = h.leaf_level;
+    v.res = h.grid.resolution;
+    v.n_leaves = uint32_t(h.leaves().size());
+    t->device = dev;
+    return v;
+}
+
+DevCamera to_dev_camera(const svlf_camera& c) {
+    DevCamera d;
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    std::memcpy(d.m, c.camera_to_world, sizeof d.m);
+    d.width = c.width;
+    d.height = c.height;
+    return d;
+}
+
+void ensure_pack_f32(svlf_model* m, cudaStream_t s) {
+    if (m->pack_f32_version == m->version) return;
+    float* pk = m->pack_f32.ensure<float>(pack_f32_floats());
+    launch_pack_f32(m->view(), pk, s);
+    m->pack_f32_version = m->version;
+}
+
+void check_device_error(svlf_ctx* ctx) {
+    int* flag = ctx->misc.as<int>();
+    int code = 0;
+    SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    code = ctx->h_pinned[0];
+    if (code != 0) {
+        SVLF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+        fail(SVLF_ERR_RUNTIME, dev_error_message(code));
+    }
+}
+
+// misc buffer layout: [0] int error flag, [8] u64 fg counter, [16] u64 aux
+void reset_misc(svlf_ctx* ctx) {
+    ctx->misc.ensure<unsigned long long>(8);
+    SVLF_CUDA(cudaMemsetAsync(ctx->misc.p, 0, 64, ctx->stream));
+}
+unsigned long long* misc_fg(svlf_ctx* ctx) { return reinterpret_cast<unsigned long long*>(ctx->misc.as<char>() + 8); }
+
+// Traversal for `n` rays: rays are either generated from `cam` (rows
+// row0..) into ctx->rays, or already resident in ctx->rays. Leaves CSR
+// offsets in ctx->offsets and sorted hits in ctx->hit_*. Returns total hits.
+uint32_t run_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0,
+                       uint32_t n) {
+    cudaStream_t s = ctx->stream;
+    double* rays = ctx->rays.ensure<double>(size_t(n) * 6);
+    uint32_t* counts = ctx->counts.ensure<uint32_t>(size_t(n) + 1);
+    uint32_t* offs = ctx->offsets.ensure<uint32_t>(size_t(n) + 1);
+    SVLF_CUDA(cudaMemsetAsync(counts + n, 0, sizeof(uint32_t), s));
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
+    launch_traverse_count(dev_view(tree), cam, row0, rays, n, counts, s);
+    const size_t tb = scan_temp_bytes(n + 1);
+    void* tmp = ctx->scan_tmp.ensure<char>(tb);
+    launch_exclusive_scan(tmp, tb, counts, offs, n + 1, s);
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));
+    SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, offs + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SVLF_CUDA(cudaStreamSynchronize(s));
+    const uint32_t total = uint32_t(ctx->h_pinned[4]);
+    ctx->hit_leaf.ensure<uint32_t>(total);
+    ctx->hit_tin.ensure<double>(total);
+    ctx->hit_tout.ensure<double>(total);
+    ctx->hit_ray.ensure<uint32_t>(total);
+    launch_traverse_emit(dev_view(tree), rays, n, offs, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
+                         ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), s);
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_EMIT], s));
+    return total;
+}
+
+// decode + composite into device output buffers
+void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t total, const float* bg,
+                          svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth) {
+    cudaStream_t s = ctx->stream;
+    HitOut ho{ctx->h_tau.ensure<float>(total), ctx->h_eta.ensure<float>(total),
+              ctx->h_rgb.ensure<float>(size_t(total) * 3)};
+    const DevOctree& T = dev_view(m->tree);
+    int* err = ctx->misc.as<int>();
+    if (prec == SVLF_PRECISION_BF16) {
+        ensure_pack_bf16(m->view(), m->pack_bf16, m->pack_bf16_version, m->version, s);
+        launch_decode_bf16(T, m->view(), m->pack_bf16.as<char>(), ctx->rays.as<double>(),
+                           ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(),
+                           ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total, ho, err, s);
+    } else {
+        ensure_pack_f32(m, s);
+        launch_decode_f32(T, m->view(), pack_f32_view(m->pack_f32.as<float>()), ctx->rays.as<double>(),
+                          ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(),
+                          ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total, ho, err, s);
+    }
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_DECODE], s));
+    launch_composite(ctx->offsets.as<uint32_t>(), ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), ho, n,
+                     bg, d_rgb, d_alpha, d_depth, misc_fg(ctx), s);
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COMPOSITE], s));
+}
+
+void finish_render(svlf_ctx* ctx, uint32_t n, uint32_t total, svlf_render_stats* stats) {
+    cudaStream_t s = ctx->stream;
+    SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 8, misc_fg(ctx), 8, cudaMemcpyDeviceToHost, s));
+    check_device_error(ctx);  // synchronizes
+    unsigned long long fg = 0;
+    std::memcpy(&fg, ctx->h_pinned + 8, 8);
+    float ms[4] = {};
+    cudaEventElapsedTime(&ms[0], ctx->ev[EV_START], ctx->ev[EV_COUNT]);
+    cudaEventElapsedTime(&ms[1], ctx->ev[EV_COUNT], ctx->ev[EV_EMIT]);
+    cudaEventElapsedTime(&ms[2], ctx->ev[EV_EMIT], ctx->ev[EV_DECODE]);
+    cudaEventElapsedTime(&ms[3], ctx->ev[EV_DECODE], ctx->ev[EV_COMPOSITE]);
+    ctx->last = svlf_timings{ms[0], ms[1], ms[2], ms[3], 0.f, 0.f, ms[0] + ms[1] + ms[2] + ms[3],
+                             (long long)total};
+    if (stats) {
+        stats->rays += n;
+        stats->rays_with_hits += (long long)fg;
+        stats->traversal_hits += total;
+        stats->thickness_queries += total;
+        stats->color_queries += total;
+    }
+}
+
+void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_t row0, uint32_t rows,
+                   const float* bg, svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth,
+                   svlf_render_stats* stats) {
+    require(cam != nullptr, "camera is null");
+    if (cam->width == 0 || cam->height == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "zero-size image");
+    require(row0 + rows <= cam->height, "row range outside the image");
+    const uint64_t n64 = uint64_t(cam->width) * rows;
+    require(n64 < (1ull << 31), "too many pixels in one call");
+    const uint32_t n = uint32_t(n64);
+    const DevCamera dc = to_dev_camera(*cam);
+    reset_misc(ctx);
+    const uint32_t total = run_traversal(ctx, m->tree, &dc, row0, n);
+    run_decode_composite(ctx, m, n, total, bg, prec, d_rgb, d_alpha, d_depth);
+    finish_render(ctx, n, total, stats);
+}
+
+size_t model_param_count(uint32_t V) { return size_t(V) * 96 + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE; }
+
+}  // namespace
+}  // namespace svlfb
+
+// ============================================================================
+extern "C" {
+
+const char* svlf_last_error(void) { return g_last_error.c_str(); }
+int svlf_abi_version(void) { return SVLF_ABI_VERSION; }
+long long svlf_ctx_kernel_launches(const svlf_ctx*) { return g_kernel_launches.load(); }
+
+svlf_status svlf_ctx_create(int device, svlf_ctx** out) {
+    return guard([&] {
+        require(out != nullptr, "out is null");
+        int count = 0;
+        const cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0)
+            fail(SVLF_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+        require(device >= 0 && device < count, "device ordinal out of range");
+        auto ctx = std::make_unique<svlf_ctx>();
+        ctx->device = device;
+        DeviceGuard g(device);
+        SVLF_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+        ctx->stream = ctx->own_stream;
+        SVLF_CUDA(cudaMallocHost(&ctx->h_pinned, 256));
+        for (auto& e2 : ctx->ev) SVLF_CUDA(cudaEventCreate(&e2));
+        ctx->misc.ensure<unsigned long long>(8);
+        SVLF_CUDA(cudaMemset(ctx->misc.p, 0, 64));
+        *out = ctx.release();
+    });
+}
+
+svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        {
+            DeviceGuard g(ctx->device);
+            cudaStreamSynchronize(ctx->stream);
+            for (auto& e : ctx->ev) cudaEventDestroy(e);
+            if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+            cudaStreamDestroy(ctx->own_stream);
+        }
+        delete ctx;
+    });
+}
+
+svlf_status svlf_ctx_set_stream(svlf_ctx* ctx, void* stream) {
+    return guard([&] {
+        require(ctx != nullptr, "ctx is null");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    });
+}
+
+svlf_status svlf_ctx_synchronize(svlf_ctx* ctx) {
+    return guard([&] {
+        require(ctx != nullptr, "ctx is null");
+        DeviceGuard g(ctx->device);
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out) {
+    return guard([&] {
+        require(ctx && out, "null argument");
+        *out = ctx->last;
+    });
+}
+
+// ---- octree -----------------------------------------------------------------
+static svlf_status make_octree(svlf_ctx* ctx, HostOctree&& h, svlf_octree** out) {
+    return guard([&] {
+        auto t = std::make_unique<svlf_octree>();
+        t->host = std::move(h);
+        if (ctx) {
+            DeviceGuard g(ctx->device);
+            dev_view(t.get());
+        }
+        *out = t.release();
+    });
+}
+
+svlf_status svlf_octree_build(svlf_ctx* ctx, const svlf_grid* grid, const double* pts, size_t n,
+                              svlf_octree** out) {
+    HostOctree h;
+    const svlf_status st = guard([&] {
+        require(grid && out, "null argument");
+        require(pts != nullptr || n == 0, "points is null");
+        h = HostOctree::build(std::span<const double>(pts, pts ? 3 * n : 0), *grid);
+    });
+    if (st != SVLF_OK) return st;
+    return make_octree(ctx, std::move(h), out);
+}
+
+svlf_status svlf_octree_from_leaves(svlf_ctx* ctx, const svlf_grid* grid, const uint64_t* codes, size_t n,
+                                    svlf_octree** out) {
+    HostOctree h;
+    const svlf_status st = guard([&] {
+        require(grid && out, "null argument");
+        require(codes != nullptr || n == 0, "codes is null");
+        h = HostOctree::from_leaves(std::vector<uint64_t>(codes, codes + n), *grid);
+    });
+    if (st != SVLF_OK) return st;
+    return make_octree(ctx, std::move(h), out);
+}
+
+svlf_status svlf_octree_destroy(svlf_octree* t) {
+    return guard([&] {
+        if (!t) return;
+        if (t->device >= 0) {
+            DeviceGuard g(t->device);
+            delete t;
+        } else {
+            delete t;
+        }
+    });
+}
+
+svlf_status svlf_octree_get_info(const svlf_octree* t, svlf_octree_info* out) {
+    return guard([&] {
+        require(t && out, "null argument");
+        *out = svlf_octree_info{};
+        out->leaf_level = t->host.leaf_level;
+        out->vertex_count = t->host.vertex_count;
+        out->leaf_count = t->host.leaves().size();
+        out->dropped_points = t->host.dropped_points;
+        out->cell_size = t->host.cell_size;
+        for (int l = 0; l <= t->host.leaf_level; ++l) out->level_size[l] = t->host.levels[l].size();
+    });
+}
+
+svlf_status svlf_octree_level_codes(const svlf_octree* t, int level, uint64_t* out) {
+    return guard([&] {
+        require(t && out, "null argument");
+        require(level >= 0 && level <= t->host.leaf_level, "level out of range");
+        const auto& v = t->host.levels[level];
+        std::memcpy(out, v.data(), v.size() * 8);
+    });
+}
+
+svlf_status svlf_octree_corner_ids(const svlf_octree* t, uint32_t* out) {
+    return guard([&] {
+        require(t && out, "null argument");
+        std::memcpy(out, t->host.corner_ids.data(), t->host.corner_ids.size() * 4);
+    });
+}
+
+// ---- traversal --------------------------------------------------------------
+svlf_status svlf_traverse(svlf_ctx* ctx, const svlf_octree* tree, const double* rays, size_t n,
+                          uint64_t* offsets, size_t capacity, uint64_t* voxel_ids, double* t_in,
+                          double* t_out, double* x12, size_t* total) {
+    return guard([&] {
+        require(ctx && tree && offsets && total, "null argument");
+        require(rays != nullptr || n == 0, "rays is null");
+        require(n < (1ull << 31), "too many rays");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        cudaStream_t s = ctx->stream;
+        const uint32_t nn = uint32_t(n);
+        reset_misc(ctx);
+        double* d_rays = ctx->rays.ensure<double>(size_t(nn) * 6 + 6);
+        if (nn) SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyHostToDevice, s));
+        const uint32_t tot = nn ? run_traversal(ctx, tree, nullptr, 0, nn) : 0;
+        *total = tot;
+        std::vector<uint32_t> off32(size_t(nn) + 1, 0);
+        if (nn) SVLF_CUDA(cudaMemcpyAsync(off32.data(), ctx->offsets.as<uint32_t>(), (size_t(nn) + 1) * 4,
+                                          cudaMemcpyDeviceToHost, s));
+        if (tot <= capacity && tot > 0) {
+            require(voxel_ids && t_in && t_out, "hit output is null");
+            uint64_t* codes = ctx->tmp64.ensure<uint64_t>(tot);
+            launch_gather_leaf_codes(dev_view(tree).leaf_codes, ctx->hit_leaf.as<uint32_t>(), codes, tot, s);
+            SVLF_CUDA(cudaMemcpyAsync(voxel_ids, codes, size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
+            SVLF_CUDA(cudaMemcpyAsync(t_in, ctx->hit_tin.as<double>(), size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
+            SVLF_CUDA(cudaMemcpyAsync(t_out, ctx->hit_tout.as<double>(), size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
+            if (x12) {
+                double* dx = ctx->tmpx12.ensure<double>(size_t(tot) * 6);
+                launch_hit_points(d_rays, ctx->hit_ray.as<uint32_t>(), ctx->hit_tin.as<double>(),
+                                  ctx->hit_tout.as<double>(), dx, tot, s);
+                SVLF_CUDA(cudaMemcpyAsync(x12, dx, size_t(tot) * 48, cudaMemcpyDeviceToHost, s));
+            }
+        }
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        for (size_t i = 0; i <= n; ++i) offsets[i] = off32[i];
+        if (tot > capacity) fail(SVLF_ERR_CAPACITY, "hit capacity too small");
+    });
+}
+
+// ---- model --------------------------------------------------------------------
+svlf_status svlf_model_create(svlf_ctx* ctx, const svlf_octree* tree, svlf_model** out) {
+    return guard([&] {
+        require(ctx && tree && out, "null argument");
+        DeviceGuard g(ctx->device);
+        auto m = std::make_unique<svlf_model>();
+        m->ctx = ctx;
+        m->tree = tree;
+        m->V = tree->host.vertex_count;
+        m->n_ft = size_t(m->V) * SVLF_FEAT_T_DIM;
+        m->n_fc = size_t(m->V) * SVLF_FEAT_C_DIM;
+        m->n_total = model_param_count(m->V);
+        for (DevBuf* b : {&m->params, &m->grads, &m->adam_m, &m->adam_v}) {
+            b->ensure<float>(m->n_total);
+            SVLF_CUDA(cudaMemset(b->p, 0, m->n_total * 4));
+        }
+        *out = m.release();
+    });
+}
+
+svlf_status svlf_model_destroy(svlf_model* m) {
+    return guard([&] {
+        if (!m) return;
+        DeviceGuard g(m->ctx->device);
+        delete m;
+    });
+}
+
+size_t svlf_model_param_count(const svlf_model* m) { return m ? m->n_total : 0; }
+
+svlf_status svlf_model_init(svlf_model* m, uint64_t seed) {
+    return guard([&] {
+        require(m != nullptr, "model is null");
+        // init_model, src/model.cpp:15-28; init_features features.cpp:10-19;
+        // MlpParams::init mlp.cpp:40-56
+        std::vector<float> host(m->n_total);
+        const HostRng root(seed);
+        auto features = [&](float* dst, size_t count, uint32_t dim, uint64_t s) {
+            const double bound = 1.0 / std::sqrt(double(dim));
+            HostRng r(s);
+            for (size_t i = 0; i < count; ++i) dst[i] = float(r.uniform(-bound, bound));
+        };
+        auto mlp = [&](float* dst, const uint32_t* dims, int layers, uint64_t s) {
+            HostRng r(s);
+            size_t o = 0;
+            for (int l = 0; l < layers; ++l) {
+                const uint32_t in = dims[l], outd = dims[l + 1];
+                const double bound = std::sqrt(6.0 / (in + outd));
+                for (size_t i = 0; i < size_t(in) * outd; ++i) dst[o++] = float(r.uniform(-bound, bound));
+                for (uint32_t i = 0; i < outd; ++i) dst[o++] = 0.f;
+            }
+        };
+        static const uint32_t dt[3] = {134, 128, 2}, dc[5] = {38, 128, 128, 128, 3};
+        features(host.data(), m->n_ft, SVLF_FEAT_T_DIM, root.sub(kStreamFeatT).next_u64());
+        features(host.data() + m->n_ft, m->n_fc, SVLF_FEAT_C_DIM, root.sub(kStreamFeatC).next_u64());
+        mlp(host.data() + m->n_ft + m->n_fc, dt, 2, root.sub(kStreamDecT).next_u64());
+        mlp(host.data() + m->n_ft + m->n_fc + SVLF_DEC_T_SIZE, dc, 4, root.sub(kStreamDecC).next_u64());
+        DeviceGuard g(m->ctx->device);
+        SVLF_CUDA(cudaMemcpy(m->params.p, host.data(), m->n_total * 4, cudaMemcpyHostToDevice));
+        for (DevBuf* b : {&m->grads, &m->adam_m, &m->adam_v}) SVLF_CUDA(cudaMemset(b->p, 0, m->n_total * 4));
+        std::fill(std::begin(m->steps), std::end(m->steps), 0);
+        ++m->version;
+    });
+}
+
+static void copy_params(svlf_model* m, DevBuf& buf, float* ft, float* fc, float* dt, float* dc, bool to_dev,
+                        const float* sft = nullptr, const float* sfc = nullptr, const float* sdt = nullptr,
+                        const float* sdc = nullptr) {
+    DeviceGuard g(m->ctx->device);
+    float* base = buf.as<float>();
+    const size_t sizes[4] = {m->n_ft, m->n_fc, SVLF_DEC_T_SIZE, SVLF_DEC_C_SIZE};
+    size_t off = 0;
+    for (int i = 0; i < 4; ++i) {
+        if (to_dev) {
+            const float* src = i == 0 ? sft : i == 1 ? sfc : i == 2 ? sdt : sdc;
+            if (src) SVLF_CUDA(cudaMemcpy(base + off, src, sizes[i] * 4, cudaMemcpyHostToDevice));
+        } else {
+            float* dst = i == 0 ? ft : i == 1 ? fc : i == 2 ? dt : dc;
+            if (dst) SVLF_CUDA(cudaMemcpy(dst, base + off, sizes[i] * 4, cudaMemcpyDeviceToHost));
+        }
+        off += sizes[i];
+    }
+}
+
+svlf_status svlf_model_set_params(svlf_model* m, const float* ft, const float* fc, const float* dt,
+                                  const float* dc) {
+    return guard([&] {
+        require(m != nullptr, "model is null");
+        copy_params(m, m->params, nullptr, nullptr, nullptr, nullptr, true, ft, fc, dt, dc);
+        ++m->version;
+    });
+}
+
+svlf_status svlf_model_get_params(svlf_model* m, float* ft, float* fc, float* dt, float* dc) {
+    return guard([&] {
+        require(m != nullptr, "model is null");
+        SVLF_CUDA(cudaStreamSynchronize(m->ctx->stream));
+        copy_params(m, m->params, ft, fc, dt, dc, false);
+    });
+}
+
+svlf_status svlf_model_get_grads(svlf_model* m, float* ft, float* fc, float* dt, float* dc) {
+    return guard([&] {
+        require(m != nullptr, "model is null");
+        SVLF_CUDA(cudaStreamSynchronize(m->ctx->stream));
+        copy_params(m, m->grads, ft, fc, dt, dc, false);
+    });
+}
+
+svlf_status svlf_model_get_adam(svlf_model* m, float* m_all, float* v_all, uint64_t* steps) {
+    return guard([&] {
+        require(m != nullptr, "model is null");
+        DeviceGuard g(m->ctx->device);
+        SVLF_CUDA(cudaStreamSynchronize(m->ctx->stream));
+        if (m_all) SVLF_CUDA(cudaMemcpy(m_all, m->adam_m.p, m->n_total * 4, cudaMemcpyDeviceToHost));
+        if (v_all) SVLF_CUDA(cudaMemcpy(v_all, m->adam_v.p, m->n_total * 4, cudaMemcpyDeviceToHost));
+        if (steps) std::memcpy(steps, m->steps, sizeof m->steps);
+    });
+}
+
+svlf_status svlf_model_set_adam(svlf_model* m, const float* m_all, const float* v_all, const uint64_t* steps) {
+    return guard([&] {
+        require(m != nullptr, "model is null");
+        DeviceGuard g(m->ctx->device);
+        if (m_all) SVLF_CUDA(cudaMemcpy(m->adam_m.p, m_all, m->n_total * 4, cudaMemcpyHostToDevice));
+        if (v_all) SVLF_CUDA(cudaMemcpy(m->adam_v.p, v_all, m->n_total * 4, cudaMemcpyHostToDevice));
+        if (steps) std::memcpy(m->steps, steps, sizeof m->steps);
+    });
+}
+
+// ---- render -------------------------------------------------------------------
+svlf_status svlf_render_frame_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg,
+                                     svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth,
+                                     svlf_render_stats* stats) {
+    return guard([&] {
+        require(ctx && m && cam && d_rgb && d_alpha && d_depth, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        render_device(ctx, m, cam, 0, cam->height, bg, prec, d_rgb, d_alpha, d_depth, stats);
+    });
+}
+
+svlf_status svlf_render_rows_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_t row0,
+                                    uint32_t rows, const float* bg, svlf_precision prec, float* d_rgb,
+                                    float* d_alpha, float* d_depth, svlf_render_stats* stats) {
+    return guard([&] {
+        require(ctx && m && cam && d_rgb && d_alpha && d_depth, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        render_device(ctx, m, cam, row0, rows, bg, prec, d_rgb, d_alpha, d_depth, stats);
+    });
+}
+
+svlf_status svlf_render_frame(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg,
+                              svlf_precision prec, float* rgb, float* alpha, float* depth,
+                              svlf_render_stats* stats) {
+    return guard([&] {
+        require(ctx && m && cam && rgb && alpha && depth, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const size_t n = size_t(cam->width) * cam->height;
+        float* d_rgb = ctx->out_rgb.ensure<float>(n * 3);
+        float* d_alpha = ctx->out_alpha.ensure<float>(n);
+        float* d_depth = ctx->out_depth.ensure<float>(n);
+        render_device(ctx, m, cam, 0, cam->height, bg, prec, d_rgb, d_alpha, d_depth, stats);
+        cudaStream_t s = ctx->stream;
+        SVLF_CUDA(cudaMemcpyAsync(rgb, d_rgb, n * 12, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaMemcpyAsync(alpha, d_alpha, n * 4, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaMemcpyAsync(depth, d_depth, n * 4, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+svlf_status svlf_render_rays(svlf_ctx* ctx, svlf_model* m, const double* rays, size_t n, const float* bg,
+                             svlf_precision prec, float* rgb, float* alpha, float* depth,
+                             svlf_render_stats* stats) {
+    return guard([&] {
+        require(ctx && m, "null argument");
+        require(n == 0 || (rays && rgb && alpha && depth), "null argument");
+        require(n < (1ull << 31), "too many rays");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        const uint32_t nn = uint32_t(n);
+        reset_misc(ctx);
+        double* d_rays = ctx->rays.ensure<double>(size_t(nn) * 6);
+        SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyHostToDevice, s));
+        float* d_rgb = ctx->out_rgb.ensure<float>(n * 3);
+        float* d_alpha = ctx->out_alpha.ensure<float>(n);
+        float* d_depth = ctx->out_depth.ensure<float>(n);
+        const uint32_t total = run_traversal(ctx, m->tree, nullptr, 0, nn);
+        run_decode_composite(ctx, m, nn, total, bg, prec, d_rgb, d_alpha, d_depth);
+        finish_render(ctx, nn, total, stats);
+        SVLF_CUDA(cudaMemcpyAsync(rgb, d_rgb, n * 12, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaMemcpyAsync(alpha, d_alpha, n * 4, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaMemcpyAsync(depth, d_depth, n * 4, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// ---- train --------------------------------------------------------------------
+static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const float* c_gt,
+                         const double* depth_gt, const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
+                         int color_frozen, const svlf_loss_weights* lw, bool adam, float lr,
+                         svlf_loss_stats* stats, double* loss_sum) {
+    require(ctx && m && lw, "null argument");
+    require(n == 0 || (rays && c_gt && depth_gt && alpha_gt), "null argument");
+    require(n < (1ull << 31), "too many rays");
+    require(mode == SVLF_LOSS_SURFACE || mode == SVLF_LOSS_VOLUMETRIC, "bad loss mode");
+    DeviceGuard g(ctx->device);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    TrainArgs a{};
+    a.rays = rays;
+    a.c_gt = c_gt;
+    a.depth_gt = depth_gt;
+    a.alpha_gt = alpha_gt;
+    a.n = uint32_t(n);
+    a.surface = mode == SVLF_LOSS_SURFACE;
+    a.color_frozen = color_frozen != 0;
+    a.lw = *lw;
+    a.adam = adam;
+    a.lr = lr;
+    TrainModelRefs mr{m->view(), m->params.as<float>(), m->grads.as<float>(), m->adam_m.as<float>(),
+                      m->adam_v.as<float>(), m->n_ft, m->n_fc, m->steps};
+    TrainResult r = run_train_step(ctx->train, dev_view(m->tree), mr, a, ctx->stream, ctx->misc.as<int>());
+    if (r.error) fail(SVLF_ERR_RUNTIME, dev_error_message(r.error));
+    if (adam) ++m->version;
+    ctx->last = r.timings;
+    if (stats) {
+        stats->rays += r.rays;
+        stats->skipped_rays += r.skipped;
+        stats->eta_skipped += r.eta_skipped;
+    }
+    if (loss_sum) *loss_sum = r.loss;
+}
+
+svlf_status svlf_train_step(svlf_ctx* ctx, svlf_model* m, const double* rays, const float* c_gt,
+                            const double* depth_gt, const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
+                            int color_frozen, float lr, const svlf_loss_weights* lw, svlf_loss_stats* stats,
+                            double* loss_sum) {
+    return guard([&] {
+        train_common(ctx, m, rays, c_gt, depth_gt, alpha_gt, n, mode, color_frozen, lw, true, lr, stats,
+                     loss_sum);
+    });
+}
+
+svlf_status svlf_loss_grads(svlf_ctx* ctx, svlf_model* m, const double* rays, const float* c_gt,
+                            const double* depth_gt, const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
+                            int color_frozen, const svlf_loss_weights* lw, svlf_loss_stats* stats,
+                            double* loss_sum) {
+    return guard([&] {
+        train_common(ctx, m, rays, c_gt, depth_gt, alpha_gt, n, mode, color_frozen, lw, false, 0.f, stats,
+                     loss_sum);
+    });
+}
+
+}  // extern "C"

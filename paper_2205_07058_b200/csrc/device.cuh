@@ -1,0 +1,136 @@
+// Kernel launch interface between the C ABI (capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+
+#include "common.hpp"
+#include "geom.cuh"
+
+namespace svlfb {
+
+// Process-wide count of this library's kernel launches (svlf_ctx_kernel_launches).
+extern std::atomic<long long> g_kernel_launches;
+inline void note_launch(long long n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
+
+constexpr int kFt = 64;       // thickness feature dim
+constexpr int kFc = 32;       // color feature dim
+constexpr int kHid = 128;     // hidden width
+constexpr int kInT = 6 + 2 * kFt;  // 134
+constexpr int kInC = 6 + kFc;      // 38
+
+// Flat decoder offsets (W_l row-major [out][in], then b_l), mlp.hpp:50-53.
+struct DecOffsets {
+    // f_T
+    static constexpr int T_W0 = 0, T_B0 = T_W0 + kHid * kInT, T_W1 = T_B0 + kHid, T_B1 = T_W1 + 2 * kHid,
+                         T_SIZE = T_B1 + 2;
+    // f_C
+    static constexpr int C_W0 = 0, C_B0 = C_W0 + kHid * kInC, C_W1 = C_B0 + kHid,
+                         C_B1 = C_W1 + kHid * kHid, C_W2 = C_B1 + kHid, C_B2 = C_W2 + kHid * kHid,
+                         C_W3 = C_B2 + kHid, C_B3 = C_W3 + 3 * kHid, C_SIZE = C_B3 + 3;
+};
+static_assert(DecOffsets::T_SIZE == SVLF_DEC_T_SIZE, "f_T size");
+static_assert(DecOffsets::C_SIZE == SVLF_DEC_C_SIZE, "f_C size");
+
+// Device view of a model's learnable tensors.
+struct DevModel {
+    const float* ft;  // [V][64]
+    const float* fc;  // [V][32]
+    const float* mt;  // f_T flat
+    const float* mc;  // f_C flat
+    uint32_t V;
+};
+
+// fp32 decoder pack for the CUDA-core path: hidden layers transposed to
+// [in][128] so a thread streams 16 consecutive outputs per float4 x4 load.
+struct DecPackF32 {
+    const float* t_w0t;  // [134][128]
+    const float* t_b0;   // [128]
+    const float* t_w1;   // [2][128]
+    const float* t_b1;   // [2]
+    const float* c_w0t;  // [38][128]
+    const float* c_b0;
+    const float* c_w1t;  // [128][128]
+    const float* c_b1;
+    const float* c_w2t;
+    const float* c_b2;
+    const float* c_w3;   // [3][128]
+    const float* c_b3;
+};
+constexpr size_t kPackF32Floats = size_t(kInT) * kHid + kHid + 2 * kHid + 2 + size_t(kInC) * kHid + kHid +
+                                  2 * (size_t(kHid) * kHid + kHid) + 3 * kHid + 3;
+
+// Grow-only device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* ensure(size_t n) {
+        const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+        if (bytes > cap) {
+            if (p) SVLF_CUDA(cudaFree(p));
+            p = nullptr;
+            cap = 0;
+            const size_t want = bytes + bytes / 4;
+            SVLF_CUDA(cudaMalloc(&p, want));
+            cap = want;
+        }
+        return static_cast<T*>(p);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// Per-hit decoder outputs consumed by composite.
+struct HitOut {
+    float* tau;
+    float* eta;
+    float* rgb;  // 3 per hit
+};
+
+// ---- traversal (traverse.cu)
+void launch_traverse_count(const DevOctree& T, const DevCamera* cam, uint32_t row0, double* rays,
+                           uint32_t n, uint32_t* counts, cudaStream_t s);
+void launch_traverse_emit(const DevOctree& T, const double* rays, uint32_t n, const uint32_t* offsets,
+                          uint32_t* hit_leaf, double* hit_tin, double* hit_tout, uint32_t* hit_ray,
+                          cudaStream_t s);
+size_t scan_temp_bytes(uint32_t n);
+void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
+                           uint32_t n, cudaStream_t s);
+
+// ---- render (render.cu)
+DecPackF32 pack_f32_view(float* base);
+void launch_pack_f32(const DevModel& M, float* pack, cudaStream_t s);
+void launch_decode_f32(const DevOctree& T, const DevModel& M, const DecPackF32& P, const double* rays,
+                       const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
+                       const double* hit_tout, uint32_t n_hits, HitOut out, int* err, cudaStream_t s);
+void launch_composite(const uint32_t* offsets, const double* hit_tin, const double* hit_tout,
+                      HitOut hits, uint32_t n_rays, const float* bg3, float* rgb, float* alpha,
+                      float* depth, unsigned long long* fg_count, cudaStream_t s);
+
+// ---- tcgen05 decoder (decode_tc.cu)
+void ensure_pack_bf16(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version,
+                      cudaStream_t s);
+void launch_decode_bf16(const DevOctree& T, const DevModel& M, const char* pack, const double* rays,
+                        const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
+                        const double* hit_tout, uint32_t n_hits, HitOut out, int* err, cudaStream_t s);
+
+// ---- misc device utilities (traverse.cu)
+void launch_gather_leaf_codes(const uint64_t* leaf_codes, const uint32_t* hit_leaf, uint64_t* out,
+                              size_t n, cudaStream_t s);
+void launch_hit_points(const double* rays, const uint32_t* hit_ray, const double* tin,
+                       const double* tout, double* x12, size_t n, cudaStream_t s);
+
+}  // namespace svlfb

@@ -1,0 +1,164 @@
+// Device-side geometry shared by the traversal, decode and train kernels.
+//
+// Bit-exactness rule: every fp64 expression is written with
+// explicit round-to-nearest intrinsics in the reference's operand order, so
+// no multiply-add is ever contracted (the library is also compiled with
+// -fmad=false). With that, ray generation, box bounds, slab tests and hit
+// points are bit-identical to the reference built with -ffp-contract=off.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+namespace svlfb {
+
+constexpr int kMaxLevelsDev = 21;
+
+// Read-only device mirror of a HostOctree (see host_octree.hpp for layout).
+struct DevOctree {
+    const uint32_t* first_child;  // per internal node
+    const uint8_t* mask;          // per internal node
+    const uint32_t* corners;      // 8 per leaf
+    const uint64_t* leaf_codes;   // sorted
+    uint32_t level_off[kMaxLevelsDev + 2];
+    double cell[kMaxLevelsDev + 1];  // extent / (1u << level), src/octree.cpp:205
+    double lo[3];
+    double cell_size;                // extent / resolution (voxel_aabb, local_coords)
+    double hi[3];
+    int L;
+    uint32_t res;
+    uint32_t n_leaves;
+};
+
+struct Ray {
+    double o[3];
+    double d[3];
+};
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// dot(a, b) = a.x*b.x + a.y*b.y + a.z*b.z, left to right (geometry.hpp:34)
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+    return dadd(dadd(dmul(a[0], b[0]), dmul(a[1], b[1])), dmul(a[2], b[2]));
+}
+
+// origin + dir * t (geometry.hpp:56)
+__device__ __forceinline__ void ray_at(const Ray& r, double t, double* p) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p[a] = dadd(r.o[a], dmul(r.d[a], t));
+}
+
+// Camera::pixel_ray (camera.hpp:26-29): pixel centre, row-major c2w rotation,
+// normalized() = three true divisions by sqrt(dot(v, v)).
+struct DevCamera {
+    double fx, fy, cx, cy;
+    double m[16];
+    uint32_t width, height;
+};
+
+__device__ __forceinline__ Ray pixel_ray(const DevCamera& c, uint32_t ix, uint32_t iy) {
+    const double v[3] = {ddiv(dsub(dadd(double(ix), 0.5), c.cx), c.fx),
+                         ddiv(dsub(dadd(double(iy), 0.5), c.cy), c.fy), 1.0};
+    double r[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        r[i] = dadd(dadd(dmul(c.m[4 * i], v[0]), dmul(c.m[4 * i + 1], v[1])), dmul(c.m[4 * i + 2], v[2]));
+    const double n = __dsqrt_rn(dot3(r, r));
+    Ray out;
+    out.o[0] = c.m[3];
+    out.o[1] = c.m[7];
+    out.o[2] = c.m[11];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) out.d[i] = ddiv(r[i], n);
+    return out;
+}
+
+// Ray with the per-axis reciprocal hoisted: 1.0/d is the same IEEE result in
+// every ray_aabb call of a ray, so computing it once is bit-neutral.
+struct RayPre {
+    Ray r;
+    double inv[3];
+};
+
+__device__ __forceinline__ RayPre precompute(const Ray& r) {
+    RayPre p;
+    p.r = r;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p.inv[a] = r.d[a] == 0.0 ? 0.0 : ddiv(1.0, r.d[a]);
+    return p;
+}
+
+// ray_aabb, src/geometry.cpp:5-26: slab test clipped to t >= 0; a zero
+// direction component is an inside-the-slab test; reject iff t1 < t0.
+__device__ __forceinline__ bool slab_test(const RayPre& p, const double* lo, const double* hi,
+                                          double& t0, double& t1) {
+    t0 = 0.0;
+    t1 = CUDART_INF;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double o = p.r.o[a];
+        if (p.r.d[a] == 0.0) {
+            if (o < lo[a] || o > hi[a]) return false;
+            continue;
+        }
+        double ta = dmul(dsub(lo[a], o), p.inv[a]);
+        double tb = dmul(dsub(hi[a], o), p.inv[a]);
+        if (ta > tb) {
+            const double s = ta;
+            ta = tb;
+            tb = s;
+        }
+        if (ta > t0) t0 = ta;
+        if (tb < t1) t1 = tb;
+        if (t1 < t0) return false;
+    }
+    return true;
+}
+
+// Cell box at a level from integer coordinates: lo + x*cell, lo + (x+1)*cell
+// (src/octree.cpp:205-210; voxel_aabb, :144-152 at the leaf level).
+__device__ __forceinline__ void cell_box(const DevOctree& T, double cell, uint32_t x, uint32_t y,
+                                         uint32_t z, double* lo, double* hi) {
+    const uint32_t c[3] = {x, y, z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = dadd(T.lo[a], dmul(double(c[a]), cell));
+        hi[a] = dadd(T.lo[a], dmul(double(c[a] + 1u), cell));
+    }
+}
+
+__device__ __forceinline__ uint32_t morton_gather3_dev(uint64_t v) {
+    v &= 0x1249249249249249ULL;
+    v = (v ^ (v >> 2)) & 0x10c30c30c30c30c3ULL;
+    v = (v ^ (v >> 4)) & 0x100f00f00f00f00fULL;
+    v = (v ^ (v >> 8)) & 0x1f0000ff0000ffULL;
+    v = (v ^ (v >> 16)) & 0x1f00000000ffffULL;
+    v = (v ^ (v >> 32)) & 0x1fffffULL;
+    return uint32_t(v);
+}
+
+__device__ __forceinline__ void leaf_box(const DevOctree& T, uint32_t leaf, double* lo, double* hi) {
+    const uint64_t code = T.leaf_codes[leaf];
+    cell_box(T, T.cell_size, morton_gather3_dev(code), morton_gather3_dev(code >> 1),
+             morton_gather3_dev(code >> 2), lo, hi);
+}
+
+// Device error codes raised by kernels, mapped to the reference's messages.
+enum DevError : int {
+    kErrNone = 0,
+    kErrTangentRay = 1,       // "tangent ray" (render.cpp:23)
+    kErrPointNotInVoxel = 2,  // "point not in voxel" (features.cpp:25)
+    kErrSurfaceOutside = 3,   // "surface point outside voxel" (train.cpp:32)
+    kErrNegativeTau = 4,
+};
+
+__device__ __forceinline__ void raise_error(int* flag, int code) {
+    if (*flag == 0) atomicCAS(flag, 0, code);
+}
+
+}  // namespace svlfb

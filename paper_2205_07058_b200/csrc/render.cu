@@ -1,0 +1,347 @@
+// Render-path kernels besides traversal:
+//   pack_f32     decoder weights -> transposed fp32 pack (per parameter version)
+//   decode_f32   per hit: ray parameterisation, trilinear gather at x1/x2,
+//                f_T, x_s, gather at x_s, f_C  (CUDA cores, fp32, the
+//                reference's accumulation order, no FMA contraction)
+//   composite    per ray: front-to-back alpha compositing in fp64
+//
+// References: parameterize_ray src/render.cpp:16-28; local_coords
+// src/features.cpp:22-31; trilinear_weights include/svlf/features.hpp:13-21;
+// interp_into_column src/voxel_batch.hpp:22-37; batch_forward_thickness /
+// _color src/voxel_batch.hpp:69-142; dense_forward src/mlp.cpp:98-116;
+// render_tile composite src/render.cpp:160-193.
+#include "device.cuh"
+
+namespace svlfb {
+
+namespace {
+
+__host__ __device__ constexpr size_t r4(size_t x) { return (x + 3) & ~size_t(3); }
+
+struct PackOff {
+    size_t t_w0t, t_b0, t_w1, t_b1, c_w0t, c_b0, c_w1t, c_b1, c_w2t, c_b2, c_w3, c_b3, total;
+};
+
+__host__ __device__ constexpr PackOff pack_offsets() {
+    PackOff p{};
+    size_t o = 0;
+    p.t_w0t = o; o = r4(o + size_t(kInT) * kHid);
+    p.t_b0 = o;  o = r4(o + kHid);
+    p.t_w1 = o;  o = r4(o + 2 * kHid);
+    p.t_b1 = o;  o = r4(o + 2);
+    p.c_w0t = o; o = r4(o + size_t(kInC) * kHid);
+    p.c_b0 = o;  o = r4(o + kHid);
+    p.c_w1t = o; o = r4(o + size_t(kHid) * kHid);
+    p.c_b1 = o;  o = r4(o + kHid);
+    p.c_w2t = o; o = r4(o + size_t(kHid) * kHid);
+    p.c_b2 = o;  o = r4(o + kHid);
+    p.c_w3 = o;  o = r4(o + 3 * kHid);
+    p.c_b3 = o;  o = r4(o + 3);
+    p.total = o;
+    return p;
+}
+constexpr PackOff kPack = pack_offsets();
+static_assert(kPack.total >= kPackF32Floats, "pack size");
+
+__global__ void k_pack_f32(const float* __restrict__ mt, const float* __restrict__ mc, float* pack) {
+    using D = DecOffsets;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    // transposes: dst[k*128 + o] = W[o*in + k]
+    auto tr = [&](const float* W, int in, float* dst, int idx) {
+        if (idx < in * kHid) {
+            const int k = idx / kHid, o = idx % kHid;
+            dst[idx] = W[o * in + k];
+        }
+    };
+    tr(mt + D::T_W0, kInT, pack + kPack.t_w0t, tid);
+    tr(mc + D::C_W0, kInC, pack + kPack.c_w0t, tid);
+    tr(mc + D::C_W1, kHid, pack + kPack.c_w1t, tid);
+    tr(mc + D::C_W2, kHid, pack + kPack.c_w2t, tid);
+    if (tid < kHid) {
+        pack[kPack.t_b0 + tid] = mt[D::T_B0 + tid];
+        pack[kPack.c_b0 + tid] = mc[D::C_B0 + tid];
+        pack[kPack.c_b1 + tid] = mc[D::C_B1 + tid];
+        pack[kPack.c_b2 + tid] = mc[D::C_B2 + tid];
+    }
+    if (tid < 2 * kHid) pack[kPack.t_w1 + tid] = mt[D::T_W1 + tid];
+    if (tid < 3 * kHid) pack[kPack.c_w3 + tid] = mc[D::C_W3 + tid];
+    if (tid < 2) pack[kPack.t_b1 + tid] = mt[D::T_B1 + tid];
+    if (tid < 3) pack[kPack.c_b3 + tid] = mc[D::C_B3 + tid];
+}
+
+// ---- per-hit geometry (fp64, reference operand order) -------------------
+
+// parameterize_ray, src/render.cpp:16-28. Returns false on "tangent ray".
+__device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, const double* hi, float* r6) {
+    double c[3], oc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        c[a] = dmul(dadd(lo[a], hi[a]), 0.5);
+        oc[a] = dsub(r.o[a], c[a]);
+    }
+    const double radius = dmul(dmul(0.5, __dsqrt_rn(3.0)), dsub(hi[0], lo[0]));
+    const double b = dot3(oc, r.d);
+    const double cc = dsub(dot3(oc, oc), dmul(radius, radius));
+    const double disc = dsub(dmul(b, b), cc);
+    if (disc < 1e-14) return false;
+    const double s = __dsqrt_rn(disc);
+    double p1[3], p2[3];
+    ray_at(r, dsub(-b, s), p1);
+    ray_at(r, dadd(-b, s), p2);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        p1[a] = dsub(p1[a], c[a]);
+        p2[a] = dsub(p2[a], c[a]);
+    }
+    const double n1 = __dsqrt_rn(dot3(p1, p1)), n2 = __dsqrt_rn(dot3(p2, p2));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r6[a] = float(ddiv(p1[a], n1));
+        r6[3 + a] = float(ddiv(p2[a], n2));
+    }
+    return true;
+}
+
+// local_coords + trilinear_weights (features.cpp:22-31, features.hpp:13-21).
+// Returns false on "point not in voxel".
+__device__ __forceinline__ bool trilinear_at(const double* p, const double* lo, const double* hi,
+                                             double h, float* w) {
+    double u[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!(p[a] >= dsub(lo[a], 1e-7) && p[a] <= dadd(hi[a], 1e-7))) return false;
+        u[a] = fmin(fmax(ddiv(dsub(p[a], lo[a]), h), 0.0), 1.0);
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const double wx = (b & 1) ? u[0] : dsub(1.0, u[0]);
+        const double wy = (b & 2) ? u[1] : dsub(1.0, u[1]);
+        const double wz = (b & 4) ? u[2] : dsub(1.0, u[2]);
+        w[b] = float(dmul(dmul(wx, wy), wz));
+    }
+    return true;
+}
+
+// z = sum_b w_b * row_b (b in order, fp32, no FMA) into a feature-major column.
+template <int DIM>
+__device__ __forceinline__ void gather_col(const float* __restrict__ vol, const uint32_t* corners,
+                                           const float* w, float* col, int stride) {
+#pragma unroll 1
+    for (int d4 = 0; d4 < DIM / 4; ++d4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(vol + size_t(corners[b]) * DIM) + d4);
+            acc.x = __fadd_rn(acc.x, __fmul_rn(w[b], v.x));
+            acc.y = __fadd_rn(acc.y, __fmul_rn(w[b], v.y));
+            acc.z = __fadd_rn(acc.z, __fmul_rn(w[b], v.z));
+            acc.w = __fadd_rn(acc.w, __fmul_rn(w[b], v.w));
+        }
+        col[(4 * d4 + 0) * stride] = acc.x;
+        col[(4 * d4 + 1) * stride] = acc.y;
+        col[(4 * d4 + 2) * stride] = acc.z;
+        col[(4 * d4 + 3) * stride] = acc.w;
+    }
+}
+
+// Hidden layer over one column: y[o] = relu(b[o] + sum_k W[o][k] x[k]), k in order.
+__device__ __forceinline__ void dense_relu_col(const float* __restrict__ wt, const float* __restrict__ bias,
+                                               const float* x, int in, float* y, int stride) {
+#pragma unroll 1
+    for (int o0 = 0; o0 < kHid; o0 += 16) {
+        float acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = __ldg(bias + o0 + i);
+#pragma unroll 2
+        for (int k = 0; k < in; ++k) {
+            const float xv = x[k * stride];
+            const float4* wr = reinterpret_cast<const float4*>(wt + size_t(k) * kHid + o0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 w = __ldg(wr + q);
+                acc[4 * q + 0] = __fadd_rn(acc[4 * q + 0], __fmul_rn(w.x, xv));
+                acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(w.y, xv));
+                acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(w.z, xv));
+                acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(w.w, xv));
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[(o0 + i) * stride] = acc[i] > 0.f ? acc[i] : 0.f;
+    }
+}
+
+// Output unit o over a 128-wide hidden column (pre-activation).
+__device__ __forceinline__ float head_dot(const float* __restrict__ w, float b, const float* x, int stride) {
+    float acc = b;
+#pragma unroll 4
+    for (int k = 0; k < kHid; ++k) acc = __fadd_rn(acc, __fmul_rn(__ldg(w + k), x[k * stride]));
+    return acc;
+}
+
+// sigmoid as T(1)/(T(1)+exp(-x)) (mlp.cpp:81-84). exp is evaluated in fp64
+// and rounded, which reproduces a correctly rounded expf.
+__device__ __forceinline__ float sigmoid_ref(float x) {
+    const float e = float(exp(-double(x)));
+    return __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
+}
+
+constexpr int kDecBlock = 64;
+constexpr int kXRows = 136;  // >= 134 input rows, reused for hidden columns
+
+__global__ void __launch_bounds__(kDecBlock) k_decode_f32(DevOctree T, DevModel M, DecPackF32 P,
+                                                          const double* __restrict__ rays,
+                                                          const uint32_t* __restrict__ hit_ray,
+                                                          const uint32_t* __restrict__ hit_leaf,
+                                                          const double* __restrict__ hit_tin,
+                                                          const double* __restrict__ hit_tout,
+                                                          uint32_t n, HitOut out, int* err) {
+    extern __shared__ float smem[];
+    const uint32_t j = blockIdx.x * kDecBlock + threadIdx.x;
+    if (j >= n) return;
+    float* X = smem + threadIdx.x;                      // [136][64] column
+    float* H = smem + kXRows * kDecBlock + threadIdx.x; // [128][64] column
+    constexpr int S = kDecBlock;
+
+    Ray r;
+    const uint32_t ri = hit_ray[j];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r.o[a] = rays[6 * size_t(ri) + a];
+        r.d[a] = rays[6 * size_t(ri) + 3 + a];
+    }
+    const uint32_t leaf = hit_leaf[j];
+    const double tin = hit_tin[j], tout = hit_tout[j];
+    double lo[3], hi[3], x1[3], x2[3];
+    leaf_box(T, leaf, lo, hi);
+    ray_at(r, tin, x1);
+    ray_at(r, tout, x2);
+
+    float r6[6];
+    if (!parameterize(r, lo, hi, r6)) {
+        raise_error(err, kErrTangentRay);
+        return;
+    }
+    uint32_t corners[8];
+    {
+        const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
+        const uint4 a = __ldg(cp), b = __ldg(cp + 1);
+        corners[0] = a.x; corners[1] = a.y; corners[2] = a.z; corners[3] = a.w;
+        corners[4] = b.x; corners[5] = b.y; corners[6] = b.z; corners[7] = b.w;
+    }
+    float w1[8], w2[8];
+    if (!trilinear_at(x1, lo, hi, T.cell_size, w1) || !trilinear_at(x2, lo, hi, T.cell_size, w2)) {
+        raise_error(err, kErrPointNotInVoxel);
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) X[k * S] = r6[k];
+    gather_col<kFt>(M.ft, corners, w1, X + 6 * S, S);
+    gather_col<kFt>(M.ft, corners, w2, X + (6 + kFt) * S, S);
+
+    // f_T: 134 -> 128 (relu) -> (tau relu, eta sigmoid)
+    dense_relu_col(P.t_w0t, P.t_b0, X, kInT, H, S);
+    const float y0 = head_dot(P.t_w1, __ldg(P.t_b1), H, S);
+    const float y1 = head_dot(P.t_w1 + kHid, __ldg(P.t_b1 + 1), H, S);
+    const float tau = y0 > 0.f ? y0 : 0.f;
+    const float eta = sigmoid_ref(y1);
+    out.tau[j] = tau;
+    out.eta[j] = eta;
+
+    // x_s = x1*eta + x2*(1-eta) (voxel_batch.hpp:111)
+    const double e = double(eta), ome = dsub(1.0, e);
+    double xs[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) xs[a] = dadd(dmul(x1[a], e), dmul(x2[a], ome));
+    float ws[8];
+    if (!trilinear_at(xs, lo, hi, T.cell_size, ws)) {
+        raise_error(err, kErrPointNotInVoxel);
+        return;
+    }
+    // f_C input: [r6 | psi_C(x_s)] in X rows 0..37
+    gather_col<kFc>(M.fc, corners, ws, X + 6 * S, S);
+    dense_relu_col(P.c_w0t, P.c_b0, X, kInC, H, S);
+    dense_relu_col(P.c_w1t, P.c_b1, H, kHid, X, S);
+    dense_relu_col(P.c_w2t, P.c_b2, X, kHid, H, S);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        out.rgb[3 * size_t(j) + c] = sigmoid_ref(head_dot(P.c_w3 + c * kHid, __ldg(P.c_b3 + c), H, S));
+}
+
+// render_tile composite, src/render.cpp:165-193 (fp64 accumulation).
+__global__ void __launch_bounds__(128) k_composite(const uint32_t* __restrict__ offsets,
+                                                   const double* __restrict__ tin,
+                                                   const double* __restrict__ tout, HitOut h,
+                                                   uint32_t n, float bg0, float bg1, float bg2,
+                                                   float* rgb, float* alpha, float* depth,
+                                                   unsigned long long* fg_count) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool fg = false;
+    if (i < n) {
+        const uint32_t h0 = offsets[i], h1 = offsets[i + 1];
+        double c0 = 0, c1 = 0, c2 = 0, a = 0, dacc = 0, T = 1.0;
+        for (uint32_t j = h0; j < h1; ++j) {
+            const double e = exp(-double(h.tau[j]));
+            const double w = dmul(T, dsub(1.0, e));
+            c0 = dadd(c0, dmul(w, double(h.rgb[3 * size_t(j)])));
+            c1 = dadd(c1, dmul(w, double(h.rgb[3 * size_t(j) + 1])));
+            c2 = dadd(c2, dmul(w, double(h.rgb[3 * size_t(j) + 2])));
+            const double eta = double(h.eta[j]);
+            const double ts = dadd(dmul(tin[j], eta), dmul(tout[j], dsub(1.0, eta)));
+            dacc = dadd(dacc, dmul(w, ts));
+            a = dadd(a, w);
+            T = dmul(T, e);
+        }
+        fg = h1 > h0;
+        const double oma = dsub(1.0, a);
+        rgb[3 * size_t(i)] = float(dadd(c0, dmul(oma, double(bg0))));
+        rgb[3 * size_t(i) + 1] = float(dadd(c1, dmul(oma, double(bg1))));
+        rgb[3 * size_t(i) + 2] = float(dadd(c2, dmul(oma, double(bg2))));
+        alpha[i] = float(a);
+        depth[i] = a > 1e-4 ? float(ddiv(dacc, a)) : 0.f;
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, fg);
+    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(fg_count, (unsigned long long)__popc(ballot));
+}
+
+}  // namespace
+
+DecPackF32 pack_f32_view(float* b) {
+    return DecPackF32{b + kPack.t_w0t, b + kPack.t_b0, b + kPack.t_w1, b + kPack.t_b1,
+                      b + kPack.c_w0t, b + kPack.c_b0, b + kPack.c_w1t, b + kPack.c_b1,
+                      b + kPack.c_w2t, b + kPack.c_b2, b + kPack.c_w3,  b + kPack.c_b3};
+}
+
+size_t pack_f32_floats() { return kPack.total; }
+
+void launch_pack_f32(const DevModel& M, float* pack, cudaStream_t s) {
+    const int n = kInT * kHid;  // largest segment
+    k_pack_f32<<<(n + 255) / 256, 256, 0, s>>>(M.mt, M.mc, pack);
+    note_launch();
+}
+
+void launch_decode_f32(const DevOctree& T, const DevModel& M, const DecPackF32& P, const double* rays,
+                       const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
+                       const double* hit_tout, uint32_t n_hits, HitOut out, int* err, cudaStream_t s) {
+    if (n_hits == 0) return;
+    const size_t smem = size_t(kXRows + kHid) * kDecBlock * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        SVLF_CUDA(cudaFuncSetAttribute(k_decode_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+    }
+    k_decode_f32<<<(n_hits + kDecBlock - 1) / kDecBlock, kDecBlock, smem, s>>>(
+        T, M, P, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits, out, err);
+    note_launch();
+}
+
+void launch_composite(const uint32_t* offsets, const double* hit_tin, const double* hit_tout,
+                      HitOut hits, uint32_t n_rays, const float* bg3, float* rgb, float* alpha,
+                      float* depth, unsigned long long* fg_count, cudaStream_t s) {
+    if (n_rays == 0) return;
+    k_composite<<<(n_rays + 127) / 128, 128, 0, s>>>(offsets, hit_tin, hit_tout, hits, n_rays,
+                                                      bg3 ? bg3[0] : 0.f, bg3 ? bg3[1] : 0.f,
+                                                      bg3 ? bg3[2] : 0.f, rgb, alpha, depth, fg_count);
+    note_launch();
+}
+
+}  // namespace svlfb

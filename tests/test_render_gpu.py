@@ -1,0 +1,138 @@
+"""GPU parity: traversal and render through the C ABI vs the CPU oracle.
+
+Bars (BASELINE.json north_star): voxel hit lists bit-exact (ids, order,
+t_in, t_out, x1, x2); fp32 render max-abs <= 1e-3 on rgb/alpha/depth (the
+kernel keeps the reference's accumulation order, so the observed error is
+~1e-7); render statistics identical.
+"""
+import numpy as np
+import pytest
+
+import paper_2205_07058_b200 as P
+import paper_2205_07058_b200.synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+TOL_FP32 = 1e-3  # north_star: RGB/depth max-abs <= 1e-3 with the fp32 MLP
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def c1(ctx, oracle):
+    pts, res, dil, cam, W, H = S.c1_workload()
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    otree = oracle.tree_build(pts, res, dil)
+    return tree, otree, cam, W, H
+
+
+def _assert_hits_equal(got, want):
+    off_g, ids_g, tin_g, tout_g = got[:4]
+    off_w, ids_w, tin_w, tout_w = want[:4]
+    assert np.array_equal(off_g, off_w)
+    assert np.array_equal(ids_g, ids_w)
+    assert np.array_equal(tin_g, tin_w)  # bit-exact doubles
+    assert np.array_equal(tout_g, tout_w)
+
+
+def test_traversal_c1_camera_rays_bit_exact(c1, oracle):
+    tree, otree, cam, W, H = c1
+    rays = oracle.camera_rays(cam, W, H)
+    got = tree.traverse(rays, with_points=True)
+    want = oracle.traverse(otree, rays)
+    assert want[1].size == 59905  # C1 has 59,905 hits
+    _assert_hits_equal(got, want)
+    # x1/x2 = ray.at(t) exactly
+    ray_of = np.repeat(np.arange(rays.shape[0]), np.diff(got[0]))
+    o, d = rays[ray_of, :3], rays[ray_of, 3:]
+    assert np.array_equal(got[4][:, :3], o + d * got[2][:, None])
+    assert np.array_equal(got[4][:, 3:], o + d * got[3][:, None])
+
+
+def test_traversal_reference_random_rays(ctx, oracle):
+    """tests/test_octree.cpp:140-154: random 16^3 density-0.1 seed-7 octree, 1000 rays (Rng 11)."""
+    pts = S.random_occupancy_points(16, 0.1, 7)
+    tree = P.SparseOctree.build(pts, P.GridConfig(16, dilation=0), ctx)
+    otree = oracle.tree_build(pts, 16, 0)
+    rays = S.random_rays(11, 1000)
+    _assert_hits_equal(tree.traverse(rays), oracle.traverse(otree, rays))
+
+
+def test_traversal_tie_rule_grazing_face(ctx):
+    """tests/test_octree.cpp:156-173: a ray in the shared x=0.5 face hits both leaves, Morton order."""
+    pts = np.array([[0.25, 0.25, 0.25], [0.75, 0.25, 0.25]])
+    tree = P.SparseOctree.build(pts, P.GridConfig(2, dilation=0), ctx)
+    off, ids, tin, tout = tree.traverse(np.array([[0.5, -1.0, 0.25, 0.0, 1.0, 0.0]]))
+    assert ids.size == 2 and ids[0] < ids[1] and tin[0] == tin[1]
+
+
+def test_traversal_empty_and_missing_rays(ctx, oracle):
+    pts = S.random_occupancy_points(16, 0.1, 7)
+    tree = P.SparseOctree.build(pts, P.GridConfig(16, dilation=0), ctx)
+    off, ids, *_ = tree.traverse(np.zeros((0, 6)))
+    assert off.tolist() == [0] and ids.size == 0
+    # rays pointing away from the cube
+    rays = np.array([[2.0, 2.0, 2.0, 0.0, 0.0, 1.0], [-1.0, 0.5, 0.5, -1.0, 0.0, 0.0]])
+    off, ids, *_ = tree.traverse(rays)
+    assert off.tolist() == [0, 0, 0]
+
+
+def test_traversal_many_hit_rays(ctx, oracle):
+    """Long-tailed hit lists: a dense 64^3 block, diagonal rays."""
+    pts = S.random_occupancy_points(64, 0.6, 3)
+    tree = P.SparseOctree.build(pts, P.GridConfig(64, dilation=1), ctx)
+    otree = oracle.tree_build(pts, 64, 1)
+    rays = S.random_rays(5, 300)
+    got, want = tree.traverse(rays), oracle.traverse(otree, rays)
+    assert np.diff(want[0]).max() > 100
+    _assert_hits_equal(got, want)
+
+
+def test_render_c1_fp32(c1, oracle, ctx):
+    tree, otree, cam, W, H = c1
+    model = P.Model(tree, seed=1, ctx=ctx)
+    om = oracle.init_model(otree, 1)
+    ft, fc, mt, mc = model.get_params()
+    assert np.array_equal(ft, om.ft) and np.array_equal(mt, om.mt) and np.array_equal(mc, om.mc)
+    st = P.RenderStats()
+    rgb, a, d = P.render_frame(model, P.Camera.from_record(cam, W, H), stats=st)
+    orgb, oa, od, ost = oracle.render_frame(otree, om, cam, W, H)
+    assert np.abs(rgb.reshape(-1) - orgb).max() <= TOL_FP32
+    assert np.abs(a.reshape(-1) - oa).max() <= TOL_FP32
+    assert np.abs(d.reshape(-1) - od).max() <= TOL_FP32
+    assert [st.rays, st.rays_with_hits, st.traversal_hits, st.thickness_queries, st.color_queries] == list(ost)
+    # the fp32 path keeps the reference's order: observed error is ulp-level
+    assert np.abs(rgb.reshape(-1) - orgb).max() <= 1e-5
+
+
+def test_render_background_and_rays_api(c1, oracle, ctx):
+    tree, otree, cam, W, H = c1
+    model = P.Model(tree, seed=3, ctx=ctx)
+    om = oracle.init_model(otree, 3)
+    rays = oracle.camera_rays(cam, W, H)[::7]
+    bg = np.array([0.2, 0.5, 0.9], np.float32)
+    rgb, a, d = P.render_rays(model, rays, background=bg)
+    orgb, oa, od, _ = oracle.render_rays(otree, om, rays, bg=bg)
+    assert np.abs(rgb.reshape(-1) - orgb).max() <= 1e-5
+    assert np.abs(d - od).max() <= 1e-5
+
+
+def test_render_rtmv_small_fp32(ctx, oracle):
+    """RTMV-shaped scene (20 objects), reduced sizes so the oracle finishes in seconds."""
+    sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=20, n_views=8, view_res=96, res=64, width=160)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    otree = oracle.tree_build(pts, res, dil)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    om = oracle.init_model(otree, 1)
+    st = P.RenderStats()
+    rgb, a, d = P.render_frame(model, P.Camera.from_record(cam, W, H), stats=st)
+    orgb, oa, od, ost = oracle.render_frame(otree, om, cam, W, H)
+    assert ost[2] > 10 * W  # a non-trivial number of hits
+    assert np.abs(rgb.reshape(-1) - orgb).max() <= 1e-5
+    assert np.abs(d.reshape(-1) - od).max() <= 1e-5
+    assert st.traversal_hits == ost[2] and st.rays_with_hits == ost[1]
