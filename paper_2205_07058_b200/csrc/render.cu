@@ -69,59 +69,6 @@ __global__ void k_pack_f32(const float* __restrict__ mt, const float* __restrict
     if (tid < 3) pack[kPack.c_b3 + tid] = mc[D::C_B3 + tid];
 }
 
-// ---- per-hit geometry (fp64, reference operand order) -------------------
-
-// parameterize_ray, src/render.cpp:16-28. Returns false on "tangent ray".
-__device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, const double* hi, float* r6) {
-    double c[3], oc[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        c[a] = dmul(dadd(lo[a], hi[a]), 0.5);
-        oc[a] = dsub(r.o[a], c[a]);
-    }
-    const double radius = dmul(dmul(0.5, __dsqrt_rn(3.0)), dsub(hi[0], lo[0]));
-    const double b = dot3(oc, r.d);
-    const double cc = dsub(dot3(oc, oc), dmul(radius, radius));
-    const double disc = dsub(dmul(b, b), cc);
-    if (disc < 1e-14) return false;
-    const double s = __dsqrt_rn(disc);
-    double p1[3], p2[3];
-    ray_at(r, dsub(-b, s), p1);
-    ray_at(r, dadd(-b, s), p2);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        p1[a] = dsub(p1[a], c[a]);
-        p2[a] = dsub(p2[a], c[a]);
-    }
-    const double n1 = __dsqrt_rn(dot3(p1, p1)), n2 = __dsqrt_rn(dot3(p2, p2));
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        r6[a] = float(ddiv(p1[a], n1));
-        r6[3 + a] = float(ddiv(p2[a], n2));
-    }
-    return true;
-}
-
-// local_coords + trilinear_weights (features.cpp:22-31, features.hpp:13-21).
-// Returns false on "point not in voxel".
-__device__ __forceinline__ bool trilinear_at(const double* p, const double* lo, const double* hi,
-                                             double h, float* w) {
-    double u[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (!(p[a] >= dsub(lo[a], 1e-7) && p[a] <= dadd(hi[a], 1e-7))) return false;
-        u[a] = fmin(fmax(ddiv(dsub(p[a], lo[a]), h), 0.0), 1.0);
-    }
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        const double wx = (b & 1) ? u[0] : dsub(1.0, u[0]);
-        const double wy = (b & 2) ? u[1] : dsub(1.0, u[1]);
-        const double wz = (b & 4) ? u[2] : dsub(1.0, u[2]);
-        w[b] = float(dmul(dmul(wx, wy), wz));
-    }
-    return true;
-}
-
 // z = sum_b w_b * row_b (b in order, fp32, no FMA) into a feature-major column.
 template <int DIM>
 __device__ __forceinline__ void gather_col(const float* __restrict__ vol, const uint32_t* corners,

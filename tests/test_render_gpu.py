@@ -136,3 +136,46 @@ def test_render_rtmv_small_fp32(ctx, oracle):
     assert np.abs(rgb.reshape(-1) - orgb).max() <= 1e-5
     assert np.abs(d.reshape(-1) - od).max() <= 1e-5
     assert st.traversal_hits == ost[2] and st.rays_with_hits == ost[1]
+
+
+def _psnr(a, b):
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return 99.0 if mse == 0 else 10.0 * np.log10(1.0 / mse)
+
+
+TOL_BF16_PSNR_DELTA = 0.05  # north_star: PSNR delta <= 0.05 dB with the bf16 MLP
+
+
+@pytest.mark.parametrize("objects", [4, 20])
+def test_render_bf16_tensor_core(ctx, oracle, objects):
+    """tcgen05 bf16 decoder vs the fp32 oracle: PSNR(vs GT) delta <= 0.05 dB."""
+    sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=objects, n_views=8, view_res=96, res=64, width=192)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    otree = oracle.tree_build(pts, res, dil)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    om = oracle.init_model(otree, 1)
+    st = P.RenderStats()
+    rgb, a, d = P.render_frame(model, P.Camera.from_record(cam, W, H), stats=st, precision="bf16")
+    orgb, oa, od, ost = oracle.render_frame(otree, om, cam, W, H)
+    gt, _, _ = S.render_gt(sc, cam, W, H)
+    p16, p32, pv = _psnr(rgb.reshape(-1), gt), _psnr(orgb, gt), _psnr(rgb.reshape(-1), orgb)
+    print(f"objects={objects} psnr_bf16={p16:.4f} psnr_oracle={p32:.4f} psnr_bf16_vs_oracle={pv:.2f} "
+          f"maxabs_rgb={np.abs(rgb.reshape(-1) - orgb).max():.3g} maxabs_depth={np.abs(d.reshape(-1) - od).max():.3g}")
+    assert abs(p16 - p32) <= TOL_BF16_PSNR_DELTA
+    assert pv > 40.0  # bf16 vs fp32 image agreement
+    assert np.abs(a.reshape(-1) - oa).max() < 2e-2
+    assert st.traversal_hits == ost[2]
+
+
+def test_render_bf16_matches_fp32_path(c1, ctx):
+    tree, otree, cam, W, H = c1
+    model = P.Model(tree, seed=1, ctx=ctx)
+    camera = P.Camera.from_record(cam, W, H)
+    r32, a32, d32 = P.render_frame(model, camera, precision="fp32")
+    r16, a16, d16 = P.render_frame(model, camera, precision="bf16")
+    print(f"c1 bf16 vs fp32 psnr={_psnr(r16, r32):.2f} maxabs={np.abs(r16 - r32).max():.3g}")
+    assert _psnr(r16, r32) > 40.0
+    # depth = sum(w t_s) / alpha is ill-conditioned near the 1e-4 alpha cut; compare where alpha is material
+    m = (a32 > 1e-2) & (a16 > 1e-2)
+    assert m.sum() > 1000
+    assert np.abs(d16 - d32)[m].max() < 5e-2
