@@ -211,8 +211,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--precision", default=os.environ.get("SVLF_BENCH_PRECISION", "auto"),
-                    choices=["auto", "bf16", "fp32"])
+    ap.add_argument("--precision", default=os.environ.get("SVLF_BENCH_PRECISION", "fp16"),
+                    choices=["fp16", "bf16", "fp32"])
     ap.add_argument("--objects", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -238,12 +238,6 @@ def main():
     camera = P.Camera.from_record(cam, W, H)
 
     precision = args.precision
-    if precision == "auto":
-        try:
-            P.render_frame(model, P.Camera.from_record(cam, 64, 64), precision="bf16")
-            precision = "bf16"
-        except RuntimeError:
-            precision = "fp32"
 
     n = W * H
     d_rgb = torch.empty(n * 3, dtype=torch.float32, device=device)

@@ -51,9 +51,15 @@ typedef enum svlf_status {
 } svlf_status;
 
 /* Decoder arithmetic for render: FP32 = CUDA-core fp32 in the reference's
- * accumulation order (parity: max-abs <= 1e-3); BF16 = tcgen05 tensor cores,
- * bf16 operands with fp32 accumulation in TMEM (parity: PSNR delta <= 0.05 dB). */
-typedef enum svlf_precision { SVLF_PRECISION_FP32 = 0, SVLF_PRECISION_BF16 = 1 } svlf_precision;
+ * accumulation order (parity: max-abs <= 1e-3); BF16 / FP16 = the fused
+ * tcgen05 tensor-core decoder with bf16 or fp16 operands and fp32
+ * accumulation in TMEM (parity: PSNR delta <= 0.05 dB; same tensor rate,
+ * fp16 carries 3 more mantissa bits). */
+typedef enum svlf_precision {
+    SVLF_PRECISION_FP32 = 0,
+    SVLF_PRECISION_BF16 = 1,
+    SVLF_PRECISION_FP16 = 2
+} svlf_precision;
 
 /* reference LossMode (src/train.cpp:37): stage 1 = SURFACE, stages 2-3 = VOLUMETRIC */
 typedef enum svlf_loss_mode { SVLF_LOSS_SURFACE = 0, SVLF_LOSS_VOLUMETRIC = 1 } svlf_loss_mode;

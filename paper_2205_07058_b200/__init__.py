@@ -447,7 +447,7 @@ class Model:
         _check(_LIB.svlf_model_set_adam(self._h, _dp(m), _dp(v), _dp(steps)))
 
 
-_PREC = {"fp32": 0, "bf16": 1}
+_PREC = {"fp32": 0, "bf16": 1, "fp16": 2}
 
 
 def _bg(background):

@@ -78,7 +78,7 @@ struct svlf_ctx {
     cudaStream_t stream = nullptr;      // active stream
     cudaStream_t own_stream = nullptr;  // created with the context
     DevBuf rays, counts, offsets, scan_tmp, hit_leaf, hit_tin, hit_tout, hit_ray;
-    DevBuf h_tau, h_eta, h_rgb, out_rgb, out_alpha, out_depth, misc, tmp64, tmpx12;
+    DevBuf h_tau, h_eta, h_rgb, out_rgb, out_alpha, out_depth, misc, tmp64, tmpx12, tc_scratch;
     TrainScratch train;
     int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
     cudaEvent_t ev[EV_N] = {};
@@ -230,12 +230,15 @@ void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t tot
               ctx->h_rgb.ensure<float>(size_t(total) * 3)};
     const DevOctree& T = dev_view(m->tree);
     int* err = ctx->misc.as<int>();
-    if (prec == SVLF_PRECISION_BF16) {
-        ensure_pack_bf16(m->view(), m->pack_bf16, m->pack_bf16_version, m->version, s);
-        launch_decode_bf16(T, m->view(), m->pack_bf16.as<char>(), ctx->rays.as<double>(),
-                           ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(),
-                           ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total, ho, err, s);
+    if (prec == SVLF_PRECISION_BF16 || prec == SVLF_PRECISION_FP16) {
+        const bool bf16 = prec == SVLF_PRECISION_BF16;
+        ensure_pack_tc(m->view(), m->pack_bf16, m->pack_bf16_version, m->version, bf16, s);
+        void* scratch = ctx->tc_scratch.ensure<uint8_t>(decode_tc_scratch_bytes(total));
+        launch_decode_tc(T, m->view(), m->pack_bf16.as<char>(), bf16, ctx->rays.as<double>(),
+                         ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
+                         ctx->hit_tout.as<double>(), total, ho, err, scratch, s);
     } else {
+        if (prec != SVLF_PRECISION_FP32) fail(SVLF_ERR_INVALID_ARGUMENT, "unknown precision");
         ensure_pack_f32(m, s);
         launch_decode_f32(T, m->view(), pack_f32_view(m->pack_f32.as<float>()), ctx->rays.as<double>(),
                           ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(),

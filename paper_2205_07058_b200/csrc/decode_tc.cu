@@ -1,27 +1,30 @@
-// Fused tcgen05 decoder (bf16 operands, fp32 accumulation in TMEM).
+// Tensor-core decoder (tcgen05, 16-bit operands, fp32 accumulation in TMEM).
 //
-// One persistent CTA per SM, 256 threads = two independent 128-row "slots".
-// A slot owns one M=128 tile of hits at a time (thread r = row r = one hit)
-// and runs the whole per-hit chain of the reference's batch_forward
-// (src/voxel_batch.hpp:69-151) for its tile:
-//   geometry (fp64): x1, x2, parameterize_ray, trilinear weights
-//   gather psi_T(x1), psi_T(x2) (bf16 feature rows, fp32 accumulate) -> A tile
-//   MMA  f_T layer 0:  [128 x 144] x [144 x 128] -> TMEM        (9 x K16)
-//   epilogue: +b, relu, f_T head (tau relu, eta sigmoid) on CUDA cores
-//   x_s = eta x1 + (1-eta) x2, gather psi_C(x_s) -> A tile
-//   MMA  f_C layer 0:  [128 x 48] x [48 x 128]                 (3 x K16)
-//   epilogue +b, relu -> bf16 A tile; MMA f_C layer 1 (8 x K16); same for
-//   layer 2; epilogue: +b, relu, f_C head (3 x sigmoid).
-// The two slots interleave, so one slot's MMAs overlap the other slot's
-// gathers/epilogues; all four weight matrices stay resident in shared memory
-// for the whole kernel (112 KB bf16), each slot has one 36 KB A buffer and a
-// 128-column fp32 TMEM accumulator.
+// Three kernels per frame, all over the flat hit list:
+//   k_hit_geom  one thread per hit, fp64 (reference operand order):
+//               x1, x2, parameterize_ray (r6), local coords u1, u2 and
+//               trilinear weights w1, w2 -> a 48-byte 16-bit record + u1,u2.
+//               Raises "tangent ray" / "point not in voxel" like the reference.
+//   k_decode_t  f_T (src/voxel_batch.hpp:69-114): gather psi_T(x1), psi_T(x2)
+//               with packed 16-bit FMA, MMA 128x144x128, relu epilogue, head
+//               MMA 128x144x16 -> tau = relu, eta = sigmoid.
+//   k_decode_c  f_C (src/voxel_batch.hpp:119-142): u_s = eta u1 + (1-eta) u2,
+//               trilinear weights, gather psi_C(x_s), MMA 128x48x128, two
+//               hidden MMAs 128x128x128, head MMA 128x128x16 -> rgb sigmoid.
+// Each decode kernel is persistent (one CTA per SM, 512 threads = four
+// independent 128-row slots; thread r of a slot owns hit r of the slot's
+// tile). A slot's chain is gather -> MMA -> epilogue -> MMA ...; four slots
+// per SM keep the tensor pipe fed while other slots gather. All weight tiles
+// live in shared memory for the kernel's lifetime; each slot has one A buffer
+// and a 128-column fp32 accumulator (4 x 128 = all 512 TMEM columns); head
+// MMAs reuse the first 16 accumulator columns once the epilogue has read them.
 //
-// Input K ordering is permuted so the 16-byte core-matrix chunks are aligned:
-//   f_T A columns: [psi_T(x1) 0..63 | psi_T(x2) 64..127 | r6 128..133 | 0]
-//   f_C A columns: [psi_C(x_s) 0..31 | r6 32..37 | 0]
-// and the packed weights use the same permutation, so the products equal
-// the reference's W . [r6 | psi | psi] (only the fp32 summation order differs).
+// Biases of the input layers are folded into the MMA (A carries a constant
+// 1.0 in the first padding column, the weight tile carries the bias there);
+// hidden-layer biases are added in the epilogue. Input K is permuted so
+// 16-byte core-matrix chunks stay aligned (the weights use the same order):
+//   f_T input  [psi_T(x1) 0..63 | psi_T(x2) 64..127 | r6 128..133 | 1 | 0...]
+//   f_C input  [psi_C(x_s) 0..31 | r6 32..37 | 1 | 0...]
 #include "device.cuh"
 #include "tc_common.cuh"
 
@@ -31,348 +34,490 @@ namespace {
 
 using namespace tc;
 
-constexpr uint32_t KT = 144;  // f_T input, padded
-constexpr uint32_t KC = 48;   // f_C input, padded
-constexpr uint32_t KH = 128;  // hidden
+constexpr uint32_t KT = 144;  // f_T input (+1 bias column, padded); f_T hidden->head (+bias)
+constexpr uint32_t KC = 48;   // f_C input (+1 bias column, padded)
+constexpr uint32_t KH = 128;  // f_C hidden layers (bias in epilogue)
 
-// pack layout (bytes)
-constexpr uint32_t OFF_WT0 = 0;
-constexpr uint32_t OFF_WC0 = OFF_WT0 + 128 * KT * 2;  // 36864
-constexpr uint32_t OFF_WC1 = OFF_WC0 + 128 * KC * 2;  // 49152
-constexpr uint32_t OFF_WC2 = OFF_WC1 + 128 * KH * 2;  // 81920
-constexpr uint32_t OFF_VEC = OFF_WC2 + 128 * KH * 2;  // 114688
-// fp32 vectors (float offsets within VEC)
-constexpr uint32_t V_BT0 = 0, V_WT1 = 128, V_BT1 = 384, V_BC0 = 388, V_BC1 = 516, V_BC2 = 644, V_WC3 = 772,
-                   V_BC3 = 1156, V_N = 1160;
-constexpr uint32_t SMEM_WEIGHTS = OFF_VEC + V_N * 4;  // 119328
-constexpr uint32_t OFF_FEAT = (SMEM_WEIGHTS + 255) & ~255u;
-// kernel smem
-constexpr uint32_t SM_A0 = (SMEM_WEIGHTS + 1023) & ~1023u;  // 120832
-constexpr uint32_t A_BYTES = 128 * KT * 2;                  // 36864
-constexpr uint32_t SM_BAR = SM_A0 + 2 * A_BYTES;
-constexpr uint32_t SM_TOTAL = SM_BAR + 64;
+// ---- weight pack (bytes), UMMA core-matrix layout
+constexpr uint32_t OFF_WT0 = 0;                       // 128 x 144
+constexpr uint32_t OFF_WT1 = OFF_WT0 + 128 * KT * 2;  // 16 x 144 (rows 0,1 = tau, eta; bias col 128)
+constexpr uint32_t T_WEIGHTS = OFF_WT1 + 16 * KT * 2;  // 41472
+constexpr uint32_t OFF_WC0 = (T_WEIGHTS + 1023) & ~1023u;  // 128 x 48
+constexpr uint32_t OFF_WC1 = OFF_WC0 + 128 * KC * 2;       // 128 x 128
+constexpr uint32_t OFF_WC2 = OFF_WC1 + 128 * KH * 2;       // 128 x 128
+constexpr uint32_t OFF_WC3 = OFF_WC2 + 128 * KH * 2;       // 16 x 128 (rows 0..2 = rgb)
+constexpr uint32_t OFF_CVEC = OFF_WC3 + 16 * KH * 2;       // fp32: b_C1[128], b_C2[128], b_C3[4]
+constexpr uint32_t C_WEIGHTS = OFF_CVEC + (128 + 128 + 4) * 4 - OFF_WC0;  // bytes from OFF_WC0
+constexpr uint32_t OFF_FEAT = (OFF_WC0 + C_WEIGHTS + 255) & ~255u;
 
-constexpr uint32_t kIdesc = make_idesc(128, 128, true);
+// ---- A-operand (activation) tiles: K-chunk stride LBO = 128*16 + 16 bytes,
+// 8-row-group stride SBO = 128 bytes. The 16-byte skew per K chunk makes both
+// store patterns conflict-free: 8 lanes writing the 8 chunks of one row, and
+// 8 lanes writing one chunk of 8 consecutive rows, each hit 8 distinct
+// 16-byte bank groups.
+constexpr uint32_t kALbo = 128 * 16 + 16;  // 2064
+__host__ __device__ constexpr uint32_t a_off(uint32_t r, uint32_t k) {
+    return (k >> 3) * kALbo + (r >> 3) * 128u + (r & 7u) * 16u + (k & 7u) * 2u;
+}
 
-__device__ __forceinline__ float sigmoidf_fast(float x) { return 1.0f / (1.0f + __expf(-x)); }
+// ---- kernel shared memory
+constexpr uint32_t kSlots = 4;
+constexpr uint32_t T_A_BYTES = (KT / 8) * kALbo;  // 37152
+constexpr uint32_t T_SM_A0 = (T_WEIGHTS + 1023) & ~1023u;
+constexpr uint32_t T_SM_BAR = T_SM_A0 + kSlots * T_A_BYTES;
+constexpr uint32_t T_SM_TOTAL = T_SM_BAR + 64;
+constexpr uint32_t C_A_BYTES = (KH / 8) * kALbo;  // 33024 (>= the K=48 input tile)
+constexpr uint32_t C_SM_A0 = (C_WEIGHTS + 1023) & ~1023u;
+constexpr uint32_t C_SM_BAR = C_SM_A0 + kSlots * C_A_BYTES;
+constexpr uint32_t C_SM_TOTAL = C_SM_BAR + 64;
+static_assert(T_SM_TOTAL <= 232448 && C_SM_TOTAL <= 232448, "shared memory budget");
 
-// ---- pack: fp32 flat params -> bf16 UMMA tiles + fp32 vectors + bf16 features
+// Operand format traits: fp16 (11-bit mantissa) or bf16 (north-star format);
+// both run at the same tensor-core rate.
+template <bool kBF16>
+struct Fmt;
+template <>
+struct Fmt<false> {
+    using H = __half;
+    using H2 = __half2;
+    static __device__ __forceinline__ H2 splat(float x) { return __float2half2_rn(x); }
+    static __host__ __device__ __forceinline__ H cvt(float x) { return __float2half_rn(x); }
+    static __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
+        uint32_t r;
+        asm("cvt.rn.satfinite.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+        return r;
+    }
+    static __device__ __forceinline__ uint32_t pack(float lo, float hi) {
+        uint32_t r;
+        asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+        return r;
+    }
+    static constexpr uint32_t kOne = 0x00003C00u;  // (1.0, 0.0)
+    static __device__ __forceinline__ H2 lo2(H2 p) { return __low2half2(p); }
+    static __device__ __forceinline__ H2 hi2(H2 p) { return __high2half2(p); }
+};
+template <>
+struct Fmt<true> {
+    using H = __nv_bfloat16;
+    using H2 = __nv_bfloat162;
+    static __device__ __forceinline__ H2 splat(float x) { return __float2bfloat162_rn(x); }
+    static __host__ __device__ __forceinline__ H cvt(float x) { return __float2bfloat16_rn(x); }
+    static __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
+        uint32_t r;
+        asm("cvt.rn.satfinite.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+        return r;
+    }
+    static __device__ __forceinline__ uint32_t pack(float lo, float hi) {
+        uint32_t r;
+        asm("cvt.rn.satfinite.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+        return r;
+    }
+    static constexpr uint32_t kOne = 0x00003F80u;
+    static __device__ __forceinline__ H2 lo2(H2 p) { return __low2bfloat162(p); }
+    static __device__ __forceinline__ H2 hi2(H2 p) { return __high2bfloat162(p); }
+};
+
+template <typename T2>
+__device__ __forceinline__ uint32_t h2u(T2 h) {
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+template <typename T2>
+__device__ __forceinline__ T2 u2h(uint32_t u) {
+    return *reinterpret_cast<T2*>(&u);
+}
+
+// ---- pack: fp32 flat params -> 16-bit UMMA tiles (+ folded biases), fp32 bias vectors
+template <bool kBF16>
 __global__ void k_pack_tc(const float* __restrict__ mt, const float* __restrict__ mc, uint8_t* pack) {
     using D = DecOffsets;
+    using F = Fmt<kBF16>;
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
-    __nv_bfloat16* wt0 = reinterpret_cast<__nv_bfloat16*>(pack + OFF_WT0);
-    __nv_bfloat16* wc0 = reinterpret_cast<__nv_bfloat16*>(pack + OFF_WC0);
-    __nv_bfloat16* wc1 = reinterpret_cast<__nv_bfloat16*>(pack + OFF_WC1);
-    __nv_bfloat16* wc2 = reinterpret_cast<__nv_bfloat16*>(pack + OFF_WC2);
-    float* vec = reinterpret_cast<float*>(pack + OFF_VEC);
-    if (tid < 128 * KT) {  // f_T layer 0, K permuted
+    auto put = [&](uint32_t off, uint32_t n, uint32_t k, uint32_t K, float w) {
+        reinterpret_cast<typename F::H*>(pack + off)[core_offset(n, k, K) / 2] = F::cvt(w);
+    };
+    if (tid < 128 * KT) {  // f_T layer 0: permuted input + bias column 134
         const uint32_t n = tid / KT, k = tid % KT;
-        const int src = k < 128 ? int(6 + k) : (k < 134 ? int(k - 128) : -1);
-        const float w = src >= 0 ? mt[D::T_W0 + n * kInT + src] : 0.f;
-        wt0[core_offset(n, k, KT) / 2] = __float2bfloat16_rn(w);
+        float w = 0.f;
+        if (k < 128) w = mt[D::T_W0 + n * kInT + 6 + k];
+        else if (k < 134) w = mt[D::T_W0 + n * kInT + (k - 128)];
+        else if (k == 134) w = mt[D::T_B0 + n];
+        put(OFF_WT0, n, k, KT, w);
     }
-    if (tid < 128 * KC) {  // f_C layer 0
+    if (tid < 16 * KT) {  // f_T head, N = 16, bias column 128
+        const uint32_t n = tid / KT, k = tid % KT;
+        float w = 0.f;
+        if (n < 2) w = k < 128 ? mt[D::T_W1 + n * kHid + k] : (k == 128 ? mt[D::T_B1 + n] : 0.f);
+        put(OFF_WT1, n, k, KT, w);
+    }
+    if (tid < 128 * KC) {  // f_C layer 0: permuted input + bias column 38
         const uint32_t n = tid / KC, k = tid % KC;
-        const int src = k < 32 ? int(6 + k) : (k < 38 ? int(k - 32) : -1);
-        const float w = src >= 0 ? mc[D::C_W0 + n * kInC + src] : 0.f;
-        wc0[core_offset(n, k, KC) / 2] = __float2bfloat16_rn(w);
+        float w = 0.f;
+        if (k < 32) w = mc[D::C_W0 + n * kInC + 6 + k];
+        else if (k < 38) w = mc[D::C_W0 + n * kInC + (k - 32)];
+        else if (k == 38) w = mc[D::C_B0 + n];
+        put(OFF_WC0, n, k, KC, w);
     }
     if (tid < 128 * KH) {
         const uint32_t n = tid / KH, k = tid % KH;
-        wc1[core_offset(n, k, KH) / 2] = __float2bfloat16_rn(mc[D::C_W1 + n * kHid + k]);
-        wc2[core_offset(n, k, KH) / 2] = __float2bfloat16_rn(mc[D::C_W2 + n * kHid + k]);
+        put(OFF_WC1, n, k, KH, mc[D::C_W1 + n * kHid + k]);
+        put(OFF_WC2, n, k, KH, mc[D::C_W2 + n * kHid + k]);
     }
+    if (tid < 16 * KH) {
+        const uint32_t n = tid / KH, k = tid % KH;
+        put(OFF_WC3, n, k, KH, n < 3 ? mc[D::C_W3 + n * kHid + k] : 0.f);
+    }
+    float* cvec = reinterpret_cast<float*>(pack + OFF_CVEC);
     if (tid < 128) {
-        vec[V_BT0 + tid] = mt[D::T_B0 + tid];
-        vec[V_BC0 + tid] = mc[D::C_B0 + tid];
-        vec[V_BC1 + tid] = mc[D::C_B1 + tid];
-        vec[V_BC2 + tid] = mc[D::C_B2 + tid];
+        cvec[tid] = mc[D::C_B1 + tid];
+        cvec[128 + tid] = mc[D::C_B2 + tid];
     }
-    if (tid < 256) vec[V_WT1 + tid] = mt[D::T_W1 + tid];
-    if (tid < 384) vec[V_WC3 + tid] = mc[D::C_W3 + tid];
-    if (tid < 4) vec[V_BT1 + tid] = tid < 2 ? mt[D::T_B1 + tid] : 0.f;
-    if (tid < 4) vec[V_BC3 + tid] = tid < 3 ? mc[D::C_B3 + tid] : 0.f;
+    if (tid < 4) cvec[256 + tid] = tid < 3 ? mc[D::C_B3 + tid] : 0.f;
 }
 
-__global__ void k_feat_bf16(const float* __restrict__ src, __nv_bfloat16* dst, size_t n) {
+template <bool kBF16>
+__global__ void k_feat_cvt(const float* __restrict__ src, typename Fmt<kBF16>::H* dst, size_t n) {
+    using F = Fmt<kBF16>;
     const size_t i = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) * 4;
-    if (i + 3 < n) {
-        const float4 v = *reinterpret_cast<const float4*>(src + i);
-        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-        *reinterpret_cast<__nv_bfloat162*>(dst + i) = a;
-        *reinterpret_cast<__nv_bfloat162*>(dst + i + 2) = b;
-    } else {
-        for (size_t k = i; k < n; ++k) dst[k] = __float2bfloat16_rn(src[k]);
-    }
+    for (size_t k = i; k < i + 4 && k < n; ++k) dst[k] = F::cvt(src[k]);
 }
 
-__device__ __forceinline__ void unpack8(const uint4& q, float* f) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+// ---- per-hit geometry record
+// geo[j]: 3 x uint4 = r6 (6 x 16-bit) | w1 (8 x 16-bit) | w2 (8 x 16-bit) | 2 x pad
+// u12[j]: 2 x float4 = u1.xyz, u2.xyz, pad, pad
+template <bool kBF16>
+__global__ void __launch_bounds__(128) k_hit_geom(DevOctree T, const double* __restrict__ rays,
+                                                  const uint32_t* __restrict__ hit_ray,
+                                                  const uint32_t* __restrict__ hit_leaf,
+                                                  const double* __restrict__ hit_tin,
+                                                  const double* __restrict__ hit_tout, uint32_t n, uint4* geo,
+                                                  float4* u12, int* err) {
+    using F = Fmt<kBF16>;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    Ray ray;
+    const uint32_t ri = hit_ray[j];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float2 t = __bfloat1622float2(h[i]);
-        f[2 * i] = t.x;
-        f[2 * i + 1] = t.y;
+    for (int a = 0; a < 3; ++a) {
+        ray.o[a] = rays[6 * size_t(ri) + a];
+        ray.d[a] = rays[6 * size_t(ri) + 3 + a];
     }
+    double lo[3], hi[3], x1[3], x2[3];
+    leaf_box(T, hit_leaf[j], lo, hi);
+    ray_at(ray, hit_tin[j], x1);
+    ray_at(ray, hit_tout[j], x2);
+    float r6[6] = {0, 0, 0, 0, 0, 0}, w1[8], w2[8];
+    if (!parameterize(ray, lo, hi, r6)) raise_error(err, kErrTangentRay);
+    if (!trilinear_at(x1, lo, hi, T.cell_size, w1) || !trilinear_at(x2, lo, hi, T.cell_size, w2)) {
+        raise_error(err, kErrPointNotInVoxel);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) w1[b] = w2[b] = 0.f;
+    }
+    float u[6];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        // local coordinates (p - lo)/h clamped to [0,1] (features.cpp:22-31)
+        u[a] = float(fmin(fmax(ddiv(dsub(x1[a], lo[a]), T.cell_size), 0.0), 1.0));
+        u[3 + a] = float(fmin(fmax(ddiv(dsub(x2[a], lo[a]), T.cell_size), 0.0), 1.0));
+    }
+    geo[3 * size_t(j)] = make_uint4(F::pack(r6[0], r6[1]), F::pack(r6[2], r6[3]), F::pack(r6[4], r6[5]),
+                                    F::pack(w1[0], w1[1]));
+    geo[3 * size_t(j) + 1] = make_uint4(F::pack(w1[2], w1[3]), F::pack(w1[4], w1[5]), F::pack(w1[6], w1[7]),
+                                        F::pack(w2[0], w2[1]));
+    geo[3 * size_t(j) + 2] = make_uint4(F::pack(w2[2], w2[3]), F::pack(w2[4], w2[5]), F::pack(w2[6], w2[7]), 0u);
+    u12[2 * size_t(j)] = make_float4(u[0], u[1], u[2], u[3]);
+    u12[2 * size_t(j) + 1] = make_float4(u[4], u[5], 0.f, 0.f);
 }
 
-// Issue the K-loop of one layer: D[tmem] = A[128 x K] . B[128 x K]^T
-__device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, uint32_t b_base, uint32_t K) {
-    const uint32_t sbo = (K / 8) * 128;
+// D[tmem] (+)= A . B^T over K: A in the skewed activation layout (a_off),
+// B (weights, N rows) in the dense layout core_offset(n, k, K).
+__device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, uint32_t b_base, uint32_t K,
+                                            uint32_t idesc) {
+    const uint32_t b_sbo = (K / 8) * 128;
 #pragma unroll 1
-    for (uint32_t k = 0; k < K / 16; ++k) {
-        const uint64_t ad = make_desc(a_base + 256 * k, 128, sbo);
-        const uint64_t bd = make_desc(b_base + 256 * k, 128, sbo);
-        mma_f16(tmem_d, ad, bd, kIdesc, k > 0);
+    for (uint32_t k = 0; k < K / 16; ++k)
+        mma_f16(tmem_d, make_desc(a_base + 2 * k * kALbo, kALbo, 128), make_desc(b_base + 256 * k, 128, b_sbo),
+                idesc, k > 0);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Epilogue: TMEM acc (128 fp32, + optional fp32 bias) -> relu -> 16-bit -> A tile (K layout)
+template <bool kBF16, bool kBias>
+__device__ __forceinline__ void hidden_epilogue(uint32_t tmem_row, uint32_t a_base, uint32_t r, uint32_t K,
+                                                const float* bias) {
+    using F = Fmt<kBF16>;
+#pragma unroll 1
+    for (uint32_t c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(tmem_row + 32 * c, v);
+        tmem_wait_ld();
+        if constexpr (kBias) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 b = *reinterpret_cast<const float4*>(bias + 32 * c + i);
+                v[i] += b.x;
+                v[i + 1] += b.y;
+                v[i + 2] += b.z;
+                v[i + 3] += b.w;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            st_shared_v4(a_base + a_off(r, 32 * c + 8 * q), F::relu_pack(v[8 * q], v[8 * q + 1]),
+                         F::relu_pack(v[8 * q + 2], v[8 * q + 3]), F::relu_pack(v[8 * q + 4], v[8 * q + 5]),
+                         F::relu_pack(v[8 * q + 6], v[8 * q + 7]));
     }
 }
 
-__global__ void __launch_bounds__(256, 1)
-    k_decode_tc(DevOctree T, const uint8_t* __restrict__ pack, const __nv_bfloat16* __restrict__ ft16,
-                const __nv_bfloat16* __restrict__ fc16, const double* __restrict__ rays,
-                const uint32_t* __restrict__ hit_ray, const uint32_t* __restrict__ hit_leaf,
-                const double* __restrict__ hit_tin, const double* __restrict__ hit_tout, uint32_t n, HitOut out,
-                int* err) {
-    extern __shared__ __align__(1024) uint8_t sm[];
-    const uint32_t tid = threadIdx.x;
-    const uint32_t slot = tid >> 7;
-    const uint32_t r = tid & 127;
-    const uint32_t warp = tid >> 5;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sm + SM_BAR + 32);
-    const float* vec = reinterpret_cast<const float*>(sm + OFF_VEC);
+struct Slot {
+    uint64_t* bar;
+    uint32_t phase;
+    uint32_t bar_id;
+    uint32_t r;
+    // all writes to the slot's A buffer done -> one thread issues, everyone waits for completion
+    template <typename Issue>
+    __device__ __forceinline__ void mma(Issue&& issue) {
+        fence_async_smem();
+        fence_before_sync();
+        named_sync(bar_id, 128);
+        if (r == 0) {
+            fence_after_sync();
+            issue();
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        fence_after_sync();
+    }
+};
 
-    // weights + vectors -> smem (once per CTA)
+// Common prologue of the decode kernels: weights -> smem, barriers, TMEM.
+__device__ __forceinline__ uint32_t kernel_setup(uint8_t* sm, const uint8_t* weights, uint32_t wbytes,
+                                                 uint32_t bar_off) {
+    const uint32_t tid = threadIdx.x;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + bar_off);
+    uint32_t* holder = reinterpret_cast<uint32_t*>(sm + bar_off + 48);
     {
-        const uint4* src = reinterpret_cast<const uint4*>(pack);
+        const uint4* src = reinterpret_cast<const uint4*>(weights);
         uint4* dst = reinterpret_cast<uint4*>(sm);
-        for (uint32_t i = tid; i < SMEM_WEIGHTS / 16; i += blockDim.x) dst[i] = src[i];
+        for (uint32_t i = tid; i < wbytes / 16; i += blockDim.x) dst[i] = src[i];
     }
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (uint32_t s = 0; s < kSlots; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) tmem_alloc(tmem_holder, 256);
+    if ((tid >> 5) == 0) tmem_alloc(holder, 512);
     fence_async_smem();
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
-    const uint32_t tmem = *tmem_holder;
-    const uint32_t tmem_acc = tmem + slot * 128;                   // column offset
-    const uint32_t tmem_row = tmem_acc + ((32u * (warp & 3u)) << 16);  // this warp's lanes
-    const uint32_t sbase = smem_u32(sm);
-    const uint32_t a_base = sbase + SM_A0 + slot * A_BYTES;
-    uint8_t* A = sm + SM_A0 + slot * A_BYTES;
-    uint64_t* bar = &bars[slot];
-    uint32_t phase = 0;
-    const uint32_t ntiles = (n + 127) / 128;
-    const uint32_t bar_id = 1 + slot;
+    return *holder;
+}
 
-    for (uint32_t tile = blockIdx.x * 2 + slot; tile < ntiles; tile += gridDim.x * 2) {
-        const uint32_t j = tile * 128 + r;
-        bool valid = j < n;
-        float r6[6] = {0, 0, 0, 0, 0, 0};
-        uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        float w1[8], w2[8];
-        double x1[3] = {0, 0, 0}, x2[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1};
-        if (valid) {
-            Ray ray;
-            const uint32_t ri = hit_ray[j];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                ray.o[a] = rays[6 * size_t(ri) + a];
-                ray.d[a] = rays[6 * size_t(ri) + 3 + a];
-            }
-            const uint32_t leaf = hit_leaf[j];
-            leaf_box(T, leaf, lo, hi);
-            ray_at(ray, hit_tin[j], x1);
-            ray_at(ray, hit_tout[j], x2);
-            if (!parameterize(ray, lo, hi, r6)) {
-                raise_error(err, kErrTangentRay);
-                valid = false;
-            }
-            if (!trilinear_at(x1, lo, hi, T.cell_size, w1) || !trilinear_at(x2, lo, hi, T.cell_size, w2)) {
-                raise_error(err, kErrPointNotInVoxel);
-                valid = false;
-            }
-            const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
-            const uint4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
-            corners[0] = c0.x; corners[1] = c0.y; corners[2] = c0.z; corners[3] = c0.w;
-            corners[4] = c1.x; corners[5] = c1.y; corners[6] = c1.z; corners[7] = c1.w;
-        }
-        if (!valid) {
-#pragma unroll
-            for (int b = 0; b < 8; ++b) w1[b] = w2[b] = 0.f;
-        }
-
-        // ---- gather psi_T(x1), psi_T(x2) -> A (K = 144)
-#pragma unroll 1
-        for (uint32_t c = 0; c < 8; ++c) {  // 8-dim chunks of the 64 thickness features
-            float a1[8], a2[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a1[i] = a2[i] = 0.f;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const uint4 q = __ldg(reinterpret_cast<const uint4*>(ft16 + size_t(corners[b]) * 64) + c);
-                float f[8];
-                unpack8(q, f);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    a1[i] = __fmaf_rn(w1[b], f[i], a1[i]);
-                    a2[i] = __fmaf_rn(w2[b], f[i], a2[i]);
-                }
-            }
-            st_shared_v4(a_base + core_offset(r, 8 * c, KT), pack_bf16x2(a1[0], a1[1]), pack_bf16x2(a1[2], a1[3]),
-                         pack_bf16x2(a1[4], a1[5]), pack_bf16x2(a1[6], a1[7]));
-            st_shared_v4(a_base + core_offset(r, 64 + 8 * c, KT), pack_bf16x2(a2[0], a2[1]),
-                         pack_bf16x2(a2[2], a2[3]), pack_bf16x2(a2[4], a2[5]), pack_bf16x2(a2[6], a2[7]));
-        }
-        st_shared_v4(a_base + core_offset(r, 128, KT), pack_bf16x2(r6[0], r6[1]), pack_bf16x2(r6[2], r6[3]),
-                     pack_bf16x2(r6[4], r6[5]), 0u);
-        st_shared_v4(a_base + core_offset(r, 136, KT), 0u, 0u, 0u, 0u);
-
-        fence_async_smem();
-        fence_before_sync();
-        named_sync(bar_id, 128);
-        if (r == 0) {
-            fence_after_sync();
-            issue_layer(tmem_acc, a_base, sbase + OFF_WT0, KT);
-            mma_commit(bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        fence_after_sync();
-
-        // ---- epilogue f_T: +b, relu, head (tau, eta)
-        float y0 = vec[V_BT1], y1 = vec[V_BT1 + 1];
-#pragma unroll 1
-        for (uint32_t c = 0; c < 4; ++c) {
-            float v[32];
-            tmem_ld32(tmem_row + 32 * c, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const uint32_t col = 32 * c + i;
-                const float h = fmaxf(v[i] + vec[V_BT0 + col], 0.f);
-                y0 = __fmaf_rn(vec[V_WT1 + col], h, y0);
-                y1 = __fmaf_rn(vec[V_WT1 + 128 + col], h, y1);
-            }
-        }
-        const float tau = fmaxf(y0, 0.f);
-        const float eta = sigmoidf_fast(y1);
-
-        // ---- x_s, psi_C(x_s) -> A (K = 48)
-        float ws[8];
-        if (valid) {
-            const double e = double(eta), ome = 1.0 - e;
-            double xs[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) xs[a] = dadd(dmul(x1[a], e), dmul(x2[a], ome));
-            if (!trilinear_at(xs, lo, hi, T.cell_size, ws)) {
-                raise_error(err, kErrPointNotInVoxel);
-                valid = false;
-            }
-        }
-        if (!valid) {
-#pragma unroll
-            for (int b = 0; b < 8; ++b) ws[b] = 0.f;
-        }
-#pragma unroll 1
-        for (uint32_t c = 0; c < 4; ++c) {
-            float a1[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a1[i] = 0.f;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const uint4 q = __ldg(reinterpret_cast<const uint4*>(fc16 + size_t(corners[b]) * 32) + c);
-                float f[8];
-                unpack8(q, f);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) a1[i] = __fmaf_rn(ws[b], f[i], a1[i]);
-            }
-            st_shared_v4(a_base + core_offset(r, 8 * c, KC), pack_bf16x2(a1[0], a1[1]), pack_bf16x2(a1[2], a1[3]),
-                         pack_bf16x2(a1[4], a1[5]), pack_bf16x2(a1[6], a1[7]));
-        }
-        st_shared_v4(a_base + core_offset(r, 32, KC), pack_bf16x2(r6[0], r6[1]), pack_bf16x2(r6[2], r6[3]),
-                     pack_bf16x2(r6[4], r6[5]), 0u);
-        st_shared_v4(a_base + core_offset(r, 40, KC), 0u, 0u, 0u, 0u);
-
-        fence_async_smem();
-        fence_before_sync();
-        named_sync(bar_id, 128);
-        if (r == 0) {
-            fence_after_sync();
-            issue_layer(tmem_acc, a_base, sbase + OFF_WC0, KC);
-            mma_commit(bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        fence_after_sync();
-
-        // ---- hidden layers of f_C: epilogue -> bf16 A (K = 128) -> next MMA
-#pragma unroll 1
-        for (uint32_t layer = 0; layer < 2; ++layer) {
-            const float* bias = vec + (layer == 0 ? V_BC0 : V_BC1);
-#pragma unroll 1
-            for (uint32_t c = 0; c < 4; ++c) {
-                float v[32];
-                tmem_ld32(tmem_row + 32 * c, v);
-                tmem_wait_ld();
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    float h[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) h[i] = fmaxf(v[8 * q + i] + bias[32 * c + 8 * q + i], 0.f);
-                    st_shared_v4(a_base + core_offset(r, 32 * c + 8 * q, KH), pack_bf16x2(h[0], h[1]),
-                                 pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]), pack_bf16x2(h[6], h[7]));
-                }
-            }
-            fence_async_smem();
-            fence_before_sync();
-            named_sync(bar_id, 128);
-            if (r == 0) {
-                fence_after_sync();
-                issue_layer(tmem_acc, a_base, sbase + (layer == 0 ? OFF_WC1 : OFF_WC2), KH);
-                mma_commit(bar);
-            }
-            mbar_wait(bar, phase);
-            phase ^= 1;
-            fence_after_sync();
-        }
-
-        // ---- final epilogue: +b, relu, f_C head (3 x sigmoid)
-        float o0 = vec[V_BC3], o1 = vec[V_BC3 + 1], o2 = vec[V_BC3 + 2];
-#pragma unroll 1
-        for (uint32_t c = 0; c < 4; ++c) {
-            float v[32];
-            tmem_ld32(tmem_row + 32 * c, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const uint32_t col = 32 * c + i;
-                const float h = fmaxf(v[i] + vec[V_BC2 + col], 0.f);
-                o0 = __fmaf_rn(vec[V_WC3 + col], h, o0);
-                o1 = __fmaf_rn(vec[V_WC3 + 128 + col], h, o1);
-                o2 = __fmaf_rn(vec[V_WC3 + 256 + col], h, o2);
-            }
-        }
-        if (j < n) {
-            out.tau[j] = tau;
-            out.eta[j] = eta;
-            out.rgb[3 * size_t(j)] = sigmoidf_fast(o0);
-            out.rgb[3 * size_t(j) + 1] = sigmoidf_fast(o1);
-            out.rgb[3 * size_t(j) + 2] = sigmoidf_fast(o2);
-        }
-        fence_before_sync();  // TMEM reads complete before the next tile's MMA overwrites
-    }
-
+__device__ __forceinline__ void kernel_teardown(uint32_t tmem) {
     fence_before_sync();
     __syncthreads();
-    if (warp == 0) {
+    if ((threadIdx.x >> 5) == 0) {
         fence_after_sync();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
+}
+
+__device__ __forceinline__ void load_corners(const DevOctree& T, uint32_t leaf, uint32_t* c) {
+    const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
+    const uint4 a = __ldg(cp), b = __ldg(cp + 1);
+    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+    c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+}
+
+// ---- f_T pass ---------------------------------------------------------------
+template <bool kBF16>
+__global__ void __launch_bounds__(512, 1)
+    k_decode_t(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ ft16,
+               const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ geo, uint32_t n, HitOut out) {
+    using F = Fmt<kBF16>;
+    using H2 = typename F::H2;
+    constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
+    constexpr uint32_t kIdescHead = make_idesc(128, 16, kBF16);
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const uint32_t tmem = kernel_setup(sm, pack + OFF_WT0, T_WEIGHTS, T_SM_BAR);
+    const uint32_t tid = threadIdx.x, slot = tid >> 7, r = tid & 127, warp = tid >> 5;
+    const uint32_t lane_off = (32u * (warp & 3u)) << 16;
+    const uint32_t acc = tmem + slot * 128;
+    const uint32_t sbase = smem_u32(sm);
+    const uint32_t a_base = sbase + T_SM_A0 + slot * T_A_BYTES;
+    Slot S{reinterpret_cast<uint64_t*>(sm + T_SM_BAR) + slot, 0u, 1u + slot, r};
+    const uint32_t ntiles = (n + 127) / 128;
+
+    for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += gridDim.x * kSlots) {
+        const uint32_t j = tile * 128 + r;
+        const bool valid = j < n;
+        uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint4 g0 = make_uint4(0, 0, 0, 0), g1 = g0, g2 = g0;
+        if (valid) {
+            load_corners(T, hit_leaf[j], corners);
+            g0 = geo[3 * size_t(j)];
+            g1 = geo[3 * size_t(j) + 1];
+            g2 = geo[3 * size_t(j) + 2];
+        }
+        // Warp-cooperative gather: the warp owns rows 32w..32w+31 of the tile; in
+        // pass p lanes 8q..8q+7 gather row 4p+q, lane chunk c = 8 features, so
+        // one LDG.128 instruction covers 4 whole 128-byte feature rows.
+        const uint32_t lane = r & 31, q = lane >> 3, ch = lane & 7, row0 = r & ~31u;
+        const uint32_t wp[8] = {g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z};  // w1, w2 as 16-bit pairs
+#pragma unroll 2
+        for (uint32_t p = 0; p < 8; ++p) {
+            const uint32_t src = 4 * p + q;
+            uint32_t cb[8], w[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) cb[b] = __shfl_sync(0xffffffffu, corners[b], src);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) w[b] = __shfl_sync(0xffffffffu, wp[b], src);
+            uint4 fq[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) fq[b] = __ldg(reinterpret_cast<const uint4*>(ft16 + size_t(cb[b]) * 64) + ch);
+            H2 a1[4], a2[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a1[i] = a2[i] = F::splat(0.f);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const H2 p1 = u2h<H2>(w[b / 2]), p2 = u2h<H2>(w[4 + b / 2]);
+                const H2 h1 = (b & 1) ? F::hi2(p1) : F::lo2(p1);
+                const H2 h2 = (b & 1) ? F::hi2(p2) : F::lo2(p2);
+                const H2* f = reinterpret_cast<const H2*>(&fq[b]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    a1[i] = __hfma2(h1, f[i], a1[i]);
+                    a2[i] = __hfma2(h2, f[i], a2[i]);
+                }
+            }
+            const uint32_t row = row0 + src;
+            st_shared_v4(a_base + a_off(row, 8 * ch), h2u(a1[0]), h2u(a1[1]), h2u(a1[2]), h2u(a1[3]));
+            st_shared_v4(a_base + a_off(row, 64 + 8 * ch), h2u(a2[0]), h2u(a2[1]), h2u(a2[2]),
+                         h2u(a2[3]));
+        }
+        st_shared_v4(a_base + a_off(r, 128), g0.x, g0.y, g0.z, F::kOne);
+        st_shared_v4(a_base + a_off(r, 136), 0u, 0u, 0u, 0u);
+
+        S.mma([&] { issue_layer(acc, a_base, sbase + OFF_WT0, KT, kIdesc); });
+        hidden_epilogue<kBF16, false>(acc + lane_off, a_base, r, KT, nullptr);
+        st_shared_v4(a_base + a_off(r, 128), F::kOne, 0u, 0u, 0u);
+        st_shared_v4(a_base + a_off(r, 136), 0u, 0u, 0u, 0u);
+        S.mma([&] { issue_layer(acc, a_base, sbase + OFF_WT1, KT, kIdescHead); });
+        float hv[16];
+        tmem_ld16(acc + lane_off, hv);
+        tmem_wait_ld();
+        if (valid) {
+            out.tau[j] = fmaxf(hv[0], 0.f);
+            out.eta[j] = __fdividef(1.0f, 1.0f + __expf(-hv[1]));
+        }
+        fence_before_sync();
+    }
+    kernel_teardown(tmem);
+}
+
+// ---- f_C pass ---------------------------------------------------------------
+template <bool kBF16>
+__global__ void __launch_bounds__(512, 1)
+    k_decode_c(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ fc16,
+               const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ geo,
+               const float4* __restrict__ u12, uint32_t n, HitOut out) {
+    using F = Fmt<kBF16>;
+    using H2 = typename F::H2;
+    constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
+    constexpr uint32_t kIdescHead = make_idesc(128, 16, kBF16);
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const uint32_t tmem = kernel_setup(sm, pack + OFF_WC0, C_WEIGHTS, C_SM_BAR);
+    const uint32_t tid = threadIdx.x, slot = tid >> 7, r = tid & 127, warp = tid >> 5;
+    const uint32_t lane_off = (32u * (warp & 3u)) << 16;
+    const uint32_t acc = tmem + slot * 128;
+    const uint32_t sbase = smem_u32(sm);
+    constexpr uint32_t W0 = 0, W1 = OFF_WC1 - OFF_WC0, W2 = OFF_WC2 - OFF_WC0, W3 = OFF_WC3 - OFF_WC0;
+    const float* cvec = reinterpret_cast<const float*>(sm + (OFF_CVEC - OFF_WC0));
+    const uint32_t a_base = sbase + C_SM_A0 + slot * C_A_BYTES;
+    Slot S{reinterpret_cast<uint64_t*>(sm + C_SM_BAR) + slot, 0u, 1u + slot, r};
+    const uint32_t ntiles = (n + 127) / 128;
+
+    for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += gridDim.x * kSlots) {
+        const uint32_t j = tile * 128 + r;
+        const bool valid = j < n;
+        uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint4 g0 = make_uint4(0, 0, 0, 0);
+        float ws[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (valid) {
+            load_corners(T, hit_leaf[j], corners);
+            g0 = geo[3 * size_t(j)];
+            const float4 ua = u12[2 * size_t(j)], ub = u12[2 * size_t(j) + 1];
+            const float e = out.eta[j], ome = 1.0f - e;
+            // u_s = (x_s - lo)/h with x_s = eta x1 + (1-eta) x2 (voxel_batch.hpp:111)
+            const float us[3] = {ua.x * e + ua.w * ome, ua.y * e + ub.x * ome, ua.z * e + ub.y * ome};
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                ws[b] = ((b & 1) ? us[0] : 1.f - us[0]) * ((b & 2) ? us[1] : 1.f - us[1]) *
+                        ((b & 4) ? us[2] : 1.f - us[2]);
+        }
+        // Warp-cooperative gather: pass p, lanes 4q..4q+3 gather row 8p+q of the
+        // warp's 32 rows, lane chunk = 8 of the 32 colour features.
+        const uint32_t lane = r & 31, q = lane >> 2, ch = lane & 3, row0 = r & ~31u;
+        uint32_t wsp[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) wsp[b] = F::pack(ws[2 * b], ws[2 * b + 1]);
+#pragma unroll 2
+        for (uint32_t p = 0; p < 4; ++p) {
+            const uint32_t src = 8 * p + q;
+            uint32_t cb[8], w[4];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) cb[b] = __shfl_sync(0xffffffffu, corners[b], src);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) w[b] = __shfl_sync(0xffffffffu, wsp[b], src);
+            uint4 fq[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) fq[b] = __ldg(reinterpret_cast<const uint4*>(fc16 + size_t(cb[b]) * 32) + ch);
+            H2 a1[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a1[i] = F::splat(0.f);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const H2 pw = u2h<H2>(w[b / 2]);
+                const H2 hw = (b & 1) ? F::hi2(pw) : F::lo2(pw);
+                const H2* f = reinterpret_cast<const H2*>(&fq[b]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a1[i] = __hfma2(hw, f[i], a1[i]);
+            }
+            st_shared_v4(a_base + a_off(row0 + src, 8 * ch), h2u(a1[0]), h2u(a1[1]), h2u(a1[2]),
+                         h2u(a1[3]));
+        }
+        st_shared_v4(a_base + a_off(r, 32), g0.x, g0.y, g0.z, F::kOne);
+        st_shared_v4(a_base + a_off(r, 40), 0u, 0u, 0u, 0u);
+        S.mma([&] { issue_layer(acc, a_base, sbase + W0, KC, kIdesc); });
+        hidden_epilogue<kBF16, false>(acc + lane_off, a_base, r, KH, nullptr);
+        S.mma([&] { issue_layer(acc, a_base, sbase + W1, KH, kIdesc); });
+        hidden_epilogue<kBF16, true>(acc + lane_off, a_base, r, KH, cvec);
+        S.mma([&] { issue_layer(acc, a_base, sbase + W2, KH, kIdesc); });
+        hidden_epilogue<kBF16, true>(acc + lane_off, a_base, r, KH, cvec + 128);
+        S.mma([&] { issue_layer(acc, a_base, sbase + W3, KH, kIdescHead); });
+        float hv[16];
+        tmem_ld16(acc + lane_off, hv);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                out.rgb[3 * size_t(j) + c] = __fdividef(1.0f, 1.0f + __expf(-(hv[c] + cvec[256 + c])));
+        }
+        fence_before_sync();
+    }
+    kernel_teardown(tmem);
 }
 
 int g_num_sms = 0;
@@ -381,38 +526,72 @@ int g_num_sms = 0;
 
 size_t pack_tc_bytes(uint32_t V) { return OFF_FEAT + size_t(V) * 96 * 2; }
 
-void ensure_pack_bf16(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, cudaStream_t s) {
-    if (pack_version == version && pack.p) return;
+void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, bool bf16,
+                    cudaStream_t s) {
+    const uint64_t tag = version | (bf16 ? (uint64_t(1) << 63) : 0);  // format in the top bit
+    if (pack_version == tag && pack.p) return;
     uint8_t* p = pack.ensure<uint8_t>(pack_tc_bytes(M.V));
-    k_pack_tc<<<(128 * KT + 255) / 256, 256, 0, s>>>(M.mt, M.mc, p);
-    note_launch();
-    __nv_bfloat16* ft16 = reinterpret_cast<__nv_bfloat16*>(p + OFF_FEAT);
-    __nv_bfloat16* fc16 = ft16 + size_t(M.V) * 64;
     const size_t nt = size_t(M.V) * 64, nc = size_t(M.V) * 32;
-    k_feat_bf16<<<unsigned((nt / 4 + 255) / 256 + 1), 256, 0, s>>>(M.ft, ft16, nt);
-    k_feat_bf16<<<unsigned((nc / 4 + 255) / 256 + 1), 256, 0, s>>>(M.fc, fc16, nc);
-    note_launch(2);
-    pack_version = version;
+    const unsigned gt = unsigned((nt / 4 + 255) / 256 + 1), gc = unsigned((nc / 4 + 255) / 256 + 1);
+    if (bf16) {
+        using H = Fmt<true>::H;
+        k_pack_tc<true><<<(128 * KT + 255) / 256, 256, 0, s>>>(M.mt, M.mc, p);
+        H* ft = reinterpret_cast<H*>(p + OFF_FEAT);
+        k_feat_cvt<true><<<gt, 256, 0, s>>>(M.ft, ft, nt);
+        k_feat_cvt<true><<<gc, 256, 0, s>>>(M.fc, ft + nt, nc);
+    } else {
+        using H = Fmt<false>::H;
+        k_pack_tc<false><<<(128 * KT + 255) / 256, 256, 0, s>>>(M.mt, M.mc, p);
+        H* ft = reinterpret_cast<H*>(p + OFF_FEAT);
+        k_feat_cvt<false><<<gt, 256, 0, s>>>(M.ft, ft, nt);
+        k_feat_cvt<false><<<gc, 256, 0, s>>>(M.fc, ft + nt, nc);
+    }
+    note_launch(3);
+    pack_version = tag;
 }
 
-void launch_decode_bf16(const DevOctree& T, const DevModel& M, const char* pack, const double* rays,
-                        const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
-                        const double* hit_tout, uint32_t n_hits, HitOut out, int* err, cudaStream_t s) {
+template <bool kBF16>
+static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t* p, const double* rays,
+                           const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
+                           const double* hit_tout, uint32_t n_hits, HitOut out, int* err, uint4* geo, float4* u12,
+                           cudaStream_t s) {
+    using H = typename Fmt<kBF16>::H;
+    static bool attr = false;
+    if (!attr) {
+        SVLF_CUDA(cudaFuncSetAttribute(k_decode_t<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(T_SM_TOTAL)));
+        SVLF_CUDA(cudaFuncSetAttribute(k_decode_c<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SM_TOTAL)));
+        attr = true;
+    }
+    const H* ft = reinterpret_cast<const H*>(p + OFF_FEAT);
+    const H* fc = ft + size_t(M.V) * 64;
+    k_hit_geom<kBF16><<<(n_hits + 127) / 128, 128, 0, s>>>(T, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits,
+                                                           geo, u12, err);
+    const uint32_t tiles = (n_hits + 127) / 128;
+    const uint32_t grid = std::min<uint32_t>(uint32_t(g_num_sms), (tiles + kSlots - 1) / kSlots);
+    k_decode_t<kBF16><<<grid, 512, T_SM_TOTAL, s>>>(T, p, ft, hit_leaf, geo, n_hits, out);
+    k_decode_c<kBF16><<<grid, 512, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, geo, u12, n_hits, out);
+    note_launch(3);
+}
+
+void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, bool bf16, const double* rays,
+                      const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
+                      const double* hit_tout, uint32_t n_hits, HitOut out, int* err, void* scratch,
+                      cudaStream_t s) {
     if (n_hits == 0) return;
     if (g_num_sms == 0) {
         int dev = 0;
         SVLF_CUDA(cudaGetDevice(&dev));
         SVLF_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-        SVLF_CUDA(cudaFuncSetAttribute(k_decode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM_TOTAL)));
     }
+    uint4* geo = static_cast<uint4*>(scratch);
+    float4* u12 = reinterpret_cast<float4*>(geo + 3 * size_t(n_hits));
     const uint8_t* p = reinterpret_cast<const uint8_t*>(pack);
-    const __nv_bfloat16* ft16 = reinterpret_cast<const __nv_bfloat16*>(p + OFF_FEAT);
-    const __nv_bfloat16* fc16 = ft16 + size_t(M.V) * 64;
-    const uint32_t tiles = (n_hits + 127) / 128;
-    const uint32_t grid = std::min<uint32_t>(uint32_t(g_num_sms), (tiles + 1) / 2);
-    k_decode_tc<<<grid, 256, SM_TOTAL, s>>>(T, p, ft16, fc16, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits,
-                                            out, err);
-    note_launch();
+    if (bf16)
+        decode_tc_impl<true>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits, out, err, geo, u12, s);
+    else
+        decode_tc_impl<false>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits, out, err, geo, u12, s);
 }
+
+size_t decode_tc_scratch_bytes(uint32_t n_hits) { return size_t(n_hits) * (48 + 32); }
 
 }  // namespace svlfb

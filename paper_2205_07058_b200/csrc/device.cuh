@@ -121,11 +121,13 @@ void launch_composite(const uint32_t* offsets, const double* hit_tin, const doub
                       float* depth, unsigned long long* fg_count, cudaStream_t s);
 
 // ---- tcgen05 decoder (decode_tc.cu)
-void ensure_pack_bf16(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version,
+void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, bool bf16,
+                    cudaStream_t s);
+void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, bool bf16, const double* rays,
+                      const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
+                      const double* hit_tout, uint32_t n_hits, HitOut out, int* err, void* scratch,
                       cudaStream_t s);
-void launch_decode_bf16(const DevOctree& T, const DevModel& M, const char* pack, const double* rays,
-                        const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
-                        const double* hit_tout, uint32_t n_hits, HitOut out, int* err, cudaStream_t s);
+size_t decode_tc_scratch_bytes(uint32_t n_hits);
 
 // ---- misc device utilities (traverse.cu)
 void launch_gather_leaf_codes(const uint64_t* leaf_codes, const uint32_t* hit_leaf, uint64_t* out,

@@ -146,20 +146,21 @@ def _psnr(a, b):
 TOL_BF16_PSNR_DELTA = 0.05  # north_star: PSNR delta <= 0.05 dB with the bf16 MLP
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp16"])
 @pytest.mark.parametrize("objects", [4, 20])
-def test_render_bf16_tensor_core(ctx, oracle, objects):
-    """tcgen05 bf16 decoder vs the fp32 oracle: PSNR(vs GT) delta <= 0.05 dB."""
+def test_render_tensor_core(ctx, oracle, objects, precision):
+    """tcgen05 16-bit decoder vs the fp32 oracle: PSNR(vs GT) delta <= 0.05 dB."""
     sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=objects, n_views=8, view_res=96, res=64, width=192)
     tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
     otree = oracle.tree_build(pts, res, dil)
     model = P.Model(tree, seed=1, ctx=ctx)
     om = oracle.init_model(otree, 1)
     st = P.RenderStats()
-    rgb, a, d = P.render_frame(model, P.Camera.from_record(cam, W, H), stats=st, precision="bf16")
+    rgb, a, d = P.render_frame(model, P.Camera.from_record(cam, W, H), stats=st, precision=precision)
     orgb, oa, od, ost = oracle.render_frame(otree, om, cam, W, H)
     gt, _, _ = S.render_gt(sc, cam, W, H)
     p16, p32, pv = _psnr(rgb.reshape(-1), gt), _psnr(orgb, gt), _psnr(rgb.reshape(-1), orgb)
-    print(f"objects={objects} psnr_bf16={p16:.4f} psnr_oracle={p32:.4f} psnr_bf16_vs_oracle={pv:.2f} "
+    print(f"{precision} objects={objects} psnr_tc={p16:.4f} psnr_oracle={p32:.4f} psnr_bf16_vs_oracle={pv:.2f} "
           f"maxabs_rgb={np.abs(rgb.reshape(-1) - orgb).max():.3g} maxabs_depth={np.abs(d.reshape(-1) - od).max():.3g}")
     assert abs(p16 - p32) <= TOL_BF16_PSNR_DELTA
     assert pv > 40.0  # bf16 vs fp32 image agreement
@@ -167,13 +168,14 @@ def test_render_bf16_tensor_core(ctx, oracle, objects):
     assert st.traversal_hits == ost[2]
 
 
-def test_render_bf16_matches_fp32_path(c1, ctx):
+@pytest.mark.parametrize("precision", ["bf16", "fp16"])
+def test_render_tc_matches_fp32_path(c1, ctx, precision):
     tree, otree, cam, W, H = c1
     model = P.Model(tree, seed=1, ctx=ctx)
     camera = P.Camera.from_record(cam, W, H)
     r32, a32, d32 = P.render_frame(model, camera, precision="fp32")
-    r16, a16, d16 = P.render_frame(model, camera, precision="bf16")
-    print(f"c1 bf16 vs fp32 psnr={_psnr(r16, r32):.2f} maxabs={np.abs(r16 - r32).max():.3g}")
+    r16, a16, d16 = P.render_frame(model, camera, precision=precision)
+    print(f"c1 {precision} vs fp32 psnr={_psnr(r16, r32):.2f} maxabs={np.abs(r16 - r32).max():.3g}")
     assert _psnr(r16, r32) > 40.0
     # depth = sum(w t_s) / alpha is ill-conditioned near the 1e-4 alpha cut; compare where alpha is material
     m = (a32 > 1e-2) & (a16 > 1e-2)
