@@ -302,6 +302,7 @@ def main():
     peak = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
     stage = {k: round(statistics.median(t[k] for t in decode_ms), 4)
              for k in ("traverse_ms", "emit_ms", "decode_ms", "composite_ms")}
+    stage["fallback_rays"] = int(decode_ms[-1].get("overflow_rays", 0))
     line = {
         "metric": "rendered rays/s at 1600x1600 (C2)",
         "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,

@@ -112,6 +112,7 @@ typedef struct svlf_octree_info {
 typedef struct svlf_timings {
     float traverse_ms, emit_ms, decode_ms, composite_ms, backward_ms, adam_ms, total_ms;
     long long hits;
+    long long overflow_rays; /* rays re-traversed by the per-ray fallback walker */
 } svlf_timings;
 
 /* ---- context -------------------------------------------------------- */

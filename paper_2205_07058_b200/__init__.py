@@ -77,7 +77,7 @@ class _OctreeInfo(C.Structure):
 class _Timings(C.Structure):
     _fields_ = [(n, C.c_float) for n in
                 ("traverse_ms", "emit_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms", "total_ms")] + \
-               [("hits", C.c_longlong)]
+               [("hits", C.c_longlong), ("overflow_rays", C.c_longlong)]
 
 
 # ---- public value types (reference structs) ----------------------------------

@@ -78,7 +78,10 @@ struct svlf_ctx {
     cudaStream_t stream = nullptr;      // active stream
     cudaStream_t own_stream = nullptr;  // created with the context
     DevBuf rays, counts, offsets, scan_tmp, hit_leaf, hit_tin, hit_tout, hit_ray;
-    DevBuf h_tau, h_eta, h_rgb, out_rgb, out_alpha, out_depth, misc, tmp64, tmpx12, tc_scratch;
+    DevBuf h_tau, h_eta, h_rgb, out_rgb, out_alpha, out_depth, misc, tmp64, tmpx12, tc_scratch, overflow;
+    DevBuf csr_off, csr_leaf, csr_tin, csr_tout, csr_ray, overflow2;
+    size_t hit_cap = 0;
+    long long last_overflow_rays = 0;  // first-pass overflow * 1e6 + dense-pass overflow
     TrainScratch train;
     int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
     cudaEvent_t ev[EV_N] = {};
@@ -92,7 +95,7 @@ struct svlf_ctx {
 struct svlf_octree {
     HostOctree host;
     mutable int device = -1;
-    mutable DevBuf first_child, mask, corners, leaf_codes;
+    mutable DevBuf nodes, corners, leaf_codes;
     mutable DevOctree view{};
 };
 
@@ -119,25 +122,24 @@ const DevOctree& dev_view(const svlf_octree* t) {
     int dev = -1;
     SVLF_CUDA(cudaGetDevice(&dev));
     if (t->device == dev) return t->view;
-    for (DevBuf* b : {&t->first_child, &t->mask, &t->corners, &t->leaf_codes}) {
+    for (DevBuf* b : {&t->nodes, &t->corners, &t->leaf_codes}) {
         if (b->p) SVLF_CUDA(cudaFree(b->p));
         b->p = nullptr;
         b->cap = 0;
     }
     const HostOctree& h = t->host;
     const size_t internal = h.node_first_child.size();
-    uint32_t* fc = t->first_child.ensure<uint32_t>(internal);
-    uint8_t* mk = t->mask.ensure<uint8_t>(internal);
+    uint2* nd = t->nodes.ensure<uint2>(internal);
+    std::vector<uint2> packed(internal);
+    for (size_t i = 0; i < internal; ++i) packed[i] = make_uint2(h.node_first_child[i], h.node_mask[i]);
     uint32_t* cr = t->corners.ensure<uint32_t>(h.corner_ids.size());
     uint64_t* lc = t->leaf_codes.ensure<uint64_t>(h.leaves().size());
-    SVLF_CUDA(cudaMemcpy(fc, h.node_first_child.data(), internal * 4, cudaMemcpyHostToDevice));
-    SVLF_CUDA(cudaMemcpy(mk, h.node_mask.data(), internal, cudaMemcpyHostToDevice));
+    SVLF_CUDA(cudaMemcpy(nd, packed.data(), internal * sizeof(uint2), cudaMemcpyHostToDevice));
     SVLF_CUDA(cudaMemcpy(cr, h.corner_ids.data(), h.corner_ids.size() * 4, cudaMemcpyHostToDevice));
     SVLF_CUDA(cudaMemcpy(lc, h.leaves().data(), h.leaves().size() * 8, cudaMemcpyHostToDevice));
     DevOctree& v = t->view;
     v = DevOctree{};
-    v.first_child = fc;
-    v.mask = mk;
+    v.nodes = nd;
     v.corners = cr;
     v.leaf_codes = lc;
     for (int l = 0; l <= h.leaf_level + 1 && l < kMaxLevelsDev + 2; ++l) v.level_off[l] = h.level_off[l];
@@ -194,32 +196,54 @@ void reset_misc(svlf_ctx* ctx) {
 unsigned long long* misc_fg(svlf_ctx* ctx) { return reinterpret_cast<unsigned long long*>(ctx->misc.as<char>() + 8); }
 
 // Traversal for `n` rays: rays are either generated from `cam` (rows
-// row0..) into ctx->rays, or already resident in ctx->rays. Leaves CSR
-// offsets in ctx->offsets and sorted hits in ctx->hit_*. Returns total hits.
+// row0 .. row0+rows) or already resident in ctx->rays. Leaves per-ray
+// segments (ctx->offsets = start, ctx->counts = count) and sorted hits in
+// ctx->hit_*. Returns the total number of hits.
 uint32_t run_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0,
-                       uint32_t n) {
+                       uint32_t rows, uint32_t n) {
     cudaStream_t s = ctx->stream;
     double* rays = ctx->rays.ensure<double>(size_t(n) * 6);
-    uint32_t* counts = ctx->counts.ensure<uint32_t>(size_t(n) + 1);
-    uint32_t* offs = ctx->offsets.ensure<uint32_t>(size_t(n) + 1);
-    SVLF_CUDA(cudaMemsetAsync(counts + n, 0, sizeof(uint32_t), s));
-    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
-    launch_traverse_count(dev_view(tree), cam, row0, rays, n, counts, s);
-    const size_t tb = scan_temp_bytes(n + 1);
-    void* tmp = ctx->scan_tmp.ensure<char>(tb);
-    launch_exclusive_scan(tmp, tb, counts, offs, n + 1, s);
-    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));
-    SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, offs + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    SVLF_CUDA(cudaStreamSynchronize(s));
-    const uint32_t total = uint32_t(ctx->h_pinned[4]);
-    ctx->hit_leaf.ensure<uint32_t>(total);
-    ctx->hit_tin.ensure<double>(total);
-    ctx->hit_tout.ensure<double>(total);
-    ctx->hit_ray.ensure<uint32_t>(total);
-    launch_traverse_emit(dev_view(tree), rays, n, offs, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
-                         ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), s);
-    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_EMIT], s));
-    return total;
+    uint32_t* ray_off = ctx->offsets.ensure<uint32_t>(size_t(n) + 1);
+    uint32_t* ray_cnt = ctx->counts.ensure<uint32_t>(size_t(n) + 1);
+    uint32_t* ovl = ctx->overflow.ensure<uint32_t>(size_t(n) + 1);
+    uint32_t* ovl2 = ctx->overflow2.ensure<uint32_t>(size_t(n) + 1);
+    uint32_t* counters = reinterpret_cast<uint32_t*>(ctx->misc.as<char>() + 16);
+    size_t cap = std::max<size_t>(ctx->hit_cap, std::max<size_t>(size_t(n) * 4, size_t(1) << 20));
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        cap = std::min<size_t>(cap, 0xffffffffu);
+        ctx->hit_leaf.ensure<uint32_t>(cap);
+        ctx->hit_tin.ensure<double>(cap);
+        ctx->hit_tout.ensure<double>(cap);
+        ctx->hit_ray.ensure<uint32_t>(cap);
+        ctx->hit_cap = cap;
+        TraverseOut o{ray_off, ray_cnt, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
+                      ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), counters, ovl, ovl2, rays,
+                      uint32_t(cap)};
+        SVLF_CUDA(cudaMemsetAsync(counters, 0, 16, s));
+        SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
+        launch_traverse(dev_view(tree), cam, row0, rows, n, o, s);
+        SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));
+        SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        const uint32_t n_ovl = uint32_t(ctx->h_pinned[5]);
+        if (n_ovl) {
+            launch_traverse_dense(dev_view(tree), cam, row0, n_ovl, o, s);
+            SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
+            SVLF_CUDA(cudaStreamSynchronize(s));
+            const uint32_t n_ovl2 = uint32_t(ctx->h_pinned[7]);
+            if (n_ovl2) {
+                launch_traverse_fallback(dev_view(tree), cam, row0, n_ovl2, o, s);
+                SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
+                SVLF_CUDA(cudaStreamSynchronize(s));
+            }
+        }
+        SVLF_CUDA(cudaEventRecord(ctx->ev[EV_EMIT], s));
+        const uint32_t total = uint32_t(ctx->h_pinned[4]);
+        ctx->last_overflow_rays = (long long)n_ovl * 1000000 + ctx->h_pinned[7];
+        if (ctx->h_pinned[6] == 0) return total;
+        cap = size_t(total) + total / 4 + 1024;  // grow and re-run
+    }
+    fail(SVLF_ERR_RUNTIME, "traversal output capacity could not be satisfied");
 }
 
 // decode + composite into device output buffers
@@ -245,8 +269,8 @@ void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t tot
                           ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total, ho, err, s);
     }
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_DECODE], s));
-    launch_composite(ctx->offsets.as<uint32_t>(), ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), ho, n,
-                     bg, d_rgb, d_alpha, d_depth, misc_fg(ctx), s);
+    launch_composite(ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(), ctx->hit_tin.as<double>(),
+                     ctx->hit_tout.as<double>(), ho, n, bg, d_rgb, d_alpha, d_depth, misc_fg(ctx), s);
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COMPOSITE], s));
 }
 
@@ -262,7 +286,7 @@ void finish_render(svlf_ctx* ctx, uint32_t n, uint32_t total, svlf_render_stats*
     cudaEventElapsedTime(&ms[2], ctx->ev[EV_EMIT], ctx->ev[EV_DECODE]);
     cudaEventElapsedTime(&ms[3], ctx->ev[EV_DECODE], ctx->ev[EV_COMPOSITE]);
     ctx->last = svlf_timings{ms[0], ms[1], ms[2], ms[3], 0.f, 0.f, ms[0] + ms[1] + ms[2] + ms[3],
-                             (long long)total};
+                             (long long)total, (long long)ctx->last_overflow_rays};
     if (stats) {
         stats->rays += n;
         stats->rays_with_hits += (long long)fg;
@@ -283,7 +307,7 @@ void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_
     const uint32_t n = uint32_t(n64);
     const DevCamera dc = to_dev_camera(*cam);
     reset_misc(ctx);
-    const uint32_t total = run_traversal(ctx, m->tree, &dc, row0, n);
+    const uint32_t total = run_traversal(ctx, m->tree, &dc, row0, rows, n);
     run_decode_composite(ctx, m, n, total, bg, prec, d_rgb, d_alpha, d_depth);
     finish_render(ctx, n, total, stats);
 }
@@ -453,23 +477,35 @@ svlf_status svlf_traverse(svlf_ctx* ctx, const svlf_octree* tree, const double* 
         reset_misc(ctx);
         double* d_rays = ctx->rays.ensure<double>(size_t(nn) * 6 + 6);
         if (nn) SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyHostToDevice, s));
-        const uint32_t tot = nn ? run_traversal(ctx, tree, nullptr, 0, nn) : 0;
+        const uint32_t tot = nn ? run_traversal(ctx, tree, nullptr, 0, 0, nn) : 0;
         *total = tot;
+        // CSR (ray order) view: row pointer = exclusive scan of per-ray counts
         std::vector<uint32_t> off32(size_t(nn) + 1, 0);
-        if (nn) SVLF_CUDA(cudaMemcpyAsync(off32.data(), ctx->offsets.as<uint32_t>(), (size_t(nn) + 1) * 4,
-                                          cudaMemcpyDeviceToHost, s));
-        if (tot <= capacity && tot > 0) {
-            require(voxel_ids && t_in && t_out, "hit output is null");
-            uint64_t* codes = ctx->tmp64.ensure<uint64_t>(tot);
-            launch_gather_leaf_codes(dev_view(tree).leaf_codes, ctx->hit_leaf.as<uint32_t>(), codes, tot, s);
-            SVLF_CUDA(cudaMemcpyAsync(voxel_ids, codes, size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
-            SVLF_CUDA(cudaMemcpyAsync(t_in, ctx->hit_tin.as<double>(), size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
-            SVLF_CUDA(cudaMemcpyAsync(t_out, ctx->hit_tout.as<double>(), size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
-            if (x12) {
-                double* dx = ctx->tmpx12.ensure<double>(size_t(tot) * 6);
-                launch_hit_points(d_rays, ctx->hit_ray.as<uint32_t>(), ctx->hit_tin.as<double>(),
-                                  ctx->hit_tout.as<double>(), dx, tot, s);
-                SVLF_CUDA(cudaMemcpyAsync(x12, dx, size_t(tot) * 48, cudaMemcpyDeviceToHost, s));
+        if (nn) {
+            uint32_t* cnt = ctx->counts.as<uint32_t>();
+            uint32_t* csr = ctx->csr_off.ensure<uint32_t>(size_t(nn) + 1);
+            SVLF_CUDA(cudaMemsetAsync(cnt + nn, 0, 4, s));
+            const size_t tb = scan_temp_bytes(nn + 1);
+            launch_exclusive_scan(ctx->scan_tmp.ensure<char>(tb), tb, cnt, csr, nn + 1, s);
+            SVLF_CUDA(cudaMemcpyAsync(off32.data(), csr, (size_t(nn) + 1) * 4, cudaMemcpyDeviceToHost, s));
+            if (tot <= capacity && tot > 0) {
+                require(voxel_ids && t_in && t_out, "hit output is null");
+                uint32_t* lf = ctx->csr_leaf.ensure<uint32_t>(tot);
+                double* ti = ctx->csr_tin.ensure<double>(tot);
+                double* to = ctx->csr_tout.ensure<double>(tot);
+                uint32_t* ry = ctx->csr_ray.ensure<uint32_t>(tot);
+                launch_to_csr(ctx->offsets.as<uint32_t>(), cnt, csr, nn, ctx->hit_leaf.as<uint32_t>(),
+                              ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), lf, ti, to, ry, s);
+                uint64_t* codes = ctx->tmp64.ensure<uint64_t>(tot);
+                launch_gather_leaf_codes(dev_view(tree).leaf_codes, lf, codes, tot, s);
+                SVLF_CUDA(cudaMemcpyAsync(voxel_ids, codes, size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
+                SVLF_CUDA(cudaMemcpyAsync(t_in, ti, size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
+                SVLF_CUDA(cudaMemcpyAsync(t_out, to, size_t(tot) * 8, cudaMemcpyDeviceToHost, s));
+                if (x12) {
+                    double* dx = ctx->tmpx12.ensure<double>(size_t(tot) * 6);
+                    launch_hit_points(d_rays, ry, ti, to, dx, tot, s);
+                    SVLF_CUDA(cudaMemcpyAsync(x12, dx, size_t(tot) * 48, cudaMemcpyDeviceToHost, s));
+                }
             }
         }
         SVLF_CUDA(cudaStreamSynchronize(s));
@@ -669,7 +705,7 @@ svlf_status svlf_render_rays(svlf_ctx* ctx, svlf_model* m, const double* rays, s
         float* d_rgb = ctx->out_rgb.ensure<float>(n * 3);
         float* d_alpha = ctx->out_alpha.ensure<float>(n);
         float* d_depth = ctx->out_depth.ensure<float>(n);
-        const uint32_t total = run_traversal(ctx, m->tree, nullptr, 0, nn);
+        const uint32_t total = run_traversal(ctx, m->tree, nullptr, 0, 0, nn);
         run_decode_composite(ctx, m, nn, total, bg, prec, d_rgb, d_alpha, d_depth);
         finish_render(ctx, nn, total, stats);
         SVLF_CUDA(cudaMemcpyAsync(rgb, d_rgb, n * 12, cudaMemcpyDeviceToHost, s));

@@ -101,11 +101,35 @@ struct HitOut {
 };
 
 // ---- traversal (traverse.cu)
-void launch_traverse_count(const DevOctree& T, const DevCamera* cam, uint32_t row0, double* rays,
-                           uint32_t n, uint32_t* counts, cudaStream_t s);
-void launch_traverse_emit(const DevOctree& T, const double* rays, uint32_t n, const uint32_t* offsets,
-                          uint32_t* hit_leaf, double* hit_tin, double* hit_tout, uint32_t* hit_ray,
-                          cudaStream_t s);
+// Output of one traversal: each ray i owns hits [ray_off[i], ray_off[i] + ray_cnt[i])
+// sorted by (t_in, leaf index); segments of different rays are placed in
+// arbitrary order. counters: [0] hits allocated, [1] overflow rays (first
+// pass), [2] capacity exceeded (host grows the buffers and re-runs),
+// [3] overflow rays of the dense second pass.
+struct TraverseOut {
+    uint32_t* ray_off;
+    uint32_t* ray_cnt;
+    uint32_t* hit_leaf;
+    double* hit_tin;
+    double* hit_tout;
+    uint32_t* hit_ray;
+    uint32_t* counters;
+    uint32_t* overflow_rays;
+    uint32_t* overflow_dense;
+    double* rays;  // n x 6: input rays (buffer mode) or camera rays written for foreground rays
+    uint32_t capacity;
+};
+void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
+                     const TraverseOut& o, cudaStream_t s);
+// second cooperative pass (8 rays per block) over the rays of overflowed tiles
+void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
+                           const TraverseOut& o, cudaStream_t s);
+// per-ray depth-first walker for whatever still overflowed
+void launch_traverse_fallback(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
+                              const TraverseOut& o, cudaStream_t s);
+void launch_to_csr(const uint32_t* ray_off, const uint32_t* ray_cnt, const uint32_t* csr, uint32_t n,
+                   const uint32_t* leaf, const double* tin, const double* tout, uint32_t* leaf_o, double* tin_o,
+                   double* tout_o, uint32_t* ray_o, cudaStream_t s);
 size_t scan_temp_bytes(uint32_t n);
 void launch_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
                            uint32_t n, cudaStream_t s);
@@ -116,9 +140,9 @@ void launch_pack_f32(const DevModel& M, float* pack, cudaStream_t s);
 void launch_decode_f32(const DevOctree& T, const DevModel& M, const DecPackF32& P, const double* rays,
                        const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
                        const double* hit_tout, uint32_t n_hits, HitOut out, int* err, cudaStream_t s);
-void launch_composite(const uint32_t* offsets, const double* hit_tin, const double* hit_tout,
-                      HitOut hits, uint32_t n_rays, const float* bg3, float* rgb, float* alpha,
-                      float* depth, unsigned long long* fg_count, cudaStream_t s);
+void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const double* hit_tin,
+                      const double* hit_tout, HitOut hits, uint32_t n_rays, const float* bg3, float* rgb,
+                      float* alpha, float* depth, unsigned long long* fg_count, cudaStream_t s);
 
 // ---- tcgen05 decoder (decode_tc.cu)
 void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, bool bf16,

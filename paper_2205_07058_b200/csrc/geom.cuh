@@ -18,8 +18,7 @@ constexpr int kMaxLevelsDev = 21;
 
 // Read-only device mirror of a HostOctree (see host_octree.hpp for layout).
 struct DevOctree {
-    const uint32_t* first_child;  // per internal node
-    const uint8_t* mask;          // per internal node
+    const uint2* nodes;           // per internal node: {first child (global index), child mask}
     const uint32_t* corners;      // 8 per leaf
     const uint64_t* leaf_codes;   // sorted
     uint32_t level_off[kMaxLevelsDev + 2];

@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kDecBlock) k_decode_f32(DevOctree T, DevModel 
 }
 
 // render_tile composite, src/render.cpp:165-193 (fp64 accumulation).
-__global__ void __launch_bounds__(128) k_composite(const uint32_t* __restrict__ offsets,
+__global__ void __launch_bounds__(128) k_composite(const uint32_t* __restrict__ ray_off,
+                                                   const uint32_t* __restrict__ ray_cnt,
                                                    const double* __restrict__ tin,
                                                    const double* __restrict__ tout, HitOut h,
                                                    uint32_t n, float bg0, float bg1, float bg2,
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(128) k_composite(const uint32_t* __restrict__ 
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     bool fg = false;
     if (i < n) {
-        const uint32_t h0 = offsets[i], h1 = offsets[i + 1];
+        const uint32_t h0 = ray_off[i], h1 = h0 + ray_cnt[i];
         double c0 = 0, c1 = 0, c2 = 0, a = 0, dacc = 0, T = 1.0;
         for (uint32_t j = h0; j < h1; ++j) {
             const double e = exp(-double(h.tau[j]));
@@ -281,11 +282,11 @@ void launch_decode_f32(const DevOctree& T, const DevModel& M, const DecPackF32& 
     note_launch();
 }
 
-void launch_composite(const uint32_t* offsets, const double* hit_tin, const double* hit_tout,
-                      HitOut hits, uint32_t n_rays, const float* bg3, float* rgb, float* alpha,
-                      float* depth, unsigned long long* fg_count, cudaStream_t s) {
+void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const double* hit_tin,
+                      const double* hit_tout, HitOut hits, uint32_t n_rays, const float* bg3, float* rgb,
+                      float* alpha, float* depth, unsigned long long* fg_count, cudaStream_t s) {
     if (n_rays == 0) return;
-    k_composite<<<(n_rays + 127) / 128, 128, 0, s>>>(offsets, hit_tin, hit_tout, hits, n_rays,
+    k_composite<<<(n_rays + 127) / 128, 128, 0, s>>>(ray_off, ray_cnt, hit_tin, hit_tout, hits, n_rays,
                                                       bg3 ? bg3[0] : 0.f, bg3 ? bg3[1] : 0.f,
                                                       bg3 ? bg3[2] : 0.f, rgb, alpha, depth, fg_count);
     note_launch();

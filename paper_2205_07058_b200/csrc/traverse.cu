@@ -1,18 +1,33 @@
 // Sparse-voxel-octree ray traversal (reference SparseOctree::traverse,
-// src/octree.cpp:192-235), one ray per thread, two passes:
-//   count: walk the tree, count kept leaves per ray (and materialise camera rays)
-//   scan:  CSR row pointer (cub::DeviceScan)
-//   emit:  walk again, write (leaf index, t_in, t_out, ray) into the ray's
-//          segment, then an in-place insertion sort by (t_in, leaf index).
+// src/octree.cpp:192-235).
 //
-// The walk visits children in front-to-back octant order (octant i ^ sign
-// mask of the direction), which leaves a segment almost sorted, so the
-// insertion sort is ~linear. Leaf index order equals Morton order (leaves
-// are stored sorted), so the (t_in, index) sort equals the reference's
-// (t_in, code) total order. The set of kept leaves is order-independent: a
-// node is tested iff its parent was hit, with the reference's exact box
-// formula and slab test (geom.cuh), so ids, order and t values match the
-// reference bit for bit.
+// Main kernel: level-synchronous, block-cooperative traversal. A block owns
+// 64 rays (an 8x8 pixel tile in camera mode). Starting from the (ray, root)
+// pairs whose root box is hit, it expands the active (ray, node) pairs one
+// level at a time: thread e takes pair e, tests the node's existing children
+// front to back, and an order-preserving block scan appends the hit children
+// to the next level's queue in shared memory. Pairs stay grouped by ray and,
+// within a ray, in front-to-back depth-first order, so at the leaf level each
+// ray's hits are contiguous and nearly sorted; an insertion sort per ray
+// finishes the (t_in, code) order, one atomic per block allocates the block's
+// output range and the hits are written coalesced. Every warp instruction
+// works on 32 independent pairs, so SIMT efficiency does not depend on how
+// unequal the rays' paths are, and the octree is walked once (no count pass).
+// Tiles whose queues overflow shared memory are handed to the per-ray
+// fallback walker (k_traverse_fallback).
+//
+// Exactness. The reference tests each child box with ray_aabb on
+// [lo + x*cell_l, lo + (x+1)*cell_l]. Child planes coincide bit-for-bit with
+// parent planes (2x * cell_l/2 and x * cell_l round the same real number;
+// cell_l/2 is exact), so a node computes its three planes per axis (lo, mid,
+// hi) and their parametric values (plane - o) * (1/d) once, exactly as
+// ray_aabb would, and each child's slab interval is a selection of those.
+// t0 = max(0, ta_x, ta_y, ta_z), t1 = min(...) with "reject iff t1 < t0" is
+// the reference's axis-by-axis early exit (t0 only grows, t1 only shrinks);
+// zero direction components are the reference's inside-the-slab test; leaves
+// are kept iff t1 - t0 > 1e-12; leaf index order is Morton order. So hit ids,
+// order and t values are bit-identical to the reference built without FMA.
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "device.cuh"
@@ -23,49 +38,115 @@ namespace {
 
 constexpr double kMinHitSpan = 1e-12;  // tie rule, src/octree.cpp:16
 
-// Depth-first walk calling on_leaf(leaf_index, t0, t1) for every kept leaf.
+// Slab intervals of the two halves of a node along each axis.
+struct NodeSplit {
+    double lo_a[3], lo_b[3];  // low half:  [lo_a, lo_b]
+    double hi_a[3], hi_b[3];  // high half: [hi_a, hi_b]
+};
+
+__device__ __forceinline__ void split_node(const DevOctree& T, const double* o, const double* d,
+                                           const double* inv, int level, uint32_t x, uint32_t y, uint32_t z,
+                                           NodeSplit& s) {
+    const uint32_t c[3] = {x, y, z};
+    const double cl = T.cell[level], ch = T.cell[level + 1];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double plo = dadd(T.lo[a], dmul(double(c[a]), cl));
+        const double phi = dadd(T.lo[a], dmul(double(c[a] + 1u), cl));
+        const double pmid = dadd(T.lo[a], dmul(double(2u * c[a] + 1u), ch));
+        if (d[a] != 0.0) {
+            const double tl = dmul(dsub(plo, o[a]), inv[a]);
+            const double tm = dmul(dsub(pmid, o[a]), inv[a]);
+            const double th = dmul(dsub(phi, o[a]), inv[a]);
+            // "if (ta > tb) swap" exactly (keeps the reference's choice of signed zeros)
+            const bool swl = tl > tm, swh = tm > th;
+            s.lo_a[a] = swl ? tm : tl;
+            s.lo_b[a] = swl ? tl : tm;
+            s.hi_a[a] = swh ? th : tm;
+            s.hi_b[a] = swh ? tm : th;
+        } else {  // inside-the-slab test per half (geometry.cpp:13-16)
+            const bool in_lo = !(o[a] < plo || o[a] > pmid);
+            const bool in_hi = !(o[a] < pmid || o[a] > phi);
+            s.lo_a[a] = in_lo ? -CUDART_INF : CUDART_INF;
+            s.lo_b[a] = in_lo ? CUDART_INF : -CUDART_INF;
+            s.hi_a[a] = in_hi ? -CUDART_INF : CUDART_INF;
+            s.hi_b[a] = in_hi ? CUDART_INF : -CUDART_INF;
+        }
+    }
+}
+
+__device__ __forceinline__ bool child_hit(const NodeSplit& s, uint32_t oct, double& t0, double& t1) {
+    t0 = 0.0;
+    t1 = CUDART_INF;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const bool hi = (oct >> a) & 1u;
+        const double ta = hi ? s.hi_a[a] : s.lo_a[a];
+        const double tb = hi ? s.hi_b[a] : s.lo_b[a];
+        if (ta > t0) t0 = ta;  // src/geometry.cpp:21-22
+        if (tb < t1) t1 = tb;
+    }
+    return !(t1 < t0);
+}
+
+__device__ __forceinline__ uint32_t sign_mask(const double* d) {
+    return (d[0] < 0.0 ? 1u : 0u) | (d[1] < 0.0 ? 2u : 0u) | (d[2] < 0.0 ? 4u : 0u);
+}
+
+__device__ __forceinline__ uint64_t pack_xyz(uint32_t x, uint32_t y, uint32_t z) {
+    return uint64_t(x) | (uint64_t(y) << 21) | (uint64_t(z) << 42);
+}
+
+// ---- per-ray depth-first walker (fallback for overflowing tiles) -----------
 template <typename OnLeaf>
 __device__ __forceinline__ void walk(const DevOctree& T, const RayPre& p, OnLeaf&& on_leaf) {
-    double lo[3], hi[3], t0, t1;
-    cell_box(T, T.cell[0], 0, 0, 0, lo, hi);
-    if (!slab_test(p, lo, hi, t0, t1)) return;
-
-    const uint32_t s = (p.r.d[0] < 0.0 ? 1u : 0u) | (p.r.d[1] < 0.0 ? 2u : 0u) | (p.r.d[2] < 0.0 ? 4u : 0u);
-    uint32_t st_node[kMaxLevelsDev], st_x[kMaxLevelsDev], st_y[kMaxLevelsDev], st_z[kMaxLevelsDev];
-    uint32_t st_it[kMaxLevelsDev];
-    int lvl = 0;
-    st_node[0] = 0;
-    st_x[0] = st_y[0] = st_z[0] = 0;
-    st_it[0] = 0;
+    {
+        double lo[3], hi[3], t0, t1;
+        cell_box(T, T.cell[0], 0, 0, 0, lo, hi);
+        if (!slab_test(p, lo, hi, t0, t1)) return;
+    }
+    const uint32_t s = sign_mask(p.r.d);
     const int L = T.L;
-    while (lvl >= 0) {
-        const uint32_t it = st_it[lvl];
+    uint2 st_node[kMaxLevelsDev];
+    uint64_t st_xyz[kMaxLevelsDev];
+    int lvl = 0;
+    uint32_t x = 0, y = 0, z = 0, it = 0;
+    uint2 node = T.nodes[0];
+    NodeSplit sp;
+    split_node(T, p.r.o, p.r.d, p.inv, 0, x, y, z, sp);
+    while (true) {
         if (it == 8) {
+            if (lvl == 0) break;
             --lvl;
+            node = st_node[lvl];
+            it = node.y >> 8;
+            node.y &= 0xffu;
+            const uint64_t c = st_xyz[lvl];
+            x = uint32_t(c & 0x1fffffu);
+            y = uint32_t((c >> 21) & 0x1fffffu);
+            z = uint32_t(c >> 42);
+            split_node(T, p.r.o, p.r.d, p.inv, lvl, x, y, z, sp);
             continue;
         }
-        st_it[lvl] = it + 1;
         const uint32_t oct = it ^ s;
-        const uint32_t g = st_node[lvl];
-        const uint32_t m = T.mask[g];
-        if (!((m >> oct) & 1u)) continue;
-        const uint32_t child = T.first_child[g] + __popc(m & ((1u << oct) - 1u));
-        const uint32_t cx = 2u * st_x[lvl] + (oct & 1u);
-        const uint32_t cy = 2u * st_y[lvl] + ((oct >> 1) & 1u);
-        const uint32_t cz = 2u * st_z[lvl] + ((oct >> 2) & 1u);
-        const int cl = lvl + 1;
-        cell_box(T, T.cell[cl], cx, cy, cz, lo, hi);
-        if (!slab_test(p, lo, hi, t0, t1)) continue;
-        if (cl == L) {
+        ++it;
+        if (!((node.y >> oct) & 1u)) continue;
+        double t0, t1;
+        if (!child_hit(sp, oct, t0, t1)) continue;
+        const uint32_t child = node.x + __popc(node.y & ((1u << oct) - 1u));
+        if (lvl + 1 == L) {
             if (dsub(t1, t0) > kMinHitSpan) on_leaf(child - T.level_off[L], t0, t1);
             continue;
         }
-        lvl = cl;
-        st_node[lvl] = child;
-        st_x[lvl] = cx;
-        st_y[lvl] = cy;
-        st_z[lvl] = cz;
-        st_it[lvl] = 0;
+        st_node[lvl] = make_uint2(node.x, node.y | (it << 8));
+        st_xyz[lvl] = pack_xyz(x, y, z);
+        x = 2u * x + (oct & 1u);
+        y = 2u * y + ((oct >> 1) & 1u);
+        z = 2u * z + ((oct >> 2) & 1u);
+        ++lvl;
+        it = 0;
+        node = T.nodes[child];
+        split_node(T, p.r.o, p.r.d, p.inv, lvl, x, y, z, sp);
     }
 }
 
@@ -79,63 +160,357 @@ __device__ __forceinline__ Ray load_ray(const double* rays, size_t i) {
     return r;
 }
 
-template <bool kCamera>
-__global__ void __launch_bounds__(128) k_traverse_count(DevOctree T, DevCamera cam, uint32_t row0,
-                                                        double* rays, uint32_t n, uint32_t* counts) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    Ray r;
-    if constexpr (kCamera) {
-        const uint64_t px = uint64_t(row0) * cam.width + i;
-        r = pixel_ray(cam, uint32_t(px % cam.width), uint32_t(px / cam.width));
+__device__ __forceinline__ void store_ray(double* rays, size_t i, const Ray& r) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        rays[6 * i + a] = r.o[a];
+        rays[6 * i + 3 + a] = r.d[a];
+    }
+}
+
+// Insertion sort of hits [b, e) by (t_in, leaf index).
+template <typename TinArr, typename LeafArr>
+__device__ __forceinline__ void sort_segment(TinArr tin, LeafArr leaf, uint32_t b, uint32_t e) {
+    for (uint32_t a = b + 1; a < e; ++a) {
+        const double ti = tin[a];
+        const uint32_t lf = leaf[a];
+        uint32_t k = a;
+        while (k > b) {
+            const double tp = tin[k - 1];
+            const uint32_t lp = leaf[k - 1];
+            if (tp < ti || (tp == ti && lp < lf)) break;
+            tin[k] = tp;
+            leaf[k] = lp;
+            --k;
+        }
+        tin[k] = ti;
+        leaf[k] = lf;
+    }
+}
+
+// ---- block-cooperative level-synchronous traversal -------------------------
+constexpr int kRays = 64;      // rays per block, first pass (8 x 8 pixel tile)
+constexpr int kRaysDense = 8;  // rays per block, second pass over overflowed tiles
+constexpr int kThreads = 256;  // threads per block
+constexpr int kQCap = 1536;    // (ray, node) pairs per level
+constexpr int kHCap = 2048;    // leaf hits per tile
+
+struct BfsSmem {
+    double o[3][kRays], d[3][kRays], inv[3][kRays];
+    uint64_t qxyz[2][kQCap];
+    uint32_t qnode[2][kQCap];
+    double htin[kHCap];
+    uint32_t hleaf[kHCap];
+    uint8_t qray[2][kQCap];
+    uint8_t hray[kHCap];
+    uint32_t rcount[kRays], roff[kRays];
+    uint32_t gray[kRays];
+    uint32_t n_q, n_h, base, overflow;
+    typename cub::BlockScan<uint32_t, kThreads>::TempStorage scan;
+};
+
+struct BfsArgs {
+    uint32_t* ray_off;
+    uint32_t* ray_cnt;
+    uint32_t* hit_leaf;
+    double* hit_tin;
+    double* hit_tout;
+    uint32_t* hit_ray;
+    uint32_t* counters;  // [0] hits allocated, [1] overflow rays, [2] capacity exceeded, [3] dense overflow
+    uint32_t* overflow_rays;
+    uint32_t* overflow_dense;
+    double* rays;
+    uint32_t capacity;
+};
+
+// kR rays per block. kList = false: tiles of the image / ray buffer (first
+// pass, overflow -> overflow_rays); kList = true: consecutive entries of
+// overflow_rays (second pass, overflow -> overflow_dense).
+template <bool kCamera, int kR, bool kList>
+__global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0,
+                                                           uint32_t rows, uint32_t n, BfsArgs A) {
+    extern __shared__ __align__(16) uint8_t bfs_smem[];
+    BfsSmem& S = *reinterpret_cast<BfsSmem*>(bfs_smem);
+    using Scan = cub::BlockScan<uint32_t, kThreads>;
+    const uint32_t tid = threadIdx.x;
+
+    // ---- rays of this tile; root test
+    uint32_t my_ray = 0xffffffffu;
+    if (tid < kR) {
+        uint32_t gi;
+        bool ok;
+        if constexpr (kList) {
+            const uint32_t k = blockIdx.x * kR + tid;
+            gi = k < A.counters[1] ? A.overflow_rays[k] : 0xffffffffu;
+            ok = gi != 0xffffffffu;
+        } else if constexpr (kCamera) {
+            const uint32_t tiles_x = (cam.width + 7) / 8;
+            const uint32_t tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+            const uint32_t px = tx * 8 + (tid & 7), py = ty * 8 + (tid >> 3);
+            ok = px < cam.width && py < rows;
+            gi = py * cam.width + px;
+        } else {
+            gi = blockIdx.x * kR + tid;
+            ok = gi < n;
+        }
+        S.gray[tid] = ok ? gi : 0xffffffffu;
+        S.rcount[tid] = 0;
+        if (ok) {
+            my_ray = gi;
+            Ray r;
+            if constexpr (kCamera)
+                r = pixel_ray(cam, gi % cam.width, row0 + gi / cam.width);
+            else
+                r = load_ray(A.rays, gi);
+            const RayPre p = precompute(r);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                S.o[a][tid] = r.o[a];
+                S.d[a][tid] = r.d[a];
+                S.inv[a][tid] = p.inv[a];
+            }
+        }
+    }
+    if (tid == 0) {
+        S.n_q = 0;
+        S.n_h = 0;
+        S.overflow = 0;
+    }
+    __syncthreads();
+    {
+        uint32_t hit = 0;
+        if (my_ray != 0xffffffffu) {
+            double lo[3], hi[3], t0, t1, o[3], d[3];
+            RayPre p;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                o[a] = S.o[a][tid];
+                d[a] = S.d[a][tid];
+                p.r.o[a] = o[a];
+                p.r.d[a] = d[a];
+                p.inv[a] = S.inv[a][tid];
+            }
+            cell_box(T, T.cell[0], 0, 0, 0, lo, hi);
+            hit = slab_test(p, lo, hi, t0, t1) ? 1u : 0u;
+        }
+        uint32_t off, tot;
+        Scan(S.scan).ExclusiveSum(hit, off, tot);
+        if (hit) {
+            S.qnode[0][off] = 0;
+            S.qxyz[0][off] = 0;
+            S.qray[0][off] = uint8_t(tid);
+        }
+        if (tid == 0) S.n_q = tot;
+        __syncthreads();
+    }
+
+    // ---- level by level
+    int cur = 0;
+    uint32_t n_cur = S.n_q;
+    for (int level = 0; level < T.L && n_cur > 0; ++level) {
+        const bool to_leaves = level + 1 == T.L;
+        uint32_t n_out = 0;
+        for (uint32_t base = 0; base < n_cur; base += kThreads) {
+            const uint32_t e = base + tid;
+            // pass 1: which children of pair e are hit (bit = octant), front-to-back order kept below
+            uint32_t hitmask = 0, cnt = 0;
+            NodeSplit sp;
+            uint2 node = make_uint2(0, 0);
+            uint32_t ri = 0, x = 0, y = 0, z = 0, s = 0;
+            if (e < n_cur) {
+                ri = S.qray[cur][e];
+                node = T.nodes[S.qnode[cur][e]];
+                const uint64_t xyz = S.qxyz[cur][e];
+                x = uint32_t(xyz & 0x1fffffu);
+                y = uint32_t((xyz >> 21) & 0x1fffffu);
+                z = uint32_t(xyz >> 42);
+                double o[3], d[3], inv[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    o[a] = S.o[a][ri];
+                    d[a] = S.d[a][ri];
+                    inv[a] = S.inv[a][ri];
+                }
+                split_node(T, o, d, inv, level, x, y, z, sp);
+                s = sign_mask(d);
+#pragma unroll
+                for (uint32_t oct = 0; oct < 8; ++oct) {
+                    if (!((node.y >> oct) & 1u)) continue;
+                    double t0, t1;
+                    if (!child_hit(sp, oct, t0, t1)) continue;
+                    if (to_leaves && !(dsub(t1, t0) > kMinHitSpan)) continue;
+                    hitmask |= 1u << oct;
+                }
+                cnt = __popc(hitmask);
+            }
+            uint32_t off, tot;
+            Scan(S.scan).ExclusiveSum(cnt, off, tot);
+            const uint32_t cap = to_leaves ? kHCap : kQCap;
+            if (n_out + tot > cap) {
+                if (tid == 0) S.overflow = 1;
+                __syncthreads();
+                break;
+            }
+            // pass 2: write the hit children in front-to-back octant order
+            uint32_t w = n_out + off;
+            for (uint32_t it = 0; it < 8 && hitmask; ++it) {
+                const uint32_t oct = it ^ s;
+                if (!((hitmask >> oct) & 1u)) continue;
+                const uint32_t child = node.x + __popc(node.y & ((1u << oct) - 1u));
+                if (to_leaves) {
+                    double t0, t1;
+                    child_hit(sp, oct, t0, t1);
+                    S.hleaf[w] = child - T.level_off[T.L];
+                    S.htin[w] = t0;
+                    S.hray[w] = uint8_t(ri);
+                } else {
+                    S.qnode[cur ^ 1][w] = child;
+                    S.qxyz[cur ^ 1][w] = pack_xyz(2u * x + (oct & 1u), 2u * y + ((oct >> 1) & 1u),
+                                                  2u * z + ((oct >> 2) & 1u));
+                    S.qray[cur ^ 1][w] = uint8_t(ri);
+                }
+                ++w;
+            }
+            n_out += tot;
+            __syncthreads();
+        }
+        if (S.overflow) break;
+        if (to_leaves) {
+            if (tid == 0) S.n_h = n_out;
+            n_cur = 0;
+        } else {
+            n_cur = n_out;
+            cur ^= 1;
+        }
+        __syncthreads();
+    }
+
+    if (S.overflow) {  // hand the whole tile (kept contiguous) to the next pass
+        if (tid == 0) S.base = atomicAdd(&A.counters[kList ? 3 : 1], uint32_t(kR));
+        __syncthreads();
+        if (tid < kR) (kList ? A.overflow_dense : A.overflow_rays)[S.base + tid] = S.gray[tid];
+        return;
+    }
+
+    // ---- per-ray segments: counts, offsets, sort, allocate, write
+    const uint32_t nh = S.n_h;
+    for (uint32_t i = tid; i < nh; i += kThreads) atomicAdd(&S.rcount[S.hray[i]], 1u);
+    __syncthreads();
+    {
+        const uint32_t c = tid < kR ? S.rcount[tid] : 0u;
+        uint32_t off, tot;
+        Scan(S.scan).ExclusiveSum(c, off, tot);
+        if (tid < kR) S.roff[tid] = off;
+        if (tid == 0) {
+            const uint32_t b = tot ? atomicAdd(&A.counters[0], tot) : 0u;
+            S.base = b;
+            if (b + tot > A.capacity) atomicExch(&A.counters[2], 1u);
+        }
+        __syncthreads();
+        if (tid < kR) sort_segment(S.htin, S.hleaf, off, off + c);
+    }
+    __syncthreads();
+    const uint32_t base = S.base;
+    if (base + nh > A.capacity) return;  // host re-runs with a larger buffer
+    if (tid < kR && S.gray[tid] != 0xffffffffu) {
+        A.ray_off[S.gray[tid]] = base + S.roff[tid];
+        A.ray_cnt[S.gray[tid]] = S.rcount[tid];
+        if (kCamera && S.rcount[tid] > 0) {  // later stages read foreground rays only
+            Ray r;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                r.o[a] = S.o[a][tid];
+                r.d[a] = S.d[a][tid];
+            }
+            store_ray(A.rays, S.gray[tid], r);
+        }
+    }
+    for (uint32_t i = tid; i < nh; i += kThreads) {
+        // hits stay grouped by ray (the sort permutes within segments only)
+        const uint32_t ri = S.hray[i];
+        const uint32_t leaf = S.hleaf[i];
+        double lo[3], hi[3], t0, t1;
+        RayPre p;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            rays[6 * size_t(i) + a] = r.o[a];
-            rays[6 * size_t(i) + 3 + a] = r.d[a];
+            p.r.o[a] = S.o[a][ri];
+            p.r.d[a] = S.d[a][ri];
+            p.inv[a] = S.inv[a][ri];
         }
+        leaf_box(T, leaf, lo, hi);
+        slab_test(p, lo, hi, t0, t1);  // t_out of the leaf (t0 equals the stored t_in)
+        A.hit_leaf[base + i] = leaf;
+        A.hit_tin[base + i] = S.htin[i];
+        A.hit_tout[base + i] = t1;
+        A.hit_ray[base + i] = S.gray[ri];
+    }
+}
+
+// Per-ray depth-first traversal of the rays of overflowing tiles.
+template <bool kCamera>
+__global__ void __launch_bounds__(128) k_traverse_fallback(DevOctree T, DevCamera cam, uint32_t row0,
+                                                           const uint32_t* n_list, BfsArgs A) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *n_list) return;
+    const uint32_t i = A.overflow_dense[k];
+    if (i == 0xffffffffu) return;
+    Ray r;
+    if constexpr (kCamera) {
+        r = pixel_ray(cam, i % cam.width, row0 + i / cam.width);
     } else {
-        r = load_ray(rays, i);
+        r = load_ray(A.rays, i);
     }
     const RayPre p = precompute(r);
     uint32_t c = 0;
     walk(T, p, [&](uint32_t, double, double) { ++c; });
-    counts[i] = c;
-}
-
-__global__ void __launch_bounds__(128) k_traverse_emit(DevOctree T, const double* rays, uint32_t n,
-                                                       const uint32_t* offsets, uint32_t* hit_leaf,
-                                                       double* hit_tin, double* hit_tout,
-                                                       uint32_t* hit_ray) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t base = offsets[i], end = offsets[i + 1];
-    if (base == end) return;
-    const RayPre p = precompute(load_ray(rays, i));
-    uint32_t k = base;
+    const uint32_t base = c ? atomicAdd(&A.counters[0], c) : 0u;
+    A.ray_off[i] = base;
+    A.ray_cnt[i] = c;
+    if (kCamera && c > 0) store_ray(A.rays, i, r);
+    if (base + c > A.capacity) {
+        atomicExch(&A.counters[2], 1u);
+        return;
+    }
+    uint32_t w = base;
     walk(T, p, [&](uint32_t leaf, double t0, double t1) {
-        hit_leaf[k] = leaf;
-        hit_tin[k] = t0;
-        hit_tout[k] = t1;
-        hit_ray[k] = i;
-        ++k;
+        A.hit_leaf[w] = leaf;
+        A.hit_tin[w] = t0;
+        A.hit_tout[w] = t1;
+        A.hit_ray[w] = i;
+        ++w;
     });
-    // insertion sort of the (nearly sorted) segment by (t_in, leaf index)
-    for (uint32_t a = base + 1; a < end; ++a) {
-        const double ti = hit_tin[a], to = hit_tout[a];
-        const uint32_t lf = hit_leaf[a];
+    // sort (t_in, leaf) carrying t_out
+    for (uint32_t a = base + 1; a < base + c; ++a) {
+        const double ti = A.hit_tin[a], to = A.hit_tout[a];
+        const uint32_t lf = A.hit_leaf[a];
         uint32_t b = a;
         while (b > base) {
-            const double tp = hit_tin[b - 1];
-            const uint32_t lp = hit_leaf[b - 1];
+            const double tp = A.hit_tin[b - 1];
+            const uint32_t lp = A.hit_leaf[b - 1];
             if (tp < ti || (tp == ti && lp < lf)) break;
-            hit_tin[b] = tp;
-            hit_tout[b] = hit_tout[b - 1];
-            hit_leaf[b] = lp;
+            A.hit_tin[b] = tp;
+            A.hit_tout[b] = A.hit_tout[b - 1];
+            A.hit_leaf[b] = lp;
             --b;
         }
-        hit_tin[b] = ti;
-        hit_tout[b] = to;
-        hit_leaf[b] = lf;
+        A.hit_tin[b] = ti;
+        A.hit_tout[b] = to;
+        A.hit_leaf[b] = lf;
+    }
+}
+
+// CSR view (ray order) of the traversal output: out[csr[i] + k] = in[off[i] + k]
+__global__ void k_to_csr(const uint32_t* ray_off, const uint32_t* ray_cnt, const uint32_t* csr, uint32_t n,
+                         const uint32_t* leaf, const double* tin, const double* tout, uint32_t* leaf_o,
+                         double* tin_o, double* tout_o, uint32_t* ray_o) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t s = ray_off[i], c = ray_cnt[i], d = csr[i];
+    for (uint32_t k = 0; k < c; ++k) {
+        leaf_o[d + k] = leaf[s + k];
+        tin_o[d + k] = tin[s + k];
+        tout_o[d + k] = tout[s + k];
+        ray_o[d + k] = i;
     }
 }
 
@@ -173,23 +548,71 @@ void launch_hit_points(const double* rays, const uint32_t* hit_ray, const double
     note_launch();
 }
 
-void launch_traverse_count(const DevOctree& T, const DevCamera* cam, uint32_t row0, double* rays,
-                           uint32_t n, uint32_t* counts, cudaStream_t s) {
+template <bool kCamera, int kR, bool kList>
+static void set_bfs_attr() {
+    static bool done = false;
+    if (!done) {
+        SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kList>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BfsSmem))));
+        done = true;
+    }
+}
+
+static BfsArgs bfs_args(const TraverseOut& o) {
+    return BfsArgs{o.ray_off, o.ray_cnt, o.hit_leaf, o.hit_tin, o.hit_tout, o.hit_ray,
+                   o.counters, o.overflow_rays, o.overflow_dense, o.rays, o.capacity};
+}
+
+void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
+                     const TraverseOut& o, cudaStream_t s) {
     if (n == 0) return;
-    const uint32_t blocks = (n + 127) / 128;
-    if (cam)
-        k_traverse_count<true><<<blocks, 128, 0, s>>>(T, *cam, row0, rays, n, counts);
-    else
-        k_traverse_count<false><<<blocks, 128, 0, s>>>(T, DevCamera{}, 0, rays, n, counts);
+    const BfsArgs A = bfs_args(o);
+    if (cam) {
+        set_bfs_attr<true, kRays, false>();
+        const uint32_t tiles = ((cam->width + 7) / 8) * ((rows + 7) / 8);
+        k_traverse_bfs<true, kRays, false><<<tiles, kThreads, sizeof(BfsSmem), s>>>(T, *cam, row0, rows, n, A);
+    } else {
+        set_bfs_attr<false, kRays, false>();
+        k_traverse_bfs<false, kRays, false><<<(n + kRays - 1) / kRays, kThreads, sizeof(BfsSmem), s>>>(
+            T, DevCamera{}, 0, 0, n, A);
+    }
     note_launch();
 }
 
-void launch_traverse_emit(const DevOctree& T, const double* rays, uint32_t n, const uint32_t* offsets,
-                          uint32_t* hit_leaf, double* hit_tin, double* hit_tout, uint32_t* hit_ray,
-                          cudaStream_t s) {
+void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
+                           const TraverseOut& o, cudaStream_t s) {
+    if (n_overflow == 0) return;
+    const BfsArgs A = bfs_args(o);
+    const uint32_t blocks = (n_overflow + kRaysDense - 1) / kRaysDense;
+    if (cam) {
+        set_bfs_attr<true, kRaysDense, true>();
+        k_traverse_bfs<true, kRaysDense, true><<<blocks, kThreads, sizeof(BfsSmem), s>>>(T, *cam, row0, 0, 0, A);
+    } else {
+        set_bfs_attr<false, kRaysDense, true>();
+        k_traverse_bfs<false, kRaysDense, true><<<blocks, kThreads, sizeof(BfsSmem), s>>>(T, DevCamera{}, 0, 0,
+                                                                                          0, A);
+    }
+    note_launch();
+}
+
+void launch_traverse_fallback(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
+                              const TraverseOut& o, cudaStream_t s) {
+    if (n_overflow == 0) return;
+    const BfsArgs A = bfs_args(o);
+    const uint32_t blocks = (n_overflow + 127) / 128;
+    if (cam)
+        k_traverse_fallback<true><<<blocks, 128, 0, s>>>(T, *cam, row0, o.counters + 3, A);
+    else
+        k_traverse_fallback<false><<<blocks, 128, 0, s>>>(T, DevCamera{}, 0, o.counters + 3, A);
+    note_launch();
+}
+
+void launch_to_csr(const uint32_t* ray_off, const uint32_t* ray_cnt, const uint32_t* csr, uint32_t n,
+                   const uint32_t* leaf, const double* tin, const double* tout, uint32_t* leaf_o, double* tin_o,
+                   double* tout_o, uint32_t* ray_o, cudaStream_t s) {
     if (n == 0) return;
-    k_traverse_emit<<<(n + 127) / 128, 128, 0, s>>>(T, rays, n, offsets, hit_leaf, hit_tin, hit_tout,
-                                                     hit_ray);
+    k_to_csr<<<(n + 127) / 128, 128, 0, s>>>(ray_off, ray_cnt, csr, n, leaf, tin, tout, leaf_o, tin_o, tout_o,
+                                             ray_o);
     note_launch();
 }
 
