@@ -726,20 +726,30 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
     require(mode == SVLF_LOSS_SURFACE || mode == SVLF_LOSS_VOLUMETRIC, "bad loss mode");
     DeviceGuard g(ctx->device);
     std::lock_guard<std::mutex> lk(ctx->mu);
-    TrainArgs a{};
-    a.rays = rays;
-    a.c_gt = c_gt;
-    a.depth_gt = depth_gt;
-    a.alpha_gt = alpha_gt;
-    a.n = uint32_t(n);
-    a.surface = mode == SVLF_LOSS_SURFACE;
-    a.color_frozen = color_frozen != 0;
-    a.lw = *lw;
-    a.adam = adam;
-    a.lr = lr;
+    cudaStream_t s = ctx->stream;
+    const uint32_t nn = uint32_t(n);
+    reset_misc(ctx);
+    TrainScratch& S = ctx->train;
+    double* d_rays = ctx->rays.ensure<double>(size_t(nn) * 6 + 6);
+    float* d_cgt = S.c_gt.ensure<float>(size_t(nn) * 3 + 3);
+    double* d_depth = S.depth.ensure<double>(size_t(nn) + 1);
+    uint8_t* d_alpha = S.alpha.ensure<uint8_t>(size_t(nn) + 1);
+    if (nn) {
+        SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyHostToDevice, s));
+        SVLF_CUDA(cudaMemcpyAsync(d_cgt, c_gt, size_t(nn) * 12, cudaMemcpyHostToDevice, s));
+        SVLF_CUDA(cudaMemcpyAsync(d_depth, depth_gt, size_t(nn) * 8, cudaMemcpyHostToDevice, s));
+        SVLF_CUDA(cudaMemcpyAsync(d_alpha, alpha_gt, size_t(nn), cudaMemcpyHostToDevice, s));
+    }
+    const uint32_t total = nn ? run_traversal(ctx, m->tree, nullptr, 0, 0, nn) : 0;
+    const float trav_ms = ctx->last.traverse_ms;
+    TrainBatchDev b{d_rays, d_cgt, d_depth, d_alpha, nn, ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(),
+                    ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total};
+    TrainOptions opt{mode == SVLF_LOSS_SURFACE, color_frozen != 0, adam, *lw, lr};
+    ensure_pack_f32(m, s);
     TrainModelRefs mr{m->view(), m->params.as<float>(), m->grads.as<float>(), m->adam_m.as<float>(),
-                      m->adam_v.as<float>(), m->n_ft, m->n_fc, m->steps};
-    TrainResult r = run_train_step(ctx->train, dev_view(m->tree), mr, a, ctx->stream, ctx->misc.as<int>());
+                      m->adam_v.as<float>(), m->n_ft, m->n_fc, m->steps, pack_f32_view(m->pack_f32.as<float>())};
+    TrainResult r = run_train_step(S, dev_view(m->tree), mr, b, opt, s, ctx->misc.as<int>());
+    r.timings.traverse_ms = trav_ms;
     if (r.error) fail(SVLF_ERR_RUNTIME, dev_error_message(r.error));
     if (adam) ++m->version;
     ctx->last = r.timings;

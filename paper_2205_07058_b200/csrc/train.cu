@@ -1,7 +1,565 @@
-// Train step: placeholder until the fused backward lands.
+// Train step on the GPU: the per-frame body of the reference's train()
+// (src/train.cpp:443-479): loss_chunk over the batch (:65-287), gradient sum,
+// adam_model_step (:345-360).
+//
+// Pipeline (rays already traversed, per-ray hit segments sorted):
+//   k_prep     per ray: surface voxel (locate() of ray.at(depth_gt) matched
+//              against the ray's hits), eta_gt with the reference's
+//              "surface point outside voxel" check, active hit range per mode
+//              (stage 1 keeps pre-surface + surface hits, or the surface hit
+//              only when lambda_empty == 0), skipped / eta_skipped counters.
+//   scan/expand  dense list of active hits.
+//   k_fwd      per hit: f_T (and f_C where the loss needs colour) forward in
+//              fp32, reference accumulation order; activations stored
+//              feature-major in global scratch for the backward pass.
+//   k_loss     per ray: Eq. 4 surface loss or composite + volumetric loss in
+//              fp64 and the composite backward dtau_j = dw_j T_j e_j -
+//              sum_{i>j} dw_i w_i (reverse scan), per-ray loss.
+//   k_bwd      per hit: f_C backward (input gradient always; feature
+//              gradients unless colour is frozen) incl. the positional
+//              Jacobian d eta += <dx_s, x1 - x2>, then f_T backward; feature
+//              gradients scattered with atomics; layer deltas stored.
+//   k_gemm_dw  weight gradients dW = D^T X per layer (split over hits).
+//   k_adam     dense bias-corrected Adam in fp64 over every parameter
+//              (src/mlp.cpp:277-296), colour tensors skipped when frozen.
+// Gradients are sums over rays (no 1/N), as in the reference.
+#include <cmath>
+#include <cstring>
+
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "mlp_simt.cuh"
 #include "train.cuh"
 
 namespace svlfb {
+
+namespace {
+
+// feature-major activation rows (x N hits)
+constexpr int A_XT = 0, A_HT = 134, A_XC = 262, A_H1 = 300, A_H2 = 428, A_H3 = 556, A_ROWS = 684;
+// feature-major delta rows (dL/d pre-activation of each layer)
+constexpr int D_T0 = 0, D_T1 = 128, D_C0 = 130, D_C1 = 258, D_C2 = 386, D_C3 = 514, D_ROWS = 517;
+
+struct PrepArgs {
+    const double* rays;
+    const double* depth;
+    const uint8_t* alpha;
+    uint32_t n;
+    const uint32_t* ray_off;
+    const uint32_t* ray_cnt;
+    const uint32_t* hit_leaf;
+    const double* hit_tin;
+    const double* hit_tout;
+    bool surface;
+    bool empty_zero;
+    uint32_t* act_first;
+    uint32_t* act_cnt;
+    int* surf_rel;
+    double* eta_gt;
+    unsigned long long* counters;  // [0] skipped, [1] eta_skipped
+};
+
+__device__ __forceinline__ Ray ray_of(const double* rays, uint32_t i) {
+    Ray r;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r.o[a] = rays[6 * size_t(i) + a];
+        r.d[a] = rays[6 * size_t(i) + 3 + a];
+    }
+    return r;
+}
+
+// loss_chunk gather step (src/train.cpp:75-124) for one ray.
+__global__ void k_prep(DevOctree T, PrepArgs A, int* err) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= A.n) return;
+    const uint32_t off = A.ray_off[r], cnt = A.ray_cnt[r];
+    int surf = -1;
+    double eg = 0.0;
+    if (A.alpha[r]) {
+        const Ray ray = ray_of(A.rays, r);
+        double p[3];
+        ray_at(ray, A.depth[r], p);
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) inside = inside && p[a] >= T.lo[a] && p[a] <= T.hi[a];
+        if (inside) {  // locate(), src/octree.cpp:173-183
+            uint32_t c[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const uint32_t q = uint32_t(ddiv(dsub(p[a], T.lo[a]), T.cell_size));
+                c[a] = q < T.res - 1 ? q : T.res - 1;
+            }
+            uint64_t code = 0;
+            for (int bit = 0; bit < 21; ++bit)
+                code |= (uint64_t((c[0] >> bit) & 1u) << (3 * bit)) | (uint64_t((c[1] >> bit) & 1u) << (3 * bit + 1)) |
+                        (uint64_t((c[2] >> bit) & 1u) << (3 * bit + 2));
+            for (uint32_t k = 0; k < cnt; ++k) {
+                if (T.leaf_codes[A.hit_leaf[off + k]] == code) {
+                    surf = int(k);
+                    const double tin = A.hit_tin[off + k], tout = A.hit_tout[off + k], d = A.depth[r];
+                    if (d < dsub(tin, 1e-6) || d > dadd(tout, 1e-6)) raise_error(err, kErrSurfaceOutside);
+                    // eta_gt, src/train.cpp:30-35
+                    eg = fmin(fmax(ddiv(dsub(tout, d), dsub(tout, tin)), 0.0), 1.0);
+                    break;
+                }
+            }
+        }
+    }
+    uint32_t first = off, n_act = cnt;
+    int srel = surf;
+    if (A.surface) {
+        if (!A.alpha[r] || surf < 0) {
+            atomicAdd(&A.counters[0], 1ull);
+            n_act = 0;
+            srel = -1;
+        } else if (A.empty_zero) {  // surface voxel only (src/train.cpp:105-109)
+            first = off + uint32_t(surf);
+            n_act = 1;
+            srel = 0;
+        } else {
+            n_act = uint32_t(surf) + 1;
+        }
+    } else if (A.alpha[r] && surf < 0) {
+        atomicAdd(&A.counters[1], 1ull);
+    }
+    A.act_first[r] = first;
+    A.act_cnt[r] = n_act;
+    A.surf_rel[r] = srel;
+    A.eta_gt[r] = eg;
+}
+
+__global__ void k_expand(uint32_t n, const uint32_t* act_first, const uint32_t* act_cnt, const uint32_t* dpos,
+                         uint32_t* dhit, uint32_t* dray) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t b = dpos[r], f = act_first[r];
+    for (uint32_t k = 0; k < act_cnt[r]; ++k) {
+        dhit[b + k] = f + k;
+        dray[b + k] = r;
+    }
+}
+
+struct HitArgs {
+    const double* rays;
+    const uint32_t* hit_leaf;
+    const double* hit_tin;
+    const double* hit_tout;
+    const uint32_t* dhit;
+    const uint32_t* dray;
+    const uint32_t* dpos;
+    const int* surf_rel;
+    uint32_t N;
+    bool surface;
+    float* acts;    // A_ROWS x N
+    float* deltas;  // D_ROWS x N
+    float* tau;
+    float* eta;
+    float* rgb;     // 3 x N (channel-major)
+    float* drgb;    // 3 x N
+    double* dtau;
+    double* deta;
+};
+
+__device__ __forceinline__ bool has_color(const HitArgs& H, uint32_t j) {
+    if (!H.surface) return true;
+    const uint32_t r = H.dray[j];
+    return H.surf_rel[r] >= 0 && j == H.dpos[r] + uint32_t(H.surf_rel[r]);
+}
+
+// Per-hit geometry shared by forward and backward.
+struct HitGeom {
+    Ray ray;
+    double lo[3], hi[3], x1[3], x2[3];
+    uint32_t corners[8];
+    float r6[6], w1[8], w2[8];
+};
+
+__device__ __forceinline__ bool hit_geom(const DevOctree& T, const HitArgs& H, uint32_t j, HitGeom& g, int* err) {
+    const uint32_t h = H.dhit[j];
+    g.ray = ray_of(H.rays, H.dray[j]);
+    const uint32_t leaf = H.hit_leaf[h];
+    leaf_box(T, leaf, g.lo, g.hi);
+    ray_at(g.ray, H.hit_tin[h], g.x1);
+    ray_at(g.ray, H.hit_tout[h], g.x2);
+    if (!parameterize(g.ray, g.lo, g.hi, g.r6)) {
+        raise_error(err, kErrTangentRay);
+        return false;
+    }
+    if (!trilinear_at(g.x1, g.lo, g.hi, T.cell_size, g.w1) || !trilinear_at(g.x2, g.lo, g.hi, T.cell_size, g.w2)) {
+        raise_error(err, kErrPointNotInVoxel);
+        return false;
+    }
+    const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
+    const uint4 a = __ldg(cp), b = __ldg(cp + 1);
+    g.corners[0] = a.x; g.corners[1] = a.y; g.corners[2] = a.z; g.corners[3] = a.w;
+    g.corners[4] = b.x; g.corners[5] = b.y; g.corners[6] = b.z; g.corners[7] = b.w;
+    return true;
+}
+
+// x_s = x1*eta + x2*(1-eta) and its local coordinates (voxel_batch.hpp:111,129)
+__device__ __forceinline__ bool xs_coords(const DevOctree& T, const HitGeom& g, float eta, double* xs, double* u) {
+    const double e = double(eta), ome = dsub(1.0, e);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) xs[a] = dadd(dmul(g.x1[a], e), dmul(g.x2[a], ome));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!(xs[a] >= dsub(g.lo[a], 1e-7) && xs[a] <= dadd(g.hi[a], 1e-7))) return false;
+        u[a] = fmin(fmax(ddiv(dsub(xs[a], g.lo[a]), T.cell_size), 0.0), 1.0);
+    }
+    return true;
+}
+
+__device__ __forceinline__ void weights_from_u(const double* u, float* w) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const double wx = (b & 1) ? u[0] : dsub(1.0, u[0]);
+        const double wy = (b & 2) ? u[1] : dsub(1.0, u[1]);
+        const double wz = (b & 4) ? u[2] : dsub(1.0, u[2]);
+        w[b] = float(dmul(dmul(wx, wy), wz));
+    }
+}
+
+// ---- forward ------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_fwd(DevOctree T, DevModel M, DecPackF32 P, HitArgs H, int* err) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= H.N) return;
+    const size_t N = H.N;
+    float* X = H.acts + j;
+    HitGeom g;
+    if (!hit_geom(T, H, j, g, err)) {
+        H.tau[j] = 0.f;
+        H.eta[j] = 0.5f;
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) X[(A_XT + k) * N] = g.r6[k];
+    gather_col<kFt>(M.ft, g.corners, g.w1, X + (A_XT + 6) * N, N);
+    gather_col<kFt>(M.ft, g.corners, g.w2, X + (A_XT + 6 + kFt) * N, N);
+    dense_relu_col(P.t_w0t, P.t_b0, X + A_XT * N, kInT, X + A_HT * N, N);
+    const float y0 = head_dot(P.t_w1, __ldg(P.t_b1), X + A_HT * N, N);
+    const float y1 = head_dot(P.t_w1 + kHid, __ldg(P.t_b1 + 1), X + A_HT * N, N);
+    const float tau = y0 > 0.f ? y0 : 0.f;
+    const float eta = sigmoid_ref(y1);
+    H.tau[j] = tau;
+    H.eta[j] = eta;
+    if (!has_color(H, j)) return;
+    double xs[3], u[3];
+    float ws[8];
+    if (!xs_coords(T, g, eta, xs, u)) {
+        raise_error(err, kErrPointNotInVoxel);
+        return;
+    }
+    weights_from_u(u, ws);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) X[(A_XC + k) * N] = g.r6[k];
+    gather_col<kFc>(M.fc, g.corners, ws, X + (A_XC + 6) * N, N);
+    dense_relu_col(P.c_w0t, P.c_b0, X + A_XC * N, kInC, X + A_H1 * N, N);
+    dense_relu_col(P.c_w1t, P.c_b1, X + A_H1 * N, kHid, X + A_H2 * N, N);
+    dense_relu_col(P.c_w2t, P.c_b2, X + A_H2 * N, kHid, X + A_H3 * N, N);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) H.rgb[c * N + j] = sigmoid_ref(head_dot(P.c_w3 + c * kHid, __ldg(P.c_b3 + c), X + A_H3 * N, N));
+}
+
+// ---- loss + composite backward (per ray) ---------------------------------------
+struct LossArgs {
+    const float* c_gt;
+    const uint8_t* alpha;
+    const uint32_t* dpos;
+    const uint32_t* act_cnt;
+    const int* surf_rel;
+    const double* eta_gt;
+    const double* hit_tin;  // unused: t_s is not part of the loss
+    uint32_t n;
+    bool surface;
+    svlf_loss_weights lw;
+    double* ray_loss;
+    double* ehit;
+    double* trans;
+    double* wgt;
+};
+
+__global__ void k_loss(LossArgs L, HitArgs H) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= L.n) return;
+    const size_t N = H.N;
+    const uint32_t b = L.dpos[r], cnt = L.act_cnt[r];
+    const int srel = L.surf_rel[r];
+    const double eg = L.eta_gt[r];
+    double loss = 0.0;
+    const double cg[3] = {double(L.c_gt[3 * size_t(r)]), double(L.c_gt[3 * size_t(r) + 1]),
+                          double(L.c_gt[3 * size_t(r) + 2])};
+    if (L.surface) {  // src/train.cpp:158-181
+        if (cnt == 0) {
+            L.ray_loss[r] = 0.0;
+            return;
+        }
+        const uint32_t js = b + uint32_t(srel);
+        double dc[3];
+        for (int ch = 0; ch < 3; ++ch) {
+            const double diff = dsub(double(H.rgb[ch * N + js]), cg[ch]);
+            loss = dadd(loss, dmul(diff, diff));
+            dc[ch] = dmul(2.0, diff);
+        }
+        const double ediff = dsub(double(H.eta[js]), eg);
+        loss = dadd(loss, dmul(dmul(L.lw.eta, ediff), ediff));
+        H.deta[js] = dadd(H.deta[js], dmul(dmul(2.0, L.lw.eta), ediff));
+        const double e2 = exp(dmul(-2.0, double(H.tau[js])));
+        loss = dadd(loss, dmul(L.lw.tau, e2));
+        H.dtau[js] = dadd(H.dtau[js], dmul(dmul(-2.0, L.lw.tau), e2));
+        for (uint32_t k = 0; k < uint32_t(srel); ++k) {
+            const uint32_t j = b + k;
+            const double e = exp(-double(H.tau[j]));
+            const double olap = dsub(1.0, e);
+            loss = dadd(loss, dmul(dmul(L.lw.empty, olap), olap));
+            H.dtau[j] = dadd(H.dtau[j], dmul(dmul(dmul(2.0, L.lw.empty), olap), e));
+        }
+        for (int ch = 0; ch < 3; ++ch) H.drgb[ch * N + js] = float(dc[ch]);
+        L.ray_loss[r] = loss;
+        return;
+    }
+    // volumetric: composite, src/train.cpp:184-232
+    double color[3] = {0.0, 0.0, 0.0}, alpha = 0.0, Tr = 1.0;
+    for (uint32_t k = 0; k < cnt; ++k) {
+        const uint32_t j = b + k;
+        const double e = exp(-double(H.tau[j]));
+        const double w = dmul(Tr, dsub(1.0, e));
+        L.ehit[j] = e;
+        L.trans[j] = Tr;
+        L.wgt[j] = w;
+        for (int ch = 0; ch < 3; ++ch) color[ch] = dadd(color[ch], dmul(w, double(H.rgb[ch * N + j])));
+        alpha = dadd(alpha, w);
+        Tr = dmul(Tr, e);
+    }
+    double d_color[3];
+    for (int ch = 0; ch < 3; ++ch) {
+        const double diff = dsub(color[ch], cg[ch]);
+        loss = dadd(loss, dmul(diff, diff));
+        d_color[ch] = dmul(2.0, diff);
+    }
+    const double agt = L.alpha[r] ? 1.0 : 0.0;
+    loss = dadd(loss, dmul(dmul(L.lw.alpha, dsub(alpha, agt)), dsub(alpha, agt)));
+    const double d_alpha = dmul(dmul(2.0, L.lw.alpha), dsub(alpha, agt));
+    if (L.alpha[r] && srel >= 0) {
+        const uint32_t js = b + uint32_t(srel);
+        const double ediff = dsub(double(H.eta[js]), eg);
+        loss = dadd(loss, dmul(dmul(L.lw.eta, ediff), ediff));
+        H.deta[js] = dadd(H.deta[js], dmul(dmul(2.0, L.lw.eta), ediff));
+    }
+    double suffix = 0.0;
+    for (int64_t k = int64_t(cnt) - 1; k >= 0; --k) {
+        const uint32_t j = b + uint32_t(k);
+        double dw = d_alpha;
+        for (int ch = 0; ch < 3; ++ch) dw = dadd(dw, dmul(d_color[ch], double(H.rgb[ch * N + j])));
+        H.dtau[j] = dadd(H.dtau[j], dsub(dmul(dmul(dw, L.trans[j]), L.ehit[j]), suffix));
+        suffix = dadd(suffix, dmul(dw, L.wgt[j]));
+        for (int ch = 0; ch < 3; ++ch) H.drgb[ch * N + j] = float(dmul(L.wgt[j], d_color[ch]));
+    }
+    L.ray_loss[r] = loss;
+}
+
+// ---- backward -----------------------------------------------------------------
+// dx[k] = sum_o W[o][k] d[o] for k in [0, K) (o outer, k inner: the reference's
+// d_prev accumulation order, src/mlp.cpp:205-215), optional relu mask by the
+// layer input activation, stored at out[k * N].
+template <int O>
+__device__ __forceinline__ void back_matvec(const float* __restrict__ W, int K, const float* d, size_t dstride,
+                                            const float* mask, size_t N, float* out) {
+#pragma unroll 1
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        float acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+#pragma unroll 2
+        for (int o = 0; o < O; ++o) {
+            const float dv = d[o * dstride];
+            const float* wr = W + size_t(o) * K + k0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (k0 + i < K) acc[i] = __fadd_rn(acc[i], __fmul_rn(__ldg(wr + i), dv));
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (k0 + i >= K) break;
+            float v = acc[i];
+            if (mask && !(mask[(k0 + i) * N] > 0.f)) v = 0.f;
+            out[(k0 + i) * N] = v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) k_bwd(DevOctree T, DevModel M, HitArgs H, bool color_frozen, float* g_ft,
+                                             float* g_fc, int* err) {
+    using D = DecOffsets;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= H.N) return;
+    const size_t N = H.N;
+    const float* X = H.acts + j;
+    float* Dl = H.deltas + j;
+    HitGeom g;
+    if (!hit_geom(T, H, j, g, err)) return;
+    double deta = H.deta[j];
+    if (has_color(H, j)) {
+        // head: sigmoid' (src/mlp.cpp:174-176)
+        for (int o = 0; o < 3; ++o) {
+            const float a = H.rgb[o * N + j];
+            Dl[(D_C3 + o) * N] = __fmul_rn(__fmul_rn(H.drgb[o * N + j], a), __fsub_rn(1.0f, a));
+        }
+        back_matvec<3>(M.mc + D::C_W3, kHid, Dl + D_C3 * N, N, X + A_H3 * N, N, Dl + D_C2 * N);
+        back_matvec<kHid>(M.mc + D::C_W2, kHid, Dl + D_C2 * N, N, X + A_H2 * N, N, Dl + D_C1 * N);
+        back_matvec<kHid>(M.mc + D::C_W1, kHid, Dl + D_C1 * N, N, X + A_H1 * N, N, Dl + D_C0 * N);
+        // d input of f_C: only the 32 colour-feature rows are needed (the r6 part has no parameters)
+        float dz[kFc];
+        {
+            float tmp[kInC];
+#pragma unroll 1
+            for (int k = 0; k < kInC; ++k) tmp[k] = 0.f;
+            for (int o = 0; o < kHid; ++o) {
+                const float dv = Dl[(D_C0 + o) * N];
+                const float* wr = M.mc + D::C_W0 + size_t(o) * kInC;
+#pragma unroll
+                for (int k = 0; k < kInC; ++k) tmp[k] = __fadd_rn(tmp[k], __fmul_rn(__ldg(wr + k), dv));
+            }
+#pragma unroll
+            for (int d = 0; d < kFc; ++d) dz[d] = tmp[6 + d];
+        }
+        double xs[3], u[3];
+        if (!xs_coords(T, g, H.eta[j], xs, u)) {
+            raise_error(err, kErrPointNotInVoxel);
+            return;
+        }
+        if (!color_frozen) {  // src/train.cpp:244-253
+            float ws[8];
+            weights_from_u(u, ws);
+            for (int b = 0; b < 8; ++b) {
+                float* grow = g_fc + size_t(g.corners[b]) * kFc;
+#pragma unroll 4
+                for (int d = 0; d < kFc; ++d) atomicAdd(grow + d, __fmul_rn(ws[b], dz[d]));
+            }
+        }
+        // d eta via x_s: dx_s = sum_b dw_b/du <z_b, dz> / h (src/train.cpp:254-265)
+        const double inv_h = ddiv(1.0, T.cell_size);
+        const double wxv[2] = {dsub(1.0, u[0]), u[0]}, wyv[2] = {dsub(1.0, u[1]), u[1]},
+                     wzv[2] = {dsub(1.0, u[2]), u[2]}, dxv[2] = {-1.0, 1.0};
+        double dxs[3] = {0.0, 0.0, 0.0};
+        for (int b = 0; b < 8; ++b) {
+            const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
+            const double gw[3] = {dmul(dmul(dxv[bx], wyv[by]), wzv[bz]), dmul(dmul(wxv[bx], dxv[by]), wzv[bz]),
+                                  dmul(dmul(wxv[bx], wyv[by]), dxv[bz])};
+            const float* zb = M.fc + size_t(g.corners[b]) * kFc;
+            double dotv = 0.0;
+            for (int d = 0; d < kFc; ++d) dotv = dadd(dotv, dmul(double(__ldg(zb + d)), double(dz[d])));
+            const double sc = dmul(dotv, inv_h);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) dxs[a] = dadd(dxs[a], dmul(gw[a], sc));
+        }
+        const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
+        deta = dadd(deta, dot3(dxs, dx12));
+    }
+    // f_T: heads relu (tau) and sigmoid (eta)
+    const float dt = float(H.dtau[j]), de = float(deta);
+    const float tau = H.tau[j], eta = H.eta[j];
+    Dl[D_T1 * N] = tau > 0.f ? dt : 0.f;
+    Dl[(D_T1 + 1) * N] = __fmul_rn(__fmul_rn(de, eta), __fsub_rn(1.0f, eta));
+    back_matvec<2>(M.mt + D::T_W1, kHid, Dl + D_T1 * N, N, X + A_HT * N, N, Dl + D_T0 * N);
+    // d input of f_T, feature rows only: dz1 = rows 6..69, dz2 = rows 70..133
+#pragma unroll 1
+    for (int k0 = 6; k0 < kInT; k0 += 16) {
+        float acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+        for (int o = 0; o < kHid; ++o) {
+            const float dv = Dl[(D_T0 + o) * N];
+            const float* wr = M.mt + D::T_W0 + size_t(o) * kInT + k0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (k0 + i < kInT) acc[i] = __fadd_rn(acc[i], __fmul_rn(__ldg(wr + i), dv));
+        }
+        // scatter: grow[d] += w1_b * dz1[d] + w2_b * dz2[d]; chunks cover both halves
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int k = k0 + i;
+            if (k >= kInT) break;
+            const bool first = k < 6 + kFt;
+            const int d = first ? k - 6 : k - 6 - kFt;
+            for (int b = 0; b < 8; ++b)
+                atomicAdd(g_ft + size_t(g.corners[b]) * kFt + d, __fmul_rn(first ? g.w1[b] : g.w2[b], acc[i]));
+        }
+    }
+}
+
+// dW[o][k] += sum_j D[o][j] X[k][j] (split over hits), db[o] += sum_j D[o][j]
+__global__ void __launch_bounds__(256) k_gemm_dw(const float* __restrict__ Dm, int O, const float* __restrict__ Xm,
+                                                 int K, size_t N, size_t chunk, float* dW, float* db) {
+    __shared__ float Ds[32][33], Xs[32][33];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int o0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const size_t j0 = size_t(blockIdx.z) * chunk, j1 = min(N, j0 + chunk);
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, bacc[2] = {0.f, 0.f};
+    for (size_t jb = j0; jb < j1; jb += 32) {
+        for (int t = threadIdx.x; t < 32 * 32; t += 256) {
+            const int rr = t >> 5, cc = t & 31;
+            const size_t jj = jb + cc;
+            Ds[rr][cc] = (o0 + rr < O && jj < j1) ? Dm[size_t(o0 + rr) * N + jj] : 0.f;
+            Xs[rr][cc] = (k0 + rr < K && jj < j1) ? Xm[size_t(k0 + rr) * N + jj] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) {
+            const float d0 = Ds[ty * 2][c], d1 = Ds[ty * 2 + 1][c];
+            const float x0 = Xs[tx * 2][c], x1 = Xs[tx * 2 + 1][c];
+            acc[0][0] += d0 * x0;
+            acc[0][1] += d0 * x1;
+            acc[1][0] += d1 * x0;
+            acc[1][1] += d1 * x1;
+            if (tx == 0) {
+                bacc[0] += d0;
+                bacc[1] += d1;
+            }
+        }
+        __syncthreads();
+    }
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            const int o = o0 + ty * 2 + a, k = k0 + tx * 2 + b;
+            if (o < O && k < K) atomicAdd(dW + size_t(o) * K + k, acc[a][b]);
+        }
+    if (tx == 0 && blockIdx.y == 0 && db)
+        for (int a = 0; a < 2; ++a)
+            if (o0 + ty * 2 + a < O) atomicAdd(db + o0 + ty * 2 + a, bacc[a]);
+}
+
+struct AdamSeg {
+    float* p;
+    const float* g;
+    float* m;
+    float* v;
+    size_t n;
+    double corr1, corr2;
+};
+struct AdamSegs {
+    AdamSeg seg[14];
+    int count;
+};
+
+// adam_step, src/mlp.cpp:277-296 (fp64 math, fp32 storage; beta/eps are
+// float fields promoted to double; lr is rounded to float first, :427).
+__global__ void k_adam(AdamSegs S, float lr) {
+    const AdamSeg sg = S.seg[blockIdx.y];
+    const double b1 = double(0.9f), b2 = double(0.999f), eps = double(1e-8f);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < sg.n; i += size_t(gridDim.x) * blockDim.x) {
+        const double g = sg.g[i];
+        const double m = dadd(dmul(b1, double(sg.m[i])), dmul(dsub(1.0, b1), g));
+        const double v = dadd(dmul(b2, double(sg.v[i])), dmul(dmul(dsub(1.0, b2), g), g));
+        sg.m[i] = float(m);
+        sg.v[i] = float(v);
+        const double mh = ddiv(m, sg.corr1), vh = ddiv(v, sg.corr2);
+        sg.p[i] = float(dsub(double(sg.p[i]), ddiv(dmul(double(lr), mh), dadd(__dsqrt_rn(vh), eps))));
+    }
+}
+
+}  // namespace
 
 TrainScratch::~TrainScratch() {
     if (h_pinned) cudaFreeHost(h_pinned);
@@ -9,9 +567,151 @@ TrainScratch::~TrainScratch() {
         if (e) cudaEventDestroy(e);
 }
 
-TrainResult run_train_step(TrainScratch&, const DevOctree&, TrainModelRefs&, const TrainArgs&, cudaStream_t,
-                           int*) {
-    fail(SVLF_ERR_RUNTIME, "train step not implemented yet");
+TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& M, const TrainBatchDev& b,
+                           const TrainOptions& o, cudaStream_t s, int* err_flag) {
+    using D = DecOffsets;
+    TrainResult res;
+    res.rays = b.n;
+    if (!S.h_pinned) {
+        SVLF_CUDA(cudaMallocHost(&S.h_pinned, 64));
+        for (auto& e : S.ev) SVLF_CUDA(cudaEventCreate(&e));
+    }
+    const size_t P = M.n_ft + M.n_fc + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE;
+    SVLF_CUDA(cudaMemsetAsync(M.grads, 0, P * 4, s));
+    const uint32_t n = b.n;
+    SVLF_CUDA(cudaEventRecord(S.ev[0], s));
+
+    // ---- per-ray preparation and dense active-hit list
+    uint32_t* act_first = S.act_first.ensure<uint32_t>(n + 1);
+    uint32_t* act_cnt = S.act_cnt.ensure<uint32_t>(n + 1);
+    uint32_t* dpos = S.dpos.ensure<uint32_t>(n + 1);
+    int* surf_rel = S.surf_rel.ensure<int>(n + 1);
+    double* eta_gt = S.eta_gt.ensure<double>(n + 1);
+    double* ray_loss = S.ray_loss.ensure<double>(n + 1);
+    unsigned long long* counters = S.counters.ensure<unsigned long long>(4);
+    double* loss_out = S.loss_out.ensure<double>(1);
+    SVLF_CUDA(cudaMemsetAsync(counters, 0, 32, s));
+    SVLF_CUDA(cudaMemsetAsync(act_cnt + n, 0, 4, s));
+    PrepArgs pa{b.rays, b.depth_gt, b.alpha_gt, n, b.ray_off, b.ray_cnt, b.hit_leaf, b.hit_tin, b.hit_tout,
+                o.surface, o.lw.empty == 0.0, act_first, act_cnt, surf_rel, eta_gt, counters};
+    if (n) k_prep<<<(n + 127) / 128, 128, 0, s>>>(T, pa, err_flag);
+    {
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, act_cnt, dpos, int(n + 1));
+        SVLF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.ensure<char>(tb), tb, act_cnt, dpos, int(n + 1), s));
+    }
+    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned, dpos + n, 4, cudaMemcpyDeviceToHost, s));
+    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
+    SVLF_CUDA(cudaStreamSynchronize(s));
+    const uint32_t N = uint32_t(S.h_pinned[0]);
+    unsigned long long cnts[2];
+    std::memcpy(cnts, S.h_pinned + 4, 16);
+    res.skipped = (long long)cnts[0];
+    res.eta_skipped = (long long)cnts[1];
+
+    uint32_t* dhit = S.dhit.ensure<uint32_t>(N + 1);
+    uint32_t* dray = S.dray.ensure<uint32_t>(N + 1);
+    float* hitf = S.hitf.ensure<float>(size_t(N) * 8 + 8);
+    double* hitd = S.hitd.ensure<double>(size_t(N) * 5 + 5);
+    float* acts = S.acts.ensure<float>(size_t(A_ROWS) * N + 1);
+    float* deltas = S.deltas.ensure<float>(size_t(D_ROWS) * N + 1);
+    SVLF_CUDA(cudaMemsetAsync(hitd, 0, size_t(N) * 2 * 8, s));                 // dtau, deta
+    SVLF_CUDA(cudaMemsetAsync(hitf + size_t(N) * 5, 0, size_t(N) * 3 * 4, s));  // drgb
+    if (N) {
+        SVLF_CUDA(cudaMemsetAsync(acts, 0, size_t(A_ROWS) * N * 4, s));
+        SVLF_CUDA(cudaMemsetAsync(deltas, 0, size_t(D_ROWS) * N * 4, s));
+    }
+    if (n) k_expand<<<(n + 127) / 128, 128, 0, s>>>(n, act_first, act_cnt, dpos, dhit, dray);
+
+    HitArgs H{b.rays, b.hit_leaf, b.hit_tin, b.hit_tout, dhit, dray, dpos, surf_rel, N, o.surface, acts, deltas,
+              hitf, hitf + N, hitf + 2 * size_t(N), hitf + 5 * size_t(N), hitd, hitd + N};
+    SVLF_CUDA(cudaEventRecord(S.ev[1], s));
+    if (N) k_fwd<<<(N + 127) / 128, 128, 0, s>>>(T, M.view, M.pack, H, err_flag);
+    SVLF_CUDA(cudaEventRecord(S.ev[2], s));
+    LossArgs L{b.c_gt, b.alpha_gt, dpos, act_cnt, surf_rel, eta_gt, b.hit_tin, n, o.surface, o.lw, ray_loss,
+               hitd + 2 * size_t(N), hitd + 3 * size_t(N), hitd + 4 * size_t(N)};
+    if (n) k_loss<<<(n + 127) / 128, 128, 0, s>>>(L, H);
+    {
+        size_t tb = 0;
+        cub::DeviceReduce::Sum(nullptr, tb, ray_loss, loss_out, int(n));
+        if (n) SVLF_CUDA(cub::DeviceReduce::Sum(S.scan_tmp.ensure<char>(std::max(tb, size_t(16))), tb, ray_loss,
+                                                loss_out, int(n), s));
+        else SVLF_CUDA(cudaMemsetAsync(loss_out, 0, 8, s));
+    }
+    SVLF_CUDA(cudaEventRecord(S.ev[3], s));
+
+    // ---- backward
+    float* g_ft = M.grads;
+    float* g_fc = M.grads + M.n_ft;
+    float* g_mt = g_fc + M.n_fc;
+    float* g_mc = g_mt + SVLF_DEC_T_SIZE;
+    if (N) {
+        k_bwd<<<(N + 127) / 128, 128, 0, s>>>(T, M.view, H, o.color_frozen, g_ft, g_fc, err_flag);
+        const size_t chunk = std::max<size_t>(2048, (size_t(N) + 63) / 64);
+        const unsigned gz = unsigned((N + chunk - 1) / chunk);
+        auto gemm = [&](int drow, int O, int arow, int K, float* dW, float* db) {
+            dim3 grid((O + 31) / 32, (K + 31) / 32, gz);
+            k_gemm_dw<<<grid, 256, 0, s>>>(deltas + size_t(drow) * N, O, acts + size_t(arow) * N, K, N, chunk, dW, db);
+        };
+        gemm(D_T0, kHid, A_XT, kInT, g_mt + D::T_W0, g_mt + D::T_B0);
+        gemm(D_T1, 2, A_HT, kHid, g_mt + D::T_W1, g_mt + D::T_B1);
+        if (!o.color_frozen) {
+            gemm(D_C0, kHid, A_XC, kInC, g_mc + D::C_W0, g_mc + D::C_B0);
+            gemm(D_C1, kHid, A_H1, kHid, g_mc + D::C_W1, g_mc + D::C_B1);
+            gemm(D_C2, kHid, A_H2, kHid, g_mc + D::C_W2, g_mc + D::C_B2);
+            gemm(D_C3, 3, A_H3, kHid, g_mc + D::C_W3, g_mc + D::C_B3);
+        }
+        note_launch(o.color_frozen ? 3 : 7);
+    }
+    SVLF_CUDA(cudaEventRecord(S.ev[4], s));
+
+    // ---- Adam (adam_model_step, src/train.cpp:345-360)
+    if (o.adam) {
+        AdamSegs segs{};
+        float* p_ft = M.params;
+        float* p_fc = p_ft + M.n_ft;
+        float* p_mt = p_fc + M.n_fc;
+        float* p_mc = p_mt + SVLF_DEC_T_SIZE;
+        const size_t off_fc = M.n_ft, off_mt = M.n_ft + M.n_fc, off_mc = off_mt + SVLF_DEC_T_SIZE;
+        auto add = [&](int sid, size_t off, size_t cnt) {
+            const uint64_t step = ++M.steps[sid];
+            const double c1 = 1.0 - std::pow(double(0.9f), double(step));
+            const double c2 = 1.0 - std::pow(double(0.999f), double(step));
+            segs.seg[segs.count++] = AdamSeg{M.params + off, M.grads + off, M.adam_m + off, M.adam_v + off, cnt, c1, c2};
+        };
+        (void)p_ft; (void)p_fc; (void)p_mt; (void)p_mc;
+        // ModelAdam tensor order: feat_t, feat_c, f_T (W0,b0,W1,b1), f_C (W0,b0,...,W3,b3)
+        add(0, 0, M.n_ft);
+        const size_t t_seg[4][2] = {{D::T_W0, kHid * kInT}, {D::T_B0, kHid}, {D::T_W1, 2 * kHid}, {D::T_B1, 2}};
+        for (int i = 0; i < 4; ++i) add(2 + i, off_mt + t_seg[i][0], t_seg[i][1]);
+        if (!o.color_frozen) {
+            add(1, off_fc, M.n_fc);
+            const size_t c_seg[8][2] = {{D::C_W0, kHid * kInC}, {D::C_B0, kHid},  {D::C_W1, kHid * kHid},
+                                        {D::C_B1, kHid},        {D::C_W2, kHid * kHid}, {D::C_B2, kHid},
+                                        {D::C_W3, 3 * kHid},    {D::C_B3, 3}};
+            for (int i = 0; i < 8; ++i) add(6 + i, off_mc + c_seg[i][0], c_seg[i][1]);
+        }
+        dim3 grid(1024, segs.count);
+        k_adam<<<grid, 256, 0, s>>>(segs, o.lr);
+        note_launch();
+    }
+    SVLF_CUDA(cudaEventRecord(S.ev[5], s));
+    note_launch(6);
+
+    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 8, loss_out, 8, cudaMemcpyDeviceToHost, s));
+    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 10, err_flag, 4, cudaMemcpyDeviceToHost, s));
+    SVLF_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&res.loss, S.h_pinned + 8, 8);
+    res.error = S.h_pinned[10];
+    if (res.error) SVLF_CUDA(cudaMemsetAsync(err_flag, 0, 4, s));
+    float t[5] = {};
+    cudaEventElapsedTime(&t[0], S.ev[0], S.ev[1]);
+    cudaEventElapsedTime(&t[1], S.ev[1], S.ev[2]);
+    cudaEventElapsedTime(&t[2], S.ev[2], S.ev[3]);
+    cudaEventElapsedTime(&t[3], S.ev[3], S.ev[4]);
+    cudaEventElapsedTime(&t[4], S.ev[4], S.ev[5]);
+    res.timings = svlf_timings{t[0], 0.f, t[1], t[2], t[3], t[4], t[0] + t[1] + t[2] + t[3] + t[4], (long long)N, 0};
+    return res;
 }
 
 }  // namespace svlfb

@@ -5,16 +5,27 @@
 
 namespace svlfb {
 
-struct TrainArgs {
-    const double* rays;      // host, n x 6
-    const float* c_gt;       // host, n x 3
-    const double* depth_gt;  // host, n
-    const uint8_t* alpha_gt; // host, n
+// A supervised ray batch resident on the device plus its traversal output
+// (per-ray segments of sorted hits, see TraverseOut).
+struct TrainBatchDev {
+    const double* rays;      // n x 6
+    const float* c_gt;       // n x 3
+    const double* depth_gt;  // n (Euclidean, 0 = background)
+    const uint8_t* alpha_gt; // n (0/1)
     uint32_t n;
-    bool surface;       // LossMode::Surface (stage 1) vs Volumetric
+    const uint32_t* ray_off;
+    const uint32_t* ray_cnt;
+    const uint32_t* hit_leaf;
+    const double* hit_tin;
+    const double* hit_tout;
+    uint32_t total_hits;
+};
+
+struct TrainOptions {
+    bool surface;       // LossMode::Surface (stage 1) vs Volumetric (stages 2-3)
     bool color_frozen;  // stage 2
+    bool adam;          // false: loss + gradients only
     svlf_loss_weights lw;
-    bool adam;  // false: loss + grads only
     float lr;
 };
 
@@ -25,7 +36,8 @@ struct TrainModelRefs {
     float* adam_m;
     float* adam_v;
     size_t n_ft, n_fc;
-    uint64_t* steps;  // 14 Adam step counters (host)
+    uint64_t* steps;  // 14 Adam step counters (host), ModelAdam order
+    DecPackF32 pack;  // transposed fp32 decoders (current version)
 };
 
 struct TrainResult {
@@ -36,16 +48,17 @@ struct TrainResult {
 };
 
 struct TrainScratch {
-    DevBuf in_rays, in_cgt, in_depth, in_alpha;         // uploaded batch
-    DevBuf counts, offsets, scan_tmp, hit_leaf, hit_tin, hit_tout, hit_ray;
-    DevBuf ray_info, hit_state, hit_col, stats, pack;   // per-ray / per-hit state
-    DevBuf loss_parts;
+    DevBuf c_gt, depth, alpha;                                    // uploaded supervision
+    DevBuf act_first, act_cnt, dpos, surf_rel, eta_gt, ray_loss;  // per ray
+    DevBuf dhit, dray, hitf, hitd;                                // per active hit
+    DevBuf acts, deltas;                                          // feature-major scratch
+    DevBuf scan_tmp, counters, loss_out;
     int* h_pinned = nullptr;
     cudaEvent_t ev[8] = {};
     ~TrainScratch();
 };
 
-TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& M, const TrainArgs& a,
-                           cudaStream_t s, int* err_flag);
+TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& M, const TrainBatchDev& b,
+                           const TrainOptions& o, cudaStream_t s, int* err_flag);
 
 }  // namespace svlfb
