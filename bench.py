@@ -159,6 +159,83 @@ def cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1):
             "seconds_per_frame": round(s, 3)}
 
 
+def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True):
+    """C3: one 512^2 frame (2^18 rays), stage-3 volumetric step (lr 2e-4), octree depth 8 from
+    that frame's back-projected depth (train()'s occupancy for a one-frame dataset)."""
+    import paper_2205_07058_b200.synthetic as S
+
+    sc, cam, pts, res, dil, rays, cgt, depth, alpha = S.c3_workload()
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=0, ctx=ctx)
+    n = rays.shape[0]
+    d_rays = torch.from_numpy(np.ascontiguousarray(rays)).to(device)
+    d_cgt = torch.from_numpy(np.ascontiguousarray(cgt, dtype=np.float32)).to(device)
+    d_depth = torch.from_numpy(np.ascontiguousarray(depth)).to(device)
+    d_alpha = torch.from_numpy(np.ascontiguousarray(alpha, dtype=np.uint8)).to(device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    def step():
+        return P.train_step_device(model, d_rays.data_ptr(), d_cgt.data_ptr(), d_depth.data_ptr(),
+                                   d_alpha.data_ptr(), n, mode="volumetric", lr=2e-4)
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            step()
+        stream.synchronize()
+        ms, parts = [], []
+        for _ in range(steps):
+            flush.zero_()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            loss = step()
+            b_.record(stream)
+            stream.synchronize()
+            ms.append(a.elapsed_time(b_))
+            parts.append(ctx.last_timings())
+    step_ms = statistics.median(ms)
+    e2e = []
+    for _ in range(max(3, min(steps, 5))):
+        t0 = time.perf_counter()
+        P.train_step(model, rays, cgt, depth, alpha, mode="volumetric", lr=2e-4)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = statistics.median(e2e)
+    hits = int(statistics.median(p["hits"] for p in parts))
+    out = {"metric": "train rays/s (C3: 2^18-ray 512x512 batch, stage-3 volumetric step incl. Adam)",
+           "value": round(n / (step_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s", "ms_per_step": round(step_ms, 4),
+           "rays": n, "active_hits": hits, "vertices": int(tree.vertex_count), "leaves": int(tree.leaf_count),
+           "stages_ms": {k: round(statistics.median(p[k] for p in parts), 4)
+                         for k in ("traverse_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms")},
+           "dtype": "fp32 (reference accumulation order) / f64 geometry and loss",
+           "e2e": {"value": round(n / (e2e_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
+                   "h2d_bytes_per_step": n * (48 + 12 + 8 + 1), "d2h_bytes_per_step": 8,
+                   "api": "paper_2205_07058_b200.train_step (C ABI svlf_train_step, host batch)"}}
+    if cpu:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O
+
+            if O.reference_available():
+                R = O.Reference()
+                scene = R.scene_make(7, 4)
+                cams = np.ascontiguousarray(cam.reshape(1, 20))
+                log = np.zeros(8)
+                import ctypes as C
+
+                nlog = C.c_int()
+                epochs = np.array([0, 0, 1], dtype=np.int32)
+                if R.lib.ref_train(scene.h, cams, 1, 512, 512, epochs, 256, 1, 0, log, 4, C.byref(nlog), None):
+                    raise RuntimeError(R.lib.ref_last_error().decode())
+                secs = float(log[0])
+                out["cpu_baseline"] = {"value": round(n / secs / 1e6, 5), "unit": "Mrays/s",
+                                       "cores": R.thread_count(), "kind": "reference",
+                                       "sample": "train() epochs {0,0,1} on the same one-frame 512^2 dataset "
+                                                 "(one stage-3 step; EpochLog.seconds)",
+                                       "seconds_per_step": round(secs, 3)}
+        except Exception as e:
+            out["cpu_baseline"] = {"error": str(e)}
+    return out
+
+
 def run_reference(args):
     world, rank, local, dist = dist_init()
     if rank != 0:
@@ -215,6 +292,7 @@ def main():
                     choices=["fp16", "bf16", "fp32"])
     ap.add_argument("--objects", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the C3 train-step section")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -334,6 +412,12 @@ def main():
             line["cpu_baseline"] = cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1)
         except Exception as e:  # reported, never silently dropped
             line["cpu_baseline"] = {"error": str(e)}
+    if not args.no_train:
+        try:
+            line["train"] = bench_train(P, torch, device, stream, ctx, max(3, args.steps), 3,
+                                        cpu=not args.no_cpu_baseline and world == 1)
+        except Exception as e:
+            line["train"] = {"error": str(e)}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

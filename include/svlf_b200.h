@@ -204,6 +204,13 @@ svlf_status svlf_train_step(svlf_ctx* ctx, svlf_model* model, const double* rays
                             size_t n, svlf_loss_mode mode, int color_frozen, float lr,
                             const svlf_loss_weights* lw, svlf_loss_stats* stats,
                             double* loss_sum);
+/* Same with the batch already resident in DEVICE memory (rays, c_gt,
+ * depth_gt, alpha_gt are device pointers). */
+svlf_status svlf_train_step_device(svlf_ctx* ctx, svlf_model* model, const double* rays,
+                                   const float* c_gt, const double* depth_gt,
+                                   const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
+                                   int color_frozen, float lr, const svlf_loss_weights* lw,
+                                   svlf_loss_stats* stats, double* loss_sum);
 /* Loss and summed gradients only (no Adam), the gradient oracle entry for
  * surface_loss / volumetric_loss summed over rays (train.hpp:60-71). */
 svlf_status svlf_loss_grads(svlf_ctx* ctx, svlf_model* model, const double* rays,

@@ -203,6 +203,8 @@ def load_library():
         "svlf_render_rays": ([vp, vp, vp, sz, vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
         "svlf_train_step": ([vp, vp, vp, vp, vp, vp, sz, C.c_int, C.c_int, C.c_float, C.POINTER(_LossWeights),
                              C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
+        "svlf_train_step_device": ([vp, vp, vp, vp, vp, vp, sz, C.c_int, C.c_int, C.c_float,
+                                    C.POINTER(_LossWeights), C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
         "svlf_loss_grads": ([vp, vp, vp, vp, vp, vp, sz, C.c_int, C.c_int, C.POINTER(_LossWeights),
                              C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
     }
@@ -529,6 +531,20 @@ def train_step(model: Model, rays, c_gt, depth_gt, alpha_gt, mode: str = "volume
     _check(_LIB.svlf_train_step(model.ctx.handle, model.handle, _dp(r), _dp(c), _dp(d), _dp(a), n,
                                 0 if mode == "surface" else 1, int(color_frozen), C.c_float(lr), C.byref(lw),
                                 C.byref(st), C.byref(loss)))
+    _add_loss_stats(stats, st)
+    return loss.value
+
+
+def train_step_device(model: Model, d_rays: int, d_cgt: int, d_depth: int, d_alpha: int, n: int,
+                      mode: str = "volumetric", color_frozen: bool = False, lr: float = 1e-3,
+                      weights: LossWeights | None = None, stats: LossStats | None = None) -> float:
+    """train_step with the batch resident in device memory (pointers as ints)."""
+    lw = (weights or LossWeights())._c()
+    st = _LossStats()
+    loss = C.c_double()
+    _check(_LIB.svlf_train_step_device(model.ctx.handle, model.handle, C.c_void_p(d_rays), C.c_void_p(d_cgt),
+                                       C.c_void_p(d_depth), C.c_void_p(d_alpha), n, 0 if mode == "surface" else 1,
+                                       int(color_frozen), C.c_float(lr), C.byref(lw), C.byref(st), C.byref(loss)))
     _add_loss_stats(stats, st)
     return loss.value
 

@@ -719,7 +719,7 @@ svlf_status svlf_render_rays(svlf_ctx* ctx, svlf_model* m, const double* rays, s
 static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const float* c_gt,
                          const double* depth_gt, const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
                          int color_frozen, const svlf_loss_weights* lw, bool adam, float lr,
-                         svlf_loss_stats* stats, double* loss_sum) {
+                         svlf_loss_stats* stats, double* loss_sum, bool device_inputs = false) {
     require(ctx && m && lw, "null argument");
     require(n == 0 || (rays && c_gt && depth_gt && alpha_gt), "null argument");
     require(n < (1ull << 31), "too many rays");
@@ -735,10 +735,17 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
     double* d_depth = S.depth.ensure<double>(size_t(nn) + 1);
     uint8_t* d_alpha = S.alpha.ensure<uint8_t>(size_t(nn) + 1);
     if (nn) {
-        SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyHostToDevice, s));
-        SVLF_CUDA(cudaMemcpyAsync(d_cgt, c_gt, size_t(nn) * 12, cudaMemcpyHostToDevice, s));
-        SVLF_CUDA(cudaMemcpyAsync(d_depth, depth_gt, size_t(nn) * 8, cudaMemcpyHostToDevice, s));
-        SVLF_CUDA(cudaMemcpyAsync(d_alpha, alpha_gt, size_t(nn), cudaMemcpyHostToDevice, s));
+        const cudaMemcpyKind kind = device_inputs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, kind, s));
+        if (device_inputs) {  // supervision read in place
+            d_cgt = const_cast<float*>(c_gt);
+            d_depth = const_cast<double*>(depth_gt);
+            d_alpha = const_cast<uint8_t*>(alpha_gt);
+        } else {
+            SVLF_CUDA(cudaMemcpyAsync(d_cgt, c_gt, size_t(nn) * 12, kind, s));
+            SVLF_CUDA(cudaMemcpyAsync(d_depth, depth_gt, size_t(nn) * 8, kind, s));
+            SVLF_CUDA(cudaMemcpyAsync(d_alpha, alpha_gt, size_t(nn), kind, s));
+        }
     }
     const uint32_t total = nn ? run_traversal(ctx, m->tree, nullptr, 0, 0, nn) : 0;
     const float trav_ms = ctx->last.traverse_ms;
@@ -768,6 +775,16 @@ svlf_status svlf_train_step(svlf_ctx* ctx, svlf_model* m, const double* rays, co
     return guard([&] {
         train_common(ctx, m, rays, c_gt, depth_gt, alpha_gt, n, mode, color_frozen, lw, true, lr, stats,
                      loss_sum);
+    });
+}
+
+svlf_status svlf_train_step_device(svlf_ctx* ctx, svlf_model* m, const double* rays, const float* c_gt,
+                                   const double* depth_gt, const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
+                                   int color_frozen, float lr, const svlf_loss_weights* lw, svlf_loss_stats* stats,
+                                   double* loss_sum) {
+    return guard([&] {
+        train_common(ctx, m, rays, c_gt, depth_gt, alpha_gt, n, mode, color_frozen, lw, true, lr, stats, loss_sum,
+                     true);
     });
 }
 

@@ -342,3 +342,15 @@ def rtmv_workload(n_objects=4, n_views=100, view_res=400, res=256, dilation=1, w
     eye = tuple(0.5 + 1.8 * c for c in C1_EYE_DIR)
     cam = lookat_camera(eye, (0.5, 0.5, 0.5), width, width, 1.5 * width)
     return sc, pts, res, dilation, cam, width, width
+
+
+def c3_workload(width=512, objects=4, res=256, dilation=1, seed=7):
+    """Config 3: one hemisphere frame (width^2 rays, 2^18 at 512) of make_random_scene(seed, objects)
+    with ground truth from the analytic ray-caster; the octree is train()'s occupancy for that
+    one-frame dataset (back-projected foreground depth, res 256 = depth 8, dilation 1)."""
+    sc = make_random_scene(seed, objects)
+    cam = hemisphere_cameras(1, 1.8, seed, width, width, 1.5 * width)[0]
+    rgb, depth, mask = render_gt(sc, cam, width, width)
+    pts = backproject(cam, width, width, depth)
+    rays = camera_rays(cam, width, width)
+    return sc, cam, pts, res, dilation, rays, rgb.reshape(-1, 3), depth.astype(np.float64), (mask > 0.5)
