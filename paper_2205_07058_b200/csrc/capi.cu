@@ -196,77 +196,87 @@ void reset_misc(svlf_ctx* ctx) {
 unsigned long long* misc_fg(svlf_ctx* ctx) { return reinterpret_cast<unsigned long long*>(ctx->misc.as<char>() + 8); }
 
 // Traversal for `n` rays: rays are either generated from `cam` (rows
-// row0 .. row0+rows) or already resident in ctx->rays. Leaves per-ray
-// segments (ctx->offsets = start, ctx->counts = count) and sorted hits in
-// ctx->hit_*. Returns the total number of hits.
-uint32_t run_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0,
-                       uint32_t rows, uint32_t n) {
+// row0 .. row0+rows) or already resident in ctx->rays. Enqueues the three
+// traversal kernels (cooperative pass, dense pass over overflowed tiles,
+// per-ray fallback) with no host round trip; leaves per-ray segments
+// (ctx->offsets = start, ctx->counts = count) and sorted hits in ctx->hit_*,
+// counters at traversal_counters(ctx): [0] hits, [1] overflow, [2] capacity
+// exceeded, [3] dense overflow.
+uint32_t* traversal_counters(svlf_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->misc.as<char>() + 16); }
+
+void enqueue_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0, uint32_t rows,
+                       uint32_t n) {
     cudaStream_t s = ctx->stream;
-    double* rays = ctx->rays.ensure<double>(size_t(n) * 6);
+    double* rays = ctx->rays.ensure<double>(size_t(n) * 6 + 6);
     uint32_t* ray_off = ctx->offsets.ensure<uint32_t>(size_t(n) + 1);
     uint32_t* ray_cnt = ctx->counts.ensure<uint32_t>(size_t(n) + 1);
-    uint32_t* ovl = ctx->overflow.ensure<uint32_t>(size_t(n) + 1);
-    uint32_t* ovl2 = ctx->overflow2.ensure<uint32_t>(size_t(n) + 1);
-    uint32_t* counters = reinterpret_cast<uint32_t*>(ctx->misc.as<char>() + 16);
+    uint32_t* ovl = ctx->overflow.ensure<uint32_t>(size_t(n) + 64);
+    uint32_t* ovl2 = ctx->overflow2.ensure<uint32_t>(size_t(n) + 64);
+    uint32_t* counters = traversal_counters(ctx);
     size_t cap = std::max<size_t>(ctx->hit_cap, std::max<size_t>(size_t(n) * 4, size_t(1) << 20));
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        cap = std::min<size_t>(cap, 0xffffffffu);
-        ctx->hit_leaf.ensure<uint32_t>(cap);
-        ctx->hit_tin.ensure<double>(cap);
-        ctx->hit_tout.ensure<double>(cap);
-        ctx->hit_ray.ensure<uint32_t>(cap);
-        ctx->hit_cap = cap;
-        TraverseOut o{ray_off, ray_cnt, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
-                      ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), counters, ovl, ovl2, rays,
-                      uint32_t(cap)};
-        SVLF_CUDA(cudaMemsetAsync(counters, 0, 16, s));
-        SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
-        launch_traverse(dev_view(tree), cam, row0, rows, n, o, s);
-        SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));
-        SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaStreamSynchronize(s));
-        const uint32_t n_ovl = uint32_t(ctx->h_pinned[5]);
-        if (n_ovl) {
-            launch_traverse_dense(dev_view(tree), cam, row0, n_ovl, o, s);
-            SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
-            SVLF_CUDA(cudaStreamSynchronize(s));
-            const uint32_t n_ovl2 = uint32_t(ctx->h_pinned[7]);
-            if (n_ovl2) {
-                launch_traverse_fallback(dev_view(tree), cam, row0, n_ovl2, o, s);
-                SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
-                SVLF_CUDA(cudaStreamSynchronize(s));
-            }
-        }
-        SVLF_CUDA(cudaEventRecord(ctx->ev[EV_EMIT], s));
-        const uint32_t total = uint32_t(ctx->h_pinned[4]);
-        ctx->last_overflow_rays = (long long)n_ovl * 1000000 + ctx->h_pinned[7];
-        if (ctx->h_pinned[6] == 0) return total;
-        cap = size_t(total) + total / 4 + 1024;  // grow and re-run
+    cap = std::min<size_t>(cap, 0xfffff000u);
+    ctx->hit_leaf.ensure<uint32_t>(cap);
+    ctx->hit_tin.ensure<double>(cap);
+    ctx->hit_tout.ensure<double>(cap);
+    ctx->hit_ray.ensure<uint32_t>(cap);
+    ctx->hit_cap = cap;
+    TraverseOut o{ray_off, ray_cnt, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
+                  ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), counters, ovl, ovl2, rays, uint32_t(cap)};
+    SVLF_CUDA(cudaMemsetAsync(counters, 0, 16, s));
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
+    launch_traverse(dev_view(tree), cam, row0, rows, n, o, s);
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));
+    launch_traverse_dense(dev_view(tree), cam, row0, o, s);
+    launch_traverse_fallback(dev_view(tree), cam, row0, o, s);
+    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_EMIT], s));
+}
+
+// Reads the traversal counters (synchronizes). Returns false when the hit
+// buffers were too small (ctx->hit_cap has been grown; re-run the traversal).
+bool read_traversal(svlf_ctx* ctx, uint32_t* total) {
+    SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, traversal_counters(ctx), 16, cudaMemcpyDeviceToHost, ctx->stream));
+    SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    *total = uint32_t(ctx->h_pinned[4]);
+    ctx->last_overflow_rays = (long long)ctx->h_pinned[5] * 1000000 + ctx->h_pinned[7];
+    if (ctx->h_pinned[6] == 0) return true;
+    ctx->hit_cap = size_t(*total) + *total / 4 + 1024;
+    return false;
+}
+
+// Traversal with a synchronous hit count (fp32 render, API traversal, train).
+uint32_t run_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0,
+                       uint32_t rows, uint32_t n) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        enqueue_traversal(ctx, tree, cam, row0, rows, n);
+        uint32_t total = 0;
+        if (read_traversal(ctx, &total)) return total;
     }
     fail(SVLF_ERR_RUNTIME, "traversal output capacity could not be satisfied");
 }
 
-// decode + composite into device output buffers
-void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t total, const float* bg,
+// decode + composite into device output buffers. total_host = hit count if
+// known on the host (fp32 path needs it); the tensor-core path reads the
+// device-side counter.
+void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t total_host, const float* bg,
                           svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth) {
     cudaStream_t s = ctx->stream;
-    HitOut ho{ctx->h_tau.ensure<float>(total), ctx->h_eta.ensure<float>(total),
-              ctx->h_rgb.ensure<float>(size_t(total) * 3)};
+    const uint32_t cap = uint32_t(ctx->hit_cap);
+    HitOut ho{ctx->h_tau.ensure<float>(cap), ctx->h_eta.ensure<float>(cap), ctx->h_rgb.ensure<float>(size_t(cap) * 3)};
     const DevOctree& T = dev_view(m->tree);
     int* err = ctx->misc.as<int>();
     if (prec == SVLF_PRECISION_BF16 || prec == SVLF_PRECISION_FP16) {
         const bool bf16 = prec == SVLF_PRECISION_BF16;
         ensure_pack_tc(m->view(), m->pack_bf16, m->pack_bf16_version, m->version, bf16, s);
-        void* scratch = ctx->tc_scratch.ensure<uint8_t>(decode_tc_scratch_bytes(total));
+        void* scratch = ctx->tc_scratch.ensure<uint8_t>(decode_tc_scratch_bytes(cap));
         launch_decode_tc(T, m->view(), m->pack_bf16.as<char>(), bf16, ctx->rays.as<double>(),
                          ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
-                         ctx->hit_tout.as<double>(), total, ho, err, scratch, s);
+                         ctx->hit_tout.as<double>(), traversal_counters(ctx), cap, ho, err, scratch, s);
     } else {
         if (prec != SVLF_PRECISION_FP32) fail(SVLF_ERR_INVALID_ARGUMENT, "unknown precision");
         ensure_pack_f32(m, s);
         launch_decode_f32(T, m->view(), pack_f32_view(m->pack_f32.as<float>()), ctx->rays.as<double>(),
                           ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(),
-                          ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total, ho, err, s);
+                          ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total_host, ho, err, s);
     }
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_DECODE], s));
     launch_composite(ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(), ctx->hit_tin.as<double>(),
@@ -274,10 +284,19 @@ void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t tot
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COMPOSITE], s));
 }
 
-void finish_render(svlf_ctx* ctx, uint32_t n, uint32_t total, svlf_render_stats* stats) {
+// One synchronization per frame: counters, fg count and error flag.
+// Returns false if the traversal overflowed the hit buffers (re-render).
+bool finish_render(svlf_ctx* ctx, uint32_t n, svlf_render_stats* stats) {
     cudaStream_t s = ctx->stream;
     SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 8, misc_fg(ctx), 8, cudaMemcpyDeviceToHost, s));
+    SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, traversal_counters(ctx), 16, cudaMemcpyDeviceToHost, s));
     check_device_error(ctx);  // synchronizes
+    const uint32_t total = uint32_t(ctx->h_pinned[4]);
+    ctx->last_overflow_rays = (long long)ctx->h_pinned[5] * 1000000 + ctx->h_pinned[7];
+    if (ctx->h_pinned[6] != 0) {
+        ctx->hit_cap = size_t(total) + total / 4 + 1024;
+        return false;
+    }
     unsigned long long fg = 0;
     std::memcpy(&fg, ctx->h_pinned + 8, 8);
     float ms[4] = {};
@@ -294,6 +313,25 @@ void finish_render(svlf_ctx* ctx, uint32_t n, uint32_t total, svlf_render_stats*
         stats->thickness_queries += total;
         stats->color_queries += total;
     }
+    return true;
+}
+
+// Full frame (or row band) into device buffers: traversal, decode, composite.
+void render_pipeline(svlf_ctx* ctx, svlf_model* m, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
+                     const float* bg, svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth,
+                     svlf_render_stats* stats) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        reset_misc(ctx);
+        uint32_t total = 0;
+        if (prec == SVLF_PRECISION_FP32) {
+            total = run_traversal(ctx, m->tree, cam, row0, rows, n);
+        } else {
+            enqueue_traversal(ctx, m->tree, cam, row0, rows, n);
+        }
+        run_decode_composite(ctx, m, n, total, bg, prec, d_rgb, d_alpha, d_depth);
+        if (finish_render(ctx, n, stats)) return;
+    }
+    fail(SVLF_ERR_RUNTIME, "traversal output capacity could not be satisfied");
 }
 
 void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_t row0, uint32_t rows,
@@ -306,10 +344,7 @@ void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_
     require(n64 < (1ull << 31), "too many pixels in one call");
     const uint32_t n = uint32_t(n64);
     const DevCamera dc = to_dev_camera(*cam);
-    reset_misc(ctx);
-    const uint32_t total = run_traversal(ctx, m->tree, &dc, row0, rows, n);
-    run_decode_composite(ctx, m, n, total, bg, prec, d_rgb, d_alpha, d_depth);
-    finish_render(ctx, n, total, stats);
+    render_pipeline(ctx, m, &dc, row0, rows, n, bg, prec, d_rgb, d_alpha, d_depth, stats);
 }
 
 size_t model_param_count(uint32_t V) { return size_t(V) * 96 + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE; }
@@ -700,14 +735,12 @@ svlf_status svlf_render_rays(svlf_ctx* ctx, svlf_model* m, const double* rays, s
         cudaStream_t s = ctx->stream;
         const uint32_t nn = uint32_t(n);
         reset_misc(ctx);
-        double* d_rays = ctx->rays.ensure<double>(size_t(nn) * 6);
+        double* d_rays = ctx->rays.ensure<double>(size_t(nn) * 6 + 6);
         SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyHostToDevice, s));
         float* d_rgb = ctx->out_rgb.ensure<float>(n * 3);
         float* d_alpha = ctx->out_alpha.ensure<float>(n);
         float* d_depth = ctx->out_depth.ensure<float>(n);
-        const uint32_t total = run_traversal(ctx, m->tree, nullptr, 0, 0, nn);
-        run_decode_composite(ctx, m, nn, total, bg, prec, d_rgb, d_alpha, d_depth);
-        finish_render(ctx, nn, total, stats);
+        render_pipeline(ctx, m, nullptr, 0, 0, nn, bg, prec, d_rgb, d_alpha, d_depth, stats);
         SVLF_CUDA(cudaMemcpyAsync(rgb, d_rgb, n * 12, cudaMemcpyDeviceToHost, s));
         SVLF_CUDA(cudaMemcpyAsync(alpha, d_alpha, n * 4, cudaMemcpyDeviceToHost, s));
         SVLF_CUDA(cudaMemcpyAsync(depth, d_depth, n * 4, cudaMemcpyDeviceToHost, s));
@@ -748,7 +781,8 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
         }
     }
     const uint32_t total = nn ? run_traversal(ctx, m->tree, nullptr, 0, 0, nn) : 0;
-    const float trav_ms = ctx->last.traverse_ms;
+    float trav_ms = 0.f;
+    if (nn) cudaEventElapsedTime(&trav_ms, ctx->ev[EV_START], ctx->ev[EV_EMIT]);
     TrainBatchDev b{d_rays, d_cgt, d_depth, d_alpha, nn, ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(),
                     ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total};
     TrainOptions opt{mode == SVLF_LOSS_SURFACE, color_frozen != 0, adam, *lw, lr};

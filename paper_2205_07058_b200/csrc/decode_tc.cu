@@ -185,15 +185,13 @@ __global__ void k_feat_cvt(const float* __restrict__ src, typename Fmt<kBF16>::H
 // geo[j]: 3 x uint4 = r6 (6 x 16-bit) | w1 (8 x 16-bit) | w2 (8 x 16-bit) | 2 x pad
 // u12[j]: 2 x float4 = u1.xyz, u2.xyz, pad, pad
 template <bool kBF16>
-__global__ void __launch_bounds__(128) k_hit_geom(DevOctree T, const double* __restrict__ rays,
-                                                  const uint32_t* __restrict__ hit_ray,
-                                                  const uint32_t* __restrict__ hit_leaf,
-                                                  const double* __restrict__ hit_tin,
-                                                  const double* __restrict__ hit_tout, uint32_t n, uint4* geo,
-                                                  float4* u12, int* err) {
+__device__ __forceinline__ void hit_geom_one(DevOctree T, const double* __restrict__ rays,
+                                             const uint32_t* __restrict__ hit_ray,
+                                             const uint32_t* __restrict__ hit_leaf,
+                                             const double* __restrict__ hit_tin,
+                                             const double* __restrict__ hit_tout, uint32_t j, uint4* geo,
+                                             float4* u12, int* err) {
     using F = Fmt<kBF16>;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
     Ray ray;
     const uint32_t ri = hit_ray[j];
 #pragma unroll
@@ -230,6 +228,18 @@ __global__ void __launch_bounds__(128) k_hit_geom(DevOctree T, const double* __r
 
 // D[tmem] (+)= A . B^T over K: A in the skewed activation layout (a_off),
 // B (weights, N rows) in the dense layout core_offset(n, k, K).
+template <bool kBF16>
+__global__ void __launch_bounds__(128) k_hit_geom(DevOctree T, const double* __restrict__ rays,
+                                                  const uint32_t* __restrict__ hit_ray,
+                                                  const uint32_t* __restrict__ hit_leaf,
+                                                  const double* __restrict__ hit_tin,
+                                                  const double* __restrict__ hit_tout, const uint32_t* n_dev,
+                                                  uint32_t cap, uint4* geo, float4* u12, int* err) {
+    using F = Fmt<kBF16>;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;  // grid covers the capacity; early exit
+    if (j < min(*n_dev, cap)) hit_geom_one<kBF16>(T, rays, hit_ray, hit_leaf, hit_tin, hit_tout, j, geo, u12, err);
+}
+
 __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, uint32_t b_base, uint32_t K,
                                             uint32_t idesc) {
     const uint32_t b_sbo = (K / 8) * 128;
@@ -345,7 +355,8 @@ __device__ __forceinline__ void load_corners(const DevOctree& T, uint32_t leaf, 
 template <bool kBF16>
 __global__ void __launch_bounds__(512, 1)
     k_decode_t(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ ft16,
-               const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ geo, uint32_t n, HitOut out) {
+               const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ geo, const uint32_t* n_dev,
+               uint32_t cap, HitOut out) {
     using F = Fmt<kBF16>;
     using H2 = typename F::H2;
     constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
@@ -358,6 +369,7 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t sbase = smem_u32(sm);
     const uint32_t a_base = sbase + T_SM_A0 + slot * T_A_BYTES;
     Slot S{reinterpret_cast<uint64_t*>(sm + T_SM_BAR) + slot, 0u, 1u + slot, r};
+    const uint32_t n = min(*n_dev, cap);
     const uint32_t ntiles = (n + 127) / 128;
 
     for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += gridDim.x * kSlots) {
@@ -432,7 +444,7 @@ template <bool kBF16>
 __global__ void __launch_bounds__(512, 1)
     k_decode_c(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ fc16,
                const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ geo,
-               const float4* __restrict__ u12, uint32_t n, HitOut out) {
+               const float4* __restrict__ u12, const uint32_t* n_dev, uint32_t cap, HitOut out) {
     using F = Fmt<kBF16>;
     using H2 = typename F::H2;
     constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
@@ -447,6 +459,7 @@ __global__ void __launch_bounds__(512, 1)
     const float* cvec = reinterpret_cast<const float*>(sm + (OFF_CVEC - OFF_WC0));
     const uint32_t a_base = sbase + C_SM_A0 + slot * C_A_BYTES;
     Slot S{reinterpret_cast<uint64_t*>(sm + C_SM_BAR) + slot, 0u, 1u + slot, r};
+    const uint32_t n = min(*n_dev, cap);
     const uint32_t ntiles = (n + 127) / 128;
 
     for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += gridDim.x * kSlots) {
@@ -553,8 +566,8 @@ void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uin
 template <bool kBF16>
 static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t* p, const double* rays,
                            const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
-                           const double* hit_tout, uint32_t n_hits, HitOut out, int* err, uint4* geo, float4* u12,
-                           cudaStream_t s) {
+                           const double* hit_tout, const uint32_t* n_dev, uint32_t cap, HitOut out, int* err,
+                           uint4* geo, float4* u12, cudaStream_t s) {
     using H = typename Fmt<kBF16>::H;
     static bool attr = false;
     if (!attr) {
@@ -564,32 +577,30 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
     }
     const H* ft = reinterpret_cast<const H*>(p + OFF_FEAT);
     const H* fc = ft + size_t(M.V) * 64;
-    k_hit_geom<kBF16><<<(n_hits + 127) / 128, 128, 0, s>>>(T, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits,
-                                                           geo, u12, err);
-    const uint32_t tiles = (n_hits + 127) / 128;
-    const uint32_t grid = std::min<uint32_t>(uint32_t(g_num_sms), (tiles + kSlots - 1) / kSlots);
-    k_decode_t<kBF16><<<grid, 512, T_SM_TOTAL, s>>>(T, p, ft, hit_leaf, geo, n_hits, out);
-    k_decode_c<kBF16><<<grid, 512, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, geo, u12, n_hits, out);
+    k_hit_geom<kBF16><<<(cap + 127) / 128, 128, 0, s>>>(T, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap,
+                                                       geo, u12, err);
+    k_decode_t<kBF16><<<g_num_sms, 512, T_SM_TOTAL, s>>>(T, p, ft, hit_leaf, geo, n_dev, cap, out);
+    k_decode_c<kBF16><<<g_num_sms, 512, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, geo, u12, n_dev, cap, out);
     note_launch(3);
 }
 
 void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, bool bf16, const double* rays,
                       const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
-                      const double* hit_tout, uint32_t n_hits, HitOut out, int* err, void* scratch,
-                      cudaStream_t s) {
-    if (n_hits == 0) return;
+                      const double* hit_tout, const uint32_t* n_dev, uint32_t cap, HitOut out, int* err,
+                      void* scratch, cudaStream_t s) {
+    if (cap == 0) return;
     if (g_num_sms == 0) {
         int dev = 0;
         SVLF_CUDA(cudaGetDevice(&dev));
         SVLF_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     uint4* geo = static_cast<uint4*>(scratch);
-    float4* u12 = reinterpret_cast<float4*>(geo + 3 * size_t(n_hits));
+    float4* u12 = reinterpret_cast<float4*>(geo + 3 * size_t(cap));
     const uint8_t* p = reinterpret_cast<const uint8_t*>(pack);
     if (bf16)
-        decode_tc_impl<true>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits, out, err, geo, u12, s);
+        decode_tc_impl<true>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap, out, err, geo, u12, s);
     else
-        decode_tc_impl<false>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_hits, out, err, geo, u12, s);
+        decode_tc_impl<false>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap, out, err, geo, u12, s);
 }
 
 size_t decode_tc_scratch_bytes(uint32_t n_hits) { return size_t(n_hits) * (48 + 32); }

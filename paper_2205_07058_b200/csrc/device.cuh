@@ -122,11 +122,11 @@ struct TraverseOut {
 void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
                      const TraverseOut& o, cudaStream_t s);
 // second cooperative pass (8 rays per block) over the rays of overflowed tiles
-void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
-                           const TraverseOut& o, cudaStream_t s);
+void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
+                           cudaStream_t s);
 // per-ray depth-first walker for whatever still overflowed
-void launch_traverse_fallback(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
-                              const TraverseOut& o, cudaStream_t s);
+void launch_traverse_fallback(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
+                              cudaStream_t s);
 void launch_to_csr(const uint32_t* ray_off, const uint32_t* ray_cnt, const uint32_t* csr, uint32_t n,
                    const uint32_t* leaf, const double* tin, const double* tout, uint32_t* leaf_o, double* tin_o,
                    double* tout_o, uint32_t* ray_o, cudaStream_t s);
@@ -147,10 +147,11 @@ void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const do
 // ---- tcgen05 decoder (decode_tc.cu)
 void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, bool bf16,
                     cudaStream_t s);
+// n_dev: device-side hit count (traversal counter), clamped to cap (buffer capacity)
 void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, bool bf16, const double* rays,
                       const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
-                      const double* hit_tout, uint32_t n_hits, HitOut out, int* err, void* scratch,
-                      cudaStream_t s);
+                      const double* hit_tout, const uint32_t* n_dev, uint32_t cap, HitOut out, int* err,
+                      void* scratch, cudaStream_t s);
 size_t decode_tc_scratch_bytes(uint32_t n_hits);
 
 // ---- misc device utilities (traverse.cu)

@@ -193,19 +193,16 @@ constexpr int kRays = 64;      // rays per block, first pass (8 x 8 pixel tile)
 constexpr int kRaysDense = 8;  // rays per block, second pass over overflowed tiles
 constexpr int kThreads = 256;  // threads per block
 constexpr int kQCap = 1536;    // (ray, node) pairs per level
-constexpr int kHCap = 2048;    // leaf hits per tile
 
 struct BfsSmem {
     double o[3][kRays], d[3][kRays], inv[3][kRays];
     uint64_t qxyz[2][kQCap];
     uint32_t qnode[2][kQCap];
-    double htin[kHCap];
-    uint32_t hleaf[kHCap];
+    uint32_t pos[kQCap];  // leaf level: output position of each pair's first hit
     uint8_t qray[2][kQCap];
-    uint8_t hray[kHCap];
     uint32_t rcount[kRays], roff[kRays];
     uint32_t gray[kRays];
-    uint32_t n_q, n_h, base, overflow;
+    uint32_t n_q, base, overflow;
     typename cub::BlockScan<uint32_t, kThreads>::TempStorage scan;
 };
 
@@ -227,10 +224,8 @@ struct BfsArgs {
 // pass, overflow -> overflow_rays); kList = true: consecutive entries of
 // overflow_rays (second pass, overflow -> overflow_dense).
 template <bool kCamera, int kR, bool kList>
-__global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0,
-                                                           uint32_t rows, uint32_t n, BfsArgs A) {
-    extern __shared__ __align__(16) uint8_t bfs_smem[];
-    BfsSmem& S = *reinterpret_cast<BfsSmem*>(bfs_smem);
+__device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& cam, uint32_t row0, uint32_t rows,
+                                         uint32_t n, const BfsArgs& A, BfsSmem& S, uint32_t tile) {
     using Scan = cub::BlockScan<uint32_t, kThreads>;
     const uint32_t tid = threadIdx.x;
 
@@ -240,17 +235,17 @@ __global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamer
         uint32_t gi;
         bool ok;
         if constexpr (kList) {
-            const uint32_t k = blockIdx.x * kR + tid;
+            const uint32_t k = tile * kR + tid;
             gi = k < A.counters[1] ? A.overflow_rays[k] : 0xffffffffu;
             ok = gi != 0xffffffffu;
         } else if constexpr (kCamera) {
             const uint32_t tiles_x = (cam.width + 7) / 8;
-            const uint32_t tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+            const uint32_t tx = tile % tiles_x, ty = tile / tiles_x;
             const uint32_t px = tx * 8 + (tid & 7), py = ty * 8 + (tid >> 3);
             ok = px < cam.width && py < rows;
             gi = py * cam.width + px;
         } else {
-            gi = blockIdx.x * kR + tid;
+            gi = tile * kR + tid;
             ok = gi < n;
         }
         S.gray[tid] = ok ? gi : 0xffffffffu;
@@ -273,7 +268,6 @@ __global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamer
     }
     if (tid == 0) {
         S.n_q = 0;
-        S.n_h = 0;
         S.overflow = 0;
     }
     __syncthreads();
@@ -304,19 +298,16 @@ __global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamer
         __syncthreads();
     }
 
-    // ---- level by level
+    // ---- internal levels: expand (ray, node) pairs into the next level's queue
     int cur = 0;
     uint32_t n_cur = S.n_q;
-    for (int level = 0; level < T.L && n_cur > 0; ++level) {
-        const bool to_leaves = level + 1 == T.L;
+    int level = 0;
+    for (; level + 1 < T.L && n_cur > 0; ++level) {
         uint32_t n_out = 0;
         for (uint32_t base = 0; base < n_cur; base += kThreads) {
             const uint32_t e = base + tid;
-            // pass 1: which children of pair e are hit (bit = octant), front-to-back order kept below
-            uint32_t hitmask = 0, cnt = 0;
-            NodeSplit sp;
+            uint32_t hitmask = 0, cnt = 0, ri = 0, x = 0, y = 0, z = 0, s = 0;
             uint2 node = make_uint2(0, 0);
-            uint32_t ri = 0, x = 0, y = 0, z = 0, s = 0;
             if (e < n_cur) {
                 ri = S.qray[cur][e];
                 node = T.nodes[S.qnode[cur][e]];
@@ -331,57 +322,40 @@ __global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamer
                     d[a] = S.d[a][ri];
                     inv[a] = S.inv[a][ri];
                 }
+                NodeSplit sp;
                 split_node(T, o, d, inv, level, x, y, z, sp);
                 s = sign_mask(d);
 #pragma unroll
                 for (uint32_t oct = 0; oct < 8; ++oct) {
                     if (!((node.y >> oct) & 1u)) continue;
                     double t0, t1;
-                    if (!child_hit(sp, oct, t0, t1)) continue;
-                    if (to_leaves && !(dsub(t1, t0) > kMinHitSpan)) continue;
-                    hitmask |= 1u << oct;
+                    if (child_hit(sp, oct, t0, t1)) hitmask |= 1u << oct;
                 }
                 cnt = __popc(hitmask);
             }
             uint32_t off, tot;
             Scan(S.scan).ExclusiveSum(cnt, off, tot);
-            const uint32_t cap = to_leaves ? kHCap : kQCap;
-            if (n_out + tot > cap) {
+            if (n_out + tot > kQCap) {
                 if (tid == 0) S.overflow = 1;
                 __syncthreads();
                 break;
             }
-            // pass 2: write the hit children in front-to-back octant order
-            uint32_t w = n_out + off;
+            uint32_t w = n_out + off;  // children in front-to-back octant order
             for (uint32_t it = 0; it < 8 && hitmask; ++it) {
                 const uint32_t oct = it ^ s;
                 if (!((hitmask >> oct) & 1u)) continue;
-                const uint32_t child = node.x + __popc(node.y & ((1u << oct) - 1u));
-                if (to_leaves) {
-                    double t0, t1;
-                    child_hit(sp, oct, t0, t1);
-                    S.hleaf[w] = child - T.level_off[T.L];
-                    S.htin[w] = t0;
-                    S.hray[w] = uint8_t(ri);
-                } else {
-                    S.qnode[cur ^ 1][w] = child;
-                    S.qxyz[cur ^ 1][w] = pack_xyz(2u * x + (oct & 1u), 2u * y + ((oct >> 1) & 1u),
-                                                  2u * z + ((oct >> 2) & 1u));
-                    S.qray[cur ^ 1][w] = uint8_t(ri);
-                }
+                S.qnode[cur ^ 1][w] = node.x + __popc(node.y & ((1u << oct) - 1u));
+                S.qxyz[cur ^ 1][w] =
+                    pack_xyz(2u * x + (oct & 1u), 2u * y + ((oct >> 1) & 1u), 2u * z + ((oct >> 2) & 1u));
+                S.qray[cur ^ 1][w] = uint8_t(ri);
                 ++w;
             }
             n_out += tot;
             __syncthreads();
         }
         if (S.overflow) break;
-        if (to_leaves) {
-            if (tid == 0) S.n_h = n_out;
-            n_cur = 0;
-        } else {
-            n_cur = n_out;
-            cur ^= 1;
-        }
+        n_cur = n_out;
+        cur ^= 1;
         __syncthreads();
     }
 
@@ -392,10 +366,45 @@ __global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamer
         return;
     }
 
-    // ---- per-ray segments: counts, offsets, sort, allocate, write
-    const uint32_t nh = S.n_h;
-    for (uint32_t i = tid; i < nh; i += kThreads) atomicAdd(&S.rcount[S.hray[i]], 1u);
-    __syncthreads();
+    // ---- leaf level, two passes: (A) count kept leaves per pair, scan, allocate;
+    // (B) recompute and write each pair's leaves straight to their final slots.
+    // Pairs are grouped by ray in order, so the pair scan is also the per-ray
+    // segment layout; each ray's segment is then sorted in place.
+    const bool leaf_pass = level + 1 == T.L && n_cur > 0;
+    uint32_t total = 0;
+    if (leaf_pass) {
+        for (uint32_t base = 0; base < n_cur; base += kThreads) {
+            const uint32_t e = base + tid;
+            uint32_t cnt = 0, ri = 0;
+            if (e < n_cur) {
+                ri = S.qray[cur][e];
+                const uint2 node = T.nodes[S.qnode[cur][e]];
+                const uint64_t xyz = S.qxyz[cur][e];
+                double o[3], d[3], inv[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    o[a] = S.o[a][ri];
+                    d[a] = S.d[a][ri];
+                    inv[a] = S.inv[a][ri];
+                }
+                NodeSplit sp;
+                split_node(T, o, d, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
+                           uint32_t(xyz >> 42), sp);
+#pragma unroll
+                for (uint32_t oct = 0; oct < 8; ++oct) {
+                    if (!((node.y >> oct) & 1u)) continue;
+                    double t0, t1;
+                    if (child_hit(sp, oct, t0, t1) && dsub(t1, t0) > kMinHitSpan) ++cnt;
+                }
+                if (cnt) atomicAdd(&S.rcount[ri], cnt);
+            }
+            uint32_t off, tot;
+            Scan(S.scan).ExclusiveSum(cnt, off, tot);
+            if (e < n_cur) S.pos[e] = total + off;
+            total += tot;
+            __syncthreads();
+        }
+    }
     {
         const uint32_t c = tid < kR ? S.rcount[tid] : 0u;
         uint32_t off, tot;
@@ -407,15 +416,64 @@ __global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamer
             if (b + tot > A.capacity) atomicExch(&A.counters[2], 1u);
         }
         __syncthreads();
-        if (tid < kR) sort_segment(S.htin, S.hleaf, off, off + c);
+    }
+    const uint32_t gbase = S.base;
+    const bool fits = gbase + total <= A.capacity;
+    if (leaf_pass && fits) {
+        for (uint32_t e = tid; e < n_cur; e += kThreads) {
+            const uint32_t ri = S.qray[cur][e];
+            const uint2 node = T.nodes[S.qnode[cur][e]];
+            const uint64_t xyz = S.qxyz[cur][e];
+            double o[3], d[3], inv[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                o[a] = S.o[a][ri];
+                d[a] = S.d[a][ri];
+                inv[a] = S.inv[a][ri];
+            }
+            NodeSplit sp;
+            split_node(T, o, d, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
+                       uint32_t(xyz >> 42), sp);
+            const uint32_t s = sign_mask(d);
+            uint32_t w = gbase + S.pos[e];
+            const uint32_t gr = S.gray[ri];
+            for (uint32_t it = 0; it < 8; ++it) {
+                const uint32_t oct = it ^ s;
+                if (!((node.y >> oct) & 1u)) continue;
+                double t0, t1;
+                if (!child_hit(sp, oct, t0, t1) || !(dsub(t1, t0) > kMinHitSpan)) continue;
+                A.hit_leaf[w] = node.x + __popc(node.y & ((1u << oct) - 1u)) - T.level_off[T.L];
+                A.hit_tin[w] = t0;
+                A.hit_tout[w] = t1;
+                A.hit_ray[w] = gr;
+                ++w;
+            }
+        }
     }
     __syncthreads();
-    const uint32_t base = S.base;
-    if (base + nh > A.capacity) return;  // host re-runs with a larger buffer
-    if (tid < kR && S.gray[tid] != 0xffffffffu) {
-        A.ray_off[S.gray[tid]] = base + S.roff[tid];
-        A.ray_cnt[S.gray[tid]] = S.rcount[tid];
-        if (kCamera && S.rcount[tid] > 0) {  // later stages read foreground rays only
+    if (tid < kR && S.gray[tid] != 0xffffffffu && fits) {
+        const uint32_t c = S.rcount[tid], b = gbase + S.roff[tid];
+        A.ray_off[S.gray[tid]] = b;
+        A.ray_cnt[S.gray[tid]] = c;
+        // insertion sort of the (nearly sorted) segment by (t_in, leaf index), carrying t_out
+        for (uint32_t a = b + 1; a < b + c; ++a) {
+            const double ti = A.hit_tin[a], to = A.hit_tout[a];
+            const uint32_t lf = A.hit_leaf[a];
+            uint32_t k = a;
+            while (k > b) {
+                const double tp = A.hit_tin[k - 1];
+                const uint32_t lp = A.hit_leaf[k - 1];
+                if (tp < ti || (tp == ti && lp < lf)) break;
+                A.hit_tin[k] = tp;
+                A.hit_tout[k] = A.hit_tout[k - 1];
+                A.hit_leaf[k] = lp;
+                --k;
+            }
+            A.hit_tin[k] = ti;
+            A.hit_tout[k] = to;
+            A.hit_leaf[k] = lf;
+        }
+        if (kCamera && c > 0) {  // later stages read foreground rays only
             Ray r;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -425,34 +483,26 @@ __global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamer
             store_ray(A.rays, S.gray[tid], r);
         }
     }
-    for (uint32_t i = tid; i < nh; i += kThreads) {
-        // hits stay grouped by ray (the sort permutes within segments only)
-        const uint32_t ri = S.hray[i];
-        const uint32_t leaf = S.hleaf[i];
-        double lo[3], hi[3], t0, t1;
-        RayPre p;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            p.r.o[a] = S.o[a][ri];
-            p.r.d[a] = S.d[a][ri];
-            p.inv[a] = S.inv[a][ri];
-        }
-        leaf_box(T, leaf, lo, hi);
-        slab_test(p, lo, hi, t0, t1);  // t_out of the leaf (t0 equals the stored t_in)
-        A.hit_leaf[base + i] = leaf;
-        A.hit_tin[base + i] = S.htin[i];
-        A.hit_tout[base + i] = t1;
-        A.hit_ray[base + i] = S.gray[ri];
+}
+
+// Persistent: a block processes tiles tile = blockIdx.x + k * gridDim.x.
+// kList passes read their tile count from the device (no host round trip).
+template <bool kCamera, int kR, bool kList>
+__global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0,
+                                                           uint32_t rows, uint32_t n, uint32_t n_tiles,
+                                                           BfsArgs A) {
+    extern __shared__ __align__(16) uint8_t bfs_smem[];
+    BfsSmem& S = *reinterpret_cast<BfsSmem*>(bfs_smem);
+    const uint32_t tiles = kList ? (A.counters[1] + kR - 1) / kR : n_tiles;
+    for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        bfs_tile<kCamera, kR, kList>(T, cam, row0, rows, n, A, S, tile);
+        __syncthreads();
     }
 }
 
-// Per-ray depth-first traversal of the rays of overflowing tiles.
 template <bool kCamera>
-__global__ void __launch_bounds__(128) k_traverse_fallback(DevOctree T, DevCamera cam, uint32_t row0,
-                                                           const uint32_t* n_list, BfsArgs A) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *n_list) return;
-    const uint32_t i = A.overflow_dense[k];
+__device__ __forceinline__ void fallback_ray(const DevOctree& T, const DevCamera& cam, uint32_t row0,
+                                                  const BfsArgs& A, uint32_t i) {
     if (i == 0xffffffffu) return;
     Ray r;
     if constexpr (kCamera) {
@@ -497,6 +547,15 @@ __global__ void __launch_bounds__(128) k_traverse_fallback(DevOctree T, DevCamer
         A.hit_tout[b] = to;
         A.hit_leaf[b] = lf;
     }
+}
+
+// Per-ray depth-first traversal of the rays that overflowed both cooperative
+// passes (persistent grid-stride over the device-side list).
+template <bool kCamera>
+__global__ void __launch_bounds__(128) k_traverse_fallback(DevOctree T, DevCamera cam, uint32_t row0,
+                                                           const uint32_t* n_list, BfsArgs A) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < *n_list; k += gridDim.x * blockDim.x)
+        fallback_ray<kCamera>(T, cam, row0, A, A.overflow_dense[k]);
 }
 
 // CSR view (ray order) of the traversal output: out[csr[i] + k] = in[off[i] + k]
@@ -563,47 +622,60 @@ static BfsArgs bfs_args(const TraverseOut& o) {
                    o.counters, o.overflow_rays, o.overflow_dense, o.rays, o.capacity};
 }
 
+static int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        SVLF_CUDA(cudaGetDevice(&dev));
+        SVLF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return sms;
+}
+
+constexpr int kBfsBlocksPerSm = 4;
+
 void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
                      const TraverseOut& o, cudaStream_t s) {
     if (n == 0) return;
     const BfsArgs A = bfs_args(o);
+    const uint32_t cap_grid = uint32_t(num_sms() * kBfsBlocksPerSm);
     if (cam) {
         set_bfs_attr<true, kRays, false>();
         const uint32_t tiles = ((cam->width + 7) / 8) * ((rows + 7) / 8);
-        k_traverse_bfs<true, kRays, false><<<tiles, kThreads, sizeof(BfsSmem), s>>>(T, *cam, row0, rows, n, A);
+        k_traverse_bfs<true, kRays, false><<<std::min(tiles, cap_grid), kThreads, sizeof(BfsSmem), s>>>(
+            T, *cam, row0, rows, n, tiles, A);
     } else {
         set_bfs_attr<false, kRays, false>();
-        k_traverse_bfs<false, kRays, false><<<(n + kRays - 1) / kRays, kThreads, sizeof(BfsSmem), s>>>(
-            T, DevCamera{}, 0, 0, n, A);
+        const uint32_t tiles = (n + kRays - 1) / kRays;
+        k_traverse_bfs<false, kRays, false><<<std::min(tiles, cap_grid), kThreads, sizeof(BfsSmem), s>>>(
+            T, DevCamera{}, 0, 0, n, tiles, A);
     }
     note_launch();
 }
 
-void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
-                           const TraverseOut& o, cudaStream_t s) {
-    if (n_overflow == 0) return;
+void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
+                           cudaStream_t s) {
     const BfsArgs A = bfs_args(o);
-    const uint32_t blocks = (n_overflow + kRaysDense - 1) / kRaysDense;
+    const uint32_t grid = uint32_t(num_sms() * kBfsBlocksPerSm);
     if (cam) {
         set_bfs_attr<true, kRaysDense, true>();
-        k_traverse_bfs<true, kRaysDense, true><<<blocks, kThreads, sizeof(BfsSmem), s>>>(T, *cam, row0, 0, 0, A);
+        k_traverse_bfs<true, kRaysDense, true><<<grid, kThreads, sizeof(BfsSmem), s>>>(T, *cam, row0, 0, 0, 0, A);
     } else {
         set_bfs_attr<false, kRaysDense, true>();
-        k_traverse_bfs<false, kRaysDense, true><<<blocks, kThreads, sizeof(BfsSmem), s>>>(T, DevCamera{}, 0, 0,
-                                                                                          0, A);
+        k_traverse_bfs<false, kRaysDense, true><<<grid, kThreads, sizeof(BfsSmem), s>>>(T, DevCamera{}, 0, 0, 0, 0,
+                                                                                        A);
     }
     note_launch();
 }
 
-void launch_traverse_fallback(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t n_overflow,
-                              const TraverseOut& o, cudaStream_t s) {
-    if (n_overflow == 0) return;
+void launch_traverse_fallback(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
+                              cudaStream_t s) {
     const BfsArgs A = bfs_args(o);
-    const uint32_t blocks = (n_overflow + 127) / 128;
+    const uint32_t grid = uint32_t(num_sms() * 4);
     if (cam)
-        k_traverse_fallback<true><<<blocks, 128, 0, s>>>(T, *cam, row0, o.counters + 3, A);
+        k_traverse_fallback<true><<<grid, 128, 0, s>>>(T, *cam, row0, o.counters + 3, A);
     else
-        k_traverse_fallback<false><<<blocks, 128, 0, s>>>(T, DevCamera{}, 0, o.counters + 3, A);
+        k_traverse_fallback<false><<<grid, 128, 0, s>>>(T, DevCamera{}, 0, o.counters + 3, A);
     note_launch();
 }
 
