@@ -159,10 +159,17 @@ def cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1):
             "seconds_per_frame": round(s, 3)}
 
 
-def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True):
+def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=None, world=1):
     """C3: one 512^2 frame (2^18 rays), stage-3 volumetric step (lr 2e-4), octree depth 8 from
-    that frame's back-projected depth (train()'s occupancy for a one-frame dataset)."""
+    that frame's back-projected depth (train()'s occupancy for a one-frame dataset).
+    With N ranks (C5 shape): data-parallel, every rank steps its own 2^18-ray batch and the
+    library all-reduces loss, decoder gradients and touched feature rows over NCCL before the
+    replicated Adam step (weak scaling; value = N * 2^18 / max-over-ranks step time)."""
     import paper_2205_07058_b200.synthetic as S
+    from paper_2205_07058_b200.parallel import init_data_parallel
+
+    if world > 1:
+        init_data_parallel(ctx, dist)
 
     sc, cam, pts, res, dil, rays, cgt, depth, alpha = S.c3_workload()
     tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
@@ -182,6 +189,7 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True):
         for _ in range(warmup):
             step()
         stream.synchronize()
+        barrier(dist)
         ms, parts = [], []
         for _ in range(steps):
             flush.zero_()
@@ -192,24 +200,28 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True):
             stream.synchronize()
             ms.append(a.elapsed_time(b_))
             parts.append(ctx.last_timings())
-    step_ms = statistics.median(ms)
+    step_ms = max_over_ranks(statistics.median(ms), dist, device)
     e2e = []
     for _ in range(max(3, min(steps, 5))):
+        barrier(dist)
         t0 = time.perf_counter()
         P.train_step(model, rays, cgt, depth, alpha, mode="volumetric", lr=2e-4)
         e2e.append((time.perf_counter() - t0) * 1e3)
-    e2e_ms = statistics.median(e2e)
+    e2e_ms = max_over_ranks(statistics.median(e2e), dist, device)
     hits = int(statistics.median(p["hits"] for p in parts))
+    if world > 1:
+        ctx.detach_nccl()
     out = {"metric": "train rays/s (C3: 2^18-ray 512x512 batch, stage-3 volumetric step incl. Adam)",
-           "value": round(n / (step_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s", "ms_per_step": round(step_ms, 4),
+           "n_gpus": world, "parallelism": f"dp{world} (NCCL all-reduce of loss, decoder grads, touched rows)",
+           "value": round(world * n / (step_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s", "ms_per_step": round(step_ms, 4),
            "rays": n, "active_hits": hits, "vertices": int(tree.vertex_count), "leaves": int(tree.leaf_count),
            "stages_ms": {k: round(statistics.median(p[k] for p in parts), 4)
                          for k in ("traverse_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms")},
            "dtype": "fp32 (reference accumulation order) / f64 geometry and loss",
-           "e2e": {"value": round(n / (e2e_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
+           "e2e": {"value": round(world * n / (e2e_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
                    "h2d_bytes_per_step": n * (48 + 12 + 8 + 1), "d2h_bytes_per_step": 8,
                    "api": "paper_2205_07058_b200.train_step (C ABI svlf_train_step, host batch)"}}
-    if cpu:
+    if cpu and world == 1:
         try:
             sys.path.insert(0, os.path.join(ROOT, "oracle"))
             import oracle as O
@@ -366,6 +378,14 @@ def main():
     e2e_step = max_over_ranks(statistics.median(e2e_ms), dist, device)
     e2e_value = world * n / (e2e_step * 1e-3) / 1e6
 
+    train = None
+    if not args.no_train:
+        try:
+            train = bench_train(P, torch, device, stream, ctx, max(3, args.steps), 3,
+                                cpu=not args.no_cpu_baseline and world == 1 and rank == 0, dist=dist, world=world)
+        except Exception as e:
+            train = {"error": str(e)}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -380,6 +400,7 @@ def main():
     peak = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
     stage = {k: round(statistics.median(t[k] for t in decode_ms), 4)
              for k in ("traverse_ms", "emit_ms", "decode_ms", "composite_ms")}
+    stage["dense_pass_rays"] = int(decode_ms[-1].get("dense_rays", 0))
     stage["fallback_rays"] = int(decode_ms[-1].get("overflow_rays", 0))
     line = {
         "metric": "rendered rays/s at 1600x1600 (C2)",
@@ -412,12 +433,8 @@ def main():
             line["cpu_baseline"] = cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1)
         except Exception as e:  # reported, never silently dropped
             line["cpu_baseline"] = {"error": str(e)}
-    if not args.no_train:
-        try:
-            line["train"] = bench_train(P, torch, device, stream, ctx, max(3, args.steps), 3,
-                                        cpu=not args.no_cpu_baseline and world == 1)
-        except Exception as e:
-            line["train"] = {"error": str(e)}
+    if train is not None:
+        line["train"] = train
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -113,6 +113,7 @@ typedef struct svlf_timings {
     float traverse_ms, emit_ms, decode_ms, composite_ms, backward_ms, adam_ms, total_ms;
     long long hits;
     long long overflow_rays; /* rays re-traversed by the per-ray fallback walker */
+    long long dense_rays;    /* rays whose block queue overflowed, re-run by the dense 8-ray pass */
 } svlf_timings;
 
 /* ---- context -------------------------------------------------------- */
@@ -128,6 +129,18 @@ svlf_status svlf_ctx_set_stream(svlf_ctx* ctx, void* cuda_stream);
 svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out);
 /* Count of this library's kernel launches on the context since creation. */
 long long svlf_ctx_kernel_launches(const svlf_ctx* ctx);
+
+/* ---- data parallelism (one process per GPU, NCCL over NVLink) ----------
+ * svlf_nccl_unique_id fills 128 bytes on one rank; every rank passes the same
+ * bytes to svlf_ctx_attach_nccl. With a communicator attached, train steps
+ * all-reduce (sum) the loss, the loss statistics, the decoder gradients and
+ * the feature gradients before the (replicated, identical) Adam update, so
+ * each rank trains on its own shard of the batch. Feature
+ * gradients are exchanged sparsely: only rows touched by any rank's hits
+ * (union of per-rank touched-row masks) are reduced. */
+svlf_status svlf_nccl_unique_id(void* out128);
+svlf_status svlf_ctx_attach_nccl(svlf_ctx* ctx, const void* unique_id128, int rank, int world);
+svlf_status svlf_ctx_detach_nccl(svlf_ctx* ctx);
 
 /* ---- octree: SparseOctree::build / from_leaves (octree.hpp:47,82; src/octree.cpp:30-142)
  * ctx may be NULL: the octree is then host-only and is uploaded to the device

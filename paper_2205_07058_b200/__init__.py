@@ -77,7 +77,7 @@ class _OctreeInfo(C.Structure):
 class _Timings(C.Structure):
     _fields_ = [(n, C.c_float) for n in
                 ("traverse_ms", "emit_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms", "total_ms")] + \
-               [("hits", C.c_longlong), ("overflow_rays", C.c_longlong)]
+               [("hits", C.c_longlong), ("overflow_rays", C.c_longlong), ("dense_rays", C.c_longlong)]
 
 
 # ---- public value types (reference structs) ----------------------------------
@@ -179,6 +179,9 @@ def load_library():
         "svlf_ctx_set_stream": ([vp, vp], st),
         "svlf_ctx_last_timings": ([vp, C.POINTER(_Timings)], st),
         "svlf_ctx_kernel_launches": ([vp], C.c_longlong),
+        "svlf_nccl_unique_id": ([vp], st),
+        "svlf_ctx_attach_nccl": ([vp, vp, C.c_int, C.c_int], st),
+        "svlf_ctx_detach_nccl": ([vp], st),
         "svlf_octree_build": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
         "svlf_octree_from_leaves": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
         "svlf_octree_destroy": ([vp], st),
@@ -280,6 +283,22 @@ class Context:
     @staticmethod
     def kernel_launches() -> int:
         return int(load_library().svlf_ctx_kernel_launches(None))
+
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int):
+        """Data-parallel training: all-reduce loss, statistics and gradients over NCCL."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(_LIB.svlf_ctx_attach_nccl(self._h, buf, rank, world))
+
+    def detach_nccl(self):
+        _check(_LIB.svlf_ctx_detach_nccl(self._h))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (create on one rank, share with the others)."""
+    load_library()
+    buf = C.create_string_buffer(128)
+    _check(_LIB.svlf_nccl_unique_id(buf))
+    return buf.raw
 
 
 _DEFAULT_CTX = None

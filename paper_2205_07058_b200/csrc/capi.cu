@@ -12,6 +12,8 @@
 #include "device.cuh"
 #include "host_octree.hpp"
 #include "host_rng.hpp"
+#include <nccl.h>
+
 #include "train.cuh"
 
 namespace svlfb {
@@ -81,7 +83,10 @@ struct svlf_ctx {
     DevBuf h_tau, h_eta, h_rgb, out_rgb, out_alpha, out_depth, misc, tmp64, tmpx12, tc_scratch, overflow;
     DevBuf csr_off, csr_leaf, csr_tin, csr_tout, csr_ray, overflow2;
     size_t hit_cap = 0;
-    long long last_overflow_rays = 0;  // first-pass overflow * 1e6 + dense-pass overflow
+    long long last_overflow_rays = 0;  // rays that reached the per-ray fallback walker
+    long long last_dense_rays = 0;     // rays re-run by the dense 8-ray pass
+    ncclComm_t nccl = nullptr;          // data-parallel communicator (optional)
+    int rank = 0, world = 1;
     TrainScratch train;
     int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
     cudaEvent_t ev[EV_N] = {};
@@ -237,7 +242,8 @@ bool read_traversal(svlf_ctx* ctx, uint32_t* total) {
     SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, traversal_counters(ctx), 16, cudaMemcpyDeviceToHost, ctx->stream));
     SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
     *total = uint32_t(ctx->h_pinned[4]);
-    ctx->last_overflow_rays = (long long)ctx->h_pinned[5] * 1000000 + ctx->h_pinned[7];
+    ctx->last_overflow_rays = ctx->h_pinned[7];
+    ctx->last_dense_rays = ctx->h_pinned[5];
     if (ctx->h_pinned[6] == 0) return true;
     ctx->hit_cap = size_t(*total) + *total / 4 + 1024;
     return false;
@@ -292,7 +298,8 @@ bool finish_render(svlf_ctx* ctx, uint32_t n, svlf_render_stats* stats) {
     SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, traversal_counters(ctx), 16, cudaMemcpyDeviceToHost, s));
     check_device_error(ctx);  // synchronizes
     const uint32_t total = uint32_t(ctx->h_pinned[4]);
-    ctx->last_overflow_rays = (long long)ctx->h_pinned[5] * 1000000 + ctx->h_pinned[7];
+    ctx->last_overflow_rays = ctx->h_pinned[7];
+    ctx->last_dense_rays = ctx->h_pinned[5];
     if (ctx->h_pinned[6] != 0) {
         ctx->hit_cap = size_t(total) + total / 4 + 1024;
         return false;
@@ -305,7 +312,7 @@ bool finish_render(svlf_ctx* ctx, uint32_t n, svlf_render_stats* stats) {
     cudaEventElapsedTime(&ms[2], ctx->ev[EV_EMIT], ctx->ev[EV_DECODE]);
     cudaEventElapsedTime(&ms[3], ctx->ev[EV_DECODE], ctx->ev[EV_COMPOSITE]);
     ctx->last = svlf_timings{ms[0], ms[1], ms[2], ms[3], 0.f, 0.f, ms[0] + ms[1] + ms[2] + ms[3],
-                             (long long)total, (long long)ctx->last_overflow_rays};
+                             (long long)total, ctx->last_overflow_rays, ctx->last_dense_rays};
     if (stats) {
         stats->rays += n;
         stats->rays_with_hits += (long long)fg;
@@ -386,11 +393,52 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
         {
             DeviceGuard g(ctx->device);
             cudaStreamSynchronize(ctx->stream);
+            if (ctx->nccl) ncclCommDestroy(ctx->nccl);
             for (auto& e : ctx->ev) cudaEventDestroy(e);
             if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
             cudaStreamDestroy(ctx->own_stream);
         }
         delete ctx;
+    });
+}
+
+svlf_status svlf_nccl_unique_id(void* out128) {
+    return guard([&] {
+        require(out128 != nullptr, "out is null");
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId id;
+        const ncclResult_t r = ncclGetUniqueId(&id);
+        if (r != ncclSuccess) fail(SVLF_ERR_CUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+        std::memcpy(out128, &id, sizeof id);
+    });
+}
+
+svlf_status svlf_ctx_attach_nccl(svlf_ctx* ctx, const void* id128, int rank, int world) {
+    return guard([&] {
+        require(ctx && id128, "null argument");
+        require(world >= 1 && rank >= 0 && rank < world, "bad rank/world");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+        ctx->nccl = nullptr;
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof id);
+        const ncclResult_t r = ncclCommInitRank(&ctx->nccl, world, id, rank);
+        if (r != ncclSuccess) fail(SVLF_ERR_CUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+        ctx->rank = rank;
+        ctx->world = world;
+    });
+}
+
+svlf_status svlf_ctx_detach_nccl(svlf_ctx* ctx) {
+    return guard([&] {
+        require(ctx != nullptr, "ctx is null");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+        ctx->nccl = nullptr;
+        ctx->rank = 0;
+        ctx->world = 1;
     });
 }
 
@@ -785,7 +833,7 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
     if (nn) cudaEventElapsedTime(&trav_ms, ctx->ev[EV_START], ctx->ev[EV_EMIT]);
     TrainBatchDev b{d_rays, d_cgt, d_depth, d_alpha, nn, ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(),
                     ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total};
-    TrainOptions opt{mode == SVLF_LOSS_SURFACE, color_frozen != 0, adam, *lw, lr};
+    TrainOptions opt{mode == SVLF_LOSS_SURFACE, color_frozen != 0, adam, *lw, lr, ctx->nccl, ctx->world};
     ensure_pack_f32(m, s);
     TrainModelRefs mr{m->view(), m->params.as<float>(), m->grads.as<float>(), m->adam_m.as<float>(),
                       m->adam_v.as<float>(), m->n_ft, m->n_fc, m->steps, pack_f32_view(m->pack_f32.as<float>())};

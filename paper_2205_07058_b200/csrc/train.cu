@@ -26,8 +26,12 @@
 #include <cmath>
 #include <cstring>
 
+#include <nccl.h>
+
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "mlp_simt.cuh"
 #include "train.cuh"
@@ -530,6 +534,33 @@ __global__ void __launch_bounds__(256) k_gemm_dw(const float* __restrict__ Dm, i
             if (o0 + ty * 2 + a < O) atomicAdd(db + o0 + ty * 2 + a, bacc[a]);
 }
 
+// rows (vertices) whose features any active hit touches
+__global__ void k_touched(DevOctree T, const uint32_t* hit_leaf, const uint32_t* dhit, uint32_t N, uint8_t* touched) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const uint32_t* c = T.corners + 8 * size_t(hit_leaf[dhit[j]]);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) touched[c[b]] = 1;
+}
+
+// pack / unpack the touched rows of both feature gradients: row r -> [ft 64 | fc 32]
+__global__ void k_pack_rows(const uint32_t* rows, const uint32_t* n_rows, const float* g_ft, const float* g_fc,
+                            float* packed, bool unpack, float* g_ft_w, float* g_fc_w) {
+    const uint32_t k = blockIdx.x;
+    if (k >= *n_rows) return;
+    const size_t r = rows[k];
+    for (uint32_t d = threadIdx.x; d < 96; d += blockDim.x) {
+        float* dst = packed + size_t(k) * 96 + d;
+        if (!unpack) {
+            *dst = d < 64 ? g_ft[r * 64 + d] : g_fc[r * 32 + (d - 64)];
+        } else if (d < 64) {
+            g_ft_w[r * 64 + d] = *dst;
+        } else {
+            g_fc_w[r * 32 + (d - 64)] = *dst;
+        }
+    }
+}
+
 struct AdamSeg {
     float* p;
     const float* g;
@@ -573,7 +604,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     TrainResult res;
     res.rays = b.n;
     if (!S.h_pinned) {
-        SVLF_CUDA(cudaMallocHost(&S.h_pinned, 64));
+        SVLF_CUDA(cudaMallocHost(&S.h_pinned, 256));
         for (auto& e : S.ev) SVLF_CUDA(cudaEventCreate(&e));
     }
     const size_t P = M.n_ft + M.n_fc + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE;
@@ -662,6 +693,53 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
             gemm(D_C3, 3, A_H3, kHid, g_mc + D::C_W3, g_mc + D::C_B3);
         }
         note_launch(o.color_frozen ? 3 : 7);
+    }
+    // ---- data parallel: all-reduce loss, statistics and gradients (NCCL)
+    if (o.nccl_comm) {
+        ncclComm_t comm = static_cast<ncclComm_t>(o.nccl_comm);
+        auto nccl = [](ncclResult_t r) {
+            if (r != ncclSuccess) fail(SVLF_ERR_CUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+        };
+        // loss and counters (as doubles) in one reduction
+        double* red = S.red.ensure<double>(4);
+        SVLF_CUDA(cudaMemcpyAsync(red, loss_out, 8, cudaMemcpyDeviceToDevice, s));
+        const double local_cnt[3] = {double(res.skipped), double(res.eta_skipped), double(res.rays)};
+        SVLF_CUDA(cudaMemcpyAsync(red + 1, local_cnt, 24, cudaMemcpyHostToDevice, s));
+        nccl(ncclAllReduce(red, red, 4, ncclFloat64, ncclSum, comm, s));
+        SVLF_CUDA(cudaMemcpyAsync(loss_out, red, 8, cudaMemcpyDeviceToDevice, s));
+        // decoders: dense
+        nccl(ncclAllReduce(g_mt, g_mt, SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE, ncclFloat32, ncclSum, comm, s));
+        // features: union of touched rows (max of 0/1 flags), compacted, summed, scattered back
+        const uint32_t V = M.view.V;
+        uint8_t* touched = S.touched.ensure<uint8_t>(V);
+        SVLF_CUDA(cudaMemsetAsync(touched, 0, V, s));
+        if (N) k_touched<<<(N + 127) / 128, 128, 0, s>>>(T, b.hit_leaf, dhit, N, touched);
+        nccl(ncclAllReduce(touched, touched, V, ncclUint8, ncclMax, comm, s));
+        uint32_t* rows = S.rows.ensure<uint32_t>(V);
+        uint32_t* n_rows = S.n_rows.ensure<uint32_t>(1);
+        size_t tb = 0;
+        cub::CountingInputIterator<uint32_t> idx(0);
+        cub::DeviceSelect::Flagged(nullptr, tb, idx, touched, rows, n_rows, int(V));
+        SVLF_CUDA(cub::DeviceSelect::Flagged(S.scan_tmp.ensure<char>(tb), tb, idx, touched, rows, n_rows, int(V), s));
+        SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 12, n_rows, 4, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        const uint32_t K = uint32_t(S.h_pinned[12]);
+        res.exchanged_rows = K;
+        if (K) {
+            float* packed = S.packed.ensure<float>(size_t(K) * 96);
+            k_pack_rows<<<K, 96, 0, s>>>(rows, n_rows, g_ft, g_fc, packed, false, g_ft, g_fc);
+            nccl(ncclAllReduce(packed, packed, size_t(K) * 96, ncclFloat32, ncclSum, comm, s));
+            k_pack_rows<<<K, 96, 0, s>>>(rows, n_rows, g_ft, g_fc, packed, true, g_ft, g_fc);
+            note_launch(2);
+        }
+        SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 16, red + 1, 24, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        double cnt[3];
+        std::memcpy(cnt, S.h_pinned + 16, 24);
+        res.skipped = (long long)cnt[0];
+        res.eta_skipped = (long long)cnt[1];
+        res.rays = (long long)cnt[2];  // statistics of the whole (all-rank) batch
+        note_launch(2);
     }
     SVLF_CUDA(cudaEventRecord(S.ev[4], s));
 

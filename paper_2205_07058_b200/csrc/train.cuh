@@ -27,6 +27,8 @@ struct TrainOptions {
     bool adam;          // false: loss + gradients only
     svlf_loss_weights lw;
     float lr;
+    void* nccl_comm = nullptr;  // ncclComm_t: data-parallel gradient exchange when set
+    int world = 1;
 };
 
 struct TrainModelRefs {
@@ -45,6 +47,7 @@ struct TrainResult {
     long long rays = 0, skipped = 0, eta_skipped = 0;
     int error = 0;
     svlf_timings timings{};
+    long long exchanged_rows = 0;  // feature rows all-reduced (data-parallel)
 };
 
 struct TrainScratch {
@@ -53,6 +56,7 @@ struct TrainScratch {
     DevBuf dhit, dray, hitf, hitd;                                // per active hit
     DevBuf acts, deltas;                                          // feature-major scratch
     DevBuf scan_tmp, counters, loss_out;
+    DevBuf touched, rows, n_rows, packed, red;  // sparse feature-gradient exchange
     int* h_pinned = nullptr;
     cudaEvent_t ev[8] = {};
     ~TrainScratch();

@@ -1,0 +1,49 @@
+"""Multi-GPU plumbing for the SVLF path.
+
+* Render shards with no collective: the octree and model are replicated and
+  each rank renders its own frames (weak scaling) or a row band of one frame
+  (`row_band`, strong scaling), written into its own buffers.
+* Training is data-parallel: the ray batch is split across ranks
+  (`shard_slice`); each rank's train step computes loss and gradients of its
+  shard, and the library all-reduces them over NCCL (decoders densely,
+  feature rows sparsely: union of touched rows) before the replicated Adam
+  step. Because the reference's gradients are sums over rays (no 1/N,
+  src/train.cpp:473-478), the sum of the shards' gradients is the full
+  batch's gradient; any partition is valid.
+
+torch.distributed is used only to rendezvous (share the NCCL id, barriers and
+max-over-ranks timing); the gradient traffic goes over the library's own
+NCCL communicator.
+"""
+from __future__ import annotations
+
+
+def shard_slice(n: int, rank: int, world: int) -> slice:
+    """Contiguous, balanced split of n items: rank r gets [r*n//w, (r+1)*n//w)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return slice(rank * n // world, (rank + 1) * n // world)
+
+
+def row_band(height: int, rank: int, world: int) -> tuple[int, int]:
+    """(row0, rows) of rank's band of an image, balanced to within one row."""
+    s = shard_slice(height, rank, world)
+    return s.start, s.stop - s.start
+
+
+def init_data_parallel(ctx, dist=None) -> bool:
+    """Attach an NCCL communicator to `ctx` spanning the current
+    torch.distributed world (rank 0 creates the id and broadcasts it).
+    Returns False (nothing attached) when torch.distributed is not
+    initialised."""
+    import paper_2205_07058_b200 as P
+
+    if dist is None:
+        import torch.distributed as dist
+    if not dist.is_initialized():
+        return False
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [P.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx.attach_nccl(obj[0], rank, world)
+    return True
