@@ -1,0 +1,54 @@
+// svlf/b200.hpp — B200-specific controls of the C++ API (no reference
+// counterpart).
+//
+// * Process-wide session: one svlf_ctx (CUDA device + stream + arenas) used by
+//   the drop-in functions in render.hpp / train.hpp / octree.hpp. Calls are
+//   serialised by a mutex, so concurrent read-only renders are safe.
+// * DeviceModel: the explicit fast path. The device copy is authoritative;
+//   train steps do not round-trip the tensors to the host; sync_to() copies
+//   them back on demand (validation renders on the host side, checkpoints).
+#pragma once
+
+#include <span>
+
+#include "svlf/render.hpp"
+#include "svlf/train.hpp"
+
+struct svlf_ctx;
+struct svlf_model;
+
+namespace svlf::b200 {
+
+enum class Precision { FP32 = 0, BF16 = 1, FP16 = 2 };
+
+void set_device(int device);  // before first use; default $SVLF_DEVICE or 0
+void set_render_precision(Precision p);
+Precision render_precision();
+svlf_ctx* session_context();  // creates the session on first call
+
+class DeviceModel {
+  public:
+    explicit DeviceModel(const SvlfModel& model);
+    DeviceModel(const SvlfModel& model, const ModelAdam& adam);
+    ~DeviceModel();
+    DeviceModel(const DeviceModel&) = delete;
+    DeviceModel& operator=(const DeviceModel&) = delete;
+
+    void upload(const SvlfModel& model);
+    void upload(const ModelAdam& adam);
+    void sync_to(SvlfModel& model) const;
+    void sync_to(ModelAdam& adam) const;
+
+    void render(const Camera& camera, FrameBuffers& out, RenderStats* stats = nullptr,
+                const float* background = nullptr) const;
+    double train_step(std::span<const RaySupervision> batch, LossMode mode, bool color_frozen, float lr,
+                      const LossWeights& lw = {}, LossStats* stats = nullptr);
+
+    svlf_model* handle() const { return m_; }
+
+  private:
+    SparseOctree octree_;  // keeps the library octree alive
+    svlf_model* m_ = nullptr;
+};
+
+}  // namespace svlf::b200

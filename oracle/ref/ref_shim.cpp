@@ -411,4 +411,14 @@ int ref_train(void* sp, const double* cams, int n_frames, uint32_t w, uint32_t h
     });
 }
 
+// ---- checkpoints: load_checkpoint + save_checkpoint (src/model.cpp:182-235)
+int ref_checkpoint_roundtrip(const char* in, const char* out) {
+    return guarded([&] {
+        SvlfModel m;
+        ModelAdam a;
+        load_checkpoint(in, m, a);
+        save_checkpoint(out, m, a);
+    });
+}
+
 }  // extern "C"
