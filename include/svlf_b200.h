@@ -166,6 +166,7 @@ svlf_status svlf_traverse(svlf_ctx* ctx, const svlf_octree* tree, const double* 
                           double* t_out, double* x12, size_t* total);
 
 /* ---- model: SvlfModel + ModelAdam (model.hpp:16-34,80-90) ----------- */
+/* The model runs on `ctx`; destroy models before their context. */
 svlf_status svlf_model_create(svlf_ctx* ctx, const svlf_octree* tree, svlf_model** out);
 svlf_status svlf_model_destroy(svlf_model* model);
 /* init_model(octree, seed), src/model.cpp:15-28 (bit-identical parameters) */

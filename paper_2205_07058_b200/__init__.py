@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -253,13 +254,17 @@ class Context:
         _check(L.svlf_ctx_create(device, C.byref(h)))
         self._h = h
         self.device = device
+        self._deps = weakref.WeakSet()  # models bound to this context
 
     @property
     def handle(self):
         return self._h
 
     def close(self):
+        """Destroys the context; models created on it are released first."""
         if getattr(self, "_h", None):
+            for dep in list(getattr(self, "_deps", ())):
+                dep._release()
             _LIB.svlf_ctx_destroy(self._h)
             self._h = None
 
@@ -286,6 +291,7 @@ class Context:
 
     def attach_nccl(self, unique_id: bytes, rank: int, world: int):
         """Data-parallel training: all-reduce loss, statistics and gradients over NCCL."""
+        _load_framework_nccl()
         buf = C.create_string_buffer(bytes(unique_id), 128)
         _check(_LIB.svlf_ctx_attach_nccl(self._h, buf, rank, world))
 
@@ -293,8 +299,19 @@ class Context:
         _check(_LIB.svlf_ctx_detach_nccl(self._h))
 
 
+def _load_framework_nccl():
+    # The library resolves NCCL with dlopen("libnccl.so.2"): make sure PyTorch's
+    # bundled NCCL is the one in the process (a different build loaded first
+    # would break a later `import torch`).
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """128-byte ncclUniqueId (create on one rank, share with the others)."""
+    _load_framework_nccl()
     load_library()
     buf = C.create_string_buffer(128)
     _check(_LIB.svlf_nccl_unique_id(buf))
@@ -413,14 +430,18 @@ class Model:
         h = C.c_void_p()
         _check(_LIB.svlf_model_create(self.ctx.handle, octree.handle, C.byref(h)))
         self._h = h
+        self.ctx._deps.add(self)
         self.V = octree.vertex_count
         if seed is not None:
             self.init(seed)
 
-    def __del__(self):
+    def _release(self):
         if getattr(self, "_h", None) and _LIB is not None:
             _LIB.svlf_model_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        self._release()
 
     @property
     def handle(self):
@@ -479,12 +500,23 @@ def _bg(background):
 
 
 def render_frame(model: Model, camera: Camera, stats: RenderStats | None = None, background=None,
-                 precision: str = "fp32"):
-    """render_frame (include/svlf/render.hpp:104): returns (rgb HxWx3, alpha HxW, depth HxW)."""
+                 precision: str = "fp32", out=None):
+    """render_frame (include/svlf/render.hpp:104): returns (rgb HxWx3, alpha HxW, depth HxW).
+
+    `out` = (rgb, alpha, depth) float32 C-contiguous arrays with W*H*3, W*H, W*H
+    elements to render into (the reference's caller-owned FrameBuffers, reused
+    across frames); fresh arrays are allocated otherwise."""
     n = camera.width * camera.height
-    rgb = np.zeros(n * 3, np.float32)
-    alpha = np.zeros(n, np.float32)
-    depth = np.zeros(n, np.float32)
+    if out is None:
+        rgb = np.empty(n * 3, np.float32)
+        alpha = np.empty(n, np.float32)
+        depth = np.empty(n, np.float32)
+    else:
+        rgb, alpha, depth = out
+        for arr, k in ((rgb, 3 * n), (alpha, n), (depth, n)):
+            if not (isinstance(arr, np.ndarray) and arr.dtype == np.float32 and arr.size == k
+                    and arr.flags.c_contiguous and arr.flags.writeable):
+                raise ValueError("out arrays must be writeable C-contiguous float32 of sizes W*H*3, W*H, W*H")
     st = _RenderStats()
     keep, bgp = _bg(background)
     cam = camera._c()

@@ -1,18 +1,23 @@
 // C ABI implementation (include/svlf_b200.h): contexts, device mirrors of
 // octrees and models, and the render / traversal / train pipelines.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "device.cuh"
 #include "host_octree.hpp"
+#include "host_pool.hpp"
 #include "host_rng.hpp"
-#include <nccl.h>
+#include "nccl_dyn.hpp"
 
 #include "train.cuh"
 
@@ -90,6 +95,15 @@ struct svlf_ctx {
     TrainScratch train;
     int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
     cudaEvent_t ev[EV_N] = {};
+    // host-buffer frames: banded render, D2H on a copy stream into pinned
+    // staging, parallel host copies into the caller's buffers (overlapped)
+    static constexpr int kMaxBands = 8;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t band_done[kMaxBands] = {}, band_copied[kMaxBands] = {};
+    float* h_stage = nullptr;
+    size_t h_stage_floats = 0;
+    DevBuf band_ctr;
+    std::unique_ptr<HostPool> pool;
     svlf_timings last{};
     std::mutex mu;  // one pipeline at a time per context
 };
@@ -105,7 +119,8 @@ struct svlf_octree {
 };
 
 struct svlf_model {
-    svlf_ctx* ctx = nullptr;
+    svlf_ctx* ctx = nullptr;  // must outlive the model (destroy models first)
+    int device = 0;
     const svlf_octree* tree = nullptr;
     uint32_t V = 0;
     size_t n_ft = 0, n_fc = 0, n_total = 0;
@@ -181,7 +196,10 @@ void ensure_pack_f32(svlf_model* m, cudaStream_t s) {
     m->pack_f32_version = m->version;
 }
 
-void check_device_error(svlf_ctx* ctx) {
+// Synchronizes and raises the device error flag, unless `discard` (the
+// pass is being redone, e.g. after a hit-buffer overflow, so errors raised on
+// its partial data are meaningless): then the flag is just cleared.
+void check_device_error(svlf_ctx* ctx, bool discard = false) {
     int* flag = ctx->misc.as<int>();
     int code = 0;
     SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -189,7 +207,7 @@ void check_device_error(svlf_ctx* ctx) {
     code = ctx->h_pinned[0];
     if (code != 0) {
         SVLF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-        fail(SVLF_ERR_RUNTIME, dev_error_message(code));
+        if (!discard) fail(SVLF_ERR_RUNTIME, dev_error_message(code));
     }
 }
 
@@ -296,14 +314,16 @@ bool finish_render(svlf_ctx* ctx, uint32_t n, svlf_render_stats* stats) {
     cudaStream_t s = ctx->stream;
     SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 8, misc_fg(ctx), 8, cudaMemcpyDeviceToHost, s));
     SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 4, traversal_counters(ctx), 16, cudaMemcpyDeviceToHost, s));
-    check_device_error(ctx);  // synchronizes
+    SVLF_CUDA(cudaStreamSynchronize(s));
     const uint32_t total = uint32_t(ctx->h_pinned[4]);
     ctx->last_overflow_rays = ctx->h_pinned[7];
     ctx->last_dense_rays = ctx->h_pinned[5];
-    if (ctx->h_pinned[6] != 0) {
+    if (ctx->h_pinned[6] != 0) {  // hit buffers overflowed: decode saw partial lists, redo
+        check_device_error(ctx, true);
         ctx->hit_cap = size_t(total) + total / 4 + 1024;
         return false;
     }
+    check_device_error(ctx);
     unsigned long long fg = 0;
     std::memcpy(&fg, ctx->h_pinned + 8, 8);
     float ms[4] = {};
@@ -354,6 +374,132 @@ void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_
     render_pipeline(ctx, m, &dc, row0, rows, n, bg, prec, d_rgb, d_alpha, d_depth, stats);
 }
 
+// Frame into HOST buffers. The image is rendered in up to kMaxBands row
+// bands, all enqueued without host round trips; each finished band is copied
+// D2H on ctx->copy_stream into pinned staging while later bands render, and
+// the host copies staging -> caller buffers with a worker pool while the GPU
+// is still busy. Per-band traversal counters are kept so a capacity overflow
+// in any band re-renders the frame with larger hit buffers.
+void render_frame_host(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg, svlf_precision prec,
+                       float* rgb, float* alpha, float* depth, svlf_render_stats* stats) {
+    require(cam != nullptr, "camera is null");
+    if (cam->width == 0 || cam->height == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "zero-size image");
+    const uint64_t n64 = uint64_t(cam->width) * cam->height;
+    require(n64 < (1ull << 31), "too many pixels in one call");
+    const uint32_t W = cam->width, H = cam->height, n = uint32_t(n64);
+    const DevCamera dc = to_dev_camera(*cam);
+    cudaStream_t s = ctx->stream;
+    float* d_rgb = ctx->out_rgb.ensure<float>(size_t(n) * 3);
+    float* d_alpha = ctx->out_alpha.ensure<float>(n);
+    float* d_depth = ctx->out_depth.ensure<float>(n);
+    if (ctx->h_stage_floats < size_t(n) * 5) {
+        if (ctx->h_stage) SVLF_CUDA(cudaFreeHost(ctx->h_stage));
+        ctx->h_stage = nullptr;
+        SVLF_CUDA(cudaMallocHost(&ctx->h_stage, size_t(n) * 5 * sizeof(float)));
+        ctx->h_stage_floats = size_t(n) * 5;
+    }
+    if (!ctx->pool) {
+        const char* e = std::getenv("SVLF_COPY_THREADS");
+        const int hw = int(std::thread::hardware_concurrency());
+        ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
+    }
+    float* st_rgb = ctx->h_stage;
+    float* st_alpha = st_rgb + size_t(n) * 3;
+    float* st_depth = st_alpha + n;
+    // ~700K rays per band (fewer bands: less per-band launch/tail cost; more:
+    // shorter exposed D2H + copy of the last band), at most kMaxBands
+    static const uint32_t band_rays = [] {
+        const char* e = std::getenv("SVLF_BAND_RAYS");
+        return e ? uint32_t(std::max(1, std::atoi(e))) : 700000u;  // measured best for C2 (3 bands)
+    }();
+    const uint32_t bands = std::max<uint32_t>(1, std::min<uint32_t>(svlf_ctx::kMaxBands, std::min(H, n / band_rays)));
+    const uint32_t band_rows = (H + bands - 1) / bands;
+    uint32_t* bctr = ctx->band_ctr.ensure<uint32_t>(4 * svlf_ctx::kMaxBands);
+    static const bool trace = std::getenv("SVLF_TRACE") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t_start = now();
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        reset_misc(ctx);
+        uint32_t nb = 0;
+        for (uint32_t r0 = 0; r0 < H; r0 += band_rows, ++nb) {
+            const uint32_t rows = std::min(band_rows, H - r0);
+            const size_t off = size_t(r0) * W, cnt = size_t(rows) * W;
+            uint32_t total = 0;
+            if (prec == SVLF_PRECISION_FP32) total = run_traversal(ctx, m->tree, &dc, r0, rows, uint32_t(cnt));
+            else enqueue_traversal(ctx, m->tree, &dc, r0, rows, uint32_t(cnt));
+            run_decode_composite(ctx, m, uint32_t(cnt), total, bg, prec, d_rgb + off * 3, d_alpha + off,
+                                 d_depth + off);
+            SVLF_CUDA(cudaMemcpyAsync(bctr + 4 * nb, traversal_counters(ctx), 16, cudaMemcpyDeviceToDevice, s));
+            SVLF_CUDA(cudaEventRecord(ctx->band_done[nb], s));
+            SVLF_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_done[nb], 0));
+            cudaStream_t c = ctx->copy_stream;
+            SVLF_CUDA(cudaMemcpyAsync(st_rgb + off * 3, d_rgb + off * 3, cnt * 12, cudaMemcpyDeviceToHost, c));
+            SVLF_CUDA(cudaMemcpyAsync(st_alpha + off, d_alpha + off, cnt * 4, cudaMemcpyDeviceToHost, c));
+            SVLF_CUDA(cudaMemcpyAsync(st_depth + off, d_depth + off, cnt * 4, cudaMemcpyDeviceToHost, c));
+            SVLF_CUDA(cudaEventRecord(ctx->band_copied[nb], c));
+        }
+        // drain bands in order: host copies overlap the GPU's later bands
+        const double t_enq = now();
+        if (trace) std::fprintf(stderr, "enqueue %.3f ms\n", t_enq - t_start);
+        for (uint32_t b = 0; b < nb; ++b) {
+            const double t0 = now();
+            SVLF_CUDA(cudaEventSynchronize(ctx->band_copied[b]));
+            const double t1 = now();
+            if (trace) std::fprintf(stderr, "band %u wait %.3f ms (since enqueue %.3f)\n", b, t1 - t0, t1 - t_enq);
+            const size_t off = size_t(b) * band_rows * W;
+            const size_t cnt = size_t(std::min(band_rows, H - b * band_rows)) * W;
+            constexpr size_t kPart = 64 * 1024;  // pixels per host copy task
+            const int parts = int((cnt + kPart - 1) / kPart);
+            ctx->pool->parallel_for(parts, [&](int i) {
+                const size_t p0 = off + size_t(i) * kPart, pc = std::min(kPart, off + cnt - p0);
+                std::memcpy(rgb + p0 * 3, st_rgb + p0 * 3, pc * 12);
+                std::memcpy(alpha + p0, st_alpha + p0, pc * 4);
+                std::memcpy(depth + p0, st_depth + p0, pc * 4);
+            });
+            if (trace) std::fprintf(stderr, "band %u copy %.3f ms\n", b, now() - t1);
+        }
+        SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 16, bctr, 16 * nb, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 8, misc_fg(ctx), 8, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        uint64_t total = 0, dense = 0, fallback = 0, worst = 0;
+        bool overflow = false;
+        for (uint32_t b = 0; b < nb; ++b) {
+            const uint32_t* c = reinterpret_cast<const uint32_t*>(ctx->h_pinned + 16 + 4 * b);
+            total += c[0];
+            dense += c[1];
+            overflow |= c[2] != 0;
+            fallback += c[3];
+            worst = std::max<uint64_t>(worst, c[0]);
+        }
+        ctx->last_overflow_rays = (long long)fallback;
+        ctx->last_dense_rays = (long long)dense;
+        check_device_error(ctx, overflow);
+        if (trace) std::fprintf(stderr, "final sync at %.3f ms\n", now() - t_start);
+        if (overflow) {
+            ctx->hit_cap = size_t(worst) + worst / 4 + 1024;
+            continue;
+        }
+        unsigned long long fg = 0;
+        std::memcpy(&fg, ctx->h_pinned + 8, 8);
+        float ms[4] = {};  // last band's stage times
+        cudaEventElapsedTime(&ms[0], ctx->ev[EV_START], ctx->ev[EV_COUNT]);
+        cudaEventElapsedTime(&ms[1], ctx->ev[EV_COUNT], ctx->ev[EV_EMIT]);
+        cudaEventElapsedTime(&ms[2], ctx->ev[EV_EMIT], ctx->ev[EV_DECODE]);
+        cudaEventElapsedTime(&ms[3], ctx->ev[EV_DECODE], ctx->ev[EV_COMPOSITE]);
+        ctx->last = svlf_timings{ms[0], ms[1], ms[2], ms[3], 0.f, 0.f, ms[0] + ms[1] + ms[2] + ms[3],
+                                 (long long)total, ctx->last_overflow_rays, ctx->last_dense_rays};
+        if (stats) {
+            stats->rays += n;
+            stats->rays_with_hits += (long long)fg;
+            stats->traversal_hits += (long long)total;
+            stats->thickness_queries += (long long)total;
+            stats->color_queries += (long long)total;
+        }
+        return;
+    }
+    fail(SVLF_ERR_RUNTIME, "traversal output capacity could not be satisfied");
+}
+
 size_t model_param_count(uint32_t V) { return size_t(V) * 96 + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE; }
 
 }  // namespace
@@ -381,6 +527,11 @@ svlf_status svlf_ctx_create(int device, svlf_ctx** out) {
         ctx->stream = ctx->own_stream;
         SVLF_CUDA(cudaMallocHost(&ctx->h_pinned, 256));
         for (auto& e2 : ctx->ev) SVLF_CUDA(cudaEventCreate(&e2));
+        SVLF_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < svlf_ctx::kMaxBands; ++b) {
+            SVLF_CUDA(cudaEventCreateWithFlags(&ctx->band_done[b], cudaEventDisableTiming));
+            SVLF_CUDA(cudaEventCreateWithFlags(&ctx->band_copied[b], cudaEventDisableTiming));
+        }
         ctx->misc.ensure<unsigned long long>(8);
         SVLF_CUDA(cudaMemset(ctx->misc.p, 0, 64));
         *out = ctx.release();
@@ -393,9 +544,16 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
         {
             DeviceGuard g(ctx->device);
             cudaStreamSynchronize(ctx->stream);
-            if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+            if (ctx->nccl) nccl_api().CommDestroy(ctx->nccl);
+            cudaStreamSynchronize(ctx->copy_stream);
             for (auto& e : ctx->ev) cudaEventDestroy(e);
+            for (int b = 0; b < svlf_ctx::kMaxBands; ++b) {
+                cudaEventDestroy(ctx->band_done[b]);
+                cudaEventDestroy(ctx->band_copied[b]);
+            }
             if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+            if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+            cudaStreamDestroy(ctx->copy_stream);
             cudaStreamDestroy(ctx->own_stream);
         }
         delete ctx;
@@ -407,8 +565,7 @@ svlf_status svlf_nccl_unique_id(void* out128) {
         require(out128 != nullptr, "out is null");
         static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
         ncclUniqueId id;
-        const ncclResult_t r = ncclGetUniqueId(&id);
-        if (r != ncclSuccess) fail(SVLF_ERR_CUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+        nccl_check(nccl_api().GetUniqueId(&id));
         std::memcpy(out128, &id, sizeof id);
     });
 }
@@ -419,12 +576,11 @@ svlf_status svlf_ctx_attach_nccl(svlf_ctx* ctx, const void* id128, int rank, int
         require(world >= 1 && rank >= 0 && rank < world, "bad rank/world");
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
-        if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+        if (ctx->nccl) nccl_api().CommDestroy(ctx->nccl);
         ctx->nccl = nullptr;
         ncclUniqueId id;
         std::memcpy(&id, id128, sizeof id);
-        const ncclResult_t r = ncclCommInitRank(&ctx->nccl, world, id, rank);
-        if (r != ncclSuccess) fail(SVLF_ERR_CUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+        nccl_check(nccl_api().CommInitRank(&ctx->nccl, world, id, rank));
         ctx->rank = rank;
         ctx->world = world;
     });
@@ -435,7 +591,7 @@ svlf_status svlf_ctx_detach_nccl(svlf_ctx* ctx) {
         require(ctx != nullptr, "ctx is null");
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
-        if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+        if (ctx->nccl) nccl_api().CommDestroy(ctx->nccl);
         ctx->nccl = nullptr;
         ctx->rank = 0;
         ctx->world = 1;
@@ -604,6 +760,7 @@ svlf_status svlf_model_create(svlf_ctx* ctx, const svlf_octree* tree, svlf_model
         DeviceGuard g(ctx->device);
         auto m = std::make_unique<svlf_model>();
         m->ctx = ctx;
+        m->device = ctx->device;
         m->tree = tree;
         m->V = tree->host.vertex_count;
         m->n_ft = size_t(m->V) * SVLF_FEAT_T_DIM;
@@ -620,7 +777,7 @@ svlf_status svlf_model_create(svlf_ctx* ctx, const svlf_octree* tree, svlf_model
 svlf_status svlf_model_destroy(svlf_model* m) {
     return guard([&] {
         if (!m) return;
-        DeviceGuard g(m->ctx->device);
+        DeviceGuard g(m->device);
         delete m;
     });
 }
@@ -757,16 +914,7 @@ svlf_status svlf_render_frame(svlf_ctx* ctx, svlf_model* m, const svlf_camera* c
         require(ctx && m && cam && rgb && alpha && depth, "null argument");
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
-        const size_t n = size_t(cam->width) * cam->height;
-        float* d_rgb = ctx->out_rgb.ensure<float>(n * 3);
-        float* d_alpha = ctx->out_alpha.ensure<float>(n);
-        float* d_depth = ctx->out_depth.ensure<float>(n);
-        render_device(ctx, m, cam, 0, cam->height, bg, prec, d_rgb, d_alpha, d_depth, stats);
-        cudaStream_t s = ctx->stream;
-        SVLF_CUDA(cudaMemcpyAsync(rgb, d_rgb, n * 12, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaMemcpyAsync(alpha, d_alpha, n * 4, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaMemcpyAsync(depth, d_depth, n * 4, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaStreamSynchronize(s));
+        render_frame_host(ctx, m, cam, bg, prec, rgb, alpha, depth, stats);
     });
 }
 

@@ -26,7 +26,7 @@
 #include <cmath>
 #include <cstring>
 
-#include <nccl.h>
+#include "nccl_dyn.hpp"
 
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -697,24 +697,23 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     // ---- data parallel: all-reduce loss, statistics and gradients (NCCL)
     if (o.nccl_comm) {
         ncclComm_t comm = static_cast<ncclComm_t>(o.nccl_comm);
-        auto nccl = [](ncclResult_t r) {
-            if (r != ncclSuccess) fail(SVLF_ERR_CUDA, std::string("NCCL: ") + ncclGetErrorString(r));
-        };
+        const NcclApi& api = nccl_api();
+        auto nccl = nccl_check;
         // loss and counters (as doubles) in one reduction
         double* red = S.red.ensure<double>(4);
         SVLF_CUDA(cudaMemcpyAsync(red, loss_out, 8, cudaMemcpyDeviceToDevice, s));
         const double local_cnt[3] = {double(res.skipped), double(res.eta_skipped), double(res.rays)};
         SVLF_CUDA(cudaMemcpyAsync(red + 1, local_cnt, 24, cudaMemcpyHostToDevice, s));
-        nccl(ncclAllReduce(red, red, 4, ncclFloat64, ncclSum, comm, s));
+        nccl(api.AllReduce(red, red, 4, ncclFloat64, ncclSum, comm, s));
         SVLF_CUDA(cudaMemcpyAsync(loss_out, red, 8, cudaMemcpyDeviceToDevice, s));
         // decoders: dense
-        nccl(ncclAllReduce(g_mt, g_mt, SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE, ncclFloat32, ncclSum, comm, s));
+        nccl(api.AllReduce(g_mt, g_mt, SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE, ncclFloat32, ncclSum, comm, s));
         // features: union of touched rows (max of 0/1 flags), compacted, summed, scattered back
         const uint32_t V = M.view.V;
         uint8_t* touched = S.touched.ensure<uint8_t>(V);
         SVLF_CUDA(cudaMemsetAsync(touched, 0, V, s));
         if (N) k_touched<<<(N + 127) / 128, 128, 0, s>>>(T, b.hit_leaf, dhit, N, touched);
-        nccl(ncclAllReduce(touched, touched, V, ncclUint8, ncclMax, comm, s));
+        nccl(api.AllReduce(touched, touched, V, ncclUint8, ncclMax, comm, s));
         uint32_t* rows = S.rows.ensure<uint32_t>(V);
         uint32_t* n_rows = S.n_rows.ensure<uint32_t>(1);
         size_t tb = 0;
@@ -728,7 +727,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
         if (K) {
             float* packed = S.packed.ensure<float>(size_t(K) * 96);
             k_pack_rows<<<K, 96, 0, s>>>(rows, n_rows, g_ft, g_fc, packed, false, g_ft, g_fc);
-            nccl(ncclAllReduce(packed, packed, size_t(K) * 96, ncclFloat32, ncclSum, comm, s));
+            nccl(api.AllReduce(packed, packed, size_t(K) * 96, ncclFloat32, ncclSum, comm, s));
             k_pack_rows<<<K, 96, 0, s>>>(rows, n_rows, g_ft, g_fc, packed, true, g_ft, g_fc);
             note_launch(2);
         }

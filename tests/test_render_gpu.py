@@ -181,3 +181,29 @@ def test_render_tc_matches_fp32_path(c1, ctx, precision):
     m = (a32 > 1e-2) & (a16 > 1e-2)
     assert m.sum() > 1000
     assert np.abs(d16 - d32)[m].max() < 5e-2
+
+
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+def test_render_hit_buffer_overflow_retry(oracle, precision):
+    """A fresh context sizes its hit buffers for ~4 hits/ray; a dense scene (~10 hits/ray,
+    > 1M hits) overflows them on the first frame. The frame must be redone transparently
+    (banded host path and device path), with no spurious geometry errors from the partial
+    hit lists, and match the oracle."""
+    pts = S.random_occupancy_points(32, 0.3, 5)
+    W = 448
+    cam = S.lookat_camera((0.5 + 1.8 * 0.6, 0.5 + 1.8 * 0.3, 0.5 + 1.8 * 0.7416), (0.5, 0.5, 0.5), W, W, 1.2 * W)
+    otree = oracle.tree_build(pts, 32, 0)
+    om = oracle.init_model(otree, 2)
+    orgb, oa, od, ost = oracle.render_frame(otree, om, cam, W, W)
+    assert ost[2] > (1 << 20) and ost[2] > 4 * W * W  # really overflows the initial capacity
+    for fresh in range(2):  # first call overflows; second reuses the grown buffers
+        c = P.Context(0)
+        tree = P.SparseOctree.build(pts, P.GridConfig(32, dilation=0), c)
+        model = P.Model(tree, seed=2, ctx=c)
+        st = P.RenderStats()
+        rgb, a, d = P.render_frame(model, P.Camera.from_record(cam, W, W), stats=st, precision=precision)
+        assert st.traversal_hits == ost[2]
+        tol = TOL_FP32 if precision == "fp32" else 2e-2
+        assert np.abs(rgb.reshape(-1) - orgb).max() <= tol
+        assert np.abs(a.reshape(-1) - oa).max() <= tol
+        c.close()
