@@ -9,23 +9,26 @@
 //              (stage 1 keeps pre-surface + surface hits, or the surface hit
 //              only when lambda_empty == 0), skipped / eta_skipped counters.
 //   scan/expand  dense list of active hits.
-//   k_fwd      per hit: f_T (and f_C where the loss needs colour) forward in
-//              fp32, reference accumulation order; activations stored
-//              feature-major in global scratch for the backward pass.
+//   forward    per hit: f_T input column (geometry, trilinear gathers);
+//              dense layers as fp32 GEMMs on feature-major activation
+//              matrices (cuBLAS SGEMM, pedantic fp32) + bias/relu epilogue;
+//              per hit: f_T heads, x_s, f_C input column; f_C layers as
+//              GEMMs; per hit: rgb head. Activations kept for backward.
 //   k_loss     per ray: Eq. 4 surface loss or composite + volumetric loss in
 //              fp64 and the composite backward dtau_j = dw_j T_j e_j -
 //              sum_{i>j} dw_i w_i (reverse scan), per-ray loss.
-//   k_bwd      per hit: f_C backward (input gradient always; feature
-//              gradients unless colour is frozen) incl. the positional
-//              Jacobian d eta += <dx_s, x1 - x2>, then f_T backward; feature
-//              gradients scattered with atomics; layer deltas stored.
-//   k_gemm_dw  weight gradients dW = D^T X per layer (split over hits).
+//   backward   per hit: f_C head; GEMMs dX = W^T D with relu masks; per hit:
+//              colour-feature scatter (unless frozen), positional Jacobian
+//              d eta += <dx_s, x1 - x2>, f_T heads; GEMM dX_T; per hit:
+//              thickness-feature scatter (atomics); weight gradients
+//              dW = D X^T and db = D 1 as GEMM/GEMV over all hits.
 //   k_adam     dense bias-corrected Adam in fp64 over every parameter
 //              (src/mlp.cpp:277-296), colour tensors skipped when frozen.
 // Gradients are sums over rays (no 1/N), as in the reference.
 #include <cmath>
 #include <cstring>
 
+#include "cublas_dyn.hpp"
 #include "nccl_dyn.hpp"
 
 #include <cub/device/device_reduce.cuh>
@@ -226,44 +229,95 @@ __device__ __forceinline__ void weights_from_u(const double* u, float* w) {
 }
 
 // ---- forward ------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_fwd(DevOctree T, DevModel M, DecPackF32 P, HitArgs H, int* err) {
+// The dense layers are GEMMs over the feature-major activation matrices
+// (cuBLAS SGEMM, fp32; see run_train_step); these kernels are the per-hit
+// parts around them.
+
+// f_T input column: [r6 | psi_T(x1) | psi_T(x2)] (voxel_batch.hpp:69-96)
+__global__ void __launch_bounds__(128) k_fwd_in_t(DevOctree T, DevModel M, HitArgs H, int* err) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= H.N) return;
     const size_t N = H.N;
     float* X = H.acts + j;
     HitGeom g;
     if (!hit_geom(T, H, j, g, err)) {
-        H.tau[j] = 0.f;
-        H.eta[j] = 0.5f;
+        for (int k = 0; k < kInT; ++k) X[(A_XT + k) * N] = 0.f;
         return;
     }
 #pragma unroll
     for (int k = 0; k < 6; ++k) X[(A_XT + k) * N] = g.r6[k];
     gather_col<kFt>(M.ft, g.corners, g.w1, X + (A_XT + 6) * N, N);
     gather_col<kFt>(M.ft, g.corners, g.w2, X + (A_XT + 6 + kFt) * N, N);
-    dense_relu_col(P.t_w0t, P.t_b0, X + A_XT * N, kInT, X + A_HT * N, N);
-    const float y0 = head_dot(P.t_w1, __ldg(P.t_b1), X + A_HT * N, N);
-    const float y1 = head_dot(P.t_w1 + kHid, __ldg(P.t_b1 + 1), X + A_HT * N, N);
+}
+
+// y = relu(y + b[row]) over a rows x N feature-major block (GEMM epilogue)
+__global__ void k_bias_relu(float* __restrict__ Y, const float* __restrict__ bias, size_t N) {
+    const uint32_t row = blockIdx.y;
+    const float b = __ldg(bias + row);
+    float* y = Y + size_t(row) * N;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < N; i += size_t(gridDim.x) * blockDim.x)
+        y[i] = fmaxf(y[i] + b, 0.f);
+}
+
+// f_T head (tau relu, eta sigmoid), x_s and the f_C input column
+// [r6 | psi_C(x_s)] for hits whose colour enters the loss (zeros otherwise).
+__global__ void __launch_bounds__(128) k_fwd_mid(DevOctree T, DevModel M, HitArgs H, int* err) {
+    using D = DecOffsets;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= H.N) return;
+    const size_t N = H.N;
+    float* X = H.acts + j;
+    const float* h = X + A_HT * N;
+    float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
+#pragma unroll 4
+    for (int k = 0; k < kHid; ++k) {
+        const float v = h[k * N];
+        y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
+        y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
+    }
     const float tau = y0 > 0.f ? y0 : 0.f;
     const float eta = sigmoid_ref(y1);
     H.tau[j] = tau;
     H.eta[j] = eta;
-    if (!has_color(H, j)) return;
-    double xs[3], u[3];
-    float ws[8];
-    if (!xs_coords(T, g, eta, xs, u)) {
-        raise_error(err, kErrPointNotInVoxel);
+    bool wrote = false;
+    HitGeom g;
+    if (has_color(H, j) && hit_geom(T, H, j, g, err)) {
+        double xs[3], u[3];
+        if (!xs_coords(T, g, eta, xs, u)) {
+            raise_error(err, kErrPointNotInVoxel);
+        } else {
+            float ws[8];
+            weights_from_u(u, ws);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) X[(A_XC + k) * N] = g.r6[k];
+            gather_col<kFc>(M.fc, g.corners, ws, X + (A_XC + 6) * N, N);
+            wrote = true;
+        }
+    }
+    if (!wrote)
+        for (int k = 0; k < kInC; ++k) X[(A_XC + k) * N] = 0.f;
+}
+
+// f_C head: rgb = sigmoid(W3 h3 + b3)
+__global__ void __launch_bounds__(128) k_fwd_rgb(DevModel M, HitArgs H) {
+    using D = DecOffsets;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= H.N) return;
+    const size_t N = H.N;
+    if (!has_color(H, j)) {
+        for (int c = 0; c < 3; ++c) H.rgb[c * N + j] = 0.f;
         return;
     }
-    weights_from_u(u, ws);
+    const float* h = H.acts + A_H3 * N + j;
+    float y[3] = {__ldg(M.mc + D::C_B3), __ldg(M.mc + D::C_B3 + 1), __ldg(M.mc + D::C_B3 + 2)};
+#pragma unroll 4
+    for (int k = 0; k < kHid; ++k) {
+        const float v = h[k * N];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) X[(A_XC + k) * N] = g.r6[k];
-    gather_col<kFc>(M.fc, g.corners, ws, X + (A_XC + 6) * N, N);
-    dense_relu_col(P.c_w0t, P.c_b0, X + A_XC * N, kInC, X + A_H1 * N, N);
-    dense_relu_col(P.c_w1t, P.c_b1, X + A_H1 * N, kHid, X + A_H2 * N, N);
-    dense_relu_col(P.c_w2t, P.c_b2, X + A_H2 * N, kHid, X + A_H3 * N, N);
+        for (int c = 0; c < 3; ++c) y[c] = fmaf(__ldg(M.mc + D::C_W3 + c * kHid + k), v, y[c]);
+    }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) H.rgb[c * N + j] = sigmoid_ref(head_dot(P.c_w3 + c * kHid, __ldg(P.c_b3 + c), X + A_H3 * N, N));
+    for (int c = 0; c < 3; ++c) H.rgb[c * N + j] = sigmoid_ref(y[c]);
 }
 
 // ---- loss + composite backward (per ray) ---------------------------------------
@@ -364,174 +418,142 @@ __global__ void k_loss(LossArgs L, HitArgs H) {
 }
 
 // ---- backward -----------------------------------------------------------------
-// dx[k] = sum_o W[o][k] d[o] for k in [0, K) (o outer, k inner: the reference's
-// d_prev accumulation order, src/mlp.cpp:205-215), optional relu mask by the
-// layer input activation, stored at out[k * N].
-template <int O>
-__device__ __forceinline__ void back_matvec(const float* __restrict__ W, int K, const float* d, size_t dstride,
-                                            const float* mask, size_t N, float* out) {
-#pragma unroll 1
-    for (int k0 = 0; k0 < K; k0 += 16) {
-        float acc[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-#pragma unroll 2
-        for (int o = 0; o < O; ++o) {
-            const float dv = d[o * dstride];
-            const float* wr = W + size_t(o) * K + k0;
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-                if (k0 + i < K) acc[i] = __fadd_rn(acc[i], __fmul_rn(__ldg(wr + i), dv));
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            if (k0 + i >= K) break;
-            float v = acc[i];
-            if (mask && !(mask[(k0 + i) * N] > 0.f)) v = 0.f;
-            out[(k0 + i) * N] = v;
-        }
-    }
-}
+// Layer deltas D (dL/d pre-activation, feature-major) flow through cuBLAS
+// GEMMs dX = W^T D; these kernels are the per-hit heads, relu masks and the
+// feature-gradient scatters (src/mlp.cpp:151-230, src/train.cpp:243-285).
 
-__global__ void __launch_bounds__(128) k_bwd(DevOctree T, DevModel M, HitArgs H, bool color_frozen, float* g_ft,
-                                             float* g_fc, int* err) {
+// f_C head (sigmoid') and its 3 -> 128 back-projection masked by relu'(h3)
+__global__ void __launch_bounds__(128) k_bwd_head_c(DevModel M, HitArgs H) {
     using D = DecOffsets;
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= H.N) return;
     const size_t N = H.N;
-    const float* X = H.acts + j;
     float* Dl = H.deltas + j;
-    HitGeom g;
-    if (!hit_geom(T, H, j, g, err)) return;
-    double deta = H.deta[j];
-    if (has_color(H, j)) {
-        // head: sigmoid' (src/mlp.cpp:174-176)
+    float d3[3] = {0.f, 0.f, 0.f};
+    if (has_color(H, j))
         for (int o = 0; o < 3; ++o) {
             const float a = H.rgb[o * N + j];
-            Dl[(D_C3 + o) * N] = __fmul_rn(__fmul_rn(H.drgb[o * N + j], a), __fsub_rn(1.0f, a));
+            d3[o] = H.drgb[o * N + j] * a * (1.0f - a);
         }
-        back_matvec<3>(M.mc + D::C_W3, kHid, Dl + D_C3 * N, N, X + A_H3 * N, N, Dl + D_C2 * N);
-        back_matvec<kHid>(M.mc + D::C_W2, kHid, Dl + D_C2 * N, N, X + A_H2 * N, N, Dl + D_C1 * N);
-        back_matvec<kHid>(M.mc + D::C_W1, kHid, Dl + D_C1 * N, N, X + A_H1 * N, N, Dl + D_C0 * N);
-        // d input of f_C: only the 32 colour-feature rows are needed (the r6 part has no parameters)
+#pragma unroll
+    for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * N] = d3[o];
+    const float* h3 = H.acts + A_H3 * N + j;
+#pragma unroll 4
+    for (int k = 0; k < kHid; ++k) {
+        float v = 0.f;
+        if (h3[k * N] > 0.f) {
+            v = __ldg(M.mc + D::C_W3 + k) * d3[0];
+            v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
+            v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
+        }
+        Dl[(D_C2 + k) * N] = v;
+    }
+}
+
+// D *= relu'(H) over a rows x N block
+__global__ void k_relu_mask(float* __restrict__ Dm, const float* __restrict__ Hm, size_t count) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x)
+        if (!(Hm[i] > 0.f)) Dm[i] = 0.f;
+}
+
+// Colour-feature gradient scatter (unless frozen) and the positional
+// Jacobian into eta (src/train.cpp:244-265), then the f_T heads' deltas and
+// their 2 -> 128 back-projection masked by relu'(h_T).
+__global__ void __launch_bounds__(128) k_bwd_feat_c(DevOctree T, DevModel M, HitArgs H, const float* __restrict__ dX,
+                                                    bool color_frozen, float* g_fc, int* err) {
+    using D = DecOffsets;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= H.N) return;
+    const size_t N = H.N;
+    double deta = H.deta[j];
+    HitGeom g;
+    if (has_color(H, j) && hit_geom(T, H, j, g, err)) {
         float dz[kFc];
-        {
-            float tmp[kInC];
-#pragma unroll 1
-            for (int k = 0; k < kInC; ++k) tmp[k] = 0.f;
-            for (int o = 0; o < kHid; ++o) {
-                const float dv = Dl[(D_C0 + o) * N];
-                const float* wr = M.mc + D::C_W0 + size_t(o) * kInC;
 #pragma unroll
-                for (int k = 0; k < kInC; ++k) tmp[k] = __fadd_rn(tmp[k], __fmul_rn(__ldg(wr + k), dv));
-            }
-#pragma unroll
-            for (int d = 0; d < kFc; ++d) dz[d] = tmp[6 + d];
-        }
+        for (int d = 0; d < kFc; ++d) dz[d] = dX[(6 + d) * N + j];
         double xs[3], u[3];
         if (!xs_coords(T, g, H.eta[j], xs, u)) {
             raise_error(err, kErrPointNotInVoxel);
-            return;
-        }
-        if (!color_frozen) {  // src/train.cpp:244-253
-            float ws[8];
-            weights_from_u(u, ws);
-            for (int b = 0; b < 8; ++b) {
-                float* grow = g_fc + size_t(g.corners[b]) * kFc;
+        } else {
+            if (!color_frozen) {
+                float ws[8];
+                weights_from_u(u, ws);
+                for (int b = 0; b < 8; ++b) {
+                    float* grow = g_fc + size_t(g.corners[b]) * kFc;
 #pragma unroll 4
-                for (int d = 0; d < kFc; ++d) atomicAdd(grow + d, __fmul_rn(ws[b], dz[d]));
+                    for (int d = 0; d < kFc; ++d) atomicAdd(grow + d, ws[b] * dz[d]);
+                }
             }
-        }
-        // d eta via x_s: dx_s = sum_b dw_b/du <z_b, dz> / h (src/train.cpp:254-265)
-        const double inv_h = ddiv(1.0, T.cell_size);
-        const double wxv[2] = {dsub(1.0, u[0]), u[0]}, wyv[2] = {dsub(1.0, u[1]), u[1]},
-                     wzv[2] = {dsub(1.0, u[2]), u[2]}, dxv[2] = {-1.0, 1.0};
-        double dxs[3] = {0.0, 0.0, 0.0};
-        for (int b = 0; b < 8; ++b) {
-            const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
-            const double gw[3] = {dmul(dmul(dxv[bx], wyv[by]), wzv[bz]), dmul(dmul(wxv[bx], dxv[by]), wzv[bz]),
-                                  dmul(dmul(wxv[bx], wyv[by]), dxv[bz])};
-            const float* zb = M.fc + size_t(g.corners[b]) * kFc;
-            double dotv = 0.0;
-            for (int d = 0; d < kFc; ++d) dotv = dadd(dotv, dmul(double(__ldg(zb + d)), double(dz[d])));
-            const double sc = dmul(dotv, inv_h);
+            // dx_s = sum_b dw_b/du <z_b, dz> / h; d eta += <dx_s, x1 - x2>
+            const double inv_h = ddiv(1.0, T.cell_size);
+            const double wxv[2] = {dsub(1.0, u[0]), u[0]}, wyv[2] = {dsub(1.0, u[1]), u[1]},
+                         wzv[2] = {dsub(1.0, u[2]), u[2]}, dxv[2] = {-1.0, 1.0};
+            double dxs[3] = {0.0, 0.0, 0.0};
+            for (int b = 0; b < 8; ++b) {
+                const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
+                const double gw[3] = {dmul(dmul(dxv[bx], wyv[by]), wzv[bz]), dmul(dmul(wxv[bx], dxv[by]), wzv[bz]),
+                                      dmul(dmul(wxv[bx], wyv[by]), dxv[bz])};
+                const float4* zb = reinterpret_cast<const float4*>(M.fc + size_t(g.corners[b]) * kFc);
+                double dotv = 0.0;
 #pragma unroll
-            for (int a = 0; a < 3; ++a) dxs[a] = dadd(dxs[a], dmul(gw[a], sc));
+                for (int d4 = 0; d4 < kFc / 4; ++d4) {
+                    const float4 z = __ldg(zb + d4);
+                    dotv = dadd(dotv, dmul(double(z.x), double(dz[4 * d4])));
+                    dotv = dadd(dotv, dmul(double(z.y), double(dz[4 * d4 + 1])));
+                    dotv = dadd(dotv, dmul(double(z.z), double(dz[4 * d4 + 2])));
+                    dotv = dadd(dotv, dmul(double(z.w), double(dz[4 * d4 + 3])));
+                }
+                const double sc = dmul(dotv, inv_h);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) dxs[a] = dadd(dxs[a], dmul(gw[a], sc));
+            }
+            const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
+            deta = dadd(deta, dot3(dxs, dx12));
         }
-        const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
-        deta = dadd(deta, dot3(dxs, dx12));
     }
-    // f_T: heads relu (tau) and sigmoid (eta)
-    const float dt = float(H.dtau[j]), de = float(deta);
+    // f_T heads: relu (tau), sigmoid (eta)
+    float* Dl = H.deltas + j;
     const float tau = H.tau[j], eta = H.eta[j];
-    Dl[D_T1 * N] = tau > 0.f ? dt : 0.f;
-    Dl[(D_T1 + 1) * N] = __fmul_rn(__fmul_rn(de, eta), __fsub_rn(1.0f, eta));
-    back_matvec<2>(M.mt + D::T_W1, kHid, Dl + D_T1 * N, N, X + A_HT * N, N, Dl + D_T0 * N);
-    // d input of f_T, feature rows only: dz1 = rows 6..69, dz2 = rows 70..133
+    const float d0 = tau > 0.f ? float(H.dtau[j]) : 0.f;
+    const float d1 = float(deta) * eta * (1.0f - eta);
+    Dl[D_T1 * N] = d0;
+    Dl[(D_T1 + 1) * N] = d1;
+    const float* ht = H.acts + A_HT * N + j;
+#pragma unroll 4
+    for (int k = 0; k < kHid; ++k) {
+        float v = 0.f;
+        if (ht[k * N] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
+        Dl[(D_T0 + k) * N] = v;
+    }
+}
+
+// Thickness-feature gradient scatter: g[corner_b] += w1_b dz1 + w2_b dz2
+// (dz1, dz2 = rows 6..69 and 70..133 of dX_T).
+__global__ void __launch_bounds__(128) k_bwd_feat_t(DevOctree T, HitArgs H, const float* __restrict__ dX, float* g_ft,
+                                                    int* err) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= H.N) return;
+    const size_t N = H.N;
+    HitGeom g;
+    if (!hit_geom(T, H, j, g, err)) return;
 #pragma unroll 1
-    for (int k0 = 6; k0 < kInT; k0 += 16) {
-        float acc[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-        for (int o = 0; o < kHid; ++o) {
-            const float dv = Dl[(D_T0 + o) * N];
-            const float* wr = M.mt + D::T_W0 + size_t(o) * kInT + k0;
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-                if (k0 + i < kInT) acc[i] = __fadd_rn(acc[i], __fmul_rn(__ldg(wr + i), dv));
-        }
-        // scatter: grow[d] += w1_b * dz1[d] + w2_b * dz2[d]; chunks cover both halves
+    for (int d0 = 0; d0 < kFt; d0 += 16) {
+        float z1[16], z2[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const int k = k0 + i;
-            if (k >= kInT) break;
-            const bool first = k < 6 + kFt;
-            const int d = first ? k - 6 : k - 6 - kFt;
-            for (int b = 0; b < 8; ++b)
-                atomicAdd(g_ft + size_t(g.corners[b]) * kFt + d, __fmul_rn(first ? g.w1[b] : g.w2[b], acc[i]));
+            z1[i] = dX[(6 + d0 + i) * N + j];
+            z2[i] = dX[(6 + kFt + d0 + i) * N + j];
+        }
+        for (int b = 0; b < 8; ++b) {
+            float* grow = g_ft + size_t(g.corners[b]) * kFt + d0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) atomicAdd(grow + i, fmaf(g.w1[b], z1[i], g.w2[b] * z2[i]));
         }
     }
 }
 
-// dW[o][k] += sum_j D[o][j] X[k][j] (split over hits), db[o] += sum_j D[o][j]
-__global__ void __launch_bounds__(256) k_gemm_dw(const float* __restrict__ Dm, int O, const float* __restrict__ Xm,
-                                                 int K, size_t N, size_t chunk, float* dW, float* db) {
-    __shared__ float Ds[32][33], Xs[32][33];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int o0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
-    const size_t j0 = size_t(blockIdx.z) * chunk, j1 = min(N, j0 + chunk);
-    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, bacc[2] = {0.f, 0.f};
-    for (size_t jb = j0; jb < j1; jb += 32) {
-        for (int t = threadIdx.x; t < 32 * 32; t += 256) {
-            const int rr = t >> 5, cc = t & 31;
-            const size_t jj = jb + cc;
-            Ds[rr][cc] = (o0 + rr < O && jj < j1) ? Dm[size_t(o0 + rr) * N + jj] : 0.f;
-            Xs[rr][cc] = (k0 + rr < K && jj < j1) ? Xm[size_t(k0 + rr) * N + jj] : 0.f;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int c = 0; c < 32; ++c) {
-            const float d0 = Ds[ty * 2][c], d1 = Ds[ty * 2 + 1][c];
-            const float x0 = Xs[tx * 2][c], x1 = Xs[tx * 2 + 1][c];
-            acc[0][0] += d0 * x0;
-            acc[0][1] += d0 * x1;
-            acc[1][0] += d1 * x0;
-            acc[1][1] += d1 * x1;
-            if (tx == 0) {
-                bacc[0] += d0;
-                bacc[1] += d1;
-            }
-        }
-        __syncthreads();
-    }
-    for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b) {
-            const int o = o0 + ty * 2 + a, k = k0 + tx * 2 + b;
-            if (o < O && k < K) atomicAdd(dW + size_t(o) * K + k, acc[a][b]);
-        }
-    if (tx == 0 && blockIdx.y == 0 && db)
-        for (int a = 0; a < 2; ++a)
-            if (o0 + ty * 2 + a < O) atomicAdd(db + o0 + ty * 2 + a, bacc[a]);
+__global__ void k_fill(float* p, float v, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = v;
 }
 
 // rows (vertices) whose features any active hit touches
@@ -593,6 +615,7 @@ __global__ void k_adam(AdamSegs S, float lr) {
 }  // namespace
 
 TrainScratch::~TrainScratch() {
+    if (blas) cublas_api().Destroy(static_cast<cublasHandle_t>(blas));
     if (h_pinned) cudaFreeHost(h_pinned);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
@@ -648,16 +671,63 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     float* deltas = S.deltas.ensure<float>(size_t(D_ROWS) * N + 1);
     SVLF_CUDA(cudaMemsetAsync(hitd, 0, size_t(N) * 2 * 8, s));                 // dtau, deta
     SVLF_CUDA(cudaMemsetAsync(hitf + size_t(N) * 5, 0, size_t(N) * 3 * 4, s));  // drgb
-    if (N) {
-        SVLF_CUDA(cudaMemsetAsync(acts, 0, size_t(A_ROWS) * N * 4, s));
-        SVLF_CUDA(cudaMemsetAsync(deltas, 0, size_t(D_ROWS) * N * 4, s));
-    }
+    float* dxs = S.dxs.ensure<float>(size_t(kInT) * N + 1);                     // dL/d layer-0 inputs
     if (n) k_expand<<<(n + 127) / 128, 128, 0, s>>>(n, act_first, act_cnt, dpos, dhit, dray);
+
+    // Dense layers as fp32 GEMMs on the feature-major matrices. A feature-major
+    // R x N block is the column-major N x R matrix (ld N); a row-major [O][K]
+    // weight is the column-major K x O matrix (ld K).
+    if (!S.blas) {
+        const CublasApi& B = cublas_api();
+        cublasHandle_t hb = nullptr;
+        cublas_check(B.Create(&hb), "cublasCreate");
+        cublas_check(B.SetMathMode(hb, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true fp32, no TF32
+        S.blas = hb;
+    }
+    const CublasApi& B = cublas_api();
+    cublasHandle_t hb = static_cast<cublasHandle_t>(S.blas);
+    cublas_check(B.SetStream(hb, s), "cublasSetStream");
+    const float one = 1.f, zero = 0.f;
+    const int Ni = int(N);
+    // Y(O x N) = W X: rows [xrow, xrow+K) -> [yrow, yrow+O) of acts
+    auto layer_fwd = [&](const float* W, int O, int K, int xrow, int yrow, const float* bias) {
+        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Ni, O, K, &one, acts + size_t(xrow) * N, Ni, W, K, &zero,
+                             acts + size_t(yrow) * N, Ni),
+                     "sgemm fwd");
+        k_bias_relu<<<dim3(unsigned(std::min<size_t>((N + 255) / 256, 1184)), unsigned(O)), 256, 0, s>>>(
+            acts + size_t(yrow) * N, bias, N);
+    };
+    // dX rows [k0, K) (x N) = W^T D, D = delta rows [drow, drow+O)
+    auto layer_bwd = [&](const float* W, int O, int K, int k0, int drow, float* dst) {
+        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, Ni, K - k0, O, &one, deltas + size_t(drow) * N, Ni, W + k0,
+                             K, &zero, dst, Ni),
+                     "sgemm bwd");
+    };
+    // dW(O x K) = D X^T, db = D 1
+    float* ones = S.ones.ensure<float>(size_t(N) + 1);
+    auto layer_dw = [&](int drow, int O, int xrow, int K, float* dW, float* db) {
+        cublas_check(B.Sgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, K, O, Ni, &one, acts + size_t(xrow) * N, Ni,
+                             deltas + size_t(drow) * N, Ni, &zero, dW, K),
+                     "sgemm dW");
+        cublas_check(B.Sgemv(hb, CUBLAS_OP_T, Ni, O, &one, deltas + size_t(drow) * N, Ni, ones, 1, &zero, db, 1),
+                     "sgemv db");
+    };
+    const unsigned hit_blocks = (N + 127) / 128;
 
     HitArgs H{b.rays, b.hit_leaf, b.hit_tin, b.hit_tout, dhit, dray, dpos, surf_rel, N, o.surface, acts, deltas,
               hitf, hitf + N, hitf + 2 * size_t(N), hitf + 5 * size_t(N), hitd, hitd + N};
     SVLF_CUDA(cudaEventRecord(S.ev[1], s));
-    if (N) k_fwd<<<(N + 127) / 128, 128, 0, s>>>(T, M.view, M.pack, H, err_flag);
+    if (N) {
+        k_fill<<<std::min<unsigned>(hit_blocks, 1184), 128, 0, s>>>(ones, 1.f, N);
+        k_fwd_in_t<<<hit_blocks, 128, 0, s>>>(T, M.view, H, err_flag);
+        layer_fwd(M.view.mt + D::T_W0, kHid, kInT, A_XT, A_HT, M.view.mt + D::T_B0);
+        k_fwd_mid<<<hit_blocks, 128, 0, s>>>(T, M.view, H, err_flag);
+        layer_fwd(M.view.mc + D::C_W0, kHid, kInC, A_XC, A_H1, M.view.mc + D::C_B0);
+        layer_fwd(M.view.mc + D::C_W1, kHid, kHid, A_H1, A_H2, M.view.mc + D::C_B1);
+        layer_fwd(M.view.mc + D::C_W2, kHid, kHid, A_H2, A_H3, M.view.mc + D::C_B2);
+        k_fwd_rgb<<<hit_blocks, 128, 0, s>>>(M.view, H);
+        note_launch(9);
+    }
     SVLF_CUDA(cudaEventRecord(S.ev[2], s));
     LossArgs L{b.c_gt, b.alpha_gt, dpos, act_cnt, surf_rel, eta_gt, b.hit_tin, n, o.surface, o.lw, ray_loss,
                hitd + 2 * size_t(N), hitd + 3 * size_t(N), hitd + 4 * size_t(N)};
@@ -677,22 +747,28 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     float* g_mt = g_fc + M.n_fc;
     float* g_mc = g_mt + SVLF_DEC_T_SIZE;
     if (N) {
-        k_bwd<<<(N + 127) / 128, 128, 0, s>>>(T, M.view, H, o.color_frozen, g_ft, g_fc, err_flag);
-        const size_t chunk = std::max<size_t>(2048, (size_t(N) + 63) / 64);
-        const unsigned gz = unsigned((N + chunk - 1) / chunk);
-        auto gemm = [&](int drow, int O, int arow, int K, float* dW, float* db) {
-            dim3 grid((O + 31) / 32, (K + 31) / 32, gz);
-            k_gemm_dw<<<grid, 256, 0, s>>>(deltas + size_t(drow) * N, O, acts + size_t(arow) * N, K, N, chunk, dW, db);
-        };
-        gemm(D_T0, kHid, A_XT, kInT, g_mt + D::T_W0, g_mt + D::T_B0);
-        gemm(D_T1, 2, A_HT, kHid, g_mt + D::T_W1, g_mt + D::T_B1);
+        const unsigned mask_blocks = unsigned(std::min<size_t>((size_t(kHid) * N + 255) / 256, 4736));
+        // f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
+        k_bwd_head_c<<<hit_blocks, 128, 0, s>>>(M.view, H);
+        layer_bwd(M.view.mc + D::C_W2, kHid, kHid, 0, D_C2, deltas + size_t(D_C1) * N);
+        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C1) * N, acts + size_t(A_H2) * N, size_t(kHid) * N);
+        layer_bwd(M.view.mc + D::C_W1, kHid, kHid, 0, D_C1, deltas + size_t(D_C0) * N);
+        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C0) * N, acts + size_t(A_H1) * N, size_t(kHid) * N);
+        layer_bwd(M.view.mc + D::C_W0, kHid, kInC, 6, D_C0, dxs + 6 * size_t(N));
+        // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
+        k_bwd_feat_c<<<hit_blocks, 128, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
+        layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(N));
+        k_bwd_feat_t<<<hit_blocks, 128, 0, s>>>(T, H, dxs, g_ft, err_flag);
+        // weight gradients (sums over hits)
+        layer_dw(D_T0, kHid, A_XT, kInT, g_mt + D::T_W0, g_mt + D::T_B0);
+        layer_dw(D_T1, 2, A_HT, kHid, g_mt + D::T_W1, g_mt + D::T_B1);
         if (!o.color_frozen) {
-            gemm(D_C0, kHid, A_XC, kInC, g_mc + D::C_W0, g_mc + D::C_B0);
-            gemm(D_C1, kHid, A_H1, kHid, g_mc + D::C_W1, g_mc + D::C_B1);
-            gemm(D_C2, kHid, A_H2, kHid, g_mc + D::C_W2, g_mc + D::C_B2);
-            gemm(D_C3, 3, A_H3, kHid, g_mc + D::C_W3, g_mc + D::C_B3);
+            layer_dw(D_C0, kHid, A_XC, kInC, g_mc + D::C_W0, g_mc + D::C_B0);
+            layer_dw(D_C1, kHid, A_H1, kHid, g_mc + D::C_W1, g_mc + D::C_B1);
+            layer_dw(D_C2, kHid, A_H2, kHid, g_mc + D::C_W2, g_mc + D::C_B2);
+            layer_dw(D_C3, 3, A_H3, kHid, g_mc + D::C_W3, g_mc + D::C_B3);
         }
-        note_launch(o.color_frozen ? 3 : 7);
+        note_launch(6);
     }
     // ---- data parallel: all-reduce loss, statistics and gradients (NCCL)
     if (o.nccl_comm) {

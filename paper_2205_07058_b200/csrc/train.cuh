@@ -57,6 +57,8 @@ struct TrainScratch {
     DevBuf acts, deltas;                                          // feature-major scratch
     DevBuf scan_tmp, counters, loss_out;
     DevBuf touched, rows, n_rows, packed, red;  // sparse feature-gradient exchange
+    DevBuf dxs, ones;                           // layer-0 input gradients, ones vector (bias sums)
+    void* blas = nullptr;                       // cublasHandle_t (fp32 dense-layer GEMMs)
     int* h_pinned = nullptr;
     cudaEvent_t ev[8] = {};
     ~TrainScratch();

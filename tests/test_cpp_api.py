@@ -8,7 +8,7 @@
 * tests/cpp/cpp_api_probe.cpp drives the API like a reference call site
   (init_model, render_frame / render_frame_ref, loss_grads, train_step,
   checkpoints, DeviceModel); its outputs are compared with the oracle here.
-  Tolerances as elsewhere: fp32 render max-abs <= 1e-3, loss rel 1e-9,
+  Tolerances as elsewhere: fp32 render max-abs <= 1e-3, loss rel 1e-6,
   gradients rel-L2 <= 1e-4 per tensor.
 * Checkpoints are the reference container byte for byte: the reference
   (oracle/_ref) loads our file and writes back identical bytes.
@@ -120,7 +120,7 @@ def test_cpp_train_matches_oracle(tmp_path, oracle):
     assert alpha.sum() > 50, out
     loss, g, st = oracle.loss(t, m, rays, cgt, depth, alpha, 1)
     losses = _load(tmp_path, "losses.f64", np.float64)
-    assert abs(losses[0] - loss) <= 1e-9 * abs(loss)
+    assert abs(losses[0] - loss) <= 1e-6 * abs(loss)
     assert losses[1] == pytest.approx(losses[0], rel=1e-12)  # first step evaluates the same model
     assert losses[2] < losses[1]
     assert _load(tmp_path, "loss_stats.i64", np.int64).tolist() == list(st)
