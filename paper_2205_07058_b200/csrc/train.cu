@@ -456,61 +456,100 @@ __global__ void k_relu_mask(float* __restrict__ Dm, const float* __restrict__ Hm
         if (!(Hm[i] > 0.f)) Dm[i] = 0.f;
 }
 
+// The two feature-gradient kernels below are warp-cooperative: a warp owns 32
+// consecutive hits. Per-hit geometry runs lane = hit; the hits' input
+// gradients are staged transposed in shared memory (coalesced row loads), and
+// each hit's scatter is issued by the whole warp as 16-byte vector atomics
+// over contiguous feature rows (8 lanes per 32-float row segment).
+constexpr int kScWarps = 4;
+
 // Colour-feature gradient scatter (unless frozen) and the positional
 // Jacobian into eta (src/train.cpp:244-265), then the f_T heads' deltas and
 // their 2 -> 128 back-projection masked by relu'(h_T).
-__global__ void __launch_bounds__(128) k_bwd_feat_c(DevOctree T, DevModel M, HitArgs H, const float* __restrict__ dX,
-                                                    bool color_frozen, float* g_fc, int* err) {
+__global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevModel M, HitArgs H,
+                                                               const float* __restrict__ dX, bool color_frozen,
+                                                               float* g_fc, int* err) {
     using D = DecOffsets;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= H.N) return;
+    __shared__ float zs[kScWarps][kFc][33];
+    __shared__ uint32_t cs[kScWarps][32][8];
+    __shared__ float ws_s[kScWarps][32][8];
+    __shared__ double dots[kScWarps][32][8];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
-    double deta = H.deta[j];
+    const uint32_t j0 = (blockIdx.x * kScWarps + warp) * 32;
+    if (j0 >= N) return;
+    const uint32_t j = j0 + lane;
+    const bool valid = j < N;
     HitGeom g;
-    if (has_color(H, j) && hit_geom(T, H, j, g, err)) {
-        float dz[kFc];
-#pragma unroll
-        for (int d = 0; d < kFc; ++d) dz[d] = dX[(6 + d) * N + j];
-        double xs[3], u[3];
+    double u[3] = {0.0, 0.0, 0.0};
+    bool act = valid && has_color(H, j) && hit_geom(T, H, j, g, err);
+    if (act) {
+        double xs[3];
         if (!xs_coords(T, g, H.eta[j], xs, u)) {
             raise_error(err, kErrPointNotInVoxel);
-        } else {
-            if (!color_frozen) {
-                float ws[8];
-                weights_from_u(u, ws);
-                for (int b = 0; b < 8; ++b) {
-                    float* grow = g_fc + size_t(g.corners[b]) * kFc;
-#pragma unroll 4
-                    for (int d = 0; d < kFc; ++d) atomicAdd(grow + d, ws[b] * dz[d]);
-                }
-            }
-            // dx_s = sum_b dw_b/du <z_b, dz> / h; d eta += <dx_s, x1 - x2>
-            const double inv_h = ddiv(1.0, T.cell_size);
-            const double wxv[2] = {dsub(1.0, u[0]), u[0]}, wyv[2] = {dsub(1.0, u[1]), u[1]},
-                         wzv[2] = {dsub(1.0, u[2]), u[2]}, dxv[2] = {-1.0, 1.0};
-            double dxs[3] = {0.0, 0.0, 0.0};
-            for (int b = 0; b < 8; ++b) {
-                const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
-                const double gw[3] = {dmul(dmul(dxv[bx], wyv[by]), wzv[bz]), dmul(dmul(wxv[bx], dxv[by]), wzv[bz]),
-                                      dmul(dmul(wxv[bx], wyv[by]), dxv[bz])};
-                const float4* zb = reinterpret_cast<const float4*>(M.fc + size_t(g.corners[b]) * kFc);
-                double dotv = 0.0;
-#pragma unroll
-                for (int d4 = 0; d4 < kFc / 4; ++d4) {
-                    const float4 z = __ldg(zb + d4);
-                    dotv = dadd(dotv, dmul(double(z.x), double(dz[4 * d4])));
-                    dotv = dadd(dotv, dmul(double(z.y), double(dz[4 * d4 + 1])));
-                    dotv = dadd(dotv, dmul(double(z.z), double(dz[4 * d4 + 2])));
-                    dotv = dadd(dotv, dmul(double(z.w), double(dz[4 * d4 + 3])));
-                }
-                const double sc = dmul(dotv, inv_h);
-#pragma unroll
-                for (int a = 0; a < 3; ++a) dxs[a] = dadd(dxs[a], dmul(gw[a], sc));
-            }
-            const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
-            deta = dadd(deta, dot3(dxs, dx12));
+            act = false;
         }
     }
+    {
+        float ws[8];
+        if (act) weights_from_u(u, ws);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            cs[warp][lane][b] = act ? g.corners[b] : 0u;
+            ws_s[warp][lane][b] = act ? ws[b] : 0.f;
+        }
+    }
+#pragma unroll 4
+    for (int d = 0; d < kFc; ++d) zs[warp][d][lane] = act ? dX[(6 + d) * N + j] : 0.f;
+    __syncwarp();
+    unsigned live = __ballot_sync(0xffffffffu, act);
+    // scatter + <z_b, dz> per corner, hit by hit
+    const uint32_t grp = lane >> 3, f4 = (lane & 7) * 4;   // scatter: corner grp (+4), features f4..f4+3
+    const uint32_t cb = lane >> 2, ck = (lane & 3) * 8;    // dots: corner cb, features ck..ck+7
+    while (live) {
+        const int h = __ffs(live) - 1;
+        live &= live - 1;
+        if (!color_frozen) {
+#pragma unroll
+            for (int bp = 0; bp < 2; ++bp) {
+                const uint32_t b = grp + 4 * bp;
+                const float w = ws_s[warp][h][b];
+                const float4 v = make_float4(w * zs[warp][f4][h], w * zs[warp][f4 + 1][h], w * zs[warp][f4 + 2][h],
+                                             w * zs[warp][f4 + 3][h]);
+                atomicAdd(reinterpret_cast<float4*>(g_fc + size_t(cs[warp][h][b]) * kFc + f4), v);
+            }
+        }
+        const float4* zb = reinterpret_cast<const float4*>(M.fc + size_t(cs[warp][h][cb]) * kFc + ck);
+        const float4 za = __ldg(zb), zc = __ldg(zb + 1);
+        const float zv[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
+        double part = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) part = dadd(part, dmul(double(zv[i]), double(zs[warp][ck + i][h])));
+        part = dadd(part, __shfl_xor_sync(0xffffffffu, part, 1));
+        part = dadd(part, __shfl_xor_sync(0xffffffffu, part, 2));
+        if ((lane & 3) == 0) dots[warp][h][cb] = part;
+    }
+    __syncwarp();
+    double deta = valid ? H.deta[j] : 0.0;
+    if (act) {
+        // dx_s = sum_b dw_b/du <z_b, dz> / h; d eta += <dx_s, x1 - x2>
+        const double inv_h = ddiv(1.0, T.cell_size);
+        const double wxv[2] = {dsub(1.0, u[0]), u[0]}, wyv[2] = {dsub(1.0, u[1]), u[1]},
+                     wzv[2] = {dsub(1.0, u[2]), u[2]}, dxv[2] = {-1.0, 1.0};
+        double dxs[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
+            const double gw[3] = {dmul(dmul(dxv[bx], wyv[by]), wzv[bz]), dmul(dmul(wxv[bx], dxv[by]), wzv[bz]),
+                                  dmul(dmul(wxv[bx], wyv[by]), dxv[bz])};
+            const double sc = dmul(dots[warp][lane][b], inv_h);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) dxs[a] = dadd(dxs[a], dmul(gw[a], sc));
+        }
+        const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
+        deta = dadd(deta, dot3(dxs, dx12));
+    }
+    if (!valid) return;
     // f_T heads: relu (tau), sigmoid (eta)
     float* Dl = H.deltas + j;
     const float tau = H.tau[j], eta = H.eta[j];
@@ -528,26 +567,51 @@ __global__ void __launch_bounds__(128) k_bwd_feat_c(DevOctree T, DevModel M, Hit
 }
 
 // Thickness-feature gradient scatter: g[corner_b] += w1_b dz1 + w2_b dz2
-// (dz1, dz2 = rows 6..69 and 70..133 of dX_T).
-__global__ void __launch_bounds__(128) k_bwd_feat_t(DevOctree T, HitArgs H, const float* __restrict__ dX, float* g_ft,
-                                                    int* err) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= H.N) return;
+// (dz1, dz2 = rows 6..69 and 70..133 of dX_T), in two 32-feature halves.
+__global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_t(DevOctree T, HitArgs H, const float* __restrict__ dX,
+                                                               float* g_ft, int* err) {
+    __shared__ float zs[kScWarps][64][33];
+    __shared__ uint32_t cs[kScWarps][32][8];
+    __shared__ float w1s[kScWarps][32][8], w2s[kScWarps][32][8];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
+    const uint32_t j0 = (blockIdx.x * kScWarps + warp) * 32;
+    if (j0 >= N) return;
+    const uint32_t j = j0 + lane;
     HitGeom g;
-    if (!hit_geom(T, H, j, g, err)) return;
+    const bool act = j < N && hit_geom(T, H, j, g, err);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        cs[warp][lane][b] = act ? g.corners[b] : 0u;
+        w1s[warp][lane][b] = act ? g.w1[b] : 0.f;
+        w2s[warp][lane][b] = act ? g.w2[b] : 0.f;
+    }
+    const unsigned live0 = __ballot_sync(0xffffffffu, act);
+    const uint32_t grp = lane >> 3, f4 = (lane & 7) * 4;
 #pragma unroll 1
-    for (int d0 = 0; d0 < kFt; d0 += 16) {
-        float z1[16], z2[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            z1[i] = dX[(6 + d0 + i) * N + j];
-            z2[i] = dX[(6 + kFt + d0 + i) * N + j];
+    for (int half = 0; half < 2; ++half) {
+        __syncwarp();
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            zs[warp][r][lane] = act ? dX[(6 + 32 * half + r) * N + j] : 0.f;
+            zs[warp][32 + r][lane] = act ? dX[(6 + kFt + 32 * half + r) * N + j] : 0.f;
         }
-        for (int b = 0; b < 8; ++b) {
-            float* grow = g_ft + size_t(g.corners[b]) * kFt + d0;
+        __syncwarp();
+        unsigned live = live0;
+        while (live) {
+            const int h = __ffs(live) - 1;
+            live &= live - 1;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) atomicAdd(grow + i, fmaf(g.w1[b], z1[i], g.w2[b] * z2[i]));
+            for (int bp = 0; bp < 2; ++bp) {
+                const uint32_t b = grp + 4 * bp;
+                const float a1 = w1s[warp][h][b], a2 = w2s[warp][h][b];
+                float4 v;
+                v.x = fmaf(a1, zs[warp][f4][h], a2 * zs[warp][32 + f4][h]);
+                v.y = fmaf(a1, zs[warp][f4 + 1][h], a2 * zs[warp][32 + f4 + 1][h]);
+                v.z = fmaf(a1, zs[warp][f4 + 2][h], a2 * zs[warp][32 + f4 + 2][h]);
+                v.w = fmaf(a1, zs[warp][f4 + 3][h], a2 * zs[warp][32 + f4 + 3][h]);
+                atomicAdd(reinterpret_cast<float4*>(g_ft + size_t(cs[warp][h][b]) * kFt + 32 * half + f4), v);
+            }
         }
     }
 }
@@ -756,9 +820,10 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
         k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C0) * N, acts + size_t(A_H1) * N, size_t(kHid) * N);
         layer_bwd(M.view.mc + D::C_W0, kHid, kInC, 6, D_C0, dxs + 6 * size_t(N));
         // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
-        k_bwd_feat_c<<<hit_blocks, 128, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
+        const unsigned sc_blocks = unsigned((size_t(N) + 32 * kScWarps - 1) / (32 * kScWarps));
+        k_bwd_feat_c<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
         layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(N));
-        k_bwd_feat_t<<<hit_blocks, 128, 0, s>>>(T, H, dxs, g_ft, err_flag);
+        k_bwd_feat_t<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
         // weight gradients (sums over hits)
         layer_dw(D_T0, kHid, A_XT, kInT, g_mt + D::T_W0, g_mt + D::T_B0);
         layer_dw(D_T1, 2, A_HT, kHid, g_mt + D::T_W1, g_mt + D::T_B1);
