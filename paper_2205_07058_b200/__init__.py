@@ -154,7 +154,8 @@ _LIB = None
 
 
 def library_path() -> str:
-    return os.path.join(HERE, "libsvlf_b200.so")
+    # $SVLF_LIB_PATH: an alternative build of the same library (tuning experiments)
+    return os.environ.get("SVLF_LIB_PATH") or os.path.join(HERE, "libsvlf_b200.so")
 
 
 def _dp(a):

@@ -1,16 +1,17 @@
 // Tensor-core decoder (tcgen05, 16-bit operands, fp32 accumulation in TMEM).
 //
-// Three kernels per frame, all over the flat hit list:
-//   k_hit_geom  one thread per hit, fp64 (reference operand order):
-//               x1, x2, parameterize_ray (r6), local coords u1, u2 and
-//               trilinear weights w1, w2 -> a 48-byte 16-bit record + u1,u2.
-//               Raises "tangent ray" / "point not in voxel" like the reference.
-//   k_decode_t  f_T (src/voxel_batch.hpp:69-114): gather psi_T(x1), psi_T(x2)
-//               with packed 16-bit FMA, MMA 128x144x128, relu epilogue, head
-//               MMA 128x144x16 -> tau = relu, eta = sigmoid.
-//   k_decode_c  f_C (src/voxel_batch.hpp:119-142): u_s = eta u1 + (1-eta) u2,
-//               trilinear weights, gather psi_C(x_s), MMA 128x48x128, two
-//               hidden MMAs 128x128x128, head MMA 128x128x16 -> rgb sigmoid.
+// Two kernels per frame, both over the flat hit list:
+//   k_decode_t  per hit (thread = hit, fp64 in the reference's operand order):
+//               x1, x2, parameterize_ray (r6), trilinear weights w1, w2, local
+//               coordinates u1, u2 ("tangent ray" / "point not in voxel" raised
+//               like the reference); then f_T (src/voxel_batch.hpp:69-114):
+//               gather psi_T(x1), psi_T(x2) with packed 16-bit FMA, MMA
+//               128x144x128, relu epilogue, head MMA 128x144x16 -> tau = relu,
+//               eta = sigmoid; finally the f_C record of the hit: r6 and the
+//               trilinear weights at u_s = eta u1 + (1-eta) u2 (32 bytes).
+//   k_decode_c  f_C (src/voxel_batch.hpp:119-142): gather psi_C(x_s), MMA
+//               128x48x128, two hidden MMAs 128x128x128, head MMA 128x128x16
+//               -> rgb sigmoid.
 // Each decode kernel is persistent (one CTA per SM, 512 threads = four
 // independent 128-row slots; thread r of a slot owns hit r of the slot's
 // tile). A slot's chain is gather -> MMA -> epilogue -> MMA ...; four slots
@@ -181,28 +182,25 @@ __global__ void k_feat_cvt(const float* __restrict__ src, typename Fmt<kBF16>::H
     for (size_t k = i; k < i + 4 && k < n; ++k) dst[k] = F::cvt(src[k]);
 }
 
-// ---- per-hit geometry record
-// geo[j]: 3 x uint4 = r6 (6 x 16-bit) | w1 (8 x 16-bit) | w2 (8 x 16-bit) | 2 x pad
-// u12[j]: 2 x float4 = u1.xyz, u2.xyz, pad, pad
+// ---- per-hit geometry, fp64 in the reference's operand order, one thread per
+// hit: x1, x2, parameterize_ray (r6), trilinear weights w1, w2 (16-bit pairs)
+// and local coordinates u1, u2 (fp32, for x_s after the f_T pass). Raises
+// "tangent ray" / "point not in voxel" like the reference.
 template <bool kBF16>
-__device__ __forceinline__ void hit_geom_one(DevOctree T, const double* __restrict__ rays,
-                                             const uint32_t* __restrict__ hit_ray,
-                                             const uint32_t* __restrict__ hit_leaf,
-                                             const double* __restrict__ hit_tin,
-                                             const double* __restrict__ hit_tout, uint32_t j, uint4* geo,
-                                             float4* u12, int* err) {
+__device__ __forceinline__ void hit_geom_regs(const DevOctree& T, const double* __restrict__ rays, uint32_t ri,
+                                              uint32_t leaf, double tin, double tout, uint32_t* r6p, uint32_t* wp,
+                                              float* u, int* err) {
     using F = Fmt<kBF16>;
     Ray ray;
-    const uint32_t ri = hit_ray[j];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         ray.o[a] = rays[6 * size_t(ri) + a];
         ray.d[a] = rays[6 * size_t(ri) + 3 + a];
     }
     double lo[3], hi[3], x1[3], x2[3];
-    leaf_box(T, hit_leaf[j], lo, hi);
-    ray_at(ray, hit_tin[j], x1);
-    ray_at(ray, hit_tout[j], x2);
+    leaf_box(T, leaf, lo, hi);
+    ray_at(ray, tin, x1);
+    ray_at(ray, tout, x2);
     float r6[6] = {0, 0, 0, 0, 0, 0}, w1[8], w2[8];
     if (!parameterize(ray, lo, hi, r6)) raise_error(err, kErrTangentRay);
     if (!trilinear_at(x1, lo, hi, T.cell_size, w1) || !trilinear_at(x2, lo, hi, T.cell_size, w2)) {
@@ -210,36 +208,23 @@ __device__ __forceinline__ void hit_geom_one(DevOctree T, const double* __restri
 #pragma unroll
         for (int b = 0; b < 8; ++b) w1[b] = w2[b] = 0.f;
     }
-    float u[6];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         // local coordinates (p - lo)/h clamped to [0,1] (features.cpp:22-31)
         u[a] = float(fmin(fmax(ddiv(dsub(x1[a], lo[a]), T.cell_size), 0.0), 1.0));
         u[3 + a] = float(fmin(fmax(ddiv(dsub(x2[a], lo[a]), T.cell_size), 0.0), 1.0));
     }
-    geo[3 * size_t(j)] = make_uint4(F::pack(r6[0], r6[1]), F::pack(r6[2], r6[3]), F::pack(r6[4], r6[5]),
-                                    F::pack(w1[0], w1[1]));
-    geo[3 * size_t(j) + 1] = make_uint4(F::pack(w1[2], w1[3]), F::pack(w1[4], w1[5]), F::pack(w1[6], w1[7]),
-                                        F::pack(w2[0], w2[1]));
-    geo[3 * size_t(j) + 2] = make_uint4(F::pack(w2[2], w2[3]), F::pack(w2[4], w2[5]), F::pack(w2[6], w2[7]), 0u);
-    u12[2 * size_t(j)] = make_float4(u[0], u[1], u[2], u[3]);
-    u12[2 * size_t(j) + 1] = make_float4(u[4], u[5], 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r6p[i] = F::pack(r6[2 * i], r6[2 * i + 1]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        wp[i] = F::pack(w1[2 * i], w1[2 * i + 1]);
+        wp[4 + i] = F::pack(w2[2 * i], w2[2 * i + 1]);
+    }
 }
 
 // D[tmem] (+)= A . B^T over K: A in the skewed activation layout (a_off),
 // B (weights, N rows) in the dense layout core_offset(n, k, K).
-template <bool kBF16>
-__global__ void __launch_bounds__(128) k_hit_geom(DevOctree T, const double* __restrict__ rays,
-                                                  const uint32_t* __restrict__ hit_ray,
-                                                  const uint32_t* __restrict__ hit_leaf,
-                                                  const double* __restrict__ hit_tin,
-                                                  const double* __restrict__ hit_tout, const uint32_t* n_dev,
-                                                  uint32_t cap, uint4* geo, float4* u12, int* err) {
-    using F = Fmt<kBF16>;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;  // grid covers the capacity; early exit
-    if (j < min(*n_dev, cap)) hit_geom_one<kBF16>(T, rays, hit_ray, hit_leaf, hit_tin, hit_tout, j, geo, u12, err);
-}
-
 __device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, uint32_t b_base, uint32_t K,
                                             uint32_t idesc) {
     const uint32_t b_sbo = (K / 8) * 128;
@@ -355,8 +340,10 @@ __device__ __forceinline__ void load_corners(const DevOctree& T, uint32_t leaf, 
 template <bool kBF16>
 __global__ void __launch_bounds__(512, 1)
     k_decode_t(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ ft16,
-               const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ geo, const uint32_t* n_dev,
-               uint32_t cap, HitOut out) {
+               const double* __restrict__ rays, const uint32_t* __restrict__ hit_ray,
+               const uint32_t* __restrict__ hit_leaf, const double* __restrict__ hit_tin,
+               const double* __restrict__ hit_tout, const uint32_t* n_dev, uint32_t cap, HitOut out,
+               uint4* __restrict__ crec, int* err) {
     using F = Fmt<kBF16>;
     using H2 = typename F::H2;
     constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
@@ -376,18 +363,17 @@ __global__ void __launch_bounds__(512, 1)
         const uint32_t j = tile * 128 + r;
         const bool valid = j < n;
         uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint4 g0 = make_uint4(0, 0, 0, 0), g1 = g0, g2 = g0;
+        uint32_t r6p[3] = {0, 0, 0}, wp[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // r6, (w1, w2) as 16-bit pairs
+        float u[6] = {0, 0, 0, 0, 0, 0};
         if (valid) {
-            load_corners(T, hit_leaf[j], corners);
-            g0 = geo[3 * size_t(j)];
-            g1 = geo[3 * size_t(j) + 1];
-            g2 = geo[3 * size_t(j) + 2];
+            const uint32_t leaf = hit_leaf[j];
+            load_corners(T, leaf, corners);
+            hit_geom_regs<kBF16>(T, rays, hit_ray[j], leaf, hit_tin[j], hit_tout[j], r6p, wp, u, err);
         }
         // Warp-cooperative gather: the warp owns rows 32w..32w+31 of the tile; in
         // pass p lanes 8q..8q+7 gather row 4p+q, lane chunk c = 8 features, so
         // one LDG.128 instruction covers 4 whole 128-byte feature rows.
         const uint32_t lane = r & 31, q = lane >> 3, ch = lane & 7, row0 = r & ~31u;
-        const uint32_t wp[8] = {g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z};  // w1, w2 as 16-bit pairs
 #pragma unroll 2
         for (uint32_t p = 0; p < 8; ++p) {
             const uint32_t src = 4 * p + q;
@@ -419,7 +405,7 @@ __global__ void __launch_bounds__(512, 1)
             st_shared_v4(a_base + a_off(row, 64 + 8 * ch), h2u(a2[0]), h2u(a2[1]), h2u(a2[2]),
                          h2u(a2[3]));
         }
-        st_shared_v4(a_base + a_off(r, 128), g0.x, g0.y, g0.z, F::kOne);
+        st_shared_v4(a_base + a_off(r, 128), r6p[0], r6p[1], r6p[2], F::kOne);
         st_shared_v4(a_base + a_off(r, 136), 0u, 0u, 0u, 0u);
 
         S.mma([&] { issue_layer(acc, a_base, sbase + OFF_WT0, KT, kIdesc); });
@@ -431,8 +417,20 @@ __global__ void __launch_bounds__(512, 1)
         tmem_ld16(acc + lane_off, hv);
         tmem_wait_ld();
         if (valid) {
+            const float e = __fdividef(1.0f, 1.0f + __expf(-hv[1])), ome = 1.0f - e;
             out.tau[j] = fmaxf(hv[0], 0.f);
-            out.eta[j] = __fdividef(1.0f, 1.0f + __expf(-hv[1]));
+            out.eta[j] = e;
+            // f_C record: r6 and the trilinear weights at x_s = eta x1 + (1-eta) x2,
+            // u_s = eta u1 + (1-eta) u2 (voxel_batch.hpp:111)
+            const float us[3] = {u[0] * e + u[3] * ome, u[1] * e + u[4] * ome, u[2] * e + u[5] * ome};
+            float ws[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                ws[b] = ((b & 1) ? us[0] : 1.f - us[0]) * ((b & 2) ? us[1] : 1.f - us[1]) *
+                        ((b & 4) ? us[2] : 1.f - us[2]);
+            crec[2 * size_t(j)] = make_uint4(r6p[0], r6p[1], r6p[2], 0u);
+            crec[2 * size_t(j) + 1] = make_uint4(F::pack(ws[0], ws[1]), F::pack(ws[2], ws[3]), F::pack(ws[4], ws[5]),
+                                                 F::pack(ws[6], ws[7]));
         }
         fence_before_sync();
     }
@@ -443,8 +441,8 @@ __global__ void __launch_bounds__(512, 1)
 template <bool kBF16>
 __global__ void __launch_bounds__(512, 1)
     k_decode_c(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ fc16,
-               const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ geo,
-               const float4* __restrict__ u12, const uint32_t* n_dev, uint32_t cap, HitOut out) {
+               const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ crec, const uint32_t* n_dev,
+               uint32_t cap, HitOut out) {
     using F = Fmt<kBF16>;
     using H2 = typename F::H2;
     constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
@@ -466,26 +464,16 @@ __global__ void __launch_bounds__(512, 1)
         const uint32_t j = tile * 128 + r;
         const bool valid = j < n;
         uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint4 g0 = make_uint4(0, 0, 0, 0);
-        float ws[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint4 g0 = make_uint4(0, 0, 0, 0), g1 = g0;
         if (valid) {
             load_corners(T, hit_leaf[j], corners);
-            g0 = geo[3 * size_t(j)];
-            const float4 ua = u12[2 * size_t(j)], ub = u12[2 * size_t(j) + 1];
-            const float e = out.eta[j], ome = 1.0f - e;
-            // u_s = (x_s - lo)/h with x_s = eta x1 + (1-eta) x2 (voxel_batch.hpp:111)
-            const float us[3] = {ua.x * e + ua.w * ome, ua.y * e + ub.x * ome, ua.z * e + ub.y * ome};
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-                ws[b] = ((b & 1) ? us[0] : 1.f - us[0]) * ((b & 2) ? us[1] : 1.f - us[1]) *
-                        ((b & 4) ? us[2] : 1.f - us[2]);
+            g0 = crec[2 * size_t(j)];      // r6 pairs
+            g1 = crec[2 * size_t(j) + 1];  // trilinear weights at x_s, 16-bit pairs
         }
         // Warp-cooperative gather: pass p, lanes 4q..4q+3 gather row 8p+q of the
         // warp's 32 rows, lane chunk = 8 of the 32 colour features.
         const uint32_t lane = r & 31, q = lane >> 2, ch = lane & 3, row0 = r & ~31u;
-        uint32_t wsp[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) wsp[b] = F::pack(ws[2 * b], ws[2 * b + 1]);
+        const uint32_t wsp[4] = {g1.x, g1.y, g1.z, g1.w};
 #pragma unroll 2
         for (uint32_t p = 0; p < 4; ++p) {
             const uint32_t src = 8 * p + q;
@@ -567,7 +555,7 @@ template <bool kBF16>
 static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t* p, const double* rays,
                            const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
                            const double* hit_tout, const uint32_t* n_dev, uint32_t cap, HitOut out, int* err,
-                           uint4* geo, float4* u12, cudaStream_t s) {
+                           uint4* crec, cudaStream_t s) {
     using H = typename Fmt<kBF16>::H;
     static bool attr = false;
     if (!attr) {
@@ -577,11 +565,10 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
     }
     const H* ft = reinterpret_cast<const H*>(p + OFF_FEAT);
     const H* fc = ft + size_t(M.V) * 64;
-    k_hit_geom<kBF16><<<(cap + 127) / 128, 128, 0, s>>>(T, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap,
-                                                       geo, u12, err);
-    k_decode_t<kBF16><<<g_num_sms, 512, T_SM_TOTAL, s>>>(T, p, ft, hit_leaf, geo, n_dev, cap, out);
-    k_decode_c<kBF16><<<g_num_sms, 512, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, geo, u12, n_dev, cap, out);
-    note_launch(3);
+    k_decode_t<kBF16><<<g_num_sms, 512, T_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev,
+                                                         cap, out, crec, err);
+    k_decode_c<kBF16><<<g_num_sms, 512, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
+    note_launch(2);
 }
 
 void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, bool bf16, const double* rays,
@@ -594,15 +581,14 @@ void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, b
         SVLF_CUDA(cudaGetDevice(&dev));
         SVLF_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    uint4* geo = static_cast<uint4*>(scratch);
-    float4* u12 = reinterpret_cast<float4*>(geo + 3 * size_t(cap));
+    uint4* crec = static_cast<uint4*>(scratch);
     const uint8_t* p = reinterpret_cast<const uint8_t*>(pack);
     if (bf16)
-        decode_tc_impl<true>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap, out, err, geo, u12, s);
+        decode_tc_impl<true>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap, out, err, crec, s);
     else
-        decode_tc_impl<false>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap, out, err, geo, u12, s);
+        decode_tc_impl<false>(T, M, p, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev, cap, out, err, crec, s);
 }
 
-size_t decode_tc_scratch_bytes(uint32_t n_hits) { return size_t(n_hits) * (48 + 32); }
+size_t decode_tc_scratch_bytes(uint32_t n_hits) { return size_t(n_hits) * 32; }
 
 }  // namespace svlfb

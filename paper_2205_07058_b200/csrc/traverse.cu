@@ -190,8 +190,14 @@ __device__ __forceinline__ void sort_segment(TinArr tin, LeafArr leaf, uint32_t 
 
 // ---- block-cooperative level-synchronous traversal -------------------------
 constexpr int kRays = 64;      // rays per block, first pass (8 x 8 pixel tile)
-constexpr int kRaysDense = 8;  // rays per block, second pass over overflowed tiles
-constexpr int kThreads = 256;  // threads per block
+#ifndef SVLF_RAYS_DENSE
+#define SVLF_RAYS_DENSE 16
+#endif
+constexpr int kRaysDense = SVLF_RAYS_DENSE;  // rays per block, second pass over overflowed tiles
+#ifndef SVLF_BFS_THREADS
+#define SVLF_BFS_THREADS 256
+#endif
+constexpr int kThreads = SVLF_BFS_THREADS;  // threads per block
 constexpr int kQCap = 1536;    // (ray, node) pairs per level
 
 struct BfsSmem {
@@ -632,7 +638,10 @@ static int num_sms() {
     return sms;
 }
 
-constexpr int kBfsBlocksPerSm = 4;
+#ifndef SVLF_BFS_BLOCKS_PER_SM
+#define SVLF_BFS_BLOCKS_PER_SM 4
+#endif
+constexpr int kBfsBlocksPerSm = SVLF_BFS_BLOCKS_PER_SM;
 
 void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
                      const TraverseOut& o, cudaStream_t s) {
