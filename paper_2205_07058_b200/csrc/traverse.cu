@@ -189,27 +189,44 @@ __device__ __forceinline__ void sort_segment(TinArr tin, LeafArr leaf, uint32_t 
 }
 
 // ---- block-cooperative level-synchronous traversal -------------------------
-constexpr int kRays = 64;      // rays per block, first pass (8 x 8 pixel tile)
+// First pass: kRays-ray tiles (8 x kRays/8 pixels) on kThreads threads with a
+// kQCap-pair level queue, small enough for several blocks per SM. Tiles whose
+// queue overflows are redone by a second pass with fewer rays per block and a
+// much larger queue; anything still overflowing goes to a per-ray walker.
+#ifndef SVLF_BFS_RAYS
+#define SVLF_BFS_RAYS 32
+#endif
+#ifndef SVLF_BFS_THREADS
+#define SVLF_BFS_THREADS 128
+#endif
+#ifndef SVLF_BFS_QCAP
+#define SVLF_BFS_QCAP 768
+#endif
 #ifndef SVLF_RAYS_DENSE
 #define SVLF_RAYS_DENSE 16
 #endif
-constexpr int kRaysDense = SVLF_RAYS_DENSE;  // rays per block, second pass over overflowed tiles
-#ifndef SVLF_BFS_THREADS
-#define SVLF_BFS_THREADS 256
+#ifndef SVLF_DENSE_QCAP
+#define SVLF_DENSE_QCAP 2048
 #endif
-constexpr int kThreads = SVLF_BFS_THREADS;  // threads per block
-constexpr int kQCap = 1536;    // (ray, node) pairs per level
+constexpr int kRays = SVLF_BFS_RAYS;         // rays per block, first pass
+constexpr int kTileH = kRays / 8;            // camera tile height (width 8)
+constexpr int kThreads = SVLF_BFS_THREADS;   // threads per block, first pass
+constexpr int kQCap = SVLF_BFS_QCAP;         // (ray, node) pairs per level, first pass
+constexpr int kRaysDense = SVLF_RAYS_DENSE;  // rays per block, second pass
+constexpr int kThreadsDense = 256;
+constexpr int kQCapDense = SVLF_DENSE_QCAP;
 
+template <int kR, int kQ, int kT>
 struct BfsSmem {
-    double o[3][kRays], d[3][kRays], inv[3][kRays];
-    uint64_t qxyz[2][kQCap];
-    uint32_t qnode[2][kQCap];
-    uint32_t pos[kQCap];  // leaf level: output position of each pair's first hit
-    uint8_t qray[2][kQCap];
-    uint32_t rcount[kRays], roff[kRays];
-    uint32_t gray[kRays];
+    double o[3][kR], d[3][kR], inv[3][kR];
+    uint64_t qxyz[2][kQ];
+    uint32_t qnode[2][kQ];
+    uint32_t pos[kQ];  // leaf level: output position of each pair's first hit
+    uint8_t qray[2][kQ];
+    uint32_t rcount[kR], roff[kR];
+    uint32_t gray[kR];
     uint32_t n_q, base, overflow;
-    typename cub::BlockScan<uint32_t, kThreads>::TempStorage scan;
+    typename cub::BlockScan<uint32_t, kT>::TempStorage scan;
 };
 
 struct BfsArgs {
@@ -229,10 +246,10 @@ struct BfsArgs {
 // kR rays per block. kList = false: tiles of the image / ray buffer (first
 // pass, overflow -> overflow_rays); kList = true: consecutive entries of
 // overflow_rays (second pass, overflow -> overflow_dense).
-template <bool kCamera, int kR, bool kList>
+template <bool kCamera, int kR, int kQ, int kT, bool kList>
 __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& cam, uint32_t row0, uint32_t rows,
-                                         uint32_t n, const BfsArgs& A, BfsSmem& S, uint32_t tile) {
-    using Scan = cub::BlockScan<uint32_t, kThreads>;
+                                         uint32_t n, const BfsArgs& A, BfsSmem<kR, kQ, kT>& S, uint32_t tile) {
+    using Scan = cub::BlockScan<uint32_t, kT>;
     const uint32_t tid = threadIdx.x;
 
     // ---- rays of this tile; root test
@@ -247,7 +264,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         } else if constexpr (kCamera) {
             const uint32_t tiles_x = (cam.width + 7) / 8;
             const uint32_t tx = tile % tiles_x, ty = tile / tiles_x;
-            const uint32_t px = tx * 8 + (tid & 7), py = ty * 8 + (tid >> 3);
+            const uint32_t px = tx * 8 + (tid & 7), py = ty * (kR / 8) + (tid >> 3);
             ok = px < cam.width && py < rows;
             gi = py * cam.width + px;
         } else {
@@ -310,7 +327,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     int level = 0;
     for (; level + 1 < T.L && n_cur > 0; ++level) {
         uint32_t n_out = 0;
-        for (uint32_t base = 0; base < n_cur; base += kThreads) {
+        for (uint32_t base = 0; base < n_cur; base += kT) {
             const uint32_t e = base + tid;
             uint32_t hitmask = 0, cnt = 0, ri = 0, x = 0, y = 0, z = 0, s = 0;
             uint2 node = make_uint2(0, 0);
@@ -341,7 +358,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             }
             uint32_t off, tot;
             Scan(S.scan).ExclusiveSum(cnt, off, tot);
-            if (n_out + tot > kQCap) {
+            if (n_out + tot > kQ) {
                 if (tid == 0) S.overflow = 1;
                 __syncthreads();
                 break;
@@ -379,7 +396,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     const bool leaf_pass = level + 1 == T.L && n_cur > 0;
     uint32_t total = 0;
     if (leaf_pass) {
-        for (uint32_t base = 0; base < n_cur; base += kThreads) {
+        for (uint32_t base = 0; base < n_cur; base += kT) {
             const uint32_t e = base + tid;
             uint32_t cnt = 0, ri = 0;
             if (e < n_cur) {
@@ -426,7 +443,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     const uint32_t gbase = S.base;
     const bool fits = gbase + total <= A.capacity;
     if (leaf_pass && fits) {
-        for (uint32_t e = tid; e < n_cur; e += kThreads) {
+        for (uint32_t e = tid; e < n_cur; e += kT) {
             const uint32_t ri = S.qray[cur][e];
             const uint2 node = T.nodes[S.qnode[cur][e]];
             const uint64_t xyz = S.qxyz[cur][e];
@@ -493,15 +510,14 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
 
 // Persistent: a block processes tiles tile = blockIdx.x + k * gridDim.x.
 // kList passes read their tile count from the device (no host round trip).
-template <bool kCamera, int kR, bool kList>
-__global__ void __launch_bounds__(kThreads) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0,
-                                                           uint32_t rows, uint32_t n, uint32_t n_tiles,
-                                                           BfsArgs A) {
+template <bool kCamera, int kR, int kQ, int kT, bool kList>
+__global__ void __launch_bounds__(kT) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
+                                                     uint32_t n, uint32_t n_tiles, BfsArgs A) {
     extern __shared__ __align__(16) uint8_t bfs_smem[];
-    BfsSmem& S = *reinterpret_cast<BfsSmem*>(bfs_smem);
+    auto& S = *reinterpret_cast<BfsSmem<kR, kQ, kT>*>(bfs_smem);
     const uint32_t tiles = kList ? (A.counters[1] + kR - 1) / kR : n_tiles;
     for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        bfs_tile<kCamera, kR, kList>(T, cam, row0, rows, n, A, S, tile);
+        bfs_tile<kCamera, kR, kQ, kT, kList>(T, cam, row0, rows, n, A, S, tile);
         __syncthreads();
     }
 }
@@ -613,14 +629,13 @@ void launch_hit_points(const double* rays, const uint32_t* hit_ray, const double
     note_launch();
 }
 
-template <bool kCamera, int kR, bool kList>
+template <bool kCamera, int kR, int kQ, int kT, bool kList>
 static void set_bfs_attr() {
     static bool done = false;
-    if (!done) {
-        SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kList>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BfsSmem))));
-        done = true;
-    }
+    if (done) return;
+    SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kQ, kT, kList>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BfsSmem<kR, kQ, kT>))));
+    done = true;
 }
 
 static BfsArgs bfs_args(const TraverseOut& o) {
@@ -639,7 +654,7 @@ static int num_sms() {
 }
 
 #ifndef SVLF_BFS_BLOCKS_PER_SM
-#define SVLF_BFS_BLOCKS_PER_SM 4
+#define SVLF_BFS_BLOCKS_PER_SM 8
 #endif
 constexpr int kBfsBlocksPerSm = SVLF_BFS_BLOCKS_PER_SM;
 
@@ -647,16 +662,17 @@ void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, ui
                      const TraverseOut& o, cudaStream_t s) {
     if (n == 0) return;
     const BfsArgs A = bfs_args(o);
+    using Sm = BfsSmem<kRays, kQCap, kThreads>;
     const uint32_t cap_grid = uint32_t(num_sms() * kBfsBlocksPerSm);
     if (cam) {
-        set_bfs_attr<true, kRays, false>();
-        const uint32_t tiles = ((cam->width + 7) / 8) * ((rows + 7) / 8);
-        k_traverse_bfs<true, kRays, false><<<std::min(tiles, cap_grid), kThreads, sizeof(BfsSmem), s>>>(
+        set_bfs_attr<true, kRays, kQCap, kThreads, false>();
+        const uint32_t tiles = ((cam->width + 7) / 8) * ((rows + kTileH - 1) / kTileH);
+        k_traverse_bfs<true, kRays, kQCap, kThreads, false><<<std::min(tiles, cap_grid), kThreads, sizeof(Sm), s>>>(
             T, *cam, row0, rows, n, tiles, A);
     } else {
-        set_bfs_attr<false, kRays, false>();
+        set_bfs_attr<false, kRays, kQCap, kThreads, false>();
         const uint32_t tiles = (n + kRays - 1) / kRays;
-        k_traverse_bfs<false, kRays, false><<<std::min(tiles, cap_grid), kThreads, sizeof(BfsSmem), s>>>(
+        k_traverse_bfs<false, kRays, kQCap, kThreads, false><<<std::min(tiles, cap_grid), kThreads, sizeof(Sm), s>>>(
             T, DevCamera{}, 0, 0, n, tiles, A);
     }
     note_launch();
@@ -665,14 +681,17 @@ void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, ui
 void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
                            cudaStream_t s) {
     const BfsArgs A = bfs_args(o);
-    const uint32_t grid = uint32_t(num_sms() * kBfsBlocksPerSm);
+    using Sm = BfsSmem<kRaysDense, kQCapDense, kThreadsDense>;
+    const uint32_t per_sm = std::max<uint32_t>(1, uint32_t(200 * 1024 / sizeof(Sm)));
+    const uint32_t grid = uint32_t(num_sms()) * per_sm;
     if (cam) {
-        set_bfs_attr<true, kRaysDense, true>();
-        k_traverse_bfs<true, kRaysDense, true><<<grid, kThreads, sizeof(BfsSmem), s>>>(T, *cam, row0, 0, 0, 0, A);
+        set_bfs_attr<true, kRaysDense, kQCapDense, kThreadsDense, true>();
+        k_traverse_bfs<true, kRaysDense, kQCapDense, kThreadsDense, true><<<grid, kThreadsDense, sizeof(Sm), s>>>(
+            T, *cam, row0, 0, 0, 0, A);
     } else {
-        set_bfs_attr<false, kRaysDense, true>();
-        k_traverse_bfs<false, kRaysDense, true><<<grid, kThreads, sizeof(BfsSmem), s>>>(T, DevCamera{}, 0, 0, 0, 0,
-                                                                                        A);
+        set_bfs_attr<false, kRaysDense, kQCapDense, kThreadsDense, true>();
+        k_traverse_bfs<false, kRaysDense, kQCapDense, kThreadsDense, true><<<grid, kThreadsDense, sizeof(Sm), s>>>(
+            T, DevCamera{}, 0, 0, 0, 0, A);
     }
     note_launch();
 }
