@@ -130,6 +130,12 @@ svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out);
 /* Count of this library's kernel launches on the context since creation. */
 long long svlf_ctx_kernel_launches(const svlf_ctx* ctx);
 
+/* Page-locked host memory. Frame outputs passed to svlf_render_frame in
+ * page-locked memory (from here, cudaMallocHost or cudaHostRegister) receive
+ * the device-to-host copies directly, band by band, with no staging copy. */
+svlf_status svlf_host_alloc(size_t bytes, void** out);
+svlf_status svlf_host_free(void* p);
+
 /* ---- data parallelism (one process per GPU, NCCL over NVLink) ----------
  * svlf_nccl_unique_id fills 128 bytes on one rank; every rank passes the same
  * bytes to svlf_ctx_attach_nccl. With a communicator attached, train steps

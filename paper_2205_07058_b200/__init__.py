@@ -181,6 +181,8 @@ def load_library():
         "svlf_ctx_set_stream": ([vp, vp], st),
         "svlf_ctx_last_timings": ([vp, C.POINTER(_Timings)], st),
         "svlf_ctx_kernel_launches": ([vp], C.c_longlong),
+        "svlf_host_alloc": ([sz, vp], st),
+        "svlf_host_free": ([vp], st),
         "svlf_nccl_unique_id": ([vp], st),
         "svlf_ctx_attach_nccl": ([vp, vp, C.c_int, C.c_int], st),
         "svlf_ctx_detach_nccl": ([vp], st),
@@ -298,6 +300,39 @@ class Context:
 
     def detach_nccl(self):
         _check(_LIB.svlf_ctx_detach_nccl(self._h))
+
+
+class _PinnedBlock:
+    """Page-locked host allocation (svlf_host_alloc); freed with the last view."""
+
+    def __init__(self, nbytes: int):
+        load_library()
+        h = C.c_void_p()
+        _check(_LIB.svlf_host_alloc(nbytes, C.byref(h)))
+        self.ptr = h.value
+        self.nbytes = nbytes
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _LIB is not None:
+            _LIB.svlf_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def pinned_empty(n: int, dtype=np.float32) -> np.ndarray:
+    """1-D numpy array of n elements in page-locked host memory."""
+    dt = np.dtype(dtype)
+    block = _PinnedBlock(max(1, n * dt.itemsize))
+    buf = (C.c_char * block.nbytes).from_address(block.ptr)
+    arr = np.frombuffer(buf, dtype=dt, count=n)
+    weakref.finalize(arr, lambda b: None, block)  # keep the block alive with the array
+    return arr
+
+
+def pinned_frame(width: int, height: int):
+    """(rgb, alpha, depth) output buffers in page-locked memory for render_frame(out=...):
+    the frame's device-to-host copies then land in them directly."""
+    n = width * height
+    return pinned_empty(3 * n), pinned_empty(n), pinned_empty(n)
 
 
 def _load_framework_nccl():

@@ -392,7 +392,19 @@ void render_frame_host(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, con
     float* d_rgb = ctx->out_rgb.ensure<float>(size_t(n) * 3);
     float* d_alpha = ctx->out_alpha.ensure<float>(n);
     float* d_depth = ctx->out_depth.ensure<float>(n);
-    if (ctx->h_stage_floats < size_t(n) * 5) {
+    // Caller buffers in page-locked memory (svlf_host_alloc / cudaMallocHost /
+    // cudaHostRegister): bands are copied straight into them. Otherwise via
+    // the context's pinned staging buffer plus parallel host copies.
+    auto pinned = [](const void* ptr) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return at.type == cudaMemoryTypeHost;
+    };
+    const bool direct = pinned(rgb) && pinned(alpha) && pinned(depth);
+    if (!direct && ctx->h_stage_floats < size_t(n) * 5) {
         if (ctx->h_stage) SVLF_CUDA(cudaFreeHost(ctx->h_stage));
         ctx->h_stage = nullptr;
         SVLF_CUDA(cudaMallocHost(&ctx->h_stage, size_t(n) * 5 * sizeof(float)));
@@ -403,9 +415,9 @@ void render_frame_host(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, con
         const int hw = int(std::thread::hardware_concurrency());
         ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
     }
-    float* st_rgb = ctx->h_stage;
-    float* st_alpha = st_rgb + size_t(n) * 3;
-    float* st_depth = st_alpha + n;
+    float* st_rgb = direct ? rgb : ctx->h_stage;
+    float* st_alpha = direct ? alpha : st_rgb + size_t(n) * 3;
+    float* st_depth = direct ? depth : st_alpha + n;
     // ~700K rays per band (fewer bands: less per-band launch/tail cost; more:
     // shorter exposed D2H + copy of the last band), at most kMaxBands
     static const uint32_t band_rays = [] {
@@ -445,6 +457,7 @@ void render_frame_host(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, con
             const double t0 = now();
             SVLF_CUDA(cudaEventSynchronize(ctx->band_copied[b]));
             const double t1 = now();
+            if (direct) continue;
             if (trace) std::fprintf(stderr, "band %u wait %.3f ms (since enqueue %.3f)\n", b, t1 - t0, t1 - t_enq);
             const size_t off = size_t(b) * band_rows * W;
             const size_t cnt = size_t(std::min(band_rows, H - b * band_rows)) * W;
@@ -557,6 +570,20 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
             cudaStreamDestroy(ctx->own_stream);
         }
         delete ctx;
+    });
+}
+
+svlf_status svlf_host_alloc(size_t bytes, void** out) {
+    return guard([&] {
+        require(out != nullptr, "out is null");
+        *out = nullptr;
+        if (bytes) SVLF_CUDA(cudaMallocHost(out, bytes));
+    });
+}
+
+svlf_status svlf_host_free(void* p) {
+    return guard([&] {
+        if (p) SVLF_CUDA(cudaFreeHost(p));
     });
 }
 

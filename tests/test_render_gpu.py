@@ -207,3 +207,22 @@ def test_render_hit_buffer_overflow_retry(oracle, precision):
         assert np.abs(rgb.reshape(-1) - orgb).max() <= tol
         assert np.abs(a.reshape(-1) - oa).max() <= tol
         c.close()
+
+
+def test_host_frame_paths_agree(ctx, oracle):
+    """svlf_render_frame delivers the same bits through every host path: fresh pageable
+    arrays (pinned staging + parallel copies), reused pageable buffers, and page-locked
+    buffers (direct per-band copies); frame large enough for several bands."""
+    sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=4, n_views=8, view_res=96, res=64, width=1280)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    camera = P.Camera.from_record(cam, W, H)
+    ref = [x.reshape(-1).copy() for x in P.render_frame(model, camera, precision="fp16")]
+    reuse = (np.full(3 * W * H, -1, np.float32), np.full(W * H, -1, np.float32), np.full(W * H, -1, np.float32))
+    pinned = P.pinned_frame(W, H)
+    for out in (reuse, pinned):
+        for _ in range(2):
+            P.render_frame(model, camera, precision="fp16", out=out)
+            for a, b in zip(out, ref):
+                assert np.array_equal(a, b)
+    assert ref[1].max() > 0.5  # the frame is not empty
