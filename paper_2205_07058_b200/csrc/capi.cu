@@ -304,7 +304,7 @@ void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t tot
     }
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_DECODE], s));
     launch_composite(ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(), ctx->hit_tin.as<double>(),
-                     ctx->hit_tout.as<double>(), ho, n, bg, d_rgb, d_alpha, d_depth, misc_fg(ctx), s);
+                     ctx->hit_tout.as<double>(), ho, n, bg, d_rgb, d_alpha, d_depth, misc_fg(ctx), prec == SVLF_PRECISION_FP32, s);
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COMPOSITE], s));
 }
 

@@ -142,7 +142,7 @@ void launch_decode_f32(const DevOctree& T, const DevModel& M, const DecPackF32& 
                        const double* hit_tout, uint32_t n_hits, HitOut out, int* err, cudaStream_t s);
 void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const double* hit_tin,
                       const double* hit_tout, HitOut hits, uint32_t n_rays, const float* bg3, float* rgb,
-                      float* alpha, float* depth, unsigned long long* fg_count, cudaStream_t s);
+                      float* alpha, float* depth, unsigned long long* fg_count, bool exact, cudaStream_t s);
 
 // ---- tcgen05 decoder (decode_tc.cu)
 void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, bool bf16,
