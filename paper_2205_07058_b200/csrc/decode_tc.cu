@@ -359,16 +359,33 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t n = min(*n_dev, cap);
     const uint32_t ntiles = (n + 127) / 128;
 
-    for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += gridDim.x * kSlots) {
+    // The per-hit scalars of a slot's NEXT tile are loaded one tile ahead, so
+    // the dependent chain leaf -> corners -> feature rows starts from registers.
+    const uint32_t tstride = gridDim.x * kSlots;
+    uint32_t nleaf = 0, nray = 0;
+    double ntin = 0.0, ntout = 0.0;
+    auto prefetch = [&](uint32_t t) {
+        const uint32_t jn = t * 128 + r;
+        if (t < ntiles && jn < n) {
+            nleaf = hit_leaf[jn];
+            nray = hit_ray[jn];
+            ntin = hit_tin[jn];
+            ntout = hit_tout[jn];
+        }
+    };
+    prefetch(blockIdx.x * kSlots + slot);
+    for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += tstride) {
         const uint32_t j = tile * 128 + r;
         const bool valid = j < n;
         uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         uint32_t r6p[3] = {0, 0, 0}, wp[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // r6, (w1, w2) as 16-bit pairs
         float u[6] = {0, 0, 0, 0, 0, 0};
+        const uint32_t leaf = nleaf, ray_i = nray;
+        const double tin = ntin, tout = ntout;
+        prefetch(tile + tstride);
         if (valid) {
-            const uint32_t leaf = hit_leaf[j];
             load_corners(T, leaf, corners);
-            hit_geom_regs<kBF16>(T, rays, hit_ray[j], leaf, hit_tin[j], hit_tout[j], r6p, wp, u, err);
+            hit_geom_regs<kBF16>(T, rays, ray_i, leaf, tin, tout, r6p, wp, u, err);
         }
         // Warp-cooperative gather: the warp owns rows 32w..32w+31 of the tile; in
         // pass p lanes 8q..8q+7 gather row 4p+q, lane chunk c = 8 features, so
@@ -460,16 +477,35 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t n = min(*n_dev, cap);
     const uint32_t ntiles = (n + 127) / 128;
 
-    for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += gridDim.x * kSlots) {
+    // Next tile's inputs are loaded one tile ahead in two steps (its leaf index
+    // at the start of this tile, its corners and f_C record after this tile's
+    // gather), so no load waits on another inside the critical path.
+    const uint32_t tstride = gridDim.x * kSlots;
+    uint32_t ncorners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint4 ng0 = make_uint4(0, 0, 0, 0), ng1 = ng0;
+    uint32_t nleaf = 0;
+    auto fetch_leaf = [&](uint32_t t) {
+        const uint32_t jn = t * 128 + r;
+        if (t < ntiles && jn < n) nleaf = hit_leaf[jn];
+    };
+    auto fetch_rest = [&](uint32_t t) {
+        const uint32_t jn = t * 128 + r;
+        if (t < ntiles && jn < n) {
+            load_corners(T, nleaf, ncorners);
+            ng0 = crec[2 * size_t(jn)];      // r6 pairs
+            ng1 = crec[2 * size_t(jn) + 1];  // trilinear weights at x_s, 16-bit pairs
+        }
+    };
+    fetch_leaf(blockIdx.x * kSlots + slot);
+    fetch_rest(blockIdx.x * kSlots + slot);
+    for (uint32_t tile = blockIdx.x * kSlots + slot; tile < ntiles; tile += tstride) {
         const uint32_t j = tile * 128 + r;
         const bool valid = j < n;
-        uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint4 g0 = make_uint4(0, 0, 0, 0), g1 = g0;
-        if (valid) {
-            load_corners(T, hit_leaf[j], corners);
-            g0 = crec[2 * size_t(j)];      // r6 pairs
-            g1 = crec[2 * size_t(j) + 1];  // trilinear weights at x_s, 16-bit pairs
-        }
+        uint32_t corners[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) corners[b] = valid ? ncorners[b] : 0u;
+        const uint4 g0 = valid ? ng0 : make_uint4(0, 0, 0, 0), g1 = valid ? ng1 : make_uint4(0, 0, 0, 0);
+        fetch_leaf(tile + tstride);
         // Warp-cooperative gather: pass p, lanes 4q..4q+3 gather row 8p+q of the
         // warp's 32 rows, lane chunk = 8 of the 32 colour features.
         const uint32_t lane = r & 31, q = lane >> 2, ch = lane & 3, row0 = r & ~31u;
@@ -501,6 +537,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         st_shared_v4(a_base + a_off(r, 32), g0.x, g0.y, g0.z, F::kOne);
         st_shared_v4(a_base + a_off(r, 40), 0u, 0u, 0u, 0u);
+        fetch_rest(tile + tstride);
         S.mma([&] { issue_layer(acc, a_base, sbase + W0, KC, kIdesc); });
         hidden_epilogue<kBF16, false>(acc + lane_off, a_base, r, KH, nullptr);
         S.mma([&] { issue_layer(acc, a_base, sbase + W1, KH, kIdesc); });
