@@ -189,15 +189,19 @@ __device__ __forceinline__ void sort_segment(TinArr tin, LeafArr leaf, uint32_t 
 }
 
 // ---- block-cooperative level-synchronous traversal -------------------------
-// First pass: kRays-ray tiles (8 x kRays/8 pixels) on kThreads threads with a
-// kQCap-pair level queue, small enough for several blocks per SM. Tiles whose
-// queue overflows are redone by a second pass with fewer rays per block and a
-// much larger queue; anything still overflowing goes to a per-ray walker.
+// First pass: kRays-ray tiles processed by kThreads threads (one warp when
+// kThreads == 32, kBlockThreads / kThreads independent tiles per block) with
+// a kQCap-pair level queue. Tiles whose queue overflows are redone by a second
+// pass with more threads per ray and a much larger queue; anything still
+// overflowing goes to a per-ray walker.
 #ifndef SVLF_BFS_RAYS
 #define SVLF_BFS_RAYS 32
 #endif
 #ifndef SVLF_BFS_THREADS
 #define SVLF_BFS_THREADS 128
+#endif
+#ifndef SVLF_BFS_BLOCK
+#define SVLF_BFS_BLOCK SVLF_BFS_THREADS
 #endif
 #ifndef SVLF_BFS_QCAP
 #define SVLF_BFS_QCAP 768
@@ -208,9 +212,9 @@ __device__ __forceinline__ void sort_segment(TinArr tin, LeafArr leaf, uint32_t 
 #ifndef SVLF_DENSE_QCAP
 #define SVLF_DENSE_QCAP 2048
 #endif
-constexpr int kRays = SVLF_BFS_RAYS;         // rays per block, first pass
-constexpr int kTileH = kRays / 8;            // camera tile height (width 8)
-constexpr int kThreads = SVLF_BFS_THREADS;   // threads per block, first pass
+constexpr int kRays = SVLF_BFS_RAYS;         // rays per tile, first pass
+constexpr int kThreads = SVLF_BFS_THREADS;   // threads per tile, first pass
+constexpr int kBlockThreads = SVLF_BFS_BLOCK;  // threads per block, first pass
 constexpr int kQCap = SVLF_BFS_QCAP;         // (ray, node) pairs per level, first pass
 constexpr int kRaysDense = SVLF_RAYS_DENSE;  // rays per block, second pass
 constexpr int kThreadsDense = 256;
@@ -246,11 +250,43 @@ struct BfsArgs {
 // kR rays per block. kList = false: tiles of the image / ray buffer (first
 // pass, overflow -> overflow_rays); kList = true: consecutive entries of
 // overflow_rays (second pass, overflow -> overflow_dense).
+// A tile is processed by kT threads: a whole block (kT > 32, block barriers
+// and cub::BlockScan) or a single warp (kT == 32, warp barriers and shuffle
+// scans: the warps of a block then run independent tiles).
+template <int kT>
+__device__ __forceinline__ void tile_sync() {
+    if constexpr (kT == 32) __syncwarp();
+    else __syncthreads();
+}
+
+template <int kT, typename Temp>
+__device__ __forceinline__ void tile_excl_sum(Temp& temp, uint32_t v, uint32_t& off, uint32_t& tot) {
+    if constexpr (kT == 32) {
+        const uint32_t lane = threadIdx.x & 31u;
+        uint32_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= uint32_t(d)) x += y;
+        }
+        tot = __shfl_sync(0xffffffffu, x, 31);
+        off = x - v;
+    } else {
+        cub::BlockScan<uint32_t, kT>(temp).ExclusiveSum(v, off, tot);
+    }
+}
+
+// camera tile shape for kR rays: 8 x kR/8 pixels, or 4 x 2 for 8-ray tiles
+template <int kR>
+struct TileShape {
+    static constexpr int W = kR >= 32 ? 8 : 4;
+    static constexpr int H = kR / W;
+};
+
 template <bool kCamera, int kR, int kQ, int kT, bool kList>
 __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& cam, uint32_t row0, uint32_t rows,
                                          uint32_t n, const BfsArgs& A, BfsSmem<kR, kQ, kT>& S, uint32_t tile) {
-    using Scan = cub::BlockScan<uint32_t, kT>;
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x & uint32_t(kT - 1);
 
     // ---- rays of this tile; root test
     uint32_t my_ray = 0xffffffffu;
@@ -262,9 +298,10 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             gi = k < A.counters[1] ? A.overflow_rays[k] : 0xffffffffu;
             ok = gi != 0xffffffffu;
         } else if constexpr (kCamera) {
-            const uint32_t tiles_x = (cam.width + 7) / 8;
+            using TS = TileShape<kR>;
+            const uint32_t tiles_x = (cam.width + TS::W - 1) / TS::W;
             const uint32_t tx = tile % tiles_x, ty = tile / tiles_x;
-            const uint32_t px = tx * 8 + (tid & 7), py = ty * (kR / 8) + (tid >> 3);
+            const uint32_t px = tx * TS::W + tid % TS::W, py = ty * TS::H + tid / TS::W;
             ok = px < cam.width && py < rows;
             gi = py * cam.width + px;
         } else {
@@ -293,7 +330,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         S.n_q = 0;
         S.overflow = 0;
     }
-    __syncthreads();
+    tile_sync<kT>();
     {
         uint32_t hit = 0;
         if (my_ray != 0xffffffffu) {
@@ -311,14 +348,14 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             hit = slab_test(p, lo, hi, t0, t1) ? 1u : 0u;
         }
         uint32_t off, tot;
-        Scan(S.scan).ExclusiveSum(hit, off, tot);
+        tile_excl_sum<kT>(S.scan, hit, off, tot);
         if (hit) {
             S.qnode[0][off] = 0;
             S.qxyz[0][off] = 0;
             S.qray[0][off] = uint8_t(tid);
         }
         if (tid == 0) S.n_q = tot;
-        __syncthreads();
+        tile_sync<kT>();
     }
 
     // ---- internal levels: expand (ray, node) pairs into the next level's queue
@@ -357,10 +394,10 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 cnt = __popc(hitmask);
             }
             uint32_t off, tot;
-            Scan(S.scan).ExclusiveSum(cnt, off, tot);
+            tile_excl_sum<kT>(S.scan, cnt, off, tot);
             if (n_out + tot > kQ) {
                 if (tid == 0) S.overflow = 1;
-                __syncthreads();
+                tile_sync<kT>();
                 break;
             }
             uint32_t w = n_out + off;  // children in front-to-back octant order
@@ -374,17 +411,17 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 ++w;
             }
             n_out += tot;
-            __syncthreads();
+            tile_sync<kT>();
         }
         if (S.overflow) break;
         n_cur = n_out;
         cur ^= 1;
-        __syncthreads();
+        tile_sync<kT>();
     }
 
     if (S.overflow) {  // hand the whole tile (kept contiguous) to the next pass
         if (tid == 0) S.base = atomicAdd(&A.counters[kList ? 3 : 1], uint32_t(kR));
-        __syncthreads();
+        tile_sync<kT>();
         if (tid < kR) (kList ? A.overflow_dense : A.overflow_rays)[S.base + tid] = S.gray[tid];
         return;
     }
@@ -422,23 +459,23 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 if (cnt) atomicAdd(&S.rcount[ri], cnt);
             }
             uint32_t off, tot;
-            Scan(S.scan).ExclusiveSum(cnt, off, tot);
+            tile_excl_sum<kT>(S.scan, cnt, off, tot);
             if (e < n_cur) S.pos[e] = total + off;
             total += tot;
-            __syncthreads();
+            tile_sync<kT>();
         }
     }
     {
         const uint32_t c = tid < kR ? S.rcount[tid] : 0u;
         uint32_t off, tot;
-        Scan(S.scan).ExclusiveSum(c, off, tot);
+        tile_excl_sum<kT>(S.scan, c, off, tot);
         if (tid < kR) S.roff[tid] = off;
         if (tid == 0) {
             const uint32_t b = tot ? atomicAdd(&A.counters[0], tot) : 0u;
             S.base = b;
             if (b + tot > A.capacity) atomicExch(&A.counters[2], 1u);
         }
-        __syncthreads();
+        tile_sync<kT>();
     }
     const uint32_t gbase = S.base;
     const bool fits = gbase + total <= A.capacity;
@@ -473,7 +510,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             }
         }
     }
-    __syncthreads();
+    tile_sync<kT>();
     if (tid < kR && S.gray[tid] != 0xffffffffu && fits) {
         const uint32_t c = S.rcount[tid], b = gbase + S.roff[tid];
         A.ray_off[S.gray[tid]] = b;
@@ -508,17 +545,20 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     }
 }
 
-// Persistent: a block processes tiles tile = blockIdx.x + k * gridDim.x.
-// kList passes read their tile count from the device (no host round trip).
-template <bool kCamera, int kR, int kQ, int kT, bool kList>
-__global__ void __launch_bounds__(kT) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
-                                                     uint32_t n, uint32_t n_tiles, BfsArgs A) {
+// Persistent: each tile group (a block, or each warp of a block when kT ==
+// 32) processes tiles tile = group + k * groups. kList passes read their tile
+// count from the device (no host round trip).
+template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList>
+__global__ void __launch_bounds__(kBlock) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
+                                                         uint32_t n, uint32_t n_tiles, BfsArgs A) {
     extern __shared__ __align__(16) uint8_t bfs_smem[];
-    auto& S = *reinterpret_cast<BfsSmem<kR, kQ, kT>*>(bfs_smem);
+    constexpr uint32_t kGroups = kBlock / kT;
+    const uint32_t g = threadIdx.x / kT;
+    auto& S = reinterpret_cast<BfsSmem<kR, kQ, kT>*>(bfs_smem)[g];
     const uint32_t tiles = kList ? (A.counters[1] + kR - 1) / kR : n_tiles;
-    for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    for (uint32_t tile = blockIdx.x * kGroups + g; tile < tiles; tile += gridDim.x * kGroups) {
         bfs_tile<kCamera, kR, kQ, kT, kList>(T, cam, row0, rows, n, A, S, tile);
-        __syncthreads();
+        tile_sync<kT>();
     }
 }
 
@@ -629,20 +669,10 @@ void launch_hit_points(const double* rays, const uint32_t* hit_ray, const double
     note_launch();
 }
 
-template <bool kCamera, int kR, int kQ, int kT, bool kList>
-static void set_bfs_attr() {
-    static bool done = false;
-    if (done) return;
-    SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kQ, kT, kList>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BfsSmem<kR, kQ, kT>))));
-    done = true;
-}
-
 static BfsArgs bfs_args(const TraverseOut& o) {
     return BfsArgs{o.ray_off, o.ray_cnt, o.hit_leaf, o.hit_tin, o.hit_tout, o.hit_ray,
                    o.counters, o.overflow_rays, o.overflow_dense, o.rays, o.capacity};
 }
-
 static int num_sms() {
     static int sms = 0;
     if (!sms) {
@@ -652,27 +682,40 @@ static int num_sms() {
     }
     return sms;
 }
-
 #ifndef SVLF_BFS_BLOCKS_PER_SM
 #define SVLF_BFS_BLOCKS_PER_SM 8
 #endif
 constexpr int kBfsBlocksPerSm = SVLF_BFS_BLOCKS_PER_SM;
 
+template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList>
+static void set_bfs_attr() {
+    static bool done = false;
+    if (done) return;
+    SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kQ, kT, kBlock, kList>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sizeof(BfsSmem<kR, kQ, kT>) * (kBlock / kT))));
+    done = true;
+}
+
 void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
                      const TraverseOut& o, cudaStream_t s) {
     if (n == 0) return;
     const BfsArgs A = bfs_args(o);
-    using Sm = BfsSmem<kRays, kQCap, kThreads>;
+    constexpr uint32_t kGroups = kBlockThreads / kThreads;
+    const size_t smem = sizeof(BfsSmem<kRays, kQCap, kThreads>) * kGroups;
     const uint32_t cap_grid = uint32_t(num_sms() * kBfsBlocksPerSm);
     if (cam) {
-        set_bfs_attr<true, kRays, kQCap, kThreads, false>();
-        const uint32_t tiles = ((cam->width + 7) / 8) * ((rows + kTileH - 1) / kTileH);
-        k_traverse_bfs<true, kRays, kQCap, kThreads, false><<<std::min(tiles, cap_grid), kThreads, sizeof(Sm), s>>>(
+        set_bfs_attr<true, kRays, kQCap, kThreads, kBlockThreads, false>();
+        using TS = TileShape<kRays>;
+        const uint32_t tiles = ((cam->width + TS::W - 1) / TS::W) * ((rows + TS::H - 1) / TS::H);
+        const uint32_t blocks = std::min((tiles + kGroups - 1) / kGroups, cap_grid);
+        k_traverse_bfs<true, kRays, kQCap, kThreads, kBlockThreads, false><<<blocks, kBlockThreads, smem, s>>>(
             T, *cam, row0, rows, n, tiles, A);
     } else {
-        set_bfs_attr<false, kRays, kQCap, kThreads, false>();
+        set_bfs_attr<false, kRays, kQCap, kThreads, kBlockThreads, false>();
         const uint32_t tiles = (n + kRays - 1) / kRays;
-        k_traverse_bfs<false, kRays, kQCap, kThreads, false><<<std::min(tiles, cap_grid), kThreads, sizeof(Sm), s>>>(
+        const uint32_t blocks = std::min((tiles + kGroups - 1) / kGroups, cap_grid);
+        k_traverse_bfs<false, kRays, kQCap, kThreads, kBlockThreads, false><<<blocks, kBlockThreads, smem, s>>>(
             T, DevCamera{}, 0, 0, n, tiles, A);
     }
     note_launch();
@@ -685,13 +728,13 @@ void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t ro
     const uint32_t per_sm = std::max<uint32_t>(1, uint32_t(200 * 1024 / sizeof(Sm)));
     const uint32_t grid = uint32_t(num_sms()) * per_sm;
     if (cam) {
-        set_bfs_attr<true, kRaysDense, kQCapDense, kThreadsDense, true>();
-        k_traverse_bfs<true, kRaysDense, kQCapDense, kThreadsDense, true><<<grid, kThreadsDense, sizeof(Sm), s>>>(
-            T, *cam, row0, 0, 0, 0, A);
+        set_bfs_attr<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>();
+        k_traverse_bfs<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>
+            <<<grid, kThreadsDense, sizeof(Sm), s>>>(T, *cam, row0, 0, 0, 0, A);
     } else {
-        set_bfs_attr<false, kRaysDense, kQCapDense, kThreadsDense, true>();
-        k_traverse_bfs<false, kRaysDense, kQCapDense, kThreadsDense, true><<<grid, kThreadsDense, sizeof(Sm), s>>>(
-            T, DevCamera{}, 0, 0, 0, 0, A);
+        set_bfs_attr<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>();
+        k_traverse_bfs<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>
+            <<<grid, kThreadsDense, sizeof(Sm), s>>>(T, DevCamera{}, 0, 0, 0, 0, A);
     }
     note_launch();
 }
