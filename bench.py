@@ -119,6 +119,17 @@ def max_over_ranks(x: float, dist, device):
     return float(t.item())
 
 
+def ncu_traffic(prefix, path=os.path.join(ROOT, "profiles", "r1_render.json")):
+    """DRAM bytes (read + write) per launch of the kernels named prefix*, from the
+    committed ncu summary (profiles/summarize.py); None if absent."""
+    try:
+        caps = json.load(open(path))["captures"]
+        v = sum(c["dram__bytes_read.sum"] + c["dram__bytes_write.sum"] for c in caps if c["kernel"].startswith(prefix))
+        return int(v) if v else None
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -425,7 +436,9 @@ def main():
         "stages_ms": stage,
         "roofline": {"bound": "tensor", "kernel": f"decode_{precision}", "achieved": round(achieved_tflops, 3),
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved_tflops / peak, 5),
-                     "traffic": None, "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)",
+                     "traffic": ncu_traffic("k_decode"), "traffic_unit": "bytes per launch (decode_t + decode_c)",
+                     "traffic_source": "profiles/r1_render.json (ncu --set full --clock-control none)",
+                     "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)",
                      "algorithmic": f"{FLOP_PER_HIT} FLOP/hit x {int(hits)} hits per launch"},
         "e2e": {"value": round(e2e_value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": camera_bytes,
                 "d2h_bytes_per_step": n * BYTES_PER_RAY_OUT,
