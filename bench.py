@@ -391,7 +391,29 @@ def main():
         t0 = time.perf_counter()
         P.render_frame(model, camera, precision=precision, out=frame)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_step = max_over_ranks(statistics.median(e2e_ms), dist, device)
+    e2e_sync_step = max_over_ranks(statistics.median(e2e_ms), dist, device)
+    e2e_sync_value = world * n / (e2e_sync_step * 1e-3) / 1e6
+
+    # pipelined serving loop: render_frame_submit / wait with two frames in
+    # flight (frame k's device-to-host copies overlap frame k+1's rendering);
+    # every frame's result is read back inside the timed region; L2 flushed on
+    # the library's stream between frames
+    frames = [P.pinned_frame(W, H), P.pinned_frame(W, H)]
+    P.render_frame_submit(model, camera, frames[0], precision=precision).wait()
+    k_e2e = max(3, min(args.steps, 10))
+    torch.cuda.synchronize(device)
+    barrier(dist)
+    t0 = time.perf_counter()
+    pending = None
+    for i in range(k_e2e):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        tk = P.render_frame_submit(model, camera, frames[i % 2], precision=precision)
+        if pending is not None:
+            pending.wait()
+        pending = tk
+    pending.wait()
+    e2e_step = max_over_ranks((time.perf_counter() - t0) * 1e3 / k_e2e, dist, device)
     e2e_value = world * n / (e2e_step * 1e-3) / 1e6
 
     train = None
@@ -441,9 +463,13 @@ def main():
                      "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)",
                      "algorithmic": f"{FLOP_PER_HIT} FLOP/hit x {int(hits)} hits per launch"},
         "e2e": {"value": round(e2e_value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": camera_bytes,
-                "d2h_bytes_per_step": n * BYTES_PER_RAY_OUT,
-                "api": "paper_2205_07058_b200.render_frame (C ABI svlf_render_frame) into page-locked host "
-                       "buffers from paper_2205_07058_b200.pinned_frame"},
+                "d2h_bytes_per_step": n * BYTES_PER_RAY_OUT, "ms_per_step": round(e2e_step, 4),
+                "mode": "pipelined: render_frame_submit/wait, two frames in flight, page-locked outputs",
+                "sync": {"value": round(e2e_sync_value, 3), "ms_per_step": round(e2e_sync_step, 4),
+                         "api": "paper_2205_07058_b200.render_frame (one frame per call, banded copies)"},
+                "api": "paper_2205_07058_b200.render_frame_submit / FrameTicket.wait (C ABI "
+                       "svlf_render_frame_submit / svlf_render_frame_wait) into page-locked host buffers "
+                       "from paper_2205_07058_b200.pinned_frame"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -198,6 +198,15 @@ size_t svlf_model_param_count(const svlf_model* model);
 svlf_status svlf_render_frame(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
                               const float* background, svlf_precision precision, float* rgb,
                               float* alpha, float* depth, svlf_render_stats* stats);
+/* Pipelined variant: submit enqueues the whole frame and its device-to-host
+ * copies and returns a ticket; wait completes it (host buffers valid, stats
+ * added). Up to two frames may be in flight per context, so one frame's copies
+ * overlap the next frame's rendering. The host buffers must stay valid until
+ * the wait; page-locked buffers receive the copies directly. */
+svlf_status svlf_render_frame_submit(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
+                                     const float* background, svlf_precision precision, float* rgb,
+                                     float* alpha, float* depth, uint64_t* ticket);
+svlf_status svlf_render_frame_wait(svlf_ctx* ctx, uint64_t ticket, svlf_render_stats* stats);
 /* Same with DEVICE output buffers, asynchronous (inputs resident in HBM). */
 svlf_status svlf_render_frame_device(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
                                      const float* background, svlf_precision precision,

@@ -181,6 +181,8 @@ def load_library():
         "svlf_ctx_set_stream": ([vp, vp], st),
         "svlf_ctx_last_timings": ([vp, C.POINTER(_Timings)], st),
         "svlf_ctx_kernel_launches": ([vp], C.c_longlong),
+        "svlf_render_frame_submit": ([vp, vp, vp, vp, C.c_int, vp, vp, vp, C.POINTER(C.c_uint64)], st),
+        "svlf_render_frame_wait": ([vp, C.c_uint64, vp], st),
         "svlf_host_alloc": ([sz, vp], st),
         "svlf_host_free": ([vp], st),
         "svlf_nccl_unique_id": ([vp], st),
@@ -561,6 +563,42 @@ def render_frame(model: Model, camera: Camera, stats: RenderStats | None = None,
     _add_stats(stats, st)
     return (rgb.reshape(camera.height, camera.width, 3), alpha.reshape(camera.height, camera.width),
             depth.reshape(camera.height, camera.width))
+
+
+class FrameTicket:
+    """A submitted frame (render_frame_submit); wait() returns its buffers."""
+
+    def __init__(self, model, camera, ticket, out, keep):
+        self.model, self.camera, self.ticket, self.out, self._keep = model, camera, ticket, out, keep
+        self.done = False
+
+    def wait(self, stats: RenderStats | None = None):
+        if not self.done:
+            st = _RenderStats()
+            _check(_LIB.svlf_render_frame_wait(self.model.ctx.handle, C.c_uint64(self.ticket), C.byref(st)))
+            _add_stats(stats, st)
+            self.done = True
+        W, H = self.camera.width, self.camera.height
+        rgb, alpha, depth = self.out
+        return rgb.reshape(H, W, 3), alpha.reshape(H, W), depth.reshape(H, W)
+
+
+def render_frame_submit(model: Model, camera: Camera, out, background=None, precision: str = "fp32"):
+    """Pipelined render_frame: enqueue the frame (and its copies into `out`,
+    ideally from pinned_frame()) and return a FrameTicket; up to two frames in
+    flight per context. Call ticket.wait() before reading `out`."""
+    n = camera.width * camera.height
+    rgb, alpha, depth = out
+    for arr, k in ((rgb, 3 * n), (alpha, n), (depth, n)):
+        if not (isinstance(arr, np.ndarray) and arr.dtype == np.float32 and arr.size == k
+                and arr.flags.c_contiguous and arr.flags.writeable):
+            raise ValueError("out arrays must be writeable C-contiguous float32 of sizes W*H*3, W*H, W*H")
+    keep, bgp = _bg(background)
+    cam = camera._c()
+    t = C.c_uint64()
+    _check(_LIB.svlf_render_frame_submit(model.ctx.handle, model.handle, C.byref(cam), bgp, _PREC[precision],
+                                         _dp(rgb), _dp(alpha), _dp(depth), C.byref(t)))
+    return FrameTicket(model, camera, t.value, out, keep)
 
 
 def render_frame_device(model: Model, camera: Camera, d_rgb: int, d_alpha: int, d_depth: int,

@@ -95,14 +95,31 @@ struct svlf_ctx {
     TrainScratch train;
     int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
     cudaEvent_t ev[EV_N] = {};
-    // host-buffer frames: banded render, D2H on a copy stream into pinned
-    // staging, parallel host copies into the caller's buffers (overlapped)
+    // host-buffer frames: banded render, D2H on a copy stream into the caller's
+    // page-locked buffers or pinned staging (then parallel host copies); two
+    // frame slots so a submitted frame's copies overlap the next frame's work
     static constexpr int kMaxBands = 8;
+    struct FrameSlot {
+        DevBuf rgb, alpha, depth, ctr;  // device outputs; per-band counters + misc snapshot
+        float* h_stage = nullptr;
+        size_t h_stage_floats = 0;
+        uint32_t* h_ctr = nullptr;  // pinned mailbox: band counters, error flag, fg count
+        cudaEvent_t band_done[kMaxBands] = {}, band_copied[kMaxBands] = {};
+        bool busy = false;
+        uint64_t id = 0;
+        // the submission
+        svlf_model* m = nullptr;
+        svlf_camera cam{};
+        float bg[3] = {0, 0, 0};
+        bool has_bg = false;
+        svlf_precision prec = SVLF_PRECISION_FP32;
+        float *u_rgb = nullptr, *u_alpha = nullptr, *u_depth = nullptr;
+        bool direct = false;
+        uint32_t n = 0, nb = 0, band_rows = 0;
+    };
+    FrameSlot slot[2];
+    uint64_t next_frame = 1;
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t band_done[kMaxBands] = {}, band_copied[kMaxBands] = {};
-    float* h_stage = nullptr;
-    size_t h_stage_floats = 0;
-    DevBuf band_ctr;
     std::unique_ptr<HostPool> pool;
     svlf_timings last{};
     std::mutex mu;  // one pipeline at a time per context
@@ -374,143 +391,193 @@ void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_
     render_pipeline(ctx, m, &dc, row0, rows, n, bg, prec, d_rgb, d_alpha, d_depth, stats);
 }
 
-// Frame into HOST buffers. The image is rendered in up to kMaxBands row
-// bands, all enqueued without host round trips; each finished band is copied
-// D2H on ctx->copy_stream into pinned staging while later bands render, and
-// the host copies staging -> caller buffers with a worker pool while the GPU
-// is still busy. Per-band traversal counters are kept so a capacity overflow
-// in any band re-renders the frame with larger hit buffers.
-void render_frame_host(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg, svlf_precision prec,
-                       float* rgb, float* alpha, float* depth, svlf_render_stats* stats) {
-    require(cam != nullptr, "camera is null");
-    if (cam->width == 0 || cam->height == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "zero-size image");
-    const uint64_t n64 = uint64_t(cam->width) * cam->height;
-    require(n64 < (1ull << 31), "too many pixels in one call");
-    const uint32_t W = cam->width, H = cam->height, n = uint32_t(n64);
-    const DevCamera dc = to_dev_camera(*cam);
-    cudaStream_t s = ctx->stream;
-    float* d_rgb = ctx->out_rgb.ensure<float>(size_t(n) * 3);
-    float* d_alpha = ctx->out_alpha.ensure<float>(n);
-    float* d_depth = ctx->out_depth.ensure<float>(n);
-    // Caller buffers in page-locked memory (svlf_host_alloc / cudaMallocHost /
-    // cudaHostRegister): bands are copied straight into them. Otherwise via
-    // the context's pinned staging buffer plus parallel host copies.
-    auto pinned = [](const void* ptr) {
-        cudaPointerAttributes at{};
-        if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        return at.type == cudaMemoryTypeHost;
-    };
-    const bool direct = pinned(rgb) && pinned(alpha) && pinned(depth);
-    if (!direct && ctx->h_stage_floats < size_t(n) * 5) {
-        if (ctx->h_stage) SVLF_CUDA(cudaFreeHost(ctx->h_stage));
-        ctx->h_stage = nullptr;
-        SVLF_CUDA(cudaMallocHost(&ctx->h_stage, size_t(n) * 5 * sizeof(float)));
-        ctx->h_stage_floats = size_t(n) * 5;
+// Frame into HOST buffers, in two phases so frames can be pipelined.
+// submit: the image is rendered in `bands` row bands, all enqueued without a
+// host round trip; each finished band is copied device-to-host on
+// ctx->copy_stream (into the caller's buffers when they are page-locked, else
+// into the slot's pinned staging) while later bands / the next frame render.
+// complete: waits for the bands in order (host copies from staging overlap
+// the GPU), then checks the frame's counters: a hit-buffer overflow in any
+// band re-renders the frame synchronously with grown buffers (errors raised
+// on the partial hit lists are discarded).
+using FrameSlot = svlf_ctx::FrameSlot;
+
+bool is_pinned(const void* ptr) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
     }
-    if (!ctx->pool) {
+    return at.type == cudaMemoryTypeHost;
+}
+
+void frame_submit(svlf_ctx* ctx, FrameSlot& F, uint32_t bands) {
+    const uint32_t W = F.cam.width, H = F.cam.height, n = F.n;
+    const DevCamera dc = to_dev_camera(F.cam);
+    cudaStream_t s = ctx->stream, c = ctx->copy_stream;
+    float* d_rgb = F.rgb.ensure<float>(size_t(n) * 3);
+    float* d_alpha = F.alpha.ensure<float>(n);
+    float* d_depth = F.depth.ensure<float>(n);
+    if (!F.direct && F.h_stage_floats < size_t(n) * 5) {
+        if (F.h_stage) SVLF_CUDA(cudaFreeHost(F.h_stage));
+        F.h_stage = nullptr;
+        SVLF_CUDA(cudaMallocHost(&F.h_stage, size_t(n) * 5 * sizeof(float)));
+        F.h_stage_floats = size_t(n) * 5;
+    }
+    float* st_rgb = F.direct ? F.u_rgb : F.h_stage;
+    float* st_alpha = F.direct ? F.u_alpha : st_rgb + size_t(n) * 3;
+    float* st_depth = F.direct ? F.u_depth : st_alpha + n;
+    bands = std::max<uint32_t>(1, std::min<uint32_t>({bands, uint32_t(svlf_ctx::kMaxBands), H}));
+    F.band_rows = (H + bands - 1) / bands;
+    uint32_t* ctr = F.ctr.ensure<uint32_t>(4 * svlf_ctx::kMaxBands + 8);
+    const float* bg = F.has_bg ? F.bg : nullptr;
+    reset_misc(ctx);
+    uint32_t nb = 0;
+    for (uint32_t r0 = 0; r0 < H; r0 += F.band_rows, ++nb) {
+        const uint32_t rows = std::min(F.band_rows, H - r0);
+        const size_t off = size_t(r0) * W, cnt = size_t(rows) * W;
+        uint32_t total = 0;
+        if (F.prec == SVLF_PRECISION_FP32) total = run_traversal(ctx, F.m->tree, &dc, r0, rows, uint32_t(cnt));
+        else enqueue_traversal(ctx, F.m->tree, &dc, r0, rows, uint32_t(cnt));
+        run_decode_composite(ctx, F.m, uint32_t(cnt), total, bg, F.prec, d_rgb + off * 3, d_alpha + off,
+                             d_depth + off);
+        SVLF_CUDA(cudaMemcpyAsync(ctr + 4 * nb, traversal_counters(ctx), 16, cudaMemcpyDeviceToDevice, s));
+        if (r0 + F.band_rows >= H)  // last band: snapshot of the error flag and the foreground count
+            SVLF_CUDA(cudaMemcpyAsync(ctr + 4 * svlf_ctx::kMaxBands, ctx->misc.p, 16, cudaMemcpyDeviceToDevice, s));
+        SVLF_CUDA(cudaEventRecord(F.band_done[nb], s));
+        SVLF_CUDA(cudaStreamWaitEvent(c, F.band_done[nb], 0));
+        SVLF_CUDA(cudaMemcpyAsync(st_rgb + off * 3, d_rgb + off * 3, cnt * 12, cudaMemcpyDeviceToHost, c));
+        SVLF_CUDA(cudaMemcpyAsync(st_alpha + off, d_alpha + off, cnt * 4, cudaMemcpyDeviceToHost, c));
+        SVLF_CUDA(cudaMemcpyAsync(st_depth + off, d_depth + off, cnt * 4, cudaMemcpyDeviceToHost, c));
+        if (r0 + F.band_rows >= H)
+            SVLF_CUDA(cudaMemcpyAsync(F.h_ctr, ctr, 4 * (4 * svlf_ctx::kMaxBands + 4), cudaMemcpyDeviceToHost, c));
+        SVLF_CUDA(cudaEventRecord(F.band_copied[nb], c));
+    }
+    F.nb = nb;
+}
+
+// Returns false when the frame has to be redone (hit buffers overflowed).
+bool frame_complete(svlf_ctx* ctx, FrameSlot& F, svlf_render_stats* stats) {
+    const uint32_t W = F.cam.width, H = F.cam.height, n = F.n;
+    if (!F.direct && !ctx->pool) {
         const char* e = std::getenv("SVLF_COPY_THREADS");
         const int hw = int(std::thread::hardware_concurrency());
         ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
     }
-    float* st_rgb = direct ? rgb : ctx->h_stage;
-    float* st_alpha = direct ? alpha : st_rgb + size_t(n) * 3;
-    float* st_depth = direct ? depth : st_alpha + n;
-    // ~700K rays per band (fewer bands: less per-band launch/tail cost; more:
-    // shorter exposed D2H + copy of the last band), at most kMaxBands
+    const float* st_rgb = F.h_stage;
+    const float* st_alpha = st_rgb + size_t(n) * 3;
+    const float* st_depth = st_alpha + n;
+    for (uint32_t b = 0; b < F.nb; ++b) {
+        SVLF_CUDA(cudaEventSynchronize(F.band_copied[b]));
+        if (F.direct) continue;
+        const size_t off = size_t(b) * F.band_rows * W;
+        const size_t cnt = size_t(std::min(F.band_rows, H - b * F.band_rows)) * W;
+        constexpr size_t kPart = 64 * 1024;  // pixels per host copy task
+        const int parts = int((cnt + kPart - 1) / kPart);
+        ctx->pool->parallel_for(parts, [&](int i) {
+            const size_t p0 = off + size_t(i) * kPart, pc = std::min(kPart, off + cnt - p0);
+            std::memcpy(F.u_rgb + p0 * 3, st_rgb + p0 * 3, pc * 12);
+            std::memcpy(F.u_alpha + p0, st_alpha + p0, pc * 4);
+            std::memcpy(F.u_depth + p0, st_depth + p0, pc * 4);
+        });
+    }
+    uint64_t total = 0, dense = 0, fallback = 0, worst = 0;
+    bool overflow = false;
+    for (uint32_t b = 0; b < F.nb; ++b) {
+        const uint32_t* c = F.h_ctr + 4 * b;
+        total += c[0];
+        dense += c[1];
+        overflow |= c[2] != 0;
+        fallback += c[3];
+        worst = std::max<uint64_t>(worst, c[0]);
+    }
+    const uint32_t* snap = F.h_ctr + 4 * svlf_ctx::kMaxBands;
+    const int err = int(snap[0]);
+    unsigned long long fg = 0;
+    std::memcpy(&fg, snap + 2, 8);
+    ctx->last_overflow_rays = (long long)fallback;
+    ctx->last_dense_rays = (long long)dense;
+    if (overflow) {
+        ctx->hit_cap = std::max(ctx->hit_cap, size_t(worst) + worst / 4 + 1024);
+        return false;
+    }
+    if (err) fail(SVLF_ERR_RUNTIME, dev_error_message(err));
+    float ms[4] = {};  // last band's stage times
+    cudaEventElapsedTime(&ms[0], ctx->ev[EV_START], ctx->ev[EV_COUNT]);
+    cudaEventElapsedTime(&ms[1], ctx->ev[EV_COUNT], ctx->ev[EV_EMIT]);
+    cudaEventElapsedTime(&ms[2], ctx->ev[EV_EMIT], ctx->ev[EV_DECODE]);
+    cudaEventElapsedTime(&ms[3], ctx->ev[EV_DECODE], ctx->ev[EV_COMPOSITE]);
+    cudaGetLastError();
+    ctx->last = svlf_timings{ms[0], ms[1], ms[2], ms[3], 0.f, 0.f, ms[0] + ms[1] + ms[2] + ms[3],
+                             (long long)total, ctx->last_overflow_rays, ctx->last_dense_rays};
+    if (stats) {
+        stats->rays += n;
+        stats->rays_with_hits += (long long)fg;
+        stats->traversal_hits += (long long)total;
+        stats->thickness_queries += (long long)total;
+        stats->color_queries += (long long)total;
+    }
+    return true;
+}
+
+uint32_t default_bands(uint32_t n) {
+    // ~700K rays per band for a synchronous frame (fewer bands: less per-band
+    // launch/tail cost; more: shorter exposed copy of the last band)
     static const uint32_t band_rays = [] {
         const char* e = std::getenv("SVLF_BAND_RAYS");
         return e ? uint32_t(std::max(1, std::atoi(e))) : 700000u;  // measured best for C2 (3 bands)
     }();
-    const uint32_t bands = std::max<uint32_t>(1, std::min<uint32_t>(svlf_ctx::kMaxBands, std::min(H, n / band_rays)));
-    const uint32_t band_rows = (H + bands - 1) / bands;
-    uint32_t* bctr = ctx->band_ctr.ensure<uint32_t>(4 * svlf_ctx::kMaxBands);
-    static const bool trace = std::getenv("SVLF_TRACE") != nullptr;
-    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
-    const double t_start = now();
+    return std::max<uint32_t>(1, n / band_rays);
+}
+
+FrameSlot& frame_setup(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg, svlf_precision prec,
+                       float* rgb, float* alpha, float* depth) {
+    require(cam != nullptr, "camera is null");
+    if (cam->width == 0 || cam->height == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "zero-size image");
+    const uint64_t n64 = uint64_t(cam->width) * cam->height;
+    require(n64 < (1ull << 31), "too many pixels in one call");
+    if (prec != SVLF_PRECISION_FP32 && prec != SVLF_PRECISION_FP16 && prec != SVLF_PRECISION_BF16)
+        fail(SVLF_ERR_INVALID_ARGUMENT, "unknown precision");
+    FrameSlot* F = !ctx->slot[0].busy ? &ctx->slot[0] : (!ctx->slot[1].busy ? &ctx->slot[1] : nullptr);
+    if (!F) fail(SVLF_ERR_INVALID_ARGUMENT, "two frames already in flight on this context");
+    F->m = m;
+    F->cam = *cam;
+    F->has_bg = bg != nullptr;
+    for (int i = 0; i < 3; ++i) F->bg[i] = bg ? bg[i] : 0.f;
+    F->prec = prec;
+    F->u_rgb = rgb;
+    F->u_alpha = alpha;
+    F->u_depth = depth;
+    F->direct = is_pinned(rgb) && is_pinned(alpha) && is_pinned(depth);
+    F->n = uint32_t(n64);
+    F->id = ctx->next_frame++;
+    return *F;
+}
+
+// Completes F, redoing it synchronously after a hit-buffer overflow.
+void frame_finish(svlf_ctx* ctx, FrameSlot& F, svlf_render_stats* stats) {
+    struct Release {
+        FrameSlot& f;
+        ~Release() { f.busy = false; }
+    } release{F};
     for (int attempt = 0; attempt < 3; ++attempt) {
-        reset_misc(ctx);
-        uint32_t nb = 0;
-        for (uint32_t r0 = 0; r0 < H; r0 += band_rows, ++nb) {
-            const uint32_t rows = std::min(band_rows, H - r0);
-            const size_t off = size_t(r0) * W, cnt = size_t(rows) * W;
-            uint32_t total = 0;
-            if (prec == SVLF_PRECISION_FP32) total = run_traversal(ctx, m->tree, &dc, r0, rows, uint32_t(cnt));
-            else enqueue_traversal(ctx, m->tree, &dc, r0, rows, uint32_t(cnt));
-            run_decode_composite(ctx, m, uint32_t(cnt), total, bg, prec, d_rgb + off * 3, d_alpha + off,
-                                 d_depth + off);
-            SVLF_CUDA(cudaMemcpyAsync(bctr + 4 * nb, traversal_counters(ctx), 16, cudaMemcpyDeviceToDevice, s));
-            SVLF_CUDA(cudaEventRecord(ctx->band_done[nb], s));
-            SVLF_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_done[nb], 0));
-            cudaStream_t c = ctx->copy_stream;
-            SVLF_CUDA(cudaMemcpyAsync(st_rgb + off * 3, d_rgb + off * 3, cnt * 12, cudaMemcpyDeviceToHost, c));
-            SVLF_CUDA(cudaMemcpyAsync(st_alpha + off, d_alpha + off, cnt * 4, cudaMemcpyDeviceToHost, c));
-            SVLF_CUDA(cudaMemcpyAsync(st_depth + off, d_depth + off, cnt * 4, cudaMemcpyDeviceToHost, c));
-            SVLF_CUDA(cudaEventRecord(ctx->band_copied[nb], c));
-        }
-        // drain bands in order: host copies overlap the GPU's later bands
-        const double t_enq = now();
-        if (trace) std::fprintf(stderr, "enqueue %.3f ms\n", t_enq - t_start);
-        for (uint32_t b = 0; b < nb; ++b) {
-            const double t0 = now();
-            SVLF_CUDA(cudaEventSynchronize(ctx->band_copied[b]));
-            const double t1 = now();
-            if (direct) continue;
-            if (trace) std::fprintf(stderr, "band %u wait %.3f ms (since enqueue %.3f)\n", b, t1 - t0, t1 - t_enq);
-            const size_t off = size_t(b) * band_rows * W;
-            const size_t cnt = size_t(std::min(band_rows, H - b * band_rows)) * W;
-            constexpr size_t kPart = 64 * 1024;  // pixels per host copy task
-            const int parts = int((cnt + kPart - 1) / kPart);
-            ctx->pool->parallel_for(parts, [&](int i) {
-                const size_t p0 = off + size_t(i) * kPart, pc = std::min(kPart, off + cnt - p0);
-                std::memcpy(rgb + p0 * 3, st_rgb + p0 * 3, pc * 12);
-                std::memcpy(alpha + p0, st_alpha + p0, pc * 4);
-                std::memcpy(depth + p0, st_depth + p0, pc * 4);
-            });
-            if (trace) std::fprintf(stderr, "band %u copy %.3f ms\n", b, now() - t1);
-        }
-        SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 16, bctr, 16 * nb, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned + 8, misc_fg(ctx), 8, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaStreamSynchronize(s));
-        uint64_t total = 0, dense = 0, fallback = 0, worst = 0;
-        bool overflow = false;
-        for (uint32_t b = 0; b < nb; ++b) {
-            const uint32_t* c = reinterpret_cast<const uint32_t*>(ctx->h_pinned + 16 + 4 * b);
-            total += c[0];
-            dense += c[1];
-            overflow |= c[2] != 0;
-            fallback += c[3];
-            worst = std::max<uint64_t>(worst, c[0]);
-        }
-        ctx->last_overflow_rays = (long long)fallback;
-        ctx->last_dense_rays = (long long)dense;
-        check_device_error(ctx, overflow);
-        if (trace) std::fprintf(stderr, "final sync at %.3f ms\n", now() - t_start);
-        if (overflow) {
-            ctx->hit_cap = size_t(worst) + worst / 4 + 1024;
-            continue;
-        }
-        unsigned long long fg = 0;
-        std::memcpy(&fg, ctx->h_pinned + 8, 8);
-        float ms[4] = {};  // last band's stage times
-        cudaEventElapsedTime(&ms[0], ctx->ev[EV_START], ctx->ev[EV_COUNT]);
-        cudaEventElapsedTime(&ms[1], ctx->ev[EV_COUNT], ctx->ev[EV_EMIT]);
-        cudaEventElapsedTime(&ms[2], ctx->ev[EV_EMIT], ctx->ev[EV_DECODE]);
-        cudaEventElapsedTime(&ms[3], ctx->ev[EV_DECODE], ctx->ev[EV_COMPOSITE]);
-        ctx->last = svlf_timings{ms[0], ms[1], ms[2], ms[3], 0.f, 0.f, ms[0] + ms[1] + ms[2] + ms[3],
-                                 (long long)total, ctx->last_overflow_rays, ctx->last_dense_rays};
-        if (stats) {
-            stats->rays += n;
-            stats->rays_with_hits += (long long)fg;
-            stats->traversal_hits += (long long)total;
-            stats->thickness_queries += (long long)total;
-            stats->color_queries += (long long)total;
-        }
-        return;
+        if (frame_complete(ctx, F, stats)) return;
+        frame_submit(ctx, F, default_bands(F.n));
     }
     fail(SVLF_ERR_RUNTIME, "traversal output capacity could not be satisfied");
+}
+
+void render_frame_host(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg, svlf_precision prec,
+                       float* rgb, float* alpha, float* depth, svlf_render_stats* stats) {
+    FrameSlot& F = frame_setup(ctx, m, cam, bg, prec, rgb, alpha, depth);
+    F.busy = true;
+    try {
+        frame_submit(ctx, F, default_bands(F.n));
+    } catch (...) {
+        F.busy = false;
+        throw;
+    }
+    frame_finish(ctx, F, stats);
 }
 
 size_t model_param_count(uint32_t V) { return size_t(V) * 96 + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE; }
@@ -541,9 +608,12 @@ svlf_status svlf_ctx_create(int device, svlf_ctx** out) {
         SVLF_CUDA(cudaMallocHost(&ctx->h_pinned, 256));
         for (auto& e2 : ctx->ev) SVLF_CUDA(cudaEventCreate(&e2));
         SVLF_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-        for (int b = 0; b < svlf_ctx::kMaxBands; ++b) {
-            SVLF_CUDA(cudaEventCreateWithFlags(&ctx->band_done[b], cudaEventDisableTiming));
-            SVLF_CUDA(cudaEventCreateWithFlags(&ctx->band_copied[b], cudaEventDisableTiming));
+        for (auto& fs : ctx->slot) {
+            for (int b = 0; b < svlf_ctx::kMaxBands; ++b) {
+                SVLF_CUDA(cudaEventCreateWithFlags(&fs.band_done[b], cudaEventDisableTiming));
+                SVLF_CUDA(cudaEventCreateWithFlags(&fs.band_copied[b], cudaEventDisableTiming));
+            }
+            SVLF_CUDA(cudaMallocHost(&fs.h_ctr, 4 * (4 * svlf_ctx::kMaxBands + 8)));
         }
         ctx->misc.ensure<unsigned long long>(8);
         SVLF_CUDA(cudaMemset(ctx->misc.p, 0, 64));
@@ -560,12 +630,15 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
             if (ctx->nccl) nccl_api().CommDestroy(ctx->nccl);
             cudaStreamSynchronize(ctx->copy_stream);
             for (auto& e : ctx->ev) cudaEventDestroy(e);
-            for (int b = 0; b < svlf_ctx::kMaxBands; ++b) {
-                cudaEventDestroy(ctx->band_done[b]);
-                cudaEventDestroy(ctx->band_copied[b]);
+            for (auto& fs : ctx->slot) {
+                for (int b = 0; b < svlf_ctx::kMaxBands; ++b) {
+                    cudaEventDestroy(fs.band_done[b]);
+                    cudaEventDestroy(fs.band_copied[b]);
+                }
+                if (fs.h_stage) cudaFreeHost(fs.h_stage);
+                if (fs.h_ctr) cudaFreeHost(fs.h_ctr);
             }
             if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
-            if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
             cudaStreamDestroy(ctx->copy_stream);
             cudaStreamDestroy(ctx->own_stream);
         }
@@ -942,6 +1015,37 @@ svlf_status svlf_render_frame(svlf_ctx* ctx, svlf_model* m, const svlf_camera* c
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
         render_frame_host(ctx, m, cam, bg, prec, rgb, alpha, depth, stats);
+    });
+}
+
+svlf_status svlf_render_frame_submit(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg,
+                                     svlf_precision prec, float* rgb, float* alpha, float* depth, uint64_t* ticket) {
+    return guard([&] {
+        require(ctx && m && cam && rgb && alpha && depth && ticket, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        FrameSlot& F = frame_setup(ctx, m, cam, bg, prec, rgb, alpha, depth);
+        F.busy = true;
+        try {
+            frame_submit(ctx, F, 1);  // whole frame: its copies overlap the next submitted frame
+        } catch (...) {
+            F.busy = false;
+            throw;
+        }
+        *ticket = F.id;
+    });
+}
+
+svlf_status svlf_render_frame_wait(svlf_ctx* ctx, uint64_t ticket, svlf_render_stats* stats) {
+    return guard([&] {
+        require(ctx != nullptr, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        FrameSlot* F = nullptr;
+        for (auto& fs : ctx->slot)
+            if (fs.busy && fs.id == ticket) F = &fs;
+        require(F != nullptr, "unknown or already completed frame ticket");
+        frame_finish(ctx, *F, stats);
     });
 }
 

@@ -226,3 +226,30 @@ def test_host_frame_paths_agree(ctx, oracle):
             for a, b in zip(out, ref):
                 assert np.array_equal(a, b)
     assert ref[1].max() > 0.5  # the frame is not empty
+
+
+def test_pipelined_frames(ctx, oracle):
+    """render_frame_submit / wait: two frames in flight give the same bits and statistics as
+    synchronous render_frame calls; a third submit is refused until a wait."""
+    sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=4, n_views=8, view_res=96, res=64, width=640)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    cams = S.hemisphere_cameras(2, 1.8, 11, W, H, 1.5 * W)
+    cameras = [P.Camera.from_record(c, W, H) for c in cams]
+    want, want_st = [], []
+    for c in cameras:
+        st = P.RenderStats()
+        want.append([x.reshape(-1).copy() for x in P.render_frame(model, c, stats=st, precision="fp16")])
+        want_st.append(st)
+    frames = [P.pinned_frame(W, H), (np.empty(3 * W * H, np.float32), np.empty(W * H, np.float32),
+                                     np.empty(W * H, np.float32))]  # page-locked and pageable
+    for _ in range(2):
+        t = [P.render_frame_submit(model, c, f, precision="fp16") for c, f in zip(cameras, frames)]
+        with pytest.raises(ValueError):
+            P.render_frame_submit(model, cameras[0], frames[0], precision="fp16")
+        for k in range(2):
+            st = P.RenderStats()
+            got = t[k].wait(stats=st)
+            for a, b in zip(got, want[k]):
+                assert np.array_equal(a.reshape(-1), b)
+            assert st.traversal_hits == want_st[k].traversal_hits and st.rays_with_hits == want_st[k].rays_with_hits
