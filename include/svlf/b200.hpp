@@ -41,6 +41,9 @@ class DeviceModel {
 
     void render(const Camera& camera, FrameBuffers& out, RenderStats* stats = nullptr,
                 const float* background = nullptr) const;
+    // fp32 CUDA-core decoders in the reference's arithmetic order
+    void render_ref(const Camera& camera, FrameBuffers& out, RenderStats* stats = nullptr,
+                    const float* background = nullptr) const;
     double train_step(std::span<const RaySupervision> batch, LossMode mode, bool color_frozen, float lr,
                       const LossWeights& lw = {}, LossStats* stats = nullptr);
 

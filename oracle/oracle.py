@@ -348,6 +348,10 @@ class Reference:
         L.ref_train.argtypes = [C.c_void_p, _dp, C.c_int, C.c_uint32, C.c_uint32, np.ctypeslib.ndpointer(dtype=np.int32),
                                 C.c_uint32, C.c_uint32, C.c_uint64, _dp, C.c_int, C.POINTER(C.c_int), C.c_void_p]
         L.ref_thread_count.restype = C.c_int
+        L.ref_train2.argtypes = [C.c_void_p, _dp, np.ctypeslib.ndpointer(dtype=np.int32), C.c_int, C.c_uint32,
+                                 C.c_uint32, np.ctypeslib.ndpointer(dtype=np.int32), C.c_uint32, C.c_uint32,
+                                 C.c_uint64, _dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_longlong),
+                                 C.POINTER(C.c_void_p)]
 
     def _err(self):
         return OracleError(self.lib.ref_last_error().decode())
@@ -425,6 +429,24 @@ class Reference:
         self.lib.ref_model_get(h, m.ft, m.fc, m.mt, m.mc)
         self.lib.ref_model_free(h)
         return m
+
+    def train(self, scene, cams, splits, w, h, epochs, grid_res, dilation, seed):
+        """train() (src/train.cpp:364-527) on views rendered by the reference's GT ray caster:
+        returns (log rows [stage, epoch, mean_loss, val_psnr, seconds], skipped rays, Model)."""
+        cams = _f64(cams).reshape(-1, 20)
+        log = np.zeros((256, 5))
+        n_log, skipped, mh = C.c_int(), C.c_longlong(), C.c_void_p()
+        if self.lib.ref_train2(scene.h, cams, np.ascontiguousarray(splits, dtype=np.int32), cams.shape[0], w, h,
+                               np.ascontiguousarray(epochs, dtype=np.int32), grid_res, dilation, seed, log, 256,
+                               C.byref(n_log), C.byref(skipped), C.byref(mh)):
+            raise self._err()
+        sz = np.zeros(4, dtype=np.uintp)
+        self.lib.ref_model_sizes(mh, sz)
+        m = Model(np.zeros(sz[0], np.float32), np.zeros(sz[1], np.float32),
+                  np.zeros(sz[2], np.float32), np.zeros(sz[3], np.float32))
+        self.lib.ref_model_get(mh, m.ft, m.fc, m.mt, m.mc)
+        self.lib.ref_model_free(mh)
+        return log[:n_log.value], skipped.value, m
 
     def _with_model(self, tree, m):
         h = self.lib.ref_model_init(tree.h, 0)

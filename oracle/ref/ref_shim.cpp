@@ -421,4 +421,50 @@ int ref_checkpoint_roundtrip(const char* in, const char* out) {
     });
 }
 
+// train() with explicit splits (0 = train, 1 = val) and the full epoch log:
+// 5 doubles per epoch (stage, epoch, mean_loss, val_psnr, seconds).
+int ref_train2(void* sp, const double* cams, const int* splits, int n_frames, uint32_t w, uint32_t h,
+               const int* epochs, uint32_t grid_res, uint32_t dilation, uint64_t seed, double* log_out,
+               int log_cap, int* log_n, long long* skipped, void** model_out) {
+    const auto* scene = static_cast<AnalyticScene*>(sp);
+    return guarded([&] {
+        SceneDataset ds;
+        ds.width = w;
+        ds.height = h;
+        for (int f = 0; f < n_frames; ++f) {
+            DatasetFrame fr;
+            fr.name = std::to_string(f);
+            fr.split = splits[f] == 1 ? "val" : "train";
+            fr.camera = make_camera(cams + 20 * size_t(f), w, h);
+            fr.rgb = Image::make(w, h, 3);
+            fr.depth = Image::make(w, h, 1);
+            fr.mask = Image::make(w, h, 1);
+            ref_scene_render_gt(const_cast<AnalyticScene*>(scene), cams + 20 * size_t(f), w, h,
+                                fr.rgb.px.data(), fr.depth.px.data(), fr.mask.px.data());
+            ds.frames.push_back(std::move(fr));
+        }
+        TrainConfig cfg;
+        cfg.epochs = {epochs[0], epochs[1], epochs[2]};
+        cfg.grid_resolution = grid_res;
+        cfg.dilation = dilation;
+        cfg.seed = seed;
+        TrainResult r = train(cfg, ds);
+        int k = 0;
+        for (const EpochLog& e : r.log) {
+            if (k < log_cap) {
+                double* o = log_out + 5 * k;
+                o[0] = e.stage;
+                o[1] = e.epoch;
+                o[2] = e.mean_loss;
+                o[3] = e.val_psnr;
+                o[4] = e.seconds;
+            }
+            ++k;
+        }
+        *log_n = k;
+        if (skipped) *skipped = r.skipped_rays;
+        if (model_out) *model_out = new SvlfModel(std::move(r.model));
+    });
+}
+
 }  // extern "C"

@@ -689,6 +689,11 @@ void DeviceModel::render(const Camera& camera, FrameBuffers& out, RenderStats* s
     render_with(m_, camera, out, stats, bg, detail::to_c(render_precision()));
 }
 
+void DeviceModel::render_ref(const Camera& camera, FrameBuffers& out, RenderStats* stats, const float* bg) const {
+    std::lock_guard<std::recursive_mutex> lk(detail::session_mutex());
+    render_with(m_, camera, out, stats, bg, SVLF_PRECISION_FP32);
+}
+
 double DeviceModel::train_step(std::span<const RaySupervision> batch, LossMode mode, bool color_frozen, float lr,
                                const LossWeights& lw, LossStats* stats) {
     std::lock_guard<std::recursive_mutex> lk(detail::session_mutex());

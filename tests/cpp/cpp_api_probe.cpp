@@ -9,6 +9,7 @@
 //   cpp_api_probe train  <outdir>   GPU: loss/grads + two Adam steps
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
@@ -21,6 +22,7 @@
 #include "svlf/octree.hpp"
 #include "svlf/render.hpp"
 #include "svlf/rng.hpp"
+#include "svlf/dataset.hpp"
 #include "svlf/train.hpp"
 
 using namespace svlf;
@@ -257,11 +259,67 @@ int run_train() {
     return 0;
 }
 
+// ds.bin: u32 n, w, h, then per view: 20 f64 camera record (fx fy cx cy c2w[16]),
+// i32 split (0 train, 1 val), rgb w*h*3 f32, depth w*h f32, mask w*h f32.
+// argv: trainloop <dir> e1 e2 e3 grid
+int run_trainloop(int argc, char** argv) {
+    std::ifstream f(g_out + "/ds.bin", std::ios::binary);
+    uint32_t hdr[3];
+    f.read(reinterpret_cast<char*>(hdr), sizeof hdr);
+    SceneDataset ds;
+    ds.width = hdr[1];
+    ds.height = hdr[2];
+    for (uint32_t i = 0; i < hdr[0]; ++i) {
+        double rec[20];
+        int32_t split;
+        f.read(reinterpret_cast<char*>(rec), sizeof rec);
+        f.read(reinterpret_cast<char*>(&split), 4);
+        DatasetFrame fr;
+        fr.name = std::to_string(i);
+        fr.split = split == 1 ? "val" : "train";
+        fr.camera.fx = rec[0];
+        fr.camera.fy = rec[1];
+        fr.camera.cx = rec[2];
+        fr.camera.cy = rec[3];
+        std::copy(rec + 4, rec + 20, fr.camera.camera_to_world.begin());
+        fr.camera.width = ds.width;
+        fr.camera.height = ds.height;
+        fr.rgb = Image::make(ds.width, ds.height, 3);
+        fr.depth = Image::make(ds.width, ds.height, 1);
+        fr.mask = Image::make(ds.width, ds.height, 1);
+        for (Image* im : {&fr.rgb, &fr.depth, &fr.mask})
+            f.read(reinterpret_cast<char*>(im->px.data()), std::streamsize(im->px.size() * 4));
+        ds.frames.push_back(std::move(fr));
+    }
+    require(bool(f), "dataset file");
+    TrainConfig cfg;
+    cfg.epochs = {std::atoi(argv[3]), std::atoi(argv[4]), std::atoi(argv[5])};
+    cfg.grid_resolution = uint32_t(std::atoi(argv[6]));
+    cfg.dilation = 1;
+    cfg.seed = 0;
+    cfg.out_dir = g_out + "/run";
+    (void)argc;
+    const TrainResult r = train(cfg, ds);
+    std::vector<double> log;
+    for (const EpochLog& e : r.log) {
+        const double row[5] = {double(e.stage), double(e.epoch), e.mean_loss, e.val_psnr, e.seconds};
+        log.insert(log.end(), row, row + 5);
+    }
+    dump("train_log.f64", log);
+    dump("trained.f32", flat(r.model));
+    write_tree(r.model.octree);
+    dump("skipped.i64", std::vector<long long>{r.skipped_rays});
+    require(!r.diverged, "diverged");
+    require(!r.checkpoints[3].empty(), "final checkpoint");
+    std::printf("trainloop ok: %zu epochs, final loss %.6f\n", r.log.size(), r.log.empty() ? 0.0 : r.log.back().mean_loss);
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    if (argc != 3) {
-        std::fprintf(stderr, "usage: %s ckpt|render|train <outdir>\n", argv[0]);
+    if (argc < 3) {
+        std::fprintf(stderr, "usage: %s ckpt|render|train|trainloop <outdir> [...]\n", argv[0]);
         return 2;
     }
     g_out = argv[2];
@@ -270,6 +328,7 @@ int main(int argc, char** argv) {
         if (mode == "ckpt") return run_ckpt();
         if (mode == "render") return run_render();
         if (mode == "train") return run_train();
+        if (mode == "trainloop" && argc == 7) return run_trainloop(argc, argv);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 1;

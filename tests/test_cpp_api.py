@@ -143,3 +143,53 @@ def test_cpp_train_matches_oracle(tmp_path, oracle):
             diff = np.abs(a - b)
             assert np.mean(diff > 1e-6) < 1e-3, name
             assert diff.max() <= 2.5e-3, name
+
+
+@pytest.mark.gpu
+def test_cpp_train_driver_matches_reference_train(tmp_path):
+    """svlf::train (stage driver over the GPU train step) vs the reference's train() on the
+    same views (rendered by the reference's ground-truth ray caster): same octree, same
+    epoch schedule and shuffle; per-epoch mean loss within 1e-3 relative, validation PSNR
+    within 0.05 dB, same skipped-ray count, and the final model renders the validation
+    view like the reference's final model (PSNR between them >= 40 dB)."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    if not O.reference_available():
+        pytest.skip("oracle/_ref not built")
+    R = O.Reference()
+    W = 32
+    scene = R.scene_make(7, 4)
+    cams = R.hemisphere_cameras(3, 1.8, 7, W, W, 1.5 * W)
+    splits = np.array([0, 0, 1], np.int32)
+    with open(tmp_path / "ds.bin", "wb") as f:
+        f.write(np.array([3, W, W], np.uint32).tobytes())
+        for k in range(3):
+            rgb, depth, mask = R.scene_render_gt(scene, cams[k], W, W)
+            f.write(cams[k].astype(np.float64).tobytes())
+            f.write(np.array([splits[k]], np.int32).tobytes())
+            for a in (rgb, depth, mask):
+                f.write(np.ascontiguousarray(a, np.float32).tobytes())
+    epochs = (2, 2, 1)
+    _run([PROBE, "trainloop", str(tmp_path), *map(str, epochs), "16"], timeout=900)
+    got = _load(tmp_path, "train_log.f64", np.float64).reshape(-1, 5)
+    want, skipped, wm = R.train(scene, cams, splits, W, W, epochs, 16, 1, 0)
+    assert got.shape == want.shape == (sum(epochs), 5)
+    assert np.array_equal(got[:, :2], want[:, :2])
+    assert np.all(np.abs(got[:, 2] - want[:, 2]) <= 1e-3 * np.abs(want[:, 2]))
+    assert np.all(np.abs(got[:, 3] - want[:, 3]) <= 0.05)
+    assert int(_load(tmp_path, "skipped.i64", np.int64)[0]) == skipped
+    # final models: same tensor sizes, same rendering of the validation view
+    o = O.Oracle()
+    t = _tree(o, tmp_path)
+    V = t.vertex_count
+    g = _split(_load(tmp_path, "trained.f32", np.float32), V)
+    assert g[0].size == wm.ft.size and g[3].size == wm.mc.size
+    ours = o.render_frame(t, O.Model(*g), cams[2], W, W)[0]
+    theirs = o.render_frame(t, wm, cams[2], W, W)[0]
+    mse = float(np.mean((ours.astype(np.float64) - theirs) ** 2))
+    assert mse == 0.0 or 10 * np.log10(1.0 / mse) >= 40.0
+    for name in ("checkpoint_stage1.svlf", "checkpoint_stage2.svlf", "checkpoint_stage3.svlf",
+                 "checkpoint_final.svlf", "train.log"):
+        assert (tmp_path / "run" / name).exists(), name
