@@ -153,6 +153,11 @@ svlf_status svlf_ctx_detach_nccl(svlf_ctx* ctx);
  * of the first context that renders/traverses with it. */
 svlf_status svlf_octree_build(svlf_ctx* ctx, const svlf_grid* grid, const double* points_xyz,
                               size_t n_points, svlf_octree** out);
+/* With a context, svlf_octree_build runs on its GPU (radix sort / unique,
+ * octree_build.cu; byte-identical to the host build); _device takes points
+ * already in device memory (e.g. back-projected on the GPU). */
+svlf_status svlf_octree_build_device(svlf_ctx* ctx, const svlf_grid* grid, const double* d_points_xyz,
+                                     size_t n_points, svlf_octree** out);
 svlf_status svlf_octree_from_leaves(svlf_ctx* ctx, const svlf_grid* grid, const uint64_t* leaf_codes,
                                     size_t n_leaves, svlf_octree** out);
 svlf_status svlf_octree_destroy(svlf_octree* tree);

@@ -189,6 +189,7 @@ def load_library():
         "svlf_ctx_attach_nccl": ([vp, vp, C.c_int, C.c_int], st),
         "svlf_ctx_detach_nccl": ([vp], st),
         "svlf_octree_build": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
+        "svlf_octree_build_device": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
         "svlf_octree_from_leaves": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
         "svlf_octree_destroy": ([vp], st),
         "svlf_octree_get_info": ([vp, C.POINTER(_OctreeInfo)], st),
@@ -383,8 +384,18 @@ class SparseOctree:
         self._level_sizes = [info.level_size[i] for i in range(self.leaf_level + 1)]
 
     @staticmethod
+    def build_device(d_points: int, n: int, grid: GridConfig, ctx: Context) -> "SparseOctree":
+        """GPU build from n x 3 float64 points already in device memory (pointer as int)."""
+        load_library()
+        h = C.c_void_p()
+        g = grid._c()
+        _check(_LIB.svlf_octree_build_device(ctx.handle, C.byref(g), C.c_void_p(d_points), n, C.byref(h)))
+        return SparseOctree(h, ctx, grid)
+
+    @staticmethod
     def build(points, grid: GridConfig, ctx: Context | None = None) -> "SparseOctree":
-        """Host build (no device needed); uploaded on first use by a context."""
+        """With a context: GPU build (byte-identical); without: host build (no device needed,
+        uploaded on first use by a context)."""
         load_library()
         pts = _f64(points).reshape(-1, 3)
         h = C.c_void_p()

@@ -742,7 +742,32 @@ svlf_status svlf_octree_build(svlf_ctx* ctx, const svlf_grid* grid, const double
     const svlf_status st = guard([&] {
         require(grid && out, "null argument");
         require(pts != nullptr || n == 0, "points is null");
-        h = HostOctree::build(std::span<const double>(pts, pts ? 3 * n : 0), *grid);
+        if (!ctx) {  // host-only build (no device needed)
+            h = HostOctree::build(std::span<const double>(pts, pts ? 3 * n : 0), *grid);
+            return;
+        }
+        validate_grid(*grid);
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DevBuf d;
+        double* dp = d.ensure<double>(std::max<size_t>(3 * n, 1));
+        if (n) SVLF_CUDA(cudaMemcpyAsync(dp, pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        h = build_octree_gpu(*grid, dp, n, ctx->stream);
+    });
+    if (st != SVLF_OK) return st;
+    return make_octree(ctx, std::move(h), out);
+}
+
+svlf_status svlf_octree_build_device(svlf_ctx* ctx, const svlf_grid* grid, const double* d_points, size_t n,
+                                     svlf_octree** out) {
+    HostOctree h;
+    const svlf_status st = guard([&] {
+        require(ctx && grid && out, "null argument");
+        require(d_points != nullptr || n == 0, "points is null");
+        validate_grid(*grid);
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        h = build_octree_gpu(*grid, d_points, n, ctx->stream);
     });
     if (st != SVLF_OK) return st;
     return make_octree(ctx, std::move(h), out);

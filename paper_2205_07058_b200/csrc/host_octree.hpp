@@ -18,6 +18,8 @@
 #include <span>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "svlf_b200.h"
 
 namespace svlfb {
@@ -48,6 +50,10 @@ struct HostOctree {
 };
 
 void validate_grid(const svlf_grid& g);
+
+// The same build on the GPU from device-resident points (octree_build.cu);
+// byte-identical result.
+HostOctree build_octree_gpu(const svlf_grid& grid, const double* d_points, size_t n, cudaStream_t s);
 
 // Morton helpers (reference include/svlf/morton.hpp:9-37 convention: x -> bit
 // 3k, y -> 3k+1, z -> 3k+2).
