@@ -41,11 +41,13 @@ def load_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
-def workload(objects: int):
+def workload(objects: int, ctx=None):
+    """C2 inputs; with a context the 100 ground-truth views and their back-projection
+    run on the GPU (bit-identical points, so the same octree)."""
     import paper_2205_07058_b200.synthetic as S
 
     sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=objects, n_views=100, view_res=400, res=256,
-                                                   dilation=1, width=1600)
+                                                   dilation=1, width=1600, ctx=ctx)
     return pts, res, dil, cam, W, H
 
 
@@ -328,10 +330,10 @@ def main():
     device = torch.device("cuda", local)
     import paper_2205_07058_b200 as P
 
-    t_gen = time.perf_counter()
-    pts, res, dil, cam, W, H = workload(args.objects)
-    t_gen = time.perf_counter() - t_gen
     ctx = P.Context(local)
+    t_gen = time.perf_counter()
+    pts, res, dil, cam, W, H = workload(args.objects, ctx)
+    t_gen = time.perf_counter() - t_gen
     stream = torch.cuda.Stream(device)
     ctx.set_stream(stream.cuda_stream)
     tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)

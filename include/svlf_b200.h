@@ -252,6 +252,37 @@ svlf_status svlf_loss_grads(svlf_ctx* ctx, svlf_model* model, const double* rays
                             size_t n, svlf_loss_mode mode, int color_frozen,
                             const svlf_loss_weights* lw, svlf_loss_stats* stats, double* loss_sum);
 
+/* ---- ground truth, occupancy and metrics on the GPU ----
+ * Analytic scene (reference include/svlf/scene.hpp:12-33): spheres n x 7
+ * (center xyz, radius, albedo rgb), boxes n x 9 (lo xyz, hi xyz, albedo rgb),
+ * host arrays. */
+typedef struct svlf_scene_desc {
+    const double* spheres;
+    size_t n_spheres;
+    const double* boxes;
+    size_t n_boxes;
+    double light_dir[3], light_rgb[3], ambient[3], background[3];
+} svlf_scene_desc;
+
+/* generate_dataset's pixel loop (src/dataset.cpp:61-83): raycast + shade per
+ * pixel -> rgb W*H*3, Euclidean depth W*H (0 = background), mask W*H; device
+ * buffers. Bit-exact with the reference built without FMA contraction. */
+svlf_status svlf_render_gt_device(svlf_ctx* ctx, const svlf_scene_desc* scene, const svlf_camera* cam,
+                                  float* d_rgb, float* d_depth, float* d_mask);
+/* train()'s occupancy points (src/train.cpp:376-386): foreground pixels of a
+ * depth map -> ray.at(double(depth)), appended in unspecified order; *n_out =
+ * points produced (SVLF_ERR_CAPACITY when above capacity). */
+svlf_status svlf_backproject_device(svlf_ctx* ctx, const svlf_camera* cam, const float* d_depth, double* d_points,
+                                    size_t capacity, size_t* n_out);
+/* psnr (src/metrics.cpp:57-68) over n values (any channel count). */
+svlf_status svlf_psnr_device(svlf_ctx* ctx, const float* d_pred, const float* d_gt, size_t n_values,
+                             double* psnr);
+/* depth_errors (src/metrics.cpp:115-136): RMSE / MAE over pixels with gt
+ * mask >= 0.5; empty mask -> (0, 0) and *empty_mask = 1. */
+svlf_status svlf_depth_errors_device(svlf_ctx* ctx, const float* d_pred_depth, const float* d_gt_depth,
+                                     const float* d_gt_mask, size_t n_px, double* rmse, double* mae,
+                                     int* empty_mask);
+
 #ifdef __cplusplus
 }
 #endif

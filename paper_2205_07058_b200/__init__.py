@@ -70,6 +70,12 @@ class _LossStats(C.Structure):
     _fields_ = [(n, C.c_longlong) for n in ("rays", "skipped_rays", "eta_skipped")]
 
 
+class _SceneDesc(C.Structure):
+    _fields_ = [("spheres", C.c_void_p), ("n_spheres", C.c_size_t), ("boxes", C.c_void_p), ("n_boxes", C.c_size_t),
+                ("light_dir", C.c_double * 3), ("light_rgb", C.c_double * 3), ("ambient", C.c_double * 3),
+                ("background", C.c_double * 3)]
+
+
 class _OctreeInfo(C.Structure):
     _fields_ = [("leaf_level", C.c_int), ("vertex_count", C.c_uint32), ("leaf_count", C.c_size_t),
                 ("dropped_points", C.c_size_t), ("cell_size", C.c_double), ("level_size", C.c_size_t * 22)]
@@ -183,6 +189,11 @@ def load_library():
         "svlf_ctx_kernel_launches": ([vp], C.c_longlong),
         "svlf_render_frame_submit": ([vp, vp, vp, vp, C.c_int, vp, vp, vp, C.POINTER(C.c_uint64)], st),
         "svlf_render_frame_wait": ([vp, C.c_uint64, vp], st),
+        "svlf_render_gt_device": ([vp, vp, vp, vp, vp, vp], st),
+        "svlf_backproject_device": ([vp, vp, vp, vp, sz, C.POINTER(sz)], st),
+        "svlf_psnr_device": ([vp, vp, vp, sz, C.POINTER(C.c_double)], st),
+        "svlf_depth_errors_device": ([vp, vp, vp, vp, sz, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int)], st),
         "svlf_host_alloc": ([sz, vp], st),
         "svlf_host_free": ([vp], st),
         "svlf_nccl_unique_id": ([vp], st),
@@ -574,6 +585,48 @@ def render_frame(model: Model, camera: Camera, stats: RenderStats | None = None,
     _add_stats(stats, st)
     return (rgb.reshape(camera.height, camera.width, 3), alpha.reshape(camera.height, camera.width),
             depth.reshape(camera.height, camera.width))
+
+
+# ---- ground truth / occupancy / metrics on the GPU (device pointers as ints) ----
+def _scene_desc(scene):
+    sp = np.array([[*c, r, *a] for c, r, a in scene.spheres], np.float64).reshape(-1, 7)
+    bx = np.array([[*lo, *hi, *a] for lo, hi, a in scene.boxes], np.float64).reshape(-1, 9)
+    d = _SceneDesc(sp.ctypes.data if sp.size else None, sp.shape[0], bx.ctypes.data if bx.size else None,
+                   bx.shape[0], (C.c_double * 3)(*scene.light_dir), (C.c_double * 3)(*scene.light_rgb),
+                   (C.c_double * 3)(*scene.ambient), (C.c_double * 3)(*scene.background))
+    return d, (sp, bx)
+
+
+def render_gt_device(ctx: Context, scene, camera: Camera, d_rgb: int, d_depth: int, d_mask: int):
+    """Analytic-scene ground truth (raycast + shade) for every pixel into device buffers."""
+    load_library()
+    desc, keep = _scene_desc(scene)
+    cam = camera._c()
+    _check(_LIB.svlf_render_gt_device(ctx.handle, C.byref(desc), C.byref(cam), C.c_void_p(d_rgb),
+                                      C.c_void_p(d_depth), C.c_void_p(d_mask)))
+
+
+def backproject_device(ctx: Context, camera: Camera, d_depth: int, d_points: int, capacity: int) -> int:
+    """Foreground depth -> world points (n x 3 float64) appended at d_points; returns the count."""
+    n = C.c_size_t()
+    cam = camera._c()
+    _check(_LIB.svlf_backproject_device(ctx.handle, C.byref(cam), C.c_void_p(d_depth), C.c_void_p(d_points),
+                                        capacity, C.byref(n)))
+    return n.value
+
+
+def psnr_device(ctx: Context, d_pred: int, d_gt: int, n_values: int) -> float:
+    out = C.c_double()
+    _check(_LIB.svlf_psnr_device(ctx.handle, C.c_void_p(d_pred), C.c_void_p(d_gt), n_values, C.byref(out)))
+    return out.value
+
+
+def depth_errors_device(ctx: Context, d_pred: int, d_gt: int, d_mask: int, n_px: int):
+    """(rmse, mae, empty_mask) over pixels with gt mask >= 0.5."""
+    r, m, e = C.c_double(), C.c_double(), C.c_int()
+    _check(_LIB.svlf_depth_errors_device(ctx.handle, C.c_void_p(d_pred), C.c_void_p(d_gt), C.c_void_p(d_mask),
+                                         n_px, C.byref(r), C.byref(m), C.byref(e)))
+    return r.value, m.value, bool(e.value)
 
 
 class FrameTicket:

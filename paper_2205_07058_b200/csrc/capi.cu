@@ -646,6 +646,78 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
     });
 }
 
+// ---- ground truth / occupancy / metrics (scene.cu) ---------------------------
+svlf_status svlf_render_gt_device(svlf_ctx* ctx, const svlf_scene_desc* scene, const svlf_camera* cam, float* d_rgb,
+                                  float* d_depth, float* d_mask) {
+    return guard([&] {
+        require(ctx && scene && cam && d_rgb && d_depth && d_mask, "null argument");
+        require(scene->n_spheres == 0 || scene->spheres, "spheres is null");
+        require(scene->n_boxes == 0 || scene->boxes, "boxes is null");
+        if (cam->width == 0 || cam->height == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "zero-size image");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        cudaStream_t s = ctx->stream;
+        double* prims = ctx->tmp64.ensure<double>(scene->n_spheres * 7 + scene->n_boxes * 9 + 1);
+        if (scene->n_spheres)
+            SVLF_CUDA(cudaMemcpyAsync(prims, scene->spheres, scene->n_spheres * 56, cudaMemcpyHostToDevice, s));
+        if (scene->n_boxes)
+            SVLF_CUDA(cudaMemcpyAsync(prims + scene->n_spheres * 7, scene->boxes, scene->n_boxes * 72,
+                                      cudaMemcpyHostToDevice, s));
+        launch_render_gt(*scene, prims, prims + scene->n_spheres * 7, to_dev_camera(*cam), d_rgb, d_depth, d_mask, s);
+        SVLF_CUDA(cudaStreamSynchronize(s));  // the primitive upload buffer is reused by the next call
+    });
+}
+
+svlf_status svlf_backproject_device(svlf_ctx* ctx, const svlf_camera* cam, const float* d_depth, double* d_points,
+                                    size_t capacity, size_t* n_out) {
+    return guard([&] {
+        require(ctx && cam && d_depth && n_out, "null argument");
+        require(d_points != nullptr || capacity == 0, "points is null");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        cudaStream_t s = ctx->stream;
+        unsigned long long* cnt = ctx->tmpx12.ensure<unsigned long long>(1);
+        SVLF_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+        launch_backproject(to_dev_camera(*cam), d_depth, d_points, capacity, cnt, s);
+        SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned, cnt, 8, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        unsigned long long k = 0;
+        std::memcpy(&k, ctx->h_pinned, 8);
+        *n_out = size_t(k);
+        if (k > capacity) fail(SVLF_ERR_CAPACITY, "back-projected points exceed the capacity");
+    });
+}
+
+svlf_status svlf_psnr_device(svlf_ctx* ctx, const float* d_pred, const float* d_gt, size_t n, double* psnr) {
+    return guard([&] {
+        require(ctx && d_pred && d_gt && psnr, "null argument");
+        if (n == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "empty image");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        std::vector<double> h(reduction_partials());
+        const double se = device_sq_err(d_pred, d_gt, n, ctx->tmp64.ensure<double>(reduction_partials()), h.data(),
+                                        ctx->stream);
+        const double mse = se / double(n);
+        *psnr = mse == 0.0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / mse));
+    });
+}
+
+svlf_status svlf_depth_errors_device(svlf_ctx* ctx, const float* pd, const float* gd, const float* gm, size_t n,
+                                     double* rmse, double* mae, int* empty) {
+    return guard([&] {
+        require(ctx && pd && gd && gm && rmse && mae, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        std::vector<double> h(reduction_partials());
+        double s2 = 0, s1 = 0, c = 0;
+        device_depth_err(pd, gd, gm, n, ctx->tmp64.ensure<double>(reduction_partials()), h.data(), &s2, &s1, &c,
+                         ctx->stream);
+        if (empty) *empty = c == 0.0;
+        *rmse = c > 0 ? std::sqrt(s2 / c) : 0.0;
+        *mae = c > 0 ? s1 / c : 0.0;
+    });
+}
+
 svlf_status svlf_host_alloc(size_t bytes, void** out) {
     return guard([&] {
         require(out != nullptr, "out is null");

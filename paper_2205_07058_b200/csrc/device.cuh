@@ -160,4 +160,14 @@ void launch_gather_leaf_codes(const uint64_t* leaf_codes, const uint32_t* hit_le
 void launch_hit_points(const double* rays, const uint32_t* hit_ray, const double* tin,
                        const double* tout, double* x12, size_t n, cudaStream_t s);
 
+// scene.cu: ground truth, occupancy back-projection, metrics
+void launch_render_gt(const svlf_scene_desc& d, const double* d_spheres, const double* d_boxes, const DevCamera& cam,
+                      float* rgb, float* depth, float* mask, cudaStream_t s);
+void launch_backproject(const DevCamera& cam, const float* depth, double* pts, size_t cap, unsigned long long* count,
+                        cudaStream_t s);
+double device_sq_err(const float* pred, const float* gt, size_t n, double* part, double* h_part, cudaStream_t s);
+void device_depth_err(const float* pd, const float* gd, const float* gm, size_t n, double* part, double* h_part,
+                      double* sum2, double* sum1, double* count, cudaStream_t s);
+size_t reduction_partials();
+
 }  // namespace svlfb

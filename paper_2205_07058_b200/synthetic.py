@@ -332,13 +332,37 @@ def c1_workload():
     return pts, 64, 0, cam, 200, 200
 
 
-def rtmv_workload(n_objects=4, n_views=100, view_res=400, res=256, dilation=1, width=1600, seed=7):
+def occupancy_points_gpu(ctx, sc: Scene, cams, width, height):
+    """occupancy_points via the GPU ground truth + back-projection (bit-identical
+    depth and points; order differs, which the octree build ignores) -> numpy."""
+    import torch
+
+    import paper_2205_07058_b200 as P
+
+    n = width * height
+    dev = torch.device("cuda", ctx.device)
+    rgb = torch.empty(3 * n, dtype=torch.float32, device=dev)
+    depth = torch.empty(n, dtype=torch.float32, device=dev)
+    mask = torch.empty(n, dtype=torch.float32, device=dev)
+    pts = torch.empty((len(cams) * n, 3), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    total = 0
+    for c in cams:
+        cam = P.Camera.from_record(c, width, height)
+        P.render_gt_device(ctx, sc, cam, rgb.data_ptr(), depth.data_ptr(), mask.data_ptr())
+        total += P.backproject_device(ctx, cam, depth.data_ptr(), pts.data_ptr() + total * 24, n)
+    return pts[:total].cpu().numpy()
+
+
+def rtmv_workload(n_objects=4, n_views=100, view_res=400, res=256, dilation=1, width=1600, seed=7, ctx=None):
     """Config 2: RTMV-shaped scene (make_random_scene(7, n)), occupancy from
     n_views hemisphere depth maps at view_res^2, octree res 256 (depth 8),
-    render width^2 at focal 1.5*width from the survey's eye direction."""
+    render width^2 at focal 1.5*width from the survey's eye direction.
+    With a context the ground truth and back-projection run on the GPU."""
     sc = make_random_scene(seed, n_objects)
     cams = hemisphere_cameras(n_views, 1.8, seed, view_res, view_res, 1.5 * view_res)
-    pts = occupancy_points(sc, cams, view_res, view_res)
+    pts = (occupancy_points_gpu(ctx, sc, cams, view_res, view_res) if ctx is not None
+           else occupancy_points(sc, cams, view_res, view_res))
     eye = tuple(0.5 + 1.8 * c for c in C1_EYE_DIR)
     cam = lookat_camera(eye, (0.5, 0.5, 0.5), width, width, 1.5 * width)
     return sc, pts, res, dilation, cam, width, width
@@ -354,3 +378,42 @@ def c3_workload(width=512, objects=4, res=256, dilation=1, seed=7):
     pts = backproject(cam, width, width, depth)
     rays = camera_rays(cam, width, width)
     return sc, cam, pts, res, dilation, rays, rgb.reshape(-1, 3), depth.astype(np.float64), (mask > 0.5)
+
+
+def render_gt_gpu(ctx, sc: Scene, cam, width, height):
+    """render_gt on the GPU (svlf_render_gt_device) -> numpy (rgb, depth, mask)."""
+    import torch
+
+    import paper_2205_07058_b200 as P
+
+    n = width * height
+    dev = torch.device("cuda", ctx.device)
+    rgb = torch.empty(3 * n, dtype=torch.float32, device=dev)
+    depth = torch.empty(n, dtype=torch.float32, device=dev)
+    mask = torch.empty(n, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize(dev)
+    P.render_gt_device(ctx, sc, P.Camera.from_record(cam, width, height), rgb.data_ptr(), depth.data_ptr(),
+                       mask.data_ptr())
+    return rgb.cpu().numpy(), depth.cpu().numpy(), mask.cpu().numpy()
+
+
+def occupancy_octree_gpu(ctx, sc: Scene, cams, width, height, grid):
+    """train()'s occupancy pipeline entirely on the GPU: ground-truth depth per view,
+    back-projection of the foreground, octree build from the device-resident points."""
+    import torch
+
+    import paper_2205_07058_b200 as P
+
+    n = width * height
+    dev = torch.device("cuda", ctx.device)
+    rgb = torch.empty(3 * n, dtype=torch.float32, device=dev)
+    depth = torch.empty(n, dtype=torch.float32, device=dev)
+    mask = torch.empty(n, dtype=torch.float32, device=dev)
+    pts = torch.empty((len(cams) * n, 3), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    total = 0
+    for c in cams:
+        cam = P.Camera.from_record(c, width, height)
+        P.render_gt_device(ctx, sc, cam, rgb.data_ptr(), depth.data_ptr(), mask.data_ptr())
+        total += P.backproject_device(ctx, cam, depth.data_ptr(), pts.data_ptr() + total * 24, n)
+    return P.SparseOctree.build_device(pts.data_ptr(), total, grid, ctx), total
