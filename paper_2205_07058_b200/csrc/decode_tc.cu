@@ -202,17 +202,17 @@ __device__ __forceinline__ void hit_geom_regs(const DevOctree& T, const double* 
     ray_at(ray, tin, x1);
     ray_at(ray, tout, x2);
     float r6[6] = {0, 0, 0, 0, 0, 0}, w1[8], w2[8];
+    double u1[3] = {0, 0, 0}, u2[3] = {0, 0, 0};  // local coordinates (features.cpp:22-31)
     if (!parameterize(ray, lo, hi, r6)) raise_error(err, kErrTangentRay);
-    if (!trilinear_at(x1, lo, hi, T.cell_size, w1) || !trilinear_at(x2, lo, hi, T.cell_size, w2)) {
+    if (!trilinear_at(x1, lo, hi, T.cell_size, w1, u1) || !trilinear_at(x2, lo, hi, T.cell_size, w2, u2)) {
         raise_error(err, kErrPointNotInVoxel);
 #pragma unroll
         for (int b = 0; b < 8; ++b) w1[b] = w2[b] = 0.f;
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        // local coordinates (p - lo)/h clamped to [0,1] (features.cpp:22-31)
-        u[a] = float(fmin(fmax(ddiv(dsub(x1[a], lo[a]), T.cell_size), 0.0), 1.0));
-        u[3 + a] = float(fmin(fmax(ddiv(dsub(x2[a], lo[a]), T.cell_size), 0.0), 1.0));
+        u[a] = float(u1[a]);
+        u[3 + a] = float(u2[a]);
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) r6p[i] = F::pack(r6[2 * i], r6[2 * i + 1]);

@@ -181,9 +181,10 @@ __device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, con
 }
 
 // local_coords + trilinear_weights (features.cpp:22-31, features.hpp:13-21).
-// Returns false on "point not in voxel".
+// Returns false on "point not in voxel". The clamped local coordinates are
+// also returned when `u_out` is given.
 __device__ __forceinline__ bool trilinear_at(const double* p, const double* lo, const double* hi,
-                                             double h, float* w) {
+                                             double h, float* w, double* u_out = nullptr) {
     double u[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -197,6 +198,9 @@ __device__ __forceinline__ bool trilinear_at(const double* p, const double* lo, 
         const double wz = (b & 4) ? u[2] : dsub(1.0, u[2]);
         w[b] = float(dmul(dmul(wx, wy), wz));
     }
+    if (u_out)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) u_out[a] = u[a];
     return true;
 }
 
