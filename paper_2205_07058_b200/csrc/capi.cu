@@ -187,6 +187,10 @@ const DevOctree& dev_view(const svlf_octree* t) {
         v.hi[a] = h.grid.hi[a];
     }
     v.cell_size = h.cell_size;
+    {
+        int e = 0;
+        v.inv_cell_pow2 = std::frexp(h.cell_size, &e) == 0.5 ? 1.0 / h.cell_size : 0.0;
+    }
     v.L = h.leaf_level;
     v.res = h.grid.resolution;
     v.n_leaves = uint32_t(h.leaves().size());

@@ -204,7 +204,7 @@ __device__ __forceinline__ void hit_geom_regs(const DevOctree& T, const double* 
     float r6[6] = {0, 0, 0, 0, 0, 0}, w1[8], w2[8];
     double u1[3] = {0, 0, 0}, u2[3] = {0, 0, 0};  // local coordinates (features.cpp:22-31)
     if (!parameterize(ray, lo, hi, r6)) raise_error(err, kErrTangentRay);
-    if (!trilinear_at(x1, lo, hi, T.cell_size, w1, u1) || !trilinear_at(x2, lo, hi, T.cell_size, w2, u2)) {
+    if (!trilinear_at(x1, lo, hi, T, w1, u1) || !trilinear_at(x2, lo, hi, T, w2, u2)) {
         raise_error(err, kErrPointNotInVoxel);
 #pragma unroll
         for (int b = 0; b < 8; ++b) w1[b] = w2[b] = 0.f;

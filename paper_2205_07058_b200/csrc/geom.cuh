@@ -25,6 +25,7 @@ struct DevOctree {
     double cell[kMaxLevelsDev + 1];  // extent / (1u << level), src/octree.cpp:205
     double lo[3];
     double cell_size;                // extent / resolution (voxel_aabb, local_coords)
+    double inv_cell_pow2;            // 1 / cell_size when cell_size is a power of two, else 0
     double hi[3];
     int L;
     uint32_t res;
@@ -180,16 +181,24 @@ __device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, con
     return true;
 }
 
+// x / cell_size. When the cell size is a power of two (the unit scene box
+// with a power-of-two resolution, and many others) the division is an exact
+// scaling, identical bit for bit to the multiplication by the exact
+// reciprocal, which is much cheaper in fp64.
+__device__ __forceinline__ double div_cell(const DevOctree& T, double x) {
+    return T.inv_cell_pow2 != 0.0 ? dmul(x, T.inv_cell_pow2) : ddiv(x, T.cell_size);
+}
+
 // local_coords + trilinear_weights (features.cpp:22-31, features.hpp:13-21).
 // Returns false on "point not in voxel". The clamped local coordinates are
 // also returned when `u_out` is given.
 __device__ __forceinline__ bool trilinear_at(const double* p, const double* lo, const double* hi,
-                                             double h, float* w, double* u_out = nullptr) {
+                                             const DevOctree& T, float* w, double* u_out = nullptr) {
     double u[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         if (!(p[a] >= dsub(lo[a], 1e-7) && p[a] <= dadd(hi[a], 1e-7))) return false;
-        u[a] = fmin(fmax(ddiv(dsub(p[a], lo[a]), h), 0.0), 1.0);
+        u[a] = fmin(fmax(div_cell(T, dsub(p[a], lo[a])), 0.0), 1.0);
     }
 #pragma unroll
     for (int b = 0; b < 8; ++b) {

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kDecBlock) k_decode_f32(DevOctree T, DevModel 
         corners[4] = b.x; corners[5] = b.y; corners[6] = b.z; corners[7] = b.w;
     }
     float w1[8], w2[8];
-    if (!trilinear_at(x1, lo, hi, T.cell_size, w1) || !trilinear_at(x2, lo, hi, T.cell_size, w2)) {
+    if (!trilinear_at(x1, lo, hi, T, w1) || !trilinear_at(x2, lo, hi, T, w2)) {
         raise_error(err, kErrPointNotInVoxel);
         return;
     }
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kDecBlock) k_decode_f32(DevOctree T, DevModel 
 #pragma unroll
     for (int a = 0; a < 3; ++a) xs[a] = dadd(dmul(x1[a], e), dmul(x2[a], ome));
     float ws[8];
-    if (!trilinear_at(xs, lo, hi, T.cell_size, ws)) {
+    if (!trilinear_at(xs, lo, hi, T, ws)) {
         raise_error(err, kErrPointNotInVoxel);
         return;
     }

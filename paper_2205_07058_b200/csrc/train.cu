@@ -95,7 +95,7 @@ __global__ void k_prep(DevOctree T, PrepArgs A, int* err) {
             uint32_t c[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const uint32_t q = uint32_t(ddiv(dsub(p[a], T.lo[a]), T.cell_size));
+                const uint32_t q = uint32_t(div_cell(T, dsub(p[a], T.lo[a])));
                 c[a] = q < T.res - 1 ? q : T.res - 1;
             }
             uint64_t code = 0;
@@ -194,7 +194,7 @@ __device__ __forceinline__ bool hit_geom(const DevOctree& T, const HitArgs& H, u
         raise_error(err, kErrTangentRay);
         return false;
     }
-    if (!trilinear_at(g.x1, g.lo, g.hi, T.cell_size, g.w1) || !trilinear_at(g.x2, g.lo, g.hi, T.cell_size, g.w2)) {
+    if (!trilinear_at(g.x1, g.lo, g.hi, T, g.w1) || !trilinear_at(g.x2, g.lo, g.hi, T, g.w2)) {
         raise_error(err, kErrPointNotInVoxel);
         return false;
     }
@@ -213,7 +213,7 @@ __device__ __forceinline__ bool xs_coords(const DevOctree& T, const HitGeom& g, 
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         if (!(xs[a] >= dsub(g.lo[a], 1e-7) && xs[a] <= dadd(g.hi[a], 1e-7))) return false;
-        u[a] = fmin(fmax(ddiv(dsub(xs[a], g.lo[a]), T.cell_size), 0.0), 1.0);
+        u[a] = fmin(fmax(div_cell(T, dsub(xs[a], g.lo[a])), 0.0), 1.0);
     }
     return true;
 }
