@@ -158,7 +158,9 @@ __device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, con
         c[a] = dmul(dadd(lo[a], hi[a]), 0.5);
         oc[a] = dsub(r.o[a], c[a]);
     }
-    const double radius = dmul(dmul(0.5, __dsqrt_rn(3.0)), dsub(hi[0], lo[0]));
+    // 0.5 * sqrt(3.0): the correctly rounded sqrt(3) is 0x3FFBB67AE8584CAA
+    constexpr double kHalfSqrt3 = 0.5 * 1.7320508075688772;
+    const double radius = dmul(kHalfSqrt3, dsub(hi[0], lo[0]));
     const double b = dot3(oc, r.d);
     const double cc = dsub(dot3(oc, oc), dmul(radius, radius));
     const double disc = dsub(dmul(b, b), cc);
