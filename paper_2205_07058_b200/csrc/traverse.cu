@@ -230,6 +230,7 @@ struct BfsSmem {
     uint32_t rcount[kR], roff[kR];
     uint32_t gray[kR];
     uint32_t n_q, base, overflow;
+    unsigned long long unsorted;  // rays whose segment needs the insertion sort
     typename cub::BlockScan<uint32_t, kT>::TempStorage scan;
 };
 
@@ -326,9 +327,11 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             }
         }
     }
+    static_assert(kR <= 64, "per-tile ray mask");
     if (tid == 0) {
         S.n_q = 0;
         S.overflow = 0;
+        S.unsorted = 0;
     }
     tile_sync<kT>();
     {
@@ -511,11 +514,29 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         }
     }
     tile_sync<kT>();
+    // The front-to-back expansion already emits each ray's leaves in t_in order
+    // except at ties; a parallel, coalesced pass over the tile's hits finds the
+    // segments with an inversion, and only those get the serial insertion sort.
+    if (leaf_pass && fits) {
+        for (uint32_t e = tid; e + 1 < total; e += kT) {
+            const uint32_t w = gbase + e;
+            if (A.hit_ray[w] != A.hit_ray[w + 1]) continue;
+            const double t0 = A.hit_tin[w], t1 = A.hit_tin[w + 1];
+            if (t0 < t1 || (t0 == t1 && A.hit_leaf[w] < A.hit_leaf[w + 1])) continue;
+            for (uint32_t r = 0; r < uint32_t(kR); ++r)
+                if (S.rcount[r] && S.roff[r] <= e && e < S.roff[r] + S.rcount[r]) {
+                    atomicOr(&S.unsorted, 1ull << r);
+                    break;
+                }
+        }
+    }
+    tile_sync<kT>();
     if (tid < kR && S.gray[tid] != 0xffffffffu && fits) {
         const uint32_t c = S.rcount[tid], b = gbase + S.roff[tid];
         A.ray_off[S.gray[tid]] = b;
         A.ray_cnt[S.gray[tid]] = c;
         // insertion sort of the (nearly sorted) segment by (t_in, leaf index), carrying t_out
+        if ((S.unsorted >> tid) & 1ull)
         for (uint32_t a = b + 1; a < b + c; ++a) {
             const double ti = A.hit_tin[a], to = A.hit_tout[a];
             const uint32_t lf = A.hit_leaf[a];
