@@ -222,6 +222,23 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
         e2e.append((time.perf_counter() - t0) * 1e3)
     e2e_ms = max_over_ranks(statistics.median(e2e), dist, device)
     hits = int(statistics.median(p["hits"] for p in parts))
+    # the same step with the dense layers on tensor cores (TF32 operands, 16-bit tolerance mode)
+    ctx.set_train_precision("tf32")
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            step()
+        stream.synchronize()
+        tf_ms = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b_.record(stream)
+            stream.synchronize()
+            tf_ms.append(a.elapsed_time(b_))
+    ctx.set_train_precision("fp32")
+    tf_step_ms = max_over_ranks(statistics.median(tf_ms), dist, device)
     if world > 1:
         ctx.detach_nccl()
     out = {"metric": "train rays/s (C3: 2^18-ray 512x512 batch, stage-3 volumetric step incl. Adam)",
@@ -230,7 +247,10 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
            "rays": n, "active_hits": hits, "vertices": int(tree.vertex_count), "leaves": int(tree.leaf_count),
            "stages_ms": {k: round(statistics.median(p[k] for p in parts), 4)
                          for k in ("traverse_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms")},
-           "dtype": "fp32 (reference accumulation order) / f64 geometry and loss",
+           "dtype": "fp32 dense layers (cuBLAS pedantic SGEMM) / f64 geometry and loss",
+           "tf32": {"value": round(world * n / (tf_step_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
+                    "ms_per_step": round(tf_step_ms, 4),
+                    "note": "weight-gradient GEMMs on tensor cores with TF32 operands (gradient gate 2e-2)"},
            "e2e": {"value": round(world * n / (e2e_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
                    "h2d_bytes_per_step": n * (48 + 12 + 8 + 1), "d2h_bytes_per_step": 8,
                    "api": "paper_2205_07058_b200.train_step (C ABI svlf_train_step, host batch)"}}

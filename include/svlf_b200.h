@@ -58,7 +58,8 @@ typedef enum svlf_status {
 typedef enum svlf_precision {
     SVLF_PRECISION_FP32 = 0,
     SVLF_PRECISION_BF16 = 1,
-    SVLF_PRECISION_FP16 = 2
+    SVLF_PRECISION_FP16 = 2,
+    SVLF_PRECISION_TF32 = 3 /* train step only: dense layers on tensor cores with TF32 operands */
 } svlf_precision;
 
 /* reference LossMode (src/train.cpp:37): stage 1 = SURFACE, stages 2-3 = VOLUMETRIC */
@@ -127,6 +128,12 @@ svlf_status svlf_ctx_synchronize(svlf_ctx* ctx);
  * context's own stream. */
 svlf_status svlf_ctx_set_stream(svlf_ctx* ctx, void* cuda_stream);
 svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out);
+/* Arithmetic of the train step's dense layers: SVLF_PRECISION_FP32 (default:
+ * true fp32, gradients within 1e-4 of the reference) or SVLF_PRECISION_TF32
+ * (the weight-gradient GEMMs on tensor cores with TF32 operands and fp32
+ * accumulation; forward and input gradients stay fp32; gradients within
+ * 2e-2, the 16-bit tolerance of SURVEY.md §8(c)). */
+svlf_status svlf_ctx_set_train_precision(svlf_ctx* ctx, svlf_precision precision);
 /* Count of this library's kernel launches on the context since creation. */
 long long svlf_ctx_kernel_launches(const svlf_ctx* ctx);
 

@@ -196,6 +196,7 @@ def load_library():
                                       C.POINTER(C.c_int)], st),
         "svlf_host_alloc": ([sz, vp], st),
         "svlf_host_free": ([vp], st),
+        "svlf_ctx_set_train_precision": ([vp, C.c_int], st),
         "svlf_nccl_unique_id": ([vp], st),
         "svlf_ctx_attach_nccl": ([vp, vp, C.c_int, C.c_int], st),
         "svlf_ctx_detach_nccl": ([vp], st),
@@ -305,6 +306,10 @@ class Context:
     @staticmethod
     def kernel_launches() -> int:
         return int(load_library().svlf_ctx_kernel_launches(None))
+
+    def set_train_precision(self, precision: str):
+        """'fp32' (default, true fp32 dense layers) or 'tf32' (tensor cores, TF32 operands)."""
+        _check(_LIB.svlf_ctx_set_train_precision(self._h, {**_PREC, "tf32": 3}[precision]))
 
     def attach_nccl(self, unique_id: bytes, rank: int, world: int):
         """Data-parallel training: all-reduce loss, statistics and gradients over NCCL."""

@@ -745,12 +745,15 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
         const CublasApi& B = cublas_api();
         cublasHandle_t hb = nullptr;
         cublas_check(B.Create(&hb), "cublasCreate");
-        cublas_check(B.SetMathMode(hb, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true fp32, no TF32
         S.blas = hb;
     }
     const CublasApi& B = cublas_api();
     cublasHandle_t hb = static_cast<cublasHandle_t>(S.blas);
     cublas_check(B.SetStream(hb, s), "cublasSetStream");
+    // true fp32 (no TF32) for the forward and input-gradient GEMMs; the weight-
+    // gradient GEMMs (reductions over all hits, the bulk of the GEMM time) run
+    // on tensor cores with TF32 operands when the context asks for it
+    cublas_check(B.SetMathMode(hb, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");
     const float one = 1.f, zero = 0.f;
     const int Ni = int(N);
     // Y(O x N) = W X: rows [xrow, xrow+K) -> [yrow, yrow+O) of acts
@@ -825,6 +828,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
         layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(N));
         k_bwd_feat_t<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
         // weight gradients (sums over hits)
+        if (o.tf32) cublas_check(B.SetMathMode(hb, CUBLAS_TF32_TENSOR_OP_MATH), "cublasSetMathMode");
         layer_dw(D_T0, kHid, A_XT, kInT, g_mt + D::T_W0, g_mt + D::T_B0);
         layer_dw(D_T1, 2, A_HT, kHid, g_mt + D::T_W1, g_mt + D::T_B1);
         if (!o.color_frozen) {

@@ -29,6 +29,7 @@ struct TrainOptions {
     float lr;
     void* nccl_comm = nullptr;  // ncclComm_t: data-parallel gradient exchange when set
     int world = 1;
+    bool tf32 = false;          // dense layers on tensor cores (TF32 operands)
 };
 
 struct TrainModelRefs {

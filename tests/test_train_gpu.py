@@ -138,3 +138,31 @@ def test_nccl_attached_single_rank_matches_local(batch, oracle):
         assert np.abs(x - y).max() <= 2.5e-3
     assert mb.get_adam()[2].tolist() == [2] * 14
     b.detach_nccl()
+
+
+@pytest.mark.parametrize("mode,frozen,lw", MODES)
+def test_tf32_train_mode_within_16bit_tolerance(batch, oracle, mode, frozen, lw):
+    """TF32 mode (weight-gradient GEMMs on tensor cores): loss within 1e-3 relative and gradients within
+    rel-L2 2e-2 per tensor of the oracle (SURVEY.md §8(c) 16-bit-mode gates)."""
+    tree, otree, rays, cgt, depth, alpha = batch
+    c = P.Context(0)
+    c.set_train_precision("tf32")
+    t = P.SparseOctree.from_leaves(tree.leaf_codes, tree.config, c)
+    model = P.Model(t, seed=0, ctx=c)
+    om = oracle.init_model(otree, 0)
+    st = P.LossStats()
+    loss = P.loss_grads(model, rays, cgt, depth, alpha, mode=mode, color_frozen=frozen,
+                        weights=P.LossWeights(*lw), stats=st)
+    oloss, og, ost = oracle.loss(otree, om, rays, cgt, depth, alpha, 0 if mode == "surface" else 1, lw=lw,
+                                 frozen=frozen)
+    assert abs(loss - oloss) <= 1e-3 * abs(oloss)
+    assert [st.rays, st.skipped_rays, st.eta_skipped] == list(ost)
+    for name, a, b in zip(("feat_t", "feat_c", "dec_t", "dec_c"), model.get_grads(), (og.ft, og.fc, og.mt, og.mc)):
+        if frozen and name in ("feat_c", "dec_c"):
+            assert not np.any(a), name
+            continue
+        assert _rel_l2(a, b) <= 2e-2, (name, _rel_l2(a, b))
+    with pytest.raises(ValueError):
+        c.set_train_precision("fp16")
+    del model, t
+    c.close()
