@@ -253,3 +253,25 @@ def test_pipelined_frames(ctx, oracle):
             for a, b in zip(got, want[k]):
                 assert np.array_equal(a.reshape(-1), b)
             assert st.traversal_hits == want_st[k].traversal_hits and st.rays_with_hits == want_st[k].rays_with_hits
+
+
+@pytest.mark.parametrize("res", [512, 1024])
+def test_deep_octree_render_matches_oracle(ctx, oracle, res):
+    """Octree depth 9-10 (C5-scale resolution): traversal hit lists bit-exact and the fp32
+    render within 1e-3 of the oracle on a small frame of the RTMV-shaped scene."""
+    sc = S.make_random_scene(7, 4)
+    cams = S.hemisphere_cameras(12, 1.8, 7, 160, 160, 240.0)
+    pts = S.occupancy_points(sc, cams, 160, 160)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=1), ctx)
+    otree = oracle.tree_build(pts, res, 1)
+    assert tree.leaf_level == otree.leaf_level and tree.vertex_count == otree.vertex_count
+    W = 64
+    cam = S.lookat_camera((0.5 + 1.8 * 0.6, 0.5 + 1.8 * 0.3, 0.5 + 1.8 * 0.7416), (0.5, 0.5, 0.5), W, W, 1.5 * W)
+    rays = oracle.camera_rays(cam, W, W)
+    _assert_hits_equal(tree.traverse(rays), oracle.traverse(otree, rays))
+    model = P.Model(tree, seed=1, ctx=ctx)
+    om = oracle.init_model(otree, 1)
+    rgb, a, d = P.render_frame(model, P.Camera.from_record(cam, W, W), precision="fp32")
+    orgb, oa, od, _ = oracle.render_frame(otree, om, cam, W, W)
+    assert np.abs(rgb.reshape(-1) - orgb).max() <= TOL_FP32
+    assert np.abs(d.reshape(-1) - od).max() <= TOL_FP32
