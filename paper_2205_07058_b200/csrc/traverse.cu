@@ -210,14 +210,17 @@ __device__ __forceinline__ void sort_segment(TinArr tin, LeafArr leaf, uint32_t 
 #define SVLF_RAYS_DENSE 16
 #endif
 #ifndef SVLF_DENSE_QCAP
-#define SVLF_DENSE_QCAP 2048
+#define SVLF_DENSE_QCAP 1536
 #endif
 constexpr int kRays = SVLF_BFS_RAYS;         // rays per tile, first pass
 constexpr int kThreads = SVLF_BFS_THREADS;   // threads per tile, first pass
 constexpr int kBlockThreads = SVLF_BFS_BLOCK;  // threads per block, first pass
 constexpr int kQCap = SVLF_BFS_QCAP;         // (ray, node) pairs per level, first pass
 constexpr int kRaysDense = SVLF_RAYS_DENSE;  // rays per block, second pass
-constexpr int kThreadsDense = 256;
+#ifndef SVLF_DENSE_THREADS
+#define SVLF_DENSE_THREADS 256
+#endif
+constexpr int kThreadsDense = SVLF_DENSE_THREADS;
 constexpr int kQCapDense = SVLF_DENSE_QCAP;
 
 template <int kR, int kQ, int kT>
