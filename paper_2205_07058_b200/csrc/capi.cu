@@ -267,7 +267,7 @@ void enqueue_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* 
     ctx->hit_cap = cap;
     TraverseOut o{ray_off, ray_cnt, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
                   ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), counters, ovl, ovl2, rays, uint32_t(cap)};
-    SVLF_CUDA(cudaMemsetAsync(counters, 0, 16, s));
+    SVLF_CUDA(cudaMemsetAsync(counters, 0, 28, s));  // hit/overflow counters + tile cursors
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
     launch_traverse(dev_view(tree), cam, row0, rows, n, o, s);
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));

@@ -232,7 +232,7 @@ struct BfsSmem {
     uint8_t qray[2][kQ];
     uint32_t rcount[kR], roff[kR];
     uint32_t gray[kR];
-    uint32_t n_q, base, overflow;
+    uint32_t n_q, base, overflow, next_tile;
     unsigned long long unsorted;  // rays whose segment needs the insertion sort
     typename cub::BlockScan<uint32_t, kT>::TempStorage scan;
 };
@@ -244,7 +244,8 @@ struct BfsArgs {
     double* hit_tin;
     double* hit_tout;
     uint32_t* hit_ray;
-    uint32_t* counters;  // [0] hits allocated, [1] overflow rays, [2] capacity exceeded, [3] dense overflow
+    uint32_t* counters;  // [0] hits allocated, [1] overflow rays, [2] capacity exceeded, [3] dense overflow,
+                         // [5] / [6] next tile of the first / second cooperative pass
     uint32_t* overflow_rays;
     uint32_t* overflow_dense;
     double* rays;
@@ -580,7 +581,15 @@ __global__ void __launch_bounds__(kBlock) k_traverse_bfs(DevOctree T, DevCamera 
     const uint32_t g = threadIdx.x / kT;
     auto& S = reinterpret_cast<BfsSmem<kR, kQ, kT>*>(bfs_smem)[g];
     const uint32_t tiles = kList ? (A.counters[1] + kR - 1) / kR : n_tiles;
-    for (uint32_t tile = blockIdx.x * kGroups + g; tile < tiles; tile += gridDim.x * kGroups) {
+    // dynamic tile assignment (one atomic per tile): tiles differ widely in
+    // cost (background vs dense foreground), so a static round-robin leaves a
+    // long tail
+    uint32_t* next = A.counters + (kList ? 6 : 5);
+    for (;;) {
+        if ((threadIdx.x & uint32_t(kT - 1)) == 0) S.next_tile = atomicAdd(next, 1u);
+        tile_sync<kT>();
+        const uint32_t tile = S.next_tile;
+        if (tile >= tiles) break;
         bfs_tile<kCamera, kR, kQ, kT, kList>(T, cam, row0, rows, n, A, S, tile);
         tile_sync<kT>();
     }
