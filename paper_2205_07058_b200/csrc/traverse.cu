@@ -571,13 +571,13 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
 }
 
 // Persistent: each tile group (a block, or each warp of a block when kT ==
-// 32) processes tiles tile = group + k * groups. kList passes read their tile
-// count from the device (no host round trip).
+// 32) takes tiles from a device-side cursor until they run out. kList passes
+// read their tile count from the device (no host round trip).
 template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList>
 __global__ void __launch_bounds__(kBlock) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
                                                          uint32_t n, uint32_t n_tiles, BfsArgs A) {
     extern __shared__ __align__(16) uint8_t bfs_smem[];
-    constexpr uint32_t kGroups = kBlock / kT;
+    static_assert(kBlock % kT == 0, "tile groups per block");
     const uint32_t g = threadIdx.x / kT;
     auto& S = reinterpret_cast<BfsSmem<kR, kQ, kT>*>(bfs_smem)[g];
     const uint32_t tiles = kList ? (A.counters[1] + kR - 1) / kR : n_tiles;
