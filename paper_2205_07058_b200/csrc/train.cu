@@ -233,21 +233,58 @@ __device__ __forceinline__ void weights_from_u(const double* u, float* w) {
 // (cuBLAS SGEMM, fp32; see run_train_step); these kernels are the per-hit
 // parts around them.
 
-// f_T input column: [r6 | psi_T(x1) | psi_T(x2)] (voxel_batch.hpp:69-96)
-__global__ void __launch_bounds__(128) k_fwd_in_t(DevOctree T, DevModel M, HitArgs H, int* err) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= H.N) return;
+// f_T input column: [r6 | psi_T(x1) | psi_T(x2)] (voxel_batch.hpp:69-96).
+// Warp-cooperative: a warp owns 32 consecutive hits (geometry lane = hit); each
+// hit's 8 corner rows are read coalesced (lane = 2 features), accumulated in
+// the reference's corner order without FMA, staged transposed in shared
+// memory and written row by row (coalesced feature-major stores).
+constexpr int kInWarps = 2;
+__global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevModel M, HitArgs H, int* err) {
+    __shared__ float st[kInWarps][2 * kFt][33];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
-    float* X = H.acts + j;
+    const uint32_t j0 = (blockIdx.x * kInWarps + warp) * 32;
+    if (j0 >= N) return;
+    const uint32_t j = j0 + lane;
     HitGeom g;
-    if (!hit_geom(T, H, j, g, err)) {
-        for (int k = 0; k < kInT; ++k) X[(A_XT + k) * N] = 0.f;
-        return;
-    }
+    const bool ok = j < N && hit_geom(T, H, j, g, err);
+    float* X = H.acts + j;
+    if (j < N)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) X[(A_XT + k) * N] = g.r6[k];
-    gather_col<kFt>(M.ft, g.corners, g.w1, X + (A_XT + 6) * N, N);
-    gather_col<kFt>(M.ft, g.corners, g.w2, X + (A_XT + 6 + kFt) * N, N);
+        for (int k = 0; k < 6; ++k) X[(A_XT + k) * N] = ok ? g.r6[k] : 0.f;
+    uint32_t cs[8];
+    float w1[8], w2[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        cs[b] = ok ? g.corners[b] : 0u;
+        w1[b] = ok ? g.w1[b] : 0.f;
+        w2[b] = ok ? g.w2[b] : 0.f;
+    }
+    const unsigned live = __ballot_sync(0xffffffffu, ok);
+    const uint32_t d = 2 * lane;
+    for (int h = 0; h < 32; ++h) {
+        float2 a1 = make_float2(0.f, 0.f), a2 = a1;
+        if ((live >> h) & 1u) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
+                const float wa = __shfl_sync(0xffffffffu, w1[b], h), wb = __shfl_sync(0xffffffffu, w2[b], h);
+                const float2 v = __ldg(reinterpret_cast<const float2*>(M.ft + size_t(c) * kFt) + lane);
+                a1.x = __fadd_rn(a1.x, __fmul_rn(wa, v.x));
+                a1.y = __fadd_rn(a1.y, __fmul_rn(wa, v.y));
+                a2.x = __fadd_rn(a2.x, __fmul_rn(wb, v.x));
+                a2.y = __fadd_rn(a2.y, __fmul_rn(wb, v.y));
+            }
+        }
+        st[warp][d][h] = a1.x;
+        st[warp][d + 1][h] = a1.y;
+        st[warp][kFt + d][h] = a2.x;
+        st[warp][kFt + d + 1][h] = a2.y;
+    }
+    __syncwarp();
+    if (j < N)
+#pragma unroll 8
+        for (int r = 0; r < 2 * kFt; ++r) X[(A_XT + 6 + r) * N] = st[warp][r][lane];
 }
 
 // y = relu(y + b[row]) over a rows x N feature-major block (GEMM epilogue)
@@ -786,7 +823,8 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     SVLF_CUDA(cudaEventRecord(S.ev[1], s));
     if (N) {
         k_fill<<<std::min<unsigned>(hit_blocks, 1184), 128, 0, s>>>(ones, 1.f, N);
-        k_fwd_in_t<<<hit_blocks, 128, 0, s>>>(T, M.view, H, err_flag);
+        k_fwd_in_t<<<unsigned((size_t(N) + 32 * kInWarps - 1) / (32 * kInWarps)), 32 * kInWarps, 0, s>>>(
+            T, M.view, H, err_flag);
         layer_fwd(M.view.mt + D::T_W0, kHid, kInT, A_XT, A_HT, M.view.mt + D::T_B0);
         k_fwd_mid<<<hit_blocks, 128, 0, s>>>(T, M.view, H, err_flag);
         layer_fwd(M.view.mc + D::C_W0, kHid, kInC, A_XC, A_H1, M.view.mc + D::C_B0);
