@@ -298,41 +298,67 @@ __global__ void k_bias_relu(float* __restrict__ Y, const float* __restrict__ bia
 
 // f_T head (tau relu, eta sigmoid), x_s and the f_C input column
 // [r6 | psi_C(x_s)] for hits whose colour enters the loss (zeros otherwise).
-__global__ void __launch_bounds__(128) k_fwd_mid(DevOctree T, DevModel M, HitArgs H, int* err) {
+// The colour gather is warp-cooperative (lane = feature, one coalesced
+// 128-byte row per corner) with the result staged transposed in shared memory.
+__global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel M, HitArgs H, int* err) {
     using D = DecOffsets;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= H.N) return;
+    __shared__ float st[kInWarps][kFc][33];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
+    const uint32_t j0 = (blockIdx.x * kInWarps + warp) * 32;
+    if (j0 >= N) return;
+    const uint32_t j = j0 + lane;
+    const bool valid = j < N;
     float* X = H.acts + j;
-    const float* h = X + A_HT * N;
-    float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
+    float eta = 0.5f;
+    if (valid) {
+        const float* h = X + A_HT * N;
+        float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
 #pragma unroll 4
-    for (int k = 0; k < kHid; ++k) {
-        const float v = h[k * N];
-        y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
-        y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
+        for (int k = 0; k < kHid; ++k) {
+            const float v = h[k * N];
+            y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
+            y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
+        }
+        eta = sigmoid_ref(y1);
+        H.tau[j] = y0 > 0.f ? y0 : 0.f;
+        H.eta[j] = eta;
     }
-    const float tau = y0 > 0.f ? y0 : 0.f;
-    const float eta = sigmoid_ref(y1);
-    H.tau[j] = tau;
-    H.eta[j] = eta;
-    bool wrote = false;
+    bool ok = false;
     HitGeom g;
-    if (has_color(H, j) && hit_geom(T, H, j, g, err)) {
+    float ws[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (valid && has_color(H, j) && hit_geom(T, H, j, g, err)) {
         double xs[3], u[3];
         if (!xs_coords(T, g, eta, xs, u)) {
             raise_error(err, kErrPointNotInVoxel);
         } else {
-            float ws[8];
             weights_from_u(u, ws);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) X[(A_XC + k) * N] = g.r6[k];
-            gather_col<kFc>(M.fc, g.corners, ws, X + (A_XC + 6) * N, N);
-            wrote = true;
+            ok = true;
         }
     }
-    if (!wrote)
-        for (int k = 0; k < kInC; ++k) X[(A_XC + k) * N] = 0.f;
+    if (valid)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) X[(A_XC + k) * N] = ok ? g.r6[k] : 0.f;
+    uint32_t cs[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) cs[b] = ok ? g.corners[b] : 0u;
+    const unsigned live = __ballot_sync(0xffffffffu, ok);
+    for (int h = 0; h < 32; ++h) {
+        float acc = 0.f;
+        if ((live >> h) & 1u) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {  // corner order, no FMA: interp_into_column (voxel_batch.hpp:22-37)
+                const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
+                const float w = __shfl_sync(0xffffffffu, ws[b], h);
+                acc = __fadd_rn(acc, __fmul_rn(w, __ldg(M.fc + size_t(c) * kFc + lane)));
+            }
+        }
+        st[warp][lane][h] = acc;
+    }
+    __syncwarp();
+    if (valid)
+#pragma unroll 8
+        for (int r = 0; r < kFc; ++r) X[(A_XC + 6 + r) * N] = st[warp][r][lane];
 }
 
 // f_C head: rgb = sigmoid(W3 h3 + b3)
@@ -826,7 +852,8 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
         k_fwd_in_t<<<unsigned((size_t(N) + 32 * kInWarps - 1) / (32 * kInWarps)), 32 * kInWarps, 0, s>>>(
             T, M.view, H, err_flag);
         layer_fwd(M.view.mt + D::T_W0, kHid, kInT, A_XT, A_HT, M.view.mt + D::T_B0);
-        k_fwd_mid<<<hit_blocks, 128, 0, s>>>(T, M.view, H, err_flag);
+        k_fwd_mid<<<unsigned((size_t(N) + 32 * kInWarps - 1) / (32 * kInWarps)), 32 * kInWarps, 0, s>>>(
+            T, M.view, H, err_flag);
         layer_fwd(M.view.mc + D::C_W0, kHid, kInC, A_XC, A_H1, M.view.mc + D::C_B0);
         layer_fwd(M.view.mc + D::C_W1, kHid, kHid, A_H1, A_H2, M.view.mc + D::C_B1);
         layer_fwd(M.view.mc + D::C_W2, kHid, kHid, A_H2, A_H3, M.view.mc + D::C_B2);
