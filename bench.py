@@ -121,6 +121,33 @@ def max_over_ranks(x: float, dist, device):
     return float(t.item())
 
 
+def stage_rooflines(stage, hits, n, peaks):
+    """Every render stage against its roofline (north star: each stage as a
+    fraction of its roofline). Algorithmic bytes per stage:
+    traversal 24 B per emitted hit (leaf, t_in, t_out) + 8 B per ray (segment);
+    decode 110,848 FLOP per hit (tensor); composite 36 B per hit read (t_in,
+    t_out, tau, eta, rgb) + 20 B per ray written. The traversal passes are
+    fp64/latency-bound rather than HBM-bound, which the small fractions show."""
+    hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
+    tc = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
+    trav_ms = stage["traverse_ms"] + stage["emit_ms"]
+    out = {}
+    if trav_ms > 0:
+        gbs = (24 * hits + 8 * n) / (trav_ms * 1e-3) / 1e9
+        out["traversal"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                            "frac": round(gbs / hbm, 5), "ms": round(trav_ms, 4),
+                            "note": "fp64 / latency-bound (see profiles/r1_render.md)"}
+    if stage["decode_ms"] > 0:
+        tf = hits * FLOP_PER_HIT / (stage["decode_ms"] * 1e-3) / 1e12
+        out["decode"] = {"bound": "tensor", "achieved": round(tf, 2), "peak": tc, "unit": "TFLOP/s",
+                         "frac": round(tf / tc, 5), "ms": stage["decode_ms"]}
+    if stage["composite_ms"] > 0:
+        gbs = (36 * hits + BYTES_PER_RAY_OUT * n) / (stage["composite_ms"] * 1e-3) / 1e9
+        out["composite"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                            "frac": round(gbs / hbm, 5), "ms": stage["composite_ms"]}
+    return out
+
+
 def ncu_traffic(prefix, path=os.path.join(ROOT, "profiles", "r1_render.json")):
     """DRAM bytes (read + write) per launch of the kernels named prefix*, from the
     committed ncu summary (profiles/summarize.py); None if absent."""
@@ -487,6 +514,7 @@ def main():
                      "traffic_source": "profiles/r1_render.json (ncu --set full --clock-control none)",
                      "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)",
                      "algorithmic": f"{FLOP_PER_HIT} FLOP/hit x {int(hits)} hits per launch"},
+        "stage_rooflines": stage_rooflines(stage, hits, n, peaks),
         "e2e": {"value": round(e2e_value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": camera_bytes,
                 "d2h_bytes_per_step": n * BYTES_PER_RAY_OUT, "ms_per_step": round(e2e_step, 4),
                 "loops_ms_per_frame": [round(x, 4) for x in pipe_ms], "frames_per_loop": k_e2e,
