@@ -422,8 +422,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         }
         if (S.overflow) break;
         n_cur = n_out;
-        cur ^= 1;
-        tile_sync<kT>();
+        cur ^= 1;  // the chunk barrier above already orders this level's appends before the next level
     }
 
     if (S.overflow) {  // hand the whole tile (kept contiguous) to the next pass
