@@ -62,7 +62,10 @@ __host__ __device__ constexpr uint32_t a_off(uint32_t r, uint32_t k) {
 }
 
 // ---- kernel shared memory
-constexpr uint32_t kSlots = 4;
+#ifndef SVLF_DEC_SLOTS
+#define SVLF_DEC_SLOTS 4
+#endif
+constexpr uint32_t kSlots = SVLF_DEC_SLOTS;  // 128-row chains per CTA (one CTA per SM)
 constexpr uint32_t T_A_BYTES = (KT / 8) * kALbo;  // 37152
 constexpr uint32_t T_SM_A0 = (T_WEIGHTS + 1023) & ~1023u;
 constexpr uint32_t T_SM_BAR = T_SM_A0 + kSlots * T_A_BYTES;
@@ -338,7 +341,7 @@ __device__ __forceinline__ void load_corners(const DevOctree& T, uint32_t leaf, 
 
 // ---- f_T pass ---------------------------------------------------------------
 template <bool kBF16>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(kSlots * 128, 1)
     k_decode_t(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ ft16,
                const double* __restrict__ rays, const uint32_t* __restrict__ hit_ray,
                const uint32_t* __restrict__ hit_leaf, const double* __restrict__ hit_tin,
@@ -456,7 +459,7 @@ __global__ void __launch_bounds__(512, 1)
 
 // ---- f_C pass ---------------------------------------------------------------
 template <bool kBF16>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(kSlots * 128, 1)
     k_decode_c(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ fc16,
                const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ crec, const uint32_t* n_dev,
                uint32_t cap, HitOut out) {
@@ -602,9 +605,9 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
     }
     const H* ft = reinterpret_cast<const H*>(p + OFF_FEAT);
     const H* fc = ft + size_t(M.V) * 64;
-    k_decode_t<kBF16><<<g_num_sms, 512, T_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev,
+    k_decode_t<kBF16><<<g_num_sms, kSlots * 128, T_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev,
                                                          cap, out, crec, err);
-    k_decode_c<kBF16><<<g_num_sms, 512, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
+    k_decode_c<kBF16><<<g_num_sms, kSlots * 128, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
     note_launch(2);
 }
 
