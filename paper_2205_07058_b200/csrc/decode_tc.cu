@@ -22,7 +22,10 @@
 //
 // Biases of the input layers are folded into the MMA (A carries a constant
 // 1.0 in the first padding column, the weight tile carries the bias there);
-// hidden-layer biases are added in the epilogue. Input K is permuted so
+// hidden-layer biases are one extra K = 16 MMA of a shared constant-1 tile
+// against a (hi, lo) 16-bit split of the bias, so the epilogue reads no bias
+// from shared memory (those broadcast loads were a quarter of the f_C
+// kernel's LSU wavefronts). Input K is permuted so
 // 16-byte core-matrix chunks stay aligned (the weights use the same order):
 //   f_T input  [psi_T(x1) 0..63 | psi_T(x2) 64..127 | r6 128..133 | 1 | 0...]
 //   f_C input  [psi_C(x_s) 0..31 | r6 32..37 | 1 | 0...]
@@ -47,7 +50,10 @@ constexpr uint32_t OFF_WC0 = (T_WEIGHTS + 1023) & ~1023u;  // 128 x 48
 constexpr uint32_t OFF_WC1 = OFF_WC0 + 128 * KC * 2;       // 128 x 128
 constexpr uint32_t OFF_WC2 = OFF_WC1 + 128 * KH * 2;       // 128 x 128
 constexpr uint32_t OFF_WC3 = OFF_WC2 + 128 * KH * 2;       // 16 x 128 (rows 0..2 = rgb)
-constexpr uint32_t OFF_CVEC = OFF_WC3 + 16 * KH * 2;       // fp32: b_C1[128], b_C2[128], b_C3[4]
+constexpr uint32_t OFF_WB1 = OFF_WC3 + 16 * KH * 2;        // 128 x 16: b_C1 as (hi, lo) 16-bit pair in k = 0, 1
+constexpr uint32_t OFF_WB2 = OFF_WB1 + 128 * 16 * 2;       // 128 x 16: b_C2 likewise
+constexpr uint32_t OFF_ONES = OFF_WB2 + 128 * 16 * 2;      // 128 x 16 A tile: 1.0 in k = 0, 1
+constexpr uint32_t OFF_CVEC = OFF_ONES + 128 * 16 * 2;     // fp32: b_C1[128], b_C2[128], b_C3[4]
 constexpr uint32_t C_WEIGHTS = OFF_CVEC + (128 + 128 + 4) * 4 - OFF_WC0;  // bytes from OFF_WC0
 constexpr uint32_t OFF_FEAT = (OFF_WC0 + C_WEIGHTS + 255) & ~255u;
 
@@ -86,6 +92,7 @@ struct Fmt<false> {
     using H2 = __half2;
     static __device__ __forceinline__ H2 splat(float x) { return __float2half2_rn(x); }
     static __host__ __device__ __forceinline__ H cvt(float x) { return __float2half_rn(x); }
+    static __device__ __forceinline__ float tof(H x) { return __half2float(x); }
     static __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
         uint32_t r;
         asm("cvt.rn.satfinite.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -106,6 +113,7 @@ struct Fmt<true> {
     using H2 = __nv_bfloat162;
     static __device__ __forceinline__ H2 splat(float x) { return __float2bfloat162_rn(x); }
     static __host__ __device__ __forceinline__ H cvt(float x) { return __float2bfloat16_rn(x); }
+    static __device__ __forceinline__ float tof(H x) { return __bfloat162float(x); }
     static __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
         uint32_t r;
         asm("cvt.rn.satfinite.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -169,6 +177,13 @@ __global__ void k_pack_tc(const float* __restrict__ mt, const float* __restrict_
     if (tid < 16 * KH) {
         const uint32_t n = tid / KH, k = tid % KH;
         put(OFF_WC3, n, k, KH, n < 3 ? mc[D::C_W3 + n * kHid + k] : 0.f);
+    }
+    if (tid < 128 * 16) {  // hidden-layer biases as an extra K = 16 MMA against a constant-1 tile
+        const uint32_t n = tid / 16, k = tid % 16;
+        auto hilo = [&](float b) { return k == 0 ? b : (k == 1 ? b - F::tof(F::cvt(b)) : 0.f); };
+        put(OFF_WB1, n, k, 16, hilo(mc[D::C_B1 + n]));
+        put(OFF_WB2, n, k, 16, hilo(mc[D::C_B2 + n]));
+        put(OFF_ONES, n, k, 16, k < 2 ? 1.f : 0.f);
     }
     float* cvec = reinterpret_cast<float*>(pack + OFF_CVEC);
     if (tid < 128) {
@@ -474,6 +489,8 @@ __global__ void __launch_bounds__(kSlots * 128, 1)
     const uint32_t acc = tmem + slot * 128;
     const uint32_t sbase = smem_u32(sm);
     constexpr uint32_t W0 = 0, W1 = OFF_WC1 - OFF_WC0, W2 = OFF_WC2 - OFF_WC0, W3 = OFF_WC3 - OFF_WC0;
+    constexpr uint32_t WB1 = OFF_WB1 - OFF_WC0, WB2 = OFF_WB2 - OFF_WC0;
+    const uint64_t ones = make_desc(sbase + (OFF_ONES - OFF_WC0), 128, 256);
     const float* cvec = reinterpret_cast<const float*>(sm + (OFF_CVEC - OFF_WC0));
     const uint32_t a_base = sbase + C_SM_A0 + slot * C_A_BYTES;
     Slot S{reinterpret_cast<uint64_t*>(sm + C_SM_BAR) + slot, 0u, 1u + slot, r};
@@ -543,10 +560,16 @@ __global__ void __launch_bounds__(kSlots * 128, 1)
         fetch_rest(tile + tstride);
         S.mma([&] { issue_layer(acc, a_base, sbase + W0, KC, kIdesc); });
         hidden_epilogue<kBF16, false>(acc + lane_off, a_base, r, KH, nullptr);
-        S.mma([&] { issue_layer(acc, a_base, sbase + W1, KH, kIdesc); });
-        hidden_epilogue<kBF16, true>(acc + lane_off, a_base, r, KH, cvec);
-        S.mma([&] { issue_layer(acc, a_base, sbase + W2, KH, kIdesc); });
-        hidden_epilogue<kBF16, true>(acc + lane_off, a_base, r, KH, cvec + 128);
+        S.mma([&] {
+            issue_layer(acc, a_base, sbase + W1, KH, kIdesc);
+            mma_f16(acc, ones, make_desc(sbase + WB1, 128, 256), kIdesc, true);
+        });
+        hidden_epilogue<kBF16, false>(acc + lane_off, a_base, r, KH, nullptr);
+        S.mma([&] {
+            issue_layer(acc, a_base, sbase + W2, KH, kIdesc);
+            mma_f16(acc, ones, make_desc(sbase + WB2, 128, 256), kIdesc, true);
+        });
+        hidden_epilogue<kBF16, false>(acc + lane_off, a_base, r, KH, nullptr);
         S.mma([&] { issue_layer(acc, a_base, sbase + W3, KH, kIdescHead); });
         float hv[16];
         tmem_ld16(acc + lane_off, hv);

@@ -233,8 +233,11 @@ struct BfsSmem {
     uint32_t rcount[kR], roff[kR];
     uint32_t gray[kR];
     uint32_t n_q, base, overflow, next_tile;
+    uint32_t wtot[2];             // per-warp totals of the two-warp (kT == 64) scan
     unsigned long long unsorted;  // rays whose segment needs the insertion sort
-    typename cub::BlockScan<uint32_t, kT>::TempStorage scan;
+    struct NoScan {};
+    // cub's block scan only for whole-block tiles; 32/64-thread tiles scan with shuffles
+    typename std::conditional<(kT > 64), typename cub::BlockScan<uint32_t, kT>::TempStorage, NoScan>::type scan;
 };
 
 struct BfsArgs {
@@ -260,13 +263,21 @@ struct BfsArgs {
 // scans: the warps of a block then run independent tiles).
 template <int kT>
 __device__ __forceinline__ void tile_sync() {
-    if constexpr (kT == 32) __syncwarp();
-    else __syncthreads();
+    if constexpr (kT == 32) {
+        __syncwarp();
+    } else if constexpr (kT == 64) {  // two-warp group: its own named barrier (id 1 + group)
+        asm volatile("bar.sync %0, 64;" ::"r"(1u + threadIdx.x / 64u) : "memory");
+    } else {
+        __syncthreads();
+    }
 }
 
-template <int kT, typename Temp>
-__device__ __forceinline__ void tile_excl_sum(Temp& temp, uint32_t v, uint32_t& off, uint32_t& tot) {
-    if constexpr (kT == 32) {
+// Exclusive sum over the tile. Every call site is followed by a tile_sync()
+// before the next scan, so the kT == 64 variant's single barrier is enough to
+// protect its two-word exchange.
+template <int kT, typename Smem>
+__device__ __forceinline__ void tile_excl_sum(Smem& S, uint32_t v, uint32_t& off, uint32_t& tot) {
+    if constexpr (kT == 32 || kT == 64) {
         const uint32_t lane = threadIdx.x & 31u;
         uint32_t x = v;
 #pragma unroll
@@ -274,10 +285,20 @@ __device__ __forceinline__ void tile_excl_sum(Temp& temp, uint32_t v, uint32_t& 
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
             if (lane >= uint32_t(d)) x += y;
         }
-        tot = __shfl_sync(0xffffffffu, x, 31);
-        off = x - v;
+        const uint32_t wt = __shfl_sync(0xffffffffu, x, 31);
+        if constexpr (kT == 32) {
+            tot = wt;
+            off = x - v;
+        } else {
+            const uint32_t w = (threadIdx.x >> 5) & 1u;
+            if (lane == 31) S.wtot[w] = wt;
+            tile_sync<kT>();
+            const uint32_t w0 = S.wtot[0];
+            tot = w0 + S.wtot[1];
+            off = x - v + (w ? w0 : 0u);
+        }
     } else {
-        cub::BlockScan<uint32_t, kT>(temp).ExclusiveSum(v, off, tot);
+        cub::BlockScan<uint32_t, kT>(S.scan).ExclusiveSum(v, off, tot);
     }
 }
 
@@ -355,7 +376,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             hit = slab_test(p, lo, hi, t0, t1) ? 1u : 0u;
         }
         uint32_t off, tot;
-        tile_excl_sum<kT>(S.scan, hit, off, tot);
+        tile_excl_sum<kT>(S, hit, off, tot);
         if (hit) {
             S.qnode[0][off] = 0;
             S.qxyz[0][off] = 0;
@@ -401,7 +422,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 cnt = __popc(hitmask);
             }
             uint32_t off, tot;
-            tile_excl_sum<kT>(S.scan, cnt, off, tot);
+            tile_excl_sum<kT>(S, cnt, off, tot);
             if (n_out + tot > kQ) {
                 if (tid == 0) S.overflow = 1;
                 tile_sync<kT>();
@@ -465,7 +486,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 if (cnt) atomicAdd(&S.rcount[ri], cnt);
             }
             uint32_t off, tot;
-            tile_excl_sum<kT>(S.scan, cnt, off, tot);
+            tile_excl_sum<kT>(S, cnt, off, tot);
             if (e < n_cur) S.pos[e] = total + off;
             total += tot;
             tile_sync<kT>();
@@ -474,7 +495,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     {
         const uint32_t c = tid < kR ? S.rcount[tid] : 0u;
         uint32_t off, tot;
-        tile_excl_sum<kT>(S.scan, c, off, tot);
+        tile_excl_sum<kT>(S, c, off, tot);
         if (tid < kR) S.roff[tid] = off;
         if (tid == 0) {
             const uint32_t b = tot ? atomicAdd(&A.counters[0], tot) : 0u;
