@@ -68,6 +68,9 @@ __host__ __device__ constexpr uint32_t a_off(uint32_t r, uint32_t k) {
 }
 
 // ---- kernel shared memory
+#ifndef SVLF_DEC_C_TMEM
+#define SVLF_DEC_C_TMEM 1
+#endif
 #ifndef SVLF_DEC_SLOTS
 #define SVLF_DEC_SLOTS 4
 #endif
@@ -81,6 +84,17 @@ constexpr uint32_t C_SM_A0 = (C_WEIGHTS + 1023) & ~1023u;
 constexpr uint32_t C_SM_BAR = C_SM_A0 + kSlots * C_A_BYTES;
 constexpr uint32_t C_SM_TOTAL = C_SM_BAR + 64;
 static_assert(T_SM_TOTAL <= 232448 && C_SM_TOTAL <= 232448, "shared memory budget");
+// f_C with the hidden activations in TMEM (k_decode_c_tm), warp-specialised:
+// kProducers warps gather input tiles (K = 48) into a kRing-entry shared
+// ring; two 4-warp consumer chains run the MMAs, each with a 128-column
+// accumulator and a 64-column 16-bit A operand in TMEM.
+constexpr uint32_t kProducers = 8;
+constexpr uint32_t kRing = 10;
+constexpr uint32_t kCtThreads = (kProducers + 8) * 32;
+constexpr uint32_t CT_A_BYTES = (KC / 8) * kALbo;  // 12384
+constexpr uint32_t CT_SM_BAR = C_SM_A0 + kRing * CT_A_BYTES;
+constexpr uint32_t CT_SM_TOTAL = CT_SM_BAR + (2 + 2 * kRing) * 8 + 16;
+static_assert(CT_SM_TOTAL <= 232448, "shared memory budget");
 
 // Operand format traits: fp16 (11-bit mantissa) or bf16 (north-star format);
 // both run at the same tensor-core rate.
@@ -584,6 +598,213 @@ __global__ void __launch_bounds__(kSlots * 128, 1)
     kernel_teardown(tmem);
 }
 
+// ---- f_C pass, hidden activations in TMEM -----------------------------------
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B^T: A is 128 lanes x K/2 columns (16-bit K pairs per
+// 32-bit column, 8 columns per K = 16 step), B in the dense smem layout.
+__device__ __forceinline__ void issue_layer_ta(uint32_t tmem_d, uint32_t a_tmem, uint32_t b_base, uint32_t K,
+                                               uint32_t idesc) {
+    const uint32_t b_sbo = (K / 8) * 128;
+#pragma unroll 1
+    for (uint32_t k = 0; k < K / 16; ++k)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "r"(a_tmem + 8 * k), "l"(make_desc(b_base + 256 * k, 128, b_sbo)), "r"(idesc), "r"(k > 0 ? 1u : 0u));
+}
+
+template <bool kBF16>
+__global__ void __launch_bounds__(kCtThreads, 1)
+    k_decode_c_tm(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ fc16,
+                  const uint32_t* __restrict__ hit_leaf, const uint4* __restrict__ crec, const uint32_t* n_dev,
+                  uint32_t cap, HitOut out) {
+    using F = Fmt<kBF16>;
+    using H2 = typename F::H2;
+    constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
+    constexpr uint32_t kIdescHead = make_idesc(128, 16, kBF16);
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + CT_SM_BAR);  // [0,1] chains, [2..] full[R], empty[R]
+    uint64_t* full = bars + 2;
+    uint64_t* empty = full + kRing;
+    uint32_t* holder = reinterpret_cast<uint32_t*>(empty + kRing);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(pack + OFF_WC0);
+        uint4* dst = reinterpret_cast<uint4*>(sm);
+        for (uint32_t i = tid; i < C_WEIGHTS / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        for (uint32_t i = 0; i < kRing; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(holder, 512);
+    fence_async_smem();
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *holder;
+    const uint32_t sbase = smem_u32(sm);
+    const uint32_t ring0 = sbase + C_SM_A0;
+    const uint32_t n = min(*n_dev, cap);
+    const uint32_t ntiles = (n + 127) / 128;
+    auto tile_of = [&](uint32_t k) { return blockIdx.x + k * gridDim.x; };
+
+    if (warp < kProducers) {
+        // ---- producer warp: whole input tiles, k = warp, warp + kProducers, ...
+        // Per 32-row group, lane l holds row 32g + l (corners, f_C record);
+        // pass p, lanes 4q..4q+3 gather row 8p+q of the group, 8 features each.
+        const uint32_t q = lane >> 2, ch = lane & 3;
+        uint32_t c[8];
+        uint4 g0, g1;
+        auto fetch = [&](uint32_t t, uint32_t g) {
+            const uint32_t j = t * 128 + 32 * g + lane;
+            if (j < n) {
+                const uint32_t leaf = hit_leaf[j];
+                const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
+                const uint4 a = __ldg(cp), b = __ldg(cp + 1);
+                c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+                c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+                g0 = crec[2 * size_t(j)];
+                g1 = crec[2 * size_t(j) + 1];
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) c[i] = 0;
+                g0 = g1 = make_uint4(0, 0, 0, 0);
+            }
+        };
+        for (uint32_t k = warp; tile_of(k) < ntiles; k += kProducers) {
+            const uint32_t slot = k % kRing, use = k / kRing;
+            if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
+            const uint32_t a_base = ring0 + slot * CT_A_BYTES;
+            const uint32_t t = tile_of(k);
+#pragma unroll 1
+            for (uint32_t g = 0; g < 4; ++g) {
+                fetch(t, g);
+                const uint32_t wsp[4] = {g1.x, g1.y, g1.z, g1.w};
+#pragma unroll 2
+                for (uint32_t p = 0; p < 4; ++p) {
+                    const uint32_t src = 8 * p + q;
+                    uint32_t cb[8], wt[4];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) cb[b] = __shfl_sync(0xffffffffu, c[b], src);
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) wt[b] = __shfl_sync(0xffffffffu, wsp[b], src);
+                    uint4 fq[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        fq[b] = __ldg(reinterpret_cast<const uint4*>(fc16 + size_t(cb[b]) * 32) + ch);
+                    H2 a1[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) a1[i] = F::splat(0.f);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const H2 pw = u2h<H2>(wt[b / 2]);
+                        const H2 hw = (b & 1) ? F::hi2(pw) : F::lo2(pw);
+                        const H2* f = reinterpret_cast<const H2*>(&fq[b]);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) a1[i] = __hfma2(hw, f[i], a1[i]);
+                    }
+                    st_shared_v4(a_base + a_off(32 * g + src, 8 * ch), h2u(a1[0]), h2u(a1[1]), h2u(a1[2]),
+                                 h2u(a1[3]));
+                }
+                st_shared_v4(a_base + a_off(32 * g + lane, 32), g0.x, g0.y, g0.z, F::kOne);
+                st_shared_v4(a_base + a_off(32 * g + lane, 40), 0u, 0u, 0u, 0u);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
+        }
+    } else {
+        // ---- consumer chain: 4 warps, thread r owns row (TMEM lane) r; k = chain, chain + 2, ...
+        const uint32_t chain = (warp - kProducers) >> 2, r = tid & 127;
+        const uint32_t lane_off = (32u * (warp & 3u)) << 16;
+        const uint32_t acc = tmem + chain * 256, a_t = acc + 128;  // [acc 128 | A 64] columns
+        constexpr uint32_t W0 = 0, W1 = OFF_WC1 - OFF_WC0, W2 = OFF_WC2 - OFF_WC0, W3 = OFF_WC3 - OFF_WC0;
+        constexpr uint32_t WB1 = OFF_WB1 - OFF_WC0, WB2 = OFF_WB2 - OFF_WC0;
+        const uint64_t ones = make_desc(sbase + (OFF_ONES - OFF_WC0), 128, 256);
+        const float* cvec = reinterpret_cast<const float*>(sm + (OFF_CVEC - OFF_WC0));
+        uint64_t* cbar = &bars[chain];
+        uint32_t phase = 0;
+        const uint32_t bar_id = 1 + chain;
+        auto sync_issue = [&](auto&& f) {
+            fence_before_sync();
+            named_sync(bar_id, 128);
+            if (r == 0) {
+                fence_after_sync();
+                f();
+                mma_commit(cbar);
+            }
+        };
+        auto wait = [&]() {
+            mbar_wait(cbar, phase);
+            phase ^= 1;
+            fence_after_sync();
+        };
+        auto epilogue = [&]() {  // acc -> relu -> 16-bit pairs -> A (TMEM)
+#pragma unroll
+            for (uint32_t hh = 0; hh < 2; ++hh) {
+                float v[64];
+                tmem_ld32(acc + lane_off + 64 * hh, v);
+                tmem_ld32(acc + lane_off + 64 * hh + 32, v + 32);
+                tmem_wait_ld();
+                uint32_t pk[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) pk[i] = F::relu_pack(v[2 * i], v[2 * i + 1]);
+                tmem_st16(a_t + lane_off + 32 * hh, pk);
+                tmem_st16(a_t + lane_off + 32 * hh + 16, pk + 16);
+            }
+            tmem_wait_st();
+        };
+        for (uint32_t k = chain; tile_of(k) < ntiles; k += 2) {
+            const uint32_t slot = k % kRing, use = k / kRing;
+            mbar_wait(&full[slot], use & 1);
+            sync_issue([&] {
+                issue_layer(acc, ring0 + slot * CT_A_BYTES, sbase + W0, KC, kIdesc);
+                mma_commit(&empty[slot]);  // the input tile is free once layer 0 completed
+            });
+            wait();
+            epilogue();
+            sync_issue([&] {
+                issue_layer_ta(acc, a_t, sbase + W1, KH, kIdesc);
+                mma_f16(acc, ones, make_desc(sbase + WB1, 128, 256), kIdesc, true);
+            });
+            wait();
+            epilogue();
+            sync_issue([&] {
+                issue_layer_ta(acc, a_t, sbase + W2, KH, kIdesc);
+                mma_f16(acc, ones, make_desc(sbase + WB2, 128, 256), kIdesc, true);
+            });
+            wait();
+            epilogue();
+            sync_issue([&] { issue_layer_ta(acc, a_t, sbase + W3, KH, kIdescHead); });
+            wait();
+            float hv[16];
+            tmem_ld16(acc + lane_off, hv);
+            tmem_wait_ld();
+            const uint32_t j = tile_of(k) * 128 + r;
+            if (j < n) {
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc)
+                    out.rgb[3 * size_t(j) + cc] = __fdividef(1.0f, 1.0f + __expf(-(hv[cc] + cvec[256 + cc])));
+            }
+        }
+    }
+    kernel_teardown(tmem);
+}
+
 int g_num_sms = 0;
 
 }  // namespace
@@ -624,13 +845,19 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
     if (!attr) {
         SVLF_CUDA(cudaFuncSetAttribute(k_decode_t<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(T_SM_TOTAL)));
         SVLF_CUDA(cudaFuncSetAttribute(k_decode_c<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SM_TOTAL)));
+        SVLF_CUDA(cudaFuncSetAttribute(k_decode_c_tm<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(CT_SM_TOTAL)));
         attr = true;
     }
     const H* ft = reinterpret_cast<const H*>(p + OFF_FEAT);
     const H* fc = ft + size_t(M.V) * 64;
     k_decode_t<kBF16><<<g_num_sms, kSlots * 128, T_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev,
                                                          cap, out, crec, err);
+#if SVLF_DEC_C_TMEM
+    k_decode_c_tm<kBF16><<<g_num_sms, kCtThreads, CT_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
+#else
     k_decode_c<kBF16><<<g_num_sms, kSlots * 128, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
+#endif
     note_launch(2);
 }
 
