@@ -68,8 +68,14 @@ __host__ __device__ constexpr uint32_t a_off(uint32_t r, uint32_t k) {
 }
 
 // ---- kernel shared memory
+#ifndef SVLF_DEC_EXP
+#define SVLF_DEC_EXP 0  // timing experiments only: 1 = producers skip the gather, 2 = consumers skip the MMAs
+#endif
 #ifndef SVLF_DEC_C_TMEM
 #define SVLF_DEC_C_TMEM 1
+#endif
+#ifndef SVLF_DEC_EPI64
+#define SVLF_DEC_EPI64 0
 #endif
 #ifndef SVLF_DEC_SLOTS
 #define SVLF_DEC_SLOTS 4
@@ -89,11 +95,19 @@ static_assert(T_SM_TOTAL <= 232448 && C_SM_TOTAL <= 232448, "shared memory budge
 // ring; two 4-warp consumer chains run the MMAs, each with a 128-column
 // accumulator and a 64-column 16-bit A operand in TMEM.
 constexpr uint32_t kProducers = 8;
-constexpr uint32_t kRing = 10;
-constexpr uint32_t kCtThreads = (kProducers + 8) * 32;
+#ifndef SVLF_DEC_C_SMCHAINS
+#define SVLF_DEC_C_SMCHAINS 1
+#endif
+constexpr uint32_t kChainsTm = 2;                      // chains with A in TMEM (192 columns each)
+constexpr uint32_t kChainsSm = SVLF_DEC_C_SMCHAINS;    // chains with A in shared memory (128 columns)
+constexpr uint32_t kChains = kChainsTm + kChainsSm;
+constexpr uint32_t kRing = kChainsSm ? 7 : 10;
+constexpr uint32_t kCtThreads = (kProducers + 4 * kChains) * 32;
 constexpr uint32_t CT_A_BYTES = (KC / 8) * kALbo;  // 12384
-constexpr uint32_t CT_SM_BAR = C_SM_A0 + kRing * CT_A_BYTES;
-constexpr uint32_t CT_SM_TOTAL = CT_SM_BAR + (2 + 2 * kRing) * 8 + 16;
+constexpr uint32_t CT_SMA0 = C_SM_A0 + kRing * CT_A_BYTES;
+constexpr uint32_t CT_SM_BAR = CT_SMA0 + kChainsSm * C_A_BYTES;
+constexpr uint32_t CT_SM_TOTAL = CT_SM_BAR + 4 * 8 + (2 * kRing + 1) * 4;
+static_assert(kChainsTm * 192 + kChainsSm * 128 <= 512, "TMEM columns");
 static_assert(CT_SM_TOTAL <= 232448, "shared memory budget");
 
 // Operand format traits: fp16 (11-bit mantissa) or bf16 (north-star format);
@@ -608,6 +622,15 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
         : "memory");
 }
 
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
 // D[tmem] (+)= A[tmem] . B^T: A is 128 lanes x K/2 columns (16-bit K pairs per
 // 32-bit column, 8 columns per K = 16 step), B in the dense smem layout.
 __device__ __forceinline__ void issue_layer_ta(uint32_t tmem_d, uint32_t a_tmem, uint32_t b_base, uint32_t K,
@@ -631,10 +654,14 @@ __global__ void __launch_bounds__(kCtThreads, 1)
     constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
     constexpr uint32_t kIdescHead = make_idesc(128, 16, kBF16);
     extern __shared__ __align__(1024) uint8_t sm[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + CT_SM_BAR);  // [0,1] chains, [2..] full[R], empty[R]
-    uint64_t* full = bars + 2;
-    uint64_t* empty = full + kRing;
-    uint32_t* holder = reinterpret_cast<uint32_t*>(empty + kRing);
+    // Ring hand-off by tile-number flags (not mbarrier parity: several
+    // producers and chains share each ring entry, so a waiter can be more than
+    // one phase behind): full[s] = k + 1 once tile k is in entry s, empty[s] =
+    // k + 1 once the layer-0 MMA that read it completed.
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + CT_SM_BAR);  // [0..3] chain MMA barriers
+    uint32_t* full = reinterpret_cast<uint32_t*>(bars + 4);
+    uint32_t* empty = full + kRing;
+    uint32_t* holder = empty + kRing;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     {
         const uint4* src = reinterpret_cast<const uint4*>(pack + OFF_WC0);
@@ -642,11 +669,10 @@ __global__ void __launch_bounds__(kCtThreads, 1)
         for (uint32_t i = tid; i < C_WEIGHTS / 16; i += blockDim.x) dst[i] = src[i];
     }
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (uint32_t i = 0; i < kChains; ++i) mbar_init(&bars[i], 1);
         for (uint32_t i = 0; i < kRing; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            full[i] = 0;
+            empty[i] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -667,32 +693,52 @@ __global__ void __launch_bounds__(kCtThreads, 1)
         // Per 32-row group, lane l holds row 32g + l (corners, f_C record);
         // pass p, lanes 4q..4q+3 gather row 8p+q of the group, 8 features each.
         const uint32_t q = lane >> 2, ch = lane & 3;
-        uint32_t c[8];
-        uint4 g0, g1;
-        auto fetch = [&](uint32_t t, uint32_t g) {
-            const uint32_t j = t * 128 + 32 * g + lane;
-            if (j < n) {
-                const uint32_t leaf = hit_leaf[j];
-                const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
-                const uint4 a = __ldg(cp), b = __ldg(cp + 1);
-                c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
-                c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
-                g0 = crec[2 * size_t(j)];
-                g1 = crec[2 * size_t(j) + 1];
-            } else {
+        // Software pipeline: the leaf indices of a tile are loaded a tile
+        // ahead, each 32-row group's corners and f_C records a group ahead.
+        uint32_t leaves[4], c[8], nc[8];
+        uint4 g0, g1, ng0, ng1;
+        auto fetch_leaves = [&](uint32_t t) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) c[i] = 0;
-                g0 = g1 = make_uint4(0, 0, 0, 0);
+            for (uint32_t g = 0; g < 4; ++g) {
+                const uint32_t j = t * 128 + 32 * g + lane;
+                leaves[g] = (t < ntiles && j < n) ? hit_leaf[j] : 0xffffffffu;
             }
         };
+        auto fetch = [&](uint32_t t, uint32_t leaf, uint32_t g) {
+            const uint32_t j = t * 128 + 32 * g + lane;
+            if (leaf != 0xffffffffu) {
+                const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
+                const uint4 a = __ldg(cp), b = __ldg(cp + 1);
+                nc[0] = a.x; nc[1] = a.y; nc[2] = a.z; nc[3] = a.w;
+                nc[4] = b.x; nc[5] = b.y; nc[6] = b.z; nc[7] = b.w;
+                ng0 = crec[2 * size_t(j)];
+                ng1 = crec[2 * size_t(j) + 1];
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) nc[i] = 0;
+                ng0 = ng1 = make_uint4(0, 0, 0, 0);
+            }
+        };
+        fetch_leaves(tile_of(warp));
         for (uint32_t k = warp; tile_of(k) < ntiles; k += kProducers) {
             const uint32_t slot = k % kRing, use = k / kRing;
-            if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
-            const uint32_t a_base = ring0 + slot * CT_A_BYTES;
             const uint32_t t = tile_of(k);
+            fetch(t, leaves[0], 0);
+            if (use > 0)
+                while (ld_acquire(&empty[slot]) != k - kRing + 1) __nanosleep(32);
+            const uint32_t a_base = ring0 + slot * CT_A_BYTES;
 #pragma unroll 1
-            for (uint32_t g = 0; g < 4; ++g) {
-                fetch(t, g);
+            for (uint32_t g = 0; g < (SVLF_DEC_EXP == 1 ? 0 : 4); ++g) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) c[i] = nc[i];
+                g0 = ng0;
+                g1 = ng1;
+                if (g < 3) {
+                    const uint32_t lf = g == 0 ? leaves[1] : (g == 1 ? leaves[2] : leaves[3]);
+                    fetch(t, lf, g + 1);
+                } else {
+                    fetch_leaves(tile_of(k + kProducers));
+                }
                 const uint32_t wsp[4] = {g1.x, g1.y, g1.z, g1.w};
 #pragma unroll 2
                 for (uint32_t p = 0; p < 4; ++p) {
@@ -725,13 +771,18 @@ __global__ void __launch_bounds__(kCtThreads, 1)
             }
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
+            if (lane == 0) st_release(&full[slot], k + 1);
         }
     } else {
-        // ---- consumer chain: 4 warps, thread r owns row (TMEM lane) r; k = chain, chain + 2, ...
+        // ---- consumer chain: 4 warps, thread r owns row (TMEM lane) r; k = chain, chain + kChains, ...
+        // TMEM: accumulators of chains 0, 1, 2 at columns 0, 128, 256; the
+        // 16-bit A operands of chains 0, 1 at 384, 448. Chain 2 (if present)
+        // keeps its A operand in shared memory.
         const uint32_t chain = (warp - kProducers) >> 2, r = tid & 127;
+        const bool tm = chain < kChainsTm;
         const uint32_t lane_off = (32u * (warp & 3u)) << 16;
-        const uint32_t acc = tmem + chain * 256, a_t = acc + 128;  // [acc 128 | A 64] columns
+        const uint32_t acc = tmem + chain * 128, a_t = tmem + 384 + 64 * chain;
+        const uint32_t a_sm = sbase + CT_SMA0 + (chain - kChainsTm) * C_A_BYTES;
         constexpr uint32_t W0 = 0, W1 = OFF_WC1 - OFF_WC0, W2 = OFF_WC2 - OFF_WC0, W3 = OFF_WC3 - OFF_WC0;
         constexpr uint32_t WB1 = OFF_WB1 - OFF_WC0, WB2 = OFF_WB2 - OFF_WC0;
         const uint64_t ones = make_desc(sbase + (OFF_ONES - OFF_WC0), 128, 256);
@@ -740,6 +791,7 @@ __global__ void __launch_bounds__(kCtThreads, 1)
         uint32_t phase = 0;
         const uint32_t bar_id = 1 + chain;
         auto sync_issue = [&](auto&& f) {
+            fence_async_smem();
             fence_before_sync();
             named_sync(bar_id, 128);
             if (r == 0) {
@@ -753,8 +805,13 @@ __global__ void __launch_bounds__(kCtThreads, 1)
             phase ^= 1;
             fence_after_sync();
         };
-        auto epilogue = [&]() {  // acc -> relu -> 16-bit pairs -> A (TMEM)
-#pragma unroll
+        auto epilogue = [&]() {  // acc -> relu -> 16-bit pairs -> A (TMEM or shared memory)
+            if (!tm) {
+                hidden_epilogue<kBF16, false>(acc + lane_off, a_sm, r, KH, nullptr);
+                return;
+            }
+#if SVLF_DEC_EPI64
+#pragma unroll 1
             for (uint32_t hh = 0; hh < 2; ++hh) {
                 float v[64];
                 tmem_ld32(acc + lane_off + 64 * hh, v);
@@ -766,30 +823,55 @@ __global__ void __launch_bounds__(kCtThreads, 1)
                 tmem_st16(a_t + lane_off + 32 * hh, pk);
                 tmem_st16(a_t + lane_off + 32 * hh + 16, pk + 16);
             }
+#else
+#pragma unroll 1
+            for (uint32_t hh = 0; hh < 4; ++hh) {
+                float v[32];
+                tmem_ld32(acc + lane_off + 32 * hh, v);
+                tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = F::relu_pack(v[2 * i], v[2 * i + 1]);
+                tmem_st16(a_t + lane_off + 16 * hh, pk);
+            }
+#endif
             tmem_wait_st();
         };
-        for (uint32_t k = chain; tile_of(k) < ntiles; k += 2) {
+        auto hidden = [&](uint32_t w, uint32_t K, uint32_t idesc) {
+            if (tm)
+                issue_layer_ta(acc, a_t, sbase + w, K, idesc);
+            else
+                issue_layer(acc, a_sm, sbase + w, K, idesc);
+        };
+        for (uint32_t k = chain; tile_of(k) < ntiles; k += kChains) {
             const uint32_t slot = k % kRing, use = k / kRing;
-            mbar_wait(&full[slot], use & 1);
+            if (r == 0)
+                while (ld_acquire(&full[slot]) != k + 1) {
+                }
+            if (SVLF_DEC_EXP == 2) {
+                named_sync(bar_id, 128);
+                if (r == 0) st_release(&empty[slot], k + 1);
+                continue;
+            }
             sync_issue([&] {
                 issue_layer(acc, ring0 + slot * CT_A_BYTES, sbase + W0, KC, kIdesc);
-                mma_commit(&empty[slot]);  // the input tile is free once layer 0 completed
             });
             wait();
+            if (r == 0) st_release(&empty[slot], k + 1);  // the input tile is free once layer 0 completed
             epilogue();
             sync_issue([&] {
-                issue_layer_ta(acc, a_t, sbase + W1, KH, kIdesc);
+                hidden(W1, KH, kIdesc);
                 mma_f16(acc, ones, make_desc(sbase + WB1, 128, 256), kIdesc, true);
             });
             wait();
             epilogue();
             sync_issue([&] {
-                issue_layer_ta(acc, a_t, sbase + W2, KH, kIdesc);
+                hidden(W2, KH, kIdesc);
                 mma_f16(acc, ones, make_desc(sbase + WB2, 128, 256), kIdesc, true);
             });
             wait();
             epilogue();
-            sync_issue([&] { issue_layer_ta(acc, a_t, sbase + W3, KH, kIdescHead); });
+            sync_issue([&] { hidden(W3, KH, kIdescHead); });
             wait();
             float hv[16];
             tmem_ld16(acc + lane_off, hv);
