@@ -74,6 +74,9 @@ __host__ __device__ constexpr uint32_t a_off(uint32_t r, uint32_t k) {
 #ifndef SVLF_DEC_C_TMEM
 #define SVLF_DEC_C_TMEM 1
 #endif
+#ifndef SVLF_DEC_T_WS
+#define SVLF_DEC_T_WS 1
+#endif
 #ifndef SVLF_DEC_EPI64
 #define SVLF_DEC_EPI64 0
 #endif
@@ -108,6 +111,28 @@ constexpr uint32_t CT_SMA0 = C_SM_A0 + kRing * CT_A_BYTES;
 constexpr uint32_t CT_SM_BAR = CT_SMA0 + kChainsSm * C_A_BYTES;
 constexpr uint32_t CT_SM_TOTAL = CT_SM_BAR + 4 * 8 + (2 * kRing + 1) * 4;
 static_assert(kChainsTm * 192 + kChainsSm * 128 <= 512, "TMEM columns");
+// f_T warp-specialised (k_decode_t_ws): 4-warp producer groups (geometry +
+// gather) feed 4-warp MMA chains through a 4-entry ring (input tile + per-row
+// side data: u1, u2, r6 pairs); entry e is filled by group e % TW_GROUPS and
+// consumed by chain e % TW_CHAINS.
+constexpr uint32_t TW_RING0 = (T_WEIGHTS + 1023) & ~1023u;
+constexpr uint32_t TW_SIDE = 9 * 128 * 4;                 // u[6] fp32, r6 pairs[3], SoA
+constexpr uint32_t TW_ENTRY = T_A_BYTES + TW_SIDE;        // 41760
+constexpr uint32_t TW_ENTRIES = 4;
+#ifndef SVLF_DEC_T_GROUPS
+#define SVLF_DEC_T_GROUPS 4
+#endif
+#ifndef SVLF_DEC_T_CHAINS
+#define SVLF_DEC_T_CHAINS 1
+#endif
+constexpr uint32_t TW_GROUPS = SVLF_DEC_T_GROUPS;  // 4-warp producer groups
+constexpr uint32_t TW_CHAINS = SVLF_DEC_T_CHAINS;  // 4-warp MMA chains
+constexpr uint32_t TW_THREADS = 128 * (TW_GROUPS + TW_CHAINS);
+static_assert(TW_ENTRIES % TW_GROUPS == 0 && TW_ENTRIES % TW_CHAINS == 0 && TW_CHAINS <= 2,
+              "each ring entry has one producer group and one chain (mbarrier parity)");
+constexpr uint32_t TW_SM_BAR = TW_RING0 + TW_ENTRIES * TW_ENTRY;
+constexpr uint32_t TW_SM_TOTAL = TW_SM_BAR + (2 + 2 * TW_ENTRIES) * 8 + 16;
+static_assert(TW_SM_TOTAL <= 232448, "shared memory budget");
 static_assert(CT_SM_TOTAL <= 232448, "shared memory budget");
 
 // Operand format traits: fp16 (11-bit mantissa) or bf16 (north-star format);
@@ -887,6 +912,191 @@ __global__ void __launch_bounds__(kCtThreads, 1)
     kernel_teardown(tmem);
 }
 
+// ---- f_T pass, warp-specialised ----------------------------------------------
+template <bool kBF16>
+__global__ void __launch_bounds__(TW_THREADS, 1)
+    k_decode_t_ws(DevOctree T, const uint8_t* __restrict__ pack, const typename Fmt<kBF16>::H* __restrict__ ft16,
+                  const double* __restrict__ rays, const uint32_t* __restrict__ hit_ray,
+                  const uint32_t* __restrict__ hit_leaf, const double* __restrict__ hit_tin,
+                  const double* __restrict__ hit_tout, const uint32_t* n_dev, uint32_t cap, HitOut out,
+                  uint4* __restrict__ crec, int* err) {
+    using F = Fmt<kBF16>;
+    using H2 = typename F::H2;
+    constexpr uint32_t kIdesc = make_idesc(128, 128, kBF16);
+    constexpr uint32_t kIdescHead = make_idesc(128, 16, kBF16);
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TW_SM_BAR);  // [0,1] chains, full[4], empty[4]
+    uint64_t* full = bars + 2;
+    uint64_t* empty = full + TW_ENTRIES;
+    uint32_t* holder = reinterpret_cast<uint32_t*>(empty + TW_ENTRIES);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(pack + OFF_WT0);
+        uint4* dst = reinterpret_cast<uint4*>(sm);
+        for (uint32_t i = tid; i < T_WEIGHTS / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        for (uint32_t i = 0; i < TW_ENTRIES; ++i) {
+            mbar_init(&full[i], 4);
+            mbar_init(&empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(holder, 512);
+    fence_async_smem();
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *holder;
+    const uint32_t sbase = smem_u32(sm);
+    const uint32_t n = min(*n_dev, cap);
+    const uint32_t ntiles = (n + 127) / 128;
+    auto tile_of = [&](uint32_t k) { return blockIdx.x + k * gridDim.x; };
+
+    if (warp < 4 * TW_GROUPS) {
+        // ---- producer warp: group g = warp / 4, rows 32 (warp % 4) .. + 31 of tiles k = g, g + TW_GROUPS, ...
+        const uint32_t g = warp >> 2, row = 32 * (warp & 3u) + lane;
+        const uint32_t q = lane >> 3, ch = lane & 7;
+        for (uint32_t k = g; tile_of(k) < ntiles; k += TW_GROUPS) {
+            const uint32_t e = k % TW_ENTRIES, use = k / TW_ENTRIES;
+            const uint32_t j = tile_of(k) * 128 + row;
+            uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            uint32_t r6p[3] = {0, 0, 0}, wp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            float u[6] = {0, 0, 0, 0, 0, 0};
+            if (j < n) {
+                const uint32_t leaf = hit_leaf[j];
+                load_corners(T, leaf, corners);
+                hit_geom_regs<kBF16>(T, rays, hit_ray[j], leaf, hit_tin[j], hit_tout[j], r6p, wp, u, err);
+            }
+            if (use > 0) mbar_wait(&empty[e], (use - 1) & 1);
+            const uint32_t a_base = sbase + TW_RING0 + e * TW_ENTRY;
+            uint32_t* side = reinterpret_cast<uint32_t*>(sm + TW_RING0 + e * TW_ENTRY + T_A_BYTES);
+#pragma unroll 2
+            for (uint32_t p = 0; p < 8; ++p) {
+                const uint32_t src = 4 * p + q;
+                uint32_t cb[8], w[8];
+#pragma unroll
+                for (int b = 0; b < 8; ++b) cb[b] = __shfl_sync(0xffffffffu, corners[b], src);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) w[b] = __shfl_sync(0xffffffffu, wp[b], src);
+                uint4 fq[8];
+#pragma unroll
+                for (int b = 0; b < 8; ++b) fq[b] = __ldg(reinterpret_cast<const uint4*>(ft16 + size_t(cb[b]) * 64) + ch);
+                H2 a1[4], a2[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a1[i] = a2[i] = F::splat(0.f);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const H2 p1 = u2h<H2>(w[b / 2]), p2 = u2h<H2>(w[4 + b / 2]);
+                    const H2 h1 = (b & 1) ? F::hi2(p1) : F::lo2(p1);
+                    const H2 h2 = (b & 1) ? F::hi2(p2) : F::lo2(p2);
+                    const H2* f = reinterpret_cast<const H2*>(&fq[b]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        a1[i] = __hfma2(h1, f[i], a1[i]);
+                        a2[i] = __hfma2(h2, f[i], a2[i]);
+                    }
+                }
+                const uint32_t rr = (row & ~31u) + src;
+                st_shared_v4(a_base + a_off(rr, 8 * ch), h2u(a1[0]), h2u(a1[1]), h2u(a1[2]), h2u(a1[3]));
+                st_shared_v4(a_base + a_off(rr, 64 + 8 * ch), h2u(a2[0]), h2u(a2[1]), h2u(a2[2]), h2u(a2[3]));
+            }
+            st_shared_v4(a_base + a_off(row, 128), r6p[0], r6p[1], r6p[2], F::kOne);
+            st_shared_v4(a_base + a_off(row, 136), 0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int i = 0; i < 6; ++i) side[i * 128 + row] = __float_as_uint(u[i]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) side[(6 + i) * 128 + row] = r6p[i];
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[e])) : "memory");
+        }
+    } else {
+        // ---- MMA chain c: 4 warps, thread r owns row (TMEM lane) r
+        // TMEM: accumulator of chain c at columns 128c, its 16-bit A operand
+        // (hidden activations + the head's bias column) at 256 + 128c.
+        const uint32_t c = (warp - 4 * TW_GROUPS) >> 2, r = tid & 127;
+        const uint32_t lane_off = (32u * (warp & 3u)) << 16;
+        const uint32_t acc = tmem + 128 * c, a_t = tmem + 256 + 128 * c;
+        uint64_t* cbar = &bars[c];
+        uint32_t phase = 0;
+        const uint32_t bar_id = 1 + c;
+        {  // constant head-input columns: K 128 = 1 (bias), K 129..143 = 0
+            const uint32_t k1[8] = {F::kOne, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                             a_t + lane_off + 64),
+                         "r"(k1[0]), "r"(k1[1]), "r"(k1[2]), "r"(k1[3]), "r"(k1[4]), "r"(k1[5]), "r"(k1[6]),
+                         "r"(k1[7])
+                         : "memory");
+            tmem_wait_st();
+        }
+        auto sync_issue = [&](auto&& f) {
+            fence_before_sync();
+            named_sync(bar_id, 128);
+            if (r == 0) {
+                fence_after_sync();
+                f();
+                mma_commit(cbar);
+            }
+        };
+        auto wait = [&]() {
+            mbar_wait(cbar, phase);
+            phase ^= 1;
+            fence_after_sync();
+        };
+        for (uint32_t k = c; tile_of(k) < ntiles; k += TW_CHAINS) {
+            const uint32_t e = k % TW_ENTRIES, use = k / TW_ENTRIES;
+            mbar_wait(&full[e], use & 1);
+            const uint32_t* side = reinterpret_cast<const uint32_t*>(sm + TW_RING0 + e * TW_ENTRY + T_A_BYTES);
+            float u[6];
+            uint32_t r6p[3];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) u[i] = __uint_as_float(side[i * 128 + r]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) r6p[i] = side[(6 + i) * 128 + r];
+            sync_issue([&] {
+                issue_layer(acc, sbase + TW_RING0 + e * TW_ENTRY, sbase + OFF_WT0, KT, kIdesc);
+                mma_commit(&empty[e]);  // the ring entry is free once layer 0 completed
+            });
+            wait();
+#pragma unroll 1
+            for (uint32_t hh = 0; hh < 4; ++hh) {  // acc -> relu -> 16-bit pairs -> A (TMEM)
+                float v[32];
+                tmem_ld32(acc + lane_off + 32 * hh, v);
+                tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = F::relu_pack(v[2 * i], v[2 * i + 1]);
+                tmem_st16(a_t + lane_off + 16 * hh, pk);
+            }
+            tmem_wait_st();
+            sync_issue([&] { issue_layer_ta(acc, a_t, sbase + OFF_WT1, KT, kIdescHead); });
+            wait();
+            float hv[16];
+            tmem_ld16(acc + lane_off, hv);
+            tmem_wait_ld();
+            const uint32_t j = tile_of(k) * 128 + r;
+            if (j < n) {
+                const float ee = __fdividef(1.0f, 1.0f + __expf(-hv[1])), ome = 1.0f - ee;
+                out.tau[j] = fmaxf(hv[0], 0.f);
+                out.eta[j] = ee;
+                const float us[3] = {u[0] * ee + u[3] * ome, u[1] * ee + u[4] * ome, u[2] * ee + u[5] * ome};
+                float ws[8];
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    ws[b] = ((b & 1) ? us[0] : 1.f - us[0]) * ((b & 2) ? us[1] : 1.f - us[1]) *
+                            ((b & 4) ? us[2] : 1.f - us[2]);
+                crec[2 * size_t(j)] = make_uint4(r6p[0], r6p[1], r6p[2], 0u);
+                crec[2 * size_t(j) + 1] = make_uint4(F::pack(ws[0], ws[1]), F::pack(ws[2], ws[3]),
+                                                     F::pack(ws[4], ws[5]), F::pack(ws[6], ws[7]));
+            }
+        }
+    }
+    kernel_teardown(tmem);
+}
+
 int g_num_sms = 0;
 
 }  // namespace
@@ -927,14 +1137,21 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
     if (!attr) {
         SVLF_CUDA(cudaFuncSetAttribute(k_decode_t<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(T_SM_TOTAL)));
         SVLF_CUDA(cudaFuncSetAttribute(k_decode_c<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SM_TOTAL)));
+        SVLF_CUDA(cudaFuncSetAttribute(k_decode_t_ws<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(TW_SM_TOTAL)));
         SVLF_CUDA(cudaFuncSetAttribute(k_decode_c_tm<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(CT_SM_TOTAL)));
         attr = true;
     }
     const H* ft = reinterpret_cast<const H*>(p + OFF_FEAT);
     const H* fc = ft + size_t(M.V) * 64;
+#if SVLF_DEC_T_WS
+    k_decode_t_ws<kBF16><<<g_num_sms, TW_THREADS, TW_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout,
+                                                             n_dev, cap, out, crec, err);
+#else
     k_decode_t<kBF16><<<g_num_sms, kSlots * 128, T_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev,
                                                          cap, out, crec, err);
+#endif
 #if SVLF_DEC_C_TMEM
     k_decode_c_tm<kBF16><<<g_num_sms, kCtThreads, CT_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
 #else
