@@ -69,7 +69,7 @@ __host__ __device__ constexpr uint32_t a_off(uint32_t r, uint32_t k) {
 
 // ---- kernel shared memory
 #ifndef SVLF_DEC_EXP
-#define SVLF_DEC_EXP 0  // timing experiments only: 1 = producers skip the gather, 2 = consumers skip the MMAs
+#define SVLF_DEC_EXP 0  // timing experiments only: f_C (1, 2) / f_T (3, 4) producers skip the gather / consumers skip the MMAs
 #endif
 #ifndef SVLF_DEC_C_TMEM
 #define SVLF_DEC_C_TMEM 1
@@ -959,22 +959,37 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
         // ---- producer warp: group g = warp / 4, rows 32 (warp % 4) .. + 31 of tiles k = g, g + TW_GROUPS, ...
         const uint32_t g = warp >> 2, row = 32 * (warp & 3u) + lane;
         const uint32_t q = lane >> 3, ch = lane & 7;
+        // the per-hit scalars of a group's next tile are loaded a tile ahead
+        uint32_t nleaf = 0, nray = 0;
+        double ntin = 0.0, ntout = 0.0;
+        auto prefetch = [&](uint32_t t) {
+            const uint32_t jn = t * 128 + row;
+            if (t < ntiles && jn < n) {
+                nleaf = hit_leaf[jn];
+                nray = hit_ray[jn];
+                ntin = hit_tin[jn];
+                ntout = hit_tout[jn];
+            }
+        };
+        prefetch(tile_of(g));
         for (uint32_t k = g; tile_of(k) < ntiles; k += TW_GROUPS) {
             const uint32_t e = k % TW_ENTRIES, use = k / TW_ENTRIES;
             const uint32_t j = tile_of(k) * 128 + row;
             uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             uint32_t r6p[3] = {0, 0, 0}, wp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             float u[6] = {0, 0, 0, 0, 0, 0};
-            if (j < n) {
-                const uint32_t leaf = hit_leaf[j];
+            const uint32_t leaf = nleaf, ray_i = nray;
+            const double tin = ntin, tout = ntout;
+            prefetch(tile_of(k + TW_GROUPS));
+            if (j < n && SVLF_DEC_EXP != 3) {
                 load_corners(T, leaf, corners);
-                hit_geom_regs<kBF16>(T, rays, hit_ray[j], leaf, hit_tin[j], hit_tout[j], r6p, wp, u, err);
+                hit_geom_regs<kBF16>(T, rays, ray_i, leaf, tin, tout, r6p, wp, u, err);
             }
             if (use > 0) mbar_wait(&empty[e], (use - 1) & 1);
             const uint32_t a_base = sbase + TW_RING0 + e * TW_ENTRY;
             uint32_t* side = reinterpret_cast<uint32_t*>(sm + TW_RING0 + e * TW_ENTRY + T_A_BYTES);
 #pragma unroll 2
-            for (uint32_t p = 0; p < 8; ++p) {
+            for (uint32_t p = 0; p < (SVLF_DEC_EXP == 3 ? 0 : 8); ++p) {
                 const uint32_t src = 4 * p + q;
                 uint32_t cb[8], w[8];
 #pragma unroll
@@ -1015,11 +1030,11 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
         }
     } else {
         // ---- MMA chain c: 4 warps, thread r owns row (TMEM lane) r
-        // TMEM: accumulator of chain c at columns 128c, its 16-bit A operand
-        // (hidden activations + the head's bias column) at 256 + 128c.
+        // TMEM (256 columns per chain): accumulator, head output, and the 16-bit
+        // A operand (hidden activations + the head's bias column).
         const uint32_t c = (warp - 4 * TW_GROUPS) >> 2, r = tid & 127;
         const uint32_t lane_off = (32u * (warp & 3u)) << 16;
-        const uint32_t acc = tmem + 128 * c, a_t = tmem + 256 + 128 * c;
+        const uint32_t acc = tmem + 256 * c, a_t = acc + 160;  // [acc 128 | head 16 | .. | A 72]
         uint64_t* cbar = &bars[c];
         uint32_t phase = 0;
         const uint32_t bar_id = 1 + c;
@@ -1046,21 +1061,33 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             phase ^= 1;
             fence_after_sync();
         };
-        for (uint32_t k = c; tile_of(k) < ntiles; k += TW_CHAINS) {
-            const uint32_t e = k % TW_ENTRIES, use = k / TW_ENTRIES;
-            mbar_wait(&full[e], use & 1);
+        // Software-pipelined chain: the head MMA of tile k (into columns
+        // 128..143) and layer 0 of tile k + TW_CHAINS are issued together, so
+        // each tile costs one MMA round trip; tile k's outputs are written
+        // while tile k + TW_CHAINS's epilogue is next.
+        const uint32_t d_head = acc + 128;
+        float u[6];
+        uint32_t r6p[3];
+        auto read_side = [&](uint32_t e) {
             const uint32_t* side = reinterpret_cast<const uint32_t*>(sm + TW_RING0 + e * TW_ENTRY + T_A_BYTES);
-            float u[6];
-            uint32_t r6p[3];
 #pragma unroll
             for (int i = 0; i < 6; ++i) u[i] = __uint_as_float(side[i * 128 + r]);
 #pragma unroll
             for (int i = 0; i < 3; ++i) r6p[i] = side[(6 + i) * 128 + r];
-            sync_issue([&] {
-                issue_layer(acc, sbase + TW_RING0 + e * TW_ENTRY, sbase + OFF_WT0, KT, kIdesc);
-                mma_commit(&empty[e]);  // the ring entry is free once layer 0 completed
-            });
+        };
+        auto layer0 = [&](uint32_t k) {
+            const uint32_t e = k % TW_ENTRIES;
+            issue_layer(acc, sbase + TW_RING0 + e * TW_ENTRY, sbase + OFF_WT0, KT, kIdesc);
+            mma_commit(&empty[e]);  // the ring entry is free once layer 0 completed
+        };
+        uint32_t k = c;
+        if (tile_of(k) < ntiles) {
+            mbar_wait(&full[k % TW_ENTRIES], (k / TW_ENTRIES) & 1);
+            read_side(k % TW_ENTRIES);
+            sync_issue([&] { layer0(k); });
             wait();
+        }
+        for (; tile_of(k) < ntiles; k += TW_CHAINS) {
 #pragma unroll 1
             for (uint32_t hh = 0; hh < 4; ++hh) {  // acc -> relu -> 16-bit pairs -> A (TMEM)
                 float v[32];
@@ -1072,23 +1099,38 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
                 tmem_st16(a_t + lane_off + 16 * hh, pk);
             }
             tmem_wait_st();
-            sync_issue([&] { issue_layer_ta(acc, a_t, sbase + OFF_WT1, KT, kIdescHead); });
+            const uint32_t kn = k + TW_CHAINS;
+            const bool next = tile_of(kn) < ntiles;
+            float cu[6];
+            uint32_t cr6[3];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) cu[i] = u[i];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) cr6[i] = r6p[i];
+            if (next) {
+                mbar_wait(&full[kn % TW_ENTRIES], (kn / TW_ENTRIES) & 1);
+                read_side(kn % TW_ENTRIES);
+            }
+            sync_issue([&] {
+                issue_layer_ta(d_head, a_t, sbase + OFF_WT1, KT, kIdescHead);
+                if (next) layer0(kn);
+            });
             wait();
             float hv[16];
-            tmem_ld16(acc + lane_off, hv);
+            tmem_ld16(d_head + lane_off, hv);
             tmem_wait_ld();
             const uint32_t j = tile_of(k) * 128 + r;
             if (j < n) {
                 const float ee = __fdividef(1.0f, 1.0f + __expf(-hv[1])), ome = 1.0f - ee;
                 out.tau[j] = fmaxf(hv[0], 0.f);
                 out.eta[j] = ee;
-                const float us[3] = {u[0] * ee + u[3] * ome, u[1] * ee + u[4] * ome, u[2] * ee + u[5] * ome};
+                const float us[3] = {cu[0] * ee + cu[3] * ome, cu[1] * ee + cu[4] * ome, cu[2] * ee + cu[5] * ome};
                 float ws[8];
 #pragma unroll
                 for (int b = 0; b < 8; ++b)
                     ws[b] = ((b & 1) ? us[0] : 1.f - us[0]) * ((b & 2) ? us[1] : 1.f - us[1]) *
                             ((b & 4) ? us[2] : 1.f - us[2]);
-                crec[2 * size_t(j)] = make_uint4(r6p[0], r6p[1], r6p[2], 0u);
+                crec[2 * size_t(j)] = make_uint4(cr6[0], cr6[1], cr6[2], 0u);
                 crec[2 * size_t(j) + 1] = make_uint4(F::pack(ws[0], ws[1]), F::pack(ws[2], ws[3]),
                                                      F::pack(ws[4], ws[5]), F::pack(ws[6], ws[7]));
             }
