@@ -158,9 +158,10 @@ struct HitArgs {
     const uint32_t* dpos;
     const int* surf_rel;
     uint32_t N;
+    uint32_t ld;    // row stride of acts / deltas / dX: N rounded up to 32 (aligned GEMM operands)
     bool surface;
-    float* acts;    // A_ROWS x N
-    float* deltas;  // D_ROWS x N
+    float* acts;    // A_ROWS x ld
+    float* deltas;  // D_ROWS x ld
     float* tau;
     float* eta;
     float* rgb;     // 3 x N (channel-major)
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevMode
     __shared__ float st[kInWarps][2 * kFt][33];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
+    const size_t L = H.ld;  // row stride of the feature-major matrices
     const uint32_t j0 = (blockIdx.x * kInWarps + warp) * 32;
     if (j0 >= N) return;
     const uint32_t j = j0 + lane;
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevMode
     float* X = H.acts + j;
     if (j < N)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) X[(A_XT + k) * N] = ok ? g.r6[k] : 0.f;
+        for (int k = 0; k < 6; ++k) X[(A_XT + k) * L] = ok ? g.r6[k] : 0.f;
     uint32_t cs[8];
     float w1[8], w2[8];
 #pragma unroll
@@ -284,14 +286,14 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevMode
     __syncwarp();
     if (j < N)
 #pragma unroll 8
-        for (int r = 0; r < 2 * kFt; ++r) X[(A_XT + 6 + r) * N] = st[warp][r][lane];
+        for (int r = 0; r < 2 * kFt; ++r) X[(A_XT + 6 + r) * L] = st[warp][r][lane];
 }
 
 // y = relu(y + b[row]) over a rows x N feature-major block (GEMM epilogue)
-__global__ void k_bias_relu(float* __restrict__ Y, const float* __restrict__ bias, size_t N) {
+__global__ void k_bias_relu(float* __restrict__ Y, const float* __restrict__ bias, size_t N, size_t ld) {
     const uint32_t row = blockIdx.y;
     const float b = __ldg(bias + row);
-    float* y = Y + size_t(row) * N;
+    float* y = Y + size_t(row) * ld;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < N; i += size_t(gridDim.x) * blockDim.x)
         y[i] = fmaxf(y[i] + b, 0.f);
 }
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel
     __shared__ float st[kInWarps][kFc][33];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
+    const size_t L = H.ld;  // row stride of the feature-major matrices
     const uint32_t j0 = (blockIdx.x * kInWarps + warp) * 32;
     if (j0 >= N) return;
     const uint32_t j = j0 + lane;
@@ -312,11 +315,11 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel
     float* X = H.acts + j;
     float eta = 0.5f;
     if (valid) {
-        const float* h = X + A_HT * N;
+        const float* h = X + A_HT * L;
         float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
 #pragma unroll 4
         for (int k = 0; k < kHid; ++k) {
-            const float v = h[k * N];
+            const float v = h[k * L];
             y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
             y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
         }
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel
     }
     if (valid)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) X[(A_XC + k) * N] = ok ? g.r6[k] : 0.f;
+        for (int k = 0; k < 6; ++k) X[(A_XC + k) * L] = ok ? g.r6[k] : 0.f;
     uint32_t cs[8];
 #pragma unroll
     for (int b = 0; b < 8; ++b) cs[b] = ok ? g.corners[b] : 0u;
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel
     __syncwarp();
     if (valid)
 #pragma unroll 8
-        for (int r = 0; r < kFc; ++r) X[(A_XC + 6 + r) * N] = st[warp][r][lane];
+        for (int r = 0; r < kFc; ++r) X[(A_XC + 6 + r) * L] = st[warp][r][lane];
 }
 
 // f_C head: rgb = sigmoid(W3 h3 + b3)
@@ -367,15 +370,16 @@ __global__ void __launch_bounds__(128) k_fwd_rgb(DevModel M, HitArgs H) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= H.N) return;
     const size_t N = H.N;
+    const size_t L = H.ld;  // row stride of the feature-major matrices
     if (!has_color(H, j)) {
         for (int c = 0; c < 3; ++c) H.rgb[c * N + j] = 0.f;
         return;
     }
-    const float* h = H.acts + A_H3 * N + j;
+    const float* h = H.acts + A_H3 * L + j;
     float y[3] = {__ldg(M.mc + D::C_B3), __ldg(M.mc + D::C_B3 + 1), __ldg(M.mc + D::C_B3 + 2)};
 #pragma unroll 4
     for (int k = 0; k < kHid; ++k) {
-        const float v = h[k * N];
+        const float v = h[k * L];
 #pragma unroll
         for (int c = 0; c < 3; ++c) y[c] = fmaf(__ldg(M.mc + D::C_W3 + c * kHid + k), v, y[c]);
     }
@@ -491,6 +495,7 @@ __global__ void __launch_bounds__(128) k_bwd_head_c(DevModel M, HitArgs H) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= H.N) return;
     const size_t N = H.N;
+    const size_t L = H.ld;  // row stride of the feature-major matrices
     float* Dl = H.deltas + j;
     float d3[3] = {0.f, 0.f, 0.f};
     if (has_color(H, j))
@@ -499,17 +504,17 @@ __global__ void __launch_bounds__(128) k_bwd_head_c(DevModel M, HitArgs H) {
             d3[o] = H.drgb[o * N + j] * a * (1.0f - a);
         }
 #pragma unroll
-    for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * N] = d3[o];
-    const float* h3 = H.acts + A_H3 * N + j;
+    for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * L] = d3[o];
+    const float* h3 = H.acts + A_H3 * L + j;
 #pragma unroll 4
     for (int k = 0; k < kHid; ++k) {
         float v = 0.f;
-        if (h3[k * N] > 0.f) {
+        if (h3[k * L] > 0.f) {
             v = __ldg(M.mc + D::C_W3 + k) * d3[0];
             v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
             v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
         }
-        Dl[(D_C2 + k) * N] = v;
+        Dl[(D_C2 + k) * L] = v;
     }
 }
 
@@ -539,6 +544,7 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevMo
     __shared__ double dots[kScWarps][32][8];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
+    const size_t L = H.ld;  // row stride of the feature-major matrices
     const uint32_t j0 = (blockIdx.x * kScWarps + warp) * 32;
     if (j0 >= N) return;
     const uint32_t j = j0 + lane;
@@ -563,7 +569,7 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevMo
         }
     }
 #pragma unroll 4
-    for (int d = 0; d < kFc; ++d) zs[warp][d][lane] = act ? dX[(6 + d) * N + j] : 0.f;
+    for (int d = 0; d < kFc; ++d) zs[warp][d][lane] = act ? dX[(6 + d) * L + j] : 0.f;
     __syncwarp();
     unsigned live = __ballot_sync(0xffffffffu, act);
     // scatter + <z_b, dz> per corner, hit by hit
@@ -618,14 +624,14 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevMo
     const float tau = H.tau[j], eta = H.eta[j];
     const float d0 = tau > 0.f ? float(H.dtau[j]) : 0.f;
     const float d1 = float(deta) * eta * (1.0f - eta);
-    Dl[D_T1 * N] = d0;
-    Dl[(D_T1 + 1) * N] = d1;
-    const float* ht = H.acts + A_HT * N + j;
+    Dl[D_T1 * L] = d0;
+    Dl[(D_T1 + 1) * L] = d1;
+    const float* ht = H.acts + A_HT * L + j;
 #pragma unroll 4
     for (int k = 0; k < kHid; ++k) {
         float v = 0.f;
-        if (ht[k * N] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
-        Dl[(D_T0 + k) * N] = v;
+        if (ht[k * L] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
+        Dl[(D_T0 + k) * L] = v;
     }
 }
 
@@ -638,6 +644,7 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_t(DevOctree T, HitAr
     __shared__ float w1s[kScWarps][32][8], w2s[kScWarps][32][8];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t N = H.N;
+    const size_t L = H.ld;  // row stride of the feature-major matrices
     const uint32_t j0 = (blockIdx.x * kScWarps + warp) * 32;
     if (j0 >= N) return;
     const uint32_t j = j0 + lane;
@@ -656,8 +663,8 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_t(DevOctree T, HitAr
         __syncwarp();
 #pragma unroll 4
         for (int r = 0; r < 32; ++r) {
-            zs[warp][r][lane] = act ? dX[(6 + 32 * half + r) * N + j] : 0.f;
-            zs[warp][32 + r][lane] = act ? dX[(6 + kFt + 32 * half + r) * N + j] : 0.f;
+            zs[warp][r][lane] = act ? dX[(6 + 32 * half + r) * L + j] : 0.f;
+            zs[warp][32 + r][lane] = act ? dX[(6 + kFt + 32 * half + r) * L + j] : 0.f;
         }
         __syncwarp();
         unsigned live = live0;
@@ -794,11 +801,14 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     uint32_t* dray = S.dray.ensure<uint32_t>(N + 1);
     float* hitf = S.hitf.ensure<float>(size_t(N) * 8 + 8);
     double* hitd = S.hitd.ensure<double>(size_t(N) * 5 + 5);
-    float* acts = S.acts.ensure<float>(size_t(A_ROWS) * N + 1);
-    float* deltas = S.deltas.ensure<float>(size_t(D_ROWS) * N + 1);
+    // feature-major matrices with rows padded to 32 floats: aligned leading
+    // dimensions let cuBLAS use its vectorised (align4) SGEMM kernels
+    const uint32_t Np = (N + 31u) & ~31u;
+    float* acts = S.acts.ensure<float>(size_t(A_ROWS) * Np + 1);
+    float* deltas = S.deltas.ensure<float>(size_t(D_ROWS) * Np + 1);
     SVLF_CUDA(cudaMemsetAsync(hitd, 0, size_t(N) * 2 * 8, s));                 // dtau, deta
     SVLF_CUDA(cudaMemsetAsync(hitf + size_t(N) * 5, 0, size_t(N) * 3 * 4, s));  // drgb
-    float* dxs = S.dxs.ensure<float>(size_t(kInT) * N + 1);                     // dL/d layer-0 inputs
+    float* dxs = S.dxs.ensure<float>(size_t(kInT) * Np + 1);                     // dL/d layer-0 inputs
     if (n) k_expand<<<(n + 127) / 128, 128, 0, s>>>(n, act_first, act_cnt, dpos, dhit, dray);
 
     // Dense layers as fp32 GEMMs on the feature-major matrices. A feature-major
@@ -818,33 +828,33 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     // on tensor cores with TF32 operands when the context asks for it
     cublas_check(B.SetMathMode(hb, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");
     const float one = 1.f, zero = 0.f;
-    const int Ni = int(N);
+    const int Ni = int(N), Li = int(Np);
     // Y(O x N) = W X: rows [xrow, xrow+K) -> [yrow, yrow+O) of acts
     auto layer_fwd = [&](const float* W, int O, int K, int xrow, int yrow, const float* bias) {
-        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Ni, O, K, &one, acts + size_t(xrow) * N, Ni, W, K, &zero,
-                             acts + size_t(yrow) * N, Ni),
+        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Ni, O, K, &one, acts + size_t(xrow) * Np, Li, W, K, &zero,
+                             acts + size_t(yrow) * Np, Li),
                      "sgemm fwd");
         k_bias_relu<<<dim3(unsigned(std::min<size_t>((N + 255) / 256, 1184)), unsigned(O)), 256, 0, s>>>(
-            acts + size_t(yrow) * N, bias, N);
+            acts + size_t(yrow) * Np, bias, N, Np);
     };
     // dX rows [k0, K) (x N) = W^T D, D = delta rows [drow, drow+O)
     auto layer_bwd = [&](const float* W, int O, int K, int k0, int drow, float* dst) {
-        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, Ni, K - k0, O, &one, deltas + size_t(drow) * N, Ni, W + k0,
-                             K, &zero, dst, Ni),
+        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, Ni, K - k0, O, &one, deltas + size_t(drow) * Np, Li, W + k0,
+                             K, &zero, dst, Li),
                      "sgemm bwd");
     };
     // dW(O x K) = D X^T, db = D 1
     float* ones = S.ones.ensure<float>(size_t(N) + 1);
     auto layer_dw = [&](int drow, int O, int xrow, int K, float* dW, float* db) {
-        cublas_check(B.Sgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, K, O, Ni, &one, acts + size_t(xrow) * N, Ni,
-                             deltas + size_t(drow) * N, Ni, &zero, dW, K),
+        cublas_check(B.Sgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, K, O, Ni, &one, acts + size_t(xrow) * Np, Li,
+                             deltas + size_t(drow) * Np, Li, &zero, dW, K),
                      "sgemm dW");
-        cublas_check(B.Sgemv(hb, CUBLAS_OP_T, Ni, O, &one, deltas + size_t(drow) * N, Ni, ones, 1, &zero, db, 1),
+        cublas_check(B.Sgemv(hb, CUBLAS_OP_T, Ni, O, &one, deltas + size_t(drow) * Np, Li, ones, 1, &zero, db, 1),
                      "sgemv db");
     };
     const unsigned hit_blocks = (N + 127) / 128;
 
-    HitArgs H{b.rays, b.hit_leaf, b.hit_tin, b.hit_tout, dhit, dray, dpos, surf_rel, N, o.surface, acts, deltas,
+    HitArgs H{b.rays, b.hit_leaf, b.hit_tin, b.hit_tout, dhit, dray, dpos, surf_rel, N, Np, o.surface, acts, deltas,
               hitf, hitf + N, hitf + 2 * size_t(N), hitf + 5 * size_t(N), hitd, hitd + N};
     SVLF_CUDA(cudaEventRecord(S.ev[1], s));
     if (N) {
@@ -879,18 +889,18 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     float* g_mt = g_fc + M.n_fc;
     float* g_mc = g_mt + SVLF_DEC_T_SIZE;
     if (N) {
-        const unsigned mask_blocks = unsigned(std::min<size_t>((size_t(kHid) * N + 255) / 256, 4736));
+        const unsigned mask_blocks = unsigned(std::min<size_t>((size_t(kHid) * Np + 255) / 256, 4736));
         // f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
         k_bwd_head_c<<<hit_blocks, 128, 0, s>>>(M.view, H);
-        layer_bwd(M.view.mc + D::C_W2, kHid, kHid, 0, D_C2, deltas + size_t(D_C1) * N);
-        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C1) * N, acts + size_t(A_H2) * N, size_t(kHid) * N);
-        layer_bwd(M.view.mc + D::C_W1, kHid, kHid, 0, D_C1, deltas + size_t(D_C0) * N);
-        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C0) * N, acts + size_t(A_H1) * N, size_t(kHid) * N);
-        layer_bwd(M.view.mc + D::C_W0, kHid, kInC, 6, D_C0, dxs + 6 * size_t(N));
+        layer_bwd(M.view.mc + D::C_W2, kHid, kHid, 0, D_C2, deltas + size_t(D_C1) * Np);
+        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C1) * Np, acts + size_t(A_H2) * Np, size_t(kHid) * Np);
+        layer_bwd(M.view.mc + D::C_W1, kHid, kHid, 0, D_C1, deltas + size_t(D_C0) * Np);
+        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C0) * Np, acts + size_t(A_H1) * Np, size_t(kHid) * Np);
+        layer_bwd(M.view.mc + D::C_W0, kHid, kInC, 6, D_C0, dxs + 6 * size_t(Np));
         // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
         const unsigned sc_blocks = unsigned((size_t(N) + 32 * kScWarps - 1) / (32 * kScWarps));
         k_bwd_feat_c<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
-        layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(N));
+        layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(Np));
         k_bwd_feat_t<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
         // weight gradients (sums over hits)
         if (o.tf32) cublas_check(B.SetMathMode(hb, CUBLAS_TF32_TENSOR_OP_MATH), "cublasSetMathMode");
