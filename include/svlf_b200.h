@@ -284,6 +284,13 @@ svlf_status svlf_backproject_device(svlf_ctx* ctx, const svlf_camera* cam, const
 /* psnr (src/metrics.cpp:57-68) over n values (any channel count). */
 svlf_status svlf_psnr_device(svlf_ctx* ctx, const float* d_pred, const float* d_gt, size_t n_values,
                              double* psnr);
+/* ssim (src/metrics.cpp:70-113): per-channel 11x11 Gaussian (sigma 1.5)
+ * windowed SSIM over the valid region, K1 = 0.01, K2 = 0.03, dynamic range 1,
+ * averaged over pixels and channels; images interleaved W*H*channels floats.
+ * SVLF_ERR_INVALID_ARGUMENT ("image smaller than the SSIM window") when W or
+ * H < 11. */
+svlf_status svlf_ssim_device(svlf_ctx* ctx, const float* d_pred, const float* d_gt, uint32_t width, uint32_t height,
+                             uint32_t channels, double* ssim);
 /* depth_errors (src/metrics.cpp:115-136): RMSE / MAE over pixels with gt
  * mask >= 0.5; empty mask -> (0, 0) and *empty_mask = 1. */
 svlf_status svlf_depth_errors_device(svlf_ctx* ctx, const float* d_pred_depth, const float* d_gt_depth,

@@ -362,6 +362,17 @@ class Reference:
     def thread_count(self):
         return self.lib.ref_thread_count()
 
+    def metrics(self, pred, gt, w, h, channels):
+        """(psnr, ssim) of the reference (src/metrics.cpp:57-113) on interleaved float images."""
+        a = np.ascontiguousarray(pred, dtype=np.float32).reshape(-1)
+        b = np.ascontiguousarray(gt, dtype=np.float32).reshape(-1)
+        p, q = C.c_double(), C.c_double()
+        self.lib.ref_metrics.argtypes = [_fp, _fp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]
+        if self.lib.ref_metrics(a, b, w, h, channels, C.byref(p), C.byref(q)):
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return p.value, q.value
+
     def tree_build(self, points, res, dilation=1, lo=None, hi=None):
         pts = _f64(points).reshape(-1, 3)
         h = self.lib.ref_octree_build(pts, pts.shape[0], res, dilation, _box(lo), _box(hi))
@@ -585,3 +596,30 @@ def random_rays(seed, n, o=None):
     out = np.zeros((n, 6))
     lib.or_random_rays(seed, n, out)
     return out
+
+
+def ssim(pred, gt, w, h, channels):
+    """Restatement of ssim (src/metrics.cpp:70-113) in fp64 numpy: per channel,
+    separable 11-tap Gaussian (sigma 1.5, gaussian_kernel :21-32) over the
+    valid region (blur_valid :35-54, horizontal then vertical), the SSIM map
+    with C1 = 0.01^2, C2 = 0.03^2 and its mean; channels averaged."""
+    if w < 11 or h < 11:
+        raise ValueError("image smaller than the SSIM window")
+    k = np.exp(-((np.arange(11) - 5.0) ** 2) / (2.0 * 1.5 * 1.5))
+    k = k / k.sum()
+    a = np.asarray(pred, np.float32).reshape(h, w, channels).astype(np.float64)
+    b = np.asarray(gt, np.float32).reshape(h, w, channels).astype(np.float64)
+
+    def blur(p):
+        t = sum(k[i] * p[:, i:w - 10 + i] for i in range(11))
+        return sum(k[i] * t[i:h - 10 + i, :] for i in range(11))
+
+    c1, c2 = 0.01 ** 2, 0.03 ** 2
+    total = 0.0
+    for ch in range(channels):
+        x, y = a[:, :, ch], b[:, :, ch]
+        mx, my, mxx, myy, mxy = blur(x), blur(y), blur(x * x), blur(y * y), blur(x * y)
+        vx, vy, cov = mxx - mx * mx, myy - my * my, mxy - mx * my
+        m = ((2 * mx * my + c1) * (2 * cov + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2))
+        total += m.mean()
+    return total / channels

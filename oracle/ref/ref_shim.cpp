@@ -14,6 +14,7 @@
 
 #include "svlf/camera.hpp"
 #include "svlf/dataset.hpp"
+#include "svlf/metrics.hpp"
 #include "svlf/model.hpp"
 #include "svlf/octree.hpp"
 #include "svlf/render.hpp"
@@ -464,6 +465,18 @@ int ref_train2(void* sp, const double* cams, const int* splits, int n_frames, ui
         *log_n = k;
         if (skipped) *skipped = r.skipped_rays;
         if (model_out) *model_out = new SvlfModel(std::move(r.model));
+    });
+}
+
+// ---- metrics (src/metrics.cpp): images as interleaved float planes --------
+int ref_metrics(const float* pred, const float* gt, uint32_t w, uint32_t h, uint32_t channels, double* psnr_out,
+                double* ssim_out) {
+    return guarded([&] {
+        Image a = Image::make(w, h, channels), b = Image::make(w, h, channels);
+        std::memcpy(a.px.data(), pred, a.px.size() * 4);
+        std::memcpy(b.px.data(), gt, b.px.size() * 4);
+        *psnr_out = psnr(a, b);
+        *ssim_out = ssim(a, b);
     });
 }
 

@@ -192,6 +192,7 @@ def load_library():
         "svlf_render_gt_device": ([vp, vp, vp, vp, vp, vp], st),
         "svlf_backproject_device": ([vp, vp, vp, vp, sz, C.POINTER(sz)], st),
         "svlf_psnr_device": ([vp, vp, vp, sz, C.POINTER(C.c_double)], st),
+        "svlf_ssim_device": ([vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)], st),
         "svlf_depth_errors_device": ([vp, vp, vp, vp, sz, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                       C.POINTER(C.c_int)], st),
         "svlf_host_alloc": ([sz, vp], st),
@@ -623,6 +624,14 @@ def backproject_device(ctx: Context, camera: Camera, d_depth: int, d_points: int
 def psnr_device(ctx: Context, d_pred: int, d_gt: int, n_values: int) -> float:
     out = C.c_double()
     _check(_LIB.svlf_psnr_device(ctx.handle, C.c_void_p(d_pred), C.c_void_p(d_gt), n_values, C.byref(out)))
+    return out.value
+
+
+def ssim_device(ctx: Context, d_pred: int, d_gt: int, width: int, height: int, channels: int = 3) -> float:
+    """ssim (src/metrics.cpp:70-113) of two interleaved float images on the device."""
+    out = C.c_double()
+    _check(_LIB.svlf_ssim_device(ctx.handle, C.c_void_p(d_pred), C.c_void_p(d_gt), width, height, channels,
+                                 C.byref(out)))
     return out.value
 
 

@@ -707,6 +707,22 @@ svlf_status svlf_psnr_device(svlf_ctx* ctx, const float* d_pred, const float* d_
     });
 }
 
+svlf_status svlf_ssim_device(svlf_ctx* ctx, const float* d_pred, const float* d_gt, uint32_t w, uint32_t h,
+                             uint32_t channels, double* ssim) {
+    return guard([&] {
+        require(ctx && d_pred && d_gt && ssim, "null argument");
+        if (w < 11 || h < 11) fail(SVLF_ERR_INVALID_ARGUMENT, "image smaller than the SSIM window");
+        if (channels == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "channels must be > 0");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        std::vector<double> hp(reduction_partials());
+        DevBuf tmp;
+        double* t = tmp.ensure<double>(ssim_scratch_doubles(w, h));
+        *ssim = device_ssim(d_pred, d_gt, w, h, channels, t, ctx->tmp64.ensure<double>(reduction_partials()),
+                            hp.data(), ctx->stream);
+    });
+}
+
 svlf_status svlf_depth_errors_device(svlf_ctx* ctx, const float* pd, const float* gd, const float* gm, size_t n,
                                      double* rmse, double* mae, int* empty) {
     return guard([&] {

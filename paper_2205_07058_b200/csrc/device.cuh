@@ -166,6 +166,10 @@ void launch_render_gt(const svlf_scene_desc& d, const double* d_spheres, const d
 void launch_backproject(const DevCamera& cam, const float* depth, double* pts, size_t cap, unsigned long long* count,
                         cudaStream_t s);
 double device_sq_err(const float* pred, const float* gt, size_t n, double* part, double* h_part, cudaStream_t s);
+// ssim (src/metrics.cpp:70-113); tmp holds ssim_scratch_doubles(w, h) doubles
+size_t ssim_scratch_doubles(uint32_t w, uint32_t h);
+double device_ssim(const float* pred, const float* gt, uint32_t w, uint32_t h, uint32_t channels, double* tmp,
+                   double* part, double* h_part, cudaStream_t s);
 void device_depth_err(const float* pd, const float* gd, const float* gm, size_t n, double* part, double* h_part,
                       double* sum2, double* sum1, double* count, cudaStream_t s);
 size_t reduction_partials();

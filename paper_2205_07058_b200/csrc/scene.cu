@@ -11,6 +11,11 @@
 //   k_sq_err      psnr (src/metrics.cpp:57-68) and depth RMSE/MAE over the
 //                 gt mask (:115-136): per-block fp64 partial sums in a fixed
 //                 order, summed on the host in block order (deterministic)
+//   k_ssim_h/_v   ssim (src/metrics.cpp:70-113): separable valid-region
+//                 Gaussian in fp64 (horizontal, then vertical + SSIM map and
+//                 block partial sums), per channel
+#include <cmath>
+
 #include "device.cuh"
 
 namespace svlfb {
@@ -191,7 +196,99 @@ __global__ void k_depth_err(const float* __restrict__ pd, const float* __restric
 
 constexpr unsigned kRedBlocks = 296;
 
+// ---- ssim (src/metrics.cpp:70-113): per channel, separable 11-tap Gaussian
+// over the valid region in fp64 (horizontal pass, then vertical), the SSIM
+// map, and its mean; channels averaged.
+constexpr int kSsimWin = 11;
+struct Gauss11 {
+    double k[kSsimWin];
+};
+
+// tmp planes (vw x h each): blur_h of x, y, x^2, y^2, xy
+__global__ void k_ssim_h(const float* __restrict__ pred, const float* __restrict__ gt, uint32_t w, uint32_t h,
+                         uint32_t channels, uint32_t ch, Gauss11 g, double* __restrict__ tmp) {
+    const uint32_t vw = w - kSsimWin + 1;
+    const size_t plane = size_t(vw) * h;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < plane; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t x = uint32_t(i % vw), y = uint32_t(i / vw);
+        double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int t = 0; t < kSsimWin; ++t) {
+            const size_t src = (size_t(y) * w + x + t) * channels + ch;
+            const double xv = double(pred[src]), yv = double(gt[src]);
+            const double v[5] = {xv, yv, dmul(xv, xv), dmul(yv, yv), dmul(xv, yv)};
+#pragma unroll
+            for (int q = 0; q < 5; ++q) a[q] = dadd(a[q], dmul(g.k[t], v[q]));
+        }
+#pragma unroll
+        for (int q = 0; q < 5; ++q) tmp[q * plane + i] = a[q];
+    }
+}
+
+__global__ void k_ssim_v(const double* __restrict__ tmp, uint32_t vw, uint32_t h, Gauss11 g, double c1, double c2,
+                         double* part) {
+    __shared__ double sh[kRedThreads];
+    const uint32_t vh = h - kSsimWin + 1;
+    const size_t plane = size_t(vw) * h, n = size_t(vw) * vh;
+    double acc = 0.0;
+    for (size_t i = blockIdx.x * size_t(kRedThreads) + threadIdx.x; i < n; i += size_t(gridDim.x) * kRedThreads) {
+        const uint32_t x = uint32_t(i % vw), y = uint32_t(i / vw);
+        double m[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int t = 0; t < kSsimWin; ++t) {
+            const size_t src = size_t(y + t) * vw + x;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[q] = dadd(m[q], dmul(g.k[t], tmp[q * plane + src]));
+        }
+        const double mu_x = m[0], mu_y = m[1];
+        const double var_x = dsub(m[2], dmul(mu_x, mu_x)), var_y = dsub(m[3], dmul(mu_y, mu_y));
+        const double cov = dsub(m[4], dmul(mu_x, mu_y));
+        const double num = dmul(dadd(dmul(2.0, dmul(mu_x, mu_y)), c1), dadd(dmul(2.0, cov), c2));
+        const double den = dmul(dadd(dadd(dmul(mu_x, mu_x), dmul(mu_y, mu_y)), c1), dadd(dadd(var_x, var_y), c2));
+        acc = dadd(acc, num / den);
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+        if (int(threadIdx.x) < s) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
 }  // namespace
+
+size_t ssim_scratch_doubles(uint32_t w, uint32_t h) {
+    return w < uint32_t(kSsimWin) ? 0 : size_t(5) * (w - kSsimWin + 1) * h;
+}
+
+double device_ssim(const float* pred, const float* gt, uint32_t w, uint32_t h, uint32_t channels, double* tmp,
+                   double* part, double* h_part, cudaStream_t s) {
+    Gauss11 g;  // gaussian_kernel (src/metrics.cpp:21-32)
+    double sum = 0.0;
+    for (int i = 0; i < kSsimWin; ++i) {
+        const double d = i - kSsimWin / 2;
+        g.k[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+        sum += g.k[i];
+    }
+    for (double& v : g.k) v /= sum;
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    const uint32_t vw = w - kSsimWin + 1, vh = h - kSsimWin + 1;
+    double total = 0.0;
+    for (uint32_t ch = 0; ch < channels; ++ch) {
+        const size_t plane = size_t(vw) * h;
+        k_ssim_h<<<unsigned(std::min<size_t>((plane + 255) / 256, 148 * 16)), 256, 0, s>>>(pred, gt, w, h, channels, ch,
+                                                                                         g, tmp);
+        k_ssim_v<<<kRedBlocks, kRedThreads, 0, s>>>(tmp, vw, h, g, c1, c2, part);
+        note_launch(2);
+        SVLF_CUDA(cudaMemcpyAsync(h_part, part, kRedBlocks * 8, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        double acc = 0.0;
+        for (unsigned b = 0; b < kRedBlocks; ++b) acc += h_part[b];
+        total += acc / double(size_t(vw) * vh);
+    }
+    return total / channels;
+}
 
 void launch_render_gt(const svlf_scene_desc& d, const double* d_spheres, const double* d_boxes, const DevCamera& cam,
                       float* rgb, float* depth, float* mask, cudaStream_t s) {

@@ -95,3 +95,16 @@ def test_adam(oracle, reference_nofma):
         out.append((pp, m, v))
     for x, y in zip(*out):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("w,h,c", [(40, 30, 3), (11, 11, 1), (64, 17, 3)])
+def test_metrics_port(reference, w, h, c):
+    """oracle.ssim (numpy restatement of src/metrics.cpp:70-113) against the reference's ssim."""
+    from oracle import ssim
+
+    rng = np.random.default_rng(w * h + c)
+    gt = rng.random(w * h * c).astype(np.float32)
+    pred = np.clip(gt + rng.normal(0, 0.05, gt.shape), 0, 1).astype(np.float32)
+    _, want = reference.metrics(pred, gt, w, h, c)
+    assert ssim(pred, gt, w, h, c) == pytest.approx(want, rel=1e-13)
+    assert reference.metrics(gt, gt, w, h, c) == (99.0, pytest.approx(1.0, rel=1e-15))

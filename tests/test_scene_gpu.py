@@ -5,8 +5,9 @@
   and to the reference built without FMA contraction where oracle/_ref exists.
 * The GPU occupancy pipeline (ground truth -> back-projection -> device octree
   build) gives the same octree as the host pipeline.
-* psnr / depth_errors match the reference formulas (src/metrics.cpp) in fp64
-  to 1e-12 relative.
+* psnr / depth_errors / ssim match the reference formulas (src/metrics.cpp)
+  in fp64 to 1e-12 relative (ssim also against the reference itself where
+  oracle/_ref exists).
 """
 import numpy as np
 import pytest
@@ -86,3 +87,21 @@ def test_metrics(ctx):
     z = d(np.zeros(5000, np.float32))
     torch.cuda.synchronize()
     assert P.depth_errors_device(ctx, a.data_ptr(), b.data_ptr(), z.data_ptr(), 5000) == (0.0, 0.0, True)
+
+
+@pytest.mark.parametrize("w,h,c", [(96, 64, 3), (11, 11, 1), (1600, 40, 3)])
+def test_ssim_device(ctx, w, h, c):
+    from oracle import Reference, reference_available, ssim
+
+    rng = np.random.default_rng(w + h + c)
+    gt = rng.random(w * h * c).astype(np.float32)
+    pred = np.clip(gt + rng.normal(0, 0.03, gt.shape), 0, 1).astype(np.float32)
+    tp, tg = torch.from_numpy(pred).cuda(), torch.from_numpy(gt).cuda()
+    torch.cuda.synchronize()
+    got = P.ssim_device(ctx, tp.data_ptr(), tg.data_ptr(), w, h, c)
+    assert got == pytest.approx(ssim(pred, gt, w, h, c), rel=1e-12)
+    if reference_available():
+        assert got == pytest.approx(Reference().metrics(pred, gt, w, h, c)[1], rel=1e-12)
+    assert P.ssim_device(ctx, tg.data_ptr(), tg.data_ptr(), w, h, c) == pytest.approx(1.0, rel=1e-14)
+    with pytest.raises(ValueError, match="SSIM window"):
+        P.ssim_device(ctx, tp.data_ptr(), tg.data_ptr(), 10, h, c)
