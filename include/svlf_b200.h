@@ -59,7 +59,9 @@ typedef enum svlf_precision {
     SVLF_PRECISION_FP32 = 0,
     SVLF_PRECISION_BF16 = 1,
     SVLF_PRECISION_FP16 = 2,
-    SVLF_PRECISION_TF32 = 3 /* train step only: dense layers on tensor cores with TF32 operands */
+    SVLF_PRECISION_TF32 = 3,  /* train step only: weight-gradient GEMMs on tensor cores with TF32 operands */
+    SVLF_PRECISION_TF32X3 = 4 /* train step only: every dense-layer GEMM on tensor cores as three TF32
+                                 products of split (hi, lo) operands: fp32-level accuracy */
 } svlf_precision;
 
 /* reference LossMode (src/train.cpp:37): stage 1 = SURFACE, stages 2-3 = VOLUMETRIC */
@@ -129,9 +131,11 @@ svlf_status svlf_ctx_synchronize(svlf_ctx* ctx);
 svlf_status svlf_ctx_set_stream(svlf_ctx* ctx, void* cuda_stream);
 svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out);
 /* Arithmetic of the train step's dense layers: SVLF_PRECISION_FP32 (default:
- * true fp32, gradients within 1e-4 of the reference) or SVLF_PRECISION_TF32
- * (the weight-gradient GEMMs on tensor cores with TF32 operands and fp32
- * accumulation; forward and input gradients stay fp32; gradients within
+ * true fp32 CUDA-core GEMMs, gradients within 1e-4 of the reference),
+ * SVLF_PRECISION_TF32X3 (every GEMM on tensor cores as hi*hi + hi*lo + lo*hi
+ * of TF32 splits x = hi + lo, fp32 accumulation: the same fp32 gates) or
+ * SVLF_PRECISION_TF32 (the weight-gradient GEMMs on tensor cores with plain
+ * TF32 operands; forward and input gradients stay fp32; gradients within
  * 2e-2, the 16-bit tolerance of SURVEY.md §8(c)). */
 svlf_status svlf_ctx_set_train_precision(svlf_ctx* ctx, svlf_precision precision);
 /* Count of this library's kernel launches on the context since creation. */

@@ -309,8 +309,10 @@ class Context:
         return int(load_library().svlf_ctx_kernel_launches(None))
 
     def set_train_precision(self, precision: str):
-        """'fp32' (default, true fp32 dense layers) or 'tf32' (tensor cores, TF32 operands)."""
-        _check(_LIB.svlf_ctx_set_train_precision(self._h, {**_PREC, "tf32": 3}[precision]))
+        """Dense-layer GEMMs of the train step: 'fp32' (default, true fp32 on CUDA cores),
+        'tf32x3' (tensor cores, three TF32 products of split operands: fp32-level accuracy) or
+        'tf32' (weight-gradient GEMMs on tensor cores with plain TF32 operands)."""
+        _check(_LIB.svlf_ctx_set_train_precision(self._h, {**_PREC, "tf32": 3, "tf32x3": 4}[precision]))
 
     def attach_nccl(self, unique_id: bytes, rank: int, world: int):
         """Data-parallel training: all-reduce loss, statistics and gradients over NCCL."""

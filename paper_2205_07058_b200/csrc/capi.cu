@@ -91,7 +91,8 @@ struct svlf_ctx {
     long long last_overflow_rays = 0;  // rays that reached the per-ray fallback walker
     long long last_dense_rays = 0;     // rays re-run by the dense 8-ray pass
     ncclComm_t nccl = nullptr;          // data-parallel communicator (optional)
-    bool train_tf32 = false;            // train-step dense layers on tensor cores
+    bool train_tf32 = false;            // train-step weight-gradient GEMMs on tensor cores (TF32)
+    bool train_tf32x3 = false;          // every train-step GEMM as split 3xTF32 on tensor cores
     int rank = 0, world = 1;
     TrainScratch train;
     int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
@@ -804,10 +805,12 @@ svlf_status svlf_ctx_set_stream(svlf_ctx* ctx, void* stream) {
 svlf_status svlf_ctx_set_train_precision(svlf_ctx* ctx, svlf_precision precision) {
     return guard([&] {
         require(ctx != nullptr, "null argument");
-        if (precision != SVLF_PRECISION_FP32 && precision != SVLF_PRECISION_TF32)
-            fail(SVLF_ERR_INVALID_ARGUMENT, "train precision must be fp32 or tf32");
+        if (precision != SVLF_PRECISION_FP32 && precision != SVLF_PRECISION_TF32 &&
+            precision != SVLF_PRECISION_TF32X3)
+            fail(SVLF_ERR_INVALID_ARGUMENT, "train precision must be fp32, tf32x3 or tf32");
         std::lock_guard<std::mutex> lk(ctx->mu);
         ctx->train_tf32 = precision == SVLF_PRECISION_TF32;
+        ctx->train_tf32x3 = precision == SVLF_PRECISION_TF32X3;
     });
 }
 
@@ -1241,7 +1244,7 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
     TrainBatchDev b{d_rays, d_cgt, d_depth, d_alpha, nn, ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(),
                     ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total};
     TrainOptions opt{mode == SVLF_LOSS_SURFACE, color_frozen != 0, adam, *lw, lr, ctx->nccl, ctx->world,
-                     ctx->train_tf32};
+                     ctx->train_tf32, ctx->train_tf32x3};
     ensure_pack_f32(m, s);
     TrainModelRefs mr{m->view(), m->params.as<float>(), m->grads.as<float>(), m->adam_m.as<float>(),
                       m->adam_v.as<float>(), m->n_ft, m->n_fc, m->steps, pack_f32_view(m->pack_f32.as<float>())};

@@ -36,6 +36,7 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
+#include "gemm_x3.cuh"
 #include "mlp_simt.cuh"
 #include "train.cuh"
 
@@ -823,29 +824,48 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     const CublasApi& B = cublas_api();
     cublasHandle_t hb = static_cast<cublasHandle_t>(S.blas);
     cublas_check(B.SetStream(hb, s), "cublasSetStream");
-    // true fp32 (no TF32) for the forward and input-gradient GEMMs; the weight-
-    // gradient GEMMs (reductions over all hits, the bulk of the GEMM time) run
-    // on tensor cores with TF32 operands when the context asks for it
+    // fp32 mode: true fp32 (no TF32) cuBLAS GEMMs on the CUDA cores. tf32 mode:
+    // the weight-gradient GEMMs (reductions over all hits) on tensor cores with
+    // TF32 operands. tf32x3 mode: every GEMM on the tensor cores as three
+    // products of split TF32 operands (gemm_x3.cu), fp32-level accuracy.
+    const bool x3 = o.tf32x3;
     cublas_check(B.SetMathMode(hb, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");
     const float one = 1.f, zero = 0.f;
     const int Ni = int(N), Li = int(Np);
+    uint8_t* wimg = x3 ? S.wimg.ensure<uint8_t>(gemm_x3_image_bytes(kInT)) : nullptr;
     // Y(O x N) = W X: rows [xrow, xrow+K) -> [yrow, yrow+O) of acts
     auto layer_fwd = [&](const float* W, int O, int K, int xrow, int yrow, const float* bias) {
+        if (x3) {
+            gemm_x3_fwd(acts + size_t(xrow) * Np, W, bias, acts + size_t(yrow) * Np, O, K, N, Np, wimg, s);
+            return;
+        }
         cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Ni, O, K, &one, acts + size_t(xrow) * Np, Li, W, K, &zero,
                              acts + size_t(yrow) * Np, Li),
                      "sgemm fwd");
         k_bias_relu<<<dim3(unsigned(std::min<size_t>((N + 255) / 256, 1184)), unsigned(O)), 256, 0, s>>>(
             acts + size_t(yrow) * Np, bias, N, Np);
     };
-    // dX rows [k0, K) (x N) = W^T D, D = delta rows [drow, drow+O)
-    auto layer_bwd = [&](const float* W, int O, int K, int k0, int drow, float* dst) {
+    // dX rows [k0, K) (x N) = W^T D, D = delta rows [drow, drow+O); with mask_row >= 0 the
+    // result is the next delta block: zeroed where the layer's activation (acts row mask_row..) <= 0
+    const unsigned mask_blocks = unsigned(std::min<size_t>((size_t(kHid) * Np + 255) / 256, 4736));
+    auto layer_bwd = [&](const float* W, int O, int K, int k0, int drow, float* dst, int mask_row) {
+        const float* mask = mask_row >= 0 ? acts + size_t(mask_row) * Np : nullptr;
+        if (x3) {
+            gemm_x3_bwd(deltas + size_t(drow) * Np, W, O, K, k0, dst, mask, N, Np, wimg, s);
+            return;
+        }
         cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, Ni, K - k0, O, &one, deltas + size_t(drow) * Np, Li, W + k0,
                              K, &zero, dst, Li),
                      "sgemm bwd");
+        if (mask) k_relu_mask<<<mask_blocks, 256, 0, s>>>(dst, mask, size_t(K - k0) * Np);
     };
     // dW(O x K) = D X^T, db = D 1
     float* ones = S.ones.ensure<float>(size_t(N) + 1);
     auto layer_dw = [&](int drow, int O, int xrow, int K, float* dW, float* db) {
+        if (x3) {
+            gemm_x3_dw(deltas + size_t(drow) * Np, acts + size_t(xrow) * Np, O, K, dW, db, N, Np, s);
+            return;
+        }
         cublas_check(B.Sgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, K, O, Ni, &one, acts + size_t(xrow) * Np, Li,
                              deltas + size_t(drow) * Np, Li, &zero, dW, K),
                      "sgemm dW");
@@ -889,21 +909,18 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     float* g_mt = g_fc + M.n_fc;
     float* g_mc = g_mt + SVLF_DEC_T_SIZE;
     if (N) {
-        const unsigned mask_blocks = unsigned(std::min<size_t>((size_t(kHid) * Np + 255) / 256, 4736));
         // f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
         k_bwd_head_c<<<hit_blocks, 128, 0, s>>>(M.view, H);
-        layer_bwd(M.view.mc + D::C_W2, kHid, kHid, 0, D_C2, deltas + size_t(D_C1) * Np);
-        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C1) * Np, acts + size_t(A_H2) * Np, size_t(kHid) * Np);
-        layer_bwd(M.view.mc + D::C_W1, kHid, kHid, 0, D_C1, deltas + size_t(D_C0) * Np);
-        k_relu_mask<<<mask_blocks, 256, 0, s>>>(deltas + size_t(D_C0) * Np, acts + size_t(A_H1) * Np, size_t(kHid) * Np);
-        layer_bwd(M.view.mc + D::C_W0, kHid, kInC, 6, D_C0, dxs + 6 * size_t(Np));
+        layer_bwd(M.view.mc + D::C_W2, kHid, kHid, 0, D_C2, deltas + size_t(D_C1) * Np, A_H2);
+        layer_bwd(M.view.mc + D::C_W1, kHid, kHid, 0, D_C1, deltas + size_t(D_C0) * Np, A_H1);
+        layer_bwd(M.view.mc + D::C_W0, kHid, kInC, 6, D_C0, dxs + 6 * size_t(Np), -1);
         // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
         const unsigned sc_blocks = unsigned((size_t(N) + 32 * kScWarps - 1) / (32 * kScWarps));
         k_bwd_feat_c<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
-        layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(Np));
+        layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(Np), -1);
         k_bwd_feat_t<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
         // weight gradients (sums over hits)
-        if (o.tf32) cublas_check(B.SetMathMode(hb, CUBLAS_TF32_TENSOR_OP_MATH), "cublasSetMathMode");
+        if (o.tf32 && !x3) cublas_check(B.SetMathMode(hb, CUBLAS_TF32_TENSOR_OP_MATH), "cublasSetMathMode");
         layer_dw(D_T0, kHid, A_XT, kInT, g_mt + D::T_W0, g_mt + D::T_B0);
         layer_dw(D_T1, 2, A_HT, kHid, g_mt + D::T_W1, g_mt + D::T_B1);
         if (!o.color_frozen) {

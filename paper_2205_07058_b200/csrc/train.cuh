@@ -29,7 +29,8 @@ struct TrainOptions {
     float lr;
     void* nccl_comm = nullptr;  // ncclComm_t: data-parallel gradient exchange when set
     int world = 1;
-    bool tf32 = false;          // dense layers on tensor cores (TF32 operands)
+    bool tf32 = false;          // weight-gradient GEMMs on tensor cores (TF32 operands)
+    bool tf32x3 = false;        // every GEMM as hi*hi + hi*lo + lo*hi of TF32 splits (tensor cores)
 };
 
 struct TrainModelRefs {
@@ -59,6 +60,7 @@ struct TrainScratch {
     DevBuf scan_tmp, counters, loss_out;
     DevBuf touched, rows, n_rows, packed, red;  // sparse feature-gradient exchange
     DevBuf dxs, ones;                           // layer-0 input gradients, ones vector (bias sums)
+    DevBuf wimg;                                // 3xTF32 weight image (gemm_x3.cu)
     void* blas = nullptr;                       // cublasHandle_t (fp32 dense-layer GEMMs)
     int* h_pinned = nullptr;
     cudaEvent_t ev[8] = {};

@@ -6,6 +6,8 @@ import paper_2205_07058_b200 as P
 import paper_2205_07058_b200.synthetic as S
 sc, cam, pts, res, dil, rays, cgt, depth, alpha = S.c3_workload()
 ctx = P.Context(0)
+if len(sys.argv) > 3:
+    ctx.set_train_precision(sys.argv[3])
 tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
 model = P.Model(tree, seed=0, ctx=ctx)
 n = rays.shape[0]

@@ -55,9 +55,23 @@ MODES = [("surface", False, (1.0, 0.01, 0.01, 0.1)),
          ("volumetric", True, (1.0, 0.01, 0.01, 0.1))]
 
 
+@pytest.fixture(scope="module")
+def ctx_x3():
+    c = P.Context(0)
+    c.set_train_precision("tf32x3")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("mode,frozen,lw", MODES)
-def test_loss_and_gradients_match_oracle(batch, ctx, oracle, mode, frozen, lw):
+def test_loss_and_gradients_match_oracle(batch, ctx, ctx_x3, oracle, mode, frozen, lw, precision):
+    """fp32 gates (loss 1e-6 relative, gradients 1e-4 rel-L2 per tensor) for the pedantic fp32 GEMMs and for
+    the 3xTF32 split-operand tensor-core GEMMs."""
     tree, otree, rays, cgt, depth, alpha = batch
+    if precision == "tf32x3":
+        ctx = ctx_x3
+        tree = P.SparseOctree.from_leaves(tree.leaf_codes, tree.config, ctx)
     model = P.Model(tree, seed=0, ctx=ctx)
     om = oracle.init_model(otree, 0)
     st = P.LossStats()
@@ -65,9 +79,11 @@ def test_loss_and_gradients_match_oracle(batch, ctx, oracle, mode, frozen, lw):
                         weights=P.LossWeights(*lw), stats=st)
     oloss, og, ost = oracle.loss(otree, om, rays, cgt, depth, alpha, 0 if mode == "surface" else 1, lw=lw,
                                  frozen=frozen)
+    g = model.get_grads()
+    print(precision, mode, frozen, "loss rel", abs(loss - oloss) / abs(oloss),
+          [_rel_l2(a, b) for a, b in zip(g, (og.ft, og.fc, og.mt, og.mc))])
     assert abs(loss - oloss) <= LOSS_REL * abs(oloss)
     assert [st.rays, st.skipped_rays, st.eta_skipped] == list(ost)
-    g = model.get_grads()
     for name, a, b in zip(("feat_t", "feat_c", "dec_t", "dec_c"), g, (og.ft, og.fc, og.mt, og.mc)):
         if frozen and name in ("feat_c", "dec_c"):
             assert not np.any(a), name  # colour frozen: exactly zero
