@@ -32,7 +32,7 @@ constexpr uint32_t kABytes = kRowsA * kChunk * 4;      // 16 KB per hi / lo
 constexpr uint32_t kBBytes = kMaxN * kChunk * 4;       // 18 KB per hi / lo
 constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;
 constexpr uint32_t kStages = 3;
-constexpr uint32_t kSmemBytes = kStages * kStageBytes + 64;
+constexpr uint32_t kSmemBytes = kStages * kStageBytes + 128;
 
 // K-major, no swizzle, 32-bit elements: core matrix = 8 rows x 16 B (4 elements);
 // LBO = 128 B (K-adjacent core matrices), SBO = 1024 B (8-row groups).
@@ -107,14 +107,15 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
 }
 
+// barriers: [0, kStages) stage reuse, kStages / kStages + 1 accumulator 0 / 1 done
 __device__ __forceinline__ uint32_t kernel_init(uint8_t* sm, uint64_t*& bars) {
     bars = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
-    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + kStages + 1);
+    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + kStages + 2);
     if (threadIdx.x == 0) {
-        for (uint32_t i = 0; i <= kStages; ++i) mbar_init(&bars[i], 1);
+        for (uint32_t i = 0; i < kStages + 2; ++i) mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if ((threadIdx.x >> 5) == 0) tmem_alloc(holder, 256);
+    if ((threadIdx.x >> 5) == 0) tmem_alloc(holder, 512);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
@@ -126,7 +127,7 @@ __device__ __forceinline__ void kernel_fini(uint32_t tmem) {
     __syncthreads();
     if ((threadIdx.x >> 5) == 0) {
         fence_after_sync();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -143,9 +144,9 @@ struct StageSync {
         }
         used |= 1u << s;
     }
-    __device__ __forceinline__ void wait_final() {
-        mbar_wait(&bars[kStages], (phase >> kStages) & 1u);
-        phase ^= 1u << kStages;
+    __device__ __forceinline__ void wait_final(uint32_t b = 0) {  // accumulator b's MMAs done
+        mbar_wait(&bars[kStages + b], (phase >> (kStages + b)) & 1u);
+        phase ^= 1u << (kStages + b);
         fence_after_sync();
     }
 };
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kQ = kChunk / 4 / (kThreads / 128);  // K quads per thread per chunk
     const uint32_t m = tid & 127, qb = tid >> 7;              // hit row m, quads qb, qb + kThreads/128, ...
     const uint32_t bwords = (N * kChunk * 4) / 16;            // 16 B words of one hi (or lo) B image chunk
-    float4 areg[kQ];
-    auto fetch_a = [&](uint32_t g) {
+    float4 areg[2][kQ];  // A operands of chunks g and g + 1 (prefetch distance 2)
+    auto fetch_a = [&](uint32_t g, float4* dst) {
         const uint32_t tile = blockIdx.x + (g / nch) * gridDim.x, c = g % nch, hit = tile * 128 + m;
 #pragma unroll
         for (uint32_t i = 0; i < kQ; ++i) {
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (k + 2 < kred) v.z = p[2 * size_t(ld)];
                 if (k + 3 < kred) v.w = p[3 * size_t(ld)];
             }
-            areg[i] = v;
+            dst[i] = v;
         }
     };
     auto fetch_b = [&](uint32_t g, uint32_t s) {  // weight image chunk -> stage s (async)
@@ -197,26 +198,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         cp_async_commit();
     };
-    if (total) {
-        ss.acquire(0);
-        fetch_b(0, 0);
-        fetch_a(0);
-    }
-    for (uint32_t g = 0; g < total; ++g) {
-        const uint32_t s = g % kStages, c = g % nch, sn = (g + 1) % kStages;
+    // tile t accumulates in TMEM columns 256 (t & 1); its epilogue runs after
+    // the next tile's first chunk has been issued, so the tensor pipe keeps
+    // working while the previous tile is written out
+    auto epilogue = [&](uint32_t t_local) {
+        const uint32_t b = t_local & 1u;
+        ss.wait_final(b);
+        const uint32_t tile = blockIdx.x + t_local * gridDim.x;
+        const uint32_t acc = tmem + 256 * b;
+        const uint32_t lane_off = (32u * (warp & 3u)) << 16, r = 32 * (warp & 3u) + (tid & 31);
+        const uint32_t groups = kThreads / 128, h = warp >> 2;
+        const uint32_t per = ((N + groups - 1) / groups + 31) & ~31u;
+        const uint32_t hit_r = tile * 128 + r;
+        for (uint32_t c0 = h * per; c0 < min(N, (h + 1) * per); c0 += 32) {
+            float v[32];
+            tmem_ld32(acc + lane_off + c0, v);
+            tmem_wait_ld();
+            if (hit_r < n) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const uint32_t j = c0 + i;
+                    if (j < n_out) {
+                        float y = v[i];
+                        if constexpr (!kBwd) {
+                            y = fmaxf(y + __ldg(bias + j), 0.f);
+                        } else {
+                            if (mask && !(mask[size_t(j) * ld + hit_r] > 0.f)) y = 0.f;
+                        }
+                        out[size_t(j) * ld + hit_r] = y;
+                    }
+                }
+            }
+        }
+        fence_before_sync();  // ordered before the next chunk barrier (accumulator reuse two tiles later)
+    };
+    auto body = [&](uint32_t g, float4* cur) {
+        const uint32_t s = g % kStages, c = g % nch, sn = (g + 1) % kStages, t_local = g / nch;
         const uint32_t sa = sbase + s * kStageBytes, sb = sa + 2 * kABytes;
 #pragma unroll
         for (uint32_t i = 0; i < kQ; ++i) {
             uint4 hi, lo;
-            split4(areg[i], hi, lo);
+            split4(cur[i], hi, lo);
             const uint32_t q = qb + i * (kThreads / 128);
             st_shared_v4(sa + off32(m, 4 * q), hi.x, hi.y, hi.z, hi.w);
             st_shared_v4(sa + kABytes + off32(m, 4 * q), lo.x, lo.y, lo.z, lo.w);
         }
-        if (g + 1 < total) {  // next chunk: its stage is free once chunk g-1's MMAs completed
+        if (g + 2 < total) fetch_a(g + 2, cur);  // this register set is free again
+        if (g + 1 < total) {  // next chunk's weights: its stage is free once chunk g+1-kStages completed
             ss.acquire(sn);
             fetch_b(g + 1, sn);
-            fetch_a(g + 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -226,42 +256,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         if (tid == 0) {
             fence_after_sync();
-            issue_chunk(tmem, sa, sb, idesc, c == 0);
+            issue_chunk(tmem + 256 * (t_local & 1u), sa, sb, idesc, c == 0);
             mma_commit(&bars[s]);
-            if (c + 1 == nch) mma_commit(&bars[kStages]);
+            if (c + 1 == nch) mma_commit(&bars[kStages + (t_local & 1u)]);
         }
-        if (c + 1 == nch) {  // tile done: epilogue (next chunk's loads are already in flight)
-            ss.wait_final();
-            const uint32_t tile = blockIdx.x + (g / nch) * gridDim.x;
-            const uint32_t lane_off = (32u * (warp & 3u)) << 16, r = 32 * (warp & 3u) + (tid & 31);
-            const uint32_t groups = kThreads / 128, h = warp >> 2;
-            const uint32_t per = ((N + groups - 1) / groups + 31) & ~31u;
-            const uint32_t hit_r = tile * 128 + r;
-            for (uint32_t c0 = h * per; c0 < min(N, (h + 1) * per); c0 += 32) {
-                float v[32];
-                tmem_ld32(tmem + lane_off + c0, v);
-                tmem_wait_ld();
-                if (hit_r < n) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const uint32_t j = c0 + i;
-                        if (j < n_out) {
-                            float y = v[i];
-                            if constexpr (!kBwd) {
-                                y = fmaxf(y + __ldg(bias + j), 0.f);
-                            } else {
-                                if (mask && !(mask[size_t(j) * ld + hit_r] > 0.f)) y = 0.f;
-                            }
-                            out[size_t(j) * ld + hit_r] = y;
-                        }
-                    }
-                }
-            }
-            fence_before_sync();
-            __syncthreads();  // accumulator read before the next tile's first MMA
-            fence_after_sync();
-        }
+        if (c == 0 && t_local > 0) epilogue(t_local - 1);
+    };
+    if (total) {
+        ss.acquire(0);
+        fetch_b(0, 0);
+        fetch_a(0, areg[0]);
+        if (total > 1) fetch_a(1, areg[1]);
     }
+    for (uint32_t g = 0; g < total; g += 2) {
+        body(g, areg[0]);
+        if (g + 1 < total) body(g + 1, areg[1]);
+    }
+    if (my_tiles) epilogue(my_tiles - 1);
     kernel_fini(tmem);
 }
 
@@ -284,14 +295,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t r_lo = lane & 7, q_lo = lane >> 3;
     const uint32_t units = (kRowsA / 8) * 2 + (N / 8) * 2;
     constexpr uint32_t kU = ((kRowsA / 8) * 2 + (kMaxN / 8) * 2 + kThreads / 32 - 1) / (kThreads / 32);
-    float4 reg[kU];
+    float4 reg[2][kU];  // chunks c and c + 1 (prefetch distance 2)
     auto unit_of = [&](uint32_t u, uint32_t& r, uint32_t& q, bool& isA) {
         isA = u < (kRowsA / 8) * 2;
         const uint32_t t = isA ? u : u - (kRowsA / 8) * 2;
         r = 8 * (t >> 1) + r_lo;
         q = 4 * (t & 1) + q_lo;
     };
-    auto fetch = [&](uint32_t c) {
+    auto fetch = [&](uint32_t c, float4* dst) {
         const uint32_t hb = h0 + c * kChunk;
 #pragma unroll
         for (uint32_t i = 0; i < kU; ++i) {
@@ -320,11 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     v.w = hit + 3 < h1 ? 1.f : 0.f;
                 }
             }
-            reg[i] = v;
+            dst[i] = v;
         }
     };
-    if (nch) fetch(0);
-    for (uint32_t c = 0; c < nch; ++c) {
+    auto body = [&](uint32_t c, float4* cur) {
         const uint32_t s = c % kStages;
         ss.acquire(s);
         const uint32_t sa = sbase + s * kStageBytes, sb = sa + 2 * kABytes;
@@ -336,13 +346,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bool isA;
                 unit_of(u, r, q, isA);
                 uint4 hi, lo;
-                split4(reg[i], hi, lo);
+                split4(cur[i], hi, lo);
                 const uint32_t base = isA ? sa : sb, lo_off = isA ? kABytes : kBBytes;
                 st_shared_v4(base + off32(r, 4 * q), hi.x, hi.y, hi.z, hi.w);
                 st_shared_v4(base + lo_off + off32(r, 4 * q), lo.x, lo.y, lo.z, lo.w);
             }
         }
-        if (c + 1 < nch) fetch(c + 1);  // in flight during this chunk's MMAs
+        if (c + 2 < nch) fetch(c + 2, cur);  // in flight during the next chunks' MMAs
         fence_async_smem();
         fence_before_sync();
         __syncthreads();
@@ -352,6 +362,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit(&bars[s]);
             if (c + 1 == nch) mma_commit(&bars[kStages]);
         }
+    };
+    if (nch) fetch(0, reg[0]);
+    if (nch > 1) fetch(1, reg[1]);
+    for (uint32_t c = 0; c < nch; c += 2) {
+        body(c, reg[0]);
+        if (c + 1 < nch) body(c + 1, reg[1]);
     }
     if (nch) {
         ss.wait_final();
