@@ -10,8 +10,9 @@
 //              only when lambda_empty == 0), skipped / eta_skipped counters.
 //   scan/expand  dense list of active hits.
 //   forward    per hit: f_T input column (geometry, trilinear gathers);
-//              dense layers as fp32 GEMMs on feature-major activation
-//              matrices (cuBLAS SGEMM, pedantic fp32) + bias/relu epilogue;
+//              dense layers as GEMMs on feature-major activation matrices
+//              (cuBLAS SGEMM in pedantic fp32, or the 3xTF32 tensor-core
+//              kernels of gemm_x3.cu) + bias/relu epilogue;
 //              per hit: f_T heads, x_s, f_C input column; f_C layers as
 //              GEMMs; per hit: rgb head. Activations kept for backward.
 //   k_loss     per ray: Eq. 4 surface loss or composite + volumetric loss in
