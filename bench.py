@@ -290,6 +290,23 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
            "e2e": {"value": round(world * n / (e2e_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
                    "h2d_bytes_per_step": n * (48 + 12 + 8 + 1), "d2h_bytes_per_step": 8,
                    "api": "paper_2205_07058_b200.train_step (C ABI svlf_train_step, host batch)"}}
+    # rooflines: algorithmic FLOP of the step (332,544 per active hit, stage 3)
+    # against the peak of the unit each mode runs its dense layers on
+    peaks, _ = load_peaks()
+    flop = hits * 332544.0
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * mhz * 1e6 / 1e12  # CUDA-core fp32 FMA, nominal at the max SM clock
+    tf32x3_peak = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]) / 2 / 3  # TF32 = half the bf16 rate, 3 products
+    for key, ms_, peak, bound in (("roofline", step_ms, fp32_peak, "fp32 CUDA cores (nominal peak)"),
+                                  ("tf32x3", x3_step_ms, tf32x3_peak,
+                                   "tensor, 3xTF32 (measured bf16 peak / 2 / 3)")):
+        ach = flop / (ms_ * 1e-3) / 1e12
+        r = {"bound": bound, "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
+             "frac": round(ach / peak, 4), "algorithmic": f"332544 FLOP/hit x {hits} active hits (whole step)"}
+        if key == "roofline":
+            out["roofline"] = r
+        else:
+            out["tf32x3"]["roofline"] = r
     if cpu and world == 1:
         try:
             sys.path.insert(0, os.path.join(ROOT, "oracle"))
