@@ -24,6 +24,11 @@ enum class Precision { FP32 = 0, BF16 = 1, FP16 = 2 };
 void set_device(int device);  // before first use; default $SVLF_DEVICE or 0
 void set_render_precision(Precision p);
 Precision render_precision();
+// Dense-layer GEMMs of the train step: FP32 (default, CUDA-core SGEMM),
+// TF32X3 (tensor cores, three TF32 products of split operands; the same fp32
+// parity gates) or TF32 (weight gradients in plain TF32; 16-bit gates).
+enum class TrainPrecision { FP32 = 0, TF32X3 = 4, TF32 = 3 };
+void set_train_precision(TrainPrecision p);
 svlf_ctx* session_context();  // creates the session on first call
 
 class DeviceModel {

@@ -77,6 +77,12 @@ svlf_ctx* session_context() {
     return s.ctx;
 }
 
+void set_train_precision(TrainPrecision p) {
+    auto& s = detail::session();
+    std::lock_guard<std::recursive_mutex> lk(s.mu);
+    detail::check(svlf_ctx_set_train_precision(session_context(), static_cast<svlf_precision>(int(p))));
+}
+
 }  // namespace b200
 
 // ---- decoder specs ---------------------------------------------------------

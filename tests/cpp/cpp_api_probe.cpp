@@ -246,6 +246,18 @@ int run_train() {
     dm.sync_to(synced);
     dump("params2_device.f32", flat(synced));
 
+    // the same two steps with the 3xTF32 tensor-core GEMMs (same fp32 gates)
+    b200::set_train_precision(b200::TrainPrecision::TF32X3);
+    {
+        SvlfModel m3 = init_model(tree, 0);
+        ModelAdam a3 = ModelAdam::like(m3);
+        std::vector<double> l3;
+        for (int k = 0; k < 2; ++k) l3.push_back(train_step(m3, a3, batch, LossMode::Volumetric, false, 1e-3f));
+        dump("losses_x3.f64", l3);
+        dump("params2_x3.f32", flat(m3));
+    }
+    b200::set_train_precision(b200::TrainPrecision::FP32);
+
     // checkpoint of the trained state reloads into an identical render
     save_checkpoint(g_out + "/trained.ckpt", model, adam);
     SvlfModel back;
