@@ -215,16 +215,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld32(acc + lane_off + c0, v);
             tmem_wait_ld();
             if (hit_r < n) {
+                if constexpr (kBwd) {
+                    if (mask) {  // all 32 mask loads in flight before the stores
+                        float mk[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            mk[i] = c0 + i < n_out ? __ldg(mask + size_t(c0 + i) * ld + hit_r) : 0.f;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (!(mk[i] > 0.f)) v[i] = 0.f;
+                    }
+                }
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const uint32_t j = c0 + i;
                     if (j < n_out) {
                         float y = v[i];
-                        if constexpr (!kBwd) {
-                            y = fmaxf(y + __ldg(bias + j), 0.f);
-                        } else {
-                            if (mask && !(mask[size_t(j) * ld + hit_r] > 0.f)) y = 0.f;
-                        }
+                        if constexpr (!kBwd) y = fmaxf(y + __ldg(bias + j), 0.f);
                         out[size_t(j) * ld + hit_r] = y;
                     }
                 }
