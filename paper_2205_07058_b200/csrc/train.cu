@@ -319,9 +319,9 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel
     if (valid) {
         const float* h = X + A_HT * L;
         float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
-#pragma unroll 4
+#pragma unroll 16
         for (int k = 0; k < kHid; ++k) {
-            const float v = h[k * L];
+            const float v = __ldg(h + size_t(k) * L);
             y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
             y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
         }
@@ -379,9 +379,9 @@ __global__ void __launch_bounds__(128) k_fwd_rgb(DevModel M, HitArgs H) {
     }
     const float* h = H.acts + A_H3 * L + j;
     float y[3] = {__ldg(M.mc + D::C_B3), __ldg(M.mc + D::C_B3 + 1), __ldg(M.mc + D::C_B3 + 2)};
-#pragma unroll 4
+#pragma unroll 16
     for (int k = 0; k < kHid; ++k) {
-        const float v = h[k * L];
+        const float v = __ldg(h + size_t(k) * L);
 #pragma unroll
         for (int c = 0; c < 3; ++c) y[c] = fmaf(__ldg(M.mc + D::C_W3 + c * kHid + k), v, y[c]);
     }
@@ -508,15 +508,21 @@ __global__ void __launch_bounds__(128) k_bwd_head_c(DevModel M, HitArgs H) {
 #pragma unroll
     for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * L] = d3[o];
     const float* h3 = H.acts + A_H3 * L + j;
-#pragma unroll 4
-    for (int k = 0; k < kHid; ++k) {
-        float v = 0.f;
-        if (h3[k * L] > 0.f) {
-            v = __ldg(M.mc + D::C_W3 + k) * d3[0];
-            v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
-            v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
+    for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
+        float hv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) hv[i] = __ldg(h3 + size_t(k0 + i) * L);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int k = k0 + i;
+            float v = 0.f;
+            if (hv[i] > 0.f) {
+                v = __ldg(M.mc + D::C_W3 + k) * d3[0];
+                v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
+                v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
+            }
+            Dl[(D_C2 + k) * L] = v;
         }
-        Dl[(D_C2 + k) * L] = v;
     }
 }
 
@@ -629,11 +635,17 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevMo
     Dl[D_T1 * L] = d0;
     Dl[(D_T1 + 1) * L] = d1;
     const float* ht = H.acts + A_HT * L + j;
-#pragma unroll 4
-    for (int k = 0; k < kHid; ++k) {
-        float v = 0.f;
-        if (ht[k * L] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
-        Dl[(D_T0 + k) * L] = v;
+    for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
+        float hv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) hv[i] = __ldg(ht + size_t(k0 + i) * L);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int k = k0 + i;
+            float v = 0.f;
+            if (hv[i] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
+            Dl[(D_T0 + k) * L] = v;
+        }
     }
 }
 
