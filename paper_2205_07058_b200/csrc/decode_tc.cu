@@ -97,14 +97,20 @@ static_assert(T_SM_TOTAL <= 232448 && C_SM_TOTAL <= 232448, "shared memory budge
 // kProducers warps gather input tiles (K = 48) into a kRing-entry shared
 // ring; two 4-warp consumer chains run the MMAs, each with a 128-column
 // accumulator and a 64-column 16-bit A operand in TMEM.
-constexpr uint32_t kProducers = 8;
+#ifndef SVLF_DEC_C_PRODUCERS
+#define SVLF_DEC_C_PRODUCERS 8
+#endif
+constexpr uint32_t kProducers = SVLF_DEC_C_PRODUCERS;
 #ifndef SVLF_DEC_C_SMCHAINS
 #define SVLF_DEC_C_SMCHAINS 1
 #endif
 constexpr uint32_t kChainsTm = 2;                      // chains with A in TMEM (192 columns each)
 constexpr uint32_t kChainsSm = SVLF_DEC_C_SMCHAINS;    // chains with A in shared memory (128 columns)
 constexpr uint32_t kChains = kChainsTm + kChainsSm;
-constexpr uint32_t kRing = kChainsSm ? 7 : 10;
+#ifndef SVLF_DEC_C_RING
+#define SVLF_DEC_C_RING 0
+#endif
+constexpr uint32_t kRing = SVLF_DEC_C_RING ? SVLF_DEC_C_RING : (kChainsSm ? 7 : 10);
 constexpr uint32_t kCtThreads = (kProducers + 4 * kChains) * 32;
 constexpr uint32_t CT_A_BYTES = (KC / 8) * kALbo;  // 12384
 constexpr uint32_t CT_SMA0 = C_SM_A0 + kRing * CT_A_BYTES;
