@@ -24,6 +24,9 @@ namespace {
 
 using namespace tc;
 
+#ifndef SVLF_GEMM_SWAP
+#define SVLF_GEMM_SWAP 1  // Fwd / Bwd with M = output features, N = up to 256 hits (k_gemm_feat)
+#endif
 constexpr uint32_t kChunk = 32;                        // K elements per pipeline stage
 constexpr uint32_t kThreads = 512;
 constexpr uint32_t kRowsA = 128;                       // M
@@ -283,6 +286,188 @@ __global__ void __launch_bounds__(kThreads, 1)
     kernel_fini(tmem);
 }
 
+// ---- Fwd / Bwd with the roles swapped: M = 128 output features (weights as
+// the A operand), N = nt hits (<= 256) per tile. Per K-step an MMA reads the
+// weight tile once for nt hits instead of once per 128 hits.
+constexpr uint32_t kFA = 128 * kChunk * 4;       // 16 KB: A (weights) hi or lo
+constexpr uint32_t kFB = 256 * kChunk * 4;       // 32 KB: B (hits) hi or lo
+constexpr uint32_t kFStage = 2 * kFA + 2 * kFB;  // 96 KB
+constexpr uint32_t kFStages = 2;
+constexpr uint32_t kFSmem = kFStages * kFStage + 128;
+
+template <bool kBwd>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_feat(const float* __restrict__ in, const uint8_t* __restrict__ wimg, float* __restrict__ out,
+                const float* __restrict__ bias, const float* __restrict__ mask, uint32_t n, uint32_t ld,
+                uint32_t kred, uint32_t nt, uint32_t n_out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kFStages * kFStage);  // [0,1] stages, [2,3] accumulators
+    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 4);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (uint32_t i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(holder, 512);
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *holder;
+    const uint32_t sbase = smem_u32(sm);
+    const uint32_t idesc = idesc_tf32(128, nt);
+    const uint32_t nch = (kred + kChunk - 1) / kChunk;
+    const uint32_t ntiles = (n + nt - 1) / nt;
+    const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint32_t total = my_tiles * nch;
+    uint32_t phase = 0, used = 0;
+    auto acquire = [&](uint32_t st) {
+        if ((used >> st) & 1u) {
+            mbar_wait(&bars[st], (phase >> st) & 1u);
+            phase ^= 1u << st;
+        }
+        used |= 1u << st;
+    };
+    // B staging: hit row hn of the tile, K quads qb, qb + 2, qb + 4, qb + 6
+    const uint32_t hn = tid & 255, qb = tid >> 8;
+    constexpr uint32_t kQ = kChunk / 4 / 2;
+    float4 breg[2][kQ];
+    auto fetch_b = [&](uint32_t g, float4* dst) {
+        const uint32_t tile = blockIdx.x + (g / nch) * gridDim.x, c = g % nch, hit = tile * nt + hn;
+        const bool ok = hn < nt && hit < n;
+#pragma unroll
+        for (uint32_t i = 0; i < kQ; ++i) {
+            const uint32_t k = c * kChunk + 4 * (qb + 2 * i);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) {
+                const float* p = in + size_t(k) * ld + hit;
+                if (k < kred) v.x = __ldg(p);
+                if (k + 1 < kred) v.y = __ldg(p + ld);
+                if (k + 2 < kred) v.z = __ldg(p + 2 * size_t(ld));
+                if (k + 3 < kred) v.w = __ldg(p + 3 * size_t(ld));
+            }
+            dst[i] = v;
+        }
+    };
+    auto fetch_a = [&](uint32_t g, uint32_t st) {  // weight image chunk (first 128 rows) -> stage st
+        const uint32_t c = g % nch;
+        const uint8_t* src = wimg + size_t(c) * 2 * kBBytes;
+        const uint32_t sa = sbase + st * kFStage;
+        for (uint32_t i = tid; i < 2 * (kFA / 16); i += kThreads) {
+            const uint32_t half = i >= kFA / 16, w = i - half * (kFA / 16);
+            cp_async16(sa + half * kFA + 16 * w, src + half * kBBytes + 16 * w);
+        }
+        cp_async_commit();
+    };
+    auto epilogue = [&](uint32_t t_local) {
+        const uint32_t b = t_local & 1u;
+        mbar_wait(&bars[2 + b], (phase >> (2 + b)) & 1u);
+        phase ^= 1u << (2 + b);
+        fence_after_sync();
+        const uint32_t tile = blockIdx.x + t_local * gridDim.x;
+        const uint32_t lane_off = (32u * (warp & 3u)) << 16, j = 32 * (warp & 3u) + lane, cg = warp >> 2;
+        const uint32_t batches = (nt + 31) / 32;
+        const float bj = (!kBwd && j < n_out) ? __ldg(bias + j) : 0.f;
+        for (uint32_t bt = cg; bt < batches; bt += 4) {
+            float v[32];
+            tmem_ld32(tmem + 256 * b + lane_off + 32 * bt, v);
+            tmem_wait_ld();
+            if (j >= n_out) continue;
+            const uint32_t h0 = tile * nt + 32 * bt;
+            const uint32_t cnt = min(min(32u, nt - 32 * bt), n > h0 ? n - h0 : 0u);
+            float* o = out + size_t(j) * ld + h0;
+            if constexpr (kBwd) {
+                if (mask) {
+                    const float* mk = mask + size_t(j) * ld + h0;
+                    float mv[32];
+                    if (cnt == 32) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 q = __ldg(reinterpret_cast<const float4*>(mk) + i);
+                            mv[4 * i] = q.x; mv[4 * i + 1] = q.y; mv[4 * i + 2] = q.z; mv[4 * i + 3] = q.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) mv[i] = uint32_t(i) < cnt ? __ldg(mk + i) : 0.f;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (!(mv[i] > 0.f)) v[i] = 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
+            }
+            if (cnt == 32) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    reinterpret_cast<float4*>(o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (uint32_t(i) < cnt) o[i] = v[i];
+            }
+        }
+        fence_before_sync();
+    };
+    auto body = [&](uint32_t g, float4* cur) {
+        const uint32_t st = g % kFStages, c = g % nch, t_local = g / nch;
+        const uint32_t sa = sbase + st * kFStage, sb = sa + 2 * kFA;
+        if (hn < nt) {
+#pragma unroll
+            for (uint32_t i = 0; i < kQ; ++i) {
+                uint4 hi, lo;
+                split4(cur[i], hi, lo);
+                const uint32_t q = qb + 2 * i;
+                st_shared_v4(sb + off32(hn, 4 * q), hi.x, hi.y, hi.z, hi.w);
+                st_shared_v4(sb + kFB + off32(hn, 4 * q), lo.x, lo.y, lo.z, lo.w);
+            }
+        }
+        if (g + 2 < total) fetch_b(g + 2, cur);
+        if (g + 1 < total) {
+            acquire((g + 1) % kFStages);
+            fetch_a(g + 1, (g + 1) % kFStages);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        fence_async_smem();
+        fence_before_sync();
+        __syncthreads();
+        if (tid == 0) {
+            fence_after_sync();
+            const uint32_t d = tmem + 256 * (t_local & 1u);
+#pragma unroll
+            for (uint32_t ks = 0; ks < kChunk / 8; ++ks) {
+                const uint64_t ahi = make_desc(sa + ks * 256, 128, 1024), alo = make_desc(sa + kFA + ks * 256, 128, 1024);
+                const uint64_t bhi = make_desc(sb + ks * 256, 128, 1024), blo = make_desc(sb + kFB + ks * 256, 128, 1024);
+                mma_tf32(d, ahi, blo, idesc, (c == 0 && ks == 0) ? 0u : 1u);
+                mma_tf32(d, alo, bhi, idesc, 1u);
+                mma_tf32(d, ahi, bhi, idesc, 1u);
+            }
+            mma_commit(&bars[st]);
+            if (c + 1 == nch) mma_commit(&bars[2 + (t_local & 1u)]);
+        }
+        if (c == 0 && t_local > 0) epilogue(t_local - 1);
+    };
+    if (total) {
+        acquire(0);
+        fetch_a(0, 0);
+        fetch_b(0, breg[0]);
+        if (total > 1) fetch_b(1, breg[1]);
+    }
+    for (uint32_t g = 0; g < total; g += 2) {
+        body(g, breg[0]);
+        if (g + 1 < total) body(g + 1, breg[1]);
+    }
+    if (my_tiles) epilogue(my_tiles - 1);
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after_sync();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ---- Dw: dW[o][k] += sum over this CTA's hits of D[o][n] X[k][n] -------------
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_dw(const float* __restrict__ dmat, const float* __restrict__ xmat, float* __restrict__ dW,
@@ -411,6 +596,8 @@ void setup() {
         SVLF_CUDA(cudaFuncSetAttribute(k_gemm_hits<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
         SVLF_CUDA(cudaFuncSetAttribute(k_gemm_hits<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
         SVLF_CUDA(cudaFuncSetAttribute(k_gemm_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
+        SVLF_CUDA(cudaFuncSetAttribute(k_gemm_feat<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFSmem)));
+        SVLF_CUDA(cudaFuncSetAttribute(k_gemm_feat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFSmem)));
         g_attr = true;
     }
 }
@@ -421,15 +608,31 @@ uint32_t round16(uint32_t v) { return (v + 15u) & ~15u; }
 
 size_t gemm_x3_image_bytes(uint32_t kred) { return size_t((kred + kChunk - 1) / kChunk) * 2 * kBBytes; }
 
+// hits per tile for the swapped kernels: <= 256, a multiple of 16, sized so
+// the tiles fill whole waves of one CTA per SM
+static uint32_t tile_hits(uint32_t n) {
+    const uint32_t sms = uint32_t(g_sms), waves = std::max<uint32_t>(1, (n + sms * 256 - 1) / (sms * 256));
+    const uint32_t per = (n + sms * waves - 1) / (sms * waves);
+    return std::min<uint32_t>(256, std::max<uint32_t>(16, (per + 15) / 16 * 16));
+}
+
 void gemm_x3_fwd(const float* x, const float* W, const float* bias, float* y, uint32_t O, uint32_t K, uint32_t n,
                  uint32_t ld, uint8_t* img, cudaStream_t s) {
     if (n == 0) return;
     setup();
-    const uint32_t N = round16(O), nch = (K + kChunk - 1) / kChunk;
+    const uint32_t nch = (K + kChunk - 1) / kChunk;
+#if SVLF_GEMM_SWAP
+    k_wimage<<<64, 256, 0, s>>>(W, O, K, 0, false, 128, K, nch, img);
+    const uint32_t nt = tile_hits(n), tiles = (n + nt - 1) / nt;
+    k_gemm_feat<false><<<std::min<uint32_t>(tiles, uint32_t(g_sms)), kThreads, kFSmem, s>>>(x, img, y, bias, nullptr,
+                                                                                              n, ld, K, nt, O);
+#else
+    const uint32_t N = round16(O);
     k_wimage<<<64, 256, 0, s>>>(W, O, K, 0, false, N, K, nch, img);
     const uint32_t tiles = (n + 127) / 128;
     k_gemm_hits<false><<<std::min<uint32_t>(tiles, uint32_t(g_sms)), kThreads, kSmemBytes, s>>>(
         x, img, y, bias, nullptr, n, ld, K, N, O);
+#endif
     note_launch(2);
 }
 
@@ -437,11 +640,19 @@ void gemm_x3_bwd(const float* d, const float* W, uint32_t O, uint32_t K, uint32_
                  uint32_t n, uint32_t ld, uint8_t* img, cudaStream_t s) {
     if (n == 0) return;
     setup();
-    const uint32_t nout = K - k0, N = round16(nout), nch = (O + kChunk - 1) / kChunk;
+    const uint32_t nout = K - k0, nch = (O + kChunk - 1) / kChunk;
+#if SVLF_GEMM_SWAP
+    k_wimage<<<64, 256, 0, s>>>(W, O, K, k0, true, 128, O, nch, img);
+    const uint32_t nt = tile_hits(n), tiles = (n + nt - 1) / nt;
+    k_gemm_feat<true><<<std::min<uint32_t>(tiles, uint32_t(g_sms)), kThreads, kFSmem, s>>>(d, img, dx, nullptr, mask,
+                                                                                             n, ld, O, nt, nout);
+#else
+    const uint32_t N = round16(nout);
     k_wimage<<<64, 256, 0, s>>>(W, O, K, k0, true, N, O, nch, img);
     const uint32_t tiles = (n + 127) / 128;
     k_gemm_hits<true><<<std::min<uint32_t>(tiles, uint32_t(g_sms)), kThreads, kSmemBytes, s>>>(
         d, img, dx, nullptr, mask, n, ld, O, N, nout);
+#endif
     note_launch(2);
 }
 
