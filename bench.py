@@ -121,7 +121,7 @@ def max_over_ranks(x: float, dist, device):
     return float(t.item())
 
 
-def stage_rooflines(stage, hits, n, peaks):
+def stage_rooflines(stage, hits, n, peaks, node_tests=None):
     """Every render stage against its roofline (north star: each stage as a
     fraction of its roofline). Algorithmic bytes per stage:
     traversal 24 B per emitted hit (leaf, t_in, t_out) + 8 B per ray (segment);
@@ -137,6 +137,10 @@ def stage_rooflines(stage, hits, n, peaks):
         out["traversal"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                             "frac": round(gbs / hbm, 5), "ms": round(trav_ms, 4),
                             "note": "fp64 / latency-bound (see profiles/r1_render.md)"}
+        if node_tests:  # secondary figure: ray-box tests, the reference's ray_aabb calls
+            out["traversal"]["node_tests_per_ray"] = round(node_tests / n, 2)
+            out["traversal"]["node_tests_per_s"] = round(node_tests / (trav_ms * 1e-3) / 1e9, 2)
+            out["traversal"]["node_tests_unit"] = "G tests/s"
     if stage["decode_ms"] > 0:
         tf = hits * FLOP_PER_HIT / (stage["decode_ms"] * 1e-3) / 1e12
         out["decode"] = {"bound": "tensor", "achieved": round(tf, 2), "peak": tc, "unit": "TFLOP/s",
@@ -446,6 +450,12 @@ def main():
         torch.cuda.synchronize(device)
         barrier(dist)
         launches = P.Context.kernel_launches() - launches0
+        # ray-box tests of one more frame with the counting traversal variant (outside the timed region)
+        ctx.set_node_test_counting(True)
+        step()
+        stream.synchronize()
+        node_tests = ctx.last_node_tests()
+        ctx.set_node_test_counting(False)
         step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms), dist, device)
     ms_per_step = total_ms / args.steps
@@ -540,7 +550,7 @@ def main():
                      "traffic_source": "profiles/r1_render.json (ncu --set full --clock-control none)",
                      "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)",
                      "algorithmic": f"{FLOP_PER_HIT} FLOP/hit x {int(hits)} hits per launch"},
-        "stage_rooflines": stage_rooflines(stage, hits, n, peaks),
+        "stage_rooflines": stage_rooflines(stage, hits, n, peaks, node_tests),
         "e2e": {"value": round(e2e_value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": camera_bytes,
                 "d2h_bytes_per_step": n * BYTES_PER_RAY_OUT, "ms_per_step": round(e2e_step, 4),
                 "loops_ms_per_frame": [round(x, 4) for x in pipe_ms], "frames_per_loop": k_e2e,

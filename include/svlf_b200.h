@@ -130,6 +130,15 @@ svlf_status svlf_ctx_synchronize(svlf_ctx* ctx);
  * context's own stream. */
 svlf_status svlf_ctx_set_stream(svlf_ctx* ctx, void* cuda_stream);
 svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out);
+/* Diagnostics: with counting enabled, traversals run a variant of the
+ * cooperative passes that counts ray-box tests (root + each occupied child of
+ * every expanded node: the reference's ray_aabb calls in
+ * SparseOctree::traverse, src/octree.cpp:185-235; tiles handed to the next
+ * pass are counted by the pass that completes them; the per-ray fallback
+ * walker is not counted). svlf_ctx_last_node_tests reads the count of the
+ * last traversal (last band of a banded frame; 32-bit; synchronizes). */
+svlf_status svlf_ctx_set_node_test_counting(svlf_ctx* ctx, int enable);
+svlf_status svlf_ctx_last_node_tests(svlf_ctx* ctx, long long* out);
 /* Arithmetic of the train step's dense layers: SVLF_PRECISION_FP32 (default:
  * true fp32 CUDA-core GEMMs, gradients within 1e-4 of the reference),
  * SVLF_PRECISION_TF32X3 (every GEMM on tensor cores as hi*hi + hi*lo + lo*hi

@@ -157,6 +157,12 @@ class Oracle:
         ok = self.lib.or_ray_aabb(_f64(ray6), _f64(lo), _f64(hi), t)
         return (t[0], t[1]) if ok else None
 
+    def node_tests(self, reset=True):
+        """ray_aabb calls of traverse() on this thread since the last reset (src/octree.cpp:185-235)."""
+        self.lib.or_node_tests.restype = C.c_uint64
+        self.lib.or_node_tests.argtypes = [C.c_int]
+        return int(self.lib.or_node_tests(1 if reset else 0))
+
     def traverse(self, tree, rays):
         rays = _f64(rays).reshape(-1, 6)
         n = rays.shape[0]

@@ -463,6 +463,15 @@ static void hv_push(hitvec* h, hit_t x) {
 /* SparseOctree::traverse, src/octree.cpp:192-235: DFS from the root, a
  * child is tested only when its parent box is hit; leaves kept iff
  * t1 - t0 > 1e-12; final sort by (t_in, code). */
+/* ray_aabb calls made by traverse (the reference's per-node box tests), for the
+ * GPU node-test counter's parity test */
+static __thread uint64_t g_node_tests;
+uint64_t or_node_tests(int reset) {
+    const uint64_t v = g_node_tests;
+    if (reset) g_node_tests = 0;
+    return v;
+}
+
 static void traverse(const or_tree* t, const ray_t* ray, hitvec* out) {
     const size_t first = out->n;
     const int L = t->leaf_level;
@@ -485,6 +494,7 @@ static void traverse(const or_tree* t, const ray_t* ray, hitvec* out) {
         aabb_t box = {V(lo.x + x * cell, lo.y + y * cell, lo.z + z * cell),
                       V(lo.x + (x + 1) * cell, lo.y + (y + 1) * cell, lo.z + (z + 1) * cell)};
         double t0, t1;
+        ++g_node_tests;
         if (!ray_aabb(ray, &box, &t0, &t1)) continue;
         if (level == L) {
             if (t1 - t0 > 1e-12) {

@@ -192,6 +192,8 @@ def load_library():
         "svlf_render_gt_device": ([vp, vp, vp, vp, vp, vp], st),
         "svlf_backproject_device": ([vp, vp, vp, vp, sz, C.POINTER(sz)], st),
         "svlf_psnr_device": ([vp, vp, vp, sz, C.POINTER(C.c_double)], st),
+        "svlf_ctx_last_node_tests": ([vp, C.POINTER(C.c_longlong)], st),
+        "svlf_ctx_set_node_test_counting": ([vp, C.c_int], st),
         "svlf_ssim_device": ([vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)], st),
         "svlf_depth_errors_device": ([vp, vp, vp, vp, sz, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                       C.POINTER(C.c_int)], st),
@@ -303,6 +305,16 @@ class Context:
         t = _Timings()
         _check(_LIB.svlf_ctx_last_timings(self._h, C.byref(t)))
         return {n: getattr(t, n) for n, _ in _Timings._fields_}
+
+    def set_node_test_counting(self, enable: bool):
+        """Diagnostics: run the traversal variant that counts ray-box tests (see last_node_tests)."""
+        _check(_LIB.svlf_ctx_set_node_test_counting(self._h, 1 if enable else 0))
+
+    def last_node_tests(self) -> int:
+        """Ray-box tests of the last traversal's cooperative passes (reference ray_aabb calls)."""
+        v = C.c_longlong()
+        _check(_LIB.svlf_ctx_last_node_tests(self._h, C.byref(v)))
+        return int(v.value)
 
     @staticmethod
     def kernel_launches() -> int:

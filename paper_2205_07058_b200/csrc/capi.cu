@@ -93,6 +93,7 @@ struct svlf_ctx {
     ncclComm_t nccl = nullptr;          // data-parallel communicator (optional)
     bool train_tf32 = false;            // train-step weight-gradient GEMMs on tensor cores (TF32)
     bool train_tf32x3 = false;          // every train-step GEMM as split 3xTF32 on tensor cores
+    bool count_node_tests = false;      // traversal variant that counts ray-box tests (diagnostics)
     int rank = 0, world = 1;
     TrainScratch train;
     int* h_pinned = nullptr;  // small pinned mailbox for counters/flags
@@ -247,7 +248,7 @@ unsigned long long* misc_fg(svlf_ctx* ctx) { return reinterpret_cast<unsigned lo
 // per-ray fallback) with no host round trip; leaves per-ray segments
 // (ctx->offsets = start, ctx->counts = count) and sorted hits in ctx->hit_*,
 // counters at traversal_counters(ctx): [0] hits, [1] overflow, [2] capacity
-// exceeded, [3] dense overflow.
+// exceeded, [3] dense overflow, [7] ray-box tests of the cooperative passes.
 uint32_t* traversal_counters(svlf_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->misc.as<char>() + 16); }
 
 void enqueue_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0, uint32_t rows,
@@ -268,11 +269,11 @@ void enqueue_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* 
     ctx->hit_cap = cap;
     TraverseOut o{ray_off, ray_cnt, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
                   ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), counters, ovl, ovl2, rays, uint32_t(cap)};
-    SVLF_CUDA(cudaMemsetAsync(counters, 0, 28, s));  // hit/overflow counters + tile cursors
+    SVLF_CUDA(cudaMemsetAsync(counters, 0, 32, s));  // hit/overflow counters, tile cursors, node tests
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
-    launch_traverse(dev_view(tree), cam, row0, rows, n, o, s);
+    launch_traverse(dev_view(tree), cam, row0, rows, n, o, s, ctx->count_node_tests);
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));
-    launch_traverse_dense(dev_view(tree), cam, row0, o, s);
+    launch_traverse_dense(dev_view(tree), cam, row0, o, s, ctx->count_node_tests);
     launch_traverse_fallback(dev_view(tree), cam, row0, o, s);
     SVLF_CUDA(cudaEventRecord(ctx->ev[EV_EMIT], s));
 }
@@ -811,6 +812,28 @@ svlf_status svlf_ctx_set_train_precision(svlf_ctx* ctx, svlf_precision precision
         std::lock_guard<std::mutex> lk(ctx->mu);
         ctx->train_tf32 = precision == SVLF_PRECISION_TF32;
         ctx->train_tf32x3 = precision == SVLF_PRECISION_TF32X3;
+    });
+}
+
+svlf_status svlf_ctx_set_node_test_counting(svlf_ctx* ctx, int enable) {
+    return guard([&] {
+        require(ctx != nullptr, "null argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        ctx->count_node_tests = enable != 0;
+    });
+}
+
+svlf_status svlf_ctx_last_node_tests(svlf_ctx* ctx, long long* out) {
+    return guard([&] {
+        require(ctx && out, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        uint32_t v = 0;
+        if (ctx->misc.p) {
+            SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+            SVLF_CUDA(cudaMemcpy(&v, traversal_counters(ctx) + 7, 4, cudaMemcpyDeviceToHost));
+        }
+        *out = (long long)v;
     });
 }
 

@@ -119,11 +119,12 @@ struct TraverseOut {
     double* rays;  // n x 6: input rays (buffer mode) or camera rays written for foreground rays
     uint32_t capacity;
 };
+// count = true: the variant that also counts ray-box tests into counters[7]
 void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
-                     const TraverseOut& o, cudaStream_t s);
-// second cooperative pass (8 rays per block) over the rays of overflowed tiles
+                     const TraverseOut& o, cudaStream_t s, bool count = false);
+// second cooperative pass (16 rays per block) over the rays of overflowed tiles
 void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
-                           cudaStream_t s);
+                           cudaStream_t s, bool count = false);
 // per-ray depth-first walker for whatever still overflowed
 void launch_traverse_fallback(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
                               cudaStream_t s);

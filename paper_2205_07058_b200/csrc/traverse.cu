@@ -248,7 +248,8 @@ struct BfsArgs {
     double* hit_tout;
     uint32_t* hit_ray;
     uint32_t* counters;  // [0] hits allocated, [1] overflow rays, [2] capacity exceeded, [3] dense overflow,
-                         // [5] / [6] next tile of the first / second cooperative pass
+                         // [5] / [6] next tile of the first / second cooperative pass,
+                         // [7] ray-box tests (root + every occupied child of an expanded node, 32-bit)
     uint32_t* overflow_rays;
     uint32_t* overflow_dense;
     double* rays;
@@ -309,10 +310,12 @@ struct TileShape {
     static constexpr int H = kR / W;
 };
 
-template <bool kCamera, int kR, int kQ, int kT, bool kList>
+template <bool kCamera, int kR, int kQ, int kT, bool kList, bool kCount>
 __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& cam, uint32_t row0, uint32_t rows,
-                                         uint32_t n, const BfsArgs& A, BfsSmem<kR, kQ, kT>& S, uint32_t tile) {
+                                         uint32_t n, const BfsArgs& A, BfsSmem<kR, kQ, kT>& S, uint32_t tile,
+                                         uint32_t& tests_done) {
     const uint32_t tid = threadIdx.x & uint32_t(kT - 1);
+    uint32_t tests = 0;  // this tile's ray-box tests; counted only if the tile completes here
 
     // ---- rays of this tile; root test
     uint32_t my_ray = 0xffffffffu;
@@ -374,6 +377,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             }
             cell_box(T, T.cell[0], 0, 0, 0, lo, hi);
             hit = slab_test(p, lo, hi, t0, t1) ? 1u : 0u;
+            if constexpr (kCount) ++tests;
         }
         uint32_t off, tot;
         tile_excl_sum<kT>(S, hit, off, tot);
@@ -413,6 +417,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 NodeSplit sp;
                 split_node(T, o, d, inv, level, x, y, z, sp);
                 s = sign_mask(d);
+                if constexpr (kCount) tests += __popc(node.y);
 #pragma unroll
                 for (uint32_t oct = 0; oct < 8; ++oct) {
                     if (!((node.y >> oct) & 1u)) continue;
@@ -446,7 +451,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         cur ^= 1;  // the chunk barrier above already orders this level's appends before the next level
     }
 
-    if (S.overflow) {  // hand the whole tile (kept contiguous) to the next pass
+    if (S.overflow) {  // (this tile's tests are not counted: the pass that completes its rays counts them)  // hand the whole tile (kept contiguous) to the next pass
         if (tid == 0) S.base = atomicAdd(&A.counters[kList ? 3 : 1], uint32_t(kR));
         tile_sync<kT>();
         if (tid < kR) (kList ? A.overflow_dense : A.overflow_rays)[S.base + tid] = S.gray[tid];
@@ -477,6 +482,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 NodeSplit sp;
                 split_node(T, o, d, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
                            uint32_t(xyz >> 42), sp);
+                if constexpr (kCount) tests += __popc(node.y);
 #pragma unroll
                 for (uint32_t oct = 0; oct < 8; ++oct) {
                     if (!((node.y >> oct) & 1u)) continue;
@@ -588,12 +594,13 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             store_ray(A.rays, S.gray[tid], r);
         }
     }
+    if constexpr (kCount) tests_done += tests;
 }
 
 // Persistent: each tile group (a block, or each warp of a block when kT ==
 // 32) takes tiles from a device-side cursor until they run out. kList passes
 // read their tile count from the device (no host round trip).
-template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList>
+template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList, bool kCount>
 __global__ void __launch_bounds__(kBlock) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
                                                          uint32_t n, uint32_t n_tiles, BfsArgs A) {
     extern __shared__ __align__(16) uint8_t bfs_smem[];
@@ -605,13 +612,19 @@ __global__ void __launch_bounds__(kBlock) k_traverse_bfs(DevOctree T, DevCamera 
     // cost (background vs dense foreground), so a static round-robin leaves a
     // long tail
     uint32_t* next = A.counters + (kList ? 6 : 5);
+    uint32_t tests = 0;
     for (;;) {
         if ((threadIdx.x & uint32_t(kT - 1)) == 0) S.next_tile = atomicAdd(next, 1u);
         tile_sync<kT>();
         const uint32_t tile = S.next_tile;
         if (tile >= tiles) break;
-        bfs_tile<kCamera, kR, kQ, kT, kList>(T, cam, row0, rows, n, A, S, tile);
+        bfs_tile<kCamera, kR, kQ, kT, kList, kCount>(T, cam, row0, rows, n, A, S, tile, tests);
         tile_sync<kT>();
+    }
+    if constexpr (kCount) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) tests += __shfl_xor_sync(0xffffffffu, tests, d);
+        if ((threadIdx.x & 31u) == 0 && tests) atomicAdd(&A.counters[7], tests);
     }
 }
 
@@ -740,55 +753,73 @@ static int num_sms() {
 #endif
 constexpr int kBfsBlocksPerSm = SVLF_BFS_BLOCKS_PER_SM;
 
-template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList>
+template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList, bool kCount>
 static void set_bfs_attr() {
     static bool done = false;
     if (done) return;
-    SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kQ, kT, kBlock, kList>,
+    SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kQ, kT, kBlock, kList, kCount>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(sizeof(BfsSmem<kR, kQ, kT>) * (kBlock / kT))));
     done = true;
 }
 
-void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
-                     const TraverseOut& o, cudaStream_t s) {
-    if (n == 0) return;
+template <bool kCount>
+static void launch_traverse_t(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
+                              const TraverseOut& o, cudaStream_t s) {
     const BfsArgs A = bfs_args(o);
     constexpr uint32_t kGroups = kBlockThreads / kThreads;
     const size_t smem = sizeof(BfsSmem<kRays, kQCap, kThreads>) * kGroups;
     const uint32_t cap_grid = uint32_t(num_sms() * kBfsBlocksPerSm);
     if (cam) {
-        set_bfs_attr<true, kRays, kQCap, kThreads, kBlockThreads, false>();
+        set_bfs_attr<true, kRays, kQCap, kThreads, kBlockThreads, false, kCount>();
         using TS = TileShape<kRays>;
         const uint32_t tiles = ((cam->width + TS::W - 1) / TS::W) * ((rows + TS::H - 1) / TS::H);
         const uint32_t blocks = std::min((tiles + kGroups - 1) / kGroups, cap_grid);
-        k_traverse_bfs<true, kRays, kQCap, kThreads, kBlockThreads, false><<<blocks, kBlockThreads, smem, s>>>(
+        k_traverse_bfs<true, kRays, kQCap, kThreads, kBlockThreads, false, kCount><<<blocks, kBlockThreads, smem, s>>>(
             T, *cam, row0, rows, n, tiles, A);
     } else {
-        set_bfs_attr<false, kRays, kQCap, kThreads, kBlockThreads, false>();
+        set_bfs_attr<false, kRays, kQCap, kThreads, kBlockThreads, false, kCount>();
         const uint32_t tiles = (n + kRays - 1) / kRays;
         const uint32_t blocks = std::min((tiles + kGroups - 1) / kGroups, cap_grid);
-        k_traverse_bfs<false, kRays, kQCap, kThreads, kBlockThreads, false><<<blocks, kBlockThreads, smem, s>>>(
+        k_traverse_bfs<false, kRays, kQCap, kThreads, kBlockThreads, false, kCount><<<blocks, kBlockThreads, smem, s>>>(
             T, DevCamera{}, 0, 0, n, tiles, A);
     }
+}
+
+void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
+                     const TraverseOut& o, cudaStream_t s, bool count) {
+    if (n == 0) return;
+    if (count)
+        launch_traverse_t<true>(T, cam, row0, rows, n, o, s);
+    else
+        launch_traverse_t<false>(T, cam, row0, rows, n, o, s);
     note_launch();
 }
 
-void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
-                           cudaStream_t s) {
+template <bool kCount>
+static void launch_traverse_dense_t(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
+                                    cudaStream_t s) {
     const BfsArgs A = bfs_args(o);
     using Sm = BfsSmem<kRaysDense, kQCapDense, kThreadsDense>;
     const uint32_t per_sm = std::max<uint32_t>(1, uint32_t(200 * 1024 / sizeof(Sm)));
     const uint32_t grid = uint32_t(num_sms()) * per_sm;
     if (cam) {
-        set_bfs_attr<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>();
-        k_traverse_bfs<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>
+        set_bfs_attr<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>();
+        k_traverse_bfs<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>
             <<<grid, kThreadsDense, sizeof(Sm), s>>>(T, *cam, row0, 0, 0, 0, A);
     } else {
-        set_bfs_attr<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>();
-        k_traverse_bfs<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true>
+        set_bfs_attr<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>();
+        k_traverse_bfs<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>
             <<<grid, kThreadsDense, sizeof(Sm), s>>>(T, DevCamera{}, 0, 0, 0, 0, A);
     }
+}
+
+void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
+                           cudaStream_t s, bool count) {
+    if (count)
+        launch_traverse_dense_t<true>(T, cam, row0, o, s);
+    else
+        launch_traverse_dense_t<false>(T, cam, row0, o, s);
     note_launch();
 }
 

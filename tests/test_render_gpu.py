@@ -54,6 +54,24 @@ def test_traversal_c1_camera_rays_bit_exact(c1, oracle):
     assert np.array_equal(got[4][:, 3:], o + d * got[3][:, None])
 
 
+def test_traversal_node_tests_match_reference_walk(c1, ctx, oracle):
+    """The traversal's ray-box test counter (bench's node-tests/s) equals the reference walk's ray_aabb calls
+    (src/octree.cpp:185-235; 143.8 per C1 ray)."""
+    tree, otree, cam, W, H = c1
+    rays = oracle.camera_rays(cam, W, H)
+    ctx.set_node_test_counting(True)
+    try:
+        tree.traverse(rays)
+        got = ctx.last_node_tests()
+    finally:
+        ctx.set_node_test_counting(False)
+    oracle.node_tests()
+    oracle.traverse(otree, rays)
+    want = oracle.node_tests() // 2  # oracle.traverse walks twice (count pass, then fill pass)
+    assert got == want  # C1 has no re-traversed (overflowed) tiles, so no test is repeated
+    assert abs(want / rays.shape[0] - 143.8) < 0.05
+
+
 def test_traversal_reference_random_rays(ctx, oracle):
     """tests/test_octree.cpp:140-154: random 16^3 density-0.1 seed-7 octree, 1000 rays (Rng 11)."""
     pts = S.random_occupancy_points(16, 0.1, 7)
