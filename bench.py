@@ -168,6 +168,19 @@ def barrier(dist):
         dist.barrier()
 
 
+def host_cpu():
+    """nproc and the CPU model of this host (stated beside the CPU timings)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1):
     """Reference render_frame (oracle/_ref, reference flags, all host threads) on
     the same octree/model/camera; falls back to the C restatement."""
@@ -200,7 +213,7 @@ def cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1):
     s = min(secs)
     return {"value": round(W * H / s / 1e6, 4), "unit": "Mrays/s", "cores": cores, "kind": kind,
             "sample": f"{frames} full {W}x{H} frame(s) of the same workload, render_frame, best of {frames}",
-            "seconds_per_frame": round(s, 3)}
+            "seconds_per_frame": round(s, 3), **host_cpu()}
 
 
 def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=None, world=1):
@@ -379,7 +392,8 @@ def run_reference(args):
             "config": {"workload": f"C2: RTMV-shaped {args.objects}-object scene, octree depth 8, one {W}x{H} frame",
                        "frames_per_step": 1},
             "cpu_baseline": {"value": round(value, 4), "unit": "Mrays/s", "cores": cores, "kind": kind,
-                             "sample": f"{args.steps} full {W}x{H} frames (render_frame, all host threads)"},
+                             "sample": f"{args.steps} full {W}x{H} frames (render_frame, all host threads)",
+                             **host_cpu()},
             "e2e": {"value": round(value, 4), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
