@@ -345,7 +345,7 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
                                        "cores": R.thread_count(), "kind": "reference",
                                        "sample": "train() epochs {0,0,1} on the same one-frame 512^2 dataset "
                                                  "(one stage-3 step; EpochLog.seconds)",
-                                       "seconds_per_step": round(secs, 3)}
+                                       "seconds_per_step": round(secs, 3), **host_cpu()}
         except Exception as e:
             out["cpu_baseline"] = {"error": str(e)}
     return out
