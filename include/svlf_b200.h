@@ -116,7 +116,7 @@ typedef struct svlf_timings {
     float traverse_ms, emit_ms, decode_ms, composite_ms, backward_ms, adam_ms, total_ms;
     long long hits;
     long long overflow_rays; /* rays re-traversed by the per-ray fallback walker */
-    long long dense_rays;    /* rays whose block queue overflowed, re-run by the dense 8-ray pass */
+    long long dense_rays;    /* rays whose block queue overflowed, re-run by the second (16-ray) cooperative pass */
 } svlf_timings;
 
 /* ---- context -------------------------------------------------------- */

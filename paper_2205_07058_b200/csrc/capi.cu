@@ -89,7 +89,7 @@ struct svlf_ctx {
     DevBuf csr_off, csr_leaf, csr_tin, csr_tout, csr_ray, overflow2;
     size_t hit_cap = 0;
     long long last_overflow_rays = 0;  // rays that reached the per-ray fallback walker
-    long long last_dense_rays = 0;     // rays re-run by the dense 8-ray pass
+    long long last_dense_rays = 0;     // rays re-run by the second (16-ray) cooperative pass
     ncclComm_t nccl = nullptr;          // data-parallel communicator (optional)
     bool train_tf32 = false;            // train-step weight-gradient GEMMs on tensor cores (TF32)
     bool train_tf32x3 = false;          // every train-step GEMM as split 3xTF32 on tensor cores
