@@ -122,8 +122,8 @@ static_assert(kChainsTm * 192 + kChainsSm * 128 <= 512, "TMEM columns");
 // side data: u1, u2, r6 pairs); entry e is filled by group e % TW_GROUPS and
 // consumed by chain e % TW_CHAINS.
 constexpr uint32_t TW_RING0 = (T_WEIGHTS + 1023) & ~1023u;
-constexpr uint32_t TW_SIDE = 9 * 128 * 4;                 // u[6] fp32, r6 pairs[3], SoA
-constexpr uint32_t TW_ENTRY = T_A_BYTES + TW_SIDE;        // 41760
+constexpr uint32_t TW_SIDE = 11 * 128 * 4;                // u[6] fp32, r6 pairs[3], t_in, t_out (fp32), SoA
+constexpr uint32_t TW_ENTRY = T_A_BYTES + TW_SIDE;        // 42784
 constexpr uint32_t TW_ENTRIES = 4;
 #ifndef SVLF_DEC_T_GROUPS
 #define SVLF_DEC_T_GROUPS 4
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kSlots * 128, 1)
         if (valid) {
             const float e = __fdividef(1.0f, 1.0f + __expf(-hv[1])), ome = 1.0f - e;
             out.tau[j] = fmaxf(hv[0], 0.f);
-            out.eta[j] = e;
+            out.eta[j] = float(tin) * e + float(tout) * (1.f - e);  // 16-bit path: t_s for the composite
             // f_C record: r6 and the trilinear weights at x_s = eta x1 + (1-eta) x2,
             // u_s = eta u1 + (1-eta) u2 (voxel_batch.hpp:111)
             const float us[3] = {u[0] * e + u[3] * ome, u[1] * e + u[4] * ome, u[2] * e + u[5] * ome};
@@ -1030,6 +1030,8 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             for (int i = 0; i < 6; ++i) side[i * 128 + row] = __float_as_uint(u[i]);
 #pragma unroll
             for (int i = 0; i < 3; ++i) side[(6 + i) * 128 + row] = r6p[i];
+            side[9 * 128 + row] = __float_as_uint(float(tin));
+            side[10 * 128 + row] = __float_as_uint(float(tout));
             fence_async_smem();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[e])) : "memory");
@@ -1072,7 +1074,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
         // each tile costs one MMA round trip; tile k's outputs are written
         // while tile k + TW_CHAINS's epilogue is next.
         const uint32_t d_head = acc + 128;
-        float u[6];
+        float u[6], ft[2];
         uint32_t r6p[3];
         auto read_side = [&](uint32_t e) {
             const uint32_t* side = reinterpret_cast<const uint32_t*>(sm + TW_RING0 + e * TW_ENTRY + T_A_BYTES);
@@ -1080,6 +1082,8 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             for (int i = 0; i < 6; ++i) u[i] = __uint_as_float(side[i * 128 + r]);
 #pragma unroll
             for (int i = 0; i < 3; ++i) r6p[i] = side[(6 + i) * 128 + r];
+            ft[0] = __uint_as_float(side[9 * 128 + r]);
+            ft[1] = __uint_as_float(side[10 * 128 + r]);
         };
         auto layer0 = [&](uint32_t k) {
             const uint32_t e = k % TW_ENTRIES;
@@ -1108,6 +1112,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             const uint32_t kn = k + TW_CHAINS;
             const bool next = tile_of(kn) < ntiles;
             float cu[6];
+            const float cft0 = ft[0], cft1 = ft[1];
             uint32_t cr6[3];
 #pragma unroll
             for (int i = 0; i < 6; ++i) cu[i] = u[i];
@@ -1129,7 +1134,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             if (j < n) {
                 const float ee = __fdividef(1.0f, 1.0f + __expf(-hv[1])), ome = 1.0f - ee;
                 out.tau[j] = fmaxf(hv[0], 0.f);
-                out.eta[j] = ee;
+                out.eta[j] = cft0 * ee + cft1 * (1.f - ee);  // t_s for the composite (as it computed it)
                 const float us[3] = {cu[0] * ee + cu[3] * ome, cu[1] * ee + cu[4] * ome, cu[2] * ee + cu[5] * ome};
                 float ws[8];
 #pragma unroll

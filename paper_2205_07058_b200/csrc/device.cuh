@@ -96,7 +96,8 @@ struct DevBuf {
 // Per-hit decoder outputs consumed by composite.
 struct HitOut {
     float* tau;
-    float* eta;
+    float* eta;  // fp32 decoder: eta; tensor-core decoders: t_s = eta t_in + (1 - eta) t_out (fp32), which is
+                 // all the 16-bit composite needs from eta (so it does not re-read t_in / t_out)
     float* rgb;  // 3 per hit
 };
 

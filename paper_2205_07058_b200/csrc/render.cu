@@ -196,8 +196,7 @@ __global__ void __launch_bounds__(128) k_composite_warp(const uint32_t* __restri
                 r = h.rgb[3 * size_t(j)];
                 g = h.rgb[3 * size_t(j) + 1];
                 bl = h.rgb[3 * size_t(j) + 2];
-                const float eta = h.eta[j];
-                ts = float(tin[j]) * eta + float(tout[j]) * (1.f - eta);
+                ts = h.eta[j];  // the tensor-core decoder stores t_s = eta t_in + (1 - eta) t_out (fp32)
             }
             // exclusive prefix product of e over the lanes
             float incl = e;
