@@ -125,8 +125,8 @@ def stage_rooflines(stage, hits, n, peaks, node_tests=None):
     """Every render stage against its roofline (north star: each stage as a
     fraction of its roofline). Algorithmic bytes per stage:
     traversal 24 B per emitted hit (leaf, t_in, t_out) + 8 B per ray (segment);
-    decode 110,848 FLOP per hit (tensor); composite 36 B per hit read (t_in,
-    t_out, tau, eta, rgb) + 20 B per ray written. The traversal passes are
+    decode 110,848 FLOP per hit (tensor); composite 20 B per hit read (tau,
+    rgb, t_s) + 8 B per ray read (segment) + 20 B per ray written. The traversal passes are
     fp64/latency-bound rather than HBM-bound, which the small fractions show."""
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
     tc = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
@@ -146,7 +146,7 @@ def stage_rooflines(stage, hits, n, peaks, node_tests=None):
         out["decode"] = {"bound": "tensor", "achieved": round(tf, 2), "peak": tc, "unit": "TFLOP/s",
                          "frac": round(tf / tc, 5), "ms": stage["decode_ms"]}
     if stage["composite_ms"] > 0:
-        gbs = (36 * hits + BYTES_PER_RAY_OUT * n) / (stage["composite_ms"] * 1e-3) / 1e9
+        gbs = (20 * hits + (8 + BYTES_PER_RAY_OUT) * n) / (stage["composite_ms"] * 1e-3) / 1e9
         out["composite"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                             "frac": round(gbs / hbm, 5), "ms": stage["composite_ms"]}
     return out
