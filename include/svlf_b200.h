@@ -142,7 +142,8 @@ svlf_status svlf_ctx_last_node_tests(svlf_ctx* ctx, long long* out);
 /* Arithmetic of the train step's dense layers: SVLF_PRECISION_FP32 (default:
  * true fp32 CUDA-core GEMMs, gradients within 1e-4 of the reference),
  * SVLF_PRECISION_TF32X3 (every GEMM on tensor cores as hi*hi + hi*lo + lo*hi
- * of TF32 splits x = hi + lo, fp32 accumulation: the same fp32 gates) or
+ * of TF32 splits x = hi + lo, fp32 accumulation: the same fp32 gates; weight
+ * gradients summed with fp32 atomics, so not bitwise reproducible) or
  * SVLF_PRECISION_TF32 (the weight-gradient GEMMs on tensor cores with plain
  * TF32 operands; forward and input gradients stay fp32; gradients within
  * 2e-2, the 16-bit tolerance of SURVEY.md §8(c)). */
