@@ -293,3 +293,27 @@ def test_deep_octree_render_matches_oracle(ctx, oracle, res):
     orgb, oa, od, _ = oracle.render_frame(otree, om, cam, W, W)
     assert np.abs(rgb.reshape(-1) - orgb).max() <= TOL_FP32
     assert np.abs(d.reshape(-1) - od).max() <= TOL_FP32
+
+
+@pytest.mark.parametrize("precision", ["fp16", "bf16", "fp32"])
+def test_render_empty_and_tiny_frames(c1, oracle, ctx, precision):
+    """Frames with no hit at all (camera facing away from the scene) and 1x1 / 3x2 frames through every
+    decoder path: background and zero alpha/depth exactly like the reference."""
+    tree, otree, cam, W, H = c1
+    model = P.Model(tree, seed=2, ctx=ctx)
+    om = oracle.init_model(otree, 2)
+    away = S.lookat_camera((0.5, 0.5, 3.0), (0.5, 0.5, 6.0), 64, 48, 50.0)
+    bg = np.array([0.25, 0.5, 0.75], np.float32)
+    st = P.RenderStats()
+    rgb, a, d = P.render_frame(model, P.Camera.from_record(away, 64, 48), background=bg, stats=st,
+                               precision=precision)
+    assert st.traversal_hits == 0 and st.rays_with_hits == 0
+    assert np.array_equal(rgb.reshape(-1, 3), np.broadcast_to(bg, (64 * 48, 3)))
+    assert not np.any(a) and not np.any(d)
+    for w, h in ((1, 1), (3, 2)):
+        c = S.lookat_camera(tuple(0.5 + 1.8 * x for x in S.C1_EYE_DIR), (0.5, 0.5, 0.5), w, h, 2.0)
+        rgb, a, d = P.render_frame(model, P.Camera.from_record(c, w, h), precision=precision)
+        orgb, oa, od, _ = oracle.render_frame(otree, om, c, w, h)
+        tol = 1e-3 if precision == "fp32" else 3e-2
+        assert np.abs(rgb.reshape(-1) - orgb).max() <= tol
+        assert np.abs(a.reshape(-1) - oa).max() <= tol
