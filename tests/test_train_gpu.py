@@ -135,11 +135,14 @@ def test_frozen_stage_keeps_color_parameters(batch, ctx):
     assert steps[0] == 1 and steps[1] == 0 and list(steps[2:6]) == [1] * 4 and list(steps[6:]) == [0] * 8
 
 
-def test_nccl_attached_single_rank_matches_local(batch, oracle):
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
+def test_nccl_attached_single_rank_matches_local(batch, oracle, precision):
     """Data-parallel path with a 1-rank NCCL communicator: the all-reduced step must equal the
     local step (loss identical, parameters identical up to atomic-order rounding)."""
     tree, otree, rays, cgt, depth, alpha = batch
     a, b = P.Context(0), P.Context(0)
+    a.set_train_precision(precision)
+    b.set_train_precision(precision)
     b.attach_nccl(P.nccl_unique_id(), 0, 1)
     codes = tree.leaf_codes
     ta = P.SparseOctree.from_leaves(codes, tree.config, a)
@@ -149,8 +152,9 @@ def test_nccl_attached_single_rank_matches_local(batch, oracle):
         la = P.train_step(ma, rays, cgt, depth, alpha, mode="volumetric", lr=1e-3)
         lb = P.train_step(mb, rays, cgt, depth, alpha, mode="volumetric", lr=1e-3)
         assert abs(la - lb) <= LOSS_REL * abs(la)
+    share = 1e-3 if precision == "fp32" else 5e-3  # 3xTF32 dW uses fp32 atomics (see test_cpp_api)
     for x, y in zip(ma.get_params(), mb.get_params()):
-        assert np.mean(np.abs(x - y) > 1e-6) < 1e-3
+        assert np.mean(np.abs(x - y) > 1e-6) < share
         assert np.abs(x - y).max() <= 2.5e-3
     assert mb.get_adam()[2].tolist() == [2] * 14
     b.detach_nccl()
