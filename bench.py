@@ -6,7 +6,7 @@ One step = render one full 1600x1600 frame of the C2 workload (RTMV-shaped
 maps, init_model seed 1) per GPU. N GPUs = one process per GPU (torchrun),
 octree and model replicated, each rank renders its own frame: weak scaling,
 no data-path collective. Timing: CUDA events on the
-library's stream around each step, L2 flushed (256 MiB write) between steps
+library's stream around each step, L2 flushed (a write of 1.25x the L2 size) between steps
 (the model is L2-sized), max over ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
@@ -163,6 +163,14 @@ def ncu_traffic(prefix, path=os.path.join(ROOT, "profiles", "r1_render.json")):
         return None
 
 
+def l2_flush_bytes(device):
+    """A write of 1.25x the L2 size evicts every line (timing rule: flush L2 between timed steps)."""
+    import torch
+
+    l2 = getattr(torch.cuda.get_device_properties(device), "L2_cache_size", 0) or (126 << 20)
+    return (int(l2 * 1.25) + (1 << 20) - 1) >> 20 << 20
+
+
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -236,7 +244,7 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
     d_cgt = torch.from_numpy(np.ascontiguousarray(cgt, dtype=np.float32)).to(device)
     d_depth = torch.from_numpy(np.ascontiguousarray(depth)).to(device)
     d_alpha = torch.from_numpy(np.ascontiguousarray(alpha, dtype=np.uint8)).to(device)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    flush = torch.empty(l2_flush_bytes(device), dtype=torch.uint8, device=device)
 
     def step():
         return P.train_step_device(model, d_rays.data_ptr(), d_cgt.data_ptr(), d_depth.data_ptr(),
@@ -437,7 +445,7 @@ def main():
     d_rgb = torch.empty(n * 3, dtype=torch.float32, device=device)
     d_alpha = torch.empty(n, dtype=torch.float32, device=device)
     d_depth = torch.empty(n, dtype=torch.float32, device=device)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    flush = torch.empty(l2_flush_bytes(device), dtype=torch.uint8, device=device)
 
     def step(stats=None):
         P.render_frame_device(model, camera, d_rgb.data_ptr(), d_alpha.data_ptr(), d_depth.data_ptr(),
@@ -555,7 +563,7 @@ def main():
                    "hits_per_ray": round(hits / n, 4),
                    "foreground_fraction": round(stats.rays_with_hits / args.steps / n, 4),
                    "precision": precision, "parallelism": f"replicated octree, {world} rank(s), one frame each",
-                   "l2": "flushed (256 MiB write) between timed steps",
+                   "l2": f"flushed ({flush.numel() >> 20} MiB write, 1.25x L2) between timed steps",
                    "input_gen_seconds": round(t_gen, 1)},
         "stages_ms": stage,
         "roofline": {"bound": "tensor", "kernel": f"decode_{precision}", "achieved": round(achieved_tflops, 3),
