@@ -317,3 +317,35 @@ def test_render_empty_and_tiny_frames(c1, oracle, ctx, precision):
         tol = 1e-3 if precision == "fp32" else 3e-2
         assert np.abs(rgb.reshape(-1) - orgb).max() <= tol
         assert np.abs(a.reshape(-1) - oa).max() <= tol
+
+
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_band_shards_stitch_to_the_full_frame(ctx, precision, world):
+    """SURVEY.md §8(e) render sharding: each rank renders its row band (parallel.row_band) with
+    svlf_render_rows_device; the stitched bands are bit-identical to the full frame (rays are
+    independent, so band boundaries change nothing)."""
+    import torch
+    from paper_2205_07058_b200.parallel import row_band
+
+    sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=4, n_views=8, view_res=96, res=64, width=160)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    camera = P.Camera.from_record(cam, W, H)
+    n = W * H
+
+    def bufs():
+        return (torch.zeros(n * 3, device="cuda"), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda"))
+
+    full = bufs()
+    P.render_frame_device(model, camera, *(b.data_ptr() for b in full), precision=precision)
+    parts = bufs()
+    for rank in range(world):
+        r0, rows = row_band(H, rank, world)
+        off = r0 * W
+        P.render_frame_device(model, camera, parts[0][off * 3:].data_ptr(), parts[1][off:].data_ptr(),
+                              parts[2][off:].data_ptr(), precision=precision, row0=r0, rows=rows)
+    torch.cuda.synchronize()
+    for a, b in zip(full, parts):
+        assert torch.equal(a, b)
+    assert float(full[1].sum()) > 0  # the frame has foreground
