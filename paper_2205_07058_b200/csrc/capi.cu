@@ -314,7 +314,7 @@ void run_decode_composite(svlf_ctx* ctx, svlf_model* m, uint32_t n, uint32_t tot
     int* err = ctx->misc.as<int>();
     if (prec == SVLF_PRECISION_BF16 || prec == SVLF_PRECISION_FP16) {
         const bool bf16 = prec == SVLF_PRECISION_BF16;
-        ensure_pack_tc(m->view(), m->pack_bf16, m->pack_bf16_version, m->version, bf16, s);
+        ensure_pack_tc(m->view(), T, m->pack_bf16, m->pack_bf16_version, m->version, bf16, s);
         void* scratch = ctx->tc_scratch.ensure<uint8_t>(decode_tc_scratch_bytes(cap));
         launch_decode_tc(T, m->view(), m->pack_bf16.as<char>(), bf16, ctx->rays.as<double>(),
                          ctx->hit_ray.as<uint32_t>(), ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),

@@ -721,12 +721,14 @@ __global__ void __launch_bounds__(kCtThreads, 1)
 
     if (warp < kProducers) {
         // ---- producer warp: whole input tiles, k = warp, warp + kProducers, ...
-        // Per 32-row group, lane l holds row 32g + l (corners, f_C record);
-        // pass p, lanes 4q..4q+3 gather row 8p+q of the group, 8 features each.
-        const uint32_t q = lane >> 2, ch = lane & 3;
-        // Software pipeline: the leaf indices of a tile are loaded a tile
-        // ahead, each 32-row group's corners and f_C records a group ahead.
-        uint32_t leaves[4], c[8], nc[8];
+        // Per 32-row group, lane l holds row 32g + l (leaf, f_C record). The
+        // features come from the per-leaf table (8 corner rows of 64 B per
+        // leaf): in pass p, lanes 8h..8h+7 gather row 4p+h of the group, lane
+        // (cp, ch) = corners 2k + cp of chunk ch, so one load instruction reads
+        // 4 whole 128-byte lines (corners 2k, 2k+1 of 4 rows); the two corner
+        // halves are summed with one shuffle.
+        const uint32_t hsub = lane >> 3, cp = (lane >> 2) & 1u, ch = lane & 3;
+        uint32_t leaves[4], lf_cur = 0, lf_next = 0;
         uint4 g0, g1, ng0, ng1;
         auto fetch_leaves = [&](uint32_t t) {
 #pragma unroll
@@ -737,16 +739,12 @@ __global__ void __launch_bounds__(kCtThreads, 1)
         };
         auto fetch = [&](uint32_t t, uint32_t leaf, uint32_t g) {
             const uint32_t j = t * 128 + 32 * g + lane;
+            lf_next = leaf;
             if (leaf != 0xffffffffu) {
-                const uint4* cp = reinterpret_cast<const uint4*>(T.corners + 8 * size_t(leaf));
-                const uint4 a = __ldg(cp), b = __ldg(cp + 1);
-                nc[0] = a.x; nc[1] = a.y; nc[2] = a.z; nc[3] = a.w;
-                nc[4] = b.x; nc[5] = b.y; nc[6] = b.z; nc[7] = b.w;
                 ng0 = crec[2 * size_t(j)];
                 ng1 = crec[2 * size_t(j) + 1];
             } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) nc[i] = 0;
+                lf_next = 0;
                 ng0 = ng1 = make_uint4(0, 0, 0, 0);
             }
         };
@@ -760,8 +758,7 @@ __global__ void __launch_bounds__(kCtThreads, 1)
             const uint32_t a_base = ring0 + slot * CT_A_BYTES;
 #pragma unroll 1
             for (uint32_t g = 0; g < (SVLF_DEC_EXP == 1 ? 0 : 4); ++g) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) c[i] = nc[i];
+                lf_cur = lf_next;
                 g0 = ng0;
                 g1 = ng1;
                 if (g < 3) {
@@ -772,30 +769,33 @@ __global__ void __launch_bounds__(kCtThreads, 1)
                 }
                 const uint32_t wsp[4] = {g1.x, g1.y, g1.z, g1.w};
 #pragma unroll 2
-                for (uint32_t p = 0; p < 4; ++p) {
-                    const uint32_t src = 8 * p + q;
-                    uint32_t cb[8], wt[4];
+                for (uint32_t p = 0; p < 8; ++p) {
+                    const uint32_t src = 4 * p + hsub;
+                    const uint32_t lf = __shfl_sync(0xffffffffu, lf_cur, src);
+                    uint32_t wt[4];
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) cb[b] = __shfl_sync(0xffffffffu, c[b], src);
+                    for (int i = 0; i < 4; ++i) wt[i] = __shfl_sync(0xffffffffu, wsp[i], src);
+                    const uint4* row = reinterpret_cast<const uint4*>(fc16 + size_t(lf) * 256) + cp * 4 + ch;
+                    uint4 fq[4];
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) wt[b] = __shfl_sync(0xffffffffu, wsp[b], src);
-                    uint4 fq[8];
-#pragma unroll
-                    for (int b = 0; b < 8; ++b)
-                        fq[b] = __ldg(reinterpret_cast<const uint4*>(fc16 + size_t(cb[b]) * 32) + ch);
+                    for (int i = 0; i < 4; ++i) fq[i] = __ldg(row + 8 * i);  // corner 2i + cp
                     H2 a1[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) a1[i] = F::splat(0.f);
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        const H2 pw = u2h<H2>(wt[b / 2]);
-                        const H2 hw = (b & 1) ? F::hi2(pw) : F::lo2(pw);
-                        const H2* f = reinterpret_cast<const H2*>(&fq[b]);
+                    for (int i = 0; i < 4; ++i) {
+                        const H2 pw = u2h<H2>(wt[i]);
+                        const H2 hw = cp ? F::hi2(pw) : F::lo2(pw);
+                        const H2* f = reinterpret_cast<const H2*>(&fq[i]);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) a1[i] = __hfma2(hw, f[i], a1[i]);
+                        for (int e = 0; e < 4; ++e) a1[e] = __hfma2(hw, f[e], a1[e]);
                     }
-                    st_shared_v4(a_base + a_off(32 * g + src, 8 * ch), h2u(a1[0]), h2u(a1[1]), h2u(a1[2]),
-                                 h2u(a1[3]));
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        a1[e] = __hadd2(a1[e], u2h<H2>(__shfl_xor_sync(0xffffffffu, h2u(a1[e]), 4)));
+                    if (cp == 0)
+                        st_shared_v4(a_base + a_off(32 * g + src, 8 * ch), h2u(a1[0]), h2u(a1[1]), h2u(a1[2]),
+                                     h2u(a1[3]));
                 }
                 st_shared_v4(a_base + a_off(32 * g + lane, 32), g0.x, g0.y, g0.z, F::kOne);
                 st_shared_v4(a_base + a_off(32 * g + lane, 40), 0u, 0u, 0u, 0u);
@@ -1154,13 +1154,23 @@ int g_num_sms = 0;
 
 }  // namespace
 
-size_t pack_tc_bytes(uint32_t V) { return OFF_FEAT + size_t(V) * 96 * 2; }
+// [weights | f_T 16-bit V x 64 | f_C 16-bit V x 32 | f_C per leaf: 8 corner rows, L x 8 x 32]
+size_t pack_leafc_offset(uint32_t V) { return OFF_FEAT + size_t(V) * 96 * 2; }
+size_t pack_tc_bytes(uint32_t V, uint32_t L) { return pack_leafc_offset(V) + size_t(L) * 8 * 32 * 2; }
 
-void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, bool bf16,
-                    cudaStream_t s) {
+// Per-leaf copy of the 8 corner rows of the 16-bit f_C features (512 contiguous
+// bytes per leaf), so the f_C gather reads whole 128-byte lines.
+__global__ void k_leaf_fc(const uint32_t* __restrict__ corners, const uint4* __restrict__ fc16, uint4* leafc,
+                          size_t words) {  // words = L * 8 corners * 4 (16-byte chunks of a 64-byte row)
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < words; i += size_t(gridDim.x) * blockDim.x)
+        leafc[i] = __ldg(fc16 + size_t(corners[i >> 2]) * 4 + (i & 3));
+}
+
+void ensure_pack_tc(const DevModel& M, const DevOctree& T, DevBuf& pack, uint64_t& pack_version, uint64_t version,
+                    bool bf16, cudaStream_t s) {
     const uint64_t tag = version | (bf16 ? (uint64_t(1) << 63) : 0);  // format in the top bit
     if (pack_version == tag && pack.p) return;
-    uint8_t* p = pack.ensure<uint8_t>(pack_tc_bytes(M.V));
+    uint8_t* p = pack.ensure<uint8_t>(pack_tc_bytes(M.V, T.n_leaves));
     const size_t nt = size_t(M.V) * 64, nc = size_t(M.V) * 32;
     const unsigned gt = unsigned((nt / 4 + 255) / 256 + 1), gc = unsigned((nc / 4 + 255) / 256 + 1);
     if (bf16) {
@@ -1176,7 +1186,12 @@ void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uin
         k_feat_cvt<false><<<gt, 256, 0, s>>>(M.ft, ft, nt);
         k_feat_cvt<false><<<gc, 256, 0, s>>>(M.fc, ft + nt, nc);
     }
-    note_launch(3);
+    const size_t words = size_t(T.n_leaves) * 8 * 4;
+    if (words)
+        k_leaf_fc<<<unsigned(std::min<size_t>((words + 255) / 256, 148 * 32)), 256, 0, s>>>(
+            T.corners, reinterpret_cast<const uint4*>(p + OFF_FEAT + size_t(M.V) * 64 * 2),
+            reinterpret_cast<uint4*>(p + pack_leafc_offset(M.V)), words);
+    note_launch(4);
     pack_version = tag;
 }
 
@@ -1206,7 +1221,8 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
                                                          cap, out, crec, err);
 #endif
 #if SVLF_DEC_C_TMEM
-    k_decode_c_tm<kBF16><<<g_num_sms, kCtThreads, CT_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
+    const H* leafc = reinterpret_cast<const H*>(p + pack_leafc_offset(M.V));
+    k_decode_c_tm<kBF16><<<g_num_sms, kCtThreads, CT_SM_TOTAL, s>>>(T, p, leafc, hit_leaf, crec, n_dev, cap, out);
 #else
     k_decode_c<kBF16><<<g_num_sms, kSlots * 128, C_SM_TOTAL, s>>>(T, p, fc, hit_leaf, crec, n_dev, cap, out);
 #endif

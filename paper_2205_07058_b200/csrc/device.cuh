@@ -147,8 +147,8 @@ void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const do
                       float* alpha, float* depth, unsigned long long* fg_count, bool exact, cudaStream_t s);
 
 // ---- tcgen05 decoder (decode_tc.cu)
-void ensure_pack_tc(const DevModel& M, DevBuf& pack, uint64_t& pack_version, uint64_t version, bool bf16,
-                    cudaStream_t s);
+void ensure_pack_tc(const DevModel& M, const DevOctree& T, DevBuf& pack, uint64_t& pack_version, uint64_t version,
+                    bool bf16, cudaStream_t s);
 // n_dev: device-side hit count (traversal counter), clamped to cap (buffer capacity)
 void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, bool bf16, const double* rays,
                       const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,
