@@ -981,30 +981,29 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
         for (uint32_t k = g; tile_of(k) < ntiles; k += TW_GROUPS) {
             const uint32_t e = k % TW_ENTRIES, use = k / TW_ENTRIES;
             const uint32_t j = tile_of(k) * 128 + row;
-            uint32_t corners[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             uint32_t r6p[3] = {0, 0, 0}, wp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             float u[6] = {0, 0, 0, 0, 0, 0};
             const uint32_t leaf = nleaf, ray_i = nray;
             const double tin = ntin, tout = ntout;
             prefetch(tile_of(k + TW_GROUPS));
-            if (j < n && SVLF_DEC_EXP != 3) {
-                load_corners(T, leaf, corners);
+            if (j < n && SVLF_DEC_EXP != 3)
                 hit_geom_regs<kBF16>(T, rays, ray_i, leaf, tin, tout, r6p, wp, u, err);
-            }
+            const uint32_t my_leaf = j < n ? leaf : 0u;
             if (use > 0) mbar_wait(&empty[e], (use - 1) & 1);
             const uint32_t a_base = sbase + TW_RING0 + e * TW_ENTRY;
             uint32_t* side = reinterpret_cast<uint32_t*>(sm + TW_RING0 + e * TW_ENTRY + T_A_BYTES);
 #pragma unroll 2
             for (uint32_t p = 0; p < (SVLF_DEC_EXP == 3 ? 0 : 8); ++p) {
                 const uint32_t src = 4 * p + q;
-                uint32_t cb[8], w[8];
-#pragma unroll
-                for (int b = 0; b < 8; ++b) cb[b] = __shfl_sync(0xffffffffu, corners[b], src);
+                const uint32_t lf = __shfl_sync(0xffffffffu, my_leaf, src);
+                uint32_t w[8];
 #pragma unroll
                 for (int b = 0; b < 8; ++b) w[b] = __shfl_sync(0xffffffffu, wp[b], src);
+                // the leaf's 8 corner rows are contiguous in the per-leaf table (1 KB per leaf)
+                const uint4* lrow = reinterpret_cast<const uint4*>(ft16 + size_t(lf) * 512) + ch;
                 uint4 fq[8];
 #pragma unroll
-                for (int b = 0; b < 8; ++b) fq[b] = __ldg(reinterpret_cast<const uint4*>(ft16 + size_t(cb[b]) * 64) + ch);
+                for (int b = 0; b < 8; ++b) fq[b] = __ldg(lrow + 8 * b);
                 H2 a1[4], a2[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) a1[i] = a2[i] = F::splat(0.f);
@@ -1156,14 +1155,16 @@ int g_num_sms = 0;
 
 // [weights | f_T 16-bit V x 64 | f_C 16-bit V x 32 | f_C per leaf: 8 corner rows, L x 8 x 32]
 size_t pack_leafc_offset(uint32_t V) { return OFF_FEAT + size_t(V) * 96 * 2; }
-size_t pack_tc_bytes(uint32_t V, uint32_t L) { return pack_leafc_offset(V) + size_t(L) * 8 * 32 * 2; }
+size_t pack_leaft_offset(uint32_t V, uint32_t L) { return pack_leafc_offset(V) + size_t(L) * 8 * 32 * 2; }
+size_t pack_tc_bytes(uint32_t V, uint32_t L) { return pack_leaft_offset(V, L) + size_t(L) * 8 * 64 * 2; }
 
 // Per-leaf copy of the 8 corner rows of the 16-bit f_C features (512 contiguous
 // bytes per leaf), so the f_C gather reads whole 128-byte lines.
-__global__ void k_leaf_fc(const uint32_t* __restrict__ corners, const uint4* __restrict__ fc16, uint4* leafc,
-                          size_t words) {  // words = L * 8 corners * 4 (16-byte chunks of a 64-byte row)
+template <uint32_t kChunks>  // 16-byte chunks per row: 4 (f_C, 64 B) or 8 (f_T, 128 B)
+__global__ void k_leaf_rows(const uint32_t* __restrict__ corners, const uint4* __restrict__ rows, uint4* leaf_rows,
+                            size_t words) {  // words = L * 8 corners * kChunks
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < words; i += size_t(gridDim.x) * blockDim.x)
-        leafc[i] = __ldg(fc16 + size_t(corners[i >> 2]) * 4 + (i & 3));
+        leaf_rows[i] = __ldg(rows + size_t(corners[i / kChunks]) * kChunks + (i % kChunks));
 }
 
 void ensure_pack_tc(const DevModel& M, const DevOctree& T, DevBuf& pack, uint64_t& pack_version, uint64_t version,
@@ -1187,11 +1188,15 @@ void ensure_pack_tc(const DevModel& M, const DevOctree& T, DevBuf& pack, uint64_
         k_feat_cvt<false><<<gc, 256, 0, s>>>(M.fc, ft + nt, nc);
     }
     const size_t words = size_t(T.n_leaves) * 8 * 4;
-    if (words)
-        k_leaf_fc<<<unsigned(std::min<size_t>((words + 255) / 256, 148 * 32)), 256, 0, s>>>(
-            T.corners, reinterpret_cast<const uint4*>(p + OFF_FEAT + size_t(M.V) * 64 * 2),
-            reinterpret_cast<uint4*>(p + pack_leafc_offset(M.V)), words);
-    note_launch(4);
+    if (words) {
+        const unsigned grid = unsigned(std::min<size_t>((words + 255) / 256, 148 * 32));
+        k_leaf_rows<4><<<grid, 256, 0, s>>>(T.corners, reinterpret_cast<const uint4*>(p + OFF_FEAT + size_t(M.V) * 64 * 2),
+                                           reinterpret_cast<uint4*>(p + pack_leafc_offset(M.V)), words);
+        k_leaf_rows<8><<<grid, 256, 0, s>>>(T.corners, reinterpret_cast<const uint4*>(p + OFF_FEAT),
+                                           reinterpret_cast<uint4*>(p + pack_leaft_offset(M.V, T.n_leaves)),
+                                           2 * words);
+    }
+    note_launch(5);
     pack_version = tag;
 }
 
@@ -1214,8 +1219,9 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
     const H* ft = reinterpret_cast<const H*>(p + OFF_FEAT);
     const H* fc = ft + size_t(M.V) * 64;
 #if SVLF_DEC_T_WS
-    k_decode_t_ws<kBF16><<<g_num_sms, TW_THREADS, TW_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout,
-                                                             n_dev, cap, out, crec, err);
+    const H* leaft = reinterpret_cast<const H*>(p + pack_leaft_offset(M.V, T.n_leaves));
+    k_decode_t_ws<kBF16><<<g_num_sms, TW_THREADS, TW_SM_TOTAL, s>>>(T, p, leaft, rays, hit_ray, hit_leaf, hit_tin,
+                                                                   hit_tout, n_dev, cap, out, crec, err);
 #else
     k_decode_t<kBF16><<<g_num_sms, kSlots * 128, T_SM_TOTAL, s>>>(T, p, ft, rays, hit_ray, hit_leaf, hit_tin, hit_tout, n_dev,
                                                          cap, out, crec, err);
