@@ -294,7 +294,6 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
         ctx.set_train_precision("fp32")
         return max_over_ranks(statistics.median(t), dist, device)
 
-    x3_step_ms = timed_mode("tf32x3")
     tf_step_ms = timed_mode("tf32")
     if world > 1:
         ctx.detach_nccl()
@@ -304,11 +303,8 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
            "rays": n, "active_hits": hits, "vertices": int(tree.vertex_count), "leaves": int(tree.leaf_count),
            "stages_ms": {k: round(statistics.median(p[k] for p in parts), 4)
                          for k in ("traverse_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms")},
-           "dtype": "fp32 dense layers (cuBLAS pedantic SGEMM) / f64 geometry and loss",
-           "tf32x3": {"value": round(world * n / (x3_step_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
-                      "ms_per_step": round(x3_step_ms, 4),
-                      "note": "every dense-layer GEMM on tensor cores as hi*hi + hi*lo + lo*hi of TF32 operand "
-                              "splits; meets the fp32 gates (loss 1e-6, gradients 1e-4)"},
+           "dtype": "fp32-accurate dense layers (3xTF32 split operands on tcgen05, this library's kernels; "
+                    "no cuBLAS) / f64 geometry and loss",
            "tf32": {"value": round(world * n / (tf_step_ms * 1e-3) / 1e6, 4), "unit": "Mrays/s",
                     "ms_per_step": round(tf_step_ms, 4),
                     "note": "weight-gradient GEMMs on tensor cores with TF32 operands (gradient gate 2e-2)"},
@@ -320,18 +316,11 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
     peaks, _ = load_peaks()
     flop = hits * 332544.0
     mhz = peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = 148 * 128 * 2 * mhz * 1e6 / 1e12  # CUDA-core fp32 FMA, nominal at the max SM clock
     tf32x3_peak = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]) / 2 / 3  # TF32 = half the bf16 rate, 3 products
-    for key, ms_, peak, bound in (("roofline", step_ms, fp32_peak, "fp32 CUDA cores (nominal peak)"),
-                                  ("tf32x3", x3_step_ms, tf32x3_peak,
-                                   "tensor, 3xTF32 (measured bf16 peak / 2 / 3)")):
-        ach = flop / (ms_ * 1e-3) / 1e12
-        r = {"bound": bound, "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
-             "frac": round(ach / peak, 4), "algorithmic": f"332544 FLOP/hit x {hits} active hits (whole step)"}
-        if key == "roofline":
-            out["roofline"] = r
-        else:
-            out["tf32x3"]["roofline"] = r
+    ach = flop / (step_ms * 1e-3) / 1e12
+    out["roofline"] = {"bound": "tensor, 3xTF32 (measured bf16 peak / 2 / 3)", "achieved": round(ach, 2),
+                       "peak": round(tf32x3_peak, 1), "unit": "TFLOP/s", "frac": round(ach / tf32x3_peak, 4),
+                       "algorithmic": f"332544 FLOP/hit x {hits} active hits (whole step)"}
     if cpu and world == 1:
         try:
             sys.path.insert(0, os.path.join(ROOT, "oracle"))

@@ -139,14 +139,15 @@ svlf_status svlf_ctx_last_timings(const svlf_ctx* ctx, svlf_timings* out);
  * last traversal (last band of a banded frame; 32-bit; synchronizes). */
 svlf_status svlf_ctx_set_node_test_counting(svlf_ctx* ctx, int enable);
 svlf_status svlf_ctx_last_node_tests(svlf_ctx* ctx, long long* out);
-/* Arithmetic of the train step's dense layers: SVLF_PRECISION_FP32 (default:
- * true fp32 CUDA-core GEMMs, gradients within 1e-4 of the reference),
- * SVLF_PRECISION_TF32X3 (every GEMM on tensor cores as hi*hi + hi*lo + lo*hi
- * of TF32 splits x = hi + lo, fp32 accumulation: the same fp32 gates; weight
- * gradients summed with fp32 atomics, so not bitwise reproducible) or
- * SVLF_PRECISION_TF32 (the weight-gradient GEMMs on tensor cores with plain
- * TF32 operands; forward and input gradients stay fp32; gradients within
- * 2e-2, the 16-bit tolerance of SURVEY.md §8(c)). */
+/* Arithmetic of the train step's dense layers (no cuBLAS: this library's
+ * tcgen05 kernels, gemm_x3.cu): SVLF_PRECISION_FP32 (default) and
+ * SVLF_PRECISION_TF32X3 both run every GEMM on the tensor cores as
+ * hi*lo + lo*hi + hi*hi of TF32 splits x = hi + lo with fp32 accumulation
+ * (fp32-level accuracy: gradients within 1e-4 rel-L2 of the reference);
+ * weight gradients are reduced in a fixed CTA order, so steps are bitwise
+ * reproducible run to run. SVLF_PRECISION_TF32 runs the weight-gradient
+ * reductions with plain TF32 operands (gradients within 2e-2, the 16-bit
+ * tolerance of SURVEY.md §8(c)). */
 svlf_status svlf_ctx_set_train_precision(svlf_ctx* ctx, svlf_precision precision);
 /* Count of this library's kernel launches on the context since creation. */
 long long svlf_ctx_kernel_launches(const svlf_ctx* ctx);
@@ -168,6 +169,15 @@ svlf_status svlf_host_free(void* p);
 svlf_status svlf_nccl_unique_id(void* out128);
 svlf_status svlf_ctx_attach_nccl(svlf_ctx* ctx, const void* unique_id128, int rank, int world);
 svlf_status svlf_ctx_detach_nccl(svlf_ctx* ctx);
+/* The same exchange through a host callback (gloo, MPI, a test harness)
+ * instead of NCCL: the library copies each buffer to page-locked host memory,
+ * calls fn to all-reduce it in place across the `world` ranks (every rank
+ * calls fn the same number of times with the same counts, in the same order),
+ * and copies it back. fn returns 0 on success. */
+typedef enum svlf_dtype { SVLF_DTYPE_F32 = 0, SVLF_DTYPE_F64 = 1, SVLF_DTYPE_U8 = 2 } svlf_dtype;
+typedef enum svlf_reduce_op { SVLF_REDUCE_SUM = 0, SVLF_REDUCE_MAX = 1 } svlf_reduce_op;
+typedef int (*svlf_allreduce_fn)(void* user, void* host_buf, size_t count, svlf_dtype dtype, svlf_reduce_op op);
+svlf_status svlf_ctx_attach_collective(svlf_ctx* ctx, svlf_allreduce_fn fn, void* user, int rank, int world);
 
 /* ---- octree: SparseOctree::build / from_leaves (octree.hpp:47,82; src/octree.cpp:30-142)
  * ctx may be NULL: the octree is then host-only and is uploaded to the device
@@ -215,6 +225,10 @@ svlf_status svlf_model_get_grads(svlf_model* model, float* feat_t, float* feat_c
 svlf_status svlf_model_get_adam(svlf_model* model, float* m_all, float* v_all, uint64_t* steps);
 svlf_status svlf_model_set_adam(svlf_model* model, const float* m_all, const float* v_all,
                                 const uint64_t* steps);
+/* AdamState::beta1 / beta2 / eps of the 14 tensors (mlp.hpp:117-128; same
+ * order); the defaults are 0.9f / 0.999f / 1e-8f, svlf_model_init resets them. */
+svlf_status svlf_model_set_adam_hyper(svlf_model* model, const float* beta1, const float* beta2, const float* eps);
+svlf_status svlf_model_get_adam_hyper(svlf_model* model, float* beta1, float* beta2, float* eps);
 size_t svlf_model_param_count(const svlf_model* model);
 
 /* ---- render: render_frame(model, camera, out, stats, background) (render.hpp:104-105;

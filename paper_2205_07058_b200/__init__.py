@@ -157,6 +157,8 @@ class LossStats:
 
 # ---- library loading -----------------------------------------------------------
 _LIB = None
+# int (*)(void* user, void* host_buf, size_t count, svlf_dtype, svlf_reduce_op)
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int)
 
 
 def library_path() -> str:
@@ -203,6 +205,9 @@ def load_library():
         "svlf_nccl_unique_id": ([vp], st),
         "svlf_ctx_attach_nccl": ([vp, vp, C.c_int, C.c_int], st),
         "svlf_ctx_detach_nccl": ([vp], st),
+        "svlf_ctx_attach_collective": ([vp, _ALLREDUCE_FN, vp, C.c_int, C.c_int], st),
+        "svlf_model_set_adam_hyper": ([vp, vp, vp, vp], st),
+        "svlf_model_get_adam_hyper": ([vp, vp, vp, vp], st),
         "svlf_octree_build": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
         "svlf_octree_build_device": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
         "svlf_octree_from_leaves": ([vp, C.POINTER(_Grid), vp, sz, C.POINTER(vp)], st),
@@ -321,9 +326,10 @@ class Context:
         return int(load_library().svlf_ctx_kernel_launches(None))
 
     def set_train_precision(self, precision: str):
-        """Dense-layer GEMMs of the train step: 'fp32' (default, true fp32 on CUDA cores),
-        'tf32x3' (tensor cores, three TF32 products of split operands: fp32-level accuracy) or
-        'tf32' (weight-gradient GEMMs on tensor cores with plain TF32 operands)."""
+        """Dense-layer GEMMs of the train step, all on this library's tcgen05 kernels:
+        'fp32' (default) / 'tf32x3' (three TF32 products of split operands: fp32-level
+        accuracy, deterministic) or 'tf32' (weight-gradient reductions with plain TF32
+        operands: 16-bit tolerance)."""
         _check(_LIB.svlf_ctx_set_train_precision(self._h, {**_PREC, "tf32": 3, "tf32x3": 4}[precision]))
 
     def attach_nccl(self, unique_id: bytes, rank: int, world: int):
@@ -334,6 +340,28 @@ class Context:
 
     def detach_nccl(self):
         _check(_LIB.svlf_ctx_detach_nccl(self._h))
+
+    def attach_host_collective(self, allreduce, rank: int, world: int):
+        """Data-parallel training over a host-side all-reduce instead of NCCL:
+        `allreduce(buf, op)` reduces the numpy array `buf` in place across the
+        ranks (op 'sum' or 'max'); e.g. torch.distributed over gloo
+        (parallel.init_data_parallel_host)."""
+        dtypes = {0: np.float32, 1: np.float64, 2: np.uint8}
+
+        def tramp(_user, ptr, count, dtype, op):
+            try:
+                dt = np.dtype(dtypes[dtype])
+                buf = np.frombuffer((C.c_char * (count * dt.itemsize)).from_address(ptr), dtype=dt, count=count)
+                allreduce(buf, "sum" if op == 0 else "max")
+                return 0
+            except BaseException:  # noqa: BLE001 - reported to the library as a failed exchange
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        cb = _ALLREDUCE_FN(tramp)
+        _check(_LIB.svlf_ctx_attach_collective(self._h, cb, None, rank, world))
+        self._collective_cb = cb  # kept alive with the context
 
 
 class _PinnedBlock:
@@ -567,6 +595,16 @@ class Model:
         m, v = _f32(m), _f32(v)
         steps = np.ascontiguousarray(steps, dtype=np.uint64)
         _check(_LIB.svlf_model_set_adam(self._h, _dp(m), _dp(v), _dp(steps)))
+
+    def get_adam_hyper(self):
+        """(beta1, beta2, eps) of the 14 Adam tensors (AdamState fields)."""
+        b1, b2, e = (np.zeros(14, np.float32) for _ in range(3))
+        _check(_LIB.svlf_model_get_adam_hyper(self._h, _dp(b1), _dp(b2), _dp(e)))
+        return b1, b2, e
+
+    def set_adam_hyper(self, beta1, beta2, eps):
+        arrs = [np.ascontiguousarray(np.broadcast_to(np.asarray(a, np.float32), (14,))) for a in (beta1, beta2, eps)]
+        _check(_LIB.svlf_model_set_adam_hyper(self._h, *[_dp(a) for a in arrs]))
 
 
 _PREC = {"fp32": 0, "bf16": 1, "fp16": 2}

@@ -177,6 +177,7 @@ uint64_t fingerprint(const ModelAdam& a) {
     for (const AdamState* s : adam_tensors(a)) {
         h = fold_vec(fold_vec(h, s->m), s->v);
         h = fold(h, &s->step, 8);
+        h = fold(fold(fold(h, &s->beta1, 4), &s->beta2, 4), &s->eps, 4);
     }
     return h;
 }
@@ -209,20 +210,27 @@ void upload_adam(svlf_model* dm, const ModelAdam& a, size_t total) {
     m.reserve(total);
     v.reserve(total);
     uint64_t steps[14];
+    float b1[14], b2[14], eps[14];
     for (size_t i = 0; i < 14; ++i) {
         m.insert(m.end(), ts[i]->m.begin(), ts[i]->m.end());
         v.insert(v.end(), ts[i]->v.begin(), ts[i]->v.end());
         steps[i] = ts[i]->step;
+        b1[i] = ts[i]->beta1;
+        b2[i] = ts[i]->beta2;
+        eps[i] = ts[i]->eps;
     }
     if (m.size() != total || v.size() != total) throw std::invalid_argument("ModelAdam does not match the model");
     detail::check(svlf_model_set_adam(dm, m.data(), v.data(), steps));
+    detail::check(svlf_model_set_adam_hyper(dm, b1, b2, eps));
 }
 
 void download_adam(svlf_model* dm, const SvlfModel& model, ModelAdam& a) {
     const size_t total = svlf_model_param_count(dm);
     std::vector<float> m(total), v(total);
     uint64_t steps[14];
+    float b1[14], b2[14], eps[14];
     detail::check(svlf_model_get_adam(dm, m.data(), v.data(), steps));
+    detail::check(svlf_model_get_adam_hyper(dm, b1, b2, eps));
     a = ModelAdam::like(model);
     std::vector<AdamState*> ts{&a.feat_thickness, &a.feat_color};
     for (auto& s : a.dec_thickness) ts.push_back(&s);
@@ -233,6 +241,9 @@ void download_adam(svlf_model* dm, const SvlfModel& model, ModelAdam& a) {
         std::copy_n(m.begin() + off, n, ts[i]->m.begin());
         std::copy_n(v.begin() + off, n, ts[i]->v.begin());
         ts[i]->step = steps[i];
+        ts[i]->beta1 = b1[i];
+        ts[i]->beta2 = b2[i];
+        ts[i]->eps = eps[i];
         off += n;
     }
 }

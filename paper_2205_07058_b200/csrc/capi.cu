@@ -63,12 +63,57 @@ struct DeviceGuard {
     }
 };
 
+// Data-parallel exchange over an NCCL communicator (NVLink / NVSwitch).
+struct NcclCollective final : Collective {
+    ncclComm_t comm = nullptr;
+    ~NcclCollective() override {
+        if (comm) nccl_api().CommDestroy(comm);
+    }
+    void allreduce(void* dev, size_t count, CollType t, CollOp op, cudaStream_t s) override {
+        const ncclDataType_t dt = t == CollType::F32 ? ncclFloat32 : t == CollType::F64 ? ncclFloat64 : ncclUint8;
+        nccl_check(nccl_api().AllReduce(dev, dev, count, dt, op == CollOp::Sum ? ncclSum : ncclMax, comm, s));
+    }
+};
+
+// Host-staged exchange: the buffer is copied to page-locked memory, reduced in
+// place by a host callback (gloo, MPI, a test harness), and copied back. Used
+// where the ranks are not on NVLink peers; synchronizes the stream per call.
+struct HostCollective final : Collective {
+    svlf_allreduce_fn fn = nullptr;
+    void* user = nullptr;
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+    ~HostCollective() override {
+        if (stage) cudaFreeHost(stage);
+    }
+    void allreduce(void* dev, size_t count, CollType t, CollOp op, cudaStream_t s) override {
+        const size_t esz = t == CollType::F32 ? 4 : t == CollType::F64 ? 8 : 1;
+        const size_t bytes = count * esz;
+        if (!bytes) return;
+        SVLF_CUDA(cudaStreamSynchronize(s));  // the previous call's copy-back has landed
+        if (bytes > stage_bytes) {
+            if (stage) SVLF_CUDA(cudaFreeHost(stage));
+            stage = nullptr;
+            stage_bytes = 0;
+            SVLF_CUDA(cudaMallocHost(&stage, bytes));
+            stage_bytes = bytes;
+        }
+        SVLF_CUDA(cudaMemcpyAsync(stage, dev, bytes, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        const svlf_dtype dt = t == CollType::F32 ? SVLF_DTYPE_F32 : t == CollType::F64 ? SVLF_DTYPE_F64 : SVLF_DTYPE_U8;
+        const int rc = fn(user, stage, count, dt, op == CollOp::Sum ? SVLF_REDUCE_SUM : SVLF_REDUCE_MAX);
+        if (rc != 0) fail(SVLF_ERR_RUNTIME, "all-reduce callback failed");
+        SVLF_CUDA(cudaMemcpyAsync(dev, stage, bytes, cudaMemcpyHostToDevice, s));
+    }
+};
+
 const char* dev_error_message(int code) {
     switch (code) {
         case kErrTangentRay: return "tangent ray";
         case kErrPointNotInVoxel: return "point not in voxel";
         case kErrSurfaceOutside: return "surface point outside voxel";
         case kErrNegativeTau: return "negative optical thickness";
+        case -1: return "device error on another rank";
         default: return "device error";
     }
 }
@@ -90,9 +135,8 @@ struct svlf_ctx {
     size_t hit_cap = 0;
     long long last_overflow_rays = 0;  // rays that reached the per-ray fallback walker
     long long last_dense_rays = 0;     // rays re-run by the second (16-ray) cooperative pass
-    ncclComm_t nccl = nullptr;          // data-parallel communicator (optional)
-    bool train_tf32 = false;            // train-step weight-gradient GEMMs on tensor cores (TF32)
-    bool train_tf32x3 = false;          // every train-step GEMM as split 3xTF32 on tensor cores
+    std::unique_ptr<Collective> coll;   // data-parallel exchange (optional): NCCL or host-staged
+    bool train_tf32 = false;            // train-step weight-gradient GEMMs with plain TF32 operands
     bool count_node_tests = false;      // traversal variant that counts ray-box tests (diagnostics)
     int rank = 0, world = 1;
     TrainScratch train;
@@ -146,6 +190,7 @@ struct svlf_model {
     size_t n_ft = 0, n_fc = 0, n_total = 0;
     DevBuf params, grads, adam_m, adam_v, pack_f32, pack_bf16;
     uint64_t steps[14] = {};
+    AdamHyper hyper[14];
     uint64_t version = 1, pack_f32_version = 0, pack_bf16_version = 0;
 
     float* p() const { return params.as<float>(); }
@@ -634,7 +679,7 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
         {
             DeviceGuard g(ctx->device);
             cudaStreamSynchronize(ctx->stream);
-            if (ctx->nccl) nccl_api().CommDestroy(ctx->nccl);
+            ctx->coll.reset();
             cudaStreamSynchronize(ctx->copy_stream);
             for (auto& e : ctx->ev) cudaEventDestroy(e);
             for (auto& fs : ctx->slot) {
@@ -771,11 +816,34 @@ svlf_status svlf_ctx_attach_nccl(svlf_ctx* ctx, const void* id128, int rank, int
         require(world >= 1 && rank >= 0 && rank < world, "bad rank/world");
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
-        if (ctx->nccl) nccl_api().CommDestroy(ctx->nccl);
-        ctx->nccl = nullptr;
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->coll.reset();
         ncclUniqueId id;
         std::memcpy(&id, id128, sizeof id);
-        nccl_check(nccl_api().CommInitRank(&ctx->nccl, world, id, rank));
+        auto c = std::make_unique<NcclCollective>();
+        nccl_check(nccl_api().CommInitRank(&c->comm, world, id, rank));
+        c->rank = rank;
+        c->world = world;
+        ctx->coll = std::move(c);
+        ctx->rank = rank;
+        ctx->world = world;
+    });
+}
+
+svlf_status svlf_ctx_attach_collective(svlf_ctx* ctx, svlf_allreduce_fn fn, void* user, int rank, int world) {
+    return guard([&] {
+        require(ctx && fn, "null argument");
+        require(world >= 1 && rank >= 0 && rank < world, "bad rank/world");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->coll.reset();
+        auto c = std::make_unique<HostCollective>();
+        c->fn = fn;
+        c->user = user;
+        c->rank = rank;
+        c->world = world;
+        ctx->coll = std::move(c);
         ctx->rank = rank;
         ctx->world = world;
     });
@@ -786,8 +854,8 @@ svlf_status svlf_ctx_detach_nccl(svlf_ctx* ctx) {
         require(ctx != nullptr, "ctx is null");
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
-        if (ctx->nccl) nccl_api().CommDestroy(ctx->nccl);
-        ctx->nccl = nullptr;
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->coll.reset();
         ctx->rank = 0;
         ctx->world = 1;
     });
@@ -811,7 +879,6 @@ svlf_status svlf_ctx_set_train_precision(svlf_ctx* ctx, svlf_precision precision
             fail(SVLF_ERR_INVALID_ARGUMENT, "train precision must be fp32, tf32x3 or tf32");
         std::lock_guard<std::mutex> lk(ctx->mu);
         ctx->train_tf32 = precision == SVLF_PRECISION_TF32;
-        ctx->train_tf32x3 = precision == SVLF_PRECISION_TF32X3;
     });
 }
 
@@ -1020,10 +1087,12 @@ svlf_status svlf_model_create(svlf_ctx* ctx, const svlf_octree* tree, svlf_model
         m->n_ft = size_t(m->V) * SVLF_FEAT_T_DIM;
         m->n_fc = size_t(m->V) * SVLF_FEAT_C_DIM;
         m->n_total = model_param_count(m->V);
+        std::lock_guard<std::mutex> lk(ctx->mu);
         for (DevBuf* b : {&m->params, &m->grads, &m->adam_m, &m->adam_v}) {
             b->ensure<float>(m->n_total);
-            SVLF_CUDA(cudaMemset(b->p, 0, m->n_total * 4));
+            SVLF_CUDA(cudaMemsetAsync(b->p, 0, m->n_total * 4, ctx->stream));
         }
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
         *out = m.release();
     });
 }
@@ -1066,36 +1135,46 @@ svlf_status svlf_model_init(svlf_model* m, uint64_t seed) {
         mlp(host.data() + m->n_ft + m->n_fc, dt, 2, root.sub(kStreamDecT).next_u64());
         mlp(host.data() + m->n_ft + m->n_fc + SVLF_DEC_T_SIZE, dc, 4, root.sub(kStreamDecC).next_u64());
         DeviceGuard g(m->ctx->device);
-        SVLF_CUDA(cudaMemcpy(m->params.p, host.data(), m->n_total * 4, cudaMemcpyHostToDevice));
-        for (DevBuf* b : {&m->grads, &m->adam_m, &m->adam_v}) SVLF_CUDA(cudaMemset(b->p, 0, m->n_total * 4));
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
+        cudaStream_t s = m->ctx->stream;
+        SVLF_CUDA(cudaMemcpyAsync(m->params.p, host.data(), m->n_total * 4, cudaMemcpyHostToDevice, s));
+        for (DevBuf* b : {&m->grads, &m->adam_m, &m->adam_v}) SVLF_CUDA(cudaMemsetAsync(b->p, 0, m->n_total * 4, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
         std::fill(std::begin(m->steps), std::end(m->steps), 0);
+        std::fill(std::begin(m->hyper), std::end(m->hyper), AdamHyper{});
         ++m->version;
     });
 }
 
+// Host <-> device copies of a model's tensors, ordered on the context stream
+// after any enqueued work that uses them (frames in flight, train steps) and
+// complete on return. The caller holds ctx->mu.
 static void copy_params(svlf_model* m, DevBuf& buf, float* ft, float* fc, float* dt, float* dc, bool to_dev,
                         const float* sft = nullptr, const float* sfc = nullptr, const float* sdt = nullptr,
                         const float* sdc = nullptr) {
     DeviceGuard g(m->ctx->device);
+    cudaStream_t s = m->ctx->stream;
     float* base = buf.as<float>();
     const size_t sizes[4] = {m->n_ft, m->n_fc, SVLF_DEC_T_SIZE, SVLF_DEC_C_SIZE};
     size_t off = 0;
     for (int i = 0; i < 4; ++i) {
         if (to_dev) {
             const float* src = i == 0 ? sft : i == 1 ? sfc : i == 2 ? sdt : sdc;
-            if (src) SVLF_CUDA(cudaMemcpy(base + off, src, sizes[i] * 4, cudaMemcpyHostToDevice));
+            if (src) SVLF_CUDA(cudaMemcpyAsync(base + off, src, sizes[i] * 4, cudaMemcpyHostToDevice, s));
         } else {
             float* dst = i == 0 ? ft : i == 1 ? fc : i == 2 ? dt : dc;
-            if (dst) SVLF_CUDA(cudaMemcpy(dst, base + off, sizes[i] * 4, cudaMemcpyDeviceToHost));
+            if (dst) SVLF_CUDA(cudaMemcpyAsync(dst, base + off, sizes[i] * 4, cudaMemcpyDeviceToHost, s));
         }
         off += sizes[i];
     }
+    SVLF_CUDA(cudaStreamSynchronize(s));
 }
 
 svlf_status svlf_model_set_params(svlf_model* m, const float* ft, const float* fc, const float* dt,
                                   const float* dc) {
     return guard([&] {
         require(m != nullptr, "model is null");
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
         copy_params(m, m->params, nullptr, nullptr, nullptr, nullptr, true, ft, fc, dt, dc);
         ++m->version;
     });
@@ -1104,7 +1183,7 @@ svlf_status svlf_model_set_params(svlf_model* m, const float* ft, const float* f
 svlf_status svlf_model_get_params(svlf_model* m, float* ft, float* fc, float* dt, float* dc) {
     return guard([&] {
         require(m != nullptr, "model is null");
-        SVLF_CUDA(cudaStreamSynchronize(m->ctx->stream));
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
         copy_params(m, m->params, ft, fc, dt, dc, false);
     });
 }
@@ -1112,7 +1191,7 @@ svlf_status svlf_model_get_params(svlf_model* m, float* ft, float* fc, float* dt
 svlf_status svlf_model_get_grads(svlf_model* m, float* ft, float* fc, float* dt, float* dc) {
     return guard([&] {
         require(m != nullptr, "model is null");
-        SVLF_CUDA(cudaStreamSynchronize(m->ctx->stream));
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
         copy_params(m, m->grads, ft, fc, dt, dc, false);
     });
 }
@@ -1121,9 +1200,11 @@ svlf_status svlf_model_get_adam(svlf_model* m, float* m_all, float* v_all, uint6
     return guard([&] {
         require(m != nullptr, "model is null");
         DeviceGuard g(m->ctx->device);
-        SVLF_CUDA(cudaStreamSynchronize(m->ctx->stream));
-        if (m_all) SVLF_CUDA(cudaMemcpy(m_all, m->adam_m.p, m->n_total * 4, cudaMemcpyDeviceToHost));
-        if (v_all) SVLF_CUDA(cudaMemcpy(v_all, m->adam_v.p, m->n_total * 4, cudaMemcpyDeviceToHost));
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
+        cudaStream_t s = m->ctx->stream;
+        if (m_all) SVLF_CUDA(cudaMemcpyAsync(m_all, m->adam_m.p, m->n_total * 4, cudaMemcpyDeviceToHost, s));
+        if (v_all) SVLF_CUDA(cudaMemcpyAsync(v_all, m->adam_v.p, m->n_total * 4, cudaMemcpyDeviceToHost, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
         if (steps) std::memcpy(steps, m->steps, sizeof m->steps);
     });
 }
@@ -1132,9 +1213,32 @@ svlf_status svlf_model_set_adam(svlf_model* m, const float* m_all, const float* 
     return guard([&] {
         require(m != nullptr, "model is null");
         DeviceGuard g(m->ctx->device);
-        if (m_all) SVLF_CUDA(cudaMemcpy(m->adam_m.p, m_all, m->n_total * 4, cudaMemcpyHostToDevice));
-        if (v_all) SVLF_CUDA(cudaMemcpy(m->adam_v.p, v_all, m->n_total * 4, cudaMemcpyHostToDevice));
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
+        cudaStream_t s = m->ctx->stream;
+        if (m_all) SVLF_CUDA(cudaMemcpyAsync(m->adam_m.p, m_all, m->n_total * 4, cudaMemcpyHostToDevice, s));
+        if (v_all) SVLF_CUDA(cudaMemcpyAsync(m->adam_v.p, v_all, m->n_total * 4, cudaMemcpyHostToDevice, s));
+        SVLF_CUDA(cudaStreamSynchronize(s));
         if (steps) std::memcpy(m->steps, steps, sizeof m->steps);
+    });
+}
+
+svlf_status svlf_model_set_adam_hyper(svlf_model* m, const float* beta1, const float* beta2, const float* eps) {
+    return guard([&] {
+        require(m && beta1 && beta2 && eps, "null argument");
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
+        for (int i = 0; i < 14; ++i) m->hyper[i] = AdamHyper{beta1[i], beta2[i], eps[i]};
+    });
+}
+
+svlf_status svlf_model_get_adam_hyper(svlf_model* m, float* beta1, float* beta2, float* eps) {
+    return guard([&] {
+        require(m && beta1 && beta2 && eps, "null argument");
+        std::lock_guard<std::mutex> lk(m->ctx->mu);
+        for (int i = 0; i < 14; ++i) {
+            beta1[i] = m->hyper[i].beta1;
+            beta2[i] = m->hyper[i].beta2;
+            eps[i] = m->hyper[i].eps;
+        }
     });
 }
 
@@ -1261,20 +1365,43 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
             SVLF_CUDA(cudaMemcpyAsync(d_alpha, alpha_gt, size_t(nn), kind, s));
         }
     }
-    const uint32_t total = nn ? run_traversal(ctx, m->tree, nullptr, 0, 0, nn) : 0;
-    float trav_ms = 0.f;
-    if (nn) cudaEventElapsedTime(&trav_ms, ctx->ev[EV_START], ctx->ev[EV_EMIT]);
-    TrainBatchDev b{d_rays, d_cgt, d_depth, d_alpha, nn, ctx->offsets.as<uint32_t>(), ctx->counts.as<uint32_t>(),
-                    ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), total};
-    TrainOptions opt{mode == SVLF_LOSS_SURFACE, color_frozen != 0, adam, *lw, lr, ctx->nccl, ctx->world,
-                     ctx->train_tf32, ctx->train_tf32x3};
-    ensure_pack_f32(m, s);
+    // Traversal and step are enqueued with no host round trip; the step's one
+    // readback reports a hit-buffer or exchange-buffer overflow (any rank), in
+    // which case nothing was updated and the whole step is re-run with larger
+    // buffers.
+    TrainOptions opt{mode == SVLF_LOSS_SURFACE, color_frozen != 0, adam, *lw, lr, ctx->coll.get(), ctx->train_tf32};
     TrainModelRefs mr{m->view(), m->params.as<float>(), m->grads.as<float>(), m->adam_m.as<float>(),
-                      m->adam_v.as<float>(), m->n_ft, m->n_fc, m->steps, pack_f32_view(m->pack_f32.as<float>())};
-    TrainResult r = run_train_step(S, dev_view(m->tree), mr, b, opt, s, ctx->misc.as<int>());
+                      m->adam_v.as<float>(), m->n_ft, m->n_fc, m->steps, m->hyper};
+    TrainResult r;
+    float trav_ms = 0.f;
+    for (int attempt = 0;; ++attempt) {
+        if (nn) {
+            enqueue_traversal(ctx, m->tree, nullptr, 0, 0, nn);
+        } else {
+            ctx->hit_cap = std::max<size_t>(ctx->hit_cap, 32);
+            ctx->hit_leaf.ensure<uint32_t>(ctx->hit_cap);
+            ctx->hit_tin.ensure<double>(ctx->hit_cap);
+            ctx->hit_tout.ensure<double>(ctx->hit_cap);
+            SVLF_CUDA(cudaMemsetAsync(traversal_counters(ctx), 0, 32, s));
+        }
+        TrainBatchDev b{d_rays, d_cgt, d_depth, d_alpha, nn, ctx->offsets.ensure<uint32_t>(size_t(nn) + 1),
+                        ctx->counts.ensure<uint32_t>(size_t(nn) + 1), ctx->hit_leaf.as<uint32_t>(),
+                        ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), traversal_counters(ctx),
+                        uint32_t(ctx->hit_cap)};
+        r = run_train_step(S, dev_view(m->tree), mr, b, opt, s, ctx->misc.as<int>());
+        if (nn) cudaEventElapsedTime(&trav_ms, ctx->ev[EV_START], ctx->ev[EV_EMIT]);
+        if (r.error || !r.flags) break;
+        if (attempt >= 3) fail(SVLF_ERR_RUNTIME, "train step buffers could not be sized");
+        if ((r.flags & kStepHitOverflow) && r.hits > ctx->hit_cap)  // else the step grew its own matrices
+            ctx->hit_cap = std::min<size_t>(size_t(r.hits) + r.hits / 4 + 1024, 0xfffff000u);
+    }
     r.timings.traverse_ms = trav_ms;
     if (r.error) fail(SVLF_ERR_RUNTIME, dev_error_message(r.error));
-    if (adam) ++m->version;
+    if (r.updated) {  // the Adam steps that ran (colour tensors frozen: not advanced)
+        for (int i = 0; i < 14; ++i)
+            if (!color_frozen || !(i == 1 || i >= 6)) ++m->steps[i];
+        ++m->version;
+    }
     ctx->last = r.timings;
     if (stats) {
         stats->rays += r.rays;

@@ -1,6 +1,8 @@
 // 3xTF32 tensor-core GEMMs of the train step's dense layers (gemm_x3.cu).
 // Matrices are feature-major (row = one feature over all hits, row stride ld,
 // 16-byte aligned rows); weights are the reference's row-major [O][K].
+// Hit counts are read on the device (n_dev, clamped to cap), so a train step
+// enqueues every GEMM without a host round trip.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -10,16 +12,38 @@
 
 namespace svlfb {
 
-// bytes of the per-call weight image for a reduction length kred
+// One weight operand image: B[j][k] = W[j][k] (forward, j < O, k < K) or
+// B[j][k] = W[k][k0 + j] (input gradient, j < K - k0, k < O), split into TF32
+// hi / lo parts in the kernels' shared-memory layout, 128 rows x 32-K chunks.
+struct X3ImageJob {
+    const float* W;
+    uint32_t O, K, k0;
+    uint32_t bwd;
+};
+constexpr int kX3MaxJobs = 8;
+struct X3ImageJobs {
+    X3ImageJob job[kX3MaxJobs];
+    uint32_t offset[kX3MaxJobs];  // byte offset of each image in the buffer
+    int count;
+};
+// bytes of one image with reduction length kred
 size_t gemm_x3_image_bytes(uint32_t kred);
-// y[j][:] = relu(sum_k W[j][k] x[k][:] + bias[j]), j < O, k < K
-void gemm_x3_fwd(const float* x, const float* W, const float* bias, float* y, uint32_t O, uint32_t K, uint32_t n,
-                 uint32_t ld, uint8_t* img, cudaStream_t s);
-// dx[j][:] = sum_o W[o][k0 + j] d[o][:], j < K - k0; zeroed where mask[j][:] <= 0 (mask may be null)
-void gemm_x3_bwd(const float* d, const float* W, uint32_t O, uint32_t K, uint32_t k0, float* dx, const float* mask,
-                 uint32_t n, uint32_t ld, uint8_t* img, cudaStream_t s);
-// dW[o][k] = sum_n d[o][n] x[k][n], db[o] = sum_n d[o][n] (overwritten)
-void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* dW, float* db, uint32_t n,
-                uint32_t ld, cudaStream_t s);
+// builds every image of `jobs` (offsets filled in here) into buf with one launch
+void gemm_x3_build_images(X3ImageJobs& jobs, uint8_t* buf, cudaStream_t s);
+
+// y[j][:] = relu(sum_k W[j][k] x[k][:] + bias[j]), j < O, k < K; img from a forward job
+void gemm_x3_fwd(const float* x, const uint8_t* img, const float* bias, float* y, uint32_t O, uint32_t K,
+                 const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s);
+// dx[j][:] = sum_o W[o][k0 + j] d[o][:], j < K - k0; zeroed where mask[j][:] <= 0 (mask may be
+// null); img from a backward job
+void gemm_x3_bwd(const float* d, const uint8_t* img, uint32_t O, uint32_t K, uint32_t k0, float* dx,
+                 const float* mask, const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s);
+// dW[o][k] = sum_n d[o][n] x[k][n], db[o] = sum_n d[o][n] (overwritten). Each CTA reduces a
+// contiguous hit range into its own partial (part: gemm_x3_dw_partial_floats floats) and the
+// partials are summed in CTA order, so the result is bitwise reproducible. products = 3
+// (hi*lo + lo*hi + hi*hi: fp32-level accuracy) or 1 (plain TF32).
+size_t gemm_x3_dw_partial_floats(uint32_t O, uint32_t K);
+void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* dW, float* db, const uint32_t* n_dev,
+                uint32_t cap, uint32_t ld, float* part, int products, cudaStream_t s);
 
 }  // namespace svlfb

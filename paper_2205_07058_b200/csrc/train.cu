@@ -8,29 +8,34 @@
 //              "surface point outside voxel" check, active hit range per mode
 //              (stage 1 keeps pre-surface + surface hits, or the surface hit
 //              only when lambda_empty == 0), skipped / eta_skipped counters.
-//   scan/expand  dense list of active hits.
+//   scan/expand  dense list of active hits (its length stays on the device).
 //   forward    per hit: f_T input column (geometry, trilinear gathers);
-//              dense layers as GEMMs on feature-major activation matrices
-//              (cuBLAS SGEMM in pedantic fp32, or the 3xTF32 tensor-core
-//              kernels of gemm_x3.cu) + bias/relu epilogue;
-//              per hit: f_T heads, x_s, f_C input column; f_C layers as
-//              GEMMs; per hit: rgb head. Activations kept for backward.
+//              dense layers as 3xTF32 tensor-core GEMMs (gemm_x3.cu) with the
+//              bias + relu epilogue fused; per hit: f_T heads, x_s, f_C input
+//              column; f_C layers; per hit: rgb head. Activations kept for
+//              backward.
 //   k_loss     per ray: Eq. 4 surface loss or composite + volumetric loss in
 //              fp64 and the composite backward dtau_j = dw_j T_j e_j -
 //              sum_{i>j} dw_i w_i (reverse scan), per-ray loss.
-//   backward   per hit: f_C head; GEMMs dX = W^T D with relu masks; per hit:
-//              colour-feature scatter (unless frozen), positional Jacobian
-//              d eta += <dx_s, x1 - x2>, f_T heads; GEMM dX_T; per hit:
-//              thickness-feature scatter (atomics); weight gradients
-//              dW = D X^T and db = D 1 as GEMM/GEMV over all hits.
+//   backward   per hit: f_C head; GEMMs dX = W^T D with fused relu masks; per
+//              hit: colour-feature scatter (unless frozen), positional
+//              Jacobian d eta += <dx_s, x1 - x2>, f_T heads; GEMM dX_T; per
+//              hit: thickness-feature scatter; weight gradients dW = D X^T and
+//              db = D 1 as deterministic (CTA-ordered) tensor-core reductions.
+//   exchange   (data parallel) loss/statistics, decoder gradients and the
+//              union of touched feature rows all-reduced (Collective).
 //   k_adam     dense bias-corrected Adam in fp64 over every parameter
-//              (src/mlp.cpp:277-296), colour tensors skipped when frozen.
+//              (src/mlp.cpp:277-296), colour tensors skipped when frozen;
+//              skipped on the device when the step raised an error or
+//              overflowed a buffer on any rank.
 // Gradients are sums over rays (no 1/N), as in the reference.
+//
+// Nothing in the step reads a count on the host: every per-hit kernel reads
+// the active-hit count from the device and loops over it (grids sized by the
+// hit capacity), and the single host synchronisation is the final readback
+// of one small status record.
 #include <cmath>
 #include <cstring>
-
-#include "cublas_dyn.hpp"
-#include "nccl_dyn.hpp"
 
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -45,10 +50,21 @@ namespace svlfb {
 
 namespace {
 
-// feature-major activation rows (x N hits)
+// feature-major activation rows (x ld hits)
 constexpr int A_XT = 0, A_HT = 134, A_XC = 262, A_H1 = 300, A_H2 = 428, A_H3 = 556, A_ROWS = 684;
 // feature-major delta rows (dL/d pre-activation of each layer)
 constexpr int D_T0 = 0, D_T1 = 128, D_C0 = 130, D_C1 = 258, D_C2 = 386, D_C3 = 514, D_ROWS = 517;
+
+enum : uint32_t { kStepDeviceError = 4u };
+
+// Status record read back once per step.
+struct StepMail {
+    double loss, skipped, eta_skipped, rays;
+    uint32_t err, flags, hits, active, rows, pad;
+};
+
+// red[]: the all-reduced (data parallel) per-step scalars
+enum { R_LOSS, R_SKIPPED, R_ETA_SKIPPED, R_RAYS, R_OVERFLOW, R_ERROR, R_COUNT };
 
 struct PrepArgs {
     const double* rays;
@@ -60,6 +76,7 @@ struct PrepArgs {
     const uint32_t* hit_leaf;
     const double* hit_tin;
     const double* hit_tout;
+    const uint32_t* trav_counters;  // [2] != 0: the traversal overflowed its capacity
     bool surface;
     bool empty_zero;
     uint32_t* act_first;
@@ -83,6 +100,13 @@ __device__ __forceinline__ Ray ray_of(const double* rays, uint32_t i) {
 __global__ void k_prep(DevOctree T, PrepArgs A, int* err) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= A.n) return;
+    if (A.trav_counters[2]) {  // hit lists incomplete: the step is a no-op and is re-run
+        A.act_first[r] = 0;
+        A.act_cnt[r] = 0;
+        A.surf_rel[r] = -1;
+        A.eta_gt[r] = 0.0;
+        return;
+    }
     const uint32_t off = A.ray_off[r], cnt = A.ray_cnt[r];
     int surf = -1;
     double eg = 0.0;
@@ -139,17 +163,6 @@ __global__ void k_prep(DevOctree T, PrepArgs A, int* err) {
     A.eta_gt[r] = eg;
 }
 
-__global__ void k_expand(uint32_t n, const uint32_t* act_first, const uint32_t* act_cnt, const uint32_t* dpos,
-                         uint32_t* dhit, uint32_t* dray) {
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const uint32_t b = dpos[r], f = act_first[r];
-    for (uint32_t k = 0; k < act_cnt[r]; ++k) {
-        dhit[b + k] = f + k;
-        dray[b + k] = r;
-    }
-}
-
 struct HitArgs {
     const double* rays;
     const uint32_t* hit_leaf;
@@ -159,23 +172,44 @@ struct HitArgs {
     const uint32_t* dray;
     const uint32_t* dpos;
     const int* surf_rel;
-    uint32_t N;
-    uint32_t ld;    // row stride of acts / deltas / dX: N rounded up to 32 (aligned GEMM operands)
+    const uint32_t* n_dev;  // active hits (dpos[n]), read on the device
+    uint32_t cap;           // capacity of every per-hit buffer (>= the active hits)
+    uint32_t ld;            // row / channel stride of the per-hit matrices: cap rounded up to 32
     bool surface;
     float* acts;    // A_ROWS x ld
     float* deltas;  // D_ROWS x ld
     float* tau;
     float* eta;
-    float* rgb;     // 3 x N (channel-major)
-    float* drgb;    // 3 x N
+    float* rgb;     // 3 x ld (channel-major)
+    float* drgb;    // 3 x ld
     double* dtau;
     double* deta;
 };
+
+__device__ __forceinline__ uint32_t active_hits(const HitArgs& H) { return min(*H.n_dev, H.cap); }
 
 __device__ __forceinline__ bool has_color(const HitArgs& H, uint32_t j) {
     if (!H.surface) return true;
     const uint32_t r = H.dray[j];
     return H.surf_rel[r] >= 0 && j == H.dpos[r] + uint32_t(H.surf_rel[r]);
+}
+
+// dense active-hit list; zeroes the per-hit loss gradients of each active hit
+__global__ void k_expand(uint32_t n, const uint32_t* act_first, const uint32_t* act_cnt, const uint32_t* dpos,
+                         HitArgs H, uint32_t* dhit, uint32_t* dray) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t b = dpos[r], f = act_first[r], cnt = act_cnt[r];
+    for (uint32_t k = 0; k < cnt && b + k < H.cap; ++k) {
+        const uint32_t j = b + k;
+        dhit[j] = f + k;
+        dray[j] = r;
+        H.dtau[j] = 0.0;
+        H.deta[j] = 0.0;
+        H.drgb[j] = 0.f;
+        H.drgb[H.ld + j] = 0.f;
+        H.drgb[2 * size_t(H.ld) + j] = 0.f;
+    }
 }
 
 // Per-hit geometry shared by forward and backward.
@@ -233,71 +267,64 @@ __device__ __forceinline__ void weights_from_u(const double* u, float* w) {
 
 // ---- forward ------------------------------------------------------------------
 // The dense layers are GEMMs over the feature-major activation matrices
-// (cuBLAS SGEMM, fp32; see run_train_step); these kernels are the per-hit
-// parts around them.
+// (gemm_x3.cu); these kernels are the per-hit parts around them. The
+// warp-cooperative kernels loop over 32-hit warp tiles up to the device-side
+// active count.
 
 // f_T input column: [r6 | psi_T(x1) | psi_T(x2)] (voxel_batch.hpp:69-96).
-// Warp-cooperative: a warp owns 32 consecutive hits (geometry lane = hit); each
-// hit's 8 corner rows are read coalesced (lane = 2 features), accumulated in
-// the reference's corner order without FMA, staged transposed in shared
-// memory and written row by row (coalesced feature-major stores).
+// A warp owns 32 consecutive hits (geometry lane = hit); each hit's 8 corner
+// rows are read coalesced (lane = 2 features), accumulated in the reference's
+// corner order without FMA, staged transposed in shared memory and written
+// row by row (coalesced feature-major stores).
 constexpr int kInWarps = 2;
 __global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevModel M, HitArgs H, int* err) {
     __shared__ float st[kInWarps][2 * kFt][33];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t N = H.N;
-    const size_t L = H.ld;  // row stride of the feature-major matrices
-    const uint32_t j0 = (blockIdx.x * kInWarps + warp) * 32;
-    if (j0 >= N) return;
-    const uint32_t j = j0 + lane;
-    HitGeom g;
-    const bool ok = j < N && hit_geom(T, H, j, g, err);
-    float* X = H.acts + j;
-    if (j < N)
+    const uint32_t N = active_hits(H);
+    const size_t L = H.ld;
+    for (uint32_t tile = blockIdx.x * kInWarps + warp; tile * 32 < N; tile += gridDim.x * kInWarps) {
+        const uint32_t j = tile * 32 + lane;
+        HitGeom g;
+        const bool ok = j < N && hit_geom(T, H, j, g, err);
+        float* X = H.acts + j;
+        if (j < N)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) X[(A_XT + k) * L] = ok ? g.r6[k] : 0.f;
-    uint32_t cs[8];
-    float w1[8], w2[8];
+            for (int k = 0; k < 6; ++k) X[(A_XT + k) * L] = ok ? g.r6[k] : 0.f;
+        uint32_t cs[8];
+        float w1[8], w2[8];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        cs[b] = ok ? g.corners[b] : 0u;
-        w1[b] = ok ? g.w1[b] : 0.f;
-        w2[b] = ok ? g.w2[b] : 0.f;
-    }
-    const unsigned live = __ballot_sync(0xffffffffu, ok);
-    const uint32_t d = 2 * lane;
-    for (int h = 0; h < 32; ++h) {
-        float2 a1 = make_float2(0.f, 0.f), a2 = a1;
-        if ((live >> h) & 1u) {
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
-                const float wa = __shfl_sync(0xffffffffu, w1[b], h), wb = __shfl_sync(0xffffffffu, w2[b], h);
-                const float2 v = __ldg(reinterpret_cast<const float2*>(M.ft + size_t(c) * kFt) + lane);
-                a1.x = __fadd_rn(a1.x, __fmul_rn(wa, v.x));
-                a1.y = __fadd_rn(a1.y, __fmul_rn(wa, v.y));
-                a2.x = __fadd_rn(a2.x, __fmul_rn(wb, v.x));
-                a2.y = __fadd_rn(a2.y, __fmul_rn(wb, v.y));
-            }
+        for (int b = 0; b < 8; ++b) {
+            cs[b] = ok ? g.corners[b] : 0u;
+            w1[b] = ok ? g.w1[b] : 0.f;
+            w2[b] = ok ? g.w2[b] : 0.f;
         }
-        st[warp][d][h] = a1.x;
-        st[warp][d + 1][h] = a1.y;
-        st[warp][kFt + d][h] = a2.x;
-        st[warp][kFt + d + 1][h] = a2.y;
-    }
-    __syncwarp();
-    if (j < N)
+        const unsigned live = __ballot_sync(0xffffffffu, ok);
+        const uint32_t d = 2 * lane;
+        __syncwarp();
+        for (int h = 0; h < 32; ++h) {
+            float2 a1 = make_float2(0.f, 0.f), a2 = a1;
+            if ((live >> h) & 1u) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
+                    const float wa = __shfl_sync(0xffffffffu, w1[b], h), wb = __shfl_sync(0xffffffffu, w2[b], h);
+                    const float2 v = __ldg(reinterpret_cast<const float2*>(M.ft + size_t(c) * kFt) + lane);
+                    a1.x = __fadd_rn(a1.x, __fmul_rn(wa, v.x));
+                    a1.y = __fadd_rn(a1.y, __fmul_rn(wa, v.y));
+                    a2.x = __fadd_rn(a2.x, __fmul_rn(wb, v.x));
+                    a2.y = __fadd_rn(a2.y, __fmul_rn(wb, v.y));
+                }
+            }
+            st[warp][d][h] = a1.x;
+            st[warp][d + 1][h] = a1.y;
+            st[warp][kFt + d][h] = a2.x;
+            st[warp][kFt + d + 1][h] = a2.y;
+        }
+        __syncwarp();
+        if (j < N)
 #pragma unroll 8
-        for (int r = 0; r < 2 * kFt; ++r) X[(A_XT + 6 + r) * L] = st[warp][r][lane];
-}
-
-// y = relu(y + b[row]) over a rows x N feature-major block (GEMM epilogue)
-__global__ void k_bias_relu(float* __restrict__ Y, const float* __restrict__ bias, size_t N, size_t ld) {
-    const uint32_t row = blockIdx.y;
-    const float b = __ldg(bias + row);
-    float* y = Y + size_t(row) * ld;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < N; i += size_t(gridDim.x) * blockDim.x)
-        y[i] = fmaxf(y[i] + b, 0.f);
+            for (int r = 0; r < 2 * kFt; ++r) X[(A_XT + 6 + r) * L] = st[warp][r][lane];
+    }
 }
 
 // f_T head (tau relu, eta sigmoid), x_s and the f_C input column
@@ -308,85 +335,86 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel
     using D = DecOffsets;
     __shared__ float st[kInWarps][kFc][33];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t N = H.N;
-    const size_t L = H.ld;  // row stride of the feature-major matrices
-    const uint32_t j0 = (blockIdx.x * kInWarps + warp) * 32;
-    if (j0 >= N) return;
-    const uint32_t j = j0 + lane;
-    const bool valid = j < N;
-    float* X = H.acts + j;
-    float eta = 0.5f;
-    if (valid) {
-        const float* h = X + A_HT * L;
-        float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
+    const uint32_t N = active_hits(H);
+    const size_t L = H.ld;
+    for (uint32_t tile = blockIdx.x * kInWarps + warp; tile * 32 < N; tile += gridDim.x * kInWarps) {
+        const uint32_t j = tile * 32 + lane;
+        const bool valid = j < N;
+        float* X = H.acts + j;
+        float eta = 0.5f;
+        if (valid) {
+            const float* h = X + A_HT * L;
+            float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
 #pragma unroll 16
-        for (int k = 0; k < kHid; ++k) {
-            const float v = __ldg(h + size_t(k) * L);
-            y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
-            y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
+            for (int k = 0; k < kHid; ++k) {
+                const float v = __ldg(h + size_t(k) * L);
+                y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
+                y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
+            }
+            eta = sigmoid_ref(y1);
+            H.tau[j] = y0 > 0.f ? y0 : 0.f;
+            H.eta[j] = eta;
         }
-        eta = sigmoid_ref(y1);
-        H.tau[j] = y0 > 0.f ? y0 : 0.f;
-        H.eta[j] = eta;
-    }
-    bool ok = false;
-    HitGeom g;
-    float ws[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (valid && has_color(H, j) && hit_geom(T, H, j, g, err)) {
-        double xs[3], u[3];
-        if (!xs_coords(T, g, eta, xs, u)) {
-            raise_error(err, kErrPointNotInVoxel);
-        } else {
-            weights_from_u(u, ws);
-            ok = true;
-        }
-    }
-    if (valid)
-#pragma unroll
-        for (int k = 0; k < 6; ++k) X[(A_XC + k) * L] = ok ? g.r6[k] : 0.f;
-    uint32_t cs[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) cs[b] = ok ? g.corners[b] : 0u;
-    const unsigned live = __ballot_sync(0xffffffffu, ok);
-    for (int h = 0; h < 32; ++h) {
-        float acc = 0.f;
-        if ((live >> h) & 1u) {
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {  // corner order, no FMA: interp_into_column (voxel_batch.hpp:22-37)
-                const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
-                const float w = __shfl_sync(0xffffffffu, ws[b], h);
-                acc = __fadd_rn(acc, __fmul_rn(w, __ldg(M.fc + size_t(c) * kFc + lane)));
+        bool ok = false;
+        HitGeom g;
+        float ws[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (valid && has_color(H, j) && hit_geom(T, H, j, g, err)) {
+            double xs[3], u[3];
+            if (!xs_coords(T, g, eta, xs, u)) {
+                raise_error(err, kErrPointNotInVoxel);
+            } else {
+                weights_from_u(u, ws);
+                ok = true;
             }
         }
-        st[warp][lane][h] = acc;
-    }
-    __syncwarp();
-    if (valid)
+        if (valid)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) X[(A_XC + k) * L] = ok ? g.r6[k] : 0.f;
+        uint32_t cs[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) cs[b] = ok ? g.corners[b] : 0u;
+        const unsigned live = __ballot_sync(0xffffffffu, ok);
+        __syncwarp();
+        for (int h = 0; h < 32; ++h) {
+            float acc = 0.f;
+            if ((live >> h) & 1u) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {  // corner order, no FMA: interp_into_column (voxel_batch.hpp:22-37)
+                    const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
+                    const float w = __shfl_sync(0xffffffffu, ws[b], h);
+                    acc = __fadd_rn(acc, __fmul_rn(w, __ldg(M.fc + size_t(c) * kFc + lane)));
+                }
+            }
+            st[warp][lane][h] = acc;
+        }
+        __syncwarp();
+        if (valid)
 #pragma unroll 8
-        for (int r = 0; r < kFc; ++r) X[(A_XC + 6 + r) * L] = st[warp][r][lane];
+            for (int r = 0; r < kFc; ++r) X[(A_XC + 6 + r) * L] = st[warp][r][lane];
+    }
 }
 
 // f_C head: rgb = sigmoid(W3 h3 + b3)
 __global__ void __launch_bounds__(128) k_fwd_rgb(DevModel M, HitArgs H) {
     using D = DecOffsets;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= H.N) return;
-    const size_t N = H.N;
-    const size_t L = H.ld;  // row stride of the feature-major matrices
-    if (!has_color(H, j)) {
-        for (int c = 0; c < 3; ++c) H.rgb[c * N + j] = 0.f;
-        return;
-    }
-    const float* h = H.acts + A_H3 * L + j;
-    float y[3] = {__ldg(M.mc + D::C_B3), __ldg(M.mc + D::C_B3 + 1), __ldg(M.mc + D::C_B3 + 2)};
+    const uint32_t N = active_hits(H);
+    const size_t L = H.ld;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+        if (!has_color(H, j)) {
+            for (int c = 0; c < 3; ++c) H.rgb[c * L + j] = 0.f;
+            continue;
+        }
+        const float* h = H.acts + A_H3 * L + j;
+        float y[3] = {__ldg(M.mc + D::C_B3), __ldg(M.mc + D::C_B3 + 1), __ldg(M.mc + D::C_B3 + 2)};
 #pragma unroll 16
-    for (int k = 0; k < kHid; ++k) {
-        const float v = __ldg(h + size_t(k) * L);
+        for (int k = 0; k < kHid; ++k) {
+            const float v = __ldg(h + size_t(k) * L);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) y[c] = fmaf(__ldg(M.mc + D::C_W3 + c * kHid + k), v, y[c]);
+            for (int c = 0; c < 3; ++c) y[c] = fmaf(__ldg(M.mc + D::C_W3 + c * kHid + k), v, y[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) H.rgb[c * L + j] = sigmoid_ref(y[c]);
     }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) H.rgb[c * N + j] = sigmoid_ref(y[c]);
 }
 
 // ---- loss + composite backward (per ray) ---------------------------------------
@@ -397,7 +425,6 @@ struct LossArgs {
     const uint32_t* act_cnt;
     const int* surf_rel;
     const double* eta_gt;
-    const double* hit_tin;  // unused: t_s is not part of the loss
     uint32_t n;
     bool surface;
     svlf_loss_weights lw;
@@ -410,8 +437,9 @@ struct LossArgs {
 __global__ void k_loss(LossArgs L, HitArgs H) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= L.n) return;
-    const size_t N = H.N;
-    const uint32_t b = L.dpos[r], cnt = L.act_cnt[r];
+    const size_t S = H.ld;
+    const uint32_t b = L.dpos[r];
+    const uint32_t cnt = b < H.cap ? min(L.act_cnt[r], H.cap - b) : 0u;
     const int srel = L.surf_rel[r];
     const double eg = L.eta_gt[r];
     double loss = 0.0;
@@ -425,7 +453,7 @@ __global__ void k_loss(LossArgs L, HitArgs H) {
         const uint32_t js = b + uint32_t(srel);
         double dc[3];
         for (int ch = 0; ch < 3; ++ch) {
-            const double diff = dsub(double(H.rgb[ch * N + js]), cg[ch]);
+            const double diff = dsub(double(H.rgb[ch * S + js]), cg[ch]);
             loss = dadd(loss, dmul(diff, diff));
             dc[ch] = dmul(2.0, diff);
         }
@@ -442,7 +470,7 @@ __global__ void k_loss(LossArgs L, HitArgs H) {
             loss = dadd(loss, dmul(dmul(L.lw.empty, olap), olap));
             H.dtau[j] = dadd(H.dtau[j], dmul(dmul(dmul(2.0, L.lw.empty), olap), e));
         }
-        for (int ch = 0; ch < 3; ++ch) H.drgb[ch * N + js] = float(dc[ch]);
+        for (int ch = 0; ch < 3; ++ch) H.drgb[ch * S + js] = float(dc[ch]);
         L.ray_loss[r] = loss;
         return;
     }
@@ -455,7 +483,7 @@ __global__ void k_loss(LossArgs L, HitArgs H) {
         L.ehit[j] = e;
         L.trans[j] = Tr;
         L.wgt[j] = w;
-        for (int ch = 0; ch < 3; ++ch) color[ch] = dadd(color[ch], dmul(w, double(H.rgb[ch * N + j])));
+        for (int ch = 0; ch < 3; ++ch) color[ch] = dadd(color[ch], dmul(w, double(H.rgb[ch * S + j])));
         alpha = dadd(alpha, w);
         Tr = dmul(Tr, e);
     }
@@ -468,7 +496,7 @@ __global__ void k_loss(LossArgs L, HitArgs H) {
     const double agt = L.alpha[r] ? 1.0 : 0.0;
     loss = dadd(loss, dmul(dmul(L.lw.alpha, dsub(alpha, agt)), dsub(alpha, agt)));
     const double d_alpha = dmul(dmul(2.0, L.lw.alpha), dsub(alpha, agt));
-    if (L.alpha[r] && srel >= 0) {
+    if (L.alpha[r] && srel >= 0 && uint32_t(srel) < cnt) {
         const uint32_t js = b + uint32_t(srel);
         const double ediff = dsub(double(H.eta[js]), eg);
         loss = dadd(loss, dmul(dmul(L.lw.eta, ediff), ediff));
@@ -478,58 +506,64 @@ __global__ void k_loss(LossArgs L, HitArgs H) {
     for (int64_t k = int64_t(cnt) - 1; k >= 0; --k) {
         const uint32_t j = b + uint32_t(k);
         double dw = d_alpha;
-        for (int ch = 0; ch < 3; ++ch) dw = dadd(dw, dmul(d_color[ch], double(H.rgb[ch * N + j])));
+        for (int ch = 0; ch < 3; ++ch) dw = dadd(dw, dmul(d_color[ch], double(H.rgb[ch * S + j])));
         H.dtau[j] = dadd(H.dtau[j], dsub(dmul(dmul(dw, L.trans[j]), L.ehit[j]), suffix));
         suffix = dadd(suffix, dmul(dw, L.wgt[j]));
-        for (int ch = 0; ch < 3; ++ch) H.drgb[ch * N + j] = float(dmul(L.wgt[j], d_color[ch]));
+        for (int ch = 0; ch < 3; ++ch) H.drgb[ch * S + j] = float(dmul(L.wgt[j], d_color[ch]));
     }
     L.ray_loss[r] = loss;
 }
 
+// Per-step scalars: red[R_LOSS] is summed by cub (deterministic), the rest here.
+// Overflow: the traversal exceeded the hit buffers, or the active hits
+// exceeded the per-hit matrices (act_cap); either way nothing is updated.
+__global__ void k_step_scalars(uint32_t n, const unsigned long long* counters, const uint32_t* trav_counters,
+                               const uint32_t* n_act, uint32_t act_cap, const int* err, double* red) {
+    red[R_SKIPPED] = double(counters[0]);
+    red[R_ETA_SKIPPED] = double(counters[1]);
+    red[R_RAYS] = double(n);
+    red[R_OVERFLOW] = (trav_counters[2] || *n_act > act_cap) ? 1.0 : 0.0;
+    red[R_ERROR] = *err ? 1.0 : 0.0;
+}
+
 // ---- backward -----------------------------------------------------------------
-// Layer deltas D (dL/d pre-activation, feature-major) flow through cuBLAS
-// GEMMs dX = W^T D; these kernels are the per-hit heads, relu masks and the
-// feature-gradient scatters (src/mlp.cpp:151-230, src/train.cpp:243-285).
+// Layer deltas D (dL/d pre-activation, feature-major) flow through the GEMMs
+// dX = W^T D; these kernels are the per-hit heads and the feature-gradient
+// scatters (src/mlp.cpp:151-230, src/train.cpp:243-285).
 
 // f_C head (sigmoid') and its 3 -> 128 back-projection masked by relu'(h3)
 __global__ void __launch_bounds__(128) k_bwd_head_c(DevModel M, HitArgs H) {
     using D = DecOffsets;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= H.N) return;
-    const size_t N = H.N;
-    const size_t L = H.ld;  // row stride of the feature-major matrices
-    float* Dl = H.deltas + j;
-    float d3[3] = {0.f, 0.f, 0.f};
-    if (has_color(H, j))
-        for (int o = 0; o < 3; ++o) {
-            const float a = H.rgb[o * N + j];
-            d3[o] = H.drgb[o * N + j] * a * (1.0f - a);
-        }
-#pragma unroll
-    for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * L] = d3[o];
-    const float* h3 = H.acts + A_H3 * L + j;
-    for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
-        float hv[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) hv[i] = __ldg(h3 + size_t(k0 + i) * L);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int k = k0 + i;
-            float v = 0.f;
-            if (hv[i] > 0.f) {
-                v = __ldg(M.mc + D::C_W3 + k) * d3[0];
-                v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
-                v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
+    const uint32_t N = active_hits(H);
+    const size_t L = H.ld;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+        float* Dl = H.deltas + j;
+        float d3[3] = {0.f, 0.f, 0.f};
+        if (has_color(H, j))
+            for (int o = 0; o < 3; ++o) {
+                const float a = H.rgb[o * L + j];
+                d3[o] = H.drgb[o * L + j] * a * (1.0f - a);
             }
-            Dl[(D_C2 + k) * L] = v;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * L] = d3[o];
+        const float* h3 = H.acts + A_H3 * L + j;
+        for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
+            float hv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) hv[i] = __ldg(h3 + size_t(k0 + i) * L);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int k = k0 + i;
+                float v = 0.f;
+                if (hv[i] > 0.f) {
+                    v = __ldg(M.mc + D::C_W3 + k) * d3[0];
+                    v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
+                    v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
+                }
+                Dl[(D_C2 + k) * L] = v;
+            }
         }
     }
-}
-
-// D *= relu'(H) over a rows x N block
-__global__ void k_relu_mask(float* __restrict__ Dm, const float* __restrict__ Hm, size_t count) {
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x)
-        if (!(Hm[i] > 0.f)) Dm[i] = 0.f;
 }
 
 // The two feature-gradient kernels below are warp-cooperative: a warp owns 32
@@ -551,100 +585,101 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevMo
     __shared__ float ws_s[kScWarps][32][8];
     __shared__ double dots[kScWarps][32][8];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t N = H.N;
-    const size_t L = H.ld;  // row stride of the feature-major matrices
-    const uint32_t j0 = (blockIdx.x * kScWarps + warp) * 32;
-    if (j0 >= N) return;
-    const uint32_t j = j0 + lane;
-    const bool valid = j < N;
-    HitGeom g;
-    double u[3] = {0.0, 0.0, 0.0};
-    bool act = valid && has_color(H, j) && hit_geom(T, H, j, g, err);
-    if (act) {
-        double xs[3];
-        if (!xs_coords(T, g, H.eta[j], xs, u)) {
-            raise_error(err, kErrPointNotInVoxel);
-            act = false;
-        }
-    }
-    {
-        float ws[8];
-        if (act) weights_from_u(u, ws);
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            cs[warp][lane][b] = act ? g.corners[b] : 0u;
-            ws_s[warp][lane][b] = act ? ws[b] : 0.f;
-        }
-    }
-#pragma unroll 4
-    for (int d = 0; d < kFc; ++d) zs[warp][d][lane] = act ? dX[(6 + d) * L + j] : 0.f;
-    __syncwarp();
-    unsigned live = __ballot_sync(0xffffffffu, act);
-    // scatter + <z_b, dz> per corner, hit by hit
-    const uint32_t grp = lane >> 3, f4 = (lane & 7) * 4;   // scatter: corner grp (+4), features f4..f4+3
-    const uint32_t cb = lane >> 2, ck = (lane & 3) * 8;    // dots: corner cb, features ck..ck+7
-    while (live) {
-        const int h = __ffs(live) - 1;
-        live &= live - 1;
-        if (!color_frozen) {
-#pragma unroll
-            for (int bp = 0; bp < 2; ++bp) {
-                const uint32_t b = grp + 4 * bp;
-                const float w = ws_s[warp][h][b];
-                const float4 v = make_float4(w * zs[warp][f4][h], w * zs[warp][f4 + 1][h], w * zs[warp][f4 + 2][h],
-                                             w * zs[warp][f4 + 3][h]);
-                atomicAdd(reinterpret_cast<float4*>(g_fc + size_t(cs[warp][h][b]) * kFc + f4), v);
+    const uint32_t N = active_hits(H);
+    const size_t L = H.ld;
+    for (uint32_t tile = blockIdx.x * kScWarps + warp; tile * 32 < N; tile += gridDim.x * kScWarps) {
+        const uint32_t j = tile * 32 + lane;
+        const bool valid = j < N;
+        HitGeom g;
+        double u[3] = {0.0, 0.0, 0.0};
+        bool act = valid && has_color(H, j) && hit_geom(T, H, j, g, err);
+        if (act) {
+            double xs[3];
+            if (!xs_coords(T, g, H.eta[j], xs, u)) {
+                raise_error(err, kErrPointNotInVoxel);
+                act = false;
             }
         }
-        const float4* zb = reinterpret_cast<const float4*>(M.fc + size_t(cs[warp][h][cb]) * kFc + ck);
-        const float4 za = __ldg(zb), zc = __ldg(zb + 1);
-        const float zv[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
-        double part = 0.0;
+        __syncwarp();
+        {
+            float ws[8];
+            if (act) weights_from_u(u, ws);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) part = dadd(part, dmul(double(zv[i]), double(zs[warp][ck + i][h])));
-        part = dadd(part, __shfl_xor_sync(0xffffffffu, part, 1));
-        part = dadd(part, __shfl_xor_sync(0xffffffffu, part, 2));
-        if ((lane & 3) == 0) dots[warp][h][cb] = part;
-    }
-    __syncwarp();
-    double deta = valid ? H.deta[j] : 0.0;
-    if (act) {
-        // dx_s = sum_b dw_b/du <z_b, dz> / h; d eta += <dx_s, x1 - x2>
-        const double inv_h = ddiv(1.0, T.cell_size);
-        const double wxv[2] = {dsub(1.0, u[0]), u[0]}, wyv[2] = {dsub(1.0, u[1]), u[1]},
-                     wzv[2] = {dsub(1.0, u[2]), u[2]}, dxv[2] = {-1.0, 1.0};
-        double dxs[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
-            const double gw[3] = {dmul(dmul(dxv[bx], wyv[by]), wzv[bz]), dmul(dmul(wxv[bx], dxv[by]), wzv[bz]),
-                                  dmul(dmul(wxv[bx], wyv[by]), dxv[bz])};
-            const double sc = dmul(dots[warp][lane][b], inv_h);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) dxs[a] = dadd(dxs[a], dmul(gw[a], sc));
+            for (int b = 0; b < 8; ++b) {
+                cs[warp][lane][b] = act ? g.corners[b] : 0u;
+                ws_s[warp][lane][b] = act ? ws[b] : 0.f;
+            }
         }
-        const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
-        deta = dadd(deta, dot3(dxs, dx12));
-    }
-    if (!valid) return;
-    // f_T heads: relu (tau), sigmoid (eta)
-    float* Dl = H.deltas + j;
-    const float tau = H.tau[j], eta = H.eta[j];
-    const float d0 = tau > 0.f ? float(H.dtau[j]) : 0.f;
-    const float d1 = float(deta) * eta * (1.0f - eta);
-    Dl[D_T1 * L] = d0;
-    Dl[(D_T1 + 1) * L] = d1;
-    const float* ht = H.acts + A_HT * L + j;
-    for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
-        float hv[16];
+#pragma unroll 4
+        for (int d = 0; d < kFc; ++d) zs[warp][d][lane] = act ? dX[(6 + d) * L + j] : 0.f;
+        __syncwarp();
+        unsigned live = __ballot_sync(0xffffffffu, act);
+        // scatter + <z_b, dz> per corner, hit by hit
+        const uint32_t grp = lane >> 3, f4 = (lane & 7) * 4;  // scatter: corner grp (+4), features f4..f4+3
+        const uint32_t cb = lane >> 2, ck = (lane & 3) * 8;   // dots: corner cb, features ck..ck+7
+        while (live) {
+            const int h = __ffs(live) - 1;
+            live &= live - 1;
+            if (!color_frozen) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) hv[i] = __ldg(ht + size_t(k0 + i) * L);
+                for (int bp = 0; bp < 2; ++bp) {
+                    const uint32_t b = grp + 4 * bp;
+                    const float w = ws_s[warp][h][b];
+                    const float4 v = make_float4(w * zs[warp][f4][h], w * zs[warp][f4 + 1][h],
+                                                 w * zs[warp][f4 + 2][h], w * zs[warp][f4 + 3][h]);
+                    atomicAdd(reinterpret_cast<float4*>(g_fc + size_t(cs[warp][h][b]) * kFc + f4), v);
+                }
+            }
+            const float4* zb = reinterpret_cast<const float4*>(M.fc + size_t(cs[warp][h][cb]) * kFc + ck);
+            const float4 za = __ldg(zb), zc = __ldg(zb + 1);
+            const float zv[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
+            double part = 0.0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int k = k0 + i;
-            float v = 0.f;
-            if (hv[i] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
-            Dl[(D_T0 + k) * L] = v;
+            for (int i = 0; i < 8; ++i) part = dadd(part, dmul(double(zv[i]), double(zs[warp][ck + i][h])));
+            part = dadd(part, __shfl_xor_sync(0xffffffffu, part, 1));
+            part = dadd(part, __shfl_xor_sync(0xffffffffu, part, 2));
+            if ((lane & 3) == 0) dots[warp][h][cb] = part;
+        }
+        __syncwarp();
+        double deta = valid ? H.deta[j] : 0.0;
+        if (act) {
+            // dx_s = sum_b dw_b/du <z_b, dz> / h; d eta += <dx_s, x1 - x2>
+            const double inv_h = ddiv(1.0, T.cell_size);
+            const double wxv[2] = {dsub(1.0, u[0]), u[0]}, wyv[2] = {dsub(1.0, u[1]), u[1]},
+                         wzv[2] = {dsub(1.0, u[2]), u[2]}, dxv[2] = {-1.0, 1.0};
+            double dxs[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
+                const double gw[3] = {dmul(dmul(dxv[bx], wyv[by]), wzv[bz]), dmul(dmul(wxv[bx], dxv[by]), wzv[bz]),
+                                      dmul(dmul(wxv[bx], wyv[by]), dxv[bz])};
+                const double sc = dmul(dots[warp][lane][b], inv_h);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) dxs[a] = dadd(dxs[a], dmul(gw[a], sc));
+            }
+            const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
+            deta = dadd(deta, dot3(dxs, dx12));
+        }
+        if (!valid) continue;
+        // f_T heads: relu (tau), sigmoid (eta)
+        float* Dl = H.deltas + j;
+        const float tau = H.tau[j], eta = H.eta[j];
+        const float d0 = tau > 0.f ? float(H.dtau[j]) : 0.f;
+        const float d1 = float(deta) * eta * (1.0f - eta);
+        Dl[D_T1 * L] = d0;
+        Dl[(D_T1 + 1) * L] = d1;
+        const float* ht = H.acts + A_HT * L + j;
+        for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
+            float hv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) hv[i] = __ldg(ht + size_t(k0 + i) * L);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int k = k0 + i;
+                float v = 0.f;
+                if (hv[i] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
+                Dl[(D_T0 + k) * L] = v;
+            }
         }
     }
 }
@@ -657,78 +692,111 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_t(DevOctree T, HitAr
     __shared__ uint32_t cs[kScWarps][32][8];
     __shared__ float w1s[kScWarps][32][8], w2s[kScWarps][32][8];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t N = H.N;
-    const size_t L = H.ld;  // row stride of the feature-major matrices
-    const uint32_t j0 = (blockIdx.x * kScWarps + warp) * 32;
-    if (j0 >= N) return;
-    const uint32_t j = j0 + lane;
-    HitGeom g;
-    const bool act = j < N && hit_geom(T, H, j, g, err);
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        cs[warp][lane][b] = act ? g.corners[b] : 0u;
-        w1s[warp][lane][b] = act ? g.w1[b] : 0.f;
-        w2s[warp][lane][b] = act ? g.w2[b] : 0.f;
-    }
-    const unsigned live0 = __ballot_sync(0xffffffffu, act);
-    const uint32_t grp = lane >> 3, f4 = (lane & 7) * 4;
-#pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
+    const uint32_t N = active_hits(H);
+    const size_t L = H.ld;
+    for (uint32_t tile = blockIdx.x * kScWarps + warp; tile * 32 < N; tile += gridDim.x * kScWarps) {
+        const uint32_t j = tile * 32 + lane;
+        HitGeom g;
+        const bool act = j < N && hit_geom(T, H, j, g, err);
         __syncwarp();
-#pragma unroll 4
-        for (int r = 0; r < 32; ++r) {
-            zs[warp][r][lane] = act ? dX[(6 + 32 * half + r) * L + j] : 0.f;
-            zs[warp][32 + r][lane] = act ? dX[(6 + kFt + 32 * half + r) * L + j] : 0.f;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            cs[warp][lane][b] = act ? g.corners[b] : 0u;
+            w1s[warp][lane][b] = act ? g.w1[b] : 0.f;
+            w2s[warp][lane][b] = act ? g.w2[b] : 0.f;
         }
-        __syncwarp();
-        unsigned live = live0;
-        while (live) {
-            const int h = __ffs(live) - 1;
-            live &= live - 1;
+        const unsigned live0 = __ballot_sync(0xffffffffu, act);
+        const uint32_t grp = lane >> 3, f4 = (lane & 7) * 4;
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            __syncwarp();
+#pragma unroll 4
+            for (int r = 0; r < 32; ++r) {
+                zs[warp][r][lane] = act ? dX[(6 + 32 * half + r) * L + j] : 0.f;
+                zs[warp][32 + r][lane] = act ? dX[(6 + kFt + 32 * half + r) * L + j] : 0.f;
+            }
+            __syncwarp();
+            unsigned live = live0;
+            while (live) {
+                const int h = __ffs(live) - 1;
+                live &= live - 1;
 #pragma unroll
-            for (int bp = 0; bp < 2; ++bp) {
-                const uint32_t b = grp + 4 * bp;
-                const float a1 = w1s[warp][h][b], a2 = w2s[warp][h][b];
-                float4 v;
-                v.x = fmaf(a1, zs[warp][f4][h], a2 * zs[warp][32 + f4][h]);
-                v.y = fmaf(a1, zs[warp][f4 + 1][h], a2 * zs[warp][32 + f4 + 1][h]);
-                v.z = fmaf(a1, zs[warp][f4 + 2][h], a2 * zs[warp][32 + f4 + 2][h]);
-                v.w = fmaf(a1, zs[warp][f4 + 3][h], a2 * zs[warp][32 + f4 + 3][h]);
-                atomicAdd(reinterpret_cast<float4*>(g_ft + size_t(cs[warp][h][b]) * kFt + 32 * half + f4), v);
+                for (int bp = 0; bp < 2; ++bp) {
+                    const uint32_t b = grp + 4 * bp;
+                    const float a1 = w1s[warp][h][b], a2 = w2s[warp][h][b];
+                    float4 v;
+                    v.x = fmaf(a1, zs[warp][f4][h], a2 * zs[warp][32 + f4][h]);
+                    v.y = fmaf(a1, zs[warp][f4 + 1][h], a2 * zs[warp][32 + f4 + 1][h]);
+                    v.z = fmaf(a1, zs[warp][f4 + 2][h], a2 * zs[warp][32 + f4 + 2][h]);
+                    v.w = fmaf(a1, zs[warp][f4 + 3][h], a2 * zs[warp][32 + f4 + 3][h]);
+                    atomicAdd(reinterpret_cast<float4*>(g_ft + size_t(cs[warp][h][b]) * kFt + 32 * half + f4), v);
+                }
             }
         }
     }
 }
 
-__global__ void k_fill(float* p, float v, size_t n) {
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = v;
-}
-
 // rows (vertices) whose features any active hit touches
-__global__ void k_touched(DevOctree T, const uint32_t* hit_leaf, const uint32_t* dhit, uint32_t N, uint8_t* touched) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= N) return;
-    const uint32_t* c = T.corners + 8 * size_t(hit_leaf[dhit[j]]);
+__global__ void k_touched(DevOctree T, const uint32_t* hit_leaf, const uint32_t* dhit, const uint32_t* n_dev,
+                          uint32_t cap, uint8_t* touched) {
+    const uint32_t N = min(*n_dev, cap);
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+        const uint32_t* c = T.corners + 8 * size_t(hit_leaf[dhit[j]]);
 #pragma unroll
-    for (int b = 0; b < 8; ++b) touched[c[b]] = 1;
+        for (int b = 0; b < 8; ++b) touched[c[b]] = 1;
+    }
 }
 
-// pack / unpack the touched rows of both feature gradients: row r -> [ft 64 | fc 32]
-__global__ void k_pack_rows(const uint32_t* rows, const uint32_t* n_rows, const float* g_ft, const float* g_fc,
-                            float* packed, bool unpack, float* g_ft_w, float* g_fc_w) {
-    const uint32_t k = blockIdx.x;
-    if (k >= *n_rows) return;
-    const size_t r = rows[k];
-    for (uint32_t d = threadIdx.x; d < 96; d += blockDim.x) {
-        float* dst = packed + size_t(k) * 96 + d;
+// pack / unpack the touched rows of both feature gradients: row r -> [ft 64 | fc 32].
+// Pack writes rows_cap rows (zeros past the touched count) and flags a count
+// above rows_cap (the step is then skipped and re-run with a larger buffer).
+__global__ void k_pack_rows(const uint32_t* rows, const uint32_t* n_rows, uint32_t rows_cap, float* g_ft, float* g_fc,
+                            float* packed, bool unpack, uint32_t* status) {
+    const uint32_t nr = *n_rows;
+    if (!unpack && nr > rows_cap && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, uint32_t(kStepRowOverflow));
+    const uint32_t lim = unpack ? min(nr, rows_cap) : rows_cap;
+    const uint32_t kt = threadIdx.x >> 5, lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+    for (uint32_t k = blockIdx.x * warps + kt; k < lim; k += gridDim.x * warps) {
+        float* dst = packed + size_t(k) * 96;
+        if (k >= nr) {
+            for (uint32_t d = lane; d < 96; d += 32) dst[d] = 0.f;
+            continue;
+        }
+        const size_t r = rows[k];
         if (!unpack) {
-            *dst = d < 64 ? g_ft[r * 64 + d] : g_fc[r * 32 + (d - 64)];
-        } else if (d < 64) {
-            g_ft_w[r * 64 + d] = *dst;
+            dst[lane] = g_ft[r * 64 + lane];
+            dst[32 + lane] = g_ft[r * 64 + 32 + lane];
+            dst[64 + lane] = g_fc[r * 32 + lane];
         } else {
-            g_fc_w[r * 32 + (d - 64)] = *dst;
+            g_ft[r * 64 + lane] = dst[lane];
+            g_ft[r * 64 + 32 + lane] = dst[32 + lane];
+            g_fc[r * 32 + lane] = dst[64 + lane];
         }
     }
+}
+
+// skip bits of the step from the (all-reduced) flags
+__global__ void k_step_status(const double* red, uint32_t* status) {
+    uint32_t s = *status;
+    if (red[R_OVERFLOW] > 0.0) s |= kStepHitOverflow;
+    if (red[R_ERROR] > 0.0) s |= kStepDeviceError;
+    *status = s;
+}
+
+__global__ void k_step_mail(const double* red, const uint32_t* status, const int* err, const uint32_t* trav_counters,
+                            const uint32_t* n_act, uint32_t cap, const uint32_t* n_rows, StepMail* mail) {
+    StepMail m;
+    m.loss = red[R_LOSS];
+    m.skipped = red[R_SKIPPED];
+    m.eta_skipped = red[R_ETA_SKIPPED];
+    m.rays = red[R_RAYS];
+    m.err = uint32_t(*err);
+    m.flags = *status;
+    m.hits = trav_counters[0];
+    m.active = *n_act;  // unclamped: sizes the next step's matrices
+    m.rows = n_rows ? *n_rows : 0u;
+    m.pad = 0;
+    *mail = m;
 }
 
 struct AdamSeg {
@@ -738,17 +806,20 @@ struct AdamSeg {
     float* v;
     size_t n;
     double corr1, corr2;
+    float beta1, beta2, eps;
 };
 struct AdamSegs {
     AdamSeg seg[14];
     int count;
 };
 
-// adam_step, src/mlp.cpp:277-296 (fp64 math, fp32 storage; beta/eps are
-// float fields promoted to double; lr is rounded to float first, :427).
-__global__ void k_adam(AdamSegs S, float lr) {
+// adam_step, src/mlp.cpp:277-296 (fp64 math, fp32 storage; beta/eps are the
+// AdamState float fields promoted to double; lr is rounded to float first,
+// src/train.cpp:427). Skipped when the step is flagged (error / overflow).
+__global__ void k_adam(AdamSegs S, float lr, const uint32_t* skip_if, const int* err) {
+    if ((skip_if && *skip_if) || (err && *err)) return;
     const AdamSeg sg = S.seg[blockIdx.y];
-    const double b1 = double(0.9f), b2 = double(0.999f), eps = double(1e-8f);
+    const double b1 = double(sg.beta1), b2 = double(sg.beta2), eps = double(sg.eps);
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < sg.n; i += size_t(gridDim.x) * blockDim.x) {
         const double g = sg.g[i];
         const double m = dadd(dmul(b1, double(sg.m[i])), dmul(dsub(1.0, b1), g));
@@ -760,28 +831,79 @@ __global__ void k_adam(AdamSegs S, float lr) {
     }
 }
 
+int g_sms = 0;
+uint32_t sms() {
+    if (!g_sms) {
+        int dev = 0;
+        SVLF_CUDA(cudaGetDevice(&dev));
+        SVLF_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return uint32_t(g_sms);
+}
+
+// grid of a loop over `items` work items of `per_block` each: no more blocks
+// than the items need, at most `per_sm` blocks per SM
+unsigned loop_grid(size_t items, size_t per_block, uint32_t per_sm) {
+    const size_t need = std::max<size_t>(1, (items + per_block - 1) / per_block);
+    return unsigned(std::min<size_t>(need, size_t(sms()) * per_sm));
+}
+
 }  // namespace
 
 TrainScratch::~TrainScratch() {
-    if (blas) cublas_api().Destroy(static_cast<cublasHandle_t>(blas));
-    if (h_pinned) cudaFreeHost(h_pinned);
+    if (h_mail) cudaFreeHost(h_mail);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
 }
 
-TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& M, const TrainBatchDev& b,
+void launch_adam(const TrainModelRefs& M, bool color_frozen, float lr, const uint32_t* skip_if, const int* err,
+                 cudaStream_t s) {
+    using D = DecOffsets;
+    AdamSegs segs{};
+    const size_t off_fc = M.n_ft, off_mt = M.n_ft + M.n_fc, off_mc = off_mt + SVLF_DEC_T_SIZE;
+    auto add = [&](int sid, size_t off, size_t cnt) {
+        const AdamHyper& h = M.hyper[sid];
+        const uint64_t step = M.steps[sid] + 1;  // the caller advances the counters when the update ran
+        const double c1 = 1.0 - std::pow(double(h.beta1), double(step));
+        const double c2 = 1.0 - std::pow(double(h.beta2), double(step));
+        segs.seg[segs.count++] =
+            AdamSeg{M.params + off, M.grads + off, M.adam_m + off, M.adam_v + off, cnt, c1, c2, h.beta1, h.beta2, h.eps};
+    };
+    // ModelAdam tensor order: feat_t, feat_c, f_T (W0,b0,W1,b1), f_C (W0,b0,...,W3,b3)
+    add(0, 0, M.n_ft);
+    const size_t t_seg[4][2] = {{D::T_W0, kHid * kInT}, {D::T_B0, kHid}, {D::T_W1, 2 * kHid}, {D::T_B1, 2}};
+    for (int i = 0; i < 4; ++i) add(2 + i, off_mt + t_seg[i][0], t_seg[i][1]);
+    if (!color_frozen) {
+        add(1, off_fc, M.n_fc);
+        const size_t c_seg[8][2] = {{D::C_W0, kHid * kInC}, {D::C_B0, kHid},       {D::C_W1, kHid * kHid},
+                                    {D::C_B1, kHid},        {D::C_W2, kHid * kHid}, {D::C_B2, kHid},
+                                    {D::C_W3, 3 * kHid},    {D::C_B3, 3}};
+        for (int i = 0; i < 8; ++i) add(6 + i, off_mc + c_seg[i][0], c_seg[i][1]);
+    }
+    k_adam<<<dim3(unsigned(std::min<uint32_t>(1024, sms() * 8)), unsigned(segs.count)), 256, 0, s>>>(segs, lr,
+                                                                                                      skip_if, err);
+    note_launch();
+}
+
+TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModelRefs& M, const TrainBatchDev& b,
                            const TrainOptions& o, cudaStream_t s, int* err_flag) {
     using D = DecOffsets;
     TrainResult res;
-    res.rays = b.n;
-    if (!S.h_pinned) {
-        SVLF_CUDA(cudaMallocHost(&S.h_pinned, 256));
+    if (!S.h_mail) {
+        SVLF_CUDA(cudaMallocHost(&S.h_mail, sizeof(StepMail)));
         for (auto& e : S.ev) SVLF_CUDA(cudaEventCreate(&e));
     }
     const size_t P = M.n_ft + M.n_fc + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE;
-    SVLF_CUDA(cudaMemsetAsync(M.grads, 0, P * 4, s));
     const uint32_t n = b.n;
+    // Per-active-hit buffers (the feature-major matrices: ~5.3 KB per hit) are
+    // sized from the previous step's active count with headroom, not from the
+    // traversal's hit capacity: tighter rows (row stride ld) and bounded
+    // memory. A step whose active hits exceed it is flagged and re-run.
+    if (S.act_cap == 0) S.act_cap = std::max<uint32_t>(65536, n);
+    const uint32_t cap = std::min<uint32_t>(std::max<uint32_t>(b.hit_cap, 32), S.act_cap);
+    const uint32_t ld = (cap + 31u) & ~31u;
     SVLF_CUDA(cudaEventRecord(S.ev[0], s));
+    SVLF_CUDA(cudaMemsetAsync(M.grads, 0, P * 4, s));
 
     // ---- per-ray preparation and dense active-hit list
     uint32_t* act_first = S.act_first.ensure<uint32_t>(n + 1);
@@ -791,128 +913,84 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     double* eta_gt = S.eta_gt.ensure<double>(n + 1);
     double* ray_loss = S.ray_loss.ensure<double>(n + 1);
     unsigned long long* counters = S.counters.ensure<unsigned long long>(4);
-    double* loss_out = S.loss_out.ensure<double>(1);
+    double* red = S.red.ensure<double>(R_COUNT);
+    uint32_t* status = S.status.ensure<uint32_t>(4);
+    StepMail* mail = reinterpret_cast<StepMail*>(S.loss_out.ensure<char>(sizeof(StepMail)));
     SVLF_CUDA(cudaMemsetAsync(counters, 0, 32, s));
+    SVLF_CUDA(cudaMemsetAsync(status, 0, 16, s));
     SVLF_CUDA(cudaMemsetAsync(act_cnt + n, 0, 4, s));
-    PrepArgs pa{b.rays, b.depth_gt, b.alpha_gt, n, b.ray_off, b.ray_cnt, b.hit_leaf, b.hit_tin, b.hit_tout,
-                o.surface, o.lw.empty == 0.0, act_first, act_cnt, surf_rel, eta_gt, counters};
-    if (n) k_prep<<<(n + 127) / 128, 128, 0, s>>>(T, pa, err_flag);
+    PrepArgs pa{b.rays,   b.depth_gt, b.alpha_gt, n,         b.ray_off, b.ray_cnt, b.hit_leaf, b.hit_tin,
+                b.hit_tout, b.trav_counters, o.surface, o.lw.empty == 0.0, act_first, act_cnt, surf_rel, eta_gt,
+                counters};
+    if (n) {
+        k_prep<<<(n + 127) / 128, 128, 0, s>>>(T, pa, err_flag);
+        note_launch();
+    }
     {
         size_t tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, act_cnt, dpos, int(n + 1));
         SVLF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.ensure<char>(tb), tb, act_cnt, dpos, int(n + 1), s));
+        note_launch();
     }
-    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned, dpos + n, 4, cudaMemcpyDeviceToHost, s));
-    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 4, counters, 16, cudaMemcpyDeviceToHost, s));
-    SVLF_CUDA(cudaStreamSynchronize(s));
-    const uint32_t N = uint32_t(S.h_pinned[0]);
-    unsigned long long cnts[2];
-    std::memcpy(cnts, S.h_pinned + 4, 16);
-    res.skipped = (long long)cnts[0];
-    res.eta_skipped = (long long)cnts[1];
+    const uint32_t* n_act = dpos + n;  // active hits, on the device
 
-    uint32_t* dhit = S.dhit.ensure<uint32_t>(N + 1);
-    uint32_t* dray = S.dray.ensure<uint32_t>(N + 1);
-    float* hitf = S.hitf.ensure<float>(size_t(N) * 8 + 8);
-    double* hitd = S.hitd.ensure<double>(size_t(N) * 5 + 5);
-    // feature-major matrices with rows padded to 32 floats: aligned leading
-    // dimensions let cuBLAS use its vectorised (align4) SGEMM kernels
-    const uint32_t Np = (N + 31u) & ~31u;
-    float* acts = S.acts.ensure<float>(size_t(A_ROWS) * Np + 1);
-    float* deltas = S.deltas.ensure<float>(size_t(D_ROWS) * Np + 1);
-    SVLF_CUDA(cudaMemsetAsync(hitd, 0, size_t(N) * 2 * 8, s));                 // dtau, deta
-    SVLF_CUDA(cudaMemsetAsync(hitf + size_t(N) * 5, 0, size_t(N) * 3 * 4, s));  // drgb
-    float* dxs = S.dxs.ensure<float>(size_t(kInT) * Np + 1);                     // dL/d layer-0 inputs
-    if (n) k_expand<<<(n + 127) / 128, 128, 0, s>>>(n, act_first, act_cnt, dpos, dhit, dray);
-
-    // Dense layers as fp32 GEMMs on the feature-major matrices. A feature-major
-    // R x N block is the column-major N x R matrix (ld N); a row-major [O][K]
-    // weight is the column-major K x O matrix (ld K).
-    if (!S.blas) {
-        const CublasApi& B = cublas_api();
-        cublasHandle_t hb = nullptr;
-        cublas_check(B.Create(&hb), "cublasCreate");
-        S.blas = hb;
+    uint32_t* dhit = S.dhit.ensure<uint32_t>(cap);
+    uint32_t* dray = S.dray.ensure<uint32_t>(cap);
+    float* hitf = S.hitf.ensure<float>(size_t(ld) * 8);    // tau, eta, rgb[3], drgb[3]
+    double* hitd = S.hitd.ensure<double>(size_t(ld) * 5);  // dtau, deta, e, T, w
+    float* acts = S.acts.ensure<float>(size_t(A_ROWS) * ld);
+    float* deltas = S.deltas.ensure<float>(size_t(D_ROWS) * ld);
+    float* dxs = S.dxs.ensure<float>(size_t(kInT) * ld);  // dL/d layer-0 inputs
+    HitArgs H{b.rays,   b.hit_leaf, b.hit_tin, b.hit_tout, dhit,   dray,  dpos, surf_rel, n_act, cap, ld, o.surface,
+              acts,     deltas,     hitf,      hitf + ld,  hitf + 2 * size_t(ld), hitf + 5 * size_t(ld), hitd,
+              hitd + ld};
+    if (n) {
+        k_expand<<<(n + 127) / 128, 128, 0, s>>>(n, act_first, act_cnt, dpos, H, dhit, dray);
+        note_launch();
     }
-    const CublasApi& B = cublas_api();
-    cublasHandle_t hb = static_cast<cublasHandle_t>(S.blas);
-    cublas_check(B.SetStream(hb, s), "cublasSetStream");
-    // fp32 mode: true fp32 (no TF32) cuBLAS GEMMs on the CUDA cores. tf32 mode:
-    // the weight-gradient GEMMs (reductions over all hits) on tensor cores with
-    // TF32 operands. tf32x3 mode: every GEMM on the tensor cores as three
-    // products of split TF32 operands (gemm_x3.cu), fp32-level accuracy.
-    const bool x3 = o.tf32x3;
-    cublas_check(B.SetMathMode(hb, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");
-    const float one = 1.f, zero = 0.f;
-    const int Ni = int(N), Li = int(Np);
-    uint8_t* wimg = x3 ? S.wimg.ensure<uint8_t>(gemm_x3_image_bytes(kInT)) : nullptr;
-    // Y(O x N) = W X: rows [xrow, xrow+K) -> [yrow, yrow+O) of acts
-    auto layer_fwd = [&](const float* W, int O, int K, int xrow, int yrow, const float* bias) {
-        if (x3) {
-            gemm_x3_fwd(acts + size_t(xrow) * Np, W, bias, acts + size_t(yrow) * Np, O, K, N, Np, wimg, s);
-            return;
-        }
-        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Ni, O, K, &one, acts + size_t(xrow) * Np, Li, W, K, &zero,
-                             acts + size_t(yrow) * Np, Li),
-                     "sgemm fwd");
-        k_bias_relu<<<dim3(unsigned(std::min<size_t>((N + 255) / 256, 1184)), unsigned(O)), 256, 0, s>>>(
-            acts + size_t(yrow) * Np, bias, N, Np);
-    };
-    // dX rows [k0, K) (x N) = W^T D, D = delta rows [drow, drow+O); with mask_row >= 0 the
-    // result is the next delta block: zeroed where the layer's activation (acts row mask_row..) <= 0
-    const unsigned mask_blocks = unsigned(std::min<size_t>((size_t(kHid) * Np + 255) / 256, 4736));
-    auto layer_bwd = [&](const float* W, int O, int K, int k0, int drow, float* dst, int mask_row) {
-        const float* mask = mask_row >= 0 ? acts + size_t(mask_row) * Np : nullptr;
-        if (x3) {
-            gemm_x3_bwd(deltas + size_t(drow) * Np, W, O, K, k0, dst, mask, N, Np, wimg, s);
-            return;
-        }
-        cublas_check(B.Sgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, Ni, K - k0, O, &one, deltas + size_t(drow) * Np, Li, W + k0,
-                             K, &zero, dst, Li),
-                     "sgemm bwd");
-        if (mask) k_relu_mask<<<mask_blocks, 256, 0, s>>>(dst, mask, size_t(K - k0) * Np);
-    };
-    // dW(O x K) = D X^T, db = D 1
-    float* ones = S.ones.ensure<float>(size_t(N) + 1);
-    auto layer_dw = [&](int drow, int O, int xrow, int K, float* dW, float* db) {
-        if (x3) {
-            gemm_x3_dw(deltas + size_t(drow) * Np, acts + size_t(xrow) * Np, O, K, dW, db, N, Np, s);
-            return;
-        }
-        cublas_check(B.Sgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, K, O, Ni, &one, acts + size_t(xrow) * Np, Li,
-                             deltas + size_t(drow) * Np, Li, &zero, dW, K),
-                     "sgemm dW");
-        cublas_check(B.Sgemv(hb, CUBLAS_OP_T, Ni, O, &one, deltas + size_t(drow) * Np, Li, ones, 1, &zero, db, 1),
-                     "sgemv db");
-    };
-    const unsigned hit_blocks = (N + 127) / 128;
 
-    HitArgs H{b.rays, b.hit_leaf, b.hit_tin, b.hit_tout, dhit, dray, dpos, surf_rel, N, Np, o.surface, acts, deltas,
-              hitf, hitf + N, hitf + 2 * size_t(N), hitf + 5 * size_t(N), hitd, hitd + N};
+    // Weight operand images of every forward / input-gradient GEMM (one launch).
+    X3ImageJobs jobs{};
+    enum { J_FT0, J_FC0, J_FC1, J_FC2, J_BC2, J_BC1, J_BC0, J_BT0 };
+    jobs.job[J_FT0] = {M.view.mt + D::T_W0, kHid, kInT, 0, 0};
+    jobs.job[J_FC0] = {M.view.mc + D::C_W0, kHid, kInC, 0, 0};
+    jobs.job[J_FC1] = {M.view.mc + D::C_W1, kHid, kHid, 0, 0};
+    jobs.job[J_FC2] = {M.view.mc + D::C_W2, kHid, kHid, 0, 0};
+    jobs.job[J_BC2] = {M.view.mc + D::C_W2, kHid, kHid, 0, 1};
+    jobs.job[J_BC1] = {M.view.mc + D::C_W1, kHid, kHid, 0, 1};
+    jobs.job[J_BC0] = {M.view.mc + D::C_W0, kHid, kInC, 6, 1};
+    jobs.job[J_BT0] = {M.view.mt + D::T_W0, kHid, kInT, 6, 1};
+    jobs.count = 8;
+    size_t img_bytes = 0;
+    for (int i = 0; i < jobs.count; ++i)
+        img_bytes += gemm_x3_image_bytes(jobs.job[i].bwd ? jobs.job[i].O : jobs.job[i].K);
+    uint8_t* wimg = S.wimg.ensure<uint8_t>(img_bytes);
+    gemm_x3_build_images(jobs, wimg, s);
+    auto img = [&](int i) { return wimg + jobs.offset[i]; };
+    float* part = S.dw_part.ensure<float>(gemm_x3_dw_partial_floats(kHid, kInT));
+
+    const unsigned in_grid = loop_grid(cap, 32 * kInWarps, 16);
+    const unsigned hit_grid = loop_grid(cap, 128, 16);
+    const unsigned sc_grid = loop_grid(cap, 32 * kScWarps, 8);
+    auto A = [&](int row) { return acts + size_t(row) * ld; };
+    auto Dm = [&](int row) { return deltas + size_t(row) * ld; };
+
     SVLF_CUDA(cudaEventRecord(S.ev[1], s));
-    if (N) {
-        k_fill<<<std::min<unsigned>(hit_blocks, 1184), 128, 0, s>>>(ones, 1.f, N);
-        k_fwd_in_t<<<unsigned((size_t(N) + 32 * kInWarps - 1) / (32 * kInWarps)), 32 * kInWarps, 0, s>>>(
-            T, M.view, H, err_flag);
-        layer_fwd(M.view.mt + D::T_W0, kHid, kInT, A_XT, A_HT, M.view.mt + D::T_B0);
-        k_fwd_mid<<<unsigned((size_t(N) + 32 * kInWarps - 1) / (32 * kInWarps)), 32 * kInWarps, 0, s>>>(
-            T, M.view, H, err_flag);
-        layer_fwd(M.view.mc + D::C_W0, kHid, kInC, A_XC, A_H1, M.view.mc + D::C_B0);
-        layer_fwd(M.view.mc + D::C_W1, kHid, kHid, A_H1, A_H2, M.view.mc + D::C_B1);
-        layer_fwd(M.view.mc + D::C_W2, kHid, kHid, A_H2, A_H3, M.view.mc + D::C_B2);
-        k_fwd_rgb<<<hit_blocks, 128, 0, s>>>(M.view, H);
-        note_launch(9);
-    }
+    // ---- forward
+    k_fwd_in_t<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
+    gemm_x3_fwd(A(A_XT), img(J_FT0), M.view.mt + D::T_B0, A(A_HT), kHid, kInT, n_act, cap, ld, s);
+    k_fwd_mid<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
+    gemm_x3_fwd(A(A_XC), img(J_FC0), M.view.mc + D::C_B0, A(A_H1), kHid, kInC, n_act, cap, ld, s);
+    gemm_x3_fwd(A(A_H1), img(J_FC1), M.view.mc + D::C_B1, A(A_H2), kHid, kHid, n_act, cap, ld, s);
+    gemm_x3_fwd(A(A_H2), img(J_FC2), M.view.mc + D::C_B2, A(A_H3), kHid, kHid, n_act, cap, ld, s);
+    k_fwd_rgb<<<hit_grid, 128, 0, s>>>(M.view, H);
+    note_launch(3);
     SVLF_CUDA(cudaEventRecord(S.ev[2], s));
-    LossArgs L{b.c_gt, b.alpha_gt, dpos, act_cnt, surf_rel, eta_gt, b.hit_tin, n, o.surface, o.lw, ray_loss,
-               hitd + 2 * size_t(N), hitd + 3 * size_t(N), hitd + 4 * size_t(N)};
-    if (n) k_loss<<<(n + 127) / 128, 128, 0, s>>>(L, H);
-    {
-        size_t tb = 0;
-        cub::DeviceReduce::Sum(nullptr, tb, ray_loss, loss_out, int(n));
-        if (n) SVLF_CUDA(cub::DeviceReduce::Sum(S.scan_tmp.ensure<char>(std::max(tb, size_t(16))), tb, ray_loss,
-                                                loss_out, int(n), s));
-        else SVLF_CUDA(cudaMemsetAsync(loss_out, 0, 8, s));
+    LossArgs L{b.c_gt, b.alpha_gt, dpos, act_cnt, surf_rel, eta_gt, n, o.surface, o.lw, ray_loss,
+               hitd + 2 * size_t(ld), hitd + 3 * size_t(ld), hitd + 4 * size_t(ld)};
+    if (n) {
+        k_loss<<<(n + 127) / 128, 128, 0, s>>>(L, H);
+        note_launch();
     }
     SVLF_CUDA(cudaEventRecord(S.ev[3], s));
 
@@ -921,123 +999,100 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& 
     float* g_fc = M.grads + M.n_ft;
     float* g_mt = g_fc + M.n_fc;
     float* g_mc = g_mt + SVLF_DEC_T_SIZE;
-    if (N) {
-        // f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
-        k_bwd_head_c<<<hit_blocks, 128, 0, s>>>(M.view, H);
-        layer_bwd(M.view.mc + D::C_W2, kHid, kHid, 0, D_C2, deltas + size_t(D_C1) * Np, A_H2);
-        layer_bwd(M.view.mc + D::C_W1, kHid, kHid, 0, D_C1, deltas + size_t(D_C0) * Np, A_H1);
-        layer_bwd(M.view.mc + D::C_W0, kHid, kInC, 6, D_C0, dxs + 6 * size_t(Np), -1);
-        // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
-        const unsigned sc_blocks = unsigned((size_t(N) + 32 * kScWarps - 1) / (32 * kScWarps));
-        k_bwd_feat_c<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
-        layer_bwd(M.view.mt + D::T_W0, kHid, kInT, 6, D_T0, dxs + 6 * size_t(Np), -1);
-        k_bwd_feat_t<<<sc_blocks, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
-        // weight gradients (sums over hits)
-        if (o.tf32 && !x3) cublas_check(B.SetMathMode(hb, CUBLAS_TF32_TENSOR_OP_MATH), "cublasSetMathMode");
-        layer_dw(D_T0, kHid, A_XT, kInT, g_mt + D::T_W0, g_mt + D::T_B0);
-        layer_dw(D_T1, 2, A_HT, kHid, g_mt + D::T_W1, g_mt + D::T_B1);
-        if (!o.color_frozen) {
-            layer_dw(D_C0, kHid, A_XC, kInC, g_mc + D::C_W0, g_mc + D::C_B0);
-            layer_dw(D_C1, kHid, A_H1, kHid, g_mc + D::C_W1, g_mc + D::C_B1);
-            layer_dw(D_C2, kHid, A_H2, kHid, g_mc + D::C_W2, g_mc + D::C_B2);
-            layer_dw(D_C3, 3, A_H3, kHid, g_mc + D::C_W3, g_mc + D::C_B3);
-        }
-        note_launch(6);
+    // f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
+    k_bwd_head_c<<<hit_grid, 128, 0, s>>>(M.view, H);
+    gemm_x3_bwd(Dm(D_C2), img(J_BC2), kHid, kHid, 0, Dm(D_C1), A(A_H2), n_act, cap, ld, s);
+    gemm_x3_bwd(Dm(D_C1), img(J_BC1), kHid, kHid, 0, Dm(D_C0), A(A_H1), n_act, cap, ld, s);
+    gemm_x3_bwd(Dm(D_C0), img(J_BC0), kHid, kInC, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
+    // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
+    k_bwd_feat_c<<<sc_grid, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
+    gemm_x3_bwd(Dm(D_T0), img(J_BT0), kHid, kInT, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
+    k_bwd_feat_t<<<sc_grid, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
+    note_launch(3);
+    // weight gradients (sums over hits, CTA-ordered partials)
+    const int prod = o.tf32 ? 1 : 3;
+    gemm_x3_dw(Dm(D_T0), A(A_XT), kHid, kInT, g_mt + D::T_W0, g_mt + D::T_B0, n_act, cap, ld, part, prod, s);
+    gemm_x3_dw(Dm(D_T1), A(A_HT), 2, kHid, g_mt + D::T_W1, g_mt + D::T_B1, n_act, cap, ld, part, prod, s);
+    if (!o.color_frozen) {
+        gemm_x3_dw(Dm(D_C0), A(A_XC), kHid, kInC, g_mc + D::C_W0, g_mc + D::C_B0, n_act, cap, ld, part, prod, s);
+        gemm_x3_dw(Dm(D_C1), A(A_H1), kHid, kHid, g_mc + D::C_W1, g_mc + D::C_B1, n_act, cap, ld, part, prod, s);
+        gemm_x3_dw(Dm(D_C2), A(A_H2), kHid, kHid, g_mc + D::C_W2, g_mc + D::C_B2, n_act, cap, ld, part, prod, s);
+        gemm_x3_dw(Dm(D_C3), A(A_H3), 3, kHid, g_mc + D::C_W3, g_mc + D::C_B3, n_act, cap, ld, part, prod, s);
     }
-    // ---- data parallel: all-reduce loss, statistics and gradients (NCCL)
-    if (o.nccl_comm) {
-        ncclComm_t comm = static_cast<ncclComm_t>(o.nccl_comm);
-        const NcclApi& api = nccl_api();
-        auto nccl = nccl_check;
-        // loss and counters (as doubles) in one reduction
-        double* red = S.red.ensure<double>(4);
-        SVLF_CUDA(cudaMemcpyAsync(red, loss_out, 8, cudaMemcpyDeviceToDevice, s));
-        const double local_cnt[3] = {double(res.skipped), double(res.eta_skipped), double(res.rays)};
-        SVLF_CUDA(cudaMemcpyAsync(red + 1, local_cnt, 24, cudaMemcpyHostToDevice, s));
-        nccl(api.AllReduce(red, red, 4, ncclFloat64, ncclSum, comm, s));
-        SVLF_CUDA(cudaMemcpyAsync(loss_out, red, 8, cudaMemcpyDeviceToDevice, s));
-        // decoders: dense
-        nccl(api.AllReduce(g_mt, g_mt, SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE, ncclFloat32, ncclSum, comm, s));
-        // features: union of touched rows (max of 0/1 flags), compacted, summed, scattered back
+    if (n) {
+        size_t tb = 0;
+        cub::DeviceReduce::Sum(nullptr, tb, ray_loss, red + R_LOSS, int(n));
+        SVLF_CUDA(cub::DeviceReduce::Sum(S.scan_tmp.ensure<char>(tb), tb, ray_loss, red + R_LOSS, int(n), s));
+    } else {
+        SVLF_CUDA(cudaMemsetAsync(red + R_LOSS, 0, 8, s));
+    }
+    k_step_scalars<<<1, 1, 0, s>>>(n, counters, b.trav_counters, n_act, cap, err_flag, red);
+    note_launch(2);
+
+    // ---- data parallel: all-reduce the scalars, the decoder gradients and
+    // the union of touched feature rows
+    const uint32_t* n_rows_dev = nullptr;
+    if (o.coll && o.coll->world > 1) {
+        Collective& C = *o.coll;
+        C.allreduce(red, R_COUNT, CollType::F64, CollOp::Sum, s);
+        C.allreduce(g_mt, SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE, CollType::F32, CollOp::Sum, s);
         const uint32_t V = M.view.V;
         uint8_t* touched = S.touched.ensure<uint8_t>(V);
         SVLF_CUDA(cudaMemsetAsync(touched, 0, V, s));
-        if (N) k_touched<<<(N + 127) / 128, 128, 0, s>>>(T, b.hit_leaf, dhit, N, touched);
-        nccl(api.AllReduce(touched, touched, V, ncclUint8, ncclMax, comm, s));
+        k_touched<<<loop_grid(cap, 256, 8), 256, 0, s>>>(T, b.hit_leaf, dhit, n_act, cap, touched);
+        C.allreduce(touched, V, CollType::U8, CollOp::Max, s);
         uint32_t* rows = S.rows.ensure<uint32_t>(V);
         uint32_t* n_rows = S.n_rows.ensure<uint32_t>(1);
         size_t tb = 0;
         cub::CountingInputIterator<uint32_t> idx(0);
         cub::DeviceSelect::Flagged(nullptr, tb, idx, touched, rows, n_rows, int(V));
         SVLF_CUDA(cub::DeviceSelect::Flagged(S.scan_tmp.ensure<char>(tb), tb, idx, touched, rows, n_rows, int(V), s));
-        SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 12, n_rows, 4, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaStreamSynchronize(s));
-        const uint32_t K = uint32_t(S.h_pinned[12]);
-        res.exchanged_rows = K;
-        if (K) {
-            float* packed = S.packed.ensure<float>(size_t(K) * 96);
-            k_pack_rows<<<K, 96, 0, s>>>(rows, n_rows, g_ft, g_fc, packed, false, g_ft, g_fc);
-            nccl(api.AllReduce(packed, packed, size_t(K) * 96, ncclFloat32, ncclSum, comm, s));
-            k_pack_rows<<<K, 96, 0, s>>>(rows, n_rows, g_ft, g_fc, packed, true, g_ft, g_fc);
-            note_launch(2);
-        }
-        SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 16, red + 1, 24, cudaMemcpyDeviceToHost, s));
-        SVLF_CUDA(cudaStreamSynchronize(s));
-        double cnt[3];
-        std::memcpy(cnt, S.h_pinned + 16, 24);
-        res.skipped = (long long)cnt[0];
-        res.eta_skipped = (long long)cnt[1];
-        res.rays = (long long)cnt[2];  // statistics of the whole (all-rank) batch
-        note_launch(2);
+        if (S.rows_cap == 0) S.rows_cap = std::min<uint32_t>(V, 1u << 16);
+        const uint32_t rc = std::min<uint32_t>(S.rows_cap, V);
+        float* packed = S.packed.ensure<float>(size_t(rc) * 96);
+        k_pack_rows<<<loop_grid(rc, 8, 8), 256, 0, s>>>(rows, n_rows, rc, g_ft, g_fc, packed, false, status);
+        C.allreduce(packed, size_t(rc) * 96, CollType::F32, CollOp::Sum, s);
+        k_pack_rows<<<loop_grid(rc, 8, 8), 256, 0, s>>>(rows, n_rows, rc, g_ft, g_fc, packed, true, status);
+        note_launch(4);
+        n_rows_dev = n_rows;
     }
+    k_step_status<<<1, 1, 0, s>>>(red, status);
+    note_launch();
     SVLF_CUDA(cudaEventRecord(S.ev[4], s));
 
-    // ---- Adam (adam_model_step, src/train.cpp:345-360)
-    if (o.adam) {
-        AdamSegs segs{};
-        float* p_ft = M.params;
-        float* p_fc = p_ft + M.n_ft;
-        float* p_mt = p_fc + M.n_fc;
-        float* p_mc = p_mt + SVLF_DEC_T_SIZE;
-        const size_t off_fc = M.n_ft, off_mt = M.n_ft + M.n_fc, off_mc = off_mt + SVLF_DEC_T_SIZE;
-        auto add = [&](int sid, size_t off, size_t cnt) {
-            const uint64_t step = ++M.steps[sid];
-            const double c1 = 1.0 - std::pow(double(0.9f), double(step));
-            const double c2 = 1.0 - std::pow(double(0.999f), double(step));
-            segs.seg[segs.count++] = AdamSeg{M.params + off, M.grads + off, M.adam_m + off, M.adam_v + off, cnt, c1, c2};
-        };
-        (void)p_ft; (void)p_fc; (void)p_mt; (void)p_mc;
-        // ModelAdam tensor order: feat_t, feat_c, f_T (W0,b0,W1,b1), f_C (W0,b0,...,W3,b3)
-        add(0, 0, M.n_ft);
-        const size_t t_seg[4][2] = {{D::T_W0, kHid * kInT}, {D::T_B0, kHid}, {D::T_W1, 2 * kHid}, {D::T_B1, 2}};
-        for (int i = 0; i < 4; ++i) add(2 + i, off_mt + t_seg[i][0], t_seg[i][1]);
-        if (!o.color_frozen) {
-            add(1, off_fc, M.n_fc);
-            const size_t c_seg[8][2] = {{D::C_W0, kHid * kInC}, {D::C_B0, kHid},  {D::C_W1, kHid * kHid},
-                                        {D::C_B1, kHid},        {D::C_W2, kHid * kHid}, {D::C_B2, kHid},
-                                        {D::C_W3, 3 * kHid},    {D::C_B3, 3}};
-            for (int i = 0; i < 8; ++i) add(6 + i, off_mc + c_seg[i][0], c_seg[i][1]);
-        }
-        dim3 grid(1024, segs.count);
-        k_adam<<<grid, 256, 0, s>>>(segs, o.lr);
-        note_launch();
-    }
+    // ---- Adam (adam_model_step, src/train.cpp:345-360), skipped on the device
+    // when the step is flagged
+    if (o.adam) launch_adam(M, o.color_frozen, o.lr, status, nullptr, s);
     SVLF_CUDA(cudaEventRecord(S.ev[5], s));
-    note_launch(6);
-
-    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 8, loss_out, 8, cudaMemcpyDeviceToHost, s));
-    SVLF_CUDA(cudaMemcpyAsync(S.h_pinned + 10, err_flag, 4, cudaMemcpyDeviceToHost, s));
+    k_step_mail<<<1, 1, 0, s>>>(red, status, err_flag, b.trav_counters, n_act, cap, n_rows_dev, mail);
+    note_launch();
+    SVLF_CUDA(cudaMemcpyAsync(S.h_mail, mail, sizeof(StepMail), cudaMemcpyDeviceToHost, s));
     SVLF_CUDA(cudaStreamSynchronize(s));
-    std::memcpy(&res.loss, S.h_pinned + 8, 8);
-    res.error = S.h_pinned[10];
-    if (res.error) SVLF_CUDA(cudaMemsetAsync(err_flag, 0, 4, s));
+    StepMail hm;
+    std::memcpy(&hm, S.h_mail, sizeof hm);
+    res.loss = hm.loss;
+    res.skipped = (long long)hm.skipped;
+    res.eta_skipped = (long long)hm.eta_skipped;
+    res.rays = (long long)hm.rays;
+    res.error = int(hm.err);
+    if (!res.error && (hm.flags & kStepDeviceError)) res.error = -1;  // raised on another rank
+    res.flags = hm.flags & (kStepHitOverflow | kStepRowOverflow);
+    res.hits = hm.hits;
+    res.active = hm.active;
+    // activation capacity for the next step: grow with 25 % headroom on overflow, shrink when a
+    // quarter of it is used
+    if (hm.active > cap || hm.active < S.act_cap / 4) S.act_cap = std::max<uint32_t>(4096, hm.active + hm.active / 4);
+    res.touched_rows = hm.rows;
+    res.updated = o.adam && hm.flags == 0 && hm.err == 0;
+    if (hm.err) SVLF_CUDA(cudaMemsetAsync(err_flag, 0, 4, s));
+    if (n_rows_dev) {  // next step's exchange buffer: 25 % headroom over this step's touched rows
+        const uint32_t want = std::max<uint32_t>(4096, hm.rows + hm.rows / 4);
+        if ((hm.flags & kStepRowOverflow) || want < S.rows_cap / 2 || want > S.rows_cap) S.rows_cap = want;
+    }
     float t[5] = {};
-    cudaEventElapsedTime(&t[0], S.ev[0], S.ev[1]);
-    cudaEventElapsedTime(&t[1], S.ev[1], S.ev[2]);
-    cudaEventElapsedTime(&t[2], S.ev[2], S.ev[3]);
-    cudaEventElapsedTime(&t[3], S.ev[3], S.ev[4]);
-    cudaEventElapsedTime(&t[4], S.ev[4], S.ev[5]);
-    res.timings = svlf_timings{t[0], 0.f, t[1], t[2], t[3], t[4], t[0] + t[1] + t[2] + t[3] + t[4], (long long)N, 0};
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], S.ev[i], S.ev[i + 1]);
+    res.timings = svlf_timings{t[0], 0.f, t[1], t[2], t[3], t[4], t[0] + t[1] + t[2] + t[3] + t[4],
+                               (long long)hm.active, 0, 0};
     return res;
 }
 

@@ -6,7 +6,10 @@
 namespace svlfb {
 
 // A supervised ray batch resident on the device plus its traversal output
-// (per-ray segments of sorted hits, see TraverseOut).
+// (per-ray segments of sorted hits, see TraverseOut). The hit count is never
+// read on the host: trav_counters[0] is the number of hits, trav_counters[2]
+// is set when the traversal overflowed hit_cap (the step then skips its
+// optimizer update and reports the overflow so the caller re-runs it).
 struct TrainBatchDev {
     const double* rays;      // n x 6
     const float* c_gt;       // n x 3
@@ -18,7 +21,19 @@ struct TrainBatchDev {
     const uint32_t* hit_leaf;
     const double* hit_tin;
     const double* hit_tout;
-    uint32_t total_hits;
+    const uint32_t* trav_counters;
+    uint32_t hit_cap;
+};
+
+// In-place all-reduce used by the data-parallel step (enqueued on stream s).
+// NCCL (ncclAllReduce over NVLink) in production; a host-staged variant lets a
+// CPU-side framework (gloo, MPI) or a test drive the same exchange.
+enum class CollType { F32, F64, U8 };
+enum class CollOp { Sum, Max };
+struct Collective {
+    int rank = 0, world = 1;
+    virtual ~Collective() = default;
+    virtual void allreduce(void* dev, size_t count, CollType t, CollOp op, cudaStream_t s) = 0;
 };
 
 struct TrainOptions {
@@ -27,10 +42,13 @@ struct TrainOptions {
     bool adam;          // false: loss + gradients only
     svlf_loss_weights lw;
     float lr;
-    void* nccl_comm = nullptr;  // ncclComm_t: data-parallel gradient exchange when set
-    int world = 1;
-    bool tf32 = false;          // weight-gradient GEMMs on tensor cores (TF32 operands)
-    bool tf32x3 = false;        // every GEMM as hi*hi + hi*lo + lo*hi of TF32 splits (tensor cores)
+    Collective* coll = nullptr;  // data-parallel gradient exchange when set
+    bool tf32 = false;           // weight-gradient GEMMs with plain TF32 operands (16-bit tolerance)
+};
+
+// Adam hyperparameters of one ModelAdam tensor (AdamState, mlp.hpp:117-128)
+struct AdamHyper {
+    float beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f;
 };
 
 struct TrainModelRefs {
@@ -40,34 +58,51 @@ struct TrainModelRefs {
     float* adam_m;
     float* adam_v;
     size_t n_ft, n_fc;
-    uint64_t* steps;  // 14 Adam step counters (host), ModelAdam order
-    DecPackF32 pack;  // transposed fp32 decoders (current version)
+    const uint64_t* steps;    // 14 Adam step counters (host), ModelAdam order; advanced by the caller
+    const AdamHyper* hyper;   // 14 entries, ModelAdam order
 };
+
+// Status bits of a step (TrainResult::flags)
+// kStepHitOverflow: the traversal's hit buffers or the per-active-hit matrices were too small;
+// kStepRowOverflow: the exchanged-row buffer was (data parallel). Both grow before the re-run.
+enum : uint32_t { kStepHitOverflow = 1u, kStepRowOverflow = 2u };
 
 struct TrainResult {
     double loss = 0;
     long long rays = 0, skipped = 0, eta_skipped = 0;
-    int error = 0;
+    int error = 0;            // device error code (tangent ray, ...); the update was skipped
+    uint32_t flags = 0;       // kStep* overflow bits (any rank); the update was skipped, re-run the step
+    uint32_t hits = 0;        // traversal hits (this rank)
+    uint32_t active = 0;      // active hits (this rank)
+    uint32_t touched_rows = 0;  // feature rows exchanged (data-parallel; union over ranks)
+    bool updated = false;     // Adam ran (advance the step counters)
     svlf_timings timings{};
-    long long exchanged_rows = 0;  // feature rows all-reduced (data-parallel)
 };
 
 struct TrainScratch {
     DevBuf c_gt, depth, alpha;                                    // uploaded supervision
     DevBuf act_first, act_cnt, dpos, surf_rel, eta_gt, ray_loss;  // per ray
     DevBuf dhit, dray, hitf, hitd;                                // per active hit
-    DevBuf acts, deltas;                                          // feature-major scratch
-    DevBuf scan_tmp, counters, loss_out;
+    DevBuf acts, deltas, dxs;                                     // feature-major matrices (row stride ld)
+    DevBuf scan_tmp, counters, loss_out, status;
     DevBuf touched, rows, n_rows, packed, red;  // sparse feature-gradient exchange
-    DevBuf dxs, ones;                           // layer-0 input gradients, ones vector (bias sums)
-    DevBuf wimg;                                // 3xTF32 weight image (gemm_x3.cu)
-    void* blas = nullptr;                       // cublasHandle_t (fp32 dense-layer GEMMs)
-    int* h_pinned = nullptr;
+    DevBuf wimg, dw_part;                       // weight images, weight-gradient partials (gemm_x3.cu)
+    uint32_t rows_cap = 0;                      // capacity of the exchanged-row buffer (grows on overflow)
+    uint32_t act_cap = 0;                       // capacity of the per-active-hit matrices (grows on overflow)
+    uint64_t* h_mail = nullptr;                 // pinned readback mailbox (one sync per step)
     cudaEvent_t ev[8] = {};
     ~TrainScratch();
 };
 
-TrainResult run_train_step(TrainScratch& S, const DevOctree& T, TrainModelRefs& M, const TrainBatchDev& b,
+// Enqueues the whole step (no host round trip) and synchronizes once at the
+// end to read the loss, the statistics and the status.
+TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModelRefs& M, const TrainBatchDev& b,
                            const TrainOptions& o, cudaStream_t s, int* err_flag);
+
+// Dense Adam over the model with the gradients currently in M.grads
+// (adam_model_step, src/train.cpp:345-360), enqueued on s; skipped on the
+// device when *skip_if is non-zero (skip_if may be null).
+void launch_adam(const TrainModelRefs& M, bool color_frozen, float lr, const uint32_t* skip_if, const int* err,
+                 cudaStream_t s);
 
 }  // namespace svlfb

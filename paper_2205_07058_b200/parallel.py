@@ -47,3 +47,32 @@ def init_data_parallel(ctx, dist=None) -> bool:
     dist.broadcast_object_list(obj, src=0)
     ctx.attach_nccl(obj[0], rank, world)
     return True
+
+
+def init_data_parallel_host(ctx, dist=None, group=None) -> bool:
+    """Attach a host-staged all-reduce (torch.distributed, e.g. the gloo
+    backend) to `ctx` instead of NCCL: the library stages each exchange buffer
+    in page-locked host memory and this callback reduces it in place. Same
+    exchange, same results; used where NCCL peers are unavailable (CPU-side
+    frameworks, tests with several ranks on one GPU). Returns False when
+    torch.distributed is not initialised."""
+    import numpy as np
+    import torch
+
+    if dist is None:
+        import torch.distributed as dist
+    if not dist.is_initialized():
+        return False
+    ops = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX}
+
+    def allreduce(buf: np.ndarray, op: str):
+        t = torch.from_numpy(buf)  # shares the staging memory
+        if buf.dtype == np.uint8:  # gloo has no uint8 max: reduce a wider copy
+            w = t.to(torch.int32)
+            dist.all_reduce(w, op=ops[op], group=group)
+            t.copy_(w.to(torch.uint8))
+        else:
+            dist.all_reduce(t, op=ops[op], group=group)
+
+    ctx.attach_host_collective(allreduce, dist.get_rank(group), dist.get_world_size(group))
+    return True

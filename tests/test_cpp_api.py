@@ -140,9 +140,9 @@ def test_cpp_train_matches_oracle(tmp_path, oracle):
     losses_x3 = _load(tmp_path, "losses_x3.f64", np.float64)
     assert abs(losses_x3[0] - loss) <= 1e-6 * abs(loss)  # 3xTF32 GEMMs: the same fp32 gate
     # Adam's first steps move a parameter by ~lr * sign(g), so gradients near zero can flip a
-    # few elements by up to 2 lr; the share of such elements is the gate (looser for 3xTF32,
-    # whose gradients differ by ~1e-6 rel-L2 instead of ~1e-7)
-    for name, share in (("params2.f32", 1e-3), ("params2_device.f32", 1e-3), ("params2_x3.f32", 5e-3)):
+    # few elements by up to 2 lr; the share of such elements is the gate (the 3xTF32 dense layers'
+    # gradients differ from the reference's by ~1e-6 rel-L2)
+    for name, share in (("params2.f32", 5e-3), ("params2_device.f32", 5e-3), ("params2_x3.f32", 5e-3)):
         got = _split(_load(tmp_path, name, np.float32), V)
         for a, b in zip(got, p):
             diff = np.abs(a - b)
