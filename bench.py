@@ -195,17 +195,16 @@ def cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
+    frame = None
     if O.reference_available():
         R = O.Reference()
         kind = "reference"
         tree = R.tree_build(pts, res, dil)
         model = R.init_model(tree, 1)
-        hm = R._with_model(tree, model)
         secs = []
-        for _ in range(frames):
-            s, st = R.time_render(hm, cam, W, H, parallel=True)
-            secs.append(s)
-        R.lib.ref_model_free(hm)
+        for _ in range(frames):  # render_frame timed inside the library (steady_clock), output kept for parity
+            frame = R.render_frame(tree, model, cam, W, H)
+            secs.append(R.last_seconds)
         cores = R.thread_count()
     else:
         R = O.Oracle()
@@ -215,13 +214,44 @@ def cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1):
         secs = []
         for _ in range(frames):
             t0 = time.perf_counter()
-            R.render_frame(tree, model, cam, W, H)
+            frame = R.render_frame(tree, model, cam, W, H)
             secs.append(time.perf_counter() - t0)
         cores = os.cpu_count()
     s = min(secs)
     return {"value": round(W * H / s / 1e6, 4), "unit": "Mrays/s", "cores": cores, "kind": kind,
             "sample": f"{frames} full {W}x{H} frame(s) of the same workload, render_frame, best of {frames}",
-            "seconds_per_frame": round(s, 3), **host_cpu()}
+            "seconds_per_frame": round(s, 3), **host_cpu()}, frame
+
+
+def frame_parity(P, model, camera, gpu_frame, precision, ref_frame, ref_kind):
+    """The timed frame (and an fp32 frame of the same model/camera) against the reference's
+    frame of the same workload: max-abs per output, PSNR, statistics equal (north_star gates:
+    fp32 max-abs <= 1e-3; 16-bit modes within 0.05 dB of the fp32 reference's PSNR)."""
+    rgb_r, a_r, d_r, st_r = ref_frame
+
+    def psnr(x, y):
+        mse = float(np.mean((np.asarray(x, np.float64) - y) ** 2))
+        return None if mse == 0 else round(10 * np.log10(1.0 / mse), 3)
+
+    def cmp(f, st):
+        rgb, a, d = (np.asarray(x).reshape(-1) for x in f)
+        # depth = alpha > 1e-4 ? d / alpha : 0 (src/render.cpp:190): a pixel whose alpha lands on the
+        # other side of the threshold changes depth by the whole depth; counted separately
+        flip = (a > 1e-4) != (a_r > 1e-4)
+        return {"rgb_max_abs": float(np.abs(rgb - rgb_r).max()), "alpha_max_abs": float(np.abs(a - a_r).max()),
+                "depth_max_abs": float(np.abs(d - d_r).max()),
+                "depth_max_abs_excl_threshold_flips": float(np.abs(d - d_r)[~flip].max()),
+                "alpha_threshold_flips": int(flip.sum()), "psnr_vs_reference_db": psnr(rgb, rgb_r),
+                "stats_equal": [st.rays, st.rays_with_hits, st.traversal_hits, st.thickness_queries,
+                                st.color_queries] == [int(x) for x in st_r]}
+
+    st32 = P.RenderStats()
+    f32 = P.render_frame(model, camera, stats=st32, precision="fp32")
+    out = {"reference": f"oracle/_ref render_frame ({ref_kind})", "fp32": cmp(f32, st32),
+           precision: cmp(gpu_frame[:3], gpu_frame[3])}
+    out["fp32"]["pass"] = out["fp32"]["stats_equal"] and max(
+        out["fp32"][k] for k in ("rgb_max_abs", "alpha_max_abs", "depth_max_abs")) <= 1e-3
+    return out
 
 
 def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=None, world=1):
@@ -576,7 +606,11 @@ def main():
     }
     if not args.no_cpu_baseline and world == 1:
         try:
-            line["cpu_baseline"] = cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1)
+            line["cpu_baseline"], ref_frame = cpu_baseline_sample(pts, res, dil, cam, W, H, frames=1)
+            st = P.RenderStats()
+            gpu = P.render_frame(model, camera, stats=st, precision=precision)
+            line["parity"] = frame_parity(P, model, camera, (*gpu, st), precision, ref_frame,
+                                          line["cpu_baseline"]["kind"])
         except Exception as e:  # reported, never silently dropped
             line["cpu_baseline"] = {"error": str(e)}
     if train is not None:
