@@ -107,8 +107,20 @@ def dist_init():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl" if os.environ.get("SVLF_BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+        dist.init_process_group("gloo" if SHARE_DEVICE or os.environ.get("SVLF_BENCH_BACKEND") == "gloo" else "nccl")
     return world, rank, local, dist
+
+
+# Validation of the multi-rank code paths on a one-GPU box: every rank on cuda:0,
+# torch.distributed over gloo and the library's exchange host-staged (numbers
+# from such a run are not multi-GPU measurements).
+SHARE_DEVICE = os.environ.get("SVLF_BENCH_SHARE_DEVICE") == "1"
+
+
+def attach_exchange(ctx, dist):
+    from paper_2205_07058_b200.parallel import init_data_parallel, init_data_parallel_host
+
+    return init_data_parallel_host(ctx, dist) if SHARE_DEVICE else init_data_parallel(ctx, dist)
 
 
 def max_over_ranks(x: float, dist, device):
@@ -116,7 +128,7 @@ def max_over_ranks(x: float, dist, device):
         return x
     import torch
 
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_DEVICE else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -261,10 +273,9 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
     library all-reduces loss, decoder gradients and touched feature rows over NCCL before the
     replicated Adam step (weak scaling; value = N * 2^18 / max-over-ranks step time)."""
     import paper_2205_07058_b200.synthetic as S
-    from paper_2205_07058_b200.parallel import init_data_parallel
 
     if world > 1:
-        init_data_parallel(ctx, dist)
+        attach_exchange(ctx, dist)
 
     sc, cam, pts, res, dil, rays, cgt, depth, alpha = S.c3_workload()
     tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
@@ -378,6 +389,124 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
     return out
 
 
+def bench_c4(P, torch, device, stream, ctx, model, sc_cams, W, H, precision, dist=None, world=1, rank=0):
+    """C4: the 150-view 1600^2 batch (hemisphere views of the C2 scene, octree and model replicated)
+    sharded across the ranks as whole views, round-robin (rank r renders views r, r + N, ...); one
+    step = the whole batch (strong scaling: value = 150 * W * H / max-over-ranks batch time). Plus
+    the C2 frame itself split across the ranks as round-robin 80 x 80 raster tiles
+    (svlf_render_tiles_device): single-frame latency at N GPUs. No collective on the data path."""
+    views = [P.Camera.from_record(c, W, H) for c in sc_cams]
+    mine = views[rank::world]
+    n = W * H
+    out_rgb = torch.empty(n * 3, dtype=torch.float32, device=device)
+    out_a = torch.empty(n, dtype=torch.float32, device=device)
+    out_d = torch.empty(n, dtype=torch.float32, device=device)
+    flush = torch.empty(l2_flush_bytes(device), dtype=torch.uint8, device=device)
+    st = P.RenderStats()
+
+    def frame(cam, stats=None):
+        P.render_frame_device(model, cam, out_rgb.data_ptr(), out_a.data_ptr(), out_d.data_ptr(), stats=stats,
+                              precision=precision)
+
+    with torch.cuda.stream(stream):
+        for cam in mine[:3]:
+            frame(cam)
+        flush.zero_()
+        stream.synchronize()
+        barrier(dist)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for cam in mine:
+            frame(cam, st)
+        b.record(stream)
+        stream.synchronize()
+    batch_ms = max_over_ranks(a.elapsed_time(b), dist, device)
+    out = {"metric": "rendered rays/s, C4: 150-view 1600x1600 batch, views round-robin across ranks",
+           "value": round(len(views) * n / (batch_ms * 1e-3) / 1e6, 3), "unit": "Mrays/s", "n_gpus": world,
+           "scaling": "strong", "views": len(views), "views_this_rank": len(mine),
+           "ms_per_batch": round(batch_ms, 3), "hits_per_ray_this_rank": round(st.traversal_hits / max(1, st.rays), 4),
+           "parallelism": f"replicated octree/model, whole views round-robin over {world} rank(s), no collective"}
+    # one frame as round-robin raster tiles
+    T = 80
+    k = P.tiles_owned(views[0], T, T, rank, world) if W % T == 0 and H % T == 0 else 0
+    if k:
+        m = k * T * T
+        tb = (torch.empty(m * 3, device=device), torch.empty(m, device=device), torch.empty(m, device=device))
+        tst = P.RenderStats()
+        cam0 = P.Camera.from_record(sc_cams[0], W, H)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                P.render_tiles_device(model, cam0, T, T, rank, world, *(x.data_ptr() for x in tb), precision=precision)
+            t = []
+            for _ in range(5):
+                flush.zero_()
+                stream.synchronize()
+                barrier(dist)
+                a.record(stream)
+                P.render_tiles_device(model, cam0, T, T, rank, world, *(x.data_ptr() for x in tb), stats=tst,
+                                      precision=precision)
+                b.record(stream)
+                stream.synchronize()
+                t.append(a.elapsed_time(b))
+        f_ms = max_over_ranks(statistics.median(t), dist, device)
+        out["frame_tiles"] = {"value": round(n / (f_ms * 1e-3) / 1e6, 3), "unit": "Mrays/s", "scaling": "strong",
+                              "ms_per_frame": round(f_ms, 4), "tile": T, "tiles_this_rank": k,
+                              "hits_this_rank": int(tst.traversal_hits / 5),
+                              "note": "one 1600^2 view split into 80x80 raster tiles dealt round-robin"}
+    return out
+
+
+def bench_c5(P, torch, device, stream, ctx, steps, dist=None, world=1, rank=0):
+    """C5: data-parallel training at octree depth 10 (res 1024; occupancy of the C3 frame): the
+    2^18-ray batch is split across the ranks (strong scaling: value = 2^18 / max-over-ranks step
+    time); each rank steps its shard and the library all-reduces loss, decoder gradients and the
+    union of touched feature rows (NCCL over NVLink) before the replicated Adam update."""
+    import paper_2205_07058_b200.synthetic as S
+    from paper_2205_07058_b200.parallel import shard_slice
+
+    sc, cam, pts, res, dil, rays, cgt, depth, alpha = S.c3_workload(res=1024)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=0, ctx=ctx)
+    if world > 1:
+        attach_exchange(ctx, dist)
+    sl = shard_slice(rays.shape[0], rank, world)
+    n = sl.stop - sl.start
+    d = [torch.from_numpy(np.ascontiguousarray(x[sl], dtype=dt)).to(device)
+         for x, dt in ((rays, np.float64), (cgt, np.float32), (depth, np.float64), (alpha, np.uint8))]
+    flush = torch.empty(l2_flush_bytes(device), dtype=torch.uint8, device=device)
+
+    def step():
+        return P.train_step_device(model, *(x.data_ptr() for x in d), n, mode="volumetric", lr=2e-4)
+
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            step()
+        stream.synchronize()
+        t, parts = [], []
+        for _ in range(steps):
+            flush.zero_()
+            barrier(dist)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            stream.synchronize()
+            t.append(a.elapsed_time(b))
+            parts.append(ctx.last_timings())
+    ms = max_over_ranks(statistics.median(t), dist, device)
+    if world > 1:
+        ctx.detach_nccl()
+    return {"metric": "train rays/s, C5: 2^18-ray batch split across ranks, octree depth 10",
+            "value": round(rays.shape[0] / (ms * 1e-3) / 1e6, 4), "unit": "Mrays/s", "n_gpus": world,
+            "scaling": "strong", "ms_per_step": round(ms, 4), "rays_this_rank": n,
+            "active_hits_this_rank": int(statistics.median(p["hits"] for p in parts)),
+            "leaves": int(tree.leaf_count), "vertices": int(tree.vertex_count),
+            "stages_ms": {k: round(statistics.median(p[k] for p in parts), 4)
+                          for k in ("traverse_ms", "decode_ms", "composite_ms", "backward_ms", "adam_ms")},
+            "parallelism": f"dp{world}: NCCL all-reduce of loss, decoder grads and touched feature rows"
+                           if world > 1 else "single rank (no exchange)"}
+
+
 def run_reference(args):
     world, rank, local, dist = dist_init()
     if rank != 0:
@@ -444,6 +573,7 @@ def main():
     world, rank, local, dist = dist_init()
     import torch
 
+    local = 0 if SHARE_DEVICE else local
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     import paper_2205_07058_b200 as P
@@ -545,8 +675,22 @@ def main():
     e2e_step = max_over_ranks(statistics.median(pipe_ms), dist, device)
     e2e_value = world * n / (e2e_step * 1e-3) / 1e6
 
+    import paper_2205_07058_b200.synthetic as S
+
+    c4 = None
+    try:
+        c4_cams = S.hemisphere_cameras(150, 1.8, 7, W, H, 1.5 * W)
+        c4 = bench_c4(P, torch, device, stream, ctx, model, c4_cams, W, H, precision, dist=dist, world=world,
+                      rank=rank)
+    except Exception as e:
+        c4 = {"error": str(e)}
     train = None
+    c5 = None
     if not args.no_train:
+        try:
+            c5 = bench_c5(P, torch, device, stream, ctx, max(3, args.steps), dist=dist, world=world, rank=rank)
+        except Exception as e:
+            c5 = {"error": str(e)}
         try:
             train = bench_train(P, torch, device, stream, ctx, max(3, args.steps), 3,
                                 cpu=not args.no_cpu_baseline and world == 1 and rank == 0, dist=dist, world=world)
@@ -615,6 +759,10 @@ def main():
             line["cpu_baseline"] = {"error": str(e)}
     if train is not None:
         line["train"] = train
+    if c4 is not None:
+        line["c4"] = c4
+    if c5 is not None:
+        line["c5"] = c5
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

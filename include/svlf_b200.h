@@ -254,6 +254,17 @@ svlf_status svlf_render_frame_device(svlf_ctx* ctx, svlf_model* model, const svl
                                      svlf_render_stats* stats);
 /* Sub-rectangle of rows [row0, row0+rows) of the camera's image (tile
  * sharding across ranks); output buffers hold W*rows pixels. Device buffers. */
+/* Tile-interleaved share of one frame (multi-GPU render of a frame, SURVEY.md
+ * §8(e)): the image is cut into tile_w x tile_h tiles (both must divide the
+ * image size) numbered in raster order; rank r renders tiles r, r + world,
+ * r + 2 world, ... (svlf_tiles_owned of them). Output buffers hold those tiles
+ * in that order, each tile_w x tile_h row-major. Device buffers; bit-identical
+ * to the same pixels of a full frame. */
+svlf_status svlf_render_tiles_device(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam, uint32_t tile_w,
+                                     uint32_t tile_h, uint32_t rank, uint32_t world, const float* background,
+                                     svlf_precision precision, float* d_rgb, float* d_alpha, float* d_depth,
+                                     svlf_render_stats* stats);
+size_t svlf_tiles_owned(const svlf_camera* cam, uint32_t tile_w, uint32_t tile_h, uint32_t rank, uint32_t world);
 svlf_status svlf_render_rows_device(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
                                     uint32_t row0, uint32_t rows, const float* background,
                                     svlf_precision precision, float* d_rgb, float* d_alpha,

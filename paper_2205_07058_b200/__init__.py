@@ -228,6 +228,9 @@ def load_library():
         "svlf_render_frame": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
         "svlf_render_frame_device": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp,
                                       C.POINTER(_RenderStats)], st),
+        "svlf_render_tiles_device": ([vp, vp, C.POINTER(_Camera), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                      vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
+        "svlf_tiles_owned": ([C.POINTER(_Camera), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32], sz),
         "svlf_render_rows_device": ([vp, vp, C.POINTER(_Camera), C.c_uint32, C.c_uint32, vp, C.c_int, vp, vp, vp,
                                      C.POINTER(_RenderStats)], st),
         "svlf_render_rays": ([vp, vp, vp, sz, vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
@@ -742,6 +745,28 @@ def render_frame_device(model: Model, camera: Camera, d_rgb: int, d_alpha: int, 
     _check(_LIB.svlf_render_rows_device(model.ctx.handle, model.handle, C.byref(cam), row0, rows, bgp,
                                         _PREC[precision], C.c_void_p(d_rgb), C.c_void_p(d_alpha),
                                         C.c_void_p(d_depth), C.byref(st)))
+    _add_stats(stats, st)
+
+
+def tiles_owned(camera: Camera, tile_w: int, tile_h: int, rank: int, world: int) -> int:
+    """Tiles rank renders in a tile-interleaved split of the frame (0 if the tile size does not
+    divide the image)."""
+    load_library()
+    cam = camera._c()
+    return int(_LIB.svlf_tiles_owned(C.byref(cam), tile_w, tile_h, rank, world))
+
+
+def render_tiles_device(model: Model, camera: Camera, tile_w: int, tile_h: int, rank: int, world: int,
+                        d_rgb: int, d_alpha: int, d_depth: int, stats: RenderStats | None = None,
+                        background=None, precision: str = "fp32"):
+    """Rank's share of a tile-interleaved multi-GPU frame (tiles rank, rank + world, ...) into
+    device buffers of tiles_owned(...) * tile_w * tile_h pixels, tile by tile."""
+    st = _RenderStats()
+    keep, bgp = _bg(background)
+    cam = camera._c()
+    _check(_LIB.svlf_render_tiles_device(model.ctx.handle, model.handle, C.byref(cam), tile_w, tile_h, rank, world,
+                                         bgp, _PREC[precision], C.c_void_p(d_rgb), C.c_void_p(d_alpha),
+                                         C.c_void_p(d_depth), C.byref(st)))
     _add_stats(stats, st)
 
 

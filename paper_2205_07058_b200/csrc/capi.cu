@@ -430,6 +430,34 @@ void render_pipeline(svlf_ctx* ctx, svlf_model* m, const DevCamera* cam, uint32_
     fail(SVLF_ERR_RUNTIME, "traversal output capacity could not be satisfied");
 }
 
+// Tiles of rank `rank` in a tile-interleaved split of the image across `world` ranks.
+uint32_t owned_tiles(const svlf_camera& c, uint32_t tw, uint32_t th, uint32_t rank, uint32_t world) {
+    const uint32_t total = (c.width / tw) * (c.height / th);
+    return rank < total ? (total - 1 - rank) / world + 1 : 0;
+}
+
+void render_tiles_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_t tw, uint32_t th,
+                         uint32_t rank, uint32_t world, const float* bg, svlf_precision prec, float* d_rgb,
+                         float* d_alpha, float* d_depth, svlf_render_stats* stats) {
+    require(cam != nullptr, "camera is null");
+    require(tw > 0 && th > 0 && cam->width % tw == 0 && cam->height % th == 0,
+            "tile size must divide the image size");
+    require(world >= 1 && rank < world, "bad rank/world");
+    const uint32_t k = owned_tiles(*cam, tw, th, rank, world);
+    const uint64_t n64 = uint64_t(k) * tw * th;
+    require(n64 < (1ull << 31), "too many pixels in one call");
+    if (n64 == 0) return;
+    DevCamera dc = to_dev_camera(*cam);
+    dc.width = tw;  // ray index space: this rank's tiles stacked vertically
+    dc.height = k * th;
+    dc.tile_w = tw;
+    dc.tile_h = th;
+    dc.tiles_x = cam->width / tw;
+    dc.tiles_rank = rank;
+    dc.tiles_world = world;
+    render_pipeline(ctx, m, &dc, 0, k * th, uint32_t(n64), bg, prec, d_rgb, d_alpha, d_depth, stats);
+}
+
 void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_t row0, uint32_t rows,
                    const float* bg, svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth,
                    svlf_render_stats* stats) {
@@ -1263,6 +1291,23 @@ svlf_status svlf_render_rows_device(svlf_ctx* ctx, svlf_model* m, const svlf_cam
         std::lock_guard<std::mutex> lk(ctx->mu);
         render_device(ctx, m, cam, row0, rows, bg, prec, d_rgb, d_alpha, d_depth, stats);
     });
+}
+
+svlf_status svlf_render_tiles_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_t tile_w,
+                                     uint32_t tile_h, uint32_t rank, uint32_t world, const float* bg,
+                                     svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth,
+                                     svlf_render_stats* stats) {
+    return guard([&] {
+        require(ctx && m && cam && d_rgb && d_alpha && d_depth, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        render_tiles_device(ctx, m, cam, tile_w, tile_h, rank, world, bg, prec, d_rgb, d_alpha, d_depth, stats);
+    });
+}
+
+size_t svlf_tiles_owned(const svlf_camera* cam, uint32_t tile_w, uint32_t tile_h, uint32_t rank, uint32_t world) {
+    if (!cam || !tile_w || !tile_h || !world || cam->width % tile_w || cam->height % tile_h) return 0;
+    return owned_tiles(*cam, tile_w, tile_h, rank, world);
 }
 
 svlf_status svlf_render_frame(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg,

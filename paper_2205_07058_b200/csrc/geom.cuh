@@ -55,11 +55,34 @@ __device__ __forceinline__ void ray_at(const Ray& r, double t, double* p) {
 
 // Camera::pixel_ray (camera.hpp:26-29): pixel centre, row-major c2w rotation,
 // normalized() = three true divisions by sqrt(dot(v, v)).
+// width = the row length of the ray index space (the image width, or the tile
+// width in tile-interleaved mode); tiles_world != 0 selects the interleaved
+// mapping of cam_pixel.
 struct DevCamera {
     double fx, fy, cx, cy;
     double m[16];
     uint32_t width, height;
+    uint32_t tile_w = 0, tile_h = 0, tiles_x = 0, tiles_rank = 0, tiles_world = 0;
 };
+
+// Pixel of ray index gi of a pass over rows [row0, ...) of the ray index space.
+// Plain: pixel (gi % width, row0 + gi / width). Tile-interleaved (multi-GPU
+// render of one frame): the image is cut into tile_w x tile_h tiles numbered in
+// raster order and rank r owns tiles r, r + world, r + 2 world, ...; its index
+// space stacks them vertically (tile j at rows j*tile_h ..), so every 8 x 4
+// traversal block stays inside one tile.
+__device__ __forceinline__ void cam_pixel(const DevCamera& c, uint32_t gi, uint32_t row0, uint32_t& ix,
+                                          uint32_t& iy) {
+    const uint32_t vx = gi % c.width, vy = row0 + gi / c.width;
+    if (c.tiles_world == 0) {
+        ix = vx;
+        iy = vy;
+        return;
+    }
+    const uint32_t j = vy / c.tile_h, t = c.tiles_rank + c.tiles_world * j;
+    ix = (t % c.tiles_x) * c.tile_w + vx;
+    iy = (t / c.tiles_x) * c.tile_h + vy % c.tile_h;
+}
 
 __device__ __forceinline__ Ray pixel_ray(const DevCamera& c, uint32_t ix, uint32_t iy) {
     const double v[3] = {ddiv(dsub(dadd(double(ix), 0.5), c.cx), c.fx),

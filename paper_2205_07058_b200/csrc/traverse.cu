@@ -342,10 +342,13 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         if (ok) {
             my_ray = gi;
             Ray r;
-            if constexpr (kCamera)
-                r = pixel_ray(cam, gi % cam.width, row0 + gi / cam.width);
-            else
+            if constexpr (kCamera) {
+                uint32_t ix, iy;
+                cam_pixel(cam, gi, row0, ix, iy);
+                r = pixel_ray(cam, ix, iy);
+            } else {
                 r = load_ray(A.rays, gi);
+            }
             const RayPre p = precompute(r);
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -634,7 +637,9 @@ __device__ __forceinline__ void fallback_ray(const DevOctree& T, const DevCamera
     if (i == 0xffffffffu) return;
     Ray r;
     if constexpr (kCamera) {
-        r = pixel_ray(cam, i % cam.width, row0 + i / cam.width);
+        uint32_t ix, iy;
+        cam_pixel(cam, i, row0, ix, iy);
+        r = pixel_ray(cam, ix, iy);
     } else {
         r = load_ray(A.rays, i);
     }

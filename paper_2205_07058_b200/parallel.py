@@ -1,8 +1,10 @@
 """Multi-GPU plumbing for the SVLF path.
 
 * Render shards with no collective: the octree and model are replicated and
-  each rank renders its own frames (weak scaling) or a row band of one frame
-  (`row_band`, strong scaling), written into its own buffers.
+  each rank renders its own frames / views (weak scaling; a view batch split
+  round-robin), or its tiles of one frame (`render_tiles_device`: raster tiles
+  dealt round-robin, so clustered foreground spreads over the ranks; or a
+  contiguous `row_band`), written into its own buffers.
 * Training is data-parallel: the ray batch is split across ranks
   (`shard_slice`); each rank's train step computes loss and gradients of its
   shard, and the library all-reduces them over NCCL (decoders densely,
@@ -29,6 +31,23 @@ def row_band(height: int, rank: int, world: int) -> tuple[int, int]:
     """(row0, rows) of rank's band of an image, balanced to within one row."""
     s = shard_slice(height, rank, world)
     return s.start, s.stop - s.start
+
+
+def tile_origins(width: int, height: int, tile_w: int, tile_h: int, rank: int, world: int):
+    """(x0, y0) of the tiles rank owns in a tile-interleaved split of a frame, in the order
+    render_tiles_device writes them: raster tile numbers rank, rank + world, ..."""
+    tx = width // tile_w
+    total = tx * (height // tile_h)
+    return [((t % tx) * tile_w, (t // tx) * tile_h) for t in range(rank, total, world)]
+
+
+def stitch_tiles(image, tiles, width: int, height: int, tile_w: int, tile_h: int, rank: int, world: int):
+    """Write rank's tiles (array of k*tile_h*tile_w pixels, any trailing channel dims) into
+    `image` (height x width x ...)."""
+    t = tiles.reshape(-1, tile_h, tile_w, *image.shape[2:])
+    for k, (x0, y0) in enumerate(tile_origins(width, height, tile_w, tile_h, rank, world)):
+        image[y0:y0 + tile_h, x0:x0 + tile_w] = t[k]
+    return image
 
 
 def init_data_parallel(ctx, dist=None) -> bool:

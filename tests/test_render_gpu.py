@@ -349,3 +349,46 @@ def test_row_band_shards_stitch_to_the_full_frame(ctx, precision, world):
     for a, b in zip(full, parts):
         assert torch.equal(a, b)
     assert float(full[1].sum()) > 0  # the frame has foreground
+
+
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+@pytest.mark.parametrize("world,tile", [(1, 32), (2, 16), (3, 32), (8, 8)])
+def test_tile_interleaved_shards_stitch_to_the_full_frame(ctx, precision, world, tile):
+    """one frame split across ranks as round-robin raster tiles
+    (svlf_render_tiles_device); every rank's tiles, stitched, are bit-identical to the full frame,
+    with RenderStats summing to the frame's. Round-robin tiles spread a clustered foreground over
+    the ranks (the per-rank hit counts are reported)."""
+    import torch
+    from paper_2205_07058_b200.parallel import stitch_tiles
+
+    sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=4, n_views=8, view_res=96, res=64, width=160)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    camera = P.Camera.from_record(cam, W, H)
+    n = W * H
+    full = (torch.zeros(n * 3, device="cuda"), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda"))
+    fst = P.RenderStats()
+    P.render_frame_device(model, camera, *(b.data_ptr() for b in full), stats=fst, precision=precision)
+    img = [np.zeros((H, W, 3), np.float32), np.zeros((H, W), np.float32), np.zeros((H, W), np.float32)]
+    tot = P.RenderStats()
+    hits = []
+    for rank in range(world):
+        k = P.tiles_owned(camera, tile, tile, rank, world)
+        m = k * tile * tile
+        b = (torch.zeros(max(m, 1) * 3, device="cuda"), torch.zeros(max(m, 1), device="cuda"),
+             torch.zeros(max(m, 1), device="cuda"))
+        st = P.RenderStats()
+        P.render_tiles_device(model, camera, tile, tile, rank, world, *(x.data_ptr() for x in b), stats=st,
+                              precision=precision)
+        torch.cuda.synchronize()
+        for dst, src in zip(img, b):
+            stitch_tiles(dst, src[:m * (3 if dst.ndim == 3 else 1)].cpu().numpy(), W, H, tile, tile, rank, world)
+        for f in ("rays", "rays_with_hits", "traversal_hits", "thickness_queries", "color_queries"):
+            setattr(tot, f, getattr(tot, f) + getattr(st, f))
+        hits.append(st.traversal_hits)
+    print(f"world {world} tile {tile}: hits per rank {hits}")
+    for a, b in zip(full, img):
+        assert np.array_equal(a.cpu().numpy().reshape(b.shape), b)
+    assert (tot.rays, tot.rays_with_hits, tot.traversal_hits) == (fst.rays, fst.rays_with_hits, fst.traversal_hits)
+    with pytest.raises(ValueError):
+        P.render_tiles_device(model, camera, 7, 7, 0, world, *(x.data_ptr() for x in full))
