@@ -456,6 +456,48 @@ def bench_c4(P, torch, device, stream, ctx, model, sc_cams, W, H, precision, dis
     return out
 
 
+def bench_c2_dense(P, torch, device, stream, ctx, steps, precision, dist=None, world=1):
+    """C2': the same 1600^2 frame of the 20-object scene (make_random_scene(7, 20): the
+    Google-Scanned-like case, ~10 hits per ray, decode-dominated), one frame per rank per step,
+    L2 flushed between steps; per-stage times and the decode roofline."""
+    pts, res, dil, cam, W, H = workload(20, ctx)
+    tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
+    model = P.Model(tree, seed=1, ctx=ctx)
+    camera = P.Camera.from_record(cam, W, H)
+    n = W * H
+    b = (torch.empty(n * 3, device=device), torch.empty(n, device=device), torch.empty(n, device=device))
+    flush = torch.empty(l2_flush_bytes(device), dtype=torch.uint8, device=device)
+    st = P.RenderStats()
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            P.render_frame_device(model, camera, *(x.data_ptr() for x in b), precision=precision)
+        t, parts = [], []
+        for _ in range(steps):
+            flush.zero_()
+            stream.synchronize()
+            barrier(dist)
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            P.render_frame_device(model, camera, *(x.data_ptr() for x in b), stats=st, precision=precision)
+            e.record(stream)
+            stream.synchronize()
+            t.append(a.elapsed_time(e))
+            parts.append(ctx.last_timings())
+    ms = max_over_ranks(statistics.median(t), dist, device)
+    hits = st.traversal_hits / steps
+    stage = {k: round(statistics.median(p[k] for p in parts), 4)
+             for k in ("traverse_ms", "emit_ms", "decode_ms", "composite_ms")}
+    peaks, _ = load_peaks()
+    peak = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])
+    tf = hits * FLOP_PER_HIT / (stage["decode_ms"] * 1e-3) / 1e12
+    return {"metric": "rendered rays/s at 1600x1600, C2': 20-object scene", "value": round(world * n / (ms * 1e-3) / 1e6, 3),
+            "unit": "Mrays/s", "ms_per_step": round(ms, 4), "scaling": "weak", "leaves": int(tree.leaf_count),
+            "vertices": int(tree.vertex_count), "hits_per_ray": round(hits / n, 4),
+            "foreground_fraction": round(st.rays_with_hits / steps / n, 4), "stages_ms": stage,
+            "decode_roofline": {"bound": "tensor", "achieved": round(tf, 2), "peak": peak, "unit": "TFLOP/s",
+                                "frac": round(tf / peak, 4)}, "precision": precision}
+
+
 def bench_c5(P, torch, device, stream, ctx, steps, dist=None, world=1, rank=0):
     """C5: data-parallel training at octree depth 10 (res 1024; occupancy of the C3 frame): the
     2^18-ray batch is split across the ranks (strong scaling: value = 2^18 / max-over-ranks step
@@ -684,6 +726,10 @@ def main():
                       rank=rank)
     except Exception as e:
         c4 = {"error": str(e)}
+    try:
+        c2_dense = bench_c2_dense(P, torch, device, stream, ctx, args.steps, precision, dist=dist, world=world)
+    except Exception as e:
+        c2_dense = {"error": str(e)}
     train = None
     c5 = None
     if not args.no_train:
@@ -759,6 +805,7 @@ def main():
             line["cpu_baseline"] = {"error": str(e)}
     if train is not None:
         line["train"] = train
+    line["c2_20_objects"] = c2_dense
     if c4 is not None:
         line["c4"] = c4
     if c5 is not None:

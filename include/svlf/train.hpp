@@ -15,6 +15,7 @@
 
 #include "svlf/dataset.hpp"
 #include "svlf/model.hpp"
+#include "svlf/render.hpp"
 
 namespace svlf {
 
@@ -24,6 +25,11 @@ struct RaySupervision {
     double depth_gt = 0;  // Euclidean depth along the ray, 0 = background
     bool alpha_gt = false;
 };
+
+// Within-voxel depth target (train.hpp:38-41): (t_out - depth) / (t_out - t_in)
+// clamped to [0,1]; throws runtime_error("surface point outside voxel") beyond
+// 1e-6 (svlf_eta_gt).
+double eta_gt(const RayVoxelHit& hit, double depth_gt);
 
 struct LossWeights {
     double eta = 1.0;
@@ -37,6 +43,16 @@ struct LossStats {
     long long skipped_rays = 0;
     long long eta_skipped = 0;
 };
+
+// The reference's per-ray losses (train.hpp:56-71): loss of one ray with its
+// gradients ADDED into `grads` (null: loss only), through the GPU train
+// kernels (svlf_loss_grads on a one-ray batch). Float models only.
+template <typename T>
+double surface_loss(const SvlfModelT<T>& model, const RaySupervision& sup, const LossWeights& lw,
+                    ModelGradsT<T>* grads, LossStats* stats = nullptr);
+template <typename T>
+double volumetric_loss(const SvlfModelT<T>& model, const RaySupervision& sup, const LossWeights& lw,
+                       bool color_frozen, ModelGradsT<T>* grads, LossStats* stats = nullptr);
 
 enum class LossMode { Surface = 0, Volumetric = 1 };
 

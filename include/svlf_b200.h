@@ -179,6 +179,48 @@ typedef enum svlf_reduce_op { SVLF_REDUCE_SUM = 0, SVLF_REDUCE_MAX = 1 } svlf_re
 typedef int (*svlf_allreduce_fn)(void* user, void* host_buf, size_t count, svlf_dtype dtype, svlf_reduce_op op);
 svlf_status svlf_ctx_attach_collective(svlf_ctx* ctx, svlf_allreduce_fn fn, void* user, int rank, int world);
 
+/* ---- per-point / per-ray operations of the reference's public API, batched
+ * on the GPU (host buffers in and out; tests and debugging, not the frame or
+ * train paths, which fuse the same arithmetic). Single-point results are
+ * bit-identical to the reference built without FMA contraction. Errors carry
+ * the reference's messages: "point not in voxel" (runtime), "unknown voxel
+ * id" (out_of_range), "tangent ray" (runtime), "negative optical thickness"
+ * (invalid_argument), "surface point outside voxel" (runtime). */
+/* local_coords (features.hpp:69, src/features.cpp:22-31): u n x 3 */
+svlf_status svlf_local_coords(svlf_ctx* ctx, const svlf_octree* tree, const uint64_t* voxel_ids,
+                              const double* points, size_t n, double* u_out);
+/* interpolate (features.hpp:72-74, src/features.cpp:33-47) for a volume of
+ * `rows` x `dim` values (f32 or f64): out n x dim */
+svlf_status svlf_interpolate(svlf_ctx* ctx, const svlf_octree* tree, svlf_dtype dtype, const void* volume,
+                             uint32_t rows, uint32_t dim, const uint64_t* voxel_ids, const double* points, size_t n,
+                             void* out);
+/* interpolate_backward (features.hpp:76-80, src/features.cpp:49-84):
+ * grad_buf (rows x dim) += w_b * upstream (n x dim) per point (points that
+ * share a row are summed in an unspecified order); pos_jac (n x dim x 3,
+ * optional) = d z / d point */
+svlf_status svlf_interpolate_backward(svlf_ctx* ctx, const svlf_octree* tree, svlf_dtype dtype, const void* volume,
+                                      uint32_t rows, uint32_t dim, const uint64_t* voxel_ids, const double* points,
+                                      size_t n, const void* upstream, void* grad_buf, double* pos_jac);
+/* parameterize_ray (render.hpp:28, src/render.cpp:16-28): rays n x 6, boxes
+ * n x (lo xyz, hi xyz) -> n x (p1 xyz, p2 xyz) */
+svlf_status svlf_parameterize_rays(svlf_ctx* ctx, const double* rays, const double* boxes, size_t n, double* out6);
+/* composite (render.hpp:60-62, src/render.cpp:65-87) of n_lists sample lists
+ * (list l = samples offsets[l] .. offsets[l+1]-1): colour (3 per list) and
+ * alpha; weights (per sample) optional; with t_s (per sample) the expected
+ * depth of render_ray (src/render.cpp:106-114) into out_depth */
+svlf_status svlf_composite(svlf_ctx* ctx, const uint64_t* offsets, size_t n_lists, const double* taus,
+                           const double* colors, const double* t_s, double* out_color, double* out_alpha,
+                           double* out_depth, double* weights);
+/* evaluate_voxel (render.hpp:49-51, src/render.cpp:30-63) for n (ray, hit)
+ * pairs with the fp32 decoders: tau, eta, x_s (3), t_s = eta t_in + (1 - eta)
+ * t_out, colour (3); any output may be NULL */
+svlf_status svlf_evaluate_voxels(svlf_ctx* ctx, svlf_model* model, const double* rays, const uint64_t* voxel_ids,
+                                 const double* t_in, const double* t_out, size_t n, double* tau, double* eta,
+                                 double* x_s, double* t_s, double* color);
+/* eta_gt (train.hpp:41, src/train.cpp:30-35) */
+svlf_status svlf_eta_gt(svlf_ctx* ctx, const double* t_in, const double* t_out, const double* depth, size_t n,
+                        double* out);
+
 /* ---- octree: SparseOctree::build / from_leaves (octree.hpp:47,82; src/octree.cpp:30-142)
  * ctx may be NULL: the octree is then host-only and is uploaded to the device
  * of the first context that renders/traverses with it. */

@@ -228,6 +228,13 @@ def load_library():
         "svlf_render_frame": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
         "svlf_render_frame_device": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp,
                                       C.POINTER(_RenderStats)], st),
+        "svlf_local_coords": ([vp, vp, vp, vp, sz, vp], st),
+        "svlf_interpolate": ([vp, vp, C.c_int, vp, C.c_uint32, C.c_uint32, vp, vp, sz, vp], st),
+        "svlf_interpolate_backward": ([vp, vp, C.c_int, vp, C.c_uint32, C.c_uint32, vp, vp, sz, vp, vp, vp], st),
+        "svlf_parameterize_rays": ([vp, vp, vp, sz, vp], st),
+        "svlf_composite": ([vp, vp, sz, vp, vp, vp, vp, vp, vp, vp], st),
+        "svlf_evaluate_voxels": ([vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp], st),
+        "svlf_eta_gt": ([vp, vp, vp, vp, sz, vp], st),
         "svlf_render_tiles_device": ([vp, vp, C.POINTER(_Camera), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                       vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
         "svlf_tiles_owned": ([C.POINTER(_Camera), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32], sz),
@@ -746,6 +753,117 @@ def render_frame_device(model: Model, camera: Camera, d_rgb: int, d_alpha: int, 
                                         _PREC[precision], C.c_void_p(d_rgb), C.c_void_p(d_alpha),
                                         C.c_void_p(d_depth), C.byref(st)))
     _add_stats(stats, st)
+
+
+# ---- per-point / per-ray operations of the reference API (batched on the GPU) ----
+def _ctx_of(ctx):
+    return (ctx or default_context()).handle
+
+
+def local_coords(octree: SparseOctree, voxel_ids, points, ctx: Context | None = None) -> np.ndarray:
+    """local_coords (features.hpp:69) per point: n x 3."""
+    ids = np.ascontiguousarray(voxel_ids, dtype=np.uint64).reshape(-1)
+    p = _f64(points).reshape(-1, 3)
+    u = np.zeros((ids.size, 3))
+    _check(_LIB.svlf_local_coords(_ctx_of(ctx or octree.ctx), octree.handle, _dp(ids), _dp(p), ids.size, _dp(u)))
+    return u
+
+
+def _vol(volume):
+    v = np.ascontiguousarray(volume)
+    if v.dtype not in (np.float32, np.float64) or v.ndim != 2:
+        raise ValueError("volume must be a rows x dim float32 / float64 array")
+    return v, (0 if v.dtype == np.float32 else 1)
+
+
+def interpolate(volume, octree: SparseOctree, voxel_ids, points, ctx: Context | None = None) -> np.ndarray:
+    """interpolate (features.hpp:72) per point: n x dim in the volume's dtype."""
+    v, dt = _vol(volume)
+    ids = np.ascontiguousarray(voxel_ids, dtype=np.uint64).reshape(-1)
+    p = _f64(points).reshape(-1, 3)
+    out = np.zeros((ids.size, v.shape[1]), v.dtype)
+    _check(_LIB.svlf_interpolate(_ctx_of(ctx or octree.ctx), octree.handle, dt, _dp(v), v.shape[0], v.shape[1],
+                                 _dp(ids), _dp(p), ids.size, _dp(out)))
+    return out
+
+
+def interpolate_backward(volume, octree: SparseOctree, voxel_ids, points, upstream, grad_buf, with_jacobian=False,
+                         ctx: Context | None = None):
+    """interpolate_backward (features.hpp:76): grad_buf (rows x dim) += w * upstream in place;
+    returns the positional Jacobians (n x dim x 3) when asked."""
+    v, dt = _vol(volume)
+    ids = np.ascontiguousarray(voxel_ids, dtype=np.uint64).reshape(-1)
+    p = _f64(points).reshape(-1, 3)
+    up = np.ascontiguousarray(upstream, dtype=v.dtype).reshape(ids.size, v.shape[1])
+    if not (isinstance(grad_buf, np.ndarray) and grad_buf.dtype == v.dtype and grad_buf.shape == v.shape
+            and grad_buf.flags.c_contiguous):
+        raise ValueError("grad_buf must be a C-contiguous array shaped and typed like the volume")
+    jac = np.zeros((ids.size, v.shape[1], 3)) if with_jacobian else None
+    _check(_LIB.svlf_interpolate_backward(_ctx_of(ctx or octree.ctx), octree.handle, dt, _dp(v), v.shape[0],
+                                          v.shape[1], _dp(ids), _dp(p), ids.size, _dp(up), _dp(grad_buf),
+                                          _dp(jac) if jac is not None else None))
+    return jac
+
+
+def parameterize_rays(rays, boxes, ctx: Context | None = None) -> np.ndarray:
+    """parameterize_ray (render.hpp:28) per (ray, box (lo xyz, hi xyz)): n x 6 (p1, p2)."""
+    load_library()
+    r = _f64(rays).reshape(-1, 6)
+    b = _f64(boxes).reshape(-1, 6)
+    out = np.zeros((r.shape[0], 6))
+    _check(_LIB.svlf_parameterize_rays(_ctx_of(ctx), _dp(r), _dp(b), r.shape[0], _dp(out)))
+    return out
+
+
+def composite(taus, colors, t_s=None, offsets=None, ctx: Context | None = None):
+    """composite (render.hpp:60) of one sample list, or of several (offsets = n_lists + 1 row
+    pointer): (colour n_lists x 3, alpha, weights per sample, expected depth or None)."""
+    load_library()
+    t = _f64(taus).reshape(-1)
+    c = _f64(colors).reshape(-1, 3)
+    if c.shape[0] != t.size:
+        raise ValueError("composite size mismatch")
+    off = np.array([0, t.size], np.uint64) if offsets is None else np.ascontiguousarray(offsets, dtype=np.uint64)
+    nl = off.size - 1
+    col, a, w = np.zeros((nl, 3)), np.zeros(nl), np.zeros(t.size)
+    ts = None if t_s is None else _f64(t_s).reshape(-1)
+    d = np.zeros(nl) if ts is not None else None
+    _check(_LIB.svlf_composite(_ctx_of(ctx), _dp(off), nl, _dp(t), _dp(c), _dp(ts) if ts is not None else None,
+                               _dp(col), _dp(a), _dp(d) if d is not None else None, _dp(w)))
+    return col, a, w, d
+
+
+def evaluate_voxels(model: Model, rays, voxel_ids, t_in, t_out) -> dict:
+    """evaluate_voxel (render.hpp:49) per (ray, hit) with the fp32 decoders: tau, eta, x_s, t_s, color."""
+    r = _f64(rays).reshape(-1, 6)
+    ids = np.ascontiguousarray(voxel_ids, dtype=np.uint64).reshape(-1)
+    ti, to = _f64(t_in).reshape(-1), _f64(t_out).reshape(-1)
+    n = ids.size
+    out = {"tau": np.zeros(n), "eta": np.zeros(n), "x_s": np.zeros((n, 3)), "t_s": np.zeros(n),
+           "color": np.zeros((n, 3))}
+    _check(_LIB.svlf_evaluate_voxels(model.ctx.handle, model.handle, _dp(r), _dp(ids), _dp(ti), _dp(to), n,
+                                     *[_dp(out[k]) for k in ("tau", "eta", "x_s", "t_s", "color")]))
+    return out
+
+
+def eta_gt(t_in, t_out, depth, ctx: Context | None = None) -> np.ndarray:
+    """eta_gt (train.hpp:41) per hit."""
+    load_library()
+    ti, to, d = (_f64(x).reshape(-1) for x in (t_in, t_out, depth))
+    out = np.zeros(ti.size)
+    _check(_LIB.svlf_eta_gt(_ctx_of(ctx), _dp(ti), _dp(to), _dp(d), ti.size, _dp(out)))
+    return out
+
+
+def render_ray(model: Model, ray) -> dict:
+    """render_ray (render.hpp:75): GPU traversal, every hit through evaluate_voxel, composite;
+    colour, alpha, expected depth and the samples."""
+    r = _f64(ray).reshape(1, 6)
+    off, ids, tin, tout = model.octree.traverse(r)
+    ev = evaluate_voxels(model, np.repeat(r, ids.size, axis=0), ids, tin, tout)
+    col, a, w, d = composite(ev["tau"], ev["color"], t_s=ev["t_s"], ctx=model.ctx)
+    return {"color": col[0], "alpha": float(a[0]), "expected_depth": float(d[0]),
+            "samples": {"voxel_ids": ids, "t_in": tin, "t_out": tout, **ev}}
 
 
 def tiles_owned(camera: Camera, tile_w: int, tile_h: int, rank: int, world: int) -> int:

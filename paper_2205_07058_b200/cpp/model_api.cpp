@@ -410,6 +410,8 @@ ModelAdam ModelAdam::like(const SvlfModel& m) {
     return a;
 }
 
+svlf_model* detail::device_model(const SvlfModel& m) { return device_params(m).dm; }
+
 // ---- render ----------------------------------------------------------------
 void render_frame(const SvlfModel& model, const Camera& camera, FrameBuffers& out, RenderStats* stats,
                   const float* background) {

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "svlf/b200.hpp"
+#include "svlf/model.hpp"
 #include "svlf_b200.h"
 
 namespace svlf::detail {
@@ -23,6 +24,8 @@ inline void check(svlf_status s) {
 }
 
 std::recursive_mutex& session_mutex();
+// The device copy of a host model (cached per model object, refreshed when the host tensors change).
+svlf_model* device_model(const SvlfModel& m);
 svlf_precision to_c(b200::Precision p);
 
 }  // namespace svlf::detail

@@ -113,6 +113,7 @@ const char* dev_error_message(int code) {
         case kErrPointNotInVoxel: return "point not in voxel";
         case kErrSurfaceOutside: return "surface point outside voxel";
         case kErrNegativeTau: return "negative optical thickness";
+        case kErrUnknownVoxel: return "unknown voxel id";
         case -1: return "device error on another rank";
         default: return "device error";
     }
@@ -1377,6 +1378,250 @@ svlf_status svlf_render_rays(svlf_ctx* ctx, svlf_model* m, const double* rays, s
         SVLF_CUDA(cudaStreamSynchronize(s));
     });
 }
+
+}  // extern "C"
+
+// ---- per-point / per-ray reference operations (perray.cu) ----------------------
+// Host buffers in and out, one synchronisation per call: these back the
+// reference's single-ray API (tests, debugging), not the frame / train paths.
+namespace {
+
+// device copies of a call's host arrays, freed on scope exit
+struct CallBufs {
+    std::vector<void*> ptrs;
+    cudaStream_t s;
+    explicit CallBufs(cudaStream_t st) : s(st) {}
+    ~CallBufs() {
+        cudaStreamSynchronize(s);
+        for (void* p : ptrs) cudaFree(p);
+    }
+    template <typename T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        SVLF_CUDA(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <typename T>
+    T* up(const T* h, size_t n) {
+        T* d = alloc<T>(n);
+        if (n) SVLF_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+        return d;
+    }
+    template <typename T>
+    void down(T* h, const T* d, size_t n) {
+        if (h && n) SVLF_CUDA(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+};
+
+// synchronizes; a raised device error becomes the reference's exception type
+void finish_call(svlf_ctx* ctx) {
+    int* flag = ctx->misc.as<int>();
+    SVLF_CUDA(cudaMemcpyAsync(ctx->h_pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int code = ctx->h_pinned[0];
+    if (!code) return;
+    SVLF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    const svlf_status st = code == kErrNegativeTau   ? SVLF_ERR_INVALID_ARGUMENT
+                           : code == kErrUnknownVoxel ? SVLF_ERR_OUT_OF_RANGE
+                                                      : SVLF_ERR_RUNTIME;
+    fail(st, dev_error_message(code));
+}
+
+}  // namespace
+
+extern "C" {
+
+svlf_status svlf_local_coords(svlf_ctx* ctx, const svlf_octree* tree, const uint64_t* voxel_ids,
+                              const double* points, size_t n, double* u_out) {
+    return guard([&] {
+        require(ctx && tree && (n == 0 || (voxel_ids && points && u_out)), "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        reset_misc(ctx);
+        CallBufs B(ctx->stream);
+        double* u = B.alloc<double>(3 * n);
+        launch_local_coords(dev_view(tree), B.up(voxel_ids, n), B.up(points, 3 * n), n, u, ctx->misc.as<int>(),
+                            ctx->stream);
+        finish_call(ctx);
+        B.down(u_out, u, 3 * n);
+        finish_call(ctx);
+    });
+}
+
+svlf_status svlf_interpolate(svlf_ctx* ctx, const svlf_octree* tree, svlf_dtype dtype, const void* volume,
+                             uint32_t rows, uint32_t dim, const uint64_t* voxel_ids, const double* points, size_t n,
+                             void* out) {
+    return guard([&] {
+        require(ctx && tree && volume && (n == 0 || (voxel_ids && points && out)), "null argument");
+        require(dtype == SVLF_DTYPE_F32 || dtype == SVLF_DTYPE_F64, "volume dtype must be f32 or f64");
+        require(dim >= 1, "dim must be >= 1");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        reset_misc(ctx);
+        CallBufs B(ctx->stream);
+        const DevOctree& T = dev_view(tree);
+        const uint64_t* ids = B.up(voxel_ids, n);
+        const double* pts = B.up(points, 3 * n);
+        if (dtype == SVLF_DTYPE_F32) {
+            float* o = B.alloc<float>(n * dim);
+            launch_interpolate<float>(T, B.up(static_cast<const float*>(volume), size_t(rows) * dim), rows, dim, ids,
+                                      pts, n, o, ctx->misc.as<int>(), ctx->stream);
+            finish_call(ctx);
+            B.down(static_cast<float*>(out), o, n * dim);
+        } else {
+            double* o = B.alloc<double>(n * dim);
+            launch_interpolate<double>(T, B.up(static_cast<const double*>(volume), size_t(rows) * dim), rows, dim,
+                                       ids, pts, n, o, ctx->misc.as<int>(), ctx->stream);
+            finish_call(ctx);
+            B.down(static_cast<double*>(out), o, n * dim);
+        }
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+svlf_status svlf_interpolate_backward(svlf_ctx* ctx, const svlf_octree* tree, svlf_dtype dtype, const void* volume,
+                                      uint32_t rows, uint32_t dim, const uint64_t* voxel_ids, const double* points,
+                                      size_t n, const void* upstream, void* grad_buf, double* pos_jac) {
+    return guard([&] {
+        require(ctx && tree && volume && grad_buf && (n == 0 || (voxel_ids && points && upstream)), "null argument");
+        require(dtype == SVLF_DTYPE_F32 || dtype == SVLF_DTYPE_F64, "volume dtype must be f32 or f64");
+        require(dim >= 1, "dim must be >= 1");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        reset_misc(ctx);
+        CallBufs B(ctx->stream);
+        const DevOctree& T = dev_view(tree);
+        const uint64_t* ids = B.up(voxel_ids, n);
+        const double* pts = B.up(points, 3 * n);
+        double* jac = pos_jac ? B.alloc<double>(n * dim * 3) : nullptr;
+        const size_t gsz = size_t(rows) * dim;
+        if (dtype == SVLF_DTYPE_F32) {
+            float* gb = B.up(static_cast<const float*>(grad_buf), gsz);
+            launch_interpolate_backward<float>(T, B.up(static_cast<const float*>(volume), gsz), rows, dim, ids, pts, n,
+                                               B.up(static_cast<const float*>(upstream), n * dim), gb, jac,
+                                               ctx->misc.as<int>(), ctx->stream);
+            finish_call(ctx);
+            B.down(static_cast<float*>(grad_buf), gb, gsz);
+        } else {
+            double* gb = B.up(static_cast<const double*>(grad_buf), gsz);
+            launch_interpolate_backward<double>(T, B.up(static_cast<const double*>(volume), gsz), rows, dim, ids, pts,
+                                                n, B.up(static_cast<const double*>(upstream), n * dim), gb, jac,
+                                                ctx->misc.as<int>(), ctx->stream);
+            finish_call(ctx);
+            B.down(static_cast<double*>(grad_buf), gb, gsz);
+        }
+        if (jac) B.down(pos_jac, jac, n * dim * 3);
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+svlf_status svlf_parameterize_rays(svlf_ctx* ctx, const double* rays, const double* boxes, size_t n, double* out6) {
+    return guard([&] {
+        require(ctx && (n == 0 || (rays && boxes && out6)), "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        reset_misc(ctx);
+        CallBufs B(ctx->stream);
+        double* o = B.alloc<double>(6 * n);
+        launch_parameterize(B.up(rays, 6 * n), B.up(boxes, 6 * n), n, o, ctx->misc.as<int>(), ctx->stream);
+        finish_call(ctx);
+        B.down(out6, o, 6 * n);
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+svlf_status svlf_composite(svlf_ctx* ctx, const uint64_t* offsets, size_t n_lists, const double* taus,
+                           const double* colors, const double* t_s, double* out_color, double* out_alpha,
+                           double* out_depth, double* weights) {
+    return guard([&] {
+        require(ctx && offsets && (n_lists == 0 || (out_color && out_alpha)), "null argument");
+        require(!out_depth || t_s, "expected depth needs t_s");
+        const size_t ns = offsets[n_lists];
+        require(ns == 0 || (taus && colors), "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        reset_misc(ctx);
+        CallBufs B(ctx->stream);
+        double* c = B.alloc<double>(3 * n_lists);
+        double* a = B.alloc<double>(n_lists);
+        double* d = out_depth ? B.alloc<double>(n_lists) : nullptr;
+        double* w = weights ? B.alloc<double>(ns) : nullptr;
+        launch_composite_lists(B.up(offsets, n_lists + 1), n_lists, B.up(taus, ns), B.up(colors, 3 * ns),
+                               t_s ? B.up(t_s, ns) : nullptr, c, a, d, w, ctx->misc.as<int>(), ctx->stream);
+        finish_call(ctx);
+        B.down(out_color, c, 3 * n_lists);
+        B.down(out_alpha, a, n_lists);
+        if (d) B.down(out_depth, d, n_lists);
+        if (w) B.down(weights, w, ns);
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+svlf_status svlf_evaluate_voxels(svlf_ctx* ctx, svlf_model* m, const double* rays, const uint64_t* voxel_ids,
+                                 const double* t_in, const double* t_out, size_t n, double* tau, double* eta,
+                                 double* x_s, double* t_s, double* color) {
+    return guard([&] {
+        require(ctx && m && (n == 0 || (rays && voxel_ids && t_in && t_out)), "null argument");
+        require(n < (1ull << 31), "too many voxels");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        reset_misc(ctx);
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        CallBufs B(s);
+        const DevOctree& T = dev_view(m->tree);
+        const double* dr = B.up(rays, 6 * n);
+        const double* ti = B.up(t_in, n);
+        const double* to = B.up(t_out, n);
+        uint32_t* leaf = B.alloc<uint32_t>(n);
+        uint32_t* ray = B.alloc<uint32_t>(n);
+        launch_leaf_lookup(T, B.up(voxel_ids, n), n, leaf, ray, ctx->misc.as<int>(), s);
+        finish_call(ctx);
+        // the fp32 decoders of render_frame_ref (reference arithmetic order), one hit per voxel
+        HitOut ho{B.alloc<float>(n), B.alloc<float>(n), B.alloc<float>(3 * n)};
+        ensure_pack_f32(m, s);
+        launch_decode_f32(T, m->view(), pack_f32_view(m->pack_f32.as<float>()), dr, ray, leaf, ti, to, uint32_t(n), ho,
+                          ctx->misc.as<int>(), s);
+        double* xs = B.alloc<double>(3 * n);
+        double* ts = B.alloc<double>(n);
+        launch_voxel_finish(dr, ti, to, ho.eta, n, xs, ts, s);
+        finish_call(ctx);
+        std::vector<float> ht(n), he(n), hc(3 * n);
+        B.down(ht.data(), ho.tau, n);
+        B.down(he.data(), ho.eta, n);
+        B.down(hc.data(), ho.rgb, 3 * n);
+        B.down(x_s, xs, 3 * n);
+        B.down(t_s, ts, n);
+        SVLF_CUDA(cudaStreamSynchronize(s));
+        for (size_t i = 0; i < n; ++i) {  // static_cast<double>(T) of the decoder outputs (render.cpp:46-47,58)
+            if (tau) tau[i] = double(ht[i]);
+            if (eta) eta[i] = double(he[i]);
+            if (color)
+                for (int k = 0; k < 3; ++k) color[3 * i + k] = double(hc[3 * i + k]);
+        }
+    });
+}
+
+svlf_status svlf_eta_gt(svlf_ctx* ctx, const double* t_in, const double* t_out, const double* depth, size_t n,
+                        double* out) {
+    return guard([&] {
+        require(ctx && (n == 0 || (t_in && t_out && depth && out)), "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        reset_misc(ctx);
+        CallBufs B(ctx->stream);
+        double* o = B.alloc<double>(n);
+        launch_eta_gt(B.up(t_in, n), B.up(t_out, n), B.up(depth, n), n, o, ctx->misc.as<int>(), ctx->stream);
+        finish_call(ctx);
+        B.down(out, o, n);
+        SVLF_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
 
 // ---- train --------------------------------------------------------------------
 static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const float* c_gt,

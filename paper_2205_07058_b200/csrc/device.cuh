@@ -162,6 +162,27 @@ void launch_gather_leaf_codes(const uint64_t* leaf_codes, const uint32_t* hit_le
 void launch_hit_points(const double* rays, const uint32_t* hit_ray, const double* tin,
                        const double* tout, double* x12, size_t n, cudaStream_t s);
 
+// ---- per-point / per-ray reference operations (perray.cu)
+void launch_local_coords(const DevOctree& T, const uint64_t* ids, const double* pts, size_t n, double* u, int* err,
+                         cudaStream_t s);
+template <typename Tv>
+void launch_interpolate(const DevOctree& T, const Tv* vol, uint32_t rows, uint32_t dim, const uint64_t* ids,
+                        const double* pts, size_t n, Tv* out, int* err, cudaStream_t s);
+template <typename Tv>
+void launch_interpolate_backward(const DevOctree& T, const Tv* vol, uint32_t rows, uint32_t dim, const uint64_t* ids,
+                                 const double* pts, size_t n, const Tv* up, Tv* grad, double* jac, int* err,
+                                 cudaStream_t s);
+void launch_parameterize(const double* rays, const double* boxes, size_t n, double* out, int* err, cudaStream_t s);
+void launch_composite_lists(const uint64_t* off, size_t lists, const double* taus, const double* colors,
+                            const double* t_s, double* color, double* alpha, double* depth, double* weights, int* err,
+                            cudaStream_t s);
+void launch_leaf_lookup(const DevOctree& T, const uint64_t* ids, size_t n, uint32_t* leaf, uint32_t* ray, int* err,
+                        cudaStream_t s);
+void launch_voxel_finish(const double* rays, const double* tin, const double* tout, const float* eta, size_t n,
+                         double* xs, double* ts, cudaStream_t s);
+void launch_eta_gt(const double* tin, const double* tout, const double* depth, size_t n, double* out, int* err,
+                   cudaStream_t s);
+
 // scene.cu: ground truth, occupancy back-projection, metrics
 void launch_render_gt(const svlf_scene_desc& d, const double* d_spheres, const double* d_boxes, const DevCamera& cam,
                       float* rgb, float* depth, float* mask, cudaStream_t s);

@@ -447,16 +447,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// dW / db = sum over CTAs (in CTA order) of the partials
-__global__ void k_dw_reduce(const float* __restrict__ part, uint32_t ctas, uint32_t O, uint32_t K,
-                            float* __restrict__ dW, float* __restrict__ db) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x, cols = K + 1, per = O * cols;
-    if (e >= per) return;
+// dW / db = sum over CTAs of the partials, in a fixed order (bitwise
+// reproducible): thread (g, e) of a block sums the partials of CTAs
+// c = g, g + 8, g + 16, ... in order for output element e, then group sums
+// are added g = 0..7 in order. 8-way independent load streams per element.
+constexpr uint32_t kRedGroups = 8, kRedElems = 32;
+__global__ void __launch_bounds__(kRedGroups * kRedElems)
+    k_dw_reduce(const float* __restrict__ part, uint32_t ctas, uint32_t O, uint32_t K, float* __restrict__ dW,
+                float* __restrict__ db) {
+    __shared__ float sh[kRedGroups][kRedElems];
+    const uint32_t cols = K + 1, per = O * cols;
+    const uint32_t el = threadIdx.x % kRedElems, g = threadIdx.x / kRedElems;
+    const uint32_t e = blockIdx.x * kRedElems + el;
     float acc = 0.f;
-    for (uint32_t c = 0; c < ctas; ++c) acc += __ldg(part + size_t(c) * per + e);
-    const uint32_t o = e / cols, j = e % cols;
-    if (j < K) dW[size_t(o) * K + j] = acc;
-    else db[o] = acc;
+    if (e < per) {
+        uint32_t c = g;
+        for (; c + 3 * kRedGroups < ctas; c += 4 * kRedGroups) {  // four loads in flight, adds in order
+            const float a0 = __ldg(part + size_t(c) * per + e), a1 = __ldg(part + size_t(c + kRedGroups) * per + e);
+            const float a2 = __ldg(part + size_t(c + 2 * kRedGroups) * per + e);
+            const float a3 = __ldg(part + size_t(c + 3 * kRedGroups) * per + e);
+            acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, a0), a1), a2), a3);
+        }
+        for (; c < ctas; c += kRedGroups) acc = __fadd_rn(acc, __ldg(part + size_t(c) * per + e));
+    }
+    sh[g][el] = acc;
+    __syncthreads();
+    if (g == 0 && e < per) {
+        float t = sh[0][el];
+#pragma unroll
+        for (uint32_t k = 1; k < kRedGroups; ++k) t = __fadd_rn(t, sh[k][el]);
+        const uint32_t o = e / cols, j = e % cols;
+        if (j < K) dW[size_t(o) * K + j] = t;
+        else db[o] = t;
+    }
 }
 
 int g_sms = 0;
@@ -533,7 +556,7 @@ void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* d
     else
         k_gemm_dw<true><<<ctas, kThreads, kSmemBytes, s>>>(d, x, part, n_dev, cap, ld, O, K, N);
     const uint32_t per = O * (K + 1);
-    k_dw_reduce<<<(per + 127) / 128, 128, 0, s>>>(part, ctas, O, K, dW, db);
+    k_dw_reduce<<<(per + kRedElems - 1) / kRedElems, kRedGroups * kRedElems, 0, s>>>(part, ctas, O, K, dW, db);
     note_launch(2);
 }
 

@@ -173,8 +173,9 @@ __device__ __forceinline__ void leaf_box(const DevOctree& T, uint32_t leaf, doub
 
 // ---- per-hit geometry (fp64, reference operand order) --------------------
 
-// parameterize_ray, src/render.cpp:16-28. Returns false on "tangent ray".
-__device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, const double* hi, float* r6) {
+// parameterize_ray, src/render.cpp:16-28: the RayParam6 in double (p1, p2).
+// Returns false on "tangent ray".
+__device__ __forceinline__ bool parameterize_d(const Ray& r, const double* lo, const double* hi, double* q) {
     double c[3], oc[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -200,9 +201,18 @@ __device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, con
     const double n1 = __dsqrt_rn(dot3(p1, p1)), n2 = __dsqrt_rn(dot3(p2, p2));
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        r6[a] = float(ddiv(p1[a], n1));
-        r6[3 + a] = float(ddiv(p2[a], n2));
+        q[a] = ddiv(p1[a], n1);
+        q[3 + a] = ddiv(p2[a], n2);
     }
+    return true;
+}
+
+// ... cast to the MLP's float input rows (RayParam6::write, render.hpp:16-24)
+__device__ __forceinline__ bool parameterize(const Ray& r, const double* lo, const double* hi, float* r6) {
+    double q[6];
+    if (!parameterize_d(r, lo, hi, q)) return false;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) r6[a] = float(q[a]);
     return true;
 }
 
@@ -244,7 +254,8 @@ enum DevError : int {
     kErrTangentRay = 1,       // "tangent ray" (render.cpp:23)
     kErrPointNotInVoxel = 2,  // "point not in voxel" (features.cpp:25)
     kErrSurfaceOutside = 3,   // "surface point outside voxel" (train.cpp:32)
-    kErrNegativeTau = 4,
+    kErrNegativeTau = 4,      // "negative optical thickness" (render.cpp:76)
+    kErrUnknownVoxel = 5,     // "unknown voxel id" (octree.cpp:167)
 };
 
 __device__ __forceinline__ void raise_error(int* flag, int code) {

@@ -799,35 +799,69 @@ __global__ void k_step_mail(const double* red, const uint32_t* status, const int
     *mail = m;
 }
 
-struct AdamSeg {
-    float* p;
-    const float* g;
-    float* m;
-    float* v;
-    size_t n;
-    double corr1, corr2;
-    float beta1, beta2, eps;
-};
-struct AdamSegs {
-    AdamSeg seg[14];
-    int count;
+// Dense Adam over the flat parameter buffer [feat_t | feat_c | f_T W0 b0 W1 b1 |
+// f_C W0 b0 .. W3 b3], whose tensor order is ModelAdam's: tensor t covers
+// [end[t-1], end[t]) with its own step-count correction and hyperparameters.
+struct AdamPlan {
+    size_t end[14];
+    double corr1[14], corr2[14];
+    float beta1[14], beta2[14], eps[14];
+    uint32_t active;  // bit t: tensor t is updated (colour tensors frozen: not)
 };
 
 // adam_step, src/mlp.cpp:277-296 (fp64 math, fp32 storage; beta/eps are the
 // AdamState float fields promoted to double; lr is rounded to float first,
-// src/train.cpp:427). Skipped when the step is flagged (error / overflow).
-__global__ void k_adam(AdamSegs S, float lr, const uint32_t* skip_if, const int* err) {
+// src/train.cpp:427), one element.
+__device__ __forceinline__ void adam_elem(const AdamPlan& A, int t, double lr, float& p, float g, float& m, float& v) {
+    const double b1 = double(A.beta1[t]), b2 = double(A.beta2[t]), eps = double(A.eps[t]);
+    const double gd = g;
+    const double mm = dadd(dmul(b1, double(m)), dmul(dsub(1.0, b1), gd));
+    const double vv = dadd(dmul(b2, double(v)), dmul(dmul(dsub(1.0, b2), gd), gd));
+    m = float(mm);
+    v = float(vv);
+    const double mh = ddiv(mm, A.corr1[t]), vh = ddiv(vv, A.corr2[t]);
+    p = float(dsub(double(p), ddiv(dmul(lr, mh), dadd(__dsqrt_rn(vh), eps))));
+}
+
+__device__ __forceinline__ int adam_tensor(const AdamPlan& A, size_t i) {
+    int t = 0;
+#pragma unroll 1
+    while (t < 13 && i >= A.end[t]) ++t;
+    return t;
+}
+
+// Grid-stride over float4 groups of all four arrays (HBM-bound: 28 B per
+// parameter); a group that straddles a tensor boundary goes element by element.
+// Skipped when the step is flagged (error / overflow).
+__global__ void __launch_bounds__(256) k_adam(float* __restrict__ P, const float* __restrict__ G, float* __restrict__ M,
+                                              float* __restrict__ Vv, size_t total, AdamPlan A, float lr,
+                                              const uint32_t* skip_if, const int* err) {
     if ((skip_if && *skip_if) || (err && *err)) return;
-    const AdamSeg sg = S.seg[blockIdx.y];
-    const double b1 = double(sg.beta1), b2 = double(sg.beta2), eps = double(sg.eps);
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < sg.n; i += size_t(gridDim.x) * blockDim.x) {
-        const double g = sg.g[i];
-        const double m = dadd(dmul(b1, double(sg.m[i])), dmul(dsub(1.0, b1), g));
-        const double v = dadd(dmul(b2, double(sg.v[i])), dmul(dmul(dsub(1.0, b2), g), g));
-        sg.m[i] = float(m);
-        sg.v[i] = float(v);
-        const double mh = ddiv(m, sg.corr1), vh = ddiv(v, sg.corr2);
-        sg.p[i] = float(dsub(double(sg.p[i]), ddiv(dmul(double(lr), mh), dadd(__dsqrt_rn(vh), eps))));
+    const double lrd = double(lr);
+    const size_t groups = (total + 3) / 4;
+    for (size_t q = blockIdx.x * size_t(blockDim.x) + threadIdx.x; q < groups; q += size_t(gridDim.x) * blockDim.x) {
+        const size_t i0 = 4 * q;
+        const int t = adam_tensor(A, i0);
+        if (i0 + 3 < total && i0 + 3 < A.end[t]) {
+            if (!((A.active >> t) & 1u)) continue;
+            float4 p = reinterpret_cast<float4*>(P)[q];
+            const float4 g = __ldg(reinterpret_cast<const float4*>(G) + q);
+            float4 m = reinterpret_cast<float4*>(M)[q];
+            float4 v = reinterpret_cast<float4*>(Vv)[q];
+            adam_elem(A, t, lrd, p.x, g.x, m.x, v.x);
+            adam_elem(A, t, lrd, p.y, g.y, m.y, v.y);
+            adam_elem(A, t, lrd, p.z, g.z, m.z, v.z);
+            adam_elem(A, t, lrd, p.w, g.w, m.w, v.w);
+            reinterpret_cast<float4*>(P)[q] = p;
+            reinterpret_cast<float4*>(M)[q] = m;
+            reinterpret_cast<float4*>(Vv)[q] = v;
+        } else {
+            for (size_t i = i0; i < i0 + 4 && i < total; ++i) {
+                const int te = adam_tensor(A, i);
+                if (!((A.active >> te) & 1u)) continue;
+                adam_elem(A, te, lrd, P[i], G[i], M[i], Vv[i]);
+            }
+        }
     }
 }
 
@@ -859,29 +893,28 @@ TrainScratch::~TrainScratch() {
 void launch_adam(const TrainModelRefs& M, bool color_frozen, float lr, const uint32_t* skip_if, const int* err,
                  cudaStream_t s) {
     using D = DecOffsets;
-    AdamSegs segs{};
-    const size_t off_fc = M.n_ft, off_mt = M.n_ft + M.n_fc, off_mc = off_mt + SVLF_DEC_T_SIZE;
-    auto add = [&](int sid, size_t off, size_t cnt) {
-        const AdamHyper& h = M.hyper[sid];
-        const uint64_t step = M.steps[sid] + 1;  // the caller advances the counters when the update ran
-        const double c1 = 1.0 - std::pow(double(h.beta1), double(step));
-        const double c2 = 1.0 - std::pow(double(h.beta2), double(step));
-        segs.seg[segs.count++] =
-            AdamSeg{M.params + off, M.grads + off, M.adam_m + off, M.adam_v + off, cnt, c1, c2, h.beta1, h.beta2, h.eps};
-    };
-    // ModelAdam tensor order: feat_t, feat_c, f_T (W0,b0,W1,b1), f_C (W0,b0,...,W3,b3)
-    add(0, 0, M.n_ft);
-    const size_t t_seg[4][2] = {{D::T_W0, kHid * kInT}, {D::T_B0, kHid}, {D::T_W1, 2 * kHid}, {D::T_B1, 2}};
-    for (int i = 0; i < 4; ++i) add(2 + i, off_mt + t_seg[i][0], t_seg[i][1]);
-    if (!color_frozen) {
-        add(1, off_fc, M.n_fc);
-        const size_t c_seg[8][2] = {{D::C_W0, kHid * kInC}, {D::C_B0, kHid},       {D::C_W1, kHid * kHid},
-                                    {D::C_B1, kHid},        {D::C_W2, kHid * kHid}, {D::C_B2, kHid},
-                                    {D::C_W3, 3 * kHid},    {D::C_B3, 3}};
-        for (int i = 0; i < 8; ++i) add(6 + i, off_mc + c_seg[i][0], c_seg[i][1]);
+    AdamPlan A{};
+    // tensor sizes in ModelAdam order = flat buffer order
+    const size_t sizes[14] = {M.n_ft,      M.n_fc,      size_t(kHid) * kInT, kHid, 2 * kHid, 2,
+                              size_t(kHid) * kInC, kHid, size_t(kHid) * kHid, kHid, size_t(kHid) * kHid, kHid,
+                              3 * kHid,    3};
+    static_assert(D::T_SIZE == kHid * kInT + kHid + 2 * kHid + 2, "f_T layout");
+    size_t end = 0;
+    for (int t = 0; t < 14; ++t) {
+        end += sizes[t];
+        A.end[t] = end;
+        const AdamHyper& h = M.hyper[t];
+        const uint64_t step = M.steps[t] + 1;  // the caller advances the counters when the update ran
+        A.corr1[t] = 1.0 - std::pow(double(h.beta1), double(step));
+        A.corr2[t] = 1.0 - std::pow(double(h.beta2), double(step));
+        A.beta1[t] = h.beta1;
+        A.beta2[t] = h.beta2;
+        A.eps[t] = h.eps;
+        if (!color_frozen || !(t == 1 || t >= 6)) A.active |= 1u << t;
     }
-    k_adam<<<dim3(unsigned(std::min<uint32_t>(1024, sms() * 8)), unsigned(segs.count)), 256, 0, s>>>(segs, lr,
-                                                                                                      skip_if, err);
+    const size_t groups = (end + 3) / 4;
+    const unsigned grid = unsigned(std::min<size_t>((groups + 255) / 256, size_t(sms()) * 8));
+    k_adam<<<grid, 256, 0, s>>>(M.params, M.grads, M.adam_m, M.adam_v, end, A, lr, skip_if, err);
     note_launch();
 }
 

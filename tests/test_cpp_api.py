@@ -71,6 +71,20 @@ def test_reference_octree_suite_on_cpp_api():
     assert "15 passed" in out and "0 failed" in out, out[-2000:]
 
 
+@pytest.mark.gpu
+def test_reference_features_suite_on_cpp_api():
+    """The reference's tests/test_features.cpp (10 cases: init_features, interpolate at corners /
+    centre / random points against an independent expansion, out-of-voxel rejection, partition
+    of unity, face continuity, backward scatter, positional Jacobian against finite differences in
+    64 and 32 bit), compiled unmodified against include/svlf: local_coords / interpolate /
+    interpolate_backward run on the GPU through the C ABI."""
+    exe = os.path.join(BIN, "ref_test_features")
+    if not os.path.exists(exe):
+        pytest.skip("reference tests not compiled (no reference tree at build time)")
+    out = _run([exe])
+    assert "10 passed" in out and "0 failed" in out, out[-2000:]
+
+
 def _tree(oracle, d):
     meta = _load(d, "tree_meta.u32", np.uint32)
     t = oracle.tree_from_leaves(_load(d, "leaf_codes.u64", np.uint64), int(meta[0]), int(meta[1]))
