@@ -606,7 +606,9 @@ def main():
                     choices=["fp16", "bf16", "fp32"])
     ap.add_argument("--objects", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-train", action="store_true", help="skip the C3 train-step section")
+    ap.add_argument("--no-train", action="store_true", help="skip the C3 / C5 train sections")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="only the C2 headline (and train unless --no-train): skip C4 and C2' (profiling runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -719,24 +721,26 @@ def main():
 
     import paper_2205_07058_b200.synthetic as S
 
-    c4 = None
-    try:
-        c4_cams = S.hemisphere_cameras(150, 1.8, 7, W, H, 1.5 * W)
-        c4 = bench_c4(P, torch, device, stream, ctx, model, c4_cams, W, H, precision, dist=dist, world=world,
-                      rank=rank)
-    except Exception as e:
-        c4 = {"error": str(e)}
-    try:
-        c2_dense = bench_c2_dense(P, torch, device, stream, ctx, args.steps, precision, dist=dist, world=world)
-    except Exception as e:
-        c2_dense = {"error": str(e)}
+    c4 = c2_dense = None
+    if not args.headline_only:
+        try:
+            c4_cams = S.hemisphere_cameras(150, 1.8, 7, W, H, 1.5 * W)
+            c4 = bench_c4(P, torch, device, stream, ctx, model, c4_cams, W, H, precision, dist=dist, world=world,
+                          rank=rank)
+        except Exception as e:
+            c4 = {"error": str(e)}
+        try:
+            c2_dense = bench_c2_dense(P, torch, device, stream, ctx, args.steps, precision, dist=dist, world=world)
+        except Exception as e:
+            c2_dense = {"error": str(e)}
     train = None
     c5 = None
     if not args.no_train:
-        try:
-            c5 = bench_c5(P, torch, device, stream, ctx, max(3, args.steps), dist=dist, world=world, rank=rank)
-        except Exception as e:
-            c5 = {"error": str(e)}
+        if not args.headline_only:
+            try:
+                c5 = bench_c5(P, torch, device, stream, ctx, max(3, args.steps), dist=dist, world=world, rank=rank)
+            except Exception as e:
+                c5 = {"error": str(e)}
         try:
             train = bench_train(P, torch, device, stream, ctx, max(3, args.steps), 3,
                                 cpu=not args.no_cpu_baseline and world == 1 and rank == 0, dist=dist, world=world)
@@ -805,7 +809,8 @@ def main():
             line["cpu_baseline"] = {"error": str(e)}
     if train is not None:
         line["train"] = train
-    line["c2_20_objects"] = c2_dense
+    if c2_dense is not None:
+        line["c2_20_objects"] = c2_dense
     if c4 is not None:
         line["c4"] = c4
     if c5 is not None:

@@ -813,6 +813,10 @@ struct AdamPlan {
 // AdamState float fields promoted to double; lr is rounded to float first,
 // src/train.cpp:427), one element.
 __device__ __forceinline__ void adam_elem(const AdamPlan& A, int t, double lr, float& p, float g, float& m, float& v) {
+    // g = m = v = +0: the update is exactly the identity (m, v stay +0, the step is
+    // 0 / (0 + eps) = 0 and p - 0 = p), and every fp64 operation below would take
+    // its special-case slow path; rows untouched since initialisation are all such
+    if ((__float_as_uint(g) | __float_as_uint(m) | __float_as_uint(v)) == 0u) return;
     const double b1 = double(A.beta1[t]), b2 = double(A.beta2[t]), eps = double(A.eps[t]);
     const double gd = g;
     const double mm = dadd(dmul(b1, double(m)), dmul(dsub(1.0, b1), gd));
@@ -830,33 +834,60 @@ __device__ __forceinline__ int adam_tensor(const AdamPlan& A, size_t i) {
     return t;
 }
 
-// Grid-stride over float4 groups of all four arrays (HBM-bound: 28 B per
-// parameter); a group that straddles a tensor boundary goes element by element.
-// Skipped when the step is flagged (error / overflow).
-__global__ void __launch_bounds__(256) k_adam(float* __restrict__ P, const float* __restrict__ G, float* __restrict__ M,
-                                              float* __restrict__ Vv, size_t total, AdamPlan A, float lr,
-                                              const uint32_t* skip_if, const int* err) {
+// Grid-stride over groups of kAdamVec consecutive parameters of all four
+// arrays (vector loads; 28 B per parameter); a group that straddles a tensor
+// boundary goes element by element. The fp64 divisions / square root make it
+// issue-bound rather than HBM-bound, so the group width and the occupancy are
+// build parameters (measured on the B200). Skipped when the step is flagged.
+#ifndef SVLF_ADAM_VEC
+#define SVLF_ADAM_VEC 4
+#endif
+#ifndef SVLF_ADAM_MINB
+#define SVLF_ADAM_MINB 4
+#endif
+constexpr int kAdamVec = SVLF_ADAM_VEC;
+template <int V>
+struct VecF;
+template <>
+struct VecF<1> {
+    using T = float;
+};
+template <>
+struct VecF<2> {
+    using T = float2;
+};
+template <>
+struct VecF<4> {
+    using T = float4;
+};
+
+__global__ void __launch_bounds__(256, SVLF_ADAM_MINB)
+    k_adam(float* __restrict__ P, const float* __restrict__ G, float* __restrict__ M, float* __restrict__ Vv,
+           size_t total, AdamPlan A, float lr, const uint32_t* skip_if, const int* err) {
+    using VT = typename VecF<kAdamVec>::T;
     if ((skip_if && *skip_if) || (err && *err)) return;
     const double lrd = double(lr);
-    const size_t groups = (total + 3) / 4;
+    const size_t groups = (total + kAdamVec - 1) / kAdamVec;
     for (size_t q = blockIdx.x * size_t(blockDim.x) + threadIdx.x; q < groups; q += size_t(gridDim.x) * blockDim.x) {
-        const size_t i0 = 4 * q;
+        const size_t i0 = kAdamVec * q;
         const int t = adam_tensor(A, i0);
-        if (i0 + 3 < total && i0 + 3 < A.end[t]) {
+        if (i0 + kAdamVec - 1 < total && i0 + kAdamVec - 1 < A.end[t]) {
             if (!((A.active >> t) & 1u)) continue;
-            float4 p = reinterpret_cast<float4*>(P)[q];
-            const float4 g = __ldg(reinterpret_cast<const float4*>(G) + q);
-            float4 m = reinterpret_cast<float4*>(M)[q];
-            float4 v = reinterpret_cast<float4*>(Vv)[q];
-            adam_elem(A, t, lrd, p.x, g.x, m.x, v.x);
-            adam_elem(A, t, lrd, p.y, g.y, m.y, v.y);
-            adam_elem(A, t, lrd, p.z, g.z, m.z, v.z);
-            adam_elem(A, t, lrd, p.w, g.w, m.w, v.w);
-            reinterpret_cast<float4*>(P)[q] = p;
-            reinterpret_cast<float4*>(M)[q] = m;
-            reinterpret_cast<float4*>(Vv)[q] = v;
+            VT p = reinterpret_cast<VT*>(P)[q];
+            const VT g = __ldg(reinterpret_cast<const VT*>(G) + q);
+            VT m = reinterpret_cast<VT*>(M)[q];
+            VT v = reinterpret_cast<VT*>(Vv)[q];
+            float* pp = reinterpret_cast<float*>(&p);
+            const float* gg = reinterpret_cast<const float*>(&g);
+            float* mm = reinterpret_cast<float*>(&m);
+            float* vv = reinterpret_cast<float*>(&v);
+#pragma unroll
+            for (int k = 0; k < kAdamVec; ++k) adam_elem(A, t, lrd, pp[k], gg[k], mm[k], vv[k]);
+            reinterpret_cast<VT*>(P)[q] = p;
+            reinterpret_cast<VT*>(M)[q] = m;
+            reinterpret_cast<VT*>(Vv)[q] = v;
         } else {
-            for (size_t i = i0; i < i0 + 4 && i < total; ++i) {
+            for (size_t i = i0; i < i0 + kAdamVec && i < total; ++i) {
                 const int te = adam_tensor(A, i);
                 if (!((A.active >> te) & 1u)) continue;
                 adam_elem(A, te, lrd, P[i], G[i], M[i], Vv[i]);
@@ -912,8 +943,8 @@ void launch_adam(const TrainModelRefs& M, bool color_frozen, float lr, const uin
         A.eps[t] = h.eps;
         if (!color_frozen || !(t == 1 || t >= 6)) A.active |= 1u << t;
     }
-    const size_t groups = (end + 3) / 4;
-    const unsigned grid = unsigned(std::min<size_t>((groups + 255) / 256, size_t(sms()) * 8));
+    const size_t groups = (end + kAdamVec - 1) / kAdamVec;
+    const unsigned grid = unsigned(std::min<size_t>((groups + 255) / 256, size_t(sms()) * SVLF_ADAM_MINB));
     k_adam<<<grid, 256, 0, s>>>(M.params, M.grads, M.adam_m, M.adam_v, end, A, lr, skip_if, err);
     note_launch();
 }
