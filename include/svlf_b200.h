@@ -149,6 +149,15 @@ svlf_status svlf_ctx_last_node_tests(svlf_ctx* ctx, long long* out);
  * reductions with plain TF32 operands (gradients within 2e-2, the 16-bit
  * tolerance of SURVEY.md §8(c)). */
 svlf_status svlf_ctx_set_train_precision(svlf_ctx* ctx, svlf_precision precision);
+/* Diagnostics: one train-step dense-layer GEMM (gemm_x3.cu) on device
+ * buffers of the current device, synchronous. kind 0: out[j][:n] = relu(W
+ * in[K rows] + bias) (W O x K, O <= 128); 1: out[j][:n] = sum_o W[o][k0+j]
+ * in[o][:n], zeroed where mask[j][:] <= 0 (mask may be NULL); 2: out (O x K)
+ * = in (O rows) in2^T (K rows), out2 (O) = row sums of in; matrices have row
+ * stride ld floats. products: 3 (3xTF32) or 1 (TF32, kind 2 only). */
+svlf_status svlf_debug_gemm_x3(int kind, const float* W, uint32_t O, uint32_t K, uint32_t k0, const float* bias,
+                               const float* in, const float* in2, const float* mask, float* out, float* out2,
+                               uint32_t n, uint32_t ld, int products);
 /* Count of this library's kernel launches on the context since creation. */
 long long svlf_ctx_kernel_launches(const svlf_ctx* ctx);
 

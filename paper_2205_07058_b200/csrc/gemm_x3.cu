@@ -1,21 +1,36 @@
 // Train-step dense layers on the tensor cores with fp32-level accuracy:
 // 3xTF32 (every operand x = hi + lo with hi = x rounded to TF32 and lo the
-// exact fp32 remainder; C = A_hi B_lo + A_lo B_hi + A_hi B_hi, accumulated in
-// fp32 in TMEM), tcgen05.mma.cta_group::1.kind::tf32, operands staged by the
-// threads (the split needs a register pass) into K-major shared-memory tiles.
+// remainder rounded to TF32; C = A_hi B_lo + A_lo B_hi + A_hi B_hi, fp32
+// accumulation in TMEM), tcgen05.mma.cta_group::1.kind::tf32.
 //
 // The three GEMM shapes of mlp_forward / mlp_backward (src/mlp.cpp:98-230) on
-// the feature-major matrices of train.cu (row r of a block = one feature over
-// all hits, row stride ld):
-//   Fwd  Y[j][n]  = relu(sum_k W[j][k] X[k][n] + b[j])       M = 128 output features, N = hits
-//   Bwd  dX[j][n] = sum_o W[o][k0 + j] D[o][n]  (x relu'(h))  M = 128 input features, N = hits
+// the feature-major matrices of train.cu (row r = one feature over all hits,
+// row stride ld):
+//   Fwd  Y[j][n]  = relu(sum_k W[j][k] X[k][n] + b[j])       M = 128 output features, N = hits, K = inputs
+//   Bwd  dX[j][n] = sum_o W[o][k0 + j] D[o][n]  (x relu'(h))  M = 128 input features, N = hits, K = outputs
 //   Dw   dW[o][k] = sum_n D[o][n] X[k][n], db[o] = sum_n D[o][n]
 //                                              M = O (<= 128), N = K + 1 (bias column), K = hits
-// Fwd / Bwd: persistent CTAs over tiles of up to 256 hits, the weight operand
-// from a pre-split global image (one launch builds every layer's image per
-// step). Dw: each CTA reduces a contiguous hit range into its own partial;
-// the partials are summed in CTA order (deterministic, no atomics).
-// The hit count is read on the device, so nothing here needs the host.
+// Every hit operand is read straight from its feature-major matrix by TMA
+// (cp.async.bulk.tensor, 128-byte swizzle): for Fwd / Bwd the hits are the
+// MMA's N dimension and the matrix rows are K, i.e. an MN-major B operand
+// (32 hits x 32 K-rows per box); for Dw the hits are K and both operands are
+// K-major (32 hits per 128-byte row). No register staging of global loads.
+// The only register pass is the split: converter warps rewrite each landed
+// tile in place as hi and write lo beside it (elementwise, same swizzled
+// addresses). The weight operand of Fwd / Bwd is pre-split into a global
+// image (one launch builds every layer's image per step) and fetched with a
+// 1-D bulk copy.
+//
+// Warp roles (persistent CTA, one per SM): a TMA producer thread, an MMA
+// thread, four converter warps and (Fwd / Bwd) four epilogue warps; stages
+// and TMEM accumulators handed over with mbarriers. Dw: each CTA reduces a
+// contiguous hit range into its own partial; the partials are summed in a
+// fixed order (bitwise reproducible, no atomics). Hit counts are read on the
+// device, so nothing here needs the host.
+#include <cuda.h>
+
+#include <string>
+
 #include "device.cuh"
 #include "gemm_x3.cuh"
 #include "tc_common.cuh"
@@ -27,16 +42,44 @@ namespace {
 using namespace tc;
 
 constexpr uint32_t kChunk = 32;  // K elements per pipeline stage
-constexpr uint32_t kThreads = 512;
 
-// K-major, no swizzle, 32-bit elements: core matrix = 8 rows x 16 B (4 elements);
-// LBO = 128 B (K-adjacent core matrices), SBO = 1024 B (8-row groups).
-__host__ __device__ constexpr uint32_t off32(uint32_t r, uint32_t k) {
-    return (r >> 3) * 1024u + (k >> 2) * 128u + (r & 7u) * 16u + (k & 3u) * 4u;
+// ---- PTX helpers ------------------------------------------------------------------
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+// 128-byte-swizzled operand descriptors (layout type at bits 61-63): 2 =
+// SWIZZLE_128B (16-byte granules; the K-major Dw operands), 1 =
+// SWIZZLE_128B_BASE32B (32-byte granules, 4-row atoms: the only MN-major
+// layout for 32-bit operands)
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return make_desc(saddr, lbo, sbo) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ uint64_t desc_sw128_b32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return make_desc(saddr, lbo, sbo) | (uint64_t(1) << 61);
+}
+
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -46,31 +89,32 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uin
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-__device__ __forceinline__ void split4(const float4 v, uint4& hi, uint4& lo) {
-    const float x[4] = {v.x, v.y, v.z, v.w};
-    uint32_t h[4], l[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h[i]) : "f"(x[i]));
-        l[i] = __float_as_uint(__fsub_rn(x[i], __uint_as_float(h[i])));
-    }
-    hi = make_uint4(h[0], h[1], h[2], h[3]);
-    lo = make_uint4(l[0], l[1], l[2], l[3]);
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    return h;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int kN>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
+// x -> (hi, lo): hi = x rounded to TF32 (half away from zero: add half an ulp
+// of the 10-bit mantissa to the magnitude bits, clear the low 13 bits; finite
+// inputs), lo = x - hi (exact in fp32, |lo| <= 2^-12 |x|; the tensor core
+// reads its top 19 bits, an error <= 2^-23 |x|). Three integer / fp32 ops per
+// element (cvt.rna.tf32 is an emulated sequence on sm_100a).
+__device__ __forceinline__ void split(uint32_t x, uint32_t& hi, uint32_t& lo) {
+    hi = (x + 0x1000u) & 0xffffe000u;
+    lo = __float_as_uint(__fsub_rn(__uint_as_float(x), __uint_as_float(hi)));
 }
 
 // ---- weight images ------------------------------------------------------------
-// Image of one job: chunk c (32 K) of the 128-row B operand as [hi | lo], each
-// 16 KB in the shared-memory layout, zero padded.
+// Image of one job: chunk c (32 K) of the 128-row A operand as [hi | lo], each
+// 16 KB, K-major without swizzle (core matrix = 8 rows x 16 B: LBO = 128 B
+// between K-adjacent core matrices, SBO = 1024 B between 8-row groups), zero
+// padded.
 constexpr uint32_t kFA = 128 * kChunk * 4;  // 16 KB: one 128 x 32 hi (or lo) tile
+
+__host__ __device__ constexpr uint32_t off32(uint32_t r, uint32_t k) {
+    return (r >> 3) * 1024u + (k >> 2) * 128u + (r & 7u) * 16u + (k & 3u) * 4u;
+}
 
 __global__ void k_wimages(X3ImageJobs J, uint8_t* buf) {
     const X3ImageJob jb = J.job[blockIdx.y];
@@ -86,362 +130,365 @@ __global__ void k_wimages(X3ImageJobs J, uint8_t* buf) {
             if (!jb.bwd) v = j < jb.O ? jb.W[size_t(j) * jb.K + k] : 0.f;
             else v = (jb.k0 + j < jb.K) ? jb.W[size_t(k) * jb.K + jb.k0 + j] : 0.f;
         }
-        uint32_t h;
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
-        const float l = __fsub_rn(v, __uint_as_float(h));
+        uint32_t h, l;
+        split(__float_as_uint(v), h, l);
         uint8_t* base = img + size_t(c) * 2 * kFA;
         *reinterpret_cast<uint32_t*>(base + off32(j, kk)) = h;
-        *reinterpret_cast<float*>(base + kFA + off32(j, kk)) = l;
+        *reinterpret_cast<uint32_t*>(base + kFA + off32(j, kk)) = l;
     }
 }
 
-// ---- Fwd / Bwd: M = 128 output features (weights as the A operand), N = nt
-// hits (<= 256) per tile. Per K-step an MMA reads the weight tile once for nt
-// hits. The hit operand is split in registers and staged K-major.
-constexpr uint32_t kFB = 256 * kChunk * 4;       // 32 KB: B (hits) hi or lo
-constexpr uint32_t kFStage = 2 * kFA + 2 * kFB;  // 96 KB
+// ---- Fwd / Bwd -------------------------------------------------------------------
+// Stage: A image chunk [hi 16 KB | lo 16 KB], B hi (raw tile split in place)
+// 32 KB, B lo 32 KB. B tile = up to 8 TMA boxes of 32 hits x 32 K-rows (4 KB,
+// MN-major, 128-byte swizzle with 32-byte atoms: a K-row is one 128-byte line
+// of 32 hits, swizzled in 4-row atoms); box b at +4 KB * b, so the MMA's MN
+// blocks are LBO = 4 KB apart and its 4-row K groups SBO = 512 B apart (one
+// MMA, K = 8, spans two).
+constexpr uint32_t kFB = 256 * kChunk * 4;  // 32 KB
+constexpr uint32_t kFStage = 2 * kFA + 2 * kFB;
 constexpr uint32_t kFStages = 2;
-constexpr uint32_t kFSmem = kFStages * kFStage + 128;
+constexpr uint32_t kFThreads = 448;  // warp 0 TMA, 1 MMA, 2-9 split, 10-13 epilogue
+constexpr uint32_t kFSplitWarps = 8;
+constexpr uint32_t kFSmem = kFStages * kFStage + 1024 + 256;
 
-// hits per tile: <= 256, a multiple of 16, sized so the tiles fill whole waves of the grid
+// hits per tile: <= 256, a multiple of 32, sized so the tiles fill whole waves of the grid
 __device__ __forceinline__ uint32_t tile_hits(uint32_t n, uint32_t ctas) {
     const uint32_t waves = max(1u, (n + ctas * 256 - 1) / (ctas * 256));
     const uint32_t per = (n + ctas * waves - 1) / (ctas * waves);
-    return min(256u, max(16u, (per + 15) / 16 * 16));
+    return min(256u, max(32u, (per + 31) / 32 * 32));
 }
 
 template <bool kBwd>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_feat(const float* __restrict__ in, const uint8_t* __restrict__ wimg, float* __restrict__ out,
+__global__ void __launch_bounds__(kFThreads, 1)
+    k_gemm_feat(const __grid_constant__ CUtensorMap in_map, const uint8_t* __restrict__ wimg, float* __restrict__ out,
                 const float* __restrict__ bias, const float* __restrict__ mask, const uint32_t* __restrict__ n_dev,
                 uint32_t cap, uint32_t ld, uint32_t kred, uint32_t n_out) {
-    extern __shared__ __align__(1024) uint8_t sm[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kFStages * kFStage);  // [0,1] stages, [2,3] accumulators
-    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 4);
+    extern __shared__ uint8_t sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kFStages * kFStage);
+    uint64_t* full = bars;            // [2] TMA landed
+    uint64_t* split_done = bars + 2;  // [2] converters done (one arrival per split warp)
+    uint64_t* empty = bars + 4;       // [2] MMAs of the stage done (commit)
+    uint64_t* accf = bars + 6;        // [2] accumulator ready (commit)
+    uint64_t* acce = bars + 8;        // [2] accumulator drained (4 arrivals)
+    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 10);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t n = min(*n_dev, cap);
-    const uint32_t nt = tile_hits(n, gridDim.x);
     if (tid == 0) {
-        for (uint32_t i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&split_done[i], kFSplitWarps);
+            mbar_init(&empty[i], 1);
+            mbar_init(&accf[i], 1);
+            mbar_init(&acce[i], 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&in_map);
     }
-    if (warp == 0) tmem_alloc(holder, 512);
+    if (warp == 1) tmem_alloc(holder, 512);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *holder;
     const uint32_t sbase = smem_u32(sm);
-    const uint32_t idesc = idesc_tf32(128, nt);
+    const uint32_t n = min(*n_dev, cap);
+    const uint32_t nt = tile_hits(n, gridDim.x);
+    const uint32_t nb = nt / 32;  // TMA boxes per B tile
     const uint32_t nch = (kred + kChunk - 1) / kChunk;
     const uint32_t ntiles = (n + nt - 1) / nt;
     const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const uint32_t total = my_tiles * nch;
-    uint32_t phase = 0, used = 0;
-    auto acquire = [&](uint32_t st) {
-        if ((used >> st) & 1u) {
-            mbar_wait(&bars[st], (phase >> st) & 1u);
-            phase ^= 1u << st;
-        }
-        used |= 1u << st;
-    };
-    // B staging: hit row hn of the tile, K quads qb, qb + 2, qb + 4, qb + 6
-    const uint32_t hn = tid & 255, qb = tid >> 8;
-    constexpr uint32_t kQ = kChunk / 4 / 2;
-    float4 breg[2][kQ];
-    auto fetch_b = [&](uint32_t g, float4* dst) {
-        const uint32_t tile = blockIdx.x + (g / nch) * gridDim.x, c = g % nch, hit = tile * nt + hn;
-        const bool ok = hn < nt && hit < n;
-#pragma unroll
-        for (uint32_t i = 0; i < kQ; ++i) {
-            const uint32_t k = c * kChunk + 4 * (qb + 2 * i);
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (ok) {
-                const float* p = in + size_t(k) * ld + hit;
-                if (k < kred) v.x = __ldg(p);
-                if (k + 1 < kred) v.y = __ldg(p + ld);
-                if (k + 2 < kred) v.z = __ldg(p + 2 * size_t(ld));
-                if (k + 3 < kred) v.w = __ldg(p + 3 * size_t(ld));
+    auto stage_a = [&](uint32_t s) { return sbase + s * kFStage; };
+    auto stage_b = [&](uint32_t s) { return sbase + s * kFStage + 2 * kFA; };
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            for (uint32_t g = 0; g < total; ++g) {
+                const uint32_t s = g & 1, u = g >> 1, c = g % nch;
+                const uint32_t tile = blockIdx.x + (g / nch) * gridDim.x;
+                if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+                mbar_expect_tx(&full[s], 2 * kFA + nb * 4096);
+                bulk_g2s(stage_a(s), wimg + size_t(c) * 2 * kFA, 2 * kFA, &full[s]);
+                for (uint32_t b = 0; b < nb; ++b)
+                    tma_2d(stage_b(s) + b * 4096, &in_map, int(tile * nt + 32 * b), int(c * kChunk), &full[s]);
             }
-            dst[i] = v;
         }
-    };
-    auto fetch_a = [&](uint32_t g, uint32_t st) {  // weight image chunk -> stage st
-        const uint32_t c = g % nch;
-        const uint8_t* src = wimg + size_t(c) * 2 * kFA;
-        const uint32_t sa = sbase + st * kFStage;
-        for (uint32_t i = tid; i < 2 * (kFA / 16); i += kThreads) cp_async16(sa + 16 * i, src + 16 * i);
-        cp_async_commit();
-    };
-    auto epilogue = [&](uint32_t t_local) {
-        const uint32_t b = t_local & 1u;
-        mbar_wait(&bars[2 + b], (phase >> (2 + b)) & 1u);
-        phase ^= 1u << (2 + b);
-        fence_after_sync();
-        const uint32_t tile = blockIdx.x + t_local * gridDim.x;
-        const uint32_t lane_off = (32u * (warp & 3u)) << 16, j = 32 * (warp & 3u) + lane, cg = warp >> 2;
-        const uint32_t batches = (nt + 31) / 32;
-        const float bj = (!kBwd && j < n_out) ? __ldg(bias + j) : 0.f;
-        for (uint32_t bt = cg; bt < batches; bt += 4) {
-            float v[32];
-            tmem_ld32(tmem + 256 * b + lane_off + 32 * bt, v);
-            tmem_wait_ld();
-            if (j >= n_out) continue;
-            const uint32_t h0 = tile * nt + 32 * bt;
-            const uint32_t cnt = min(min(32u, nt - 32 * bt), n > h0 ? n - h0 : 0u);
-            float* o = out + size_t(j) * ld + h0;
-            if constexpr (kBwd) {
-                if (mask) {
-                    const float* mk = mask + size_t(j) * ld + h0;
-                    float mv[32];
-                    if (cnt == 32) {
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            const uint32_t idesc = idesc_tf32(128, nt, 0, 1);
+            for (uint32_t t = 0; t < my_tiles; ++t) {
+                const uint32_t b = t & 1, v = t >> 1;
+                if (v > 0) mbar_wait(&acce[b], (v - 1) & 1);
+                fence_after_sync();
+                const uint32_t d = tmem + 256 * b;
+                for (uint32_t c = 0; c < nch; ++c) {
+                    const uint32_t g = t * nch + c, s = g & 1, u = g >> 1;
+                    mbar_wait(&full[s], u & 1);  // the A image landed (bulk copy)
+                    mbar_wait(&split_done[s], u & 1);
+                    fence_after_sync();
+                    const uint32_t sa = stage_a(s), sb = stage_b(s);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const float4 q = __ldg(reinterpret_cast<const float4*>(mk) + i);
-                            mv[4 * i] = q.x; mv[4 * i + 1] = q.y; mv[4 * i + 2] = q.z; mv[4 * i + 3] = q.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) mv[i] = uint32_t(i) < cnt ? __ldg(mk + i) : 0.f;
+                    for (uint32_t ks = 0; ks < kChunk / 8; ++ks) {
+                        const uint64_t ahi = make_desc(sa + ks * 256, 128, 1024);
+                        const uint64_t alo = make_desc(sa + kFA + ks * 256, 128, 1024);
+                        const uint64_t bhi = desc_sw128_b32(sb + ks * 1024, 4096, 512);
+                        const uint64_t blo = desc_sw128_b32(sb + kFB + ks * 1024, 4096, 512);
+                        mma_tf32(d, ahi, blo, idesc, (c | ks) ? 1u : 0u);
+                        mma_tf32(d, alo, bhi, idesc, 1u);
+                        mma_tf32(d, ahi, bhi, idesc, 1u);
                     }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&accf[b]);
+            }
+        }
+    } else if (warp < 2 + kFSplitWarps) {  // split: B tile -> hi in place, lo beside it
+        const uint32_t ct = tid - 64;
+        for (uint32_t g = 0; g < total; ++g) {
+            const uint32_t s = g & 1, u = g >> 1;
+            mbar_wait(&full[s], u & 1);
+            uint4* hi = reinterpret_cast<uint4*>(sm + s * kFStage + 2 * kFA);
+            uint4* lo = reinterpret_cast<uint4*>(sm + s * kFStage + 2 * kFA + kFB);
+#pragma unroll 4
+            for (uint32_t i = ct; i < nb * 256; i += 32 * kFSplitWarps) {
+                const uint4 x = hi[i];
+                uint4 h, l;
+                split(x.x, h.x, l.x);
+                split(x.y, h.y, l.y);
+                split(x.z, h.z, l.z);
+                split(x.w, h.w, l.w);
+                hi[i] = h;
+                lo[i] = l;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&split_done[s]);
+        }
+    } else {  // epilogue: TMEM -> bias + relu (Fwd) / relu' mask (Bwd) -> global
+        const uint32_t q = warp & 3u, j = 32 * q + lane;
+        const float bj = (!kBwd && j < n_out) ? __ldg(bias + j) : 0.f;
+        for (uint32_t t = 0; t < my_tiles; ++t) {
+            const uint32_t b = t & 1, v = t >> 1;
+            mbar_wait(&accf[b], v & 1);
+            fence_after_sync();
+            const uint32_t tile = blockIdx.x + t * gridDim.x;
+            for (uint32_t bt = 0; bt < nb; ++bt) {
+                float r[32];
+                tmem_ld32(tmem + 256 * b + ((32u * q) << 16) + 32 * bt, r);
+                tmem_wait_ld();
+                if (j >= n_out) continue;
+                const uint32_t h0 = tile * nt + 32 * bt;
+                const uint32_t cnt = n > h0 ? min(32u, n - h0) : 0u;
+                if (cnt == 0) continue;
+                float* o = out + size_t(j) * ld + h0;
+                if constexpr (kBwd) {
+                    if (mask) {
+                        const float* mk = mask + size_t(j) * ld + h0;
+                        if (cnt == 32) {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const float4 mv = __ldg(reinterpret_cast<const float4*>(mk) + i);
+                                if (!(mv.x > 0.f)) r[4 * i] = 0.f;
+                                if (!(mv.y > 0.f)) r[4 * i + 1] = 0.f;
+                                if (!(mv.z > 0.f)) r[4 * i + 2] = 0.f;
+                                if (!(mv.w > 0.f)) r[4 * i + 3] = 0.f;
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (uint32_t(i) < cnt && !(__ldg(mk + i) > 0.f)) r[i] = 0.f;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + bj, 0.f);
+                }
+                if (cnt == 32) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        reinterpret_cast<float4*>(o)[i] = make_float4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+                } else {
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
-                        if (!(mv[i] > 0.f)) v[i] = 0.f;
+                        if (uint32_t(i) < cnt) o[i] = r[i];
                 }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
             }
-            if (cnt == 32) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    reinterpret_cast<float4*>(o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (uint32_t(i) < cnt) o[i] = v[i];
-            }
+            fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&acce[b]);
         }
-        fence_before_sync();
-    };
-    auto body = [&](uint32_t g, float4* cur) {
-        const uint32_t st = g % kFStages, c = g % nch, t_local = g / nch;
-        const uint32_t sa = sbase + st * kFStage, sb = sa + 2 * kFA;
-        if (hn < nt) {
-#pragma unroll
-            for (uint32_t i = 0; i < kQ; ++i) {
-                uint4 hi, lo;
-                split4(cur[i], hi, lo);
-                const uint32_t q = qb + 2 * i;
-                st_shared_v4(sb + off32(hn, 4 * q), hi.x, hi.y, hi.z, hi.w);
-                st_shared_v4(sb + kFB + off32(hn, 4 * q), lo.x, lo.y, lo.z, lo.w);
-            }
-        }
-        if (g + 2 < total) fetch_b(g + 2, cur);
-        if (g + 1 < total) {
-            acquire((g + 1) % kFStages);
-            fetch_a(g + 1, (g + 1) % kFStages);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        fence_async_smem();
-        fence_before_sync();
-        __syncthreads();
-        if (tid == 0) {
-            fence_after_sync();
-            const uint32_t d = tmem + 256 * (t_local & 1u);
-#pragma unroll
-            for (uint32_t ks = 0; ks < kChunk / 8; ++ks) {
-                const uint64_t ahi = make_desc(sa + ks * 256, 128, 1024), alo = make_desc(sa + kFA + ks * 256, 128, 1024);
-                const uint64_t bhi = make_desc(sb + ks * 256, 128, 1024), blo = make_desc(sb + kFB + ks * 256, 128, 1024);
-                mma_tf32(d, ahi, blo, idesc, (c == 0 && ks == 0) ? 0u : 1u);
-                mma_tf32(d, alo, bhi, idesc, 1u);
-                mma_tf32(d, ahi, bhi, idesc, 1u);
-            }
-            mma_commit(&bars[st]);
-            if (c + 1 == nch) mma_commit(&bars[2 + (t_local & 1u)]);
-        }
-        if (c == 0 && t_local > 0) epilogue(t_local - 1);
-    };
-    if (total) {
-        acquire(0);
-        fetch_a(0, 0);
-        fetch_b(0, breg[0]);
-        if (total > 1) fetch_b(1, breg[1]);
     }
-    for (uint32_t g = 0; g < total; g += 2) {
-        body(g, breg[0]);
-        if (g + 1 < total) body(g + 1, breg[1]);
-    }
-    if (my_tiles) epilogue(my_tiles - 1);
     fence_before_sync();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 1) {
         fence_after_sync();
         tmem_dealloc(tmem, 512);
     }
 }
 
-// ---- Dw: part[cta][o][k] = sum over this CTA's hits of D[o][n] X[k][n] ---------
-constexpr uint32_t kRowsA = 128;                   // M
-constexpr uint32_t kMaxN = 144;                    // N = K + 1 <= 144
-constexpr uint32_t kABytes = kRowsA * kChunk * 4;  // 16 KB per hi / lo
-constexpr uint32_t kBBytes = kMaxN * kChunk * 4;   // 18 KB per hi / lo
-constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;
-constexpr uint32_t kStages = 3;
-constexpr uint32_t kSmemBytes = kStages * kStageBytes + 128;
+// ---- Dw: part[cta][o][k] = sum over this CTA's hits of D[o][n] X[k][n] ----------
+// Stage: A = D tile (128 rows x 32 hits, K-major, 128-byte swizzle: a row is
+// one 128-byte line; 8-row groups SBO = 1 KB apart) hi 16 KB + lo 16 KB;
+// B = X tile (Nr <= 144 rows x 32 hits, same layout) hi + lo. Row K of B is
+// the bias column (ones); rows past the operand's extent arrive as zeros (TMA
+// out-of-bounds fill), and hits past n are zeroed by the split.
+constexpr uint32_t kDA = 128 * 128;     // 16 KB
+constexpr uint32_t kDBMax = 144 * 128;  // 18 KB
+constexpr uint32_t kDStage = 2 * kDA + 2 * kDBMax;
+constexpr uint32_t kDStages = 3;
+constexpr uint32_t kDThreads = 320;  // warp 0 TMA, 1 MMA, 2-9 split (2-5 also the epilogue)
+constexpr uint32_t kDSplitWarps = 8;
+constexpr uint32_t kDSmem = kDStages * kDStage + 1024 + 256;
 
 template <bool kX3>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_dw(const float* __restrict__ dmat, const float* __restrict__ xmat, float* __restrict__ part,
-              const uint32_t* __restrict__ n_dev, uint32_t cap, uint32_t ld, uint32_t O, uint32_t K, uint32_t N) {
-    extern __shared__ __align__(1024) uint8_t sm[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);  // stages, then the accumulator
-    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + kStages + 1);
+__global__ void __launch_bounds__(kDThreads, 1)
+    k_gemm_dw(const __grid_constant__ CUtensorMap d_map, const __grid_constant__ CUtensorMap x_map,
+              float* __restrict__ part, const uint32_t* __restrict__ n_dev, uint32_t cap, uint32_t O, uint32_t K,
+              uint32_t Nr) {
+    extern __shared__ uint8_t sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kDStages * kDStage);
+    uint64_t* full = bars;                   // [3]
+    uint64_t* split_done = bars + kDStages;  // [3]
+    uint64_t* empty = bars + 2 * kDStages;   // [3]
+    uint64_t* accf = bars + 3 * kDStages;
+    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 3 * kDStages + 1);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (uint32_t i = 0; i < kStages + 1; ++i) mbar_init(&bars[i], 1);
+        for (uint32_t i = 0; i < kDStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&split_done[i], kDSplitWarps);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(accf, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&d_map);
+        prefetch_tmap(&x_map);
     }
-    if (warp == 0) tmem_alloc(holder, 256);
+    if (warp == 1) tmem_alloc(holder, 256);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *holder;
     const uint32_t sbase = smem_u32(sm);
-    const uint32_t idesc = idesc_tf32(128, N);
     const uint32_t n = min(*n_dev, cap);
     const uint32_t per = ((n + gridDim.x - 1) / gridDim.x + kChunk - 1) / kChunk * kChunk;
     const uint32_t h0 = min(n, blockIdx.x * per), h1 = min(n, h0 + per);
     const uint32_t nch = (h1 - h0 + kChunk - 1) / kChunk;
-    uint32_t phase = 0, used = 0;
-    // work units of a chunk: 8 rows x 4 quads (one warp instruction, conflict-free
-    // v4 stores); A units first (128 rows), then B units (N rows)
-    const uint32_t r_lo = lane & 7, q_lo = lane >> 3;
-    const uint32_t units = (kRowsA / 8) * 2 + (N / 8) * 2;
-    constexpr uint32_t kU = ((kRowsA / 8) * 2 + (kMaxN / 8) * 2 + kThreads / 32 - 1) / (kThreads / 32);
-    float4 reg[2][kU];  // chunks c and c + 1 (prefetch distance 2)
-    auto unit_of = [&](uint32_t u, uint32_t& r, uint32_t& q, bool& isA) {
-        isA = u < (kRowsA / 8) * 2;
-        const uint32_t t = isA ? u : u - (kRowsA / 8) * 2;
-        r = 8 * (t >> 1) + r_lo;
-        q = 4 * (t & 1) + q_lo;
-    };
-    auto fetch = [&](uint32_t c, float4* dst) {
-        const uint32_t hb = h0 + c * kChunk;
+    const uint32_t bB = Nr * 128;  // bytes of one B hi (or lo) tile
+    auto sa = [&](uint32_t s) { return sbase + s * kDStage; };
+    auto sb = [&](uint32_t s) { return sbase + s * kDStage + 2 * kDA; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (uint32_t c = 0; c < nch; ++c) {
+                const uint32_t s = c % kDStages, u = c / kDStages;
+                if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+                mbar_expect_tx(&full[s], kDA + bB);
+                tma_2d(sa(s), &d_map, int(h0 + c * kChunk), 0, &full[s]);
+                tma_2d(sb(s), &x_map, int(h0 + c * kChunk), 0, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_tf32(128, Nr, 0, 0);
+            for (uint32_t c = 0; c < nch; ++c) {
+                const uint32_t s = c % kDStages, u = c / kDStages;
+                mbar_wait(&full[s], u & 1);
+                mbar_wait(&split_done[s], u & 1);
+                fence_after_sync();
 #pragma unroll
-        for (uint32_t i = 0; i < kU; ++i) {
-            const uint32_t u = warp + i * (kThreads / 32);
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (u < units) {
-                uint32_t r, q;
-                bool isA;
-                unit_of(u, r, q, isA);
-                const uint32_t hit = hb + 4 * q;
-                const float* p = nullptr;
-                if (isA && r < O) p = dmat + size_t(r) * ld + hit;
-                else if (!isA && r < K) p = xmat + size_t(r) * ld + hit;
-                if (p) {
-                    if (hit + 3 < h1) {
-                        v = *reinterpret_cast<const float4*>(p);
+                for (uint32_t ks = 0; ks < kChunk / 8; ++ks) {
+                    const uint64_t ahi = desc_sw128(sa(s) + 32 * ks, 16, 1024);
+                    const uint64_t bhi = desc_sw128(sb(s) + 32 * ks, 16, 1024);
+                    if constexpr (kX3) {
+                        const uint64_t alo = desc_sw128(sa(s) + kDA + 32 * ks, 16, 1024);
+                        const uint64_t blo = desc_sw128(sb(s) + bB + 32 * ks, 16, 1024);
+                        mma_tf32(tmem, ahi, blo, idesc, (c | ks) ? 1u : 0u);
+                        mma_tf32(tmem, alo, bhi, idesc, 1u);
+                        mma_tf32(tmem, ahi, bhi, idesc, 1u);
                     } else {
-                        if (hit < h1) v.x = p[0];
-                        if (hit + 1 < h1) v.y = p[1];
-                        if (hit + 2 < h1) v.z = p[2];
+                        mma_tf32(tmem, ahi, bhi, idesc, (c | ks) ? 1u : 0u);
                     }
-                } else if (!isA && r == K) {  // bias column: ones over the valid hits
-                    v.x = hit < h1 ? 1.f : 0.f;
-                    v.y = hit + 1 < h1 ? 1.f : 0.f;
-                    v.z = hit + 2 < h1 ? 1.f : 0.f;
-                    v.w = hit + 3 < h1 ? 1.f : 0.f;
                 }
+                mma_commit(&empty[s]);
             }
-            dst[i] = v;
+            if (nch) mma_commit(accf);
         }
-    };
-    auto body = [&](uint32_t c, float4* cur) {
-        const uint32_t s = c % kStages;
-        if ((used >> s) & 1u) {
-            mbar_wait(&bars[s], (phase >> s) & 1u);
-            phase ^= 1u << s;
-        }
-        used |= 1u << s;
-        const uint32_t sa = sbase + s * kStageBytes, sb = sa + 2 * kABytes;
-#pragma unroll
-        for (uint32_t i = 0; i < kU; ++i) {
-            const uint32_t u = warp + i * (kThreads / 32);
-            if (u < units) {
-                uint32_t r, q;
-                bool isA;
-                unit_of(u, r, q, isA);
-                const uint32_t base = isA ? sa : sb, lo_off = isA ? kABytes : kBBytes;
-                if constexpr (kX3) {
-                    uint4 hi, lo;
-                    split4(cur[i], hi, lo);
-                    st_shared_v4(base + off32(r, 4 * q), hi.x, hi.y, hi.z, hi.w);
-                    st_shared_v4(base + lo_off + off32(r, 4 * q), lo.x, lo.y, lo.z, lo.w);
-                } else {  // plain TF32: the tensor core truncates the fp32 operand bits
-                    st_shared_v4(base + off32(r, 4 * q), __float_as_uint(cur[i].x), __float_as_uint(cur[i].y),
-                                 __float_as_uint(cur[i].z), __float_as_uint(cur[i].w));
+    } else {
+        const uint32_t ct = tid - 64;
+        for (uint32_t c = 0; c < nch; ++c) {
+            const uint32_t s = c % kDStages, u = c / kDStages;
+            const uint32_t hb = h0 + c * kChunk;
+            const bool tail = hb + kChunk > h1;
+            mbar_wait(&full[s], u & 1);
+            // 16-byte chunk i of a tile: row r = i / 8, physical chunk p = i % 8 holding hits
+            // 4 * (p ^ (r & 7)) .. + 3 of the chunk (128-byte swizzle)
+            auto do_tile = [&](uint8_t* base, uint32_t lo_off, uint32_t rows, bool bias_row) {
+                uint4* hi = reinterpret_cast<uint4*>(base);
+                uint4* lo = reinterpret_cast<uint4*>(base + lo_off);
+#pragma unroll 4
+                for (uint32_t i = ct; i < rows * 8; i += 32 * kDSplitWarps) {
+                    const uint32_t r = i >> 3, p = i & 7, hit = hb + 4 * (p ^ (r & 7));
+                    uint4 x = hi[i];
+                    if (bias_row && r == K) {
+                        const uint32_t one = __float_as_uint(1.f);
+                        x = make_uint4(one, one, one, one);
+                    }
+                    if (tail && hit + 4 > h1) {  // hits past the range: zero (stale matrix columns)
+                        if (hit >= h1) x.x = 0u;
+                        if (hit + 1 >= h1) x.y = 0u;
+                        if (hit + 2 >= h1) x.z = 0u;
+                        if (hit + 3 >= h1) x.w = 0u;
+                    }
+                    if constexpr (kX3) {
+                        uint4 h, l;
+                        split(x.x, h.x, l.x);
+                        split(x.y, h.y, l.y);
+                        split(x.z, h.z, l.z);
+                        split(x.w, h.w, l.w);
+                        hi[i] = h;
+                        lo[i] = l;
+                    } else {
+                        hi[i] = x;
+                    }
                 }
-            }
+            };
+            do_tile(sm + s * kDStage, kDA, 128, false);
+            do_tile(sm + s * kDStage + 2 * kDA, bB, Nr, true);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&split_done[s]);
         }
-        if (c + 2 < nch) fetch(c + 2, cur);  // in flight during the next chunks' MMAs
-        fence_async_smem();
-        fence_before_sync();
-        __syncthreads();
-        if (tid == 0) {
-            fence_after_sync();
-#pragma unroll
-            for (uint32_t ks = 0; ks < kChunk / 8; ++ks) {
-                const uint64_t ahi = make_desc(sa + ks * 256, 128, 1024), bhi = make_desc(sb + ks * 256, 128, 1024);
-                if constexpr (kX3) {
-                    const uint64_t alo = make_desc(sa + kABytes + ks * 256, 128, 1024);
-                    const uint64_t blo = make_desc(sb + kBBytes + ks * 256, 128, 1024);
-                    mma_tf32(tmem, ahi, blo, idesc, (c == 0 && ks == 0) ? 0u : 1u);
-                    mma_tf32(tmem, alo, bhi, idesc, 1u);
-                    mma_tf32(tmem, ahi, bhi, idesc, 1u);
-                } else {
-                    mma_tf32(tmem, ahi, bhi, idesc, (c == 0 && ks == 0) ? 0u : 1u);
-                }
-            }
-            mma_commit(&bars[s]);
-            if (c + 1 == nch) mma_commit(&bars[kStages]);
-        }
-    };
-    if (nch) fetch(0, reg[0]);
-    if (nch > 1) fetch(1, reg[1]);
-    for (uint32_t c = 0; c < nch; c += 2) {
-        body(c, reg[0]);
-        if (c + 1 < nch) body(c + 1, reg[1]);
-    }
-    // epilogue: this CTA's partial, rows o < O, columns j <= K (zeros for a CTA without hits)
-    if (nch) {
-        mbar_wait(&bars[kStages], 0);
-        fence_after_sync();
-    }
-    const uint32_t lane_off = (32u * (warp & 3u)) << 16, o = 32 * (warp & 3u) + lane;
-    const uint32_t groups = kThreads / 128, h = warp >> 2;
-    const uint32_t per_g = ((N + groups - 1) / groups + 31) & ~31u;
-    float* dst = part + (size_t(blockIdx.x) * O + o) * (K + 1);
-    for (uint32_t c0 = h * per_g; c0 < min(N, (h + 1) * per_g); c0 += 32) {
-        float v[32];
+        // epilogue (warps 2-5): this CTA's partial, rows o < O, columns j <= K (zeros for a CTA
+        // without hits)
+        if (warp >= 6) goto done;
         if (nch) {
-            tmem_ld32(tmem + lane_off + c0, v);
-            tmem_wait_ld();
-        } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            mbar_wait(accf, 0);
+            fence_after_sync();
         }
-        if (o < O) {
+        const uint32_t q = warp & 3u, o = 32 * q + lane;
+        float* dst = part + (size_t(blockIdx.x) * O + o) * (K + 1);
+        for (uint32_t c0 = 0; c0 <= K; c0 += 32) {
+            float v[32];
+            if (nch) {
+                tmem_ld32(tmem + ((32u * q) << 16) + c0, v);
+                tmem_wait_ld();
+            } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (c0 + i <= K) dst[c0 + i] = v[i];
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (o < O) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (c0 + i <= K) dst[c0 + i] = v[i];
+            }
         }
     }
+done:
     fence_before_sync();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 1) {
         fence_after_sync();
         tmem_dealloc(tmem, 256);
     }
@@ -492,18 +539,36 @@ void setup() {
         SVLF_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     if (!g_attr) {
-        SVLF_CUDA(cudaFuncSetAttribute(k_gemm_dw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
-        SVLF_CUDA(cudaFuncSetAttribute(k_gemm_dw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
+        SVLF_CUDA(cudaFuncSetAttribute(k_gemm_dw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDSmem)));
+        SVLF_CUDA(cudaFuncSetAttribute(k_gemm_dw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDSmem)));
         SVLF_CUDA(cudaFuncSetAttribute(k_gemm_feat<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFSmem)));
         SVLF_CUDA(cudaFuncSetAttribute(k_gemm_feat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFSmem)));
         g_attr = true;
     }
 }
 
+// Tensor map of `rows` rows of a feature-major matrix (row stride ld floats,
+// `cols` columns = hits): boxes of 32 hits x box_rows rows, 128-byte swizzle
+// (16- or 32-byte atoms); rows past `rows` and columns past `cols` read as zeros.
+CUtensorMap feature_map(const float* base, uint32_t rows, uint32_t cols, uint32_t ld, uint32_t box_rows,
+                        CUtensorMapSwizzle swz) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+    const cuuint32_t box[2] = {32, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                                              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SVLF_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
 uint32_t round16(uint32_t v) { return (v + 15u) & ~15u; }
 
-// persistent grid: one CTA per SM, fewer when the capacity has fewer tiles of 16 hits
-uint32_t feat_grid(uint32_t cap) { return std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(g_sms), (cap + 15) / 16)); }
+// persistent grid: one CTA per SM, fewer when the capacity has fewer tiles of 32 hits
+uint32_t feat_grid(uint32_t cap) { return std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(g_sms), (cap + 31) / 32)); }
 uint32_t dw_grid(uint32_t cap) { return std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(g_sms), (cap + 31) / 32)); }
 
 }  // namespace
@@ -525,7 +590,8 @@ void gemm_x3_fwd(const float* x, const uint8_t* img, const float* bias, float* y
                  const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s) {
     if (cap == 0) return;
     setup();
-    k_gemm_feat<false><<<feat_grid(cap), kThreads, kFSmem, s>>>(x, img, y, bias, nullptr, n_dev, cap, ld, K, O);
+    const CUtensorMap map = feature_map(x, K, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    k_gemm_feat<false><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, img, y, bias, nullptr, n_dev, cap, ld, K, O);
     note_launch();
 }
 
@@ -533,7 +599,8 @@ void gemm_x3_bwd(const float* d, const uint8_t* img, uint32_t O, uint32_t K, uin
                  const float* mask, const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s) {
     if (cap == 0) return;
     setup();
-    k_gemm_feat<true><<<feat_grid(cap), kThreads, kFSmem, s>>>(d, img, dx, nullptr, mask, n_dev, cap, ld, O, K - k0);
+    const CUtensorMap map = feature_map(d, O, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    k_gemm_feat<true><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, img, dx, nullptr, mask, n_dev, cap, ld, O, K - k0);
     note_launch();
 }
 
@@ -550,14 +617,50 @@ size_t gemm_x3_dw_partial_floats(uint32_t O, uint32_t K) {
 void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* dW, float* db, const uint32_t* n_dev,
                 uint32_t cap, uint32_t ld, float* part, int products, cudaStream_t s) {
     setup();
-    const uint32_t N = round16(K + 1), ctas = dw_grid(cap);
+    const uint32_t Nr = round16(K + 1), ctas = dw_grid(cap);
+    if (Nr > 144) fail(SVLF_ERR_INVALID_ARGUMENT, "weight-gradient GEMM: K too large");
+    const CUtensorMap dmap = feature_map(d, O, ld, ld, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap xmap = feature_map(x, K, ld, ld, Nr, CU_TENSOR_MAP_SWIZZLE_128B);
     if (products == 1)
-        k_gemm_dw<false><<<ctas, kThreads, kSmemBytes, s>>>(d, x, part, n_dev, cap, ld, O, K, N);
+        k_gemm_dw<false><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, part, n_dev, cap, O, K, Nr);
     else
-        k_gemm_dw<true><<<ctas, kThreads, kSmemBytes, s>>>(d, x, part, n_dev, cap, ld, O, K, N);
+        k_gemm_dw<true><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, part, n_dev, cap, O, K, Nr);
     const uint32_t per = O * (K + 1);
     k_dw_reduce<<<(per + kRedElems - 1) / kRedElems, kRedGroups * kRedElems, 0, s>>>(part, ctas, O, K, dW, db);
     note_launch(2);
 }
 
 }  // namespace svlfb
+
+// ---- unit-test entry (C ABI svlf_debug_gemm_x3; tests/test_gemm_gpu.py) ----------
+extern "C" svlf_status svlf_debug_gemm_x3(int kind, const float* W, uint32_t O, uint32_t K, uint32_t k0,
+                                          const float* bias, const float* in, const float* in2, const float* mask,
+                                          float* out, float* out2, uint32_t n, uint32_t ld, int products) {
+    using namespace svlfb;
+    try {
+        uint32_t* nd = nullptr;
+        SVLF_CUDA(cudaMalloc(&nd, 4));
+        SVLF_CUDA(cudaMemcpy(nd, &n, 4, cudaMemcpyHostToDevice));
+        uint8_t* img = nullptr;
+        float* part = nullptr;
+        if (kind == 0 || kind == 1) {
+            X3ImageJobs jobs{};
+            jobs.job[0] = {W, O, K, k0, uint32_t(kind)};
+            jobs.count = 1;
+            SVLF_CUDA(cudaMalloc(&img, gemm_x3_image_bytes(kind ? O : K)));
+            gemm_x3_build_images(jobs, img, 0);
+            if (kind == 0) gemm_x3_fwd(in, img, bias, out, O, K, nd, n, ld, 0);
+            else gemm_x3_bwd(in, img, O, K, k0, out, mask, nd, n, ld, 0);
+        } else {
+            SVLF_CUDA(cudaMalloc(&part, gemm_x3_dw_partial_floats(O, K) * 4));
+            gemm_x3_dw(in, in2, O, K, out, out2, nd, n, ld, part, products, 0);
+        }
+        SVLF_CUDA(cudaDeviceSynchronize());
+        cudaFree(nd);
+        if (img) cudaFree(img);
+        if (part) cudaFree(part);
+        return SVLF_OK;
+    } catch (const std::exception&) {
+        return SVLF_ERR_CUDA;
+    }
+}
