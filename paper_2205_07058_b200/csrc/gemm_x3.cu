@@ -28,6 +28,7 @@
 // fixed order (bitwise reproducible, no atomics). Hit counts are read on the
 // device, so nothing here needs the host.
 #include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <string>
 
@@ -550,6 +551,20 @@ void setup() {
 // Tensor map of `rows` rows of a feature-major matrix (row stride ld floats,
 // `cols` columns = hits): boxes of 32 hits x box_rows rows, 128-byte swizzle
 // (16- or 32-byte atoms); rows past `rows` and columns past `cols` read as zeros.
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time
+// libcuda dependency: the library loads on machines without a driver).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q{};
+        void* p = nullptr;
+        SVLF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) fail(SVLF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
 CUtensorMap feature_map(const float* base, uint32_t rows, uint32_t cols, uint32_t ld, uint32_t box_rows,
                         CUtensorMapSwizzle swz) {
     CUtensorMap m;
@@ -557,7 +572,7 @@ CUtensorMap feature_map(const float* base, uint32_t rows, uint32_t cols, uint32_
     const cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
     const cuuint32_t box[2] = {32, box_rows};
     const cuuint32_t es[2] = {1, 1};
-    const CUresult r = cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                                               strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                               swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
