@@ -146,18 +146,27 @@ __global__ void k_wimages(X3ImageJobs J, uint8_t* buf) {
 // of 32 hits, swizzled in 4-row atoms); box b at +4 KB * b, so the MMA's MN
 // blocks are LBO = 4 KB apart and its 4-row K groups SBO = 512 B apart (one
 // MMA, K = 8, spans two).
-constexpr uint32_t kFB = 256 * kChunk * 4;  // 32 KB
+#ifndef SVLF_GEMM_NT
+#define SVLF_GEMM_NT 128
+#endif
+#ifndef SVLF_GEMM_FSTAGES
+#define SVLF_GEMM_FSTAGES 3
+#endif
+constexpr uint32_t kNT = SVLF_GEMM_NT;                // max hits per tile (MMA N)
+constexpr uint32_t kFB = kNT * kChunk * 4;             // B hi (or lo) tile
 constexpr uint32_t kFStage = 2 * kFA + 2 * kFB;
-constexpr uint32_t kFStages = 2;
+constexpr uint32_t kFStages = SVLF_GEMM_FSTAGES;
 constexpr uint32_t kFThreads = 448;  // warp 0 TMA, 1 MMA, 2-9 split, 10-13 epilogue
 constexpr uint32_t kFSplitWarps = 8;
 constexpr uint32_t kFSmem = kFStages * kFStage + 1024 + 256;
+constexpr uint32_t kTmemAcc = kNT;  // TMEM columns per accumulator (two: tile t's epilogue overlaps t+1's MMAs)
+constexpr uint32_t kTmemCols = 2 * kTmemAcc <= 256 ? 256 : 512;  // allocation: a power of two
 
-// hits per tile: <= 256, a multiple of 32, sized so the tiles fill whole waves of the grid
+// hits per tile: <= kNT, a multiple of 32, sized so the tiles fill whole waves of the grid
 __device__ __forceinline__ uint32_t tile_hits(uint32_t n, uint32_t ctas) {
-    const uint32_t waves = max(1u, (n + ctas * 256 - 1) / (ctas * 256));
+    const uint32_t waves = max(1u, (n + ctas * kNT - 1) / (ctas * kNT));
     const uint32_t per = (n + ctas * waves - 1) / (ctas * waves);
-    return min(256u, max(32u, (per + 31) / 32 * 32));
+    return min(kNT, max(32u, (per + 31) / 32 * 32));
 }
 
 template <bool kBwd>
@@ -168,25 +177,27 @@ __global__ void __launch_bounds__(kFThreads, 1)
     extern __shared__ uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kFStages * kFStage);
-    uint64_t* full = bars;            // [2] TMA landed
-    uint64_t* split_done = bars + 2;  // [2] converters done (one arrival per split warp)
-    uint64_t* empty = bars + 4;       // [2] MMAs of the stage done (commit)
-    uint64_t* accf = bars + 6;        // [2] accumulator ready (commit)
-    uint64_t* acce = bars + 8;        // [2] accumulator drained (4 arrivals)
-    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* full = bars;                       // [stages] TMA landed
+    uint64_t* split_done = bars + kFStages;      // [stages] converters done (one arrival per split warp)
+    uint64_t* empty = bars + 2 * kFStages;       // [stages] MMAs of the stage done (commit)
+    uint64_t* accf = bars + 3 * kFStages;        // [2] accumulator ready (commit)
+    uint64_t* acce = bars + 3 * kFStages + 2;    // [2] accumulator drained (4 arrivals)
+    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 3 * kFStages + 4);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (uint32_t i = 0; i < kFStages; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&split_done[i], kFSplitWarps);
             mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&accf[i], 1);
             mbar_init(&acce[i], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&in_map);
     }
-    if (warp == 1) tmem_alloc(holder, 512);
+    if (warp == 1) tmem_alloc(holder, kTmemCols);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
@@ -205,7 +216,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
             for (uint32_t g = 0; g < total; ++g) {
-                const uint32_t s = g & 1, u = g >> 1, c = g % nch;
+                const uint32_t s = g % kFStages, u = g / kFStages, c = g % nch;
                 const uint32_t tile = blockIdx.x + (g / nch) * gridDim.x;
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
                 mbar_expect_tx(&full[s], 2 * kFA + nb * 4096);
@@ -221,9 +232,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 const uint32_t b = t & 1, v = t >> 1;
                 if (v > 0) mbar_wait(&acce[b], (v - 1) & 1);
                 fence_after_sync();
-                const uint32_t d = tmem + 256 * b;
+                const uint32_t d = tmem + kTmemAcc * b;
                 for (uint32_t c = 0; c < nch; ++c) {
-                    const uint32_t g = t * nch + c, s = g & 1, u = g >> 1;
+                    const uint32_t g = t * nch + c, s = g % kFStages, u = g / kFStages;
                     mbar_wait(&full[s], u & 1);  // the A image landed (bulk copy)
                     mbar_wait(&split_done[s], u & 1);
                     fence_after_sync();
@@ -234,6 +245,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                         const uint64_t alo = make_desc(sa + kFA + ks * 256, 128, 1024);
                         const uint64_t bhi = desc_sw128_b32(sb + ks * 1024, 4096, 512);
                         const uint64_t blo = desc_sw128_b32(sb + kFB + ks * 1024, 4096, 512);
+                        static_assert(kFB % 4096 == 0, "B tiles are whole 4 KB boxes");
                         mma_tf32(d, ahi, blo, idesc, (c | ks) ? 1u : 0u);
                         mma_tf32(d, alo, bhi, idesc, 1u);
                         mma_tf32(d, ahi, bhi, idesc, 1u);
@@ -246,7 +258,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     } else if (warp < 2 + kFSplitWarps) {  // split: B tile -> hi in place, lo beside it
         const uint32_t ct = tid - 64;
         for (uint32_t g = 0; g < total; ++g) {
-            const uint32_t s = g & 1, u = g >> 1;
+            const uint32_t s = g % kFStages, u = g / kFStages;
             mbar_wait(&full[s], u & 1);
             uint4* hi = reinterpret_cast<uint4*>(sm + s * kFStage + 2 * kFA);
             uint4* lo = reinterpret_cast<uint4*>(sm + s * kFStage + 2 * kFA + kFB);
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const uint32_t tile = blockIdx.x + t * gridDim.x;
             for (uint32_t bt = 0; bt < nb; ++bt) {
                 float r[32];
-                tmem_ld32(tmem + 256 * b + ((32u * q) << 16) + 32 * bt, r);
+                tmem_ld32(tmem + kTmemAcc * b + ((32u * q) << 16) + 32 * bt, r);
                 tmem_wait_ld();
                 if (j >= n_out) continue;
                 const uint32_t h0 = tile * nt + 32 * bt;
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     __syncthreads();
     if (warp == 1) {
         fence_after_sync();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, kTmemCols);
     }
 }
 
@@ -530,6 +542,51 @@ __global__ void __launch_bounds__(kRedGroups * kRedElems)
     }
 }
 
+struct DwRedJob {
+    const float* part;
+    float* dW;
+    float* db;
+    uint32_t O, K, blocks;  // blocks: (O * (K + 1) + kRedElems - 1) / kRedElems
+};
+struct DwRedJobs {
+    DwRedJob job[kX3MaxDwJobs];
+    uint32_t first_block[kX3MaxDwJobs + 1];
+    int count;
+};
+
+// k_dw_reduce over several jobs in one launch (blockIdx.x -> job by block ranges)
+__global__ void __launch_bounds__(kRedGroups * kRedElems) k_dw_reduce_jobs(DwRedJobs J, uint32_t ctas) {
+    __shared__ float sh[kRedGroups][kRedElems];
+    int t = 0;
+    while (t + 1 < J.count && blockIdx.x >= J.first_block[t + 1]) ++t;
+    const DwRedJob jb = J.job[t];
+    const uint32_t cols = jb.K + 1, per = jb.O * cols;
+    const uint32_t el = threadIdx.x % kRedElems, g = threadIdx.x / kRedElems;
+    const uint32_t e = (blockIdx.x - J.first_block[t]) * kRedElems + el;
+    float acc = 0.f;
+    if (e < per) {
+        uint32_t c = g;
+        for (; c + 3 * kRedGroups < ctas; c += 4 * kRedGroups) {
+            const float a0 = __ldg(jb.part + size_t(c) * per + e);
+            const float a1 = __ldg(jb.part + size_t(c + kRedGroups) * per + e);
+            const float a2 = __ldg(jb.part + size_t(c + 2 * kRedGroups) * per + e);
+            const float a3 = __ldg(jb.part + size_t(c + 3 * kRedGroups) * per + e);
+            acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, a0), a1), a2), a3);
+        }
+        for (; c < ctas; c += kRedGroups) acc = __fadd_rn(acc, __ldg(jb.part + size_t(c) * per + e));
+    }
+    sh[g][el] = acc;
+    __syncthreads();
+    if (g == 0 && e < per) {
+        float v = sh[0][el];
+#pragma unroll
+        for (uint32_t k = 1; k < kRedGroups; ++k) v = __fadd_rn(v, sh[k][el]);
+        const uint32_t o = e / cols, j = e % cols;
+        if (j < jb.K) jb.dW[size_t(o) * jb.K + j] = v;
+        else jb.db[o] = v;
+    }
+}
+
 int g_sms = 0;
 bool g_attr = false;
 
@@ -627,6 +684,38 @@ size_t gemm_x3_dw_partial_floats(uint32_t O, uint32_t K) {
         SVLF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     return size_t(sms) * O * (K + 1);
+}
+
+void gemm_x3_dw_batch(const X3DwJob* jobs, int count, const uint32_t* n_dev, uint32_t cap, uint32_t ld, float* part,
+                      int products, cudaStream_t s) {
+    if (count <= 0) return;
+    if (count > kX3MaxDwJobs) fail(SVLF_ERR_INVALID_ARGUMENT, "too many weight-gradient jobs");
+    setup();
+    const uint32_t ctas = dw_grid(cap);
+    DwRedJobs R{};
+    size_t off = 0;
+    uint32_t blocks = 0;
+    for (int i = 0; i < count; ++i) {
+        const X3DwJob& jb = jobs[i];
+        const uint32_t Nr = round16(jb.K + 1);
+        if (Nr > 144) fail(SVLF_ERR_INVALID_ARGUMENT, "weight-gradient GEMM: K too large");
+        const CUtensorMap dmap = feature_map(jb.d, jb.O, ld, ld, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        const CUtensorMap xmap = feature_map(jb.x, jb.K, ld, ld, Nr, CU_TENSOR_MAP_SWIZZLE_128B);
+        float* p = part + off;
+        if (products == 1)
+            k_gemm_dw<false><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, p, n_dev, cap, jb.O, jb.K, Nr);
+        else
+            k_gemm_dw<true><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, p, n_dev, cap, jb.O, jb.K, Nr);
+        const uint32_t per = jb.O * (jb.K + 1);
+        R.job[i] = DwRedJob{p, jb.dW, jb.db, jb.O, jb.K, (per + kRedElems - 1) / kRedElems};
+        R.first_block[i] = blocks;
+        blocks += R.job[i].blocks;
+        off += size_t(ctas) * per;
+    }
+    R.first_block[count] = blocks;
+    R.count = count;
+    k_dw_reduce_jobs<<<blocks, kRedGroups * kRedElems, 0, s>>>(R, ctas);
+    note_launch(count + 1);
 }
 
 void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* dW, float* db, const uint32_t* n_dev,

@@ -43,6 +43,19 @@ void gemm_x3_bwd(const float* d, const uint8_t* img, uint32_t O, uint32_t K, uin
 // partials are summed in CTA order, so the result is bitwise reproducible. products = 3
 // (hi*lo + lo*hi + hi*hi: fp32-level accuracy) or 1 (plain TF32).
 size_t gemm_x3_dw_partial_floats(uint32_t O, uint32_t K);
+// Several weight gradients at once: one GEMM launch per job, then one launch
+// reducing every job's partials (part holds the jobs' partials back to back:
+// sum of gemm_x3_dw_partial_floats over the jobs).
+struct X3DwJob {
+    const float* d;
+    const float* x;
+    uint32_t O, K;
+    float* dW;
+    float* db;
+};
+constexpr int kX3MaxDwJobs = 6;
+void gemm_x3_dw_batch(const X3DwJob* jobs, int count, const uint32_t* n_dev, uint32_t cap, uint32_t ld, float* part,
+                      int products, cudaStream_t s);
 void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* dW, float* db, const uint32_t* n_dev,
                 uint32_t cap, uint32_t ld, float* part, int products, cudaStream_t s);
 

@@ -1031,7 +1031,9 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     uint8_t* wimg = S.wimg.ensure<uint8_t>(img_bytes);
     gemm_x3_build_images(jobs, wimg, s);
     auto img = [&](int i) { return wimg + jobs.offset[i]; };
-    float* part = S.dw_part.ensure<float>(gemm_x3_dw_partial_floats(kHid, kInT));
+    float* part = S.dw_part.ensure<float>(gemm_x3_dw_partial_floats(kHid, kInT) + gemm_x3_dw_partial_floats(2, kHid) +
+                                          gemm_x3_dw_partial_floats(kHid, kInC) + 2 * gemm_x3_dw_partial_floats(kHid, kHid) +
+                                          gemm_x3_dw_partial_floats(3, kHid));
 
     const unsigned in_grid = loop_grid(cap, 32 * kInWarps, 16);
     const unsigned hit_grid = loop_grid(cap, 128, 16);
@@ -1075,13 +1077,18 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     note_launch(3);
     // weight gradients (sums over hits, CTA-ordered partials)
     const int prod = o.tf32 ? 1 : 3;
-    gemm_x3_dw(Dm(D_T0), A(A_XT), kHid, kInT, g_mt + D::T_W0, g_mt + D::T_B0, n_act, cap, ld, part, prod, s);
-    gemm_x3_dw(Dm(D_T1), A(A_HT), 2, kHid, g_mt + D::T_W1, g_mt + D::T_B1, n_act, cap, ld, part, prod, s);
-    if (!o.color_frozen) {
-        gemm_x3_dw(Dm(D_C0), A(A_XC), kHid, kInC, g_mc + D::C_W0, g_mc + D::C_B0, n_act, cap, ld, part, prod, s);
-        gemm_x3_dw(Dm(D_C1), A(A_H1), kHid, kHid, g_mc + D::C_W1, g_mc + D::C_B1, n_act, cap, ld, part, prod, s);
-        gemm_x3_dw(Dm(D_C2), A(A_H2), kHid, kHid, g_mc + D::C_W2, g_mc + D::C_B2, n_act, cap, ld, part, prod, s);
-        gemm_x3_dw(Dm(D_C3), A(A_H3), 3, kHid, g_mc + D::C_W3, g_mc + D::C_B3, n_act, cap, ld, part, prod, s);
+    {
+        X3DwJob dw[kX3MaxDwJobs];
+        int nj = 0;
+        dw[nj++] = {Dm(D_T0), A(A_XT), kHid, kInT, g_mt + D::T_W0, g_mt + D::T_B0};
+        dw[nj++] = {Dm(D_T1), A(A_HT), 2, kHid, g_mt + D::T_W1, g_mt + D::T_B1};
+        if (!o.color_frozen) {
+            dw[nj++] = {Dm(D_C0), A(A_XC), kHid, kInC, g_mc + D::C_W0, g_mc + D::C_B0};
+            dw[nj++] = {Dm(D_C1), A(A_H1), kHid, kHid, g_mc + D::C_W1, g_mc + D::C_B1};
+            dw[nj++] = {Dm(D_C2), A(A_H2), kHid, kHid, g_mc + D::C_W2, g_mc + D::C_B2};
+            dw[nj++] = {Dm(D_C3), A(A_H3), 3, kHid, g_mc + D::C_W3, g_mc + D::C_B3};
+        }
+        gemm_x3_dw_batch(dw, nj, n_act, cap, ld, part, prod, s);
     }
     if (n) {
         size_t tb = 0;
