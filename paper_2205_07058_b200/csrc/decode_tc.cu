@@ -1154,8 +1154,12 @@ int g_num_sms = 0;
 }  // namespace
 
 // [weights | f_T 16-bit V x 64 | f_C 16-bit V x 32 | f_C per leaf: 8 corner rows, L x 8 x 32]
-size_t pack_leafc_offset(uint32_t V) { return OFF_FEAT + size_t(V) * 96 * 2; }
-size_t pack_leaft_offset(uint32_t V, uint32_t L) { return pack_leafc_offset(V) + size_t(L) * 8 * 32 * 2; }
+// The per-leaf tables start on 1 KB boundaries, so every 128-byte row (f_T) or
+// corner pair (f_C) of a leaf is one whole L1 line (V * 192 B alone is only
+// 64-byte aligned for odd V).
+size_t align1k(size_t x) { return (x + 1023) & ~size_t(1023); }
+size_t pack_leafc_offset(uint32_t V) { return align1k(OFF_FEAT + size_t(V) * 96 * 2); }
+size_t pack_leaft_offset(uint32_t V, uint32_t L) { return align1k(pack_leafc_offset(V) + size_t(L) * 8 * 32 * 2); }
 size_t pack_tc_bytes(uint32_t V, uint32_t L) { return pack_leaft_offset(V, L) + size_t(L) * 8 * 64 * 2; }
 
 // Per-leaf copy of the 8 corner rows of the 16-bit f_C features (512 contiguous
