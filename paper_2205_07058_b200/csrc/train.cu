@@ -34,7 +34,9 @@
 // the active-hit count from the device and loops over it (grids sized by the
 // hit capacity), and the single host synchronisation is the final readback
 // of one small status record.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include <cub/device/device_reduce.cuh>
@@ -807,6 +809,7 @@ struct AdamPlan {
     double corr1[14], corr2[14];
     float beta1[14], beta2[14], eps[14];
     uint32_t active;  // bit t: tensor t is updated (colour tensors frozen: not)
+    float lr;
 };
 
 // adam_step, src/mlp.cpp:277-296 (fp64 math, fp32 storage; beta/eps are the
@@ -863,10 +866,13 @@ struct VecF<4> {
 
 __global__ void __launch_bounds__(256, SVLF_ADAM_MINB)
     k_adam(float* __restrict__ P, const float* __restrict__ G, float* __restrict__ M, float* __restrict__ Vv,
-           size_t total, AdamPlan A, float lr, const uint32_t* skip_if, const int* err) {
+           size_t total, const AdamPlan* __restrict__ plan, const uint32_t* skip_if, const int* err) {
     using VT = typename VecF<kAdamVec>::T;
     if ((skip_if && *skip_if) || (err && *err)) return;
-    const double lrd = double(lr);
+    __shared__ AdamPlan A;  // the step's corrections / hyperparameters (device memory: graph replays stay valid)
+    if (threadIdx.x == 0) A = *plan;
+    __syncthreads();
+    const double lrd = double(A.lr);
     const size_t groups = (total + kAdamVec - 1) / kAdamVec;
     for (size_t q = blockIdx.x * size_t(blockDim.x) + threadIdx.x; q < groups; q += size_t(gridDim.x) * blockDim.x) {
         const size_t i0 = kAdamVec * q;
@@ -916,16 +922,20 @@ unsigned loop_grid(size_t items, size_t per_block, uint32_t per_sm) {
 }  // namespace
 
 TrainScratch::~TrainScratch() {
+    if (graph) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph));
     if (h_mail) cudaFreeHost(h_mail);
+    if (h_plan) cudaFreeHost(h_plan);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
 }
 
-void launch_adam(const TrainModelRefs& M, bool color_frozen, float lr, const uint32_t* skip_if, const int* err,
-                 cudaStream_t s) {
+namespace {
+
+// The Adam plan of a step (per-tensor bias corrections from the step counters,
+// hyperparameters, lr), ModelAdam order = flat buffer order.
+AdamPlan adam_plan(const TrainModelRefs& M, bool color_frozen, float lr) {
     using D = DecOffsets;
     AdamPlan A{};
-    // tensor sizes in ModelAdam order = flat buffer order
     const size_t sizes[14] = {M.n_ft,      M.n_fc,      size_t(kHid) * kInT, kHid, 2 * kHid, 2,
                               size_t(kHid) * kInC, kHid, size_t(kHid) * kHid, kHid, size_t(kHid) * kHid, kHid,
                               3 * kHid,    3};
@@ -943,11 +953,45 @@ void launch_adam(const TrainModelRefs& M, bool color_frozen, float lr, const uin
         A.eps[t] = h.eps;
         if (!color_frozen || !(t == 1 || t >= 6)) A.active |= 1u << t;
     }
-    const size_t groups = (end + kAdamVec - 1) / kAdamVec;
+    A.lr = lr;
+    return A;
+}
+
+void enqueue_adam(const TrainModelRefs& M, const AdamPlan* d_plan, size_t total, const uint32_t* skip_if,
+                  const int* err, cudaStream_t s) {
+    const size_t groups = (total + kAdamVec - 1) / kAdamVec;
     const unsigned grid = unsigned(std::min<size_t>((groups + 255) / 256, size_t(sms()) * SVLF_ADAM_MINB));
-    k_adam<<<grid, 256, 0, s>>>(M.params, M.grads, M.adam_m, M.adam_v, end, A, lr, skip_if, err);
+    k_adam<<<grid, 256, 0, s>>>(M.params, M.grads, M.adam_m, M.adam_v, total, d_plan, skip_if, err);
     note_launch();
 }
+
+}  // namespace
+
+void launch_adam(const TrainModelRefs& M, bool color_frozen, float lr, const uint32_t* skip_if, const int* err,
+                 cudaStream_t s) {
+    const AdamPlan A = adam_plan(M, color_frozen, lr);
+    AdamPlan* d = nullptr;
+    SVLF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(AdamPlan), s));
+    SVLF_CUDA(cudaMemcpyAsync(d, &A, sizeof A, cudaMemcpyHostToDevice, s));
+    enqueue_adam(M, d, A.end[13], skip_if, err, s);
+    SVLF_CUDA(cudaFreeAsync(d, s));
+    SVLF_CUDA(cudaStreamSynchronize(s));  // the host plan is a stack object
+}
+
+namespace {
+
+// Graph key of a step: every pointer, size and flag its launches bake in.
+struct KeyBuilder {
+    std::vector<uint64_t> v;
+    template <typename X>
+    void add(const X& x) {
+        uint64_t w[(sizeof(X) + 7) / 8] = {};
+        std::memcpy(w, &x, sizeof(X));
+        v.insert(v.end(), w, w + (sizeof(X) + 7) / 8);
+    }
+};
+
+}  // namespace
 
 TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModelRefs& M, const TrainBatchDev& b,
                            const TrainOptions& o, cudaStream_t s, int* err_flag) {
@@ -955,6 +999,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     TrainResult res;
     if (!S.h_mail) {
         SVLF_CUDA(cudaMallocHost(&S.h_mail, sizeof(StepMail)));
+        SVLF_CUDA(cudaMallocHost(&S.h_plan, sizeof(AdamPlan)));
         for (auto& e : S.ev) SVLF_CUDA(cudaEventCreate(&e));
     }
     const size_t P = M.n_ft + M.n_fc + SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE;
@@ -966,10 +1011,11 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     if (S.act_cap == 0) S.act_cap = std::max<uint32_t>(65536, n);
     const uint32_t cap = std::min<uint32_t>(std::max<uint32_t>(b.hit_cap, 32), S.act_cap);
     const uint32_t ld = (cap + 31u) & ~31u;
-    SVLF_CUDA(cudaEventRecord(S.ev[0], s));
-    SVLF_CUDA(cudaMemsetAsync(M.grads, 0, P * 4, s));
+    const bool dp = o.coll && o.coll->world > 1;
+    const uint32_t V = M.view.V;
 
-    // ---- per-ray preparation and dense active-hit list
+    // ---- every buffer of the step, allocated before anything is enqueued (the
+    // enqueue below must not reallocate: it may be captured into a graph)
     uint32_t* act_first = S.act_first.ensure<uint32_t>(n + 1);
     uint32_t* act_cnt = S.act_cnt.ensure<uint32_t>(n + 1);
     uint32_t* dpos = S.dpos.ensure<uint32_t>(n + 1);
@@ -980,24 +1026,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     double* red = S.red.ensure<double>(R_COUNT);
     uint32_t* status = S.status.ensure<uint32_t>(4);
     StepMail* mail = reinterpret_cast<StepMail*>(S.loss_out.ensure<char>(sizeof(StepMail)));
-    SVLF_CUDA(cudaMemsetAsync(counters, 0, 32, s));
-    SVLF_CUDA(cudaMemsetAsync(status, 0, 16, s));
-    SVLF_CUDA(cudaMemsetAsync(act_cnt + n, 0, 4, s));
-    PrepArgs pa{b.rays,   b.depth_gt, b.alpha_gt, n,         b.ray_off, b.ray_cnt, b.hit_leaf, b.hit_tin,
-                b.hit_tout, b.trav_counters, o.surface, o.lw.empty == 0.0, act_first, act_cnt, surf_rel, eta_gt,
-                counters};
-    if (n) {
-        k_prep<<<(n + 127) / 128, 128, 0, s>>>(T, pa, err_flag);
-        note_launch();
-    }
-    {
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, act_cnt, dpos, int(n + 1));
-        SVLF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.ensure<char>(tb), tb, act_cnt, dpos, int(n + 1), s));
-        note_launch();
-    }
-    const uint32_t* n_act = dpos + n;  // active hits, on the device
-
+    AdamPlan* d_plan = S.plan.ensure<AdamPlan>(1);
     uint32_t* dhit = S.dhit.ensure<uint32_t>(cap);
     uint32_t* dray = S.dray.ensure<uint32_t>(cap);
     float* hitf = S.hitf.ensure<float>(size_t(ld) * 8);    // tau, eta, rgb[3], drgb[3]
@@ -1005,15 +1034,6 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     float* acts = S.acts.ensure<float>(size_t(A_ROWS) * ld);
     float* deltas = S.deltas.ensure<float>(size_t(D_ROWS) * ld);
     float* dxs = S.dxs.ensure<float>(size_t(kInT) * ld);  // dL/d layer-0 inputs
-    HitArgs H{b.rays,   b.hit_leaf, b.hit_tin, b.hit_tout, dhit,   dray,  dpos, surf_rel, n_act, cap, ld, o.surface,
-              acts,     deltas,     hitf,      hitf + ld,  hitf + 2 * size_t(ld), hitf + 5 * size_t(ld), hitd,
-              hitd + ld};
-    if (n) {
-        k_expand<<<(n + 127) / 128, 128, 0, s>>>(n, act_first, act_cnt, dpos, H, dhit, dray);
-        note_launch();
-    }
-
-    // Weight operand images of every forward / input-gradient GEMM (one launch).
     X3ImageJobs jobs{};
     enum { J_FT0, J_FC0, J_FC1, J_FC2, J_BC2, J_BC1, J_BC0, J_BT0 };
     jobs.job[J_FT0] = {M.view.mt + D::T_W0, kHid, kInT, 0, 0};
@@ -1029,115 +1049,223 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     for (int i = 0; i < jobs.count; ++i)
         img_bytes += gemm_x3_image_bytes(jobs.job[i].bwd ? jobs.job[i].O : jobs.job[i].K);
     uint8_t* wimg = S.wimg.ensure<uint8_t>(img_bytes);
-    gemm_x3_build_images(jobs, wimg, s);
-    auto img = [&](int i) { return wimg + jobs.offset[i]; };
     float* part = S.dw_part.ensure<float>(gemm_x3_dw_partial_floats(kHid, kInT) + gemm_x3_dw_partial_floats(2, kHid) +
                                           gemm_x3_dw_partial_floats(kHid, kInC) + 2 * gemm_x3_dw_partial_floats(kHid, kHid) +
                                           gemm_x3_dw_partial_floats(3, kHid));
-
+    size_t tb_scan = 0, tb_red = 0, tb_sel = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, act_cnt, dpos, int(n + 1));
+    cub::DeviceReduce::Sum(nullptr, tb_red, ray_loss, red + R_LOSS, int(std::max<uint32_t>(n, 1)));
+    uint8_t* touched = nullptr;
+    uint32_t *rows = nullptr, *n_rows = nullptr;
+    float* packed = nullptr;
+    uint32_t rc = 0;
+    if (dp) {
+        touched = S.touched.ensure<uint8_t>(V);
+        rows = S.rows.ensure<uint32_t>(V);
+        n_rows = S.n_rows.ensure<uint32_t>(1);
+        cub::CountingInputIterator<uint32_t> idx(0);
+        cub::DeviceSelect::Flagged(nullptr, tb_sel, idx, touched, rows, n_rows, int(V));
+        if (S.rows_cap == 0) S.rows_cap = std::min<uint32_t>(V, 1u << 16);
+        rc = std::min<uint32_t>(S.rows_cap, V);
+        packed = S.packed.ensure<float>(size_t(rc) * 96);
+    }
+    char* scan_tmp = S.scan_tmp.ensure<char>(std::max({tb_scan, tb_red, tb_sel, size_t(16)}));
+    const uint32_t* n_act = dpos + n;  // active hits, on the device
+    HitArgs H{b.rays,   b.hit_leaf, b.hit_tin, b.hit_tout, dhit,   dray,  dpos, surf_rel, n_act, cap, ld, o.surface,
+              acts,     deltas,     hitf,      hitf + ld,  hitf + 2 * size_t(ld), hitf + 5 * size_t(ld), hitd,
+              hitd + ld};
+    PrepArgs pa{b.rays,   b.depth_gt, b.alpha_gt, n,         b.ray_off, b.ray_cnt, b.hit_leaf, b.hit_tin,
+                b.hit_tout, b.trav_counters, o.surface, o.lw.empty == 0.0, act_first, act_cnt, surf_rel, eta_gt,
+                counters};
+    LossArgs L{b.c_gt, b.alpha_gt, dpos, act_cnt, surf_rel, eta_gt, n, o.surface, o.lw, ray_loss,
+               hitd + 2 * size_t(ld), hitd + 3 * size_t(ld), hitd + 4 * size_t(ld)};
+    float* g_ft = M.grads;
+    float* g_fc = M.grads + M.n_ft;
+    float* g_mt = g_fc + M.n_fc;
+    float* g_mc = g_mt + SVLF_DEC_T_SIZE;
     const unsigned in_grid = loop_grid(cap, 32 * kInWarps, 16);
     const unsigned hit_grid = loop_grid(cap, 128, 16);
     const unsigned sc_grid = loop_grid(cap, 32 * kScWarps, 8);
     auto A = [&](int row) { return acts + size_t(row) * ld; };
     auto Dm = [&](int row) { return deltas + size_t(row) * ld; };
-
-    SVLF_CUDA(cudaEventRecord(S.ev[1], s));
-    // ---- forward
-    k_fwd_in_t<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
-    gemm_x3_fwd(A(A_XT), img(J_FT0), M.view.mt + D::T_B0, A(A_HT), kHid, kInT, n_act, cap, ld, s);
-    k_fwd_mid<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
-    gemm_x3_fwd(A(A_XC), img(J_FC0), M.view.mc + D::C_B0, A(A_H1), kHid, kInC, n_act, cap, ld, s);
-    gemm_x3_fwd(A(A_H1), img(J_FC1), M.view.mc + D::C_B1, A(A_H2), kHid, kHid, n_act, cap, ld, s);
-    gemm_x3_fwd(A(A_H2), img(J_FC2), M.view.mc + D::C_B2, A(A_H3), kHid, kHid, n_act, cap, ld, s);
-    k_fwd_rgb<<<hit_grid, 128, 0, s>>>(M.view, H);
-    note_launch(3);
-    SVLF_CUDA(cudaEventRecord(S.ev[2], s));
-    LossArgs L{b.c_gt, b.alpha_gt, dpos, act_cnt, surf_rel, eta_gt, n, o.surface, o.lw, ray_loss,
-               hitd + 2 * size_t(ld), hitd + 3 * size_t(ld), hitd + 4 * size_t(ld)};
-    if (n) {
-        k_loss<<<(n + 127) / 128, 128, 0, s>>>(L, H);
-        note_launch();
-    }
-    SVLF_CUDA(cudaEventRecord(S.ev[3], s));
-
-    // ---- backward
-    float* g_ft = M.grads;
-    float* g_fc = M.grads + M.n_ft;
-    float* g_mt = g_fc + M.n_fc;
-    float* g_mc = g_mt + SVLF_DEC_T_SIZE;
-    // f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
-    k_bwd_head_c<<<hit_grid, 128, 0, s>>>(M.view, H);
-    gemm_x3_bwd(Dm(D_C2), img(J_BC2), kHid, kHid, 0, Dm(D_C1), A(A_H2), n_act, cap, ld, s);
-    gemm_x3_bwd(Dm(D_C1), img(J_BC1), kHid, kHid, 0, Dm(D_C0), A(A_H1), n_act, cap, ld, s);
-    gemm_x3_bwd(Dm(D_C0), img(J_BC0), kHid, kInC, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
-    // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
-    k_bwd_feat_c<<<sc_grid, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
-    gemm_x3_bwd(Dm(D_T0), img(J_BT0), kHid, kInT, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
-    k_bwd_feat_t<<<sc_grid, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
-    note_launch(3);
-    // weight gradients (sums over hits, CTA-ordered partials)
     const int prod = o.tf32 ? 1 : 3;
-    {
-        X3DwJob dw[kX3MaxDwJobs];
-        int nj = 0;
-        dw[nj++] = {Dm(D_T0), A(A_XT), kHid, kInT, g_mt + D::T_W0, g_mt + D::T_B0};
-        dw[nj++] = {Dm(D_T1), A(A_HT), 2, kHid, g_mt + D::T_W1, g_mt + D::T_B1};
-        if (!o.color_frozen) {
-            dw[nj++] = {Dm(D_C0), A(A_XC), kHid, kInC, g_mc + D::C_W0, g_mc + D::C_B0};
-            dw[nj++] = {Dm(D_C1), A(A_H1), kHid, kHid, g_mc + D::C_W1, g_mc + D::C_B1};
-            dw[nj++] = {Dm(D_C2), A(A_H2), kHid, kHid, g_mc + D::C_W2, g_mc + D::C_B2};
-            dw[nj++] = {Dm(D_C3), A(A_H3), 3, kHid, g_mc + D::C_W3, g_mc + D::C_B3};
+    const uint32_t* n_rows_dev = dp ? n_rows : nullptr;
+    bool capturing = false;  // inside a graph capture the timing events become event-record nodes
+    auto ev = [&](int k) {
+        if (capturing) SVLF_CUDA(cudaEventRecordWithFlags(S.ev[k], s, cudaEventRecordExternal));
+        else SVLF_CUDA(cudaEventRecord(S.ev[k], s));
+    };
+
+    // ---- the step, enqueued without a host round trip
+    auto enqueue = [&]() {
+        long long launches = 0;
+        ev(0);
+        SVLF_CUDA(cudaMemsetAsync(M.grads, 0, P * 4, s));
+        SVLF_CUDA(cudaMemsetAsync(counters, 0, 32, s));
+        SVLF_CUDA(cudaMemsetAsync(status, 0, 16, s));
+        SVLF_CUDA(cudaMemsetAsync(act_cnt + n, 0, 4, s));
+        // per-ray preparation and the dense active-hit list
+        if (n) {
+            k_prep<<<(n + 127) / 128, 128, 0, s>>>(T, pa, err_flag);
+            ++launches;
         }
-        gemm_x3_dw_batch(dw, nj, n_act, cap, ld, part, prod, s);
+        SVLF_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, tb_scan, act_cnt, dpos, int(n + 1), s));
+        ++launches;
+        if (n) {
+            k_expand<<<(n + 127) / 128, 128, 0, s>>>(n, act_first, act_cnt, dpos, H, dhit, dray);
+            ++launches;
+        }
+        // weight operand images of every forward / input-gradient GEMM (one launch)
+        gemm_x3_build_images(jobs, wimg, s);
+        auto img = [&](int i) { return wimg + jobs.offset[i]; };
+        ev(1);
+        // forward
+        k_fwd_in_t<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
+        gemm_x3_fwd(A(A_XT), img(J_FT0), M.view.mt + D::T_B0, A(A_HT), kHid, kInT, n_act, cap, ld, s);
+        k_fwd_mid<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
+        gemm_x3_fwd(A(A_XC), img(J_FC0), M.view.mc + D::C_B0, A(A_H1), kHid, kInC, n_act, cap, ld, s);
+        gemm_x3_fwd(A(A_H1), img(J_FC1), M.view.mc + D::C_B1, A(A_H2), kHid, kHid, n_act, cap, ld, s);
+        gemm_x3_fwd(A(A_H2), img(J_FC2), M.view.mc + D::C_B2, A(A_H3), kHid, kHid, n_act, cap, ld, s);
+        k_fwd_rgb<<<hit_grid, 128, 0, s>>>(M.view, H);
+        launches += 3;
+        ev(2);
+        if (n) {
+            k_loss<<<(n + 127) / 128, 128, 0, s>>>(L, H);
+            ++launches;
+        }
+        ev(3);
+        // backward. f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
+        k_bwd_head_c<<<hit_grid, 128, 0, s>>>(M.view, H);
+        gemm_x3_bwd(Dm(D_C2), img(J_BC2), kHid, kHid, 0, Dm(D_C1), A(A_H2), n_act, cap, ld, s);
+        gemm_x3_bwd(Dm(D_C1), img(J_BC1), kHid, kHid, 0, Dm(D_C0), A(A_H1), n_act, cap, ld, s);
+        gemm_x3_bwd(Dm(D_C0), img(J_BC0), kHid, kInC, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
+        // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
+        k_bwd_feat_c<<<sc_grid, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
+        gemm_x3_bwd(Dm(D_T0), img(J_BT0), kHid, kInT, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
+        k_bwd_feat_t<<<sc_grid, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
+        launches += 3;
+        // weight gradients (sums over hits, CTA-ordered partials, one reduction launch)
+        {
+            X3DwJob dw[kX3MaxDwJobs];
+            int nj = 0;
+            dw[nj++] = {Dm(D_T0), A(A_XT), kHid, kInT, g_mt + D::T_W0, g_mt + D::T_B0};
+            dw[nj++] = {Dm(D_T1), A(A_HT), 2, kHid, g_mt + D::T_W1, g_mt + D::T_B1};
+            if (!o.color_frozen) {
+                dw[nj++] = {Dm(D_C0), A(A_XC), kHid, kInC, g_mc + D::C_W0, g_mc + D::C_B0};
+                dw[nj++] = {Dm(D_C1), A(A_H1), kHid, kHid, g_mc + D::C_W1, g_mc + D::C_B1};
+                dw[nj++] = {Dm(D_C2), A(A_H2), kHid, kHid, g_mc + D::C_W2, g_mc + D::C_B2};
+                dw[nj++] = {Dm(D_C3), A(A_H3), 3, kHid, g_mc + D::C_W3, g_mc + D::C_B3};
+            }
+            gemm_x3_dw_batch(dw, nj, n_act, cap, ld, part, prod, s);
+        }
+        if (n) {
+            SVLF_CUDA(cub::DeviceReduce::Sum(scan_tmp, tb_red, ray_loss, red + R_LOSS, int(n), s));
+        } else {
+            SVLF_CUDA(cudaMemsetAsync(red + R_LOSS, 0, 8, s));
+        }
+        k_step_scalars<<<1, 1, 0, s>>>(n, counters, b.trav_counters, n_act, cap, err_flag, red);
+        launches += 2;
+        // data parallel: all-reduce the scalars, the decoder gradients and the union of touched feature rows
+        if (dp) {
+            Collective& C = *o.coll;
+            C.allreduce(red, R_COUNT, CollType::F64, CollOp::Sum, s);
+            C.allreduce(g_mt, SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE, CollType::F32, CollOp::Sum, s);
+            SVLF_CUDA(cudaMemsetAsync(touched, 0, V, s));
+            k_touched<<<loop_grid(cap, 256, 8), 256, 0, s>>>(T, b.hit_leaf, dhit, n_act, cap, touched);
+            C.allreduce(touched, V, CollType::U8, CollOp::Max, s);
+            cub::CountingInputIterator<uint32_t> idx(0);
+            SVLF_CUDA(cub::DeviceSelect::Flagged(scan_tmp, tb_sel, idx, touched, rows, n_rows, int(V), s));
+            k_pack_rows<<<loop_grid(rc, 8, 8), 256, 0, s>>>(rows, n_rows, rc, g_ft, g_fc, packed, false, status);
+            C.allreduce(packed, size_t(rc) * 96, CollType::F32, CollOp::Sum, s);
+            k_pack_rows<<<loop_grid(rc, 8, 8), 256, 0, s>>>(rows, n_rows, rc, g_ft, g_fc, packed, true, status);
+            launches += 4;
+        }
+        k_step_status<<<1, 1, 0, s>>>(red, status);
+        ++launches;
+        ev(4);
+        // Adam (adam_model_step, src/train.cpp:345-360), skipped on the device when the step is flagged
+        if (o.adam) {
+            enqueue_adam(M, d_plan, P, status, nullptr, s);
+            ++launches;
+        }
+        ev(5);
+        k_step_mail<<<1, 1, 0, s>>>(red, status, err_flag, b.trav_counters, n_act, cap, n_rows_dev, mail);
+        ++launches;
+        SVLF_CUDA(cudaMemcpyAsync(S.h_mail, mail, sizeof(StepMail), cudaMemcpyDeviceToHost, s));
+        return launches;
+    };
+
+    // The step's Adam plan (bias corrections change every step) goes to the
+    // device ahead of the step, outside any graph.
+    if (o.adam) {
+        *static_cast<AdamPlan*>(S.h_plan) = adam_plan(M, o.color_frozen, o.lr);
+        SVLF_CUDA(cudaMemcpyAsync(d_plan, S.h_plan, sizeof(AdamPlan), cudaMemcpyHostToDevice, s));
     }
-    if (n) {
-        size_t tb = 0;
-        cub::DeviceReduce::Sum(nullptr, tb, ray_loss, red + R_LOSS, int(n));
-        SVLF_CUDA(cub::DeviceReduce::Sum(S.scan_tmp.ensure<char>(tb), tb, ray_loss, red + R_LOSS, int(n), s));
+    // CUDA graph: the step is captured once and replayed while nothing it bakes
+    // in changes (pointers, sizes, modes, loss weights); not with a host-staged
+    // exchange (it synchronizes inside the step) or $SVLF_TRAIN_GRAPHS=0.
+    static const bool graphs_env = [] {
+        const char* e = std::getenv("SVLF_TRAIN_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    const bool use_graph = graphs_env && !dp;
+    long long launches = 0;
+    if (use_graph) {
+        KeyBuilder k;
+        k.add(T);
+        k.add(M.view);
+        k.add(M.params);
+        k.add(M.grads);
+        k.add(M.adam_m);
+        k.add(M.adam_v);
+        k.add(M.n_ft);
+        k.add(M.n_fc);
+        k.add(b);
+        k.add(o.surface);
+        k.add(o.color_frozen);
+        k.add(o.adam);
+        k.add(o.tf32);
+        k.add(o.lw);
+        k.add(s);
+        k.add(err_flag);
+        k.add(cap);
+        k.add(ld);
+        const DevBuf* bufs[] = {&S.act_first, &S.act_cnt, &S.dpos,    &S.surf_rel, &S.eta_gt, &S.ray_loss,
+                                &S.counters,  &S.red,     &S.status,  &S.loss_out, &S.plan,   &S.dhit,
+                                &S.dray,      &S.hitf,    &S.hitd,    &S.acts,     &S.deltas, &S.dxs,
+                                &S.wimg,      &S.dw_part, &S.scan_tmp};
+        for (const DevBuf* d : bufs) k.add(d->p);
+        k.add(S.h_mail);
+        if (!S.graph || k.v != S.graph_key) {
+            if (S.graph) SVLF_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(S.graph)));
+            S.graph = nullptr;
+            cudaGraph_t g = nullptr;
+            SVLF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            capturing = true;
+            try {
+                launches = enqueue();
+            } catch (...) {
+                capturing = false;
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            capturing = false;
+            SVLF_CUDA(cudaStreamEndCapture(s, &g));
+            cudaGraphExec_t ge = nullptr;
+            SVLF_CUDA(cudaGraphInstantiate(&ge, g, 0));
+            SVLF_CUDA(cudaGraphDestroy(g));
+            S.graph = ge;
+            S.graph_key = std::move(k.v);
+            S.graph_launches = launches;
+            ++S.graph_captures;
+        }
+        SVLF_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(S.graph), s));
+        ++S.graph_replays;
+        note_launch(S.graph_launches);
     } else {
-        SVLF_CUDA(cudaMemsetAsync(red + R_LOSS, 0, 8, s));
+        note_launch(enqueue());
     }
-    k_step_scalars<<<1, 1, 0, s>>>(n, counters, b.trav_counters, n_act, cap, err_flag, red);
-    note_launch(2);
-
-    // ---- data parallel: all-reduce the scalars, the decoder gradients and
-    // the union of touched feature rows
-    const uint32_t* n_rows_dev = nullptr;
-    if (o.coll && o.coll->world > 1) {
-        Collective& C = *o.coll;
-        C.allreduce(red, R_COUNT, CollType::F64, CollOp::Sum, s);
-        C.allreduce(g_mt, SVLF_DEC_T_SIZE + SVLF_DEC_C_SIZE, CollType::F32, CollOp::Sum, s);
-        const uint32_t V = M.view.V;
-        uint8_t* touched = S.touched.ensure<uint8_t>(V);
-        SVLF_CUDA(cudaMemsetAsync(touched, 0, V, s));
-        k_touched<<<loop_grid(cap, 256, 8), 256, 0, s>>>(T, b.hit_leaf, dhit, n_act, cap, touched);
-        C.allreduce(touched, V, CollType::U8, CollOp::Max, s);
-        uint32_t* rows = S.rows.ensure<uint32_t>(V);
-        uint32_t* n_rows = S.n_rows.ensure<uint32_t>(1);
-        size_t tb = 0;
-        cub::CountingInputIterator<uint32_t> idx(0);
-        cub::DeviceSelect::Flagged(nullptr, tb, idx, touched, rows, n_rows, int(V));
-        SVLF_CUDA(cub::DeviceSelect::Flagged(S.scan_tmp.ensure<char>(tb), tb, idx, touched, rows, n_rows, int(V), s));
-        if (S.rows_cap == 0) S.rows_cap = std::min<uint32_t>(V, 1u << 16);
-        const uint32_t rc = std::min<uint32_t>(S.rows_cap, V);
-        float* packed = S.packed.ensure<float>(size_t(rc) * 96);
-        k_pack_rows<<<loop_grid(rc, 8, 8), 256, 0, s>>>(rows, n_rows, rc, g_ft, g_fc, packed, false, status);
-        C.allreduce(packed, size_t(rc) * 96, CollType::F32, CollOp::Sum, s);
-        k_pack_rows<<<loop_grid(rc, 8, 8), 256, 0, s>>>(rows, n_rows, rc, g_ft, g_fc, packed, true, status);
-        note_launch(4);
-        n_rows_dev = n_rows;
-    }
-    k_step_status<<<1, 1, 0, s>>>(red, status);
-    note_launch();
-    SVLF_CUDA(cudaEventRecord(S.ev[4], s));
-
-    // ---- Adam (adam_model_step, src/train.cpp:345-360), skipped on the device
-    // when the step is flagged
-    if (o.adam) launch_adam(M, o.color_frozen, o.lr, status, nullptr, s);
-    SVLF_CUDA(cudaEventRecord(S.ev[5], s));
-    k_step_mail<<<1, 1, 0, s>>>(red, status, err_flag, b.trav_counters, n_act, cap, n_rows_dev, mail);
-    note_launch();
-    SVLF_CUDA(cudaMemcpyAsync(S.h_mail, mail, sizeof(StepMail), cudaMemcpyDeviceToHost, s));
     SVLF_CUDA(cudaStreamSynchronize(s));
     StepMail hm;
     std::memcpy(&hm, S.h_mail, sizeof hm);
@@ -1156,7 +1284,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     res.touched_rows = hm.rows;
     res.updated = o.adam && hm.flags == 0 && hm.err == 0;
     if (hm.err) SVLF_CUDA(cudaMemsetAsync(err_flag, 0, 4, s));
-    if (n_rows_dev) {  // next step's exchange buffer: 25 % headroom over this step's touched rows
+    if (dp) {  // next step's exchange buffer: 25 % headroom over this step's touched rows
         const uint32_t want = std::max<uint32_t>(4096, hm.rows + hm.rows / 4);
         if ((hm.flags & kStepRowOverflow) || want < S.rows_cap / 2 || want > S.rows_cap) S.rows_cap = want;
     }

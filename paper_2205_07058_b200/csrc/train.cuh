@@ -1,6 +1,8 @@
 // Train-step pipeline interface (train.cu).
 #pragma once
 
+#include <vector>
+
 #include "device.cuh"
 
 namespace svlfb {
@@ -90,6 +92,11 @@ struct TrainScratch {
     uint32_t rows_cap = 0;                      // capacity of the exchanged-row buffer (grows on overflow)
     uint32_t act_cap = 0;                       // capacity of the per-active-hit matrices (grows on overflow)
     uint64_t* h_mail = nullptr;                 // pinned readback mailbox (one sync per step)
+    void* h_plan = nullptr;                     // pinned staging of the step's Adam plan
+    DevBuf plan;                                // the Adam plan on the device
+    void* graph = nullptr;                      // cudaGraphExec_t of the captured step (replayed while the key holds)
+    std::vector<uint64_t> graph_key;
+    long long graph_captures = 0, graph_replays = 0, graph_launches = 0;
     cudaEvent_t ev[8] = {};
     ~TrainScratch();
 };
