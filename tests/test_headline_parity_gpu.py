@@ -218,22 +218,18 @@ def test_step_buffers_grow_and_rerun(c3):
     2^18-ray C3 batch (~154 K active hits): the step detects the overflow on the device, skips its
     update, grows the buffers and re-runs (new graph capture); the result equals a fresh context's."""
     tree, rays, cgt, depth, alpha, refs = c3
-    fresh = P.Context(0)
-    small = P.Context(0)
-    try:
-        t_f = P.SparseOctree.from_leaves(tree.leaf_codes, tree.config, fresh)
-        t_s = P.SparseOctree.from_leaves(tree.leaf_codes, tree.config, small)
-        m_f, m_s = P.Model(t_f, seed=0, ctx=fresh), P.Model(t_s, seed=0, ctx=small)
-        P.loss_grads(m_s, rays[:4096], cgt[:4096], depth[:4096], alpha[:4096], mode="volumetric")
-        l_s = P.train_step(m_s, rays, cgt, depth, alpha, mode="volumetric", lr=1e-3)
-        l_f = P.train_step(m_f, rays, cgt, depth, alpha, mode="volumetric", lr=1e-3)
-        assert l_s == l_f
-        assert m_s.get_adam()[2].tolist() == [1] * 14  # exactly one update despite the re-run
-        for a, b in zip(m_s.get_params(), m_f.get_params()):
-            d = np.abs(a - b)
-            assert np.mean(d > 1e-6) < 1e-3 and d.max() <= 2.5e-3
-    finally:
-        for x in ("m_s", "m_f", "t_s", "t_f"):
-            locals().pop(x, None)
-        fresh.close()
-        small.close()
+    fresh, small = P.Context(0), P.Context(0)
+    t_f = P.SparseOctree.from_leaves(tree.leaf_codes, tree.config, fresh)
+    t_s = P.SparseOctree.from_leaves(tree.leaf_codes, tree.config, small)
+    m_f, m_s = P.Model(t_f, seed=0, ctx=fresh), P.Model(t_s, seed=0, ctx=small)
+    P.loss_grads(m_s, rays[:4096], cgt[:4096], depth[:4096], alpha[:4096], mode="volumetric")
+    l_s = P.train_step(m_s, rays, cgt, depth, alpha, mode="volumetric", lr=1e-3)
+    l_f = P.train_step(m_f, rays, cgt, depth, alpha, mode="volumetric", lr=1e-3)
+    assert l_s == l_f
+    assert m_s.get_adam()[2].tolist() == [1] * 14  # exactly one update despite the re-run
+    for a, b in zip(m_s.get_params(), m_f.get_params()):
+        d = np.abs(a - b)
+        assert np.mean(d > 1e-6) < 1e-3 and d.max() <= 2.5e-3
+    del m_s, m_f, t_s, t_f
+    fresh.close()
+    small.close()
