@@ -1642,17 +1642,60 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
     float* d_cgt = S.c_gt.ensure<float>(size_t(nn) * 3 + 3);
     double* d_depth = S.depth.ensure<double>(size_t(nn) + 1);
     uint8_t* d_alpha = S.alpha.ensure<uint8_t>(size_t(nn) + 1);
-    if (nn) {
-        const cudaMemcpyKind kind = device_inputs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, kind, s));
-        if (device_inputs) {  // supervision read in place
-            d_cgt = const_cast<float*>(c_gt);
-            d_depth = const_cast<double*>(depth_gt);
-            d_alpha = const_cast<uint8_t*>(alpha_gt);
+    if (nn && device_inputs) {  // rays copied (the traversal writes into ctx->rays), supervision read in place
+        SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyDeviceToDevice, s));
+        d_cgt = const_cast<float*>(c_gt);
+        d_depth = const_cast<double*>(depth_gt);
+        d_alpha = const_cast<uint8_t*>(alpha_gt);
+    } else if (nn) {
+        // Host batch: page-locked inputs go straight to the device; pageable ones
+        // are copied into page-locked staging by the host worker pool in chunks,
+        // each chunk's DMA overlapping the next chunk's host copy.
+        struct Part {
+            const void* src;
+            void* dst;
+            size_t elem;
+        };
+        const Part parts[4] = {{rays, d_rays, 48}, {c_gt, d_cgt, 12}, {depth_gt, d_depth, 8}, {alpha_gt, d_alpha, 1}};
+        const size_t per_ray = 48 + 12 + 8 + 1;
+        const bool pinned = is_pinned(rays) && is_pinned(c_gt) && is_pinned(depth_gt) && is_pinned(alpha_gt);
+        if (pinned) {
+            for (const Part& p : parts) SVLF_CUDA(cudaMemcpyAsync(p.dst, p.src, p.elem * nn, cudaMemcpyHostToDevice, s));
         } else {
-            SVLF_CUDA(cudaMemcpyAsync(d_cgt, c_gt, size_t(nn) * 12, kind, s));
-            SVLF_CUDA(cudaMemcpyAsync(d_depth, depth_gt, size_t(nn) * 8, kind, s));
-            SVLF_CUDA(cudaMemcpyAsync(d_alpha, alpha_gt, size_t(nn), kind, s));
+            if (S.h_stage_bytes < per_ray * nn) {
+                if (S.h_stage) SVLF_CUDA(cudaFreeHost(S.h_stage));
+                S.h_stage = nullptr;
+                S.h_stage_bytes = 0;
+                SVLF_CUDA(cudaMallocHost(&S.h_stage, per_ray * nn));
+                S.h_stage_bytes = per_ray * nn;
+            }
+            if (!ctx->pool) {
+                const char* e = std::getenv("SVLF_HOST_THREADS");
+                const int hw = int(std::thread::hardware_concurrency());
+                ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
+            }
+            const uint32_t chunks = nn >= (1u << 16) ? 4u : 1u;
+            char* stage = static_cast<char*>(S.h_stage);
+            for (uint32_t c = 0; c < chunks; ++c) {
+                const size_t r0 = size_t(nn) * c / chunks, r1 = size_t(nn) * (c + 1) / chunks;
+                const int tasks = ctx->pool->size() * 2;
+                ctx->pool->parallel_for(tasks, [&](int i) {
+                    const size_t a = r0 + (r1 - r0) * size_t(i) / size_t(tasks);
+                    const size_t b = r0 + (r1 - r0) * size_t(i + 1) / size_t(tasks);
+                    size_t base = 0;
+                    for (const Part& p : parts) {
+                        std::memcpy(stage + base + a * p.elem, static_cast<const char*>(p.src) + a * p.elem,
+                                    (b - a) * p.elem);
+                        base += p.elem * nn;
+                    }
+                });
+                size_t base = 0;
+                for (const Part& p : parts) {
+                    SVLF_CUDA(cudaMemcpyAsync(static_cast<char*>(p.dst) + r0 * p.elem, stage + base + r0 * p.elem,
+                                              (r1 - r0) * p.elem, cudaMemcpyHostToDevice, s));
+                    base += p.elem * nn;
+                }
+            }
         }
     }
     // Traversal and step are enqueued with no host round trip; the step's one

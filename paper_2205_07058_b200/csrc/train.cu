@@ -925,6 +925,7 @@ TrainScratch::~TrainScratch() {
     if (graph) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph));
     if (h_mail) cudaFreeHost(h_mail);
     if (h_plan) cudaFreeHost(h_plan);
+    if (h_stage) cudaFreeHost(h_stage);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
 }

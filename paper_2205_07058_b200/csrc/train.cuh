@@ -93,6 +93,8 @@ struct TrainScratch {
     uint32_t act_cap = 0;                       // capacity of the per-active-hit matrices (grows on overflow)
     uint64_t* h_mail = nullptr;                 // pinned readback mailbox (one sync per step)
     void* h_plan = nullptr;                     // pinned staging of the step's Adam plan
+    void* h_stage = nullptr;                    // pinned staging of a pageable host batch
+    size_t h_stage_bytes = 0;
     DevBuf plan;                                // the Adam plan on the device
     void* graph = nullptr;                      // cudaGraphExec_t of the captured step (replayed while the key holds)
     std::vector<uint64_t> graph_key;
