@@ -59,6 +59,30 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// TMA store of a shared-memory box (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int kN>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kN) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// L2 prefetch of a future tile (no shared memory): the loads of the stages
+// then hit L2 instead of waiting out the DRAM latency
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+#ifndef SVLF_GEMM_PREFETCH
+#define SVLF_GEMM_PREFETCH 0  // chunks ahead of the one being loaded (0: off; measured: 4 and 8 slower)
+#endif
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
@@ -158,7 +182,9 @@ constexpr uint32_t kFStage = 2 * kFA + 2 * kFB;
 constexpr uint32_t kFStages = SVLF_GEMM_FSTAGES;
 constexpr uint32_t kFThreads = 448;  // warp 0 TMA, 1 MMA, 2-9 split, 10-13 epilogue
 constexpr uint32_t kFSplitWarps = 8;
-constexpr uint32_t kFSmem = kFStages * kFStage + 1024 + 256;
+// epilogue staging: per epilogue warp two 32 x 32 fp32 boxes (128-byte swizzle), stored by TMA
+constexpr uint32_t kFEpi = 4 * 2 * 4096;
+constexpr uint32_t kFSmem = kFStages * kFStage + kFEpi + 1024 + 256;
 constexpr uint32_t kTmemAcc = kNT;  // TMEM columns per accumulator (two: tile t's epilogue overlaps t+1's MMAs)
 constexpr uint32_t kTmemCols = 2 * kTmemAcc <= 256 ? 256 : 512;  // allocation: a power of two
 
@@ -171,12 +197,13 @@ __device__ __forceinline__ uint32_t tile_hits(uint32_t n, uint32_t ctas) {
 
 template <bool kBwd>
 __global__ void __launch_bounds__(kFThreads, 1)
-    k_gemm_feat(const __grid_constant__ CUtensorMap in_map, const uint8_t* __restrict__ wimg, float* __restrict__ out,
+    k_gemm_feat(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+                const uint8_t* __restrict__ wimg, float* __restrict__ out,
                 const float* __restrict__ bias, const float* __restrict__ mask, const uint32_t* __restrict__ n_dev,
                 uint32_t cap, uint32_t ld, uint32_t kred, uint32_t n_out) {
     extern __shared__ uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kFStages * kFStage);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kFStages * kFStage + kFEpi);
     uint64_t* full = bars;                       // [stages] TMA landed
     uint64_t* split_done = bars + kFStages;      // [stages] converters done (one arrival per split warp)
     uint64_t* empty = bars + 2 * kFStages;       // [stages] MMAs of the stage done (commit)
@@ -196,6 +223,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&in_map);
+        prefetch_tmap(&out_map);
     }
     if (warp == 1) tmem_alloc(holder, kTmemCols);
     fence_before_sync();
@@ -218,6 +246,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
             for (uint32_t g = 0; g < total; ++g) {
                 const uint32_t s = g % kFStages, u = g / kFStages, c = g % nch;
                 const uint32_t tile = blockIdx.x + (g / nch) * gridDim.x;
+                if (SVLF_GEMM_PREFETCH && g == 0)  // the first chunks' tiles
+                    for (uint32_t gp = 0; gp < min(total, uint32_t(SVLF_GEMM_PREFETCH)); ++gp)
+                        for (uint32_t b = 0; b < nb; ++b)
+                            tma_prefetch_2d(&in_map, int((blockIdx.x + (gp / nch) * gridDim.x) * nt + 32 * b),
+                                            int((gp % nch) * kChunk));
+                if (SVLF_GEMM_PREFETCH && g + SVLF_GEMM_PREFETCH < total) {
+                    const uint32_t gp = g + SVLF_GEMM_PREFETCH;
+                    const uint32_t tp = blockIdx.x + (gp / nch) * gridDim.x;
+                    for (uint32_t b = 0; b < nb; ++b)
+                        tma_prefetch_2d(&in_map, int(tp * nt + 32 * b), int((gp % nch) * kChunk));
+                }
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
                 mbar_expect_tx(&full[s], 2 * kFA + nb * 4096);
                 bulk_g2s(stage_a(s), wimg + size_t(c) * 2 * kFA, 2 * kFA, &full[s]);
@@ -277,25 +316,34 @@ __global__ void __launch_bounds__(kFThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive1(&split_done[s]);
         }
-    } else {  // epilogue: TMEM -> bias + relu (Fwd) / relu' mask (Bwd) -> global
+    } else {  // epilogue: TMEM -> bias + relu (Fwd) / relu' mask (Bwd) -> shared box -> TMA store
         const uint32_t q = warp & 3u, j = 32 * q + lane;
         const float bj = (!kBwd && j < n_out) ? __ldg(bias + j) : 0.f;
+        // this warp's two staging boxes: row r (= lane) holds 32 hits, 16-byte chunk c at c ^ (r & 7)
+        const uint32_t stage0 = sbase + kFStages * kFStage + (warp - 2 - kFSplitWarps) * 8192;
+        uint32_t nbox = 0;
         for (uint32_t t = 0; t < my_tiles; ++t) {
             const uint32_t b = t & 1, v = t >> 1;
+            const uint32_t tile = blockIdx.x + t * gridDim.x;
+            if constexpr (kBwd) {
+                // the relu' mask row segment of this tile to L2 while its MMAs run
+                if (mask && j < n_out) {
+                    const float* mk = mask + size_t(j) * ld + size_t(tile) * nt;
+                    for (uint32_t off = 0; off < nt; off += 32)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(mk + off));
+                }
+            }
             mbar_wait(&accf[b], v & 1);
             fence_after_sync();
-            const uint32_t tile = blockIdx.x + t * gridDim.x;
             for (uint32_t bt = 0; bt < nb; ++bt) {
                 float r[32];
                 tmem_ld32(tmem + kTmemAcc * b + ((32u * q) << 16) + 32 * bt, r);
                 tmem_wait_ld();
-                if (j >= n_out) continue;
                 const uint32_t h0 = tile * nt + 32 * bt;
-                const uint32_t cnt = n > h0 ? min(32u, n - h0) : 0u;
-                if (cnt == 0) continue;
-                float* o = out + size_t(j) * ld + h0;
+                if (32 * q >= n_out || h0 >= n) continue;  // warp-uniform: nothing of this box is stored
+                const uint32_t cnt = min(32u, n - h0);
                 if constexpr (kBwd) {
-                    if (mask) {
+                    if (mask && j < n_out) {
                         const float* mk = mask + size_t(j) * ld + h0;
                         if (cnt == 32) {
 #pragma unroll
@@ -316,20 +364,31 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + bj, 0.f);
                 }
-                if (cnt == 32) {
+                // stage the 32 x 32 box (the buffer's previous store must have read it), then TMA-store
+                // it: rows past n_out and hits past the matrix width are clipped by the tensor map;
+                // columns past n carry values of stale inputs and are never read
+                const uint32_t buf = stage0 + (nbox & 1) * 4096;
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        reinterpret_cast<float4*>(o)[i] = make_float4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (uint32_t(i) < cnt) o[i] = r[i];
+                for (uint32_t c = 0; c < 8; ++c)
+                    st_shared_v4(buf + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(r[4 * c]),
+                                 __float_as_uint(r[4 * c + 1]), __float_as_uint(r[4 * c + 2]),
+                                 __float_as_uint(r[4 * c + 3]));
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&out_map, buf, int(h0), int(32 * q));
+                    bulk_commit();
                 }
+                ++nbox;
             }
             fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive1(&acce[b]);
         }
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
     }
     fence_before_sync();
     __syncthreads();
@@ -396,6 +455,15 @@ __global__ void __launch_bounds__(kDThreads, 1)
         if (lane == 0) {
             for (uint32_t c = 0; c < nch; ++c) {
                 const uint32_t s = c % kDStages, u = c / kDStages;
+                if (SVLF_GEMM_PREFETCH && c == 0)
+                    for (uint32_t cp = 0; cp < min(nch, uint32_t(SVLF_GEMM_PREFETCH)); ++cp) {
+                        tma_prefetch_2d(&d_map, int(h0 + cp * kChunk), 0);
+                        tma_prefetch_2d(&x_map, int(h0 + cp * kChunk), 0);
+                    }
+                if (SVLF_GEMM_PREFETCH && c + SVLF_GEMM_PREFETCH < nch) {
+                    tma_prefetch_2d(&d_map, int(h0 + (c + SVLF_GEMM_PREFETCH) * kChunk), 0);
+                    tma_prefetch_2d(&x_map, int(h0 + (c + SVLF_GEMM_PREFETCH) * kChunk), 0);
+                }
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
                 mbar_expect_tx(&full[s], kDA + bB);
                 tma_2d(sa(s), &d_map, int(h0 + c * kChunk), 0, &full[s]);
@@ -663,7 +731,9 @@ void gemm_x3_fwd(const float* x, const uint8_t* img, const float* bias, float* y
     if (cap == 0) return;
     setup();
     const CUtensorMap map = feature_map(x, K, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    k_gemm_feat<false><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, img, y, bias, nullptr, n_dev, cap, ld, K, O);
+    const CUtensorMap omap = feature_map(y, O, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    k_gemm_feat<false><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, img, y, bias, nullptr, n_dev, cap, ld, K,
+                                                                 O);
     note_launch();
 }
 
@@ -672,7 +742,9 @@ void gemm_x3_bwd(const float* d, const uint8_t* img, uint32_t O, uint32_t K, uin
     if (cap == 0) return;
     setup();
     const CUtensorMap map = feature_map(d, O, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    k_gemm_feat<true><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, img, dx, nullptr, mask, n_dev, cap, ld, O, K - k0);
+    const CUtensorMap omap = feature_map(dx, K - k0, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    k_gemm_feat<true><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, img, dx, nullptr, mask, n_dev, cap, ld, O,
+                                                                K - k0);
     note_launch();
 }
 
