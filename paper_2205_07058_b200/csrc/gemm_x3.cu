@@ -114,6 +114,12 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uin
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
     uint32_t h;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
@@ -299,18 +305,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (uint32_t g = 0; g < total; ++g) {
             const uint32_t s = g % kFStages, u = g / kFStages;
             mbar_wait(&full[s], u & 1);
-            uint4* hi = reinterpret_cast<uint4*>(sm + s * kFStage + 2 * kFA);
-            uint4* lo = reinterpret_cast<uint4*>(sm + s * kFStage + 2 * kFA + kFB);
+            const uint32_t hi = stage_b(s), lo = hi + kFB;
 #pragma unroll 4
             for (uint32_t i = ct; i < nb * 256; i += 32 * kFSplitWarps) {
-                const uint4 x = hi[i];
+                const uint4 x = ld_shared_v4(hi + 16 * i);
                 uint4 h, l;
                 split(x.x, h.x, l.x);
                 split(x.y, h.y, l.y);
                 split(x.z, h.z, l.z);
                 split(x.w, h.w, l.w);
-                hi[i] = h;
-                lo[i] = l;
+                st_shared_v4(hi + 16 * i, h.x, h.y, h.z, h.w);
+                st_shared_v4(lo + 16 * i, l.x, l.y, l.z, l.w);
             }
             fence_async_smem();
             __syncwarp();
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
                     tma_prefetch_2d(&x_map, int(h0 + (c + SVLF_GEMM_PREFETCH) * kChunk), 0);
                 }
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-                mbar_expect_tx(&full[s], kDA + bB);
+                mbar_expect_tx(&full[s], 128 * (O + K));
                 tma_2d(sa(s), &d_map, int(h0 + c * kChunk), 0, &full[s]);
                 tma_2d(sb(s), &x_map, int(h0 + c * kChunk), 0, &full[s]);
             }
@@ -498,6 +503,22 @@ __global__ void __launch_bounds__(kDThreads, 1)
         }
     } else {
         const uint32_t ct = tid - 64;
+        // The boxes carry only the O rows of D and the K rows of X; the rest of every stage is
+        // constant and written once: A rows O..127 and B rows K+1.. zero (hi and lo), B row K the
+        // bias column (hi 1.0, lo 0; hits past the range zeroed in the tail chunk below).
+        for (uint32_t s = 0; s < kDStages; ++s) {
+            const uint32_t a = sa(s), bsm = sb(s);
+            for (uint32_t i = ct; i < (128 - O) * 8; i += 32 * kDSplitWarps) {
+                st_shared_v4(a + O * 128 + 16 * i, 0u, 0u, 0u, 0u);
+                st_shared_v4(a + kDA + O * 128 + 16 * i, 0u, 0u, 0u, 0u);
+            }
+            const uint32_t one = __float_as_uint(1.f);
+            for (uint32_t i = ct; i < (Nr - K) * 8; i += 32 * kDSplitWarps) {
+                const uint32_t v = i < 8 ? one : 0u;
+                st_shared_v4(bsm + K * 128 + 16 * i, v, v, v, v);
+                st_shared_v4(bsm + bB + K * 128 + 16 * i, 0u, 0u, 0u, 0u);
+            }
+        }
         for (uint32_t c = 0; c < nch; ++c) {
             const uint32_t s = c % kDStages, u = c / kDStages;
             const uint32_t hb = h0 + c * kChunk;
@@ -505,18 +526,12 @@ __global__ void __launch_bounds__(kDThreads, 1)
             mbar_wait(&full[s], u & 1);
             // 16-byte chunk i of a tile: row r = i / 8, physical chunk p = i % 8 holding hits
             // 4 * (p ^ (r & 7)) .. + 3 of the chunk (128-byte swizzle)
-            auto do_tile = [&](uint8_t* base, uint32_t lo_off, uint32_t rows, bool bias_row) {
-                uint4* hi = reinterpret_cast<uint4*>(base);
-                uint4* lo = reinterpret_cast<uint4*>(base + lo_off);
+            auto do_rows = [&](uint32_t hi, uint32_t lo_off, uint32_t rows) {
 #pragma unroll 4
                 for (uint32_t i = ct; i < rows * 8; i += 32 * kDSplitWarps) {
-                    const uint32_t r = i >> 3, p = i & 7, hit = hb + 4 * (p ^ (r & 7));
-                    uint4 x = hi[i];
-                    if (bias_row && r == K) {
-                        const uint32_t one = __float_as_uint(1.f);
-                        x = make_uint4(one, one, one, one);
-                    }
-                    if (tail && hit + 4 > h1) {  // hits past the range: zero (stale matrix columns)
+                    uint4 x = ld_shared_v4(hi + 16 * i);
+                    if (tail) {  // hits past the range: zero (stale matrix columns)
+                        const uint32_t hit = hb + 4 * ((i & 7) ^ ((i >> 3) & 7));
                         if (hit >= h1) x.x = 0u;
                         if (hit + 1 >= h1) x.y = 0u;
                         if (hit + 2 >= h1) x.z = 0u;
@@ -528,15 +543,22 @@ __global__ void __launch_bounds__(kDThreads, 1)
                         split(x.y, h.y, l.y);
                         split(x.z, h.z, l.z);
                         split(x.w, h.w, l.w);
-                        hi[i] = h;
-                        lo[i] = l;
-                    } else {
-                        hi[i] = x;
+                        st_shared_v4(hi + 16 * i, h.x, h.y, h.z, h.w);
+                        st_shared_v4(hi + lo_off + 16 * i, l.x, l.y, l.z, l.w);
+                    } else if (tail) {
+                        st_shared_v4(hi + 16 * i, x.x, x.y, x.z, x.w);
                     }
                 }
             };
-            do_tile(sm + s * kDStage, kDA, 128, false);
-            do_tile(sm + s * kDStage + 2 * kDA, bB, Nr, true);
+            do_rows(sa(s), kDA, O);
+            do_rows(sb(s), bB, K);
+            if (tail)  // the bias column: ones for the hits in range only
+                for (uint32_t i = ct; i < 8; i += 32 * kDSplitWarps) {
+                    const uint32_t hit = hb + 4 * (i ^ (K & 7));
+                    const uint32_t one = __float_as_uint(1.f);
+                    st_shared_v4(sb(s) + K * 128 + 16 * i, hit < h1 ? one : 0u, hit + 1 < h1 ? one : 0u,
+                                 hit + 2 < h1 ? one : 0u, hit + 3 < h1 ? one : 0u);
+                }
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive1(&split_done[s]);
@@ -771,8 +793,8 @@ void gemm_x3_dw_batch(const X3DwJob* jobs, int count, const uint32_t* n_dev, uin
         const X3DwJob& jb = jobs[i];
         const uint32_t Nr = round16(jb.K + 1);
         if (Nr > 144) fail(SVLF_ERR_INVALID_ARGUMENT, "weight-gradient GEMM: K too large");
-        const CUtensorMap dmap = feature_map(jb.d, jb.O, ld, ld, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-        const CUtensorMap xmap = feature_map(jb.x, jb.K, ld, ld, Nr, CU_TENSOR_MAP_SWIZZLE_128B);
+        const CUtensorMap dmap = feature_map(jb.d, jb.O, ld, ld, jb.O, CU_TENSOR_MAP_SWIZZLE_128B);
+        const CUtensorMap xmap = feature_map(jb.x, jb.K, ld, ld, jb.K, CU_TENSOR_MAP_SWIZZLE_128B);
         float* p = part + off;
         if (products == 1)
             k_gemm_dw<false><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, p, n_dev, cap, jb.O, jb.K, Nr);
@@ -795,8 +817,8 @@ void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* d
     setup();
     const uint32_t Nr = round16(K + 1), ctas = dw_grid(cap);
     if (Nr > 144) fail(SVLF_ERR_INVALID_ARGUMENT, "weight-gradient GEMM: K too large");
-    const CUtensorMap dmap = feature_map(d, O, ld, ld, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    const CUtensorMap xmap = feature_map(x, K, ld, ld, Nr, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap dmap = feature_map(d, O, ld, ld, O, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap xmap = feature_map(x, K, ld, ld, K, CU_TENSOR_MAP_SWIZZLE_128B);
     if (products == 1)
         k_gemm_dw<false><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, part, n_dev, cap, O, K, Nr);
     else
