@@ -204,7 +204,7 @@ __device__ __forceinline__ uint32_t tile_hits(uint32_t n, uint32_t ctas) {
 template <bool kBwd>
 __global__ void __launch_bounds__(kFThreads, 1)
     k_gemm_feat(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-                const uint8_t* __restrict__ wimg, float* __restrict__ out,
+                const __grid_constant__ CUtensorMap mask_map, const uint8_t* __restrict__ wimg, float* __restrict__ out,
                 const float* __restrict__ bias, const float* __restrict__ mask, const uint32_t* __restrict__ n_dev,
                 uint32_t cap, uint32_t ld, uint32_t kred, uint32_t n_out) {
     extern __shared__ uint8_t sm_raw[];
@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
     uint64_t* empty = bars + 2 * kFStages;       // [stages] MMAs of the stage done (commit)
     uint64_t* accf = bars + 3 * kFStages;        // [2] accumulator ready (commit)
     uint64_t* acce = bars + 3 * kFStages + 2;    // [2] accumulator drained (4 arrivals)
-    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 3 * kFStages + 4);
+    uint64_t* mbox = bars + 3 * kFStages + 4;    // [4 warps][2 buffers] mask box landed (Bwd)
+    uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 3 * kFStages + 12);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (uint32_t i = 0; i < kFStages; ++i) {
@@ -227,9 +228,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
             mbar_init(&accf[i], 1);
             mbar_init(&acce[i], 4);
         }
+        for (int i = 0; i < 8; ++i) mbar_init(&mbox[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&in_map);
         prefetch_tmap(&out_map);
+        if (kBwd && mask) prefetch_tmap(&mask_map);
     }
     if (warp == 1) tmem_alloc(holder, kTmemCols);
     fence_before_sync();
@@ -322,59 +325,61 @@ __global__ void __launch_bounds__(kFThreads, 1)
             if (lane == 0) mbar_arrive1(&split_done[s]);
         }
     } else {  // epilogue: TMEM -> bias + relu (Fwd) / relu' mask (Bwd) -> shared box -> TMA store
-        const uint32_t q = warp & 3u, j = 32 * q + lane;
+        const uint32_t q = warp & 3u, j = 32 * q + lane, ew = warp - 2 - kFSplitWarps;
         const float bj = (!kBwd && j < n_out) ? __ldg(bias + j) : 0.f;
-        // this warp's two staging boxes: row r (= lane) holds 32 hits, 16-byte chunk c at c ^ (r & 7)
-        const uint32_t stage0 = sbase + kFStages * kFStage + (warp - 2 - kFSplitWarps) * 8192;
-        uint32_t nbox = 0;
-        for (uint32_t t = 0; t < my_tiles; ++t) {
-            const uint32_t b = t & 1, v = t >> 1;
-            const uint32_t tile = blockIdx.x + t * gridDim.x;
-            if constexpr (kBwd) {
-                // the relu' mask row segment of this tile to L2 while its MMAs run
-                if (mask && j < n_out) {
-                    const float* mk = mask + size_t(j) * ld + size_t(tile) * nt;
-                    for (uint32_t off = 0; off < nt; off += 32)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(mk + off));
-                }
+        // this warp's two staging boxes: row r (= lane) holds 32 hits, 16-byte chunk c at c ^ (r & 7).
+        // Bwd with a mask: the box first receives the mask (TMA load, same swizzle), each thread
+        // masks its row in place, and the box is stored back to the output.
+        const uint32_t stage0 = sbase + kFStages * kFStage + ew * 8192;
+        const bool use_mask = kBwd && mask != nullptr && 32 * q < n_out;
+        const uint32_t nboxes = my_tiles * nb;
+        uint32_t mphase = 0;  // parity bit per buffer
+        auto box_h0 = [&](uint32_t k) { return (blockIdx.x + (k / nb) * gridDim.x) * nt + 32 * (k % nb); };
+        auto load_mask = [&](uint32_t k) {  // lane 0
+            if (box_h0(k) >= n) return;
+            uint64_t* bar = &mbox[2 * ew + (k & 1)];
+            mbar_expect_tx(bar, 4096);
+            tma_2d(stage0 + (k & 1) * 4096, &mask_map, int(box_h0(k)), int(32 * q), bar);
+        };
+        if (use_mask && lane == 0 && nboxes) load_mask(0);
+        for (uint32_t k = 0; k < nboxes; ++k) {
+            const uint32_t t = k / nb, bt = k % nb, b = t & 1, v = t >> 1;
+            if (bt == 0) {
+                mbar_wait(&accf[b], v & 1);
+                fence_after_sync();
             }
-            mbar_wait(&accf[b], v & 1);
-            fence_after_sync();
-            for (uint32_t bt = 0; bt < nb; ++bt) {
-                float r[32];
-                tmem_ld32(tmem + kTmemAcc * b + ((32u * q) << 16) + 32 * bt, r);
-                tmem_wait_ld();
-                const uint32_t h0 = tile * nt + 32 * bt;
-                if (32 * q >= n_out || h0 >= n) continue;  // warp-uniform: nothing of this box is stored
-                const uint32_t cnt = min(32u, n - h0);
-                if constexpr (kBwd) {
-                    if (mask && j < n_out) {
-                        const float* mk = mask + size_t(j) * ld + h0;
-                        if (cnt == 32) {
+            float r[32];
+            tmem_ld32(tmem + kTmemAcc * b + ((32u * q) << 16) + 32 * bt, r);
+            tmem_wait_ld();
+            const uint32_t h0 = box_h0(k);
+            const uint32_t buf = stage0 + (k & 1) * 4096;
+            if (32 * q < n_out && h0 < n) {  // warp-uniform: else nothing of this box is stored
+                if (use_mask) {
+                    // the next box's mask into the other buffer (its previous store must have read it)
+                    if (lane == 0) {
+                        bulk_wait_read<0>();
+                        if (k + 1 < nboxes) load_mask(k + 1);
+                    }
+                    mbar_wait(&mbox[2 * ew + (k & 1)], (mphase >> (k & 1)) & 1);
+                    mphase ^= 1u << (k & 1);
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const float4 mv = __ldg(reinterpret_cast<const float4*>(mk) + i);
-                                if (!(mv.x > 0.f)) r[4 * i] = 0.f;
-                                if (!(mv.y > 0.f)) r[4 * i + 1] = 0.f;
-                                if (!(mv.z > 0.f)) r[4 * i + 2] = 0.f;
-                                if (!(mv.w > 0.f)) r[4 * i + 3] = 0.f;
-                            }
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 32; ++i)
-                                if (uint32_t(i) < cnt && !(__ldg(mk + i) > 0.f)) r[i] = 0.f;
-                        }
+                    for (uint32_t c = 0; c < 8; ++c) {
+                        const uint4 m = ld_shared_v4(buf + lane * 128 + ((c ^ (lane & 7)) << 4));
+                        if (!(__uint_as_float(m.x) > 0.f)) r[4 * c] = 0.f;
+                        if (!(__uint_as_float(m.y) > 0.f)) r[4 * c + 1] = 0.f;
+                        if (!(__uint_as_float(m.z) > 0.f)) r[4 * c + 2] = 0.f;
+                        if (!(__uint_as_float(m.w) > 0.f)) r[4 * c + 3] = 0.f;
                     }
                 } else {
+                    if (lane == 0) bulk_wait_read<1>();  // the previous store from this buffer has read it
+                    if constexpr (!kBwd) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + bj, 0.f);
+                        for (int i = 0; i < 32; ++i) r[i] = fmaxf(r[i] + bj, 0.f);
+                    }
                 }
-                // stage the 32 x 32 box (the buffer's previous store must have read it), then TMA-store
-                // it: rows past n_out and hits past the matrix width are clipped by the tensor map;
-                // columns past n carry values of stale inputs and are never read
-                const uint32_t buf = stage0 + (nbox & 1) * 4096;
-                if (lane == 0) bulk_wait_read<1>();
                 __syncwarp();
+                // rows past n_out and hits past the matrix width are clipped by the tensor map;
+                // columns past n carry values of stale inputs and are never read
 #pragma unroll
                 for (uint32_t c = 0; c < 8; ++c)
                     st_shared_v4(buf + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(r[4 * c]),
@@ -386,11 +391,15 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     tma_store_2d(&out_map, buf, int(h0), int(32 * q));
                     bulk_commit();
                 }
-                ++nbox;
+            } else if (use_mask && lane == 0 && k + 1 < nboxes) {
+                bulk_wait_read<0>();
+                load_mask(k + 1);
             }
-            fence_before_sync();
-            __syncwarp();
-            if (lane == 0) mbar_arrive1(&acce[b]);
+            if (bt + 1 == nb) {
+                fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive1(&acce[b]);
+            }
         }
         if (lane == 0) bulk_wait_all();
         __syncwarp();
@@ -754,8 +763,8 @@ void gemm_x3_fwd(const float* x, const uint8_t* img, const float* bias, float* y
     setup();
     const CUtensorMap map = feature_map(x, K, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const CUtensorMap omap = feature_map(y, O, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    k_gemm_feat<false><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, img, y, bias, nullptr, n_dev, cap, ld, K,
-                                                                 O);
+    k_gemm_feat<false><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, omap, img, y, bias, nullptr, n_dev, cap,
+                                                                 ld, K, O);
     note_launch();
 }
 
@@ -765,8 +774,9 @@ void gemm_x3_bwd(const float* d, const uint8_t* img, uint32_t O, uint32_t K, uin
     setup();
     const CUtensorMap map = feature_map(d, O, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const CUtensorMap omap = feature_map(dx, K - k0, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    k_gemm_feat<true><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, img, dx, nullptr, mask, n_dev, cap, ld, O,
-                                                                K - k0);
+    const CUtensorMap mmap = mask ? feature_map(mask, K - k0, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B) : omap;
+    k_gemm_feat<true><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, mmap, img, dx, nullptr, mask, n_dev, cap,
+                                                                ld, O, K - k0);
     note_launch();
 }
 
