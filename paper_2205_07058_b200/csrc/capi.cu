@@ -1,6 +1,7 @@
 // C ABI implementation (include/svlf_b200.h): contexts, device mirrors of
 // octrees and models, and the render / traversal / train pipelines.
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -297,9 +298,8 @@ unsigned long long* misc_fg(svlf_ctx* ctx) { return reinterpret_cast<unsigned lo
 // exceeded, [3] dense overflow, [7] ray-box tests of the cooperative passes.
 uint32_t* traversal_counters(svlf_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->misc.as<char>() + 16); }
 
-void enqueue_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0, uint32_t rows,
-                       uint32_t n) {
-    cudaStream_t s = ctx->stream;
+// Buffers of a traversal of n rays (grown here, never inside a graph capture).
+TraverseOut prepare_traversal(svlf_ctx* ctx, uint32_t n) {
     double* rays = ctx->rays.ensure<double>(size_t(n) * 6 + 6);
     uint32_t* ray_off = ctx->offsets.ensure<uint32_t>(size_t(n) + 1);
     uint32_t* ray_cnt = ctx->counts.ensure<uint32_t>(size_t(n) + 1);
@@ -313,15 +313,33 @@ void enqueue_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* 
     ctx->hit_tout.ensure<double>(cap);
     ctx->hit_ray.ensure<uint32_t>(cap);
     ctx->hit_cap = cap;
-    TraverseOut o{ray_off, ray_cnt, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
-                  ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), counters, ovl, ovl2, rays, uint32_t(cap)};
-    SVLF_CUDA(cudaMemsetAsync(counters, 0, 32, s));  // hit/overflow counters, tile cursors, node tests
-    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_START], s));
+    return TraverseOut{ray_off, ray_cnt, ctx->hit_leaf.as<uint32_t>(), ctx->hit_tin.as<double>(),
+                       ctx->hit_tout.as<double>(), ctx->hit_ray.as<uint32_t>(), counters, ovl, ovl2, rays,
+                       uint32_t(cap)};
+}
+
+// The traversal's launches into prepared buffers; `capturing`: inside a CUDA
+// graph capture (the timing events become event-record nodes).
+void launch_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0, uint32_t rows,
+                      uint32_t n, const TraverseOut& o, bool capturing = false) {
+    cudaStream_t s = ctx->stream;
+    auto ev = [&](int k) {
+        if (capturing) SVLF_CUDA(cudaEventRecordWithFlags(ctx->ev[k], s, cudaEventRecordExternal));
+        else SVLF_CUDA(cudaEventRecord(ctx->ev[k], s));
+    };
+    SVLF_CUDA(cudaMemsetAsync(o.counters, 0, 32, s));  // hit/overflow counters, tile cursors, node tests
+    ev(EV_START);
     launch_traverse(dev_view(tree), cam, row0, rows, n, o, s, ctx->count_node_tests);
-    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_COUNT], s));
+    ev(EV_COUNT);
     launch_traverse_dense(dev_view(tree), cam, row0, o, s, ctx->count_node_tests);
     launch_traverse_fallback(dev_view(tree), cam, row0, o, s);
-    SVLF_CUDA(cudaEventRecord(ctx->ev[EV_EMIT], s));
+    ev(EV_EMIT);
+}
+
+void enqueue_traversal(svlf_ctx* ctx, const svlf_octree* tree, const DevCamera* cam, uint32_t row0, uint32_t rows,
+                       uint32_t n) {
+    const TraverseOut o = prepare_traversal(ctx, n);
+    launch_traversal(ctx, tree, cam, row0, rows, n, o);
 }
 
 // Reads the traversal counters (synchronizes). Returns false when the hit
@@ -1708,8 +1726,21 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
     TrainResult r;
     float trav_ms = 0.f;
     for (int attempt = 0;; ++attempt) {
+        // the traversal runs inside the step's graph (captured with it)
+        TraverseOut to{};
+        std::function<void(bool)> pre;
+        std::vector<uint64_t> pre_key;
         if (nn) {
-            enqueue_traversal(ctx, m->tree, nullptr, 0, 0, nn);
+            to = prepare_traversal(ctx, nn);
+            const svlf_octree* tree = m->tree;
+            pre = [ctx, tree, nn, to](bool capturing) { launch_traversal(ctx, tree, nullptr, 0, 0, nn, to, capturing); };
+            for (const void* p : {(const void*)to.ray_off, (const void*)to.ray_cnt, (const void*)to.hit_leaf,
+                                  (const void*)to.hit_tin, (const void*)to.hit_tout, (const void*)to.hit_ray,
+                                  (const void*)to.counters, (const void*)to.overflow_rays, (const void*)to.overflow_dense,
+                                  (const void*)to.rays, (const void*)tree})
+                pre_key.push_back(reinterpret_cast<uint64_t>(p));
+            pre_key.push_back(to.capacity);
+            pre_key.push_back(ctx->count_node_tests ? 1 : 0);
         } else {
             ctx->hit_cap = std::max<size_t>(ctx->hit_cap, 32);
             ctx->hit_leaf.ensure<uint32_t>(ctx->hit_cap);
@@ -1721,6 +1752,10 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
                         ctx->counts.ensure<uint32_t>(size_t(nn) + 1), ctx->hit_leaf.as<uint32_t>(),
                         ctx->hit_tin.as<double>(), ctx->hit_tout.as<double>(), traversal_counters(ctx),
                         uint32_t(ctx->hit_cap)};
+        if (nn) {
+            b.pre = &pre;
+            b.pre_key = &pre_key;
+        }
         r = run_train_step(S, dev_view(m->tree), mr, b, opt, s, ctx->misc.as<int>());
         if (nn) cudaEventElapsedTime(&trav_ms, ctx->ev[EV_START], ctx->ev[EV_EMIT]);
         if (r.error || !r.flags) break;

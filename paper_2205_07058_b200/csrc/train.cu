@@ -1100,6 +1100,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     // ---- the step, enqueued without a host round trip
     auto enqueue = [&]() {
         long long launches = 0;
+        if (b.pre) (*b.pre)(capturing);
         ev(0);
         SVLF_CUDA(cudaMemsetAsync(M.grads, 0, P * 4, s));
         SVLF_CUDA(cudaMemsetAsync(counters, 0, 32, s));
@@ -1221,7 +1222,12 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
         k.add(M.adam_v);
         k.add(M.n_ft);
         k.add(M.n_fc);
-        k.add(b);
+        {
+            TrainBatchDev kb = b;  // the pre-work is keyed by its own key, not by the functor's address
+            kb.pre = nullptr;
+            kb.pre_key = nullptr;
+            k.add(kb);
+        }
         k.add(o.surface);
         k.add(o.color_frozen);
         k.add(o.adam);
@@ -1237,6 +1243,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
                                 &S.wimg,      &S.dw_part, &S.scan_tmp};
         for (const DevBuf* d : bufs) k.add(d->p);
         k.add(S.h_mail);
+        if (b.pre_key) k.v.insert(k.v.end(), b.pre_key->begin(), b.pre_key->end());
         if (!S.graph || k.v != S.graph_key) {
             if (S.graph) SVLF_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(S.graph)));
             S.graph = nullptr;

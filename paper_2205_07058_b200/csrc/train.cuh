@@ -1,6 +1,7 @@
 // Train-step pipeline interface (train.cu).
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "device.cuh"
@@ -25,6 +26,11 @@ struct TrainBatchDev {
     const double* hit_tout;
     const uint32_t* trav_counters;
     uint32_t hit_cap;
+    // Work enqueued ahead of the step on the same stream and captured with it into
+    // the step's graph (the traversal); its key lists what it bakes in. The
+    // argument is true while a graph is being captured.
+    const std::function<void(bool)>* pre = nullptr;
+    const std::vector<uint64_t>* pre_key = nullptr;
 };
 
 // In-place all-reduce used by the data-parallel step (enqueued on stream s).
