@@ -1244,9 +1244,16 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
         for (const DevBuf* d : bufs) k.add(d->p);
         k.add(S.h_mail);
         if (b.pre_key) k.v.insert(k.v.end(), b.pre_key->begin(), b.pre_key->end());
-        if (!S.graph || k.v != S.graph_key) {
+        // Replay when the key matches the captured graph; capture when the same key
+        // came twice in a row (a steady workload); otherwise run eagerly (a batch
+        // whose size changes every step, e.g. stage 1's foreground rays, would
+        // pay a capture per step).
+        const bool replay = S.graph && k.v == S.graph_key;
+        const bool capture = !replay && k.v == S.last_key;
+        if (capture) {
             if (S.graph) SVLF_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(S.graph)));
             S.graph = nullptr;
+            S.graph_key.clear();
             cudaGraph_t g = nullptr;
             SVLF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             capturing = true;
@@ -1264,13 +1271,18 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
             SVLF_CUDA(cudaGraphInstantiate(&ge, g, 0));
             SVLF_CUDA(cudaGraphDestroy(g));
             S.graph = ge;
-            S.graph_key = std::move(k.v);
+            S.graph_key = k.v;
             S.graph_launches = launches;
             ++S.graph_captures;
         }
-        SVLF_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(S.graph), s));
-        ++S.graph_replays;
-        note_launch(S.graph_launches);
+        S.last_key = std::move(k.v);
+        if (replay || capture) {
+            SVLF_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(S.graph), s));
+            ++S.graph_replays;
+            note_launch(S.graph_launches);
+        } else {
+            note_launch(enqueue());
+        }
     } else {
         note_launch(enqueue());
     }

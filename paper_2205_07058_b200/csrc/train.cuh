@@ -103,7 +103,7 @@ struct TrainScratch {
     size_t h_stage_bytes = 0;
     DevBuf plan;                                // the Adam plan on the device
     void* graph = nullptr;                      // cudaGraphExec_t of the captured step (replayed while the key holds)
-    std::vector<uint64_t> graph_key;
+    std::vector<uint64_t> graph_key, last_key;
     long long graph_captures = 0, graph_replays = 0, graph_launches = 0;
     cudaEvent_t ev[8] = {};
     ~TrainScratch();
