@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "common.hpp"
+#include "composite.cuh"
 #include "geom.cuh"
 
 namespace svlfb {

@@ -10,6 +10,7 @@
 // interp_into_column src/voxel_batch.hpp:22-37; batch_forward_thickness /
 // _color src/voxel_batch.hpp:69-142; dense_forward src/mlp.cpp:98-116;
 // render_tile composite src/render.cpp:160-193.
+#include "composite.cuh"
 #include "device.cuh"
 #include "mlp_simt.cuh"
 
@@ -162,83 +163,52 @@ __global__ void __launch_bounds__(128) k_composite(const uint32_t* __restrict__ 
     if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(fg_count, (unsigned long long)__popc(ballot));
 }
 
-// Composite for the 16-bit tensor-core modes: a warp owns 32 consecutive rays
-// and walks each foreground ray's (sorted) segment 32 hits at a time, one hit
-// per lane with coalesced loads; transmittance is a warp prefix product and
-// the colour / alpha / depth sums are warp reductions, in fp32 (the decoder
-// outputs it composites are 16-bit-operand results; the fp32 mode keeps the
-// reference's sequential fp64 composite above).
-__global__ void __launch_bounds__(128) k_composite_warp(const uint32_t* __restrict__ ray_off,
-                                                        const uint32_t* __restrict__ ray_cnt,
-                                                        const double* __restrict__ tin,
-                                                        const double* __restrict__ tout, HitOut h, uint32_t n,
-                                                        float bg0, float bg1, float bg2, float* rgb, float* alpha,
-                                                        float* depth, unsigned long long* fg_count) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t r0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u;
-    if (r0 >= n) return;
-    const uint32_t my = r0 + lane;
-    const uint32_t cnt_l = my < n ? ray_cnt[my] : 0u, off_l = my < n ? ray_off[my] : 0u;
-    float out_c0 = 0.f, out_c1 = 0.f, out_c2 = 0.f, out_a = 0.f, out_d = 0.f;
-    unsigned fg = __ballot_sync(0xffffffffu, cnt_l > 0);
-    if (lane == 0 && fg) atomicAdd(fg_count, (unsigned long long)__popc(fg));
-    while (fg) {
-        const int src = __ffs(fg) - 1;
-        fg &= fg - 1;
+// Composite for the 16-bit tensor-core modes (fp32; the decoder outputs it
+// composites are 16-bit-operand results; the fp32 mode keeps the reference's
+// sequential fp64 composite above). A warp owns 32 consecutive rays and walks
+// each foreground ray's (sorted) segment with warp_composite_ray (coalesced
+// hit loads); the five sums of each ray land in a per-warp shared table (one
+// store by the five lanes holding them) and every lane writes its own ray's
+// pixel at the end. One foreground-count atomic per block.
+constexpr int kCompBlock = 256;
+__global__ void __launch_bounds__(kCompBlock) k_composite_warp(HitOut h, uint32_t n, PixelOut P,
+                                                               unsigned long long* fg_count) {
+    __shared__ float sums[kCompBlock / 32][32][5];
+    __shared__ uint32_t wfg[kCompBlock / 32];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t my = blockIdx.x * kCompBlock + threadIdx.x;
+    const uint32_t cnt_l = my < n ? P.ray_cnt[my] : 0u, off_l = my < n ? P.ray_off[my] : 0u;
+    const unsigned fg = __ballot_sync(0xffffffffu, cnt_l > 0);
+    if (lane == 0) wfg[warp] = __popc(fg);
+    const uint32_t vi = (lane >> 2) & 7u;  // which of the ray's five sums this lane ends up holding
+    unsigned todo = fg;
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
         const uint32_t b = __shfl_sync(0xffffffffu, off_l, src), cnt = __shfl_sync(0xffffffffu, cnt_l, src);
-        float Tr = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, a = 0.f, dacc = 0.f;
-        for (uint32_t k0 = 0; k0 < cnt; k0 += 32) {
-            const uint32_t k = k0 + lane;
-            float e = 1.f, r = 0.f, g = 0.f, bl = 0.f, ts = 0.f;
-            if (k < cnt) {
-                const uint32_t j = b + k;
-                e = __expf(-h.tau[j]);
-                r = h.rgb[3 * size_t(j)];
-                g = h.rgb[3 * size_t(j) + 1];
-                bl = h.rgb[3 * size_t(j) + 2];
-                ts = h.eta[j];  // the tensor-core decoder stores t_s = eta t_in + (1 - eta) t_out (fp32)
-            }
-            // exclusive prefix product of e over the lanes
-            float incl = e;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const float v = __shfl_up_sync(0xffffffffu, incl, d);
-                if (int(lane) >= d) incl *= v;
-            }
-            float excl = __shfl_up_sync(0xffffffffu, incl, 1);
-            if (lane == 0) excl = 1.f;
-            const float w = Tr * excl * (1.f - e);
-            float s0 = w * r, s1 = w * g, s2 = w * bl, sa = w, sd = w * ts;
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) {
-                s0 += __shfl_xor_sync(0xffffffffu, s0, d);
-                s1 += __shfl_xor_sync(0xffffffffu, s1, d);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, d);
-                sa += __shfl_xor_sync(0xffffffffu, sa, d);
-                sd += __shfl_xor_sync(0xffffffffu, sd, d);
-            }
-            c0 += s0;
-            c1 += s1;
-            c2 += s2;
-            a += sa;
-            dacc += sd;
-            Tr *= __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (int(lane) == src) {
-            out_c0 = c0;
-            out_c1 = c1;
-            out_c2 = c2;
-            out_a = a;
-            out_d = dacc;
-        }
+        const float v = warp_composite_ray(cnt, [&](uint32_t k, float& e, float& r, float& g, float& bl, float& ts) {
+            const uint32_t j = b + k;
+            e = __expf(-h.tau[j]);
+            r = h.rgb[3 * size_t(j)];
+            g = h.rgb[3 * size_t(j) + 1];
+            bl = h.rgb[3 * size_t(j) + 2];
+            ts = h.eta[j];  // the tensor-core decoder stores t_s = eta t_in + (1 - eta) t_out (fp32)
+        });
+        if ((lane & 3u) == 0 && vi < 5) sums[warp][src][vi] = v;
     }
+    __syncwarp();
     if (my < n) {
-        const float oma = 1.f - out_a;
-        rgb[3 * size_t(my)] = out_c0 + oma * bg0;
-        rgb[3 * size_t(my) + 1] = out_c1 + oma * bg1;
-        rgb[3 * size_t(my) + 2] = out_c2 + oma * bg2;
-        alpha[my] = out_a;
-        depth[my] = out_a > 1e-4f ? out_d / out_a : 0.f;
+        RayComposite c{0.f, 0.f, 0.f, 0.f, 0.f};
+        if (cnt_l > 0) c = RayComposite{sums[warp][lane][0], sums[warp][lane][1], sums[warp][lane][2],
+                                        sums[warp][lane][3], sums[warp][lane][4]};
+        write_pixel(P, my, c);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < kCompBlock / 32; ++w) t += wfg[w];
+        if (t) atomicAdd(fg_count, (unsigned long long)t);
     }
 }
 
@@ -282,8 +252,8 @@ void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const do
         k_composite<<<(n_rays + 127) / 128, 128, 0, s>>>(ray_off, ray_cnt, hit_tin, hit_tout, hits, n_rays, b0, b1,
                                                           b2, rgb, alpha, depth, fg_count);
     else
-        k_composite_warp<<<(n_rays + 127) / 128, 128, 0, s>>>(ray_off, ray_cnt, hit_tin, hit_tout, hits, n_rays, b0,
-                                                               b1, b2, rgb, alpha, depth, fg_count);
+        k_composite_warp<<<(n_rays + kCompBlock - 1) / kCompBlock, kCompBlock, 0, s>>>(
+            hits, n_rays, PixelOut{ray_off, ray_cnt, b0, b1, b2, rgb, alpha, depth}, fg_count);
     note_launch();
 }
 
