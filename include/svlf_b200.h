@@ -342,6 +342,24 @@ svlf_status svlf_train_step_device(svlf_ctx* ctx, svlf_model* model, const doubl
                                    const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
                                    int color_frozen, float lr, const svlf_loss_weights* lw,
                                    svlf_loss_stats* stats, double* loss_sum);
+/* Pipelined steps over HOST batches (the reference's per-frame loop,
+ * src/train.cpp:452-479, with the next frame's upload overlapping the current
+ * step). svlf_train_batch_stage queues a batch into one of the context's two
+ * device input slots and returns at once: page-locked inputs are copied by
+ * DMA on the context's copy stream, pageable ones through page-locked staging
+ * filled by a background host thread; *slot receives the slot. The caller
+ * keeps the arrays unchanged until the slot has been stepped or discarded.
+ * INVALID_ARGUMENT when both slots already hold batches.
+ * svlf_train_step_staged runs svlf_train_step on a staged slot (waiting for
+ * its copy) and frees the slot; svlf_train_batch_discard frees it unstepped.
+ * Loop: stage(0); for k: stage(k + 1); step_staged(k). */
+svlf_status svlf_train_batch_stage(svlf_ctx* ctx, const double* rays, const float* c_gt,
+                                   const double* depth_gt, const uint8_t* alpha_gt, size_t n,
+                                   int* slot);
+svlf_status svlf_train_step_staged(svlf_ctx* ctx, svlf_model* model, int slot, svlf_loss_mode mode,
+                                   int color_frozen, float lr, const svlf_loss_weights* lw,
+                                   svlf_loss_stats* stats, double* loss_sum);
+svlf_status svlf_train_batch_discard(svlf_ctx* ctx, int slot);
 /* Loss and summed gradients only (no Adam), the gradient oracle entry for
  * surface_loss / volumetric_loss summed over rays (train.hpp:60-71). */
 svlf_status svlf_loss_grads(svlf_ctx* ctx, svlf_model* model, const double* rays,

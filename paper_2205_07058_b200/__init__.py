@@ -245,6 +245,10 @@ def load_library():
                              C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
         "svlf_train_step_device": ([vp, vp, vp, vp, vp, vp, sz, C.c_int, C.c_int, C.c_float,
                                     C.POINTER(_LossWeights), C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
+        "svlf_train_batch_stage": ([vp, vp, vp, vp, vp, sz, C.POINTER(C.c_int)], st),
+        "svlf_train_step_staged": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_float, C.POINTER(_LossWeights),
+                                    C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
+        "svlf_train_batch_discard": ([vp, C.c_int], st),
         "svlf_loss_grads": ([vp, vp, vp, vp, vp, vp, sz, C.c_int, C.c_int, C.POINTER(_LossWeights),
                              C.POINTER(_LossStats), C.POINTER(C.c_double)], st),
     }
@@ -914,7 +918,11 @@ def _batch(rays, c_gt, depth_gt, alpha_gt):
     n = r.shape[0]
     c = _f32(c_gt).reshape(n * 3)
     d = _f64(depth_gt).reshape(n)
-    a = np.ascontiguousarray(np.asarray(alpha_gt).reshape(n) != 0, dtype=np.uint8)
+    a = np.asarray(alpha_gt).reshape(n)
+    if a.dtype == np.bool_:
+        a = a.view(np.uint8)
+    if a.dtype != np.uint8 or not a.flags.c_contiguous:  # any nonzero = foreground (the library reads != 0)
+        a = np.ascontiguousarray(a != 0, dtype=np.uint8)
     return r, c, d, a, n
 
 
@@ -945,6 +953,55 @@ def train_step_device(model: Model, d_rays: int, d_cgt: int, d_depth: int, d_alp
                                        int(color_frozen), C.c_float(lr), C.byref(lw), C.byref(st), C.byref(loss)))
     _add_loss_stats(stats, st)
     return loss.value
+
+
+class TrainPipeline:
+    """Pipelined optimizer steps over host batches (svlf_train_batch_stage /
+    svlf_train_step_staged): stage() queues batch k + 1's upload (DMA from
+    page-locked arrays, or page-locked staging filled by a background thread)
+    while step() runs batch k. At most two batches are staged; each batch's
+    arrays are kept (and must stay unchanged) until it has been stepped.
+
+        pipe = TrainPipeline(model); pipe.stage(*batch[0])
+        for k in range(K):
+            if k + 1 < K: pipe.stage(*batch[k + 1])
+            loss = pipe.step(lr=...)
+    """
+
+    def __init__(self, model: Model):
+        self.model = model
+        self._queue = []  # (slot, arrays) in staging order
+
+    def stage(self, rays, c_gt, depth_gt, alpha_gt):
+        r, c, d, a, n = _batch(rays, c_gt, depth_gt, alpha_gt)
+        slot = C.c_int()
+        _check(_LIB.svlf_train_batch_stage(self.model.ctx.handle, _dp(r), _dp(c), _dp(d), _dp(a), n,
+                                           C.byref(slot)))
+        self._queue.append((slot.value, (r, c, d, a)))
+
+    def step(self, mode: str = "volumetric", color_frozen: bool = False, lr: float = 1e-3,
+             weights: LossWeights | None = None, stats: LossStats | None = None) -> float:
+        """train_step on the oldest staged batch; returns its loss sum."""
+        if not self._queue:
+            raise ValueError("no batch staged")
+        slot, _arrays = self._queue.pop(0)
+        lw = (weights or LossWeights())._c()
+        st = _LossStats()
+        loss = C.c_double()
+        _check(_LIB.svlf_train_step_staged(self.model.ctx.handle, self.model.handle, slot,
+                                           0 if mode == "surface" else 1, int(color_frozen), C.c_float(lr),
+                                           C.byref(lw), C.byref(st), C.byref(loss)))
+        _add_loss_stats(stats, st)
+        return loss.value
+
+    def drain(self):
+        """Drops the staged batches that were not stepped."""
+        while self._queue:
+            slot, _arrays = self._queue.pop(0)
+            _check(_LIB.svlf_train_batch_discard(self.model.ctx.handle, slot))
+
+    def __len__(self):
+        return len(self._queue)
 
 
 def loss_grads(model: Model, rays, c_gt, depth_gt, alpha_gt, mode: str = "volumetric",

@@ -669,8 +669,41 @@ DeviceModel::DeviceModel(const SvlfModel& model) : octree_(model.octree) {
 
 DeviceModel::DeviceModel(const SvlfModel& model, const ModelAdam& adam) : DeviceModel(model) { upload(adam); }
 
+// a staged batch: its packed host arrays stay alive until the slot is stepped
+struct DeviceModel::StagedBatch {
+    PackedBatch batch;
+    size_t n;
+    int slot = 0;
+    explicit StagedBatch(std::span<const RaySupervision> b) : batch(b), n(b.size()) {}
+};
+
 DeviceModel::~DeviceModel() {
+    for (auto& sb : staged_) svlf_train_batch_discard(session_context(), sb->slot);
     if (m_) svlf_model_destroy(m_);
+}
+
+void DeviceModel::stage_batch(std::span<const RaySupervision> batch) {
+    std::lock_guard<std::recursive_mutex> lk(detail::session_mutex());
+    auto sb = std::make_unique<StagedBatch>(batch);
+    detail::check(svlf_train_batch_stage(session_context(), sb->batch.rays.data(), sb->batch.c_gt.data(),
+                                         sb->batch.depth.data(), sb->batch.alpha.data(), sb->n, &sb->slot));
+    staged_.push_back(std::move(sb));
+}
+
+double DeviceModel::train_staged(LossMode mode, bool color_frozen, float lr, const LossWeights& lw,
+                                 LossStats* stats) {
+    std::lock_guard<std::recursive_mutex> lk(detail::session_mutex());
+    if (staged_.empty()) throw std::logic_error("no batch staged");
+    const std::unique_ptr<StagedBatch> sb = std::move(staged_.front());
+    staged_.pop_front();
+    const svlf_loss_weights w = to_c(lw);
+    svlf_loss_stats st{};
+    double loss = 0;
+    detail::check(svlf_train_step_staged(session_context(), m_, sb->slot,
+                                         mode == LossMode::Surface ? SVLF_LOSS_SURFACE : SVLF_LOSS_VOLUMETRIC,
+                                         color_frozen ? 1 : 0, lr, &w, &st, &loss));
+    add(stats, st);
+    return loss;
 }
 
 void DeviceModel::upload(const SvlfModel& model) {

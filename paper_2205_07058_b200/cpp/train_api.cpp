@@ -151,10 +151,16 @@ TrainResult train(const TrainConfig& config, const SceneDataset& dataset) {
 
             double loss_sum = 0.0;
             long long ray_count = 0;
-            for (size_t fi : order) {
-                view_batch(dataset.frames[fi], mode == LossMode::Surface, sups);
-                loss_sum += dev.train_step(sups, mode, frozen, lr, lw, &stats_total);
+            // frame k + 1's batch uploads (copy stream) while frame k's step runs
+            auto stage_frame = [&](size_t k) {
+                view_batch(dataset.frames[order[k]], mode == LossMode::Surface, sups);
+                dev.stage_batch(sups);
                 ray_count += static_cast<long long>(sups.size());
+            };
+            if (!order.empty()) stage_frame(0);
+            for (size_t k = 0; k < order.size(); ++k) {
+                if (k + 1 < order.size()) stage_frame(k + 1);
+                loss_sum += dev.train_staged(mode, frozen, lr, lw, &stats_total);
             }
             const double mean_loss = ray_count > 0 ? loss_sum / double(ray_count) : 0.0;
             if (!std::isfinite(mean_loss)) {

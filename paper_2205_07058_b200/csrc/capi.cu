@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -172,6 +173,21 @@ struct svlf_ctx {
     std::unique_ptr<HostPool> pool;
     svlf_timings last{};
     std::mutex mu;  // one pipeline at a time per context
+    // staged train batches (svlf_train_batch_stage / svlf_train_step_staged):
+    // two device input slots, filled on the copy stream while a step runs
+    struct TrainSlot {
+        DevBuf rays, c_gt, depth, alpha;
+        char* h_stage = nullptr;  // page-locked staging for pageable batches
+        size_t h_stage_bytes = 0;
+        cudaEvent_t copied = nullptr;
+        std::future<void> job;  // pageable batch: host copy into h_stage, then the DMA
+        size_t n = 0;
+        bool staged = false;
+    };
+    TrainSlot tslot[2];
+    int next_tslot = 0;
+    std::unique_ptr<HostPool> stage_pool;  // host copies of staged batches (own pool: runs beside `pool`)
+    std::mutex stage_mu;                   // one staging job on stage_pool at a time
 };
 
 // Host octree; its device mirror is uploaded lazily to the device of the
@@ -714,6 +730,7 @@ svlf_status svlf_ctx_create(int device, svlf_ctx** out) {
             }
             SVLF_CUDA(cudaMallocHost(&fs.h_ctr, 4 * (4 * svlf_ctx::kMaxBands + 8)));
         }
+        for (auto& ts : ctx->tslot) SVLF_CUDA(cudaEventCreateWithFlags(&ts.copied, cudaEventDisableTiming));
         ctx->misc.ensure<unsigned long long>(8);
         SVLF_CUDA(cudaMemset(ctx->misc.p, 0, 64));
         *out = ctx.release();
@@ -737,6 +754,12 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
                 if (fs.h_stage) cudaFreeHost(fs.h_stage);
                 if (fs.h_ctr) cudaFreeHost(fs.h_ctr);
             }
+            for (auto& ts : ctx->tslot) {
+                if (ts.job.valid()) ts.job.wait();
+                cudaEventDestroy(ts.copied);
+                if (ts.h_stage) cudaFreeHost(ts.h_stage);
+            }
+            cudaStreamSynchronize(ctx->copy_stream);
             if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
             cudaStreamDestroy(ctx->copy_stream);
             cudaStreamDestroy(ctx->own_stream);
@@ -1642,10 +1665,69 @@ svlf_status svlf_eta_gt(svlf_ctx* ctx, const double* t_in, const double* t_out, 
 extern "C" {
 
 // ---- train --------------------------------------------------------------------
+namespace {
+
+std::unique_ptr<HostPool>& host_pool(std::unique_ptr<HostPool>& p) {
+    if (!p) {
+        const char* e = std::getenv("SVLF_HOST_THREADS");
+        const int hw = int(std::thread::hardware_concurrency());
+        p = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
+    }
+    return p;
+}
+
+// A host train batch (rays, c_gt, depth_gt, alpha_gt) and its device destinations.
+struct HostBatch {
+    struct Part {
+        const void* src;
+        void* dst;
+        size_t elem;
+    };
+    static constexpr size_t kPerRay = 48 + 12 + 8 + 1;
+    Part parts[4];
+
+    bool pinned() const {
+        for (const Part& p : parts)
+            if (!is_pinned(p.src)) return false;
+        return true;
+    }
+    void dma(cudaStream_t s, uint32_t nn) const {
+        for (const Part& p : parts) SVLF_CUDA(cudaMemcpyAsync(p.dst, p.src, p.elem * nn, cudaMemcpyHostToDevice, s));
+    }
+    // pageable: copied into page-locked `stage` by the pool in chunks, each
+    // chunk's DMA overlapping the next chunk's host copy
+    void staged_dma(std::unique_ptr<HostPool>& pool, char* stage, cudaStream_t s, uint32_t nn) const {
+        const uint32_t chunks = nn >= (1u << 16) ? 4u : 1u;
+        for (uint32_t c = 0; c < chunks; ++c) {
+            const size_t r0 = size_t(nn) * c / chunks, r1 = size_t(nn) * (c + 1) / chunks;
+            const int tasks = pool->size() * 2;
+            pool->parallel_for(tasks, [&](int i) {
+                const size_t a = r0 + (r1 - r0) * size_t(i) / size_t(tasks);
+                const size_t b = r0 + (r1 - r0) * size_t(i + 1) / size_t(tasks);
+                size_t base = 0;
+                for (const Part& p : parts) {
+                    std::memcpy(stage + base + a * p.elem, static_cast<const char*>(p.src) + a * p.elem,
+                                (b - a) * p.elem);
+                    base += p.elem * nn;
+                }
+            });
+            size_t base = 0;
+            for (const Part& p : parts) {
+                SVLF_CUDA(cudaMemcpyAsync(static_cast<char*>(p.dst) + r0 * p.elem, stage + base + r0 * p.elem,
+                                          (r1 - r0) * p.elem, cudaMemcpyHostToDevice, s));
+                base += p.elem * nn;
+            }
+        }
+    }
+};
+
+}  // namespace
+
 static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const float* c_gt,
                          const double* depth_gt, const uint8_t* alpha_gt, size_t n, svlf_loss_mode mode,
                          int color_frozen, const svlf_loss_weights* lw, bool adam, float lr,
-                         svlf_loss_stats* stats, double* loss_sum, bool device_inputs = false) {
+                         svlf_loss_stats* stats, double* loss_sum, bool device_inputs = false,
+                         cudaEvent_t inputs_ready = nullptr) {
     require(ctx && m && lw, "null argument");
     require(n == 0 || (rays && c_gt && depth_gt && alpha_gt), "null argument");
     require(n < (1ull << 31), "too many rays");
@@ -1660,60 +1742,30 @@ static void train_common(svlf_ctx* ctx, svlf_model* m, const double* rays, const
     float* d_cgt = S.c_gt.ensure<float>(size_t(nn) * 3 + 3);
     double* d_depth = S.depth.ensure<double>(size_t(nn) + 1);
     uint8_t* d_alpha = S.alpha.ensure<uint8_t>(size_t(nn) + 1);
-    if (nn && device_inputs) {  // rays copied (the traversal writes into ctx->rays), supervision read in place
+    if (inputs_ready) SVLF_CUDA(cudaStreamWaitEvent(s, inputs_ready, 0));
+    if (nn && inputs_ready) {  // a staged slot (alternating buffers): all copied, so the step's pointers repeat
+        SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyDeviceToDevice, s));
+        SVLF_CUDA(cudaMemcpyAsync(d_cgt, c_gt, size_t(nn) * 12, cudaMemcpyDeviceToDevice, s));
+        SVLF_CUDA(cudaMemcpyAsync(d_depth, depth_gt, size_t(nn) * 8, cudaMemcpyDeviceToDevice, s));
+        SVLF_CUDA(cudaMemcpyAsync(d_alpha, alpha_gt, size_t(nn), cudaMemcpyDeviceToDevice, s));
+    } else if (nn && device_inputs) {  // rays copied (the traversal writes into ctx->rays), supervision read in place
         SVLF_CUDA(cudaMemcpyAsync(d_rays, rays, size_t(nn) * 48, cudaMemcpyDeviceToDevice, s));
         d_cgt = const_cast<float*>(c_gt);
         d_depth = const_cast<double*>(depth_gt);
         d_alpha = const_cast<uint8_t*>(alpha_gt);
     } else if (nn) {
-        // Host batch: page-locked inputs go straight to the device; pageable ones
-        // are copied into page-locked staging by the host worker pool in chunks,
-        // each chunk's DMA overlapping the next chunk's host copy.
-        struct Part {
-            const void* src;
-            void* dst;
-            size_t elem;
-        };
-        const Part parts[4] = {{rays, d_rays, 48}, {c_gt, d_cgt, 12}, {depth_gt, d_depth, 8}, {alpha_gt, d_alpha, 1}};
-        const size_t per_ray = 48 + 12 + 8 + 1;
-        const bool pinned = is_pinned(rays) && is_pinned(c_gt) && is_pinned(depth_gt) && is_pinned(alpha_gt);
-        if (pinned) {
-            for (const Part& p : parts) SVLF_CUDA(cudaMemcpyAsync(p.dst, p.src, p.elem * nn, cudaMemcpyHostToDevice, s));
+        const HostBatch hb{{{rays, d_rays, 48}, {c_gt, d_cgt, 12}, {depth_gt, d_depth, 8}, {alpha_gt, d_alpha, 1}}};
+        if (hb.pinned()) {
+            hb.dma(s, nn);
         } else {
-            if (S.h_stage_bytes < per_ray * nn) {
+            if (S.h_stage_bytes < HostBatch::kPerRay * nn) {
                 if (S.h_stage) SVLF_CUDA(cudaFreeHost(S.h_stage));
                 S.h_stage = nullptr;
                 S.h_stage_bytes = 0;
-                SVLF_CUDA(cudaMallocHost(&S.h_stage, per_ray * nn));
-                S.h_stage_bytes = per_ray * nn;
+                SVLF_CUDA(cudaMallocHost(&S.h_stage, HostBatch::kPerRay * nn));
+                S.h_stage_bytes = HostBatch::kPerRay * nn;
             }
-            if (!ctx->pool) {
-                const char* e = std::getenv("SVLF_HOST_THREADS");
-                const int hw = int(std::thread::hardware_concurrency());
-                ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
-            }
-            const uint32_t chunks = nn >= (1u << 16) ? 4u : 1u;
-            char* stage = static_cast<char*>(S.h_stage);
-            for (uint32_t c = 0; c < chunks; ++c) {
-                const size_t r0 = size_t(nn) * c / chunks, r1 = size_t(nn) * (c + 1) / chunks;
-                const int tasks = ctx->pool->size() * 2;
-                ctx->pool->parallel_for(tasks, [&](int i) {
-                    const size_t a = r0 + (r1 - r0) * size_t(i) / size_t(tasks);
-                    const size_t b = r0 + (r1 - r0) * size_t(i + 1) / size_t(tasks);
-                    size_t base = 0;
-                    for (const Part& p : parts) {
-                        std::memcpy(stage + base + a * p.elem, static_cast<const char*>(p.src) + a * p.elem,
-                                    (b - a) * p.elem);
-                        base += p.elem * nn;
-                    }
-                });
-                size_t base = 0;
-                for (const Part& p : parts) {
-                    SVLF_CUDA(cudaMemcpyAsync(static_cast<char*>(p.dst) + r0 * p.elem, stage + base + r0 * p.elem,
-                                              (r1 - r0) * p.elem, cudaMemcpyHostToDevice, s));
-                    base += p.elem * nn;
-                }
-            }
+            hb.staged_dma(host_pool(ctx->pool), static_cast<char*>(S.h_stage), s, nn);
         }
     }
     // Traversal and step are enqueued with no host round trip; the step's one
@@ -1796,6 +1848,82 @@ svlf_status svlf_train_step_device(svlf_ctx* ctx, svlf_model* m, const double* r
     return guard([&] {
         train_common(ctx, m, rays, c_gt, depth_gt, alpha_gt, n, mode, color_frozen, lw, true, lr, stats, loss_sum,
                      true);
+    });
+}
+
+svlf_status svlf_train_batch_stage(svlf_ctx* ctx, const double* rays, const float* c_gt, const double* depth_gt,
+                                   const uint8_t* alpha_gt, size_t n, int* slot) {
+    return guard([&] {
+        require(ctx && slot, "null argument");
+        require(n == 0 || (rays && c_gt && depth_gt && alpha_gt), "null argument");
+        require(n < (1ull << 31), "too many rays");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const int k = ctx->next_tslot;
+        svlf_ctx::TrainSlot& T = ctx->tslot[k];
+        require(!T.staged, "both train staging slots hold batches that have not been stepped");
+        const uint32_t nn = uint32_t(n);
+        const HostBatch hb{{{rays, T.rays.ensure<double>(size_t(nn) * 6 + 6), 48},
+                            {c_gt, T.c_gt.ensure<float>(size_t(nn) * 3 + 3), 12},
+                            {depth_gt, T.depth.ensure<double>(size_t(nn) + 1), 8},
+                            {alpha_gt, T.alpha.ensure<uint8_t>(size_t(nn) + 1), 1}}};
+        cudaStream_t c = ctx->copy_stream;
+        if (nn == 0 || hb.pinned()) {
+            if (nn) hb.dma(c, nn);
+            SVLF_CUDA(cudaEventRecord(T.copied, c));
+        } else {
+            if (T.h_stage_bytes < HostBatch::kPerRay * nn) {
+                if (T.h_stage) SVLF_CUDA(cudaFreeHost(T.h_stage));
+                T.h_stage = nullptr;
+                T.h_stage_bytes = 0;
+                SVLF_CUDA(cudaMallocHost(&T.h_stage, HostBatch::kPerRay * nn));
+                T.h_stage_bytes = HostBatch::kPerRay * nn;
+            }
+            host_pool(ctx->stage_pool);
+            const int dev = ctx->device;
+            T.job = std::async(std::launch::async, [ctx, &T, hb, c, nn, dev] {
+                DeviceGuard g2(dev);
+                std::lock_guard<std::mutex> lk2(ctx->stage_mu);
+                hb.staged_dma(ctx->stage_pool, T.h_stage, c, nn);
+                SVLF_CUDA(cudaEventRecord(T.copied, c));
+            });
+        }
+        T.n = nn;
+        T.staged = true;
+        ctx->next_tslot ^= 1;
+        *slot = k;
+    });
+}
+
+static svlf_ctx::TrainSlot& staged_slot(svlf_ctx* ctx, int slot) {
+    require(ctx, "null argument");
+    require(slot == 0 || slot == 1, "bad staging slot");
+    svlf_ctx::TrainSlot& T = ctx->tslot[slot];
+    require(T.staged, "no batch staged in this slot");
+    if (T.job.valid()) T.job.get();  // rethrows a failed host copy
+    return T;
+}
+
+svlf_status svlf_train_step_staged(svlf_ctx* ctx, svlf_model* m, int slot, svlf_loss_mode mode, int color_frozen,
+                                   float lr, const svlf_loss_weights* lw, svlf_loss_stats* stats,
+                                   double* loss_sum) {
+    return guard([&] {
+        svlf_ctx::TrainSlot& T = staged_slot(ctx, slot);
+        struct Release {
+            svlf_ctx::TrainSlot& t;
+            ~Release() { t.staged = false; }
+        } release{T};
+        train_common(ctx, m, T.rays.as<double>(), T.c_gt.as<float>(), T.depth.as<double>(), T.alpha.as<uint8_t>(),
+                     T.n, mode, color_frozen, lw, true, lr, stats, loss_sum, true, T.copied);
+    });
+}
+
+svlf_status svlf_train_batch_discard(svlf_ctx* ctx, int slot) {
+    return guard([&] {
+        svlf_ctx::TrainSlot& T = staged_slot(ctx, slot);
+        DeviceGuard g(ctx->device);
+        SVLF_CUDA(cudaEventSynchronize(T.copied));
+        T.staged = false;
     });
 }
 

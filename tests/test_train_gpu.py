@@ -244,3 +244,49 @@ def test_tf32_train_mode_within_16bit_tolerance(batch, oracle, mode, frozen, lw)
         c.set_train_precision("fp16")
     del model, t
     c.close()
+
+
+def _pin(a):
+    p = P.pinned_empty(a.size, a.dtype)
+    p[:] = a.reshape(-1)
+    return p.reshape(a.shape)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipelined_steps_match_sequential_steps(batch, ctx, pinned):
+    """TrainPipeline (svlf_train_batch_stage / svlf_train_step_staged: batch k + 1 uploaded while
+    step k runs) gives the same losses and parameters as train_step batch by batch, from pageable
+    (background staging thread) and page-locked (direct DMA) arrays."""
+    tree, otree, rays, cgt, depth, alpha = batch
+    n = rays.shape[0]
+    rng = np.random.default_rng(1)
+    batches = []
+    for k in range(4):  # different sizes and orders, so a stale slot would show
+        idx = np.tile(rng.permutation(n)[: n - 97 * k], 30)  # ~65K rays: chunked, pool-parallel staging
+        b = [np.ascontiguousarray(x[idx]) for x in (rays, cgt.astype(np.float32), depth, alpha)]
+        batches.append([_pin(x) for x in b] if pinned else b)
+    m1 = P.Model(tree, seed=0, ctx=ctx)
+    seq = [P.train_step(m1, *b, mode="volumetric", lr=1e-3) for b in batches]
+    m2 = P.Model(tree, seed=0, ctx=ctx)
+    pipe = P.TrainPipeline(m2)
+    pipe.stage(*batches[0])
+    got = []
+    for k in range(len(batches)):
+        if k + 1 < len(batches):
+            pipe.stage(*batches[k + 1])
+        got.append(pipe.step(mode="volumetric", lr=1e-3))
+    assert got[0] == seq[0]  # same model, same batch: the forward and loss are deterministic
+    np.testing.assert_allclose(got, seq, rtol=1e-6)  # later steps: feature-gradient atomics reorder sums
+    for a, b in zip(m1.get_params(), m2.get_params()):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-6)
+    # two slots: a third staged batch is refused until one is stepped or discarded
+    pipe.stage(*batches[0])
+    pipe.stage(*batches[1])
+    with pytest.raises(ValueError, match="staging slots"):
+        pipe.stage(*batches[2])
+    pipe.drain()
+    assert len(pipe) == 0
+    with pytest.raises(ValueError, match="no batch staged"):
+        pipe.step()
+    pipe.stage(*batches[2])
+    assert np.isfinite(pipe.step(mode="volumetric", lr=1e-3))
