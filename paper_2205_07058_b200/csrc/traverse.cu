@@ -89,6 +89,40 @@ __device__ __forceinline__ bool child_hit(const NodeSplit& s, uint32_t oct, doub
     return !(t1 < t0);
 }
 
+// child_hit for all eight octants at once (bit oct of the result; kLeaf: also
+// t1 - t0 > kMinHitSpan). Each octant's t0 / t1 is the same left-to-right
+// max / min chain over the axes as child_hit's, so the results are
+// bit-identical; the x and xy prefixes of the chains are shared between
+// octants (14 compare-selects per chain instead of 24).
+template <bool kLeaf>
+__device__ __forceinline__ uint32_t child_hits(const NodeSplit& s) {
+    double t0x[2], t1x[2], t0xy[4], t1xy[4];
+#pragma unroll
+    for (int hx = 0; hx < 2; ++hx) {
+        const double ta = hx ? s.hi_a[0] : s.lo_a[0], tb = hx ? s.hi_b[0] : s.lo_b[0];
+        t0x[hx] = ta > 0.0 ? ta : 0.0;
+        t1x[hx] = tb < CUDART_INF ? tb : CUDART_INF;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int hx = i & 1, hy = i >> 1;
+        const double ta = hy ? s.hi_a[1] : s.lo_a[1], tb = hy ? s.hi_b[1] : s.lo_b[1];
+        t0xy[i] = ta > t0x[hx] ? ta : t0x[hx];
+        t1xy[i] = tb < t1x[hx] ? tb : t1x[hx];
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int oct = 0; oct < 8; ++oct) {
+        const int i = oct & 3, hz = oct >> 2;
+        const double ta = hz ? s.hi_a[2] : s.lo_a[2], tb = hz ? s.hi_b[2] : s.lo_b[2];
+        const double t0 = ta > t0xy[i] ? ta : t0xy[i];
+        const double t1 = tb < t1xy[i] ? tb : t1xy[i];
+        const bool hit = kLeaf ? (!(t1 < t0) && dsub(t1, t0) > kMinHitSpan) : !(t1 < t0);
+        m |= hit ? 1u << oct : 0u;
+    }
+    return m;
+}
+
 __device__ __forceinline__ uint32_t sign_mask(const double* d) {
     return (d[0] < 0.0 ? 1u : 0u) | (d[1] < 0.0 ? 2u : 0u) | (d[2] < 0.0 ? 4u : 0u);
 }
@@ -421,12 +455,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 split_node(T, o, d, inv, level, x, y, z, sp);
                 s = sign_mask(d);
                 if constexpr (kCount) tests += __popc(node.y);
-#pragma unroll
-                for (uint32_t oct = 0; oct < 8; ++oct) {
-                    if (!((node.y >> oct) & 1u)) continue;
-                    double t0, t1;
-                    if (child_hit(sp, oct, t0, t1)) hitmask |= 1u << oct;
-                }
+                hitmask = child_hits<false>(sp) & node.y & 0xffu;
                 cnt = __popc(hitmask);
             }
             uint32_t off, tot;
@@ -486,12 +515,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 split_node(T, o, d, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
                            uint32_t(xyz >> 42), sp);
                 if constexpr (kCount) tests += __popc(node.y);
-#pragma unroll
-                for (uint32_t oct = 0; oct < 8; ++oct) {
-                    if (!((node.y >> oct) & 1u)) continue;
-                    double t0, t1;
-                    if (child_hit(sp, oct, t0, t1) && dsub(t1, t0) > kMinHitSpan) ++cnt;
-                }
+                cnt = __popc(child_hits<true>(sp) & node.y & 0xffu);
                 if (cnt) atomicAdd(&S.rcount[ri], cnt);
             }
             uint32_t off, tot;
@@ -533,11 +557,12 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             const uint32_t s = sign_mask(d);
             uint32_t w = gbase + S.pos[e];
             const uint32_t gr = S.gray[ri];
+            const uint32_t keep = child_hits<true>(sp) & node.y & 0xffu;
             for (uint32_t it = 0; it < 8; ++it) {
                 const uint32_t oct = it ^ s;
-                if (!((node.y >> oct) & 1u)) continue;
+                if (!((keep >> oct) & 1u)) continue;
                 double t0, t1;
-                if (!child_hit(sp, oct, t0, t1) || !(dsub(t1, t0) > kMinHitSpan)) continue;
+                child_hit(sp, oct, t0, t1);
                 A.hit_leaf[w] = node.x + __popc(node.y & ((1u << oct) - 1u)) - T.level_off[T.L];
                 A.hit_tin[w] = t0;
                 A.hit_tout[w] = t1;
@@ -603,8 +628,11 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
 // Persistent: each tile group (a block, or each warp of a block when kT ==
 // 32) takes tiles from a device-side cursor until they run out. kList passes
 // read their tile count from the device (no host round trip).
+#ifndef SVLF_BFS_MINB
+#define SVLF_BFS_MINB 8  // resident 128-thread blocks per SM (256-thread second pass: 4): at most 64 registers
+#endif
 template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList, bool kCount>
-__global__ void __launch_bounds__(kBlock) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
+__global__ void __launch_bounds__(kBlock, kBlock == 128 ? SVLF_BFS_MINB : (kBlock == 256 ? 4 : 1)) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
                                                          uint32_t n, uint32_t n_tiles, BfsArgs A) {
     extern __shared__ __align__(16) uint8_t bfs_smem[];
     static_assert(kBlock % kT == 0, "tile groups per block");
