@@ -123,6 +123,16 @@ __device__ __forceinline__ uint32_t child_hits(const NodeSplit& s) {
     return m;
 }
 
+// Octant mask reindexed in front-to-back order: bit it of the result is bit
+// (it ^ s) of m, so walking its set bits from the lowest visits the children
+// in the order `for it: oct = it ^ s` does, one iteration per set bit.
+__device__ __forceinline__ uint32_t front_to_back(uint32_t m, uint32_t s) {
+    if (s & 1u) m = ((m & 0x55u) << 1) | ((m >> 1) & 0x55u);
+    if (s & 2u) m = ((m & 0x33u) << 2) | ((m >> 2) & 0x33u);
+    if (s & 4u) m = ((m & 0x0fu) << 4) | ((m >> 4) & 0x0fu);
+    return m;
+}
+
 __device__ __forceinline__ uint32_t sign_mask(const double* d) {
     return (d[0] < 0.0 ? 1u : 0u) | (d[1] < 0.0 ? 2u : 0u) | (d[2] < 0.0 ? 4u : 0u);
 }
@@ -466,9 +476,8 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 break;
             }
             uint32_t w = n_out + off;  // children in front-to-back octant order
-            for (uint32_t it = 0; it < 8 && hitmask; ++it) {
-                const uint32_t oct = it ^ s;
-                if (!((hitmask >> oct) & 1u)) continue;
+            for (uint32_t todo = front_to_back(hitmask, s); todo; todo &= todo - 1) {
+                const uint32_t oct = uint32_t(__ffs(todo) - 1) ^ s;
                 S.qnode[cur ^ 1][w] = node.x + __popc(node.y & ((1u << oct) - 1u));
                 S.qxyz[cur ^ 1][w] =
                     pack_xyz(2u * x + (oct & 1u), 2u * y + ((oct >> 1) & 1u), 2u * z + ((oct >> 2) & 1u));
@@ -558,9 +567,8 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             uint32_t w = gbase + S.pos[e];
             const uint32_t gr = S.gray[ri];
             const uint32_t keep = child_hits<true>(sp) & node.y & 0xffu;
-            for (uint32_t it = 0; it < 8; ++it) {
-                const uint32_t oct = it ^ s;
-                if (!((keep >> oct) & 1u)) continue;
+            for (uint32_t todo = front_to_back(keep, s); todo; todo &= todo - 1) {
+                const uint32_t oct = uint32_t(__ffs(todo) - 1) ^ s;
                 double t0, t1;
                 child_hit(sp, oct, t0, t1);
                 A.hit_leaf[w] = node.x + __popc(node.y & ((1u << oct) - 1u)) - T.level_off[T.L];
