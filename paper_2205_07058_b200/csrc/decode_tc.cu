@@ -263,6 +263,58 @@ __global__ void k_feat_cvt(const float* __restrict__ src, typename Fmt<kBF16>::H
 // hit: x1, x2, parameterize_ray (r6), trilinear weights w1, w2 (16-bit pairs)
 // and local coordinates u1, u2 (fp32, for x_s after the f_T pass). Raises
 // "tangent ray" / "point not in voxel" like the reference.
+// Hit geometry for the 16-bit decoders. The tests that raise the reference's
+// errors ("tangent ray": the discriminant; "point not in voxel": the slab
+// bounds) and the chord end points run in fp64 in the reference's operand
+// order; the results are rounded to 16 bits for the MMA, so the unit
+// direction normalisations (two fp64 square roots, six divisions) and the
+// trilinear weight products run in fp32 (their rounding is far below the
+// 16-bit quantisation).
+__device__ __forceinline__ bool parameterize_tc(const Ray& r, const double* lo, const double* hi, float* r6) {
+    double c[3], oc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        c[a] = dmul(dadd(lo[a], hi[a]), 0.5);
+        oc[a] = dsub(r.o[a], c[a]);
+    }
+    constexpr double kHalfSqrt3 = 0.5 * 1.7320508075688772;
+    const double radius = dmul(kHalfSqrt3, dsub(hi[0], lo[0]));
+    const double b = dot3(oc, r.d);
+    const double cc = dsub(dot3(oc, oc), dmul(radius, radius));
+    const double disc = dsub(dmul(b, b), cc);
+    if (disc < 1e-14) return false;
+    const double s = __dsqrt_rn(disc);
+    const double t1 = dsub(-b, s), t2 = dadd(-b, s);
+    float p1[3], p2[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        p1[a] = float(dsub(dadd(r.o[a], dmul(r.d[a], t1)), c[a]));
+        p2[a] = float(dsub(dadd(r.o[a], dmul(r.d[a], t2)), c[a]));
+    }
+    const float i1 = rsqrtf(p1[0] * p1[0] + p1[1] * p1[1] + p1[2] * p1[2]);
+    const float i2 = rsqrtf(p2[0] * p2[0] + p2[1] * p2[1] + p2[2] * p2[2]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r6[a] = p1[a] * i1;
+        r6[3 + a] = p2[a] * i2;
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool trilinear_tc(const double* p, const double* lo, const DevOctree& T, const double* hi,
+                                             float* w, double* u) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!(p[a] >= dsub(lo[a], 1e-7) && p[a] <= dadd(hi[a], 1e-7))) return false;
+        u[a] = fmin(fmax(div_cell(T, dsub(p[a], lo[a])), 0.0), 1.0);
+    }
+    const float fx[2] = {1.f - float(u[0]), float(u[0])}, fy[2] = {1.f - float(u[1]), float(u[1])},
+                fz[2] = {1.f - float(u[2]), float(u[2])};
+#pragma unroll
+    for (int b = 0; b < 8; ++b) w[b] = fx[b & 1] * fy[(b >> 1) & 1] * fz[b >> 2];
+    return true;
+}
+
 template <bool kBF16>
 __device__ __forceinline__ void hit_geom_regs(const DevOctree& T, const double* __restrict__ rays, uint32_t ri,
                                               uint32_t leaf, double tin, double tout, uint32_t* r6p, uint32_t* wp,
@@ -280,8 +332,8 @@ __device__ __forceinline__ void hit_geom_regs(const DevOctree& T, const double* 
     ray_at(ray, tout, x2);
     float r6[6] = {0, 0, 0, 0, 0, 0}, w1[8], w2[8];
     double u1[3] = {0, 0, 0}, u2[3] = {0, 0, 0};  // local coordinates (features.cpp:22-31)
-    if (!parameterize(ray, lo, hi, r6)) raise_error(err, kErrTangentRay);
-    if (!trilinear_at(x1, lo, hi, T, w1, u1) || !trilinear_at(x2, lo, hi, T, w2, u2)) {
+    if (!parameterize_tc(ray, lo, hi, r6)) raise_error(err, kErrTangentRay);
+    if (!trilinear_tc(x1, lo, T, hi, w1, u1) || !trilinear_tc(x2, lo, T, hi, w2, u2)) {
         raise_error(err, kErrPointNotInVoxel);
 #pragma unroll
         for (int b = 0; b < 8; ++b) w1[b] = w2[b] = 0.f;
