@@ -44,9 +44,10 @@ struct NodeSplit {
     double hi_a[3], hi_b[3];  // high half: [hi_a, hi_b]
 };
 
-__device__ __forceinline__ void split_node(const DevOctree& T, const double* o, const double* d,
-                                           const double* inv, int level, uint32_t x, uint32_t y, uint32_t z,
-                                           NodeSplit& s) {
+// zmask bit a: the ray's direction component a is zero
+__device__ __forceinline__ void split_node_z(const DevOctree& T, const double* o, uint32_t zmask,
+                                             const double* inv, int level, uint32_t x, uint32_t y, uint32_t z,
+                                             NodeSplit& s) {
     const uint32_t c[3] = {x, y, z};
     const double cl = T.cell[level], ch = T.cell[level + 1];
 #pragma unroll
@@ -54,7 +55,7 @@ __device__ __forceinline__ void split_node(const DevOctree& T, const double* o, 
         const double plo = dadd(T.lo[a], dmul(double(c[a]), cl));
         const double phi = dadd(T.lo[a], dmul(double(c[a] + 1u), cl));
         const double pmid = dadd(T.lo[a], dmul(double(2u * c[a] + 1u), ch));
-        if (d[a] != 0.0) {
+        if (!((zmask >> a) & 1u)) {
             const double tl = dmul(dsub(plo, o[a]), inv[a]);
             const double tm = dmul(dsub(pmid, o[a]), inv[a]);
             const double th = dmul(dsub(phi, o[a]), inv[a]);
@@ -73,6 +74,16 @@ __device__ __forceinline__ void split_node(const DevOctree& T, const double* o, 
             s.hi_b[a] = in_hi ? CUDART_INF : -CUDART_INF;
         }
     }
+}
+
+__device__ __forceinline__ uint32_t zero_mask(const double* d) {
+    return (d[0] == 0.0 ? 1u : 0u) | (d[1] == 0.0 ? 2u : 0u) | (d[2] == 0.0 ? 4u : 0u);
+}
+
+__device__ __forceinline__ void split_node(const DevOctree& T, const double* o, const double* d,
+                                           const double* inv, int level, uint32_t x, uint32_t y, uint32_t z,
+                                           NodeSplit& s) {
+    split_node_z(T, o, zero_mask(d), inv, level, x, y, z, s);
 }
 
 __device__ __forceinline__ bool child_hit(const NodeSplit& s, uint32_t oct, double& t0, double& t1) {
@@ -274,6 +285,7 @@ struct BfsSmem {
     uint32_t qnode[2][kQ];
     uint32_t pos[kQ];  // leaf level: output position of each pair's first hit
     uint8_t qray[2][kQ];
+    uint8_t dflags[kR];  // per ray: direction sign bits (0-2) and zero-component bits (3-5)
     uint32_t rcount[kR], roff[kR];
     uint32_t gray[kR];
     uint32_t n_q, base, overflow, next_tile;
@@ -400,6 +412,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 S.d[a][tid] = r.d[a];
                 S.inv[a][tid] = p.inv[a];
             }
+            S.dflags[tid] = uint8_t(sign_mask(r.d) | (zero_mask(r.d) << 3));
         }
     }
     static_assert(kR <= 64, "per-tile ray mask");
@@ -454,16 +467,16 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 x = uint32_t(xyz & 0x1fffffu);
                 y = uint32_t((xyz >> 21) & 0x1fffffu);
                 z = uint32_t(xyz >> 42);
-                double o[3], d[3], inv[3];
+                double o[3], inv[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     o[a] = S.o[a][ri];
-                    d[a] = S.d[a][ri];
                     inv[a] = S.inv[a][ri];
                 }
+                const uint32_t fl = S.dflags[ri];
                 NodeSplit sp;
-                split_node(T, o, d, inv, level, x, y, z, sp);
-                s = sign_mask(d);
+                split_node_z(T, o, fl >> 3, inv, level, x, y, z, sp);
+                s = fl & 7u;
                 if constexpr (kCount) tests += __popc(node.y);
                 hitmask = child_hits<false>(sp) & node.y & 0xffu;
                 cnt = __popc(hitmask);
@@ -513,16 +526,15 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 ri = S.qray[cur][e];
                 const uint2 node = T.nodes[S.qnode[cur][e]];
                 const uint64_t xyz = S.qxyz[cur][e];
-                double o[3], d[3], inv[3];
+                double o[3], inv[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     o[a] = S.o[a][ri];
-                    d[a] = S.d[a][ri];
                     inv[a] = S.inv[a][ri];
                 }
                 NodeSplit sp;
-                split_node(T, o, d, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
-                           uint32_t(xyz >> 42), sp);
+                split_node_z(T, o, uint32_t(S.dflags[ri]) >> 3, inv, level, uint32_t(xyz & 0x1fffffu),
+                             uint32_t((xyz >> 21) & 0x1fffffu), uint32_t(xyz >> 42), sp);
                 if constexpr (kCount) tests += __popc(node.y);
                 cnt = __popc(child_hits<true>(sp) & node.y & 0xffu);
                 if (cnt) atomicAdd(&S.rcount[ri], cnt);
@@ -553,17 +565,17 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             const uint32_t ri = S.qray[cur][e];
             const uint2 node = T.nodes[S.qnode[cur][e]];
             const uint64_t xyz = S.qxyz[cur][e];
-            double o[3], d[3], inv[3];
+            double o[3], inv[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 o[a] = S.o[a][ri];
-                d[a] = S.d[a][ri];
                 inv[a] = S.inv[a][ri];
             }
+            const uint32_t fl = S.dflags[ri];
             NodeSplit sp;
-            split_node(T, o, d, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
-                       uint32_t(xyz >> 42), sp);
-            const uint32_t s = sign_mask(d);
+            split_node_z(T, o, fl >> 3, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
+                         uint32_t(xyz >> 42), sp);
+            const uint32_t s = fl & 7u;
             uint32_t w = gbase + S.pos[e];
             const uint32_t gr = S.gray[ri];
             const uint32_t keep = child_hits<true>(sp) & node.y & 0xffu;
