@@ -645,7 +645,9 @@ struct DwRedJob {
     const float* part;
     float* dW;
     float* db;
-    uint32_t O, K, blocks;  // blocks: (O * (K + 1) + kRedElems - 1) / kRedElems
+    uint32_t O, K, blocks;  // blocks: (O * (K + 1) + elems - 1) / elems
+    uint32_t ctas;          // partials to sum
+    uint32_t groups;        // partial-sum groups per element (8, or 32 for many partials); elems = 256 / groups
 };
 struct DwRedJobs {
     DwRedJob job[kX3MaxDwJobs];
@@ -653,33 +655,38 @@ struct DwRedJobs {
     int count;
 };
 
-// k_dw_reduce over several jobs in one launch (blockIdx.x -> job by block ranges)
-__global__ void __launch_bounds__(kRedGroups * kRedElems) k_dw_reduce_jobs(DwRedJobs J, uint32_t ctas) {
-    __shared__ float sh[kRedGroups][kRedElems];
+__host__ __device__ inline uint32_t red_groups(uint32_t ctas) { return ctas > 256 ? 32u : kRedGroups; }
+
+// k_dw_reduce over several jobs in one launch (blockIdx.x -> job by block
+// ranges): thread (g, e) sums the partials g, g + G, ... of element e in
+// order, then the G group sums are added in order (G fixed per job: bitwise
+// reproducible)
+__global__ void __launch_bounds__(kRedGroups * kRedElems) k_dw_reduce_jobs(DwRedJobs J) {
+    __shared__ float sh[kRedGroups * kRedElems];
     int t = 0;
     while (t + 1 < J.count && blockIdx.x >= J.first_block[t + 1]) ++t;
     const DwRedJob jb = J.job[t];
+    const uint32_t ctas = jb.ctas, G = jb.groups, E = (kRedGroups * kRedElems) / G;
     const uint32_t cols = jb.K + 1, per = jb.O * cols;
-    const uint32_t el = threadIdx.x % kRedElems, g = threadIdx.x / kRedElems;
-    const uint32_t e = (blockIdx.x - J.first_block[t]) * kRedElems + el;
+    const uint32_t el = threadIdx.x % E, g = threadIdx.x / E;
+    const uint32_t e = (blockIdx.x - J.first_block[t]) * E + el;
     float acc = 0.f;
     if (e < per) {
         uint32_t c = g;
-        for (; c + 3 * kRedGroups < ctas; c += 4 * kRedGroups) {
+        for (; c + 3 * G < ctas; c += 4 * G) {
             const float a0 = __ldg(jb.part + size_t(c) * per + e);
-            const float a1 = __ldg(jb.part + size_t(c + kRedGroups) * per + e);
-            const float a2 = __ldg(jb.part + size_t(c + 2 * kRedGroups) * per + e);
-            const float a3 = __ldg(jb.part + size_t(c + 3 * kRedGroups) * per + e);
+            const float a1 = __ldg(jb.part + size_t(c + G) * per + e);
+            const float a2 = __ldg(jb.part + size_t(c + 2 * G) * per + e);
+            const float a3 = __ldg(jb.part + size_t(c + 3 * G) * per + e);
             acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, a0), a1), a2), a3);
         }
-        for (; c < ctas; c += kRedGroups) acc = __fadd_rn(acc, __ldg(jb.part + size_t(c) * per + e));
+        for (; c < ctas; c += G) acc = __fadd_rn(acc, __ldg(jb.part + size_t(c) * per + e));
     }
-    sh[g][el] = acc;
+    sh[g * E + el] = acc;
     __syncthreads();
     if (g == 0 && e < per) {
-        float v = sh[0][el];
-#pragma unroll
-        for (uint32_t k = 1; k < kRedGroups; ++k) v = __fadd_rn(v, sh[k][el]);
+        float v = sh[el];
+        for (uint32_t k = 1; k < G; ++k) v = __fadd_rn(v, sh[k * E + el]);
         const uint32_t o = e / cols, j = e % cols;
         if (j < jb.K) jb.dW[size_t(o) * jb.K + j] = v;
         else jb.db[o] = v;
@@ -801,6 +808,14 @@ void gemm_x3_dw_batch(const X3DwJob* jobs, int count, const uint32_t* n_dev, uin
     uint32_t blocks = 0;
     for (int i = 0; i < count; ++i) {
         const X3DwJob& jb = jobs[i];
+        const uint32_t per = jb.O * (jb.K + 1);
+        if (jb.ext_part) {  // partials from another kernel: reduction only
+            const uint32_t G = red_groups(jb.ext_ctas), E = kRedGroups * kRedElems / G;
+            R.job[i] = DwRedJob{jb.ext_part, jb.dW, jb.db, jb.O, jb.K, (per + E - 1) / E, jb.ext_ctas, G};
+            R.first_block[i] = blocks;
+            blocks += R.job[i].blocks;
+            continue;
+        }
         const uint32_t Nr = round16(jb.K + 1);
         if (Nr > 144) fail(SVLF_ERR_INVALID_ARGUMENT, "weight-gradient GEMM: K too large");
         const CUtensorMap dmap = feature_map(jb.d, jb.O, ld, ld, jb.O, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -810,16 +825,18 @@ void gemm_x3_dw_batch(const X3DwJob* jobs, int count, const uint32_t* n_dev, uin
             k_gemm_dw<false><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, p, n_dev, cap, jb.O, jb.K, Nr);
         else
             k_gemm_dw<true><<<ctas, kDThreads, kDSmem, s>>>(dmap, xmap, p, n_dev, cap, jb.O, jb.K, Nr);
-        const uint32_t per = jb.O * (jb.K + 1);
-        R.job[i] = DwRedJob{p, jb.dW, jb.db, jb.O, jb.K, (per + kRedElems - 1) / kRedElems};
+        const uint32_t G = red_groups(ctas), E = kRedGroups * kRedElems / G;
+        R.job[i] = DwRedJob{p, jb.dW, jb.db, jb.O, jb.K, (per + E - 1) / E, ctas, G};
         R.first_block[i] = blocks;
         blocks += R.job[i].blocks;
         off += size_t(ctas) * per;
     }
     R.first_block[count] = blocks;
     R.count = count;
-    k_dw_reduce_jobs<<<blocks, kRedGroups * kRedElems, 0, s>>>(R, ctas);
-    note_launch(count + 1);
+    k_dw_reduce_jobs<<<blocks, kRedGroups * kRedElems, 0, s>>>(R);
+    int gemms = 0;
+    for (int i = 0; i < count; ++i) gemms += jobs[i].ext_part ? 0 : 1;
+    note_launch(gemms + 1);
 }
 
 void gemm_x3_dw(const float* d, const float* x, uint32_t O, uint32_t K, float* dW, float* db, const uint32_t* n_dev,

@@ -52,6 +52,10 @@ struct X3DwJob {
     uint32_t O, K;
     float* dW;
     float* db;
+    // partials already produced by another kernel (ext_ctas of O x (K + 1)
+    // floats, CTA-major): no GEMM, only the fixed-order reduction
+    const float* ext_part = nullptr;
+    uint32_t ext_ctas = 0;
 };
 constexpr int kX3MaxDwJobs = 6;
 void gemm_x3_dw_batch(const X3DwJob* jobs, int count, const uint32_t* n_dev, uint32_t cap, uint32_t ld, float* part,

@@ -533,38 +533,97 @@ __global__ void k_step_scalars(uint32_t n, const unsigned long long* counters, c
 // dX = W^T D; these kernels are the per-hit heads and the feature-gradient
 // scatters (src/mlp.cpp:151-230, src/train.cpp:243-285).
 
-// f_C head (sigmoid') and its 3 -> 128 back-projection masked by relu'(h3)
-__global__ void __launch_bounds__(128) k_bwd_head_c(DevModel M, HitArgs H) {
+// f_C head (sigmoid') and its 3 -> 128 back-projection masked by relu'(h3),
+// plus the head's weight gradient dW3 = D3 H3^T, db3 = sum D3 (src/mlp.cpp:
+// 151-230) from the h3 rows this kernel reads anyway: each warp stages its 32
+// hits' h3 rows 32 at a time transposed in shared memory and lane k
+// accumulates sum_h d3[c][h] h3[k][h] (fixed order, FMA); the block's warps
+// are summed in order into one partial per block (3 x 129 floats), and the
+// weight-gradient reduction launch sums the partials in block order
+// (bitwise reproducible, like the GEMM partials).
+constexpr int kHcThreads = 256;
+constexpr uint32_t kHcPartial = 3 * (kHid + 1);
+__global__ void __launch_bounds__(kHcThreads) k_bwd_head_c(DevModel M, HitArgs H, float* __restrict__ wpart) {
     using D = DecOffsets;
+    constexpr int kW = kHcThreads / 32;
+    __shared__ float tt[kW][32][33];
+    __shared__ float4 dd[kW][32];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t N = active_hits(H);
     const size_t L = H.ld;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+    float acc[3][kHid / 32];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < kHid / 32; ++q) acc[c][q] = 0.f;
+    float accb = 0.f;  // lanes 0..2: bias gradient of output lane
+    for (uint32_t j0 = blockIdx.x * kHcThreads; j0 < N; j0 += gridDim.x * kHcThreads) {
+        const uint32_t j = j0 + threadIdx.x;
+        const bool valid = j < N;
         float* Dl = H.deltas + j;
         float d3[3] = {0.f, 0.f, 0.f};
-        if (has_color(H, j))
+        if (valid && has_color(H, j))
             for (int o = 0; o < 3; ++o) {
                 const float a = H.rgb[o * L + j];
                 d3[o] = H.drgb[o * L + j] * a * (1.0f - a);
             }
+        if (valid)
 #pragma unroll
-        for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * L] = d3[o];
+            for (int o = 0; o < 3; ++o) Dl[(D_C3 + o) * L] = d3[o];
+        dd[warp][lane] = make_float4(d3[0], d3[1], d3[2], 0.f);
         const float* h3 = H.acts + A_H3 * L + j;
-        for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
-            float hv[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) hv[i] = __ldg(h3 + size_t(k0 + i) * L);
+        for (int q = 0; q < kHid / 32; ++q) {
+            const int k0 = 32 * q;
+            float hv[32];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int k = k0 + i;
-                float v = 0.f;
-                if (hv[i] > 0.f) {
-                    v = __ldg(M.mc + D::C_W3 + k) * d3[0];
-                    v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
-                    v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
+            for (int i = 0; i < 32; ++i) hv[i] = valid ? __ldg(h3 + size_t(k0 + i) * L) : 0.f;
+            if (valid)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int k = k0 + i;
+                    float v = 0.f;
+                    if (hv[i] > 0.f) {
+                        v = __ldg(M.mc + D::C_W3 + k) * d3[0];
+                        v = fmaf(__ldg(M.mc + D::C_W3 + kHid + k), d3[1], v);
+                        v = fmaf(__ldg(M.mc + D::C_W3 + 2 * kHid + k), d3[2], v);
+                    }
+                    Dl[(D_C2 + k) * L] = v;
                 }
-                Dl[(D_C2 + k) * L] = v;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) tt[warp][i][lane] = hv[i];
+            __syncwarp();
+#pragma unroll 8
+            for (int h = 0; h < 32; ++h) {  // lane = k0 + lane, hits in order
+                const float t = tt[warp][lane][h];
+                const float4 dh = dd[warp][h];
+                acc[0][q] = __fmaf_rn(dh.x, t, acc[0][q]);
+                acc[1][q] = __fmaf_rn(dh.y, t, acc[1][q]);
+                acc[2][q] = __fmaf_rn(dh.z, t, acc[2][q]);
             }
         }
+        if (lane < 3)
+            for (int h = 0; h < 32; ++h) {
+                const float4 dh = dd[warp][h];
+                accb = __fadd_rn(accb, lane == 0 ? dh.x : (lane == 1 ? dh.y : dh.z));
+            }
+        __syncwarp();
+    }
+    // block partial: warps summed in order; element c * 129 + k (k = 128: bias)
+    __syncthreads();
+    float* red = &tt[0][0][0];  // kW x kHcPartial floats
+    static_assert(kW * kHcPartial <= kW * 32 * 33, "partial staging fits");
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < kHid / 32; ++q) red[warp * kHcPartial + c * (kHid + 1) + 32 * q + lane] = acc[c][q];
+    if (lane < 3) red[warp * kHcPartial + lane * (kHid + 1) + kHid] = accb;
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < kHcPartial; e += kHcThreads) {
+        float t = red[e];
+        for (int w = 1; w < kW; ++w) t = __fadd_rn(t, red[w * kHcPartial + e]);
+        wpart[size_t(blockIdx.x) * kHcPartial + e] = t;
     }
 }
 
@@ -576,19 +635,29 @@ __global__ void __launch_bounds__(128) k_bwd_head_c(DevModel M, HitArgs H) {
 constexpr int kScWarps = 4;
 
 // Colour-feature gradient scatter (unless frozen) and the positional
-// Jacobian into eta (src/train.cpp:244-265), then the f_T heads' deltas and
-// their 2 -> 128 back-projection masked by relu'(h_T).
+// Jacobian into eta (src/train.cpp:244-265), then the f_T heads' deltas,
+// their 2 -> 128 back-projection masked by relu'(h_T), and the f_T head's
+// weight gradient from the same h_T rows (as in k_bwd_head_c: per-warp
+// transposed staging, one partial of 2 x 129 floats per block).
+constexpr uint32_t kHtPartial = 2 * (kHid + 1);
 __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevModel M, HitArgs H,
                                                                const float* __restrict__ dX, bool color_frozen,
-                                                               float* g_fc, int* err) {
+                                                               float* g_fc, int* err, float* __restrict__ wpart) {
     using D = DecOffsets;
     __shared__ float zs[kScWarps][kFc][33];
     __shared__ uint32_t cs[kScWarps][32][8];
     __shared__ float ws_s[kScWarps][32][8];
     __shared__ double dots[kScWarps][32][8];
+    __shared__ float2 ddt[kScWarps][32];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t N = active_hits(H);
     const size_t L = H.ld;
+    float hacc[2][kHid / 32];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < kHid / 32; ++q) hacc[c][q] = 0.f;
+    float haccb = 0.f;  // lanes 0, 1: bias gradient of head output lane
     for (uint32_t tile = blockIdx.x * kScWarps + warp; tile * 32 < N; tile += gridDim.x * kScWarps) {
         const uint32_t j = tile * 32 + lane;
         const bool valid = j < N;
@@ -662,27 +731,66 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevMo
             const double dx12[3] = {dsub(g.x1[0], g.x2[0]), dsub(g.x1[1], g.x2[1]), dsub(g.x1[2], g.x2[2])};
             deta = dadd(deta, dot3(dxs, dx12));
         }
-        if (!valid) continue;
         // f_T heads: relu (tau), sigmoid (eta)
         float* Dl = H.deltas + j;
-        const float tau = H.tau[j], eta = H.eta[j];
-        const float d0 = tau > 0.f ? float(H.dtau[j]) : 0.f;
-        const float d1 = float(deta) * eta * (1.0f - eta);
-        Dl[D_T1 * L] = d0;
-        Dl[(D_T1 + 1) * L] = d1;
+        float d0 = 0.f, d1 = 0.f;
+        if (valid) {
+            const float tau = H.tau[j], eta = H.eta[j];
+            d0 = tau > 0.f ? float(H.dtau[j]) : 0.f;
+            d1 = float(deta) * eta * (1.0f - eta);
+            Dl[D_T1 * L] = d0;
+            Dl[(D_T1 + 1) * L] = d1;
+        }
+        ddt[warp][lane] = make_float2(d0, d1);
         const float* ht = H.acts + A_HT * L + j;
-        for (int k0 = 0; k0 < kHid; k0 += 16) {  // 16 activation loads in flight before the stores
-            float hv[16];
+        float* tt = &zs[warp][0][0];  // [32][33]: free once the scatter above is done
 #pragma unroll
-            for (int i = 0; i < 16; ++i) hv[i] = __ldg(ht + size_t(k0 + i) * L);
+        for (int q = 0; q < kHid / 32; ++q) {
+            const int k0 = 32 * q;
+            float hv[32];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int k = k0 + i;
-                float v = 0.f;
-                if (hv[i] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
-                Dl[(D_T0 + k) * L] = v;
+            for (int i = 0; i < 32; ++i) hv[i] = valid ? __ldg(ht + size_t(k0 + i) * L) : 0.f;
+            if (valid)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int k = k0 + i;
+                    float v = 0.f;
+                    if (hv[i] > 0.f) v = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), d1, __ldg(M.mt + D::T_W1 + k) * d0);
+                    Dl[(D_T0 + k) * L] = v;
+                }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) tt[i * 33 + lane] = hv[i];
+            __syncwarp();
+#pragma unroll 8
+            for (int h = 0; h < 32; ++h) {  // lane = k0 + lane, hits in order
+                const float t = tt[lane * 33 + h];
+                const float2 dh = ddt[warp][h];
+                hacc[0][q] = __fmaf_rn(dh.x, t, hacc[0][q]);
+                hacc[1][q] = __fmaf_rn(dh.y, t, hacc[1][q]);
             }
         }
+        if (lane < 2)
+            for (int h = 0; h < 32; ++h) {
+                const float2 dh = ddt[warp][h];
+                haccb = __fadd_rn(haccb, lane == 0 ? dh.x : dh.y);
+            }
+        __syncwarp();
+    }
+    // block partial of the f_T head's weight gradient: warps summed in order
+    __syncthreads();
+    float* red = &zs[0][0][0];
+    static_assert(kScWarps * kHtPartial <= kScWarps * kFc * 33, "partial staging fits");
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < kHid / 32; ++q) red[warp * kHtPartial + c * (kHid + 1) + 32 * q + lane] = hacc[c][q];
+    if (lane < 2) red[warp * kHtPartial + lane * (kHid + 1) + kHid] = haccb;
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < kHtPartial; e += 32 * kScWarps) {
+        float t = red[e];
+        for (uint32_t w = 1; w < kScWarps; ++w) t = __fadd_rn(t, red[w * kHtPartial + e]);
+        wpart[size_t(blockIdx.x) * kHtPartial + e] = t;
     }
 }
 
@@ -1050,9 +1158,11 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     for (int i = 0; i < jobs.count; ++i)
         img_bytes += gemm_x3_image_bytes(jobs.job[i].bwd ? jobs.job[i].O : jobs.job[i].K);
     uint8_t* wimg = S.wimg.ensure<uint8_t>(img_bytes);
-    float* part = S.dw_part.ensure<float>(gemm_x3_dw_partial_floats(kHid, kInT) + gemm_x3_dw_partial_floats(2, kHid) +
-                                          gemm_x3_dw_partial_floats(kHid, kInC) + 2 * gemm_x3_dw_partial_floats(kHid, kHid) +
-                                          gemm_x3_dw_partial_floats(3, kHid));
+    const size_t gemm_part = gemm_x3_dw_partial_floats(kHid, kInT) + gemm_x3_dw_partial_floats(kHid, kInC) +
+                             2 * gemm_x3_dw_partial_floats(kHid, kHid);
+    float* part = S.dw_part.ensure<float>(gemm_part + size_t(sms()) * (4 * kHcPartial + 8 * kHtPartial));
+    float* head_part = part + gemm_part;                    // k_bwd_head_c's block partials (<= 4 blocks per SM)
+    float* ht_part = head_part + size_t(sms()) * 4 * kHcPartial;  // k_bwd_feat_c's (<= 8 blocks per SM)
     size_t tb_scan = 0, tb_red = 0, tb_sel = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, act_cnt, dpos, int(n + 1));
     cub::DeviceReduce::Sum(nullptr, tb_red, ray_loss, red + R_LOSS, int(std::max<uint32_t>(n, 1)));
@@ -1086,6 +1196,7 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
     float* g_mc = g_mt + SVLF_DEC_T_SIZE;
     const unsigned in_grid = loop_grid(cap, 32 * kInWarps, 16);
     const unsigned hit_grid = loop_grid(cap, 128, 16);
+    const unsigned hc_grid = loop_grid(cap, kHcThreads, 4);
     const unsigned sc_grid = loop_grid(cap, 32 * kScWarps, 8);
     auto A = [&](int row) { return acts + size_t(row) * ld; };
     auto Dm = [&](int row) { return deltas + size_t(row) * ld; };
@@ -1137,12 +1248,12 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
         }
         ev(3);
         // backward. f_C: head -> D_C2; D_C1 = relu'(h2) W2^T D_C2; D_C0 = relu'(h1) W1^T D_C1; dX_C = W0^T D_C0
-        k_bwd_head_c<<<hit_grid, 128, 0, s>>>(M.view, H);
+        k_bwd_head_c<<<hc_grid, kHcThreads, 0, s>>>(M.view, H, head_part);
         gemm_x3_bwd(Dm(D_C2), img(J_BC2), kHid, kHid, 0, Dm(D_C1), A(A_H2), n_act, cap, ld, s);
         gemm_x3_bwd(Dm(D_C1), img(J_BC1), kHid, kHid, 0, Dm(D_C0), A(A_H1), n_act, cap, ld, s);
         gemm_x3_bwd(Dm(D_C0), img(J_BC0), kHid, kInC, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
         // colour-feature scatter, positional Jacobian, f_T heads -> D_T0
-        k_bwd_feat_c<<<sc_grid, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag);
+        k_bwd_feat_c<<<sc_grid, 32 * kScWarps, 0, s>>>(T, M.view, H, dxs, o.color_frozen, g_fc, err_flag, ht_part);
         gemm_x3_bwd(Dm(D_T0), img(J_BT0), kHid, kInT, 6, dxs + 6 * size_t(ld), nullptr, n_act, cap, ld, s);
         k_bwd_feat_t<<<sc_grid, 32 * kScWarps, 0, s>>>(T, H, dxs, g_ft, err_flag);
         launches += 3;
@@ -1151,12 +1262,12 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
             X3DwJob dw[kX3MaxDwJobs];
             int nj = 0;
             dw[nj++] = {Dm(D_T0), A(A_XT), kHid, kInT, g_mt + D::T_W0, g_mt + D::T_B0};
-            dw[nj++] = {Dm(D_T1), A(A_HT), 2, kHid, g_mt + D::T_W1, g_mt + D::T_B1};
+            dw[nj++] = {nullptr, nullptr, 2, kHid, g_mt + D::T_W1, g_mt + D::T_B1, ht_part, sc_grid};
             if (!o.color_frozen) {
                 dw[nj++] = {Dm(D_C0), A(A_XC), kHid, kInC, g_mc + D::C_W0, g_mc + D::C_B0};
                 dw[nj++] = {Dm(D_C1), A(A_H1), kHid, kHid, g_mc + D::C_W1, g_mc + D::C_B1};
                 dw[nj++] = {Dm(D_C2), A(A_H2), kHid, kHid, g_mc + D::C_W2, g_mc + D::C_B2};
-                dw[nj++] = {Dm(D_C3), A(A_H3), 3, kHid, g_mc + D::C_W3, g_mc + D::C_B3};
+                dw[nj++] = {nullptr, nullptr, 3, kHid, g_mc + D::C_W3, g_mc + D::C_B3, head_part, hc_grid};
             }
             gemm_x3_dw_batch(dw, nj, n_act, cap, ld, part, prod, s);
         }
