@@ -114,6 +114,12 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uin
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
@@ -206,7 +212,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
     k_gemm_feat(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
                 const __grid_constant__ CUtensorMap mask_map, const uint8_t* __restrict__ wimg, float* __restrict__ out,
                 const float* __restrict__ bias, const float* __restrict__ mask, const uint32_t* __restrict__ n_dev,
-                uint32_t cap, uint32_t ld, uint32_t kred, uint32_t n_out) {
+                uint32_t cap, uint32_t ld, uint32_t kred, uint32_t n_out, const float* __restrict__ head_w,
+                uint32_t head_c, float* __restrict__ head_out) {
     extern __shared__ uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kFStages * kFStage + kFEpi);
@@ -390,6 +397,22 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 if (lane == 0) {
                     tma_store_2d(&out_map, buf, int(h0), int(32 * q));
                     bulk_commit();
+                }
+                if (!kBwd && head_c) {
+                    // head layer partial over this warp's 32 rows, lane = hit of the box (read back
+                    // transposed from the swizzled box): head_out[q * head_c + c] = sum_r W[c][32q + r] h
+                    float hp[3] = {0.f, 0.f, 0.f};
+#pragma unroll 8
+                    for (uint32_t r = 0; r < 32; ++r) {
+                        const float v = ld_shared_f32(buf + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4);
+#pragma unroll
+                        for (uint32_t c = 0; c < 3; ++c)
+                            if (c < head_c) hp[c] = __fmaf_rn(__ldg(head_w + c * n_out + 32 * q + r), v, hp[c]);
+                    }
+                    if (h0 + lane < n)
+#pragma unroll
+                        for (uint32_t c = 0; c < 3; ++c)
+                            if (c < head_c) head_out[size_t(q * head_c + c) * ld + h0 + lane] = hp[c];
                 }
             } else if (use_mask && lane == 0 && k + 1 < nboxes) {
                 bulk_wait_read<0>();
@@ -765,13 +788,16 @@ void gemm_x3_build_images(X3ImageJobs& jobs, uint8_t* buf, cudaStream_t s) {
 }
 
 void gemm_x3_fwd(const float* x, const uint8_t* img, const float* bias, float* y, uint32_t O, uint32_t K,
-                 const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s) {
+                 const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s, const X3Head* head) {
     if (cap == 0) return;
     setup();
+    if (head && (head->c < 1 || head->c > 3 || O != 128))
+        fail(SVLF_ERR_INVALID_ARGUMENT, "head epilogue: 1..3 outputs over 128 rows");
     const CUtensorMap map = feature_map(x, K, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const CUtensorMap omap = feature_map(y, O, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    k_gemm_feat<false><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, omap, img, y, bias, nullptr, n_dev, cap,
-                                                                 ld, K, O);
+    k_gemm_feat<false><<<feat_grid(cap), kFThreads, kFSmem, s>>>(
+        map, omap, omap, img, y, bias, nullptr, n_dev, cap, ld, K, O, head ? head->w : nullptr, head ? head->c : 0u,
+        head ? head->out : nullptr);
     note_launch();
 }
 
@@ -783,7 +809,7 @@ void gemm_x3_bwd(const float* d, const uint8_t* img, uint32_t O, uint32_t K, uin
     const CUtensorMap omap = feature_map(dx, K - k0, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap mmap = mask ? feature_map(mask, K - k0, ld, ld, 32, CU_TENSOR_MAP_SWIZZLE_128B) : omap;
     k_gemm_feat<true><<<feat_grid(cap), kFThreads, kFSmem, s>>>(map, omap, mmap, img, dx, nullptr, mask, n_dev, cap,
-                                                                ld, O, K - k0);
+                                                                ld, O, K - k0, nullptr, 0u, nullptr);
     note_launch();
 }
 

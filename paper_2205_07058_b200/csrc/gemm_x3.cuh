@@ -32,8 +32,17 @@ size_t gemm_x3_image_bytes(uint32_t kred);
 void gemm_x3_build_images(X3ImageJobs& jobs, uint8_t* buf, cudaStream_t s);
 
 // y[j][:] = relu(sum_k W[j][k] x[k][:] + bias[j]), j < O, k < K; img from a forward job
+// Optional head epilogue of a forward GEMM with O = 128: the partial products of
+// a following 128 -> c layer (c <= 3, weights w row-major c x 128) over each
+// 32-row quarter q of y, written to out rows q * c + (0..c-1) (stride ld); the
+// consumer adds the bias and the four quarters in order.
+struct X3Head {
+    const float* w;
+    uint32_t c;
+    float* out;
+};
 void gemm_x3_fwd(const float* x, const uint8_t* img, const float* bias, float* y, uint32_t O, uint32_t K,
-                 const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s);
+                 const uint32_t* n_dev, uint32_t cap, uint32_t ld, cudaStream_t s, const X3Head* head = nullptr);
 // dx[j][:] = sum_o W[o][k0 + j] d[o][:], j < K - k0; zeroed where mask[j][:] <= 0 (mask may be
 // null); img from a backward job
 void gemm_x3_bwd(const float* d, const uint8_t* img, uint32_t O, uint32_t K, uint32_t k0, float* dx,

@@ -53,7 +53,9 @@ namespace svlfb {
 namespace {
 
 // feature-major activation rows (x ld hits)
-constexpr int A_XT = 0, A_HT = 134, A_XC = 262, A_H1 = 300, A_H2 = 428, A_H3 = 556, A_ROWS = 684;
+constexpr int A_XT = 0, A_HT = 134, A_XC = 262, A_H1 = 300, A_H2 = 428, A_H3 = 556;
+// head-layer partials from the forward GEMM epilogues (X3Head): 4 row quarters x outputs
+constexpr int A_YT = 684, A_YC = 692, A_ROWS = 704;
 // feature-major delta rows (dL/d pre-activation of each layer)
 constexpr int D_T0 = 0, D_T1 = 128, D_C0 = 130, D_C1 = 258, D_C2 = 386, D_C3 = 514, D_ROWS = 517;
 
@@ -345,13 +347,13 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_mid(DevOctree T, DevModel
         float* X = H.acts + j;
         float eta = 0.5f;
         if (valid) {
-            const float* h = X + A_HT * L;
+            // bias + the four 32-row partials of the f_T layer-0 GEMM's head epilogue, in order
+            const float* y = X + A_YT * L;
             float y0 = __ldg(M.mt + D::T_B1), y1 = __ldg(M.mt + D::T_B1 + 1);
-#pragma unroll 16
-            for (int k = 0; k < kHid; ++k) {
-                const float v = __ldg(h + size_t(k) * L);
-                y0 = fmaf(__ldg(M.mt + D::T_W1 + k), v, y0);
-                y1 = fmaf(__ldg(M.mt + D::T_W1 + kHid + k), v, y1);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                y0 = __fadd_rn(y0, y[size_t(2 * q) * L]);
+                y1 = __fadd_rn(y1, y[size_t(2 * q + 1) * L]);
             }
             eta = sigmoid_ref(y1);
             H.tau[j] = y0 > 0.f ? y0 : 0.f;
@@ -406,14 +408,13 @@ __global__ void __launch_bounds__(128) k_fwd_rgb(DevModel M, HitArgs H) {
             for (int c = 0; c < 3; ++c) H.rgb[c * L + j] = 0.f;
             continue;
         }
-        const float* h = H.acts + A_H3 * L + j;
+        // bias + the four 32-row partials of the last f_C GEMM's head epilogue, in order
+        const float* yq = H.acts + A_YC * L + j;
         float y[3] = {__ldg(M.mc + D::C_B3), __ldg(M.mc + D::C_B3 + 1), __ldg(M.mc + D::C_B3 + 2)};
-#pragma unroll 16
-        for (int k = 0; k < kHid; ++k) {
-            const float v = __ldg(h + size_t(k) * L);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) y[c] = fmaf(__ldg(M.mc + D::C_W3 + c * kHid + k), v, y[c]);
-        }
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) y[c] = __fadd_rn(y[c], yq[size_t(3 * q + c) * L]);
 #pragma unroll
         for (int c = 0; c < 3; ++c) H.rgb[c * L + j] = sigmoid_ref(y[c]);
     }
@@ -1234,11 +1235,12 @@ TrainResult run_train_step(TrainScratch& S, const DevOctree& T, const TrainModel
         ev(1);
         // forward
         k_fwd_in_t<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
-        gemm_x3_fwd(A(A_XT), img(J_FT0), M.view.mt + D::T_B0, A(A_HT), kHid, kInT, n_act, cap, ld, s);
+        const X3Head head_t{M.view.mt + D::T_W1, 2, A(A_YT)}, head_c{M.view.mc + D::C_W3, 3, A(A_YC)};
+        gemm_x3_fwd(A(A_XT), img(J_FT0), M.view.mt + D::T_B0, A(A_HT), kHid, kInT, n_act, cap, ld, s, &head_t);
         k_fwd_mid<<<in_grid, 32 * kInWarps, 0, s>>>(T, M.view, H, err_flag);
         gemm_x3_fwd(A(A_XC), img(J_FC0), M.view.mc + D::C_B0, A(A_H1), kHid, kInC, n_act, cap, ld, s);
         gemm_x3_fwd(A(A_H1), img(J_FC1), M.view.mc + D::C_B1, A(A_H2), kHid, kHid, n_act, cap, ld, s);
-        gemm_x3_fwd(A(A_H2), img(J_FC2), M.view.mc + D::C_B2, A(A_H3), kHid, kHid, n_act, cap, ld, s);
+        gemm_x3_fwd(A(A_H2), img(J_FC2), M.view.mc + D::C_B2, A(A_H3), kHid, kHid, n_act, cap, ld, s, &head_c);
         k_fwd_rgb<<<hit_grid, 128, 0, s>>>(M.view, H);
         launches += 3;
         ev(2);
