@@ -544,7 +544,10 @@ __global__ void k_step_scalars(uint32_t n, const unsigned long long* counters, c
 // (bitwise reproducible, like the GEMM partials).
 constexpr int kHcThreads = 256;
 constexpr uint32_t kHcPartial = 3 * (kHid + 1);
-__global__ void __launch_bounds__(kHcThreads) k_bwd_head_c(DevModel M, HitArgs H, float* __restrict__ wpart) {
+#ifndef SVLF_HC_MINB
+#define SVLF_HC_MINB 3  // resident 256-thread blocks per SM (caps the registers at 85)
+#endif
+__global__ void __launch_bounds__(kHcThreads, SVLF_HC_MINB) k_bwd_head_c(DevModel M, HitArgs H, float* __restrict__ wpart) {
     using D = DecOffsets;
     constexpr int kW = kHcThreads / 32;
     __shared__ float tt[kW][32][33];
@@ -641,7 +644,10 @@ constexpr int kScWarps = 4;
 // weight gradient from the same h_T rows (as in k_bwd_head_c: per-warp
 // transposed staging, one partial of 2 x 129 floats per block).
 constexpr uint32_t kHtPartial = 2 * (kHid + 1);
-__global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_c(DevOctree T, DevModel M, HitArgs H,
+#ifndef SVLF_FEATC_MINB
+#define SVLF_FEATC_MINB 5  // resident blocks per SM: caps the registers at 96 (no spills; 128 uncapped)
+#endif
+__global__ void __launch_bounds__(32 * kScWarps, SVLF_FEATC_MINB) k_bwd_feat_c(DevOctree T, DevModel M, HitArgs H,
                                                                const float* __restrict__ dX, bool color_frozen,
                                                                float* g_fc, int* err, float* __restrict__ wpart) {
     using D = DecOffsets;
