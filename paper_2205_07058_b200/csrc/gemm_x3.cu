@@ -196,7 +196,9 @@ constexpr uint32_t kFThreads = 448;  // warp 0 TMA, 1 MMA, 2-9 split, 10-13 epil
 constexpr uint32_t kFSplitWarps = 8;
 // epilogue staging: per epilogue warp two 32 x 32 fp32 boxes (128-byte swizzle), stored by TMA
 constexpr uint32_t kFEpi = 4 * 2 * 4096;
-constexpr uint32_t kFSmem = kFStages * kFStage + kFEpi + 1024 + 256;
+constexpr uint32_t kFHeadW = kFStages * kFStage + kFEpi + 256;  // head weights: float2 {W0, W1} + float W2 per row
+constexpr uint32_t kFSmem = kFStages * kFStage + kFEpi + 1024 + 256 + 128 * 12;
+static_assert(kFSmem <= 232448, "shared memory budget");
 constexpr uint32_t kTmemAcc = kNT;  // TMEM columns per accumulator (two: tile t's epilogue overlaps t+1's MMAs)
 constexpr uint32_t kTmemCols = 2 * kTmemAcc <= 256 ? 256 : 512;  // allocation: a power of two
 
@@ -338,6 +340,16 @@ __global__ void __launch_bounds__(kFThreads, 1)
         // Bwd with a mask: the box first receives the mask (TMA load, same swizzle), each thread
         // masks its row in place, and the box is stored back to the output.
         const uint32_t stage0 = sbase + kFStages * kFStage + ew * 8192;
+        // head weights of this warp's rows: {W[0][k], W[1][k]} pairs and W[2][k]
+        const uint32_t hw01 = sbase + kFHeadW + 8 * (32 * q), hw2 = sbase + kFHeadW + 1024 + 4 * (32 * q);
+        if (!kBwd && head_c) {
+            const uint32_t k = 32 * q + lane;
+            const float w0 = __ldg(head_w + k), w1 = head_c > 1 ? __ldg(head_w + n_out + k) : 0.f;
+            const float w2 = head_c > 2 ? __ldg(head_w + 2 * n_out + k) : 0.f;
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(hw01 + 8 * lane), "f"(w0), "f"(w1) : "memory");
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(hw2 + 4 * lane), "f"(w2) : "memory");
+            __syncwarp();
+        }
         const bool use_mask = kBwd && mask != nullptr && 32 * q < n_out;
         const uint32_t nboxes = my_tiles * nb;
         uint32_t mphase = 0;  // parity bit per buffer
@@ -405,9 +417,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll 8
                     for (uint32_t r = 0; r < 32; ++r) {
                         const float v = ld_shared_f32(buf + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4);
-#pragma unroll
-                        for (uint32_t c = 0; c < 3; ++c)
-                            if (c < head_c) hp[c] = __fmaf_rn(__ldg(head_w + c * n_out + 32 * q + r), v, hp[c]);
+                        float w0, w1, w2;  // broadcast loads
+                        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(w0), "=f"(w1) : "r"(hw01 + 8 * r));
+                        w2 = ld_shared_f32(hw2 + 4 * r);
+                        hp[0] = __fmaf_rn(w0, v, hp[0]);
+                        hp[1] = __fmaf_rn(w1, v, hp[1]);
+                        hp[2] = __fmaf_rn(w2, v, hp[2]);
                     }
                     if (h0 + lane < n)
 #pragma unroll
