@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(32 * kScWarps, SVLF_FEATC_MINB) k_bwd_feat_c(D
                 ws_s[warp][lane][b] = act ? ws[b] : 0.f;
             }
         }
-#pragma unroll 4
+#pragma unroll
         for (int d = 0; d < kFc; ++d) zs[warp][d][lane] = act ? dX[(6 + d) * L + j] : 0.f;
         __syncwarp();
         unsigned live = __ballot_sync(0xffffffffu, act);
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(32 * kScWarps, SVLF_FEATC_MINB) k_bwd_feat_c(D
 
 // Thickness-feature gradient scatter: g[corner_b] += w1_b dz1 + w2_b dz2
 // (dz1, dz2 = rows 6..69 and 70..133 of dX_T), in two 32-feature halves.
-__global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_t(DevOctree T, HitArgs H, const float* __restrict__ dX,
+__global__ void __launch_bounds__(32 * kScWarps, 4) k_bwd_feat_t(DevOctree T, HitArgs H, const float* __restrict__ dX,
                                                                float* g_ft, int* err) {
     __shared__ float zs[kScWarps][64][33];
     __shared__ uint32_t cs[kScWarps][32][8];
@@ -827,8 +827,8 @@ __global__ void __launch_bounds__(32 * kScWarps) k_bwd_feat_t(DevOctree T, HitAr
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
             __syncwarp();
-#pragma unroll 4
-            for (int r = 0; r < 32; ++r) {
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {  // all 64 row loads in flight
                 zs[warp][r][lane] = act ? dX[(6 + 32 * half + r) * L + j] : 0.f;
                 zs[warp][32 + r][lane] = act ? dX[(6 + kFt + 32 * half + r) * L + j] : 0.f;
             }
