@@ -278,11 +278,12 @@ __device__ __forceinline__ void weights_from_u(const double* u, float* w) {
 // f_T input column: [r6 | psi_T(x1) | psi_T(x2)] (voxel_batch.hpp:69-96).
 // A warp owns 32 consecutive hits (geometry lane = hit); each hit's 8 corner
 // rows are read coalesced (lane = 2 features), accumulated in the reference's
-// corner order without FMA, staged transposed in shared memory and written
-// row by row (coalesced feature-major stores).
+// corner order without FMA, staged transposed in shared memory 16 hits at a
+// time (8.7 KB per warp) and written two rows per store instruction
+// (coalesced feature-major half-rows).
 constexpr int kInWarps = 2;
 __global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevModel M, HitArgs H, int* err) {
-    __shared__ float st[kInWarps][2 * kFt][33];
+    __shared__ float st[kInWarps][2 * kFt][17];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t N = active_hits(H);
     const size_t L = H.ld;
@@ -290,10 +291,11 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevMode
         const uint32_t j = tile * 32 + lane;
         HitGeom g;
         const bool ok = j < N && hit_geom(T, H, j, g, err);
-        float* X = H.acts + j;
-        if (j < N)
+        if (j < N) {
+            float* X = H.acts + j;
 #pragma unroll
             for (int k = 0; k < 6; ++k) X[(A_XT + k) * L] = ok ? g.r6[k] : 0.f;
+        }
         uint32_t cs[8];
         float w1[8], w2[8];
 #pragma unroll
@@ -304,30 +306,38 @@ __global__ void __launch_bounds__(32 * kInWarps) k_fwd_in_t(DevOctree T, DevMode
         }
         const unsigned live = __ballot_sync(0xffffffffu, ok);
         const uint32_t d = 2 * lane;
-        __syncwarp();
-        for (int h = 0; h < 32; ++h) {
-            float2 a1 = make_float2(0.f, 0.f), a2 = a1;
-            if ((live >> h) & 1u) {
+        const uint32_t sub = lane & 15, rsel = lane >> 4;  // store: hit 16 hh + sub of row r + rsel
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+            __syncwarp();
+            for (int h = 16 * hh; h < 16 * hh + 16; ++h) {
+                float2 a1 = make_float2(0.f, 0.f), a2 = a1;
+                if ((live >> h) & 1u) {
 #pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
-                    const float wa = __shfl_sync(0xffffffffu, w1[b], h), wb = __shfl_sync(0xffffffffu, w2[b], h);
-                    const float2 v = __ldg(reinterpret_cast<const float2*>(M.ft + size_t(c) * kFt) + lane);
-                    a1.x = __fadd_rn(a1.x, __fmul_rn(wa, v.x));
-                    a1.y = __fadd_rn(a1.y, __fmul_rn(wa, v.y));
-                    a2.x = __fadd_rn(a2.x, __fmul_rn(wb, v.x));
-                    a2.y = __fadd_rn(a2.y, __fmul_rn(wb, v.y));
+                    for (int b = 0; b < 8; ++b) {
+                        const uint32_t c = __shfl_sync(0xffffffffu, cs[b], h);
+                        const float wa = __shfl_sync(0xffffffffu, w1[b], h), wb = __shfl_sync(0xffffffffu, w2[b], h);
+                        const float2 v = __ldg(reinterpret_cast<const float2*>(M.ft + size_t(c) * kFt) + lane);
+                        a1.x = __fadd_rn(a1.x, __fmul_rn(wa, v.x));
+                        a1.y = __fadd_rn(a1.y, __fmul_rn(wa, v.y));
+                        a2.x = __fadd_rn(a2.x, __fmul_rn(wb, v.x));
+                        a2.y = __fadd_rn(a2.y, __fmul_rn(wb, v.y));
+                    }
                 }
+                const int hl = h - 16 * hh;
+                st[warp][d][hl] = a1.x;
+                st[warp][d + 1][hl] = a1.y;
+                st[warp][kFt + d][hl] = a2.x;
+                st[warp][kFt + d + 1][hl] = a2.y;
             }
-            st[warp][d][h] = a1.x;
-            st[warp][d + 1][h] = a1.y;
-            st[warp][kFt + d][h] = a2.x;
-            st[warp][kFt + d + 1][h] = a2.y;
-        }
-        __syncwarp();
-        if (j < N)
+            __syncwarp();
+            const uint32_t jh = tile * 32 + 16 * hh + sub;
+            if (jh < N) {
+                float* X = H.acts + jh;
 #pragma unroll 8
-            for (int r = 0; r < 2 * kFt; ++r) X[(A_XT + 6 + r) * L] = st[warp][r][lane];
+                for (int r = 0; r < 2 * kFt; r += 2) X[(A_XT + 6 + r + rsel) * L] = st[warp][r + rsel][sub];
+            }
+        }
     }
 }
 
