@@ -101,6 +101,9 @@ static_assert(T_SM_TOTAL <= 232448 && C_SM_TOTAL <= 232448, "shared memory budge
 #define SVLF_DEC_C_PRODUCERS 8
 #endif
 constexpr uint32_t kProducers = SVLF_DEC_C_PRODUCERS;
+#ifndef SVLF_RING_SLEEP_NS
+#define SVLF_RING_SLEEP_NS 128  // f_C producers polling for a free ring entry
+#endif
 #ifndef SVLF_DEC_C_SMCHAINS
 #define SVLF_DEC_C_SMCHAINS 1
 #endif
@@ -806,7 +809,7 @@ __global__ void __launch_bounds__(kCtThreads, 1)
             const uint32_t t = tile_of(k);
             fetch(t, leaves[0], 0);
             if (use > 0)
-                while (ld_acquire(&empty[slot]) != k - kRing + 1) __nanosleep(32);
+                while (ld_acquire(&empty[slot]) != k - kRing + 1) __nanosleep(SVLF_RING_SLEEP_NS);
             const uint32_t a_base = ring0 + slot * CT_A_BYTES;
 #pragma unroll 1
             for (uint32_t g = 0; g < (SVLF_DEC_EXP == 1 ? 0 : 4); ++g) {
@@ -1041,7 +1044,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             if (j < n && SVLF_DEC_EXP != 3)
                 hit_geom_regs<kBF16>(T, rays, ray_i, leaf, tin, tout, r6p, wp, u, err);
             const uint32_t my_leaf = j < n ? leaf : 0u;
-            if (use > 0) mbar_wait(&empty[e], (use - 1) & 1);
+            if (use > 0) mbar_wait_sleep(&empty[e], (use - 1) & 1);
             const uint32_t a_base = sbase + TW_RING0 + e * TW_ENTRY;
             uint32_t* side = reinterpret_cast<uint32_t*>(sm + TW_RING0 + e * TW_ENTRY + T_A_BYTES);
 #pragma unroll 2

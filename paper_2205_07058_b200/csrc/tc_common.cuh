@@ -102,6 +102,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+#ifndef SVLF_MBAR_SLEEP_NS
+#define SVLF_MBAR_SLEEP_NS 20000
+#endif
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     asm volatile(
@@ -110,6 +114,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a),
         "r"(parity)
+        : "memory");
+}
+
+// mbar_wait for waiters that are usually early (producers waiting for a free
+// ring entry): try_wait with a suspend-time hint, so the waiting warp sleeps
+// instead of spinning on the issue port (ns; the phase completing wakes it)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a),
+        "r"(parity), "r"(SVLF_MBAR_SLEEP_NS)
         : "memory");
 }
 
