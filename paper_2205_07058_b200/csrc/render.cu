@@ -174,12 +174,17 @@ constexpr int kCompBlock = 256;
 __global__ void __launch_bounds__(kCompBlock) k_composite_warp(HitOut h, uint32_t n, PixelOut P,
                                                                unsigned long long* fg_count) {
     __shared__ float sums[kCompBlock / 32][32][5];
-    __shared__ uint32_t wfg[kCompBlock / 32];
+    __shared__ uint32_t s_fg, s_done;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        s_fg = 0;
+        s_done = 0;
+    }
+    __syncthreads();
     const uint32_t my = blockIdx.x * kCompBlock + threadIdx.x;
     const uint32_t cnt_l = my < n ? P.ray_cnt[my] : 0u, off_l = my < n ? P.ray_off[my] : 0u;
     const unsigned fg = __ballot_sync(0xffffffffu, cnt_l > 0);
-    if (lane == 0) wfg[warp] = __popc(fg);
+    if (lane == 0 && fg) atomicAdd(&s_fg, uint32_t(__popc(fg)));
     const uint32_t vi = (lane >> 2) & 7u;  // which of the ray's five sums this lane ends up holding
     unsigned todo = fg;
     while (todo) {
@@ -203,12 +208,13 @@ __global__ void __launch_bounds__(kCompBlock) k_composite_warp(HitOut h, uint32_
                                         sums[warp][lane][3], sums[warp][lane][4]};
         write_pixel(P, my, c);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-#pragma unroll
-        for (int w = 0; w < kCompBlock / 32; ++w) t += wfg[w];
-        if (t) atomicAdd(fg_count, (unsigned long long)t);
+    // the block's last warp to finish adds the block's foreground count (no block barrier at the end)
+    if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&s_done, 1u) == kCompBlock / 32 - 1) {
+            const uint32_t t = atomicAdd(&s_fg, 0u);
+            if (t) atomicAdd(fg_count, (unsigned long long)t);
+        }
     }
 }
 
