@@ -104,6 +104,9 @@ constexpr uint32_t kProducers = SVLF_DEC_C_PRODUCERS;
 #ifndef SVLF_RING_SLEEP_NS
 #define SVLF_RING_SLEEP_NS 128  // f_C producers polling for a free ring entry
 #endif
+#ifndef SVLF_DEC_EPI_PIPE
+#define SVLF_DEC_EPI_PIPE 1  // f_C TMEM chains: 16-column epilogue chunks with the next load in flight
+#endif
 #ifndef SVLF_DEC_C_SMCHAINS
 #define SVLF_DEC_C_SMCHAINS 1
 #endif
@@ -377,6 +380,32 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
         : "r"(taddr));
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 16 TMEM columns into registers, and the wait for them: the wait names the
+// destination registers as in-out operands so no use of them can be scheduled
+// before it (loads of the next chunk are then in flight while the current one
+// is converted)
+__device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
 }
 
 // Epilogue: TMEM acc (128 fp32, + optional fp32 bias) -> relu -> 16-bit -> A tile (K layout)
@@ -909,6 +938,23 @@ __global__ void __launch_bounds__(kCtThreads, 1)
                 tmem_st16(a_t + lane_off + 32 * hh, pk);
                 tmem_st16(a_t + lane_off + 32 * hh + 16, pk + 16);
             }
+#elif SVLF_DEC_EPI_PIPE
+            // 16-column chunks, the next chunk's load in flight while this one is packed
+            uint32_t ra[16], rb[16];
+            tmem_ld16u(acc + lane_off, ra);
+            tmem_wait_ld16(ra);
+#pragma unroll
+            for (uint32_t c = 0; c < 8; ++c) {
+                uint32_t(&cur)[16] = (c & 1) ? rb : ra;
+                uint32_t(&nxt)[16] = (c & 1) ? ra : rb;
+                if (c + 1 < 8) tmem_ld16u(acc + lane_off + 16 * (c + 1), nxt);
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    pk[i] = F::relu_pack(__uint_as_float(cur[2 * i]), __uint_as_float(cur[2 * i + 1]));
+                tmem_st8(a_t + lane_off + 8 * c, pk);
+                if (c + 1 < 8) tmem_wait_ld16(nxt);
+            }
 #else
 #pragma unroll 1
             for (uint32_t hh = 0; hh < 4; ++hh) {
@@ -1152,6 +1198,25 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             wait();
         }
         for (; tile_of(k) < ntiles; k += TW_CHAINS) {
+#if SVLF_DEC_EPI_PIPE
+            {  // acc -> relu -> 16-bit pairs -> A (TMEM), 16-column chunks, the next load in flight
+                uint32_t ra[16], rb[16];
+                tmem_ld16u(acc + lane_off, ra);
+                tmem_wait_ld16(ra);
+#pragma unroll
+                for (uint32_t c = 0; c < 8; ++c) {
+                    uint32_t(&cur)[16] = (c & 1) ? rb : ra;
+                    uint32_t(&nxt)[16] = (c & 1) ? ra : rb;
+                    if (c + 1 < 8) tmem_ld16u(acc + lane_off + 16 * (c + 1), nxt);
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        pk[i] = F::relu_pack(__uint_as_float(cur[2 * i]), __uint_as_float(cur[2 * i + 1]));
+                    tmem_st8(a_t + lane_off + 8 * c, pk);
+                    if (c + 1 < 8) tmem_wait_ld16(nxt);
+                }
+            }
+#else
 #pragma unroll 1
             for (uint32_t hh = 0; hh < 4; ++hh) {  // acc -> relu -> 16-bit pairs -> A (TMEM)
                 float v[32];
@@ -1162,6 +1227,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
                 for (int i = 0; i < 16; ++i) pk[i] = F::relu_pack(v[2 * i], v[2 * i + 1]);
                 tmem_st16(a_t + lane_off + 16 * hh, pk);
             }
+#endif
             tmem_wait_st();
             const uint32_t kn = k + TW_CHAINS;
             const bool next = tile_of(kn) < ntiles;
