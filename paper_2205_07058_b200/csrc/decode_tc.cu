@@ -413,6 +413,29 @@ template <bool kBF16, bool kBias>
 __device__ __forceinline__ void hidden_epilogue(uint32_t tmem_row, uint32_t a_base, uint32_t r, uint32_t K,
                                                 const float* bias) {
     using F = Fmt<kBF16>;
+    if constexpr (!kBias && SVLF_DEC_EPI_PIPE) {
+        // 16-column chunks, the next chunk's load in flight while this one is packed and stored
+        uint32_t ra[16], rb[16];
+        tmem_ld16u(tmem_row, ra);
+        tmem_wait_ld16(ra);
+#pragma unroll
+        for (uint32_t c = 0; c < 8; ++c) {
+            uint32_t(&cur)[16] = (c & 1) ? rb : ra;
+            uint32_t(&nxt)[16] = (c & 1) ? ra : rb;
+            if (c + 1 < 8) tmem_ld16u(tmem_row + 16 * (c + 1), nxt);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint32_t* w = cur + 8 * q;
+                st_shared_v4(a_base + a_off(r, 16 * c + 8 * q),
+                             F::relu_pack(__uint_as_float(w[0]), __uint_as_float(w[1])),
+                             F::relu_pack(__uint_as_float(w[2]), __uint_as_float(w[3])),
+                             F::relu_pack(__uint_as_float(w[4]), __uint_as_float(w[5])),
+                             F::relu_pack(__uint_as_float(w[6]), __uint_as_float(w[7])));
+            }
+            if (c + 1 < 8) tmem_wait_ld16(nxt);
+        }
+        return;
+    }
 #pragma unroll 1
     for (uint32_t c = 0; c < 4; ++c) {
         float v[32];
