@@ -1920,10 +1920,18 @@ svlf_status svlf_train_step_staged(svlf_ctx* ctx, svlf_model* m, int slot, svlf_
 
 svlf_status svlf_train_batch_discard(svlf_ctx* ctx, int slot) {
     return guard([&] {
-        svlf_ctx::TrainSlot& T = staged_slot(ctx, slot);
+        require(ctx, "null argument");
+        require(slot == 0 || slot == 1, "bad staging slot");
+        svlf_ctx::TrainSlot& T = ctx->tslot[slot];
+        require(T.staged, "no batch staged in this slot");
+        struct Release {
+            svlf_ctx::TrainSlot& t;
+            ~Release() { t.staged = false; }
+        } release{T};
+        if (T.job.valid()) T.job.wait();  // a failed host copy is dropped with the batch
+        T.job = {};
         DeviceGuard g(ctx->device);
         SVLF_CUDA(cudaEventSynchronize(T.copied));
-        T.staged = false;
     });
 }
 
