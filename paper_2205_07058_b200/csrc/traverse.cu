@@ -37,6 +37,9 @@ namespace svlfb {
 namespace {
 
 constexpr double kMinHitSpan = 1e-12;  // tie rule, src/octree.cpp:16
+#ifndef SVLF_BFS_PARTIAL
+#define SVLF_BFS_PARTIAL 1  // queue overflow hands only the rays reaching the overflowing chunk to the next pass
+#endif
 
 // Slab intervals of the two halves of a node along each axis.
 struct NodeSplit {
@@ -289,6 +292,7 @@ struct BfsSmem {
     uint32_t rcount[kR], roff[kR];
     uint32_t gray[kR];
     uint32_t n_q, base, overflow, next_tile;
+    uint32_t evict, cut;  // partial hand-over: rays leaving the tile, kept length of the next queue
     uint32_t wtot[2];             // per-warp totals of the two-warp (kT == 64) scan
     unsigned long long unsorted;  // rays whose segment needs the insertion sort
     struct NoScan {};
@@ -416,6 +420,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         }
     }
     static_assert(kR <= 64, "per-tile ray mask");
+    static_assert(kR <= 32 || !SVLF_BFS_PARTIAL, "partial hand-over: 32-bit ray mask");
     if (tid == 0) {
         S.n_q = 0;
         S.overflow = 0;
@@ -484,7 +489,33 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             uint32_t off, tot;
             tile_excl_sum<kT>(S, cnt, off, tot);
             if (n_out + tot > kQ) {
-                if (tid == 0) S.overflow = 1;
+                if (kCount || !SVLF_BFS_PARTIAL) {  // whole tile to the next pass (exact test counts)
+                    if (tid == 0) S.overflow = 1;
+                    tile_sync<kT>();
+                    break;
+                }
+                // Partial hand-over: the rays with pairs in this chunk or later leave the tile for
+                // the next pass (redone there from the root); the earlier rays, whose children are
+                // all in the next queue, continue here. The queues are grouped by ray in order, so
+                // the next queue is cut before the first child of the first leaving ray.
+                const uint32_t R = S.qray[cur][base];
+                if (tid == 0) {
+                    S.evict = 0;
+                    S.cut = n_out;
+                }
+                tile_sync<kT>();
+                for (uint32_t i = base + tid; i < n_cur; i += kT) atomicOr(&S.evict, 1u << S.qray[cur][i]);
+                for (uint32_t i = tid; i < n_out; i += kT)
+                    if (S.qray[cur ^ 1][i] == R && (i == 0 || S.qray[cur ^ 1][i - 1] != R)) S.cut = i;
+                tile_sync<kT>();
+                const uint32_t ev = S.evict;
+                if (tid == 0) S.base = atomicAdd(&A.counters[kList ? 3 : 1], uint32_t(__popc(ev)));
+                tile_sync<kT>();
+                if (tid < kR && ((ev >> tid) & 1u)) {
+                    (kList ? A.overflow_dense : A.overflow_rays)[S.base + __popc(ev & ((1u << tid) - 1u))] = S.gray[tid];
+                    S.gray[tid] = 0xffffffffu;  // not finalised by this pass
+                }
+                n_out = S.cut;
                 tile_sync<kT>();
                 break;
             }
