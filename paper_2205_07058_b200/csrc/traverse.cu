@@ -287,6 +287,7 @@ struct BfsSmem {
     uint64_t qxyz[2][kQ];
     uint32_t qnode[2][kQ];
     uint32_t pos[kQ];  // leaf level: output position of each pair's first hit
+    uint8_t kmask[kQ];  // leaf level: each pair's kept children (pass A -> pass B)
     uint8_t qray[2][kQ];
     uint8_t dflags[kR];  // per ray: direction sign bits (0-2) and zero-component bits (3-5)
     uint32_t rcount[kR], roff[kR];
@@ -567,7 +568,9 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 split_node_z(T, o, uint32_t(S.dflags[ri]) >> 3, inv, level, uint32_t(xyz & 0x1fffffu),
                              uint32_t((xyz >> 21) & 0x1fffffu), uint32_t(xyz >> 42), sp);
                 if constexpr (kCount) tests += __popc(node.y);
-                cnt = __popc(child_hits<true>(sp) & node.y & 0xffu);
+                const uint32_t keep = child_hits<true>(sp) & node.y & 0xffu;
+                S.kmask[e] = uint8_t(keep);
+                cnt = __popc(keep);
                 if (cnt) atomicAdd(&S.rcount[ri], cnt);
             }
             uint32_t off, tot;
@@ -593,6 +596,8 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     const bool fits = gbase + total <= A.capacity;
     if (leaf_pass && fits) {
         for (uint32_t e = tid; e < n_cur; e += kT) {
+            const uint32_t keep = S.kmask[e];  // pass A's kept children
+            if (!keep) continue;
             const uint32_t ri = S.qray[cur][e];
             const uint2 node = T.nodes[S.qnode[cur][e]];
             const uint64_t xyz = S.qxyz[cur][e];
@@ -609,7 +614,6 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             const uint32_t s = fl & 7u;
             uint32_t w = gbase + S.pos[e];
             const uint32_t gr = S.gray[ri];
-            const uint32_t keep = child_hits<true>(sp) & node.y & 0xffu;
             for (uint32_t todo = front_to_back(keep, s); todo; todo &= todo - 1) {
                 const uint32_t oct = uint32_t(__ffs(todo) - 1) ^ s;
                 double t0, t1;
