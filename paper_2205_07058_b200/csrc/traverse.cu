@@ -37,6 +37,9 @@ namespace svlfb {
 namespace {
 
 constexpr double kMinHitSpan = 1e-12;  // tie rule, src/octree.cpp:16
+#ifndef SVLF_BFS_W0
+#define SVLF_BFS_W0 1  // ray-indexed scans (root queue, segment offsets) as first-warp shuffle scans
+#endif
 #ifndef SVLF_BFS_PARTIAL
 #define SVLF_BFS_PARTIAL 1  // queue overflow hands only the rays reaching the overflowing chunk to the next pass
 #endif
@@ -294,6 +297,7 @@ struct BfsSmem {
     uint32_t gray[kR];
     uint32_t n_q, base, overflow, next_tile;
     uint32_t evict, cut;  // partial hand-over: rays leaving the tile, kept length of the next queue
+    uint32_t nlev[2];     // next-level pair counts of the first-warp levels (alternating by level)
     uint32_t wtot[2];             // per-warp totals of the two-warp (kT == 64) scan
     unsigned long long unsorted;  // rays whose segment needs the insertion sort
     struct NoScan {};
@@ -332,6 +336,20 @@ __device__ __forceinline__ void tile_sync() {
     } else {
         __syncthreads();
     }
+}
+
+// Exclusive sum over the 32 lanes of one warp (values of the tile's first warp
+// when only its lanes hold non-zero values: rays, or a level of <= 32 pairs)
+__device__ __forceinline__ void warp_excl_sum(uint32_t v, uint32_t& off, uint32_t& tot) {
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= uint32_t(d)) x += y;
+    }
+    tot = __shfl_sync(0xffffffffu, x, 31);
+    off = x - v;
 }
 
 // Exclusive sum over the tile. Every call site is followed by a tile_sync()
@@ -421,13 +439,14 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
         }
     }
     static_assert(kR <= 64, "per-tile ray mask");
+    static_assert(kR <= 32 || !SVLF_BFS_W0, "first-warp scans: at most 32 rays per tile");
     static_assert(kR <= 32 || !SVLF_BFS_PARTIAL, "partial hand-over: 32-bit ray mask");
     if (tid == 0) {
         S.n_q = 0;
         S.overflow = 0;
         S.unsorted = 0;
     }
-    tile_sync<kT>();
+    if (!SVLF_BFS_W0) tile_sync<kT>();  // (W0: every value read before the next barrier is the reader's own)
     {
         uint32_t hit = 0;
         if (my_ray != 0xffffffffu) {
@@ -445,14 +464,27 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             hit = slab_test(p, lo, hi, t0, t1) ? 1u : 0u;
             if constexpr (kCount) ++tests;
         }
-        uint32_t off, tot;
-        tile_excl_sum<kT>(S, hit, off, tot);
-        if (hit) {
-            S.qnode[0][off] = 0;
-            S.qxyz[0][off] = 0;
-            S.qray[0][off] = uint8_t(tid);
+        if (SVLF_BFS_W0 && kT > 32) {  // only the first warp holds rays: warp scan, one barrier
+            if (tid < 32) {
+                uint32_t off, tot;
+                warp_excl_sum(hit, off, tot);
+                if (hit) {
+                    S.qnode[0][off] = 0;
+                    S.qxyz[0][off] = 0;
+                    S.qray[0][off] = uint8_t(tid);
+                }
+                if (tid == 0) S.n_q = tot;
+            }
+        } else {
+            uint32_t off, tot;
+            tile_excl_sum<kT>(S, hit, off, tot);
+            if (hit) {
+                S.qnode[0][off] = 0;
+                S.qxyz[0][off] = 0;
+                S.qray[0][off] = uint8_t(tid);
+            }
+            if (tid == 0) S.n_q = tot;
         }
-        if (tid == 0) S.n_q = tot;
         tile_sync<kT>();
     }
 
@@ -462,6 +494,52 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     int level = 0;
     for (; level + 1 < T.L && n_cur > 0; ++level) {
         uint32_t n_out = 0;
+        if (SVLF_BFS_W0 && kT > 32 && n_cur <= 32) {
+            // the whole level in the first warp (at most 256 children: no overflow): warp scan,
+            // one barrier instead of three
+            static_assert(kQ >= 256, "a 32-pair level always fits the next queue");
+            if (tid < 32) {
+                uint32_t hitmask = 0, cnt = 0, ri = 0, x = 0, y = 0, z = 0, s = 0;
+                uint2 node = make_uint2(0, 0);
+                if (tid < n_cur) {
+                    ri = S.qray[cur][tid];
+                    node = T.nodes[S.qnode[cur][tid]];
+                    const uint64_t xyz = S.qxyz[cur][tid];
+                    x = uint32_t(xyz & 0x1fffffu);
+                    y = uint32_t((xyz >> 21) & 0x1fffffu);
+                    z = uint32_t(xyz >> 42);
+                    double o[3], inv[3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        o[a] = S.o[a][ri];
+                        inv[a] = S.inv[a][ri];
+                    }
+                    const uint32_t fl = S.dflags[ri];
+                    NodeSplit sp;
+                    split_node_z(T, o, fl >> 3, inv, level, x, y, z, sp);
+                    s = fl & 7u;
+                    if constexpr (kCount) tests += __popc(node.y);
+                    hitmask = child_hits<false>(sp) & node.y & 0xffu;
+                    cnt = __popc(hitmask);
+                }
+                uint32_t off, tot;
+                warp_excl_sum(cnt, off, tot);
+                uint32_t w = off;
+                for (uint32_t todo = front_to_back(hitmask, s); todo; todo &= todo - 1) {
+                    const uint32_t oct = uint32_t(__ffs(todo) - 1) ^ s;
+                    S.qnode[cur ^ 1][w] = node.x + __popc(node.y & ((1u << oct) - 1u));
+                    S.qxyz[cur ^ 1][w] =
+                        pack_xyz(2u * x + (oct & 1u), 2u * y + ((oct >> 1) & 1u), 2u * z + ((oct >> 2) & 1u));
+                    S.qray[cur ^ 1][w] = uint8_t(ri);
+                    ++w;
+                }
+                if (tid == 0) S.nlev[level & 1] = tot;
+            }
+            tile_sync<kT>();
+            n_cur = S.nlev[level & 1];  // (the next level writes the other slot)
+            cur ^= 1;
+            continue;
+        }
         for (uint32_t base = 0; base < n_cur; base += kT) {
             const uint32_t e = base + tid;
             uint32_t hitmask = 0, cnt = 0, ri = 0, x = 0, y = 0, z = 0, s = 0;
@@ -580,7 +658,20 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             tile_sync<kT>();
         }
     }
-    {
+    if (SVLF_BFS_W0 && kT > 32) {  // per-ray segment offsets: the rays are the first warp's lanes
+        if (tid < 32) {
+            const uint32_t c = tid < kR ? S.rcount[tid] : 0u;
+            uint32_t off, tot;
+            warp_excl_sum(c, off, tot);
+            if (tid < kR) S.roff[tid] = off;
+            if (tid == 0) {
+                const uint32_t b = tot ? atomicAdd(&A.counters[0], tot) : 0u;
+                S.base = b;
+                if (b + tot > A.capacity) atomicExch(&A.counters[2], 1u);
+            }
+        }
+        tile_sync<kT>();
+    } else {
         const uint32_t c = tid < kR ? S.rcount[tid] : 0u;
         uint32_t off, tot;
         tile_excl_sum<kT>(S, c, off, tot);
