@@ -192,8 +192,11 @@ constexpr uint32_t kNT = SVLF_GEMM_NT;                // max hits per tile (MMA 
 constexpr uint32_t kFB = kNT * kChunk * 4;             // B hi (or lo) tile
 constexpr uint32_t kFStage = 2 * kFA + 2 * kFB;
 constexpr uint32_t kFStages = SVLF_GEMM_FSTAGES;
-constexpr uint32_t kFThreads = 448;  // warp 0 TMA, 1 MMA, 2-9 split, 10-13 epilogue
-constexpr uint32_t kFSplitWarps = 8;
+#ifndef SVLF_FEAT_SPLIT_WARPS
+#define SVLF_FEAT_SPLIT_WARPS 8
+#endif
+constexpr uint32_t kFSplitWarps = SVLF_FEAT_SPLIT_WARPS;
+constexpr uint32_t kFThreads = 64 + 32 * kFSplitWarps + 128;  // warp 0 TMA, 1 MMA, split warps, 4 epilogue warps
 // epilogue staging: per epilogue warp two 32 x 32 fp32 boxes (128-byte swizzle), stored by TMA
 constexpr uint32_t kFEpi = 4 * 2 * 4096;
 constexpr uint32_t kFHeadW = kFStages * kFStage + kFEpi + 256;  // head weights: float2 {W0, W1} + float W2 per row
@@ -460,8 +463,11 @@ constexpr uint32_t kDA = 128 * 128;     // 16 KB
 constexpr uint32_t kDBMax = 144 * 128;  // 18 KB
 constexpr uint32_t kDStage = 2 * kDA + 2 * kDBMax;
 constexpr uint32_t kDStages = 3;
-constexpr uint32_t kDThreads = 320;  // warp 0 TMA, 1 MMA, 2-9 split (2-5 also the epilogue)
-constexpr uint32_t kDSplitWarps = 8;
+#ifndef SVLF_DW_SPLIT_WARPS
+#define SVLF_DW_SPLIT_WARPS 12  // measured: 8 -> 12 split warps, dW -1 %
+#endif
+constexpr uint32_t kDSplitWarps = SVLF_DW_SPLIT_WARPS;
+constexpr uint32_t kDThreads = 64 + 32 * kDSplitWarps;  // warp 0 TMA, 1 MMA, the rest split (2-5 also the epilogue)
 constexpr uint32_t kDSmem = kDStages * kDStage + 1024 + 256;
 
 template <bool kX3>
