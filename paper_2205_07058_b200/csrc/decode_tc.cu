@@ -386,6 +386,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 // destination registers as in-out operands so no use of them can be scheduled
 // before it (loads of the next chunk are then in flight while the current one
 // is converted)
+// 4 TMEM columns (the heads' outputs)
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -1028,8 +1038,8 @@ __global__ void __launch_bounds__(kCtThreads, 1)
             epilogue();
             sync_issue([&] { hidden(W3, KH, kIdescHead); });
             wait();
-            float hv[16];
-            tmem_ld16(acc + lane_off, hv);
+            float hv[4];  // rgb (columns 0..2)
+            tmem_ld4(acc + lane_off, hv);
             tmem_wait_ld();
             const uint32_t j = tile_of(k) * 128 + r;
             if (j < n) {
@@ -1270,8 +1280,8 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
                 if (next) layer0(kn);
             });
             wait();
-            float hv[16];
-            tmem_ld16(d_head + lane_off, hv);
+            float hv[4];  // tau, eta (columns 0, 1)
+            tmem_ld4(d_head + lane_off, hv);
             tmem_wait_ld();
             const uint32_t j = tile_of(k) * 128 + r;
             if (j < n) {
