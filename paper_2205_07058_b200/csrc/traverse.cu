@@ -51,6 +51,8 @@ struct NodeSplit {
 };
 
 // zmask bit a: the ray's direction component a is zero
+// kLoZero: the box origin is (+-0, +-0, +-0): lo + m * cell == m * cell bit for bit (m * cell >= +0)
+template <bool kLoZero = false>
 __device__ __forceinline__ void split_node_z(const DevOctree& T, const double* o, uint32_t zmask,
                                              const double* inv, int level, uint32_t x, uint32_t y, uint32_t z,
                                              NodeSplit& s) {
@@ -58,9 +60,11 @@ __device__ __forceinline__ void split_node_z(const DevOctree& T, const double* o
     const double cl = T.cell[level], ch = T.cell[level + 1];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const double plo = dadd(T.lo[a], dmul(double(c[a]), cl));
-        const double phi = dadd(T.lo[a], dmul(double(c[a] + 1u), cl));
-        const double pmid = dadd(T.lo[a], dmul(double(2u * c[a] + 1u), ch));
+        const double mlo = dmul(double(c[a]), cl), mhi = dmul(double(c[a] + 1u), cl);
+        const double mmid = dmul(double(2u * c[a] + 1u), ch);
+        const double plo = kLoZero ? mlo : dadd(T.lo[a], mlo);
+        const double phi = kLoZero ? mhi : dadd(T.lo[a], mhi);
+        const double pmid = kLoZero ? mmid : dadd(T.lo[a], mmid);
         if (!((zmask >> a) & 1u)) {
             const double tl = dmul(dsub(plo, o[a]), inv[a]);
             const double tm = dmul(dsub(pmid, o[a]), inv[a]);
@@ -389,7 +393,7 @@ struct TileShape {
     static constexpr int H = kR / W;
 };
 
-template <bool kCamera, int kR, int kQ, int kT, bool kList, bool kCount>
+template <bool kCamera, int kR, int kQ, int kT, bool kList, bool kCount, bool kLoZero>
 __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& cam, uint32_t row0, uint32_t rows,
                                          uint32_t n, const BfsArgs& A, BfsSmem<kR, kQ, kT>& S, uint32_t tile,
                                          uint32_t& tests_done) {
@@ -516,7 +520,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                     }
                     const uint32_t fl = S.dflags[ri];
                     NodeSplit sp;
-                    split_node_z(T, o, fl >> 3, inv, level, x, y, z, sp);
+                    split_node_z<kLoZero>(T, o, fl >> 3, inv, level, x, y, z, sp);
                     s = fl & 7u;
                     if constexpr (kCount) tests += __popc(node.y);
                     hitmask = child_hits<false>(sp) & node.y & 0xffu;
@@ -559,7 +563,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                 }
                 const uint32_t fl = S.dflags[ri];
                 NodeSplit sp;
-                split_node_z(T, o, fl >> 3, inv, level, x, y, z, sp);
+                split_node_z<kLoZero>(T, o, fl >> 3, inv, level, x, y, z, sp);
                 s = fl & 7u;
                 if constexpr (kCount) tests += __popc(node.y);
                 hitmask = child_hits<false>(sp) & node.y & 0xffu;
@@ -643,7 +647,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
                     inv[a] = S.inv[a][ri];
                 }
                 NodeSplit sp;
-                split_node_z(T, o, uint32_t(S.dflags[ri]) >> 3, inv, level, uint32_t(xyz & 0x1fffffu),
+                split_node_z<kLoZero>(T, o, uint32_t(S.dflags[ri]) >> 3, inv, level, uint32_t(xyz & 0x1fffffu),
                              uint32_t((xyz >> 21) & 0x1fffffu), uint32_t(xyz >> 42), sp);
                 if constexpr (kCount) tests += __popc(node.y);
                 const uint32_t keep = child_hits<true>(sp) & node.y & 0xffu;
@@ -700,7 +704,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
             }
             const uint32_t fl = S.dflags[ri];
             NodeSplit sp;
-            split_node_z(T, o, fl >> 3, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
+            split_node_z<kLoZero>(T, o, fl >> 3, inv, level, uint32_t(xyz & 0x1fffffu), uint32_t((xyz >> 21) & 0x1fffffu),
                          uint32_t(xyz >> 42), sp);
             const uint32_t s = fl & 7u;
             uint32_t w = gbase + S.pos[e];
@@ -777,7 +781,7 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
 #ifndef SVLF_BFS_MINB
 #define SVLF_BFS_MINB 8  // resident 128-thread blocks per SM (256-thread second pass: 4): at most 64 registers
 #endif
-template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList, bool kCount>
+template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList, bool kCount, bool kLoZero>
 __global__ void __launch_bounds__(kBlock, kBlock == 128 ? SVLF_BFS_MINB : (kBlock == 256 ? 4 : 1)) k_traverse_bfs(DevOctree T, DevCamera cam, uint32_t row0, uint32_t rows,
                                                          uint32_t n, uint32_t n_tiles, BfsArgs A) {
     extern __shared__ __align__(16) uint8_t bfs_smem[];
@@ -795,7 +799,7 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? SVLF_BFS_MINB : (kBloc
         tile_sync<kT>();
         const uint32_t tile = S.next_tile;
         if (tile >= tiles) break;
-        bfs_tile<kCamera, kR, kQ, kT, kList, kCount>(T, cam, row0, rows, n, A, S, tile, tests);
+        bfs_tile<kCamera, kR, kQ, kT, kList, kCount, kLoZero>(T, cam, row0, rows, n, A, S, tile, tests);
         tile_sync<kT>();
     }
     if constexpr (kCount) {
@@ -932,17 +936,20 @@ static int num_sms() {
 #endif
 constexpr int kBfsBlocksPerSm = SVLF_BFS_BLOCKS_PER_SM;
 
-template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList, bool kCount>
+// the octree box starts at the origin (the unit scene box): split planes without the origin add
+static bool box_origin_zero(const DevOctree& T) { return T.lo[0] == 0.0 && T.lo[1] == 0.0 && T.lo[2] == 0.0; }
+
+template <bool kCamera, int kR, int kQ, int kT, int kBlock, bool kList, bool kCount, bool kLoZero>
 static void set_bfs_attr() {
     static bool done = false;
     if (done) return;
-    SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kQ, kT, kBlock, kList, kCount>,
+    SVLF_CUDA(cudaFuncSetAttribute(k_traverse_bfs<kCamera, kR, kQ, kT, kBlock, kList, kCount, kLoZero>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(sizeof(BfsSmem<kR, kQ, kT>) * (kBlock / kT))));
     done = true;
 }
 
-template <bool kCount>
+template <bool kCount, bool kLoZero>
 static void launch_traverse_t(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
                               const TraverseOut& o, cudaStream_t s) {
     const BfsArgs A = bfs_args(o);
@@ -950,17 +957,17 @@ static void launch_traverse_t(const DevOctree& T, const DevCamera* cam, uint32_t
     const size_t smem = sizeof(BfsSmem<kRays, kQCap, kThreads>) * kGroups;
     const uint32_t cap_grid = uint32_t(num_sms() * kBfsBlocksPerSm);
     if (cam) {
-        set_bfs_attr<true, kRays, kQCap, kThreads, kBlockThreads, false, kCount>();
+        set_bfs_attr<true, kRays, kQCap, kThreads, kBlockThreads, false, kCount, kLoZero>();
         using TS = TileShape<kRays>;
         const uint32_t tiles = ((cam->width + TS::W - 1) / TS::W) * ((rows + TS::H - 1) / TS::H);
         const uint32_t blocks = std::min((tiles + kGroups - 1) / kGroups, cap_grid);
-        k_traverse_bfs<true, kRays, kQCap, kThreads, kBlockThreads, false, kCount><<<blocks, kBlockThreads, smem, s>>>(
+        k_traverse_bfs<true, kRays, kQCap, kThreads, kBlockThreads, false, kCount, kLoZero><<<blocks, kBlockThreads, smem, s>>>(
             T, *cam, row0, rows, n, tiles, A);
     } else {
-        set_bfs_attr<false, kRays, kQCap, kThreads, kBlockThreads, false, kCount>();
+        set_bfs_attr<false, kRays, kQCap, kThreads, kBlockThreads, false, kCount, kLoZero>();
         const uint32_t tiles = (n + kRays - 1) / kRays;
         const uint32_t blocks = std::min((tiles + kGroups - 1) / kGroups, cap_grid);
-        k_traverse_bfs<false, kRays, kQCap, kThreads, kBlockThreads, false, kCount><<<blocks, kBlockThreads, smem, s>>>(
+        k_traverse_bfs<false, kRays, kQCap, kThreads, kBlockThreads, false, kCount, kLoZero><<<blocks, kBlockThreads, smem, s>>>(
             T, DevCamera{}, 0, 0, n, tiles, A);
     }
 }
@@ -968,14 +975,17 @@ static void launch_traverse_t(const DevOctree& T, const DevCamera* cam, uint32_t
 void launch_traverse(const DevOctree& T, const DevCamera* cam, uint32_t row0, uint32_t rows, uint32_t n,
                      const TraverseOut& o, cudaStream_t s, bool count) {
     if (n == 0) return;
+    const bool lz = box_origin_zero(T);
     if (count)
-        launch_traverse_t<true>(T, cam, row0, rows, n, o, s);
+        lz ? launch_traverse_t<true, true>(T, cam, row0, rows, n, o, s)
+           : launch_traverse_t<true, false>(T, cam, row0, rows, n, o, s);
     else
-        launch_traverse_t<false>(T, cam, row0, rows, n, o, s);
+        lz ? launch_traverse_t<false, true>(T, cam, row0, rows, n, o, s)
+           : launch_traverse_t<false, false>(T, cam, row0, rows, n, o, s);
     note_launch();
 }
 
-template <bool kCount>
+template <bool kCount, bool kLoZero>
 static void launch_traverse_dense_t(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
                                     cudaStream_t s) {
     const BfsArgs A = bfs_args(o);
@@ -983,22 +993,24 @@ static void launch_traverse_dense_t(const DevOctree& T, const DevCamera* cam, ui
     const uint32_t per_sm = std::max<uint32_t>(1, uint32_t(200 * 1024 / sizeof(Sm)));
     const uint32_t grid = uint32_t(num_sms()) * per_sm;
     if (cam) {
-        set_bfs_attr<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>();
-        k_traverse_bfs<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>
+        set_bfs_attr<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount, kLoZero>();
+        k_traverse_bfs<true, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount, kLoZero>
             <<<grid, kThreadsDense, sizeof(Sm), s>>>(T, *cam, row0, 0, 0, 0, A);
     } else {
-        set_bfs_attr<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>();
-        k_traverse_bfs<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount>
+        set_bfs_attr<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount, kLoZero>();
+        k_traverse_bfs<false, kRaysDense, kQCapDense, kThreadsDense, kThreadsDense, true, kCount, kLoZero>
             <<<grid, kThreadsDense, sizeof(Sm), s>>>(T, DevCamera{}, 0, 0, 0, 0, A);
     }
 }
 
 void launch_traverse_dense(const DevOctree& T, const DevCamera* cam, uint32_t row0, const TraverseOut& o,
                            cudaStream_t s, bool count) {
+    const bool lz = box_origin_zero(T);
     if (count)
-        launch_traverse_dense_t<true>(T, cam, row0, o, s);
+        lz ? launch_traverse_dense_t<true, true>(T, cam, row0, o, s) : launch_traverse_dense_t<true, false>(T, cam, row0, o, s);
     else
-        launch_traverse_dense_t<false>(T, cam, row0, o, s);
+        lz ? launch_traverse_dense_t<false, true>(T, cam, row0, o, s)
+           : launch_traverse_dense_t<false, false>(T, cam, row0, o, s);
     note_launch();
 }
 
