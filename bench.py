@@ -811,7 +811,7 @@ def main():
         "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
-        "dtype": f"{precision} decoders (fp32 accumulate) / f64 geometry", "data": "synthetic",
+        "dtype": f"{precision} decoders (fp32 accumulate) / f64 traversal and hit geometry", "data": "synthetic",
         "config": {"workload": f"C2: RTMV-shaped {args.objects}-object scene (make_random_scene(7,{args.objects})), "
                                f"octree depth 8 (res 256, dilation 1) from 100 hemisphere 400^2 depth maps, "
                                f"one {W}x{H} frame per GPU per step, init_model seed 1",
