@@ -1140,6 +1140,10 @@ svlf_status svlf_traverse(svlf_ctx* ctx, const svlf_octree* tree, const double* 
         }
         SVLF_CUDA(cudaStreamSynchronize(s));
         for (size_t i = 0; i <= n; ++i) offsets[i] = off32[i];
+        ctx->last = svlf_timings{};  // the traversal's pass counts (diagnostics)
+        ctx->last.hits = tot;
+        ctx->last.overflow_rays = ctx->last_overflow_rays;
+        ctx->last.dense_rays = ctx->last_dense_rays;
         if (tot > capacity) fail(SVLF_ERR_CAPACITY, "hit capacity too small");
     });
 }

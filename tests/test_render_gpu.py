@@ -109,6 +109,10 @@ def test_traversal_many_hit_rays(ctx, oracle):
     got, want = tree.traverse(rays), oracle.traverse(otree, rays)
     assert np.diff(want[0]).max() > 100
     _assert_hits_equal(got, want)
+    # these rays overflow the first pass's queue: the partial hand-over (the rays reaching the
+    # overflowing chunk leave the tile) and the second cooperative pass took part
+    t = ctx.last_timings()
+    assert t["dense_rays"] > 0 and t["hits"] == want[1].size
 
 
 def test_render_c1_fp32(c1, oracle, ctx):
