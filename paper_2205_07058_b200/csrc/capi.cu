@@ -169,6 +169,17 @@ struct svlf_ctx {
     };
     FrameSlot slot[2];
     uint64_t next_frame = 1;
+    // device-buffer frame enqueued by svlf_render_frame_device_submit, not yet finished
+    struct DeviceFrame {
+        bool active = false;
+        svlf_model* m = nullptr;
+        svlf_camera cam{};
+        float bg[3] = {0, 0, 0};
+        bool has_bg = false;
+        svlf_precision prec = SVLF_PRECISION_FP32;
+        float *rgb = nullptr, *alpha = nullptr, *depth = nullptr;
+        uint32_t n = 0;
+    } dev_frame;
     cudaStream_t copy_stream = nullptr;
     std::unique_ptr<HostPool> pool;
     svlf_timings last{};
@@ -300,6 +311,9 @@ void check_device_error(svlf_ctx* ctx, bool discard = false) {
 
 // misc buffer layout: [0] int error flag, [8] u64 fg counter, [16] u64 aux
 void reset_misc(svlf_ctx* ctx) {
+    if (ctx->dev_frame.active)
+        fail(SVLF_ERR_INVALID_ARGUMENT, "a frame from svlf_render_frame_device_submit is pending on this context: "
+                                        "call svlf_render_frame_device_finish first");
     ctx->misc.ensure<unsigned long long>(8);
     SVLF_CUDA(cudaMemsetAsync(ctx->misc.p, 0, 64, ctx->stream));
 }
@@ -1325,6 +1339,56 @@ svlf_status svlf_render_frame_device(svlf_ctx* ctx, svlf_model* m, const svlf_ca
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
         render_device(ctx, m, cam, 0, cam->height, bg, prec, d_rgb, d_alpha, d_depth, stats);
+    });
+}
+
+// Two-phase svlf_render_frame_device: the submit enqueues the frame (16-bit
+// modes: no host round trip; fp32 reads the hit count) and returns; the
+// finish synchronizes, checks the counters and the error flag, fills the
+// statistics and re-renders the frame synchronously if the hit buffers
+// overflowed. Used to time the frame on the device without the host's
+// synchronisation in the timed region.
+svlf_status svlf_render_frame_device_submit(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, const float* bg,
+                                            svlf_precision prec, float* d_rgb, float* d_alpha, float* d_depth) {
+    return guard([&] {
+        require(ctx && m && cam && d_rgb && d_alpha && d_depth, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (cam->width == 0 || cam->height == 0) fail(SVLF_ERR_INVALID_ARGUMENT, "zero-size image");
+        const uint64_t n64 = uint64_t(cam->width) * cam->height;
+        require(n64 < (1ull << 31), "too many pixels in one call");
+        const uint32_t n = uint32_t(n64);
+        const DevCamera dc = to_dev_camera(*cam);
+        reset_misc(ctx);  // fails while a submitted frame is pending
+        uint32_t total = 0;
+        if (prec == SVLF_PRECISION_FP32) total = run_traversal(ctx, m->tree, &dc, 0, cam->height, n);
+        else enqueue_traversal(ctx, m->tree, &dc, 0, cam->height, n);
+        run_decode_composite(ctx, m, n, total, bg, prec, d_rgb, d_alpha, d_depth);
+        auto& D = ctx->dev_frame;
+        D.m = m;
+        D.cam = *cam;
+        D.has_bg = bg != nullptr;
+        if (bg) std::copy(bg, bg + 3, D.bg);
+        D.prec = prec;
+        D.rgb = d_rgb;
+        D.alpha = d_alpha;
+        D.depth = d_depth;
+        D.n = n;
+        D.active = true;
+    });
+}
+
+svlf_status svlf_render_frame_device_finish(svlf_ctx* ctx, svlf_render_stats* stats) {
+    return guard([&] {
+        require(ctx != nullptr, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        auto& D = ctx->dev_frame;
+        require(D.active, "no frame from svlf_render_frame_device_submit is pending");
+        D.active = false;
+        if (finish_render(ctx, D.n, stats)) return;
+        render_device(ctx, D.m, &D.cam, 0, D.cam.height, D.has_bg ? D.bg : nullptr, D.prec, D.rgb, D.alpha,
+                      D.depth, stats);
     });
 }
 

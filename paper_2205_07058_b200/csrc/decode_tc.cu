@@ -107,10 +107,31 @@ constexpr uint32_t kProducers = SVLF_DEC_C_PRODUCERS;
 #ifndef SVLF_DEC_EPI_PIPE
 #define SVLF_DEC_EPI_PIPE 1  // f_C TMEM chains: 16-column epilogue chunks with the next load in flight
 #endif
+#ifndef SVLF_DEC_C_PUNROLL
+#define SVLF_DEC_C_PUNROLL 2  // f_C producer: gather passes unrolled (loads in flight per warp)
+#endif
+#ifndef SVLF_DEC_TRACE
+#define SVLF_DEC_TRACE 0
+#endif
+#if SVLF_DEC_TRACE
+// timing probe (diagnostics build only): clock64 stamps of chains 0 and 2 of CTA 0, 10 per tile
+__device__ unsigned long long g_dec_trace[3][64][10];
+#define DEC_STAMP(i)                                                                     \
+    do {                                                                                 \
+        if (blockIdx.x == 0 && r == 0 && k / kChains < 64) g_dec_trace[chain][k / kChains][i] = clock64(); \
+    } while (0)
+#else
+#define DEC_STAMP(i) \
+    do {             \
+    } while (0)
+#endif
 #ifndef SVLF_DEC_C_SMCHAINS
 #define SVLF_DEC_C_SMCHAINS 1
 #endif
-constexpr uint32_t kChainsTm = 2;                      // chains with A in TMEM (192 columns each)
+#ifndef SVLF_DEC_C_TMCHAINS
+#define SVLF_DEC_C_TMCHAINS 2
+#endif
+constexpr uint32_t kChainsTm = SVLF_DEC_C_TMCHAINS;    // chains with A in TMEM (192 columns each)
 constexpr uint32_t kChainsSm = SVLF_DEC_C_SMCHAINS;    // chains with A in shared memory (128 columns)
 constexpr uint32_t kChains = kChainsTm + kChainsSm;
 #ifndef SVLF_DEC_C_RING
@@ -885,7 +906,15 @@ __global__ void __launch_bounds__(kCtThreads, 1)
                     fetch_leaves(tile_of(k + kProducers));
                 }
                 const uint32_t wsp[4] = {g1.x, g1.y, g1.z, g1.w};
+#if SVLF_DEC_C_PUNROLL == 4
+#pragma unroll 4
+#elif SVLF_DEC_C_PUNROLL == 8
+#pragma unroll 8
+#elif SVLF_DEC_C_PUNROLL == 1
+#pragma unroll 1
+#else
 #pragma unroll 2
+#endif
                 for (uint32_t p = 0; p < 8; ++p) {
                     const uint32_t src = 4 * p + hsub;
                     const uint32_t lf = __shfl_sync(0xffffffffu, lf_cur, src);
@@ -1010,9 +1039,11 @@ __global__ void __launch_bounds__(kCtThreads, 1)
         };
         for (uint32_t k = chain; tile_of(k) < ntiles; k += kChains) {
             const uint32_t slot = k % kRing, use = k / kRing;
+            DEC_STAMP(0);
             if (r == 0)
                 while (ld_acquire(&full[slot]) != k + 1) {
                 }
+            DEC_STAMP(1);
             if (SVLF_DEC_EXP == 2) {
                 named_sync(bar_id, 128);
                 if (r == 0) st_release(&empty[slot], k + 1);
@@ -1022,31 +1053,41 @@ __global__ void __launch_bounds__(kCtThreads, 1)
                 issue_layer(acc, ring0 + slot * CT_A_BYTES, sbase + W0, KC, kIdesc);
             });
             wait();
+            DEC_STAMP(2);
             if (r == 0) st_release(&empty[slot], k + 1);  // the input tile is free once layer 0 completed
             epilogue();
+            DEC_STAMP(3);
             sync_issue([&] {
                 hidden(W1, KH, kIdesc);
                 mma_f16(acc, ones, make_desc(sbase + WB1, 128, 256), kIdesc, true);
             });
             wait();
+            DEC_STAMP(4);
             epilogue();
+            DEC_STAMP(5);
             sync_issue([&] {
                 hidden(W2, KH, kIdesc);
                 mma_f16(acc, ones, make_desc(sbase + WB2, 128, 256), kIdesc, true);
             });
             wait();
+            DEC_STAMP(6);
             epilogue();
+            DEC_STAMP(7);
+            float hv[4];  // rgb (columns 0..2)
+            if (SVLF_DEC_EXP != 5) {
             sync_issue([&] { hidden(W3, KH, kIdescHead); });
             wait();
-            float hv[4];  // rgb (columns 0..2)
+            DEC_STAMP(8);
             tmem_ld4(acc + lane_off, hv);
             tmem_wait_ld();
+            } else { named_sync(bar_id, 128); hv[0]=hv[1]=hv[2]=0.f; }
             const uint32_t j = tile_of(k) * 128 + r;
             if (j < n) {
 #pragma unroll
                 for (int cc = 0; cc < 3; ++cc)
                     out.rgb[3 * size_t(j) + cc] = __fdividef(1.0f, 1.0f + __expf(-(hv[cc] + cvec[256 + cc])));
             }
+            DEC_STAMP(9);
         }
     }
     kernel_teardown(tmem);
@@ -1276,7 +1317,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
                 read_side(kn % TW_ENTRIES);
             }
             sync_issue([&] {
-                issue_layer_ta(d_head, a_t, sbase + OFF_WT1, KT, kIdescHead);
+                if (SVLF_DEC_EXP != 6) issue_layer_ta(d_head, a_t, sbase + OFF_WT1, KT, kIdescHead);
                 if (next) layer0(kn);
             });
             wait();
@@ -1392,6 +1433,12 @@ static void decode_tc_impl(const DevOctree& T, const DevModel& M, const uint8_t*
 #endif
     note_launch(2);
 }
+
+#if SVLF_DEC_TRACE
+extern "C" int svlf_debug_dec_trace(unsigned long long* out) {  // 3 x 64 x 10 stamps
+    return int(cudaMemcpyFromSymbol(out, g_dec_trace, sizeof(g_dec_trace)));
+}
+#endif
 
 void launch_decode_tc(const DevOctree& T, const DevModel& M, const char* pack, bool bf16, const double* rays,
                       const uint32_t* hit_ray, const uint32_t* hit_leaf, const double* hit_tin,

@@ -231,6 +231,54 @@ def test_render_hit_buffer_overflow_retry(oracle, precision):
         c.close()
 
 
+@pytest.mark.parametrize("precision", ["fp16", "bf16", "fp32"])
+def test_device_frame_submit_finish(precision):
+    """svlf_render_frame_device_submit / _finish give the bits and RenderStats of
+    svlf_render_frame_device, including a first frame that overflows a fresh context's hit
+    buffers (the finish re-renders it); while a frame is pending the context refuses other
+    work, and a finish without a submit is an error."""
+    import torch
+
+    pts = S.random_occupancy_points(32, 0.3, 5)
+    W = 448
+    cam = S.lookat_camera((0.5 + 1.8 * 0.6, 0.5 + 1.8 * 0.3, 0.5 + 1.8 * 0.7416), (0.5, 0.5, 0.5), W, W, 1.2 * W)
+    camera = P.Camera.from_record(cam, W, W)
+    bg = np.array([0.25, 0.5, 0.75], np.float32)
+    n = W * W
+
+    def bufs():
+        return (torch.full((n * 3,), -1.0, device="cuda"), torch.full((n,), -1.0, device="cuda"),
+                torch.full((n,), -1.0, device="cuda"))
+
+    c = P.Context(0)
+    tree = P.SparseOctree.build(pts, P.GridConfig(32, dilation=0), c)
+    model = P.Model(tree, seed=2, ctx=c)
+    got, gst = [], []
+    for _ in range(2):  # the first submit overflows the initial hit capacity (> 1M hits)
+        b, st = bufs(), P.RenderStats()
+        P.render_frame_device_submit(model, camera, *(x.data_ptr() for x in b), background=bg,
+                                     precision=precision)
+        if not gst:
+            with pytest.raises(Exception, match="pending"):
+                P.render_frame_device(model, camera, *(x.data_ptr() for x in b), precision=precision)
+        P.render_frame_device_finish(c, st)
+        got.append(b)
+        gst.append(st)
+    with pytest.raises(Exception, match="no frame"):
+        P.render_frame_device_finish(c)
+    ref, rst = bufs(), P.RenderStats()
+    P.render_frame_device(model, camera, *(x.data_ptr() for x in ref), stats=rst, background=bg,
+                          precision=precision)
+    torch.cuda.synchronize()
+    assert rst.traversal_hits > (1 << 20)
+    for b, st in zip(got, gst):
+        for x, y in zip(b, ref):
+            assert torch.equal(x, y)
+        for f in ("rays", "rays_with_hits", "traversal_hits", "thickness_queries", "color_queries"):
+            assert getattr(st, f) == getattr(rst, f)
+    c.close()
+
+
 def test_host_frame_paths_agree(ctx, oracle):
     """svlf_render_frame delivers the same bits through every host path: fresh pageable
     arrays (pinned staging + parallel copies), reused pageable buffers, and page-locked
