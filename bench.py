@@ -32,6 +32,14 @@ FLOP_PER_HIT = 110_848  # f_T 17,408 MAC + f_C 38,016 MAC, x2
 BYTES_PER_RAY_OUT = 20  # rgb 12 + alpha 4 + depth 4
 
 
+def sparse_d2h_bytes(n, fg):
+    """Host-link bytes of one sparse host frame (capi.cu frame_submit): the block table
+    (36 B per 256 pixels), the foreground pixels copied by the submit (the previous frame's
+    count + 1/8 + 1024, 20 B each) and the counters."""
+    fg = int(fg)
+    return 36 * ((n + 255) // 256) + 20 * min(n, fg + fg // 8 + 1024) + 4 * 44
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -834,9 +842,14 @@ def main():
                      "algorithmic": f"{FLOP_PER_HIT} FLOP/hit x {int(hits)} hits per launch"},
         "stage_rooflines": stage_rooflines(stage, hits, n, peaks, node_tests),
         "e2e": {"value": round(e2e_value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": camera_bytes,
-                "d2h_bytes_per_step": n * BYTES_PER_RAY_OUT, "ms_per_step": round(e2e_step, 4),
+                "d2h_bytes_per_step": sparse_d2h_bytes(n, stats.rays_with_hits / args.steps),
+                "d2h_dense_bytes_per_step": n * BYTES_PER_RAY_OUT, "ms_per_step": round(e2e_step, 4),
                 "loops_ms_per_frame": [round(x, 4) for x in pipe_ms], "frames_per_loop": k_e2e,
                 "mode": "pipelined: render_frame_submit/wait, two frames in flight, page-locked outputs",
+                "transfer": "sparse: the foreground pixels (rays with hits, 20 B each, copied up to the previous "
+                            "frame's count + 1/8) and a 36-byte mask/base row per 256 pixels cross the host link; "
+                            "the host fills the background pixels (all host threads); the full frame lands in "
+                            "the caller's buffers, bit-identical to the device frame",
                 "l2": "no flush in this loop: each frame streams the 16-bit per-leaf feature tables and its hit "
                       "lists, both larger than the L2",
                 "l2_flushed": {"value": round(world * n / (e2e_flush_step * 1e-3) / 1e6, 3),

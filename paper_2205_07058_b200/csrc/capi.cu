@@ -151,8 +151,13 @@ struct svlf_ctx {
     static constexpr int kMaxBands = 8;
     struct FrameSlot {
         DevBuf rgb, alpha, depth, ctr;  // device outputs; per-band counters + misc snapshot
-        float* h_stage = nullptr;
+        DevBuf pk_vals, pk_tab;         // sparse transfer: foreground pixels, per-block masks/bases
+        float* h_stage = nullptr;       // dense: the frame; sparse: the foreground pixels (5 floats each)
         size_t h_stage_floats = 0;
+        uint32_t* h_tab = nullptr;  // sparse: the block table, page-locked
+        size_t h_tab_words = 0;
+        bool sparse = false;
+        uint32_t pk_copied[kMaxBands] = {};  // foreground pixels per band copied by the submit
         uint32_t* h_ctr = nullptr;  // pinned mailbox: band counters, error flag, fg count
         cudaEvent_t band_done[kMaxBands] = {}, band_copied[kMaxBands] = {};
         bool busy = false;
@@ -169,6 +174,7 @@ struct svlf_ctx {
     };
     FrameSlot slot[2];
     uint64_t next_frame = 1;
+    uint32_t pk_hint[kMaxBands] = {};  // sparse transfer: foreground pixels per band of the last frame
     // device-buffer frame enqueued by svlf_render_frame_device_submit, not yet finished
     struct DeviceFrame {
         bool active = false;
@@ -531,6 +537,25 @@ void render_device(svlf_ctx* ctx, svlf_model* m, const svlf_camera* cam, uint32_
 // on the partial hit lists are discarded).
 using FrameSlot = svlf_ctx::FrameSlot;
 
+// Frame counters (FrameSlot::ctr / h_ctr): 4 traversal counters per band, the
+// misc snapshot (error flag, foreground count), foreground pixels per band.
+constexpr uint32_t kCtrMisc = 4 * svlf_ctx::kMaxBands, kCtrPack = kCtrMisc + 4,
+                   kCtrWords = kCtrPack + svlf_ctx::kMaxBands;
+
+// Host frames move only the foreground pixels over the host link (rays with
+// hits: ~10 % of a C2 frame) plus a 36-byte table row per 256 pixels, and the
+// host fills the background pixels ((bg, 0, 0) exactly, as the composite
+// writes them). A dense 51 MB device-to-host copy per C2 frame otherwise runs
+// beside the next frame's kernels and slows them (measured: +0.12 ms per
+// frame). $SVLF_SPARSE_FRAMES=0: dense copies.
+bool sparse_frames() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVLF_SPARSE_FRAMES");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool is_pinned(const void* ptr) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
@@ -547,7 +572,8 @@ void frame_submit(svlf_ctx* ctx, FrameSlot& F, uint32_t bands) {
     float* d_rgb = F.rgb.ensure<float>(size_t(n) * 3);
     float* d_alpha = F.alpha.ensure<float>(n);
     float* d_depth = F.depth.ensure<float>(n);
-    if (!F.direct && F.h_stage_floats < size_t(n) * 5) {
+    F.sparse = sparse_frames();
+    if ((!F.direct || F.sparse) && F.h_stage_floats < size_t(n) * 5) {
         if (F.h_stage) SVLF_CUDA(cudaFreeHost(F.h_stage));
         F.h_stage = nullptr;
         SVLF_CUDA(cudaMallocHost(&F.h_stage, size_t(n) * 5 * sizeof(float)));
@@ -558,10 +584,26 @@ void frame_submit(svlf_ctx* ctx, FrameSlot& F, uint32_t bands) {
     float* st_depth = F.direct ? F.u_depth : st_alpha + n;
     bands = std::max<uint32_t>(1, std::min<uint32_t>({bands, uint32_t(svlf_ctx::kMaxBands), H}));
     F.band_rows = (H + bands - 1) / bands;
-    uint32_t* ctr = F.ctr.ensure<uint32_t>(4 * svlf_ctx::kMaxBands + 8);
+    uint32_t* ctr = F.ctr.ensure<uint32_t>(kCtrWords);
     const float* bg = F.has_bg ? F.bg : nullptr;
+    float* pk_vals = nullptr;
+    uint32_t* pk_tab = nullptr;
+    if (F.sparse) {
+        const size_t tab_words = 9 * (size_t(n) / kPackBlock + svlf_ctx::kMaxBands + 1);
+        pk_vals = F.pk_vals.ensure<float>(size_t(n) * 5);
+        pk_tab = F.pk_tab.ensure<uint32_t>(tab_words);
+        if (F.h_tab_words < tab_words) {
+            if (F.h_tab) SVLF_CUDA(cudaFreeHost(F.h_tab));
+            F.h_tab = nullptr;
+            F.h_tab_words = 0;
+            SVLF_CUDA(cudaMallocHost(&F.h_tab, tab_words * 4));
+            F.h_tab_words = tab_words;
+        }
+    }
     reset_misc(ctx);
+    if (F.sparse) SVLF_CUDA(cudaMemsetAsync(ctr + kCtrPack, 0, 4 * svlf_ctx::kMaxBands, s));
     uint32_t nb = 0;
+    size_t tb = 0;  // sparse: table rows of the earlier bands
     for (uint32_t r0 = 0; r0 < H; r0 += F.band_rows, ++nb) {
         const uint32_t rows = std::min(F.band_rows, H - r0);
         const size_t off = size_t(r0) * W, cnt = size_t(rows) * W;
@@ -573,32 +615,98 @@ void frame_submit(svlf_ctx* ctx, FrameSlot& F, uint32_t bands) {
         SVLF_CUDA(cudaMemcpyAsync(ctr + 4 * nb, traversal_counters(ctx), 16, cudaMemcpyDeviceToDevice, s));
         if (r0 + F.band_rows >= H)  // last band: snapshot of the error flag and the foreground count
             SVLF_CUDA(cudaMemcpyAsync(ctr + 4 * svlf_ctx::kMaxBands, ctx->misc.p, 16, cudaMemcpyDeviceToDevice, s));
+        const size_t rows_tab = (cnt + kPackBlock - 1) / kPackBlock;
+        if (F.sparse)
+            launch_pack_fg(ctx->counts.as<uint32_t>(), uint32_t(cnt), d_rgb + off * 3, d_alpha + off, d_depth + off,
+                           pk_vals + 5 * off, pk_tab + 9 * tb, ctr + kCtrPack + nb, s);
         SVLF_CUDA(cudaEventRecord(F.band_done[nb], s));
         SVLF_CUDA(cudaStreamWaitEvent(c, F.band_done[nb], 0));
-        SVLF_CUDA(cudaMemcpyAsync(st_rgb + off * 3, d_rgb + off * 3, cnt * 12, cudaMemcpyDeviceToHost, c));
-        SVLF_CUDA(cudaMemcpyAsync(st_alpha + off, d_alpha + off, cnt * 4, cudaMemcpyDeviceToHost, c));
-        SVLF_CUDA(cudaMemcpyAsync(st_depth + off, d_depth + off, cnt * 4, cudaMemcpyDeviceToHost, c));
+        if (F.sparse) {
+            // the table, and as many foreground pixels as the last frame's band had (+1/8);
+            // the completion copies any excess
+            const uint32_t hint = ctx->pk_hint[nb];
+            const uint32_t est = uint32_t(std::min<size_t>(cnt, hint ? hint : cnt / 8 + 1024));
+            F.pk_copied[nb] = est;
+            SVLF_CUDA(cudaMemcpyAsync(F.h_ctr + kCtrPack + nb, ctr + kCtrPack + nb, 4, cudaMemcpyDeviceToHost, c));
+            SVLF_CUDA(cudaMemcpyAsync(F.h_tab + 9 * tb, pk_tab + 9 * tb, rows_tab * 36, cudaMemcpyDeviceToHost, c));
+            if (est)
+                SVLF_CUDA(cudaMemcpyAsync(F.h_stage + 5 * off, pk_vals + 5 * off, size_t(est) * 20,
+                                          cudaMemcpyDeviceToHost, c));
+        } else {
+            SVLF_CUDA(cudaMemcpyAsync(st_rgb + off * 3, d_rgb + off * 3, cnt * 12, cudaMemcpyDeviceToHost, c));
+            SVLF_CUDA(cudaMemcpyAsync(st_alpha + off, d_alpha + off, cnt * 4, cudaMemcpyDeviceToHost, c));
+            SVLF_CUDA(cudaMemcpyAsync(st_depth + off, d_depth + off, cnt * 4, cudaMemcpyDeviceToHost, c));
+        }
+        tb += rows_tab;
         if (r0 + F.band_rows >= H)
-            SVLF_CUDA(cudaMemcpyAsync(F.h_ctr, ctr, 4 * (4 * svlf_ctx::kMaxBands + 4), cudaMemcpyDeviceToHost, c));
+            SVLF_CUDA(cudaMemcpyAsync(F.h_ctr, ctr, 4 * kCtrWords, cudaMemcpyDeviceToHost, c));
         SVLF_CUDA(cudaEventRecord(F.band_copied[nb], c));
     }
     F.nb = nb;
 }
 
+// Sparse transfer, host side, one band (as soon as its copies landed, while
+// later bands render): copies the foreground pixels the submit did not (more
+// than the estimate), then writes the band into the caller's buffers from the
+// block table: foreground pixels from the packed values, background pixels
+// (bg, 0, 0); the thread pool takes 64 table rows (16 K pixels) per task.
+void frame_expand_band(svlf_ctx* ctx, FrameSlot& F, uint32_t b) {
+    const uint32_t W = F.cam.width, H = F.cam.height;
+    const size_t off = size_t(b) * F.band_rows * W, cnt = size_t(std::min(F.band_rows, H - b * F.band_rows)) * W;
+    const size_t tab0 = size_t(b) * ((size_t(F.band_rows) * W + kPackBlock - 1) / kPackBlock);  // earlier bands' rows
+    const size_t rows = (cnt + kPackBlock - 1) / kPackBlock;
+    const uint32_t fg = F.h_ctr[kCtrPack + b];
+    if (fg > F.pk_copied[b]) {
+        // (blocking copy: the band's values are complete; the copy stream may already hold
+        // later bands' copies waiting for their kernels)
+        SVLF_CUDA(cudaMemcpy(F.h_stage + 5 * (off + F.pk_copied[b]), F.pk_vals.as<float>() + 5 * (off + F.pk_copied[b]),
+                             size_t(fg - F.pk_copied[b]) * 20, cudaMemcpyDeviceToHost));
+    }
+    ctx->pk_hint[b] = uint32_t(std::min<size_t>(cnt, size_t(fg) + fg / 8 + 1024));
+    float bg_row[3 * kPackBlock];  // a table row's worth of background rgb
+    for (uint32_t i = 0; i < kPackBlock; ++i)
+        for (int c = 0; c < 3; ++c) bg_row[3 * i + c] = F.bg[c];
+    constexpr size_t kRows = 64;  // table rows per task
+    ctx->pool->parallel_for(int((rows + kRows - 1) / kRows), [&](int t) {
+        for (size_t r = size_t(t) * kRows; r < std::min(rows, size_t(t + 1) * kRows); ++r) {
+            const uint32_t* row = F.h_tab + 9 * (tab0 + r);
+            const size_t p0 = off + r * kPackBlock, pe = std::min(off + cnt, p0 + kPackBlock);
+            const float* v = F.h_stage + 5 * (off + row[8]);
+            // background everywhere (streaming fills), then the foreground pixels over it
+            std::memcpy(F.u_rgb + 3 * p0, bg_row, (pe - p0) * 12);
+            std::memset(F.u_alpha + p0, 0, (pe - p0) * 4);
+            std::memset(F.u_depth + p0, 0, (pe - p0) * 4);
+            for (uint32_t w = 0; w < kPackBlock / 32; ++w)
+                for (uint32_t m = row[w]; m; m &= m - 1) {
+                    const size_t p = p0 + 32 * w + uint32_t(__builtin_ctz(m));
+                    F.u_rgb[3 * p] = v[0];
+                    F.u_rgb[3 * p + 1] = v[1];
+                    F.u_rgb[3 * p + 2] = v[2];
+                    F.u_alpha[p] = v[3];
+                    F.u_depth[p] = v[4];
+                    v += 5;
+                }
+        }
+    });
+}
+
 // Returns false when the frame has to be redone (hit buffers overflowed).
 bool frame_complete(svlf_ctx* ctx, FrameSlot& F, svlf_render_stats* stats) {
     const uint32_t W = F.cam.width, H = F.cam.height, n = F.n;
-    if (!F.direct && !ctx->pool) {
+    if ((!F.direct || F.sparse) && !ctx->pool) {
         const char* e = std::getenv("SVLF_COPY_THREADS");
         const int hw = int(std::thread::hardware_concurrency());
-        ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
+        // all host threads: the sparse expansion writes the whole frame (51 MB on C2) while the
+        // GPU renders the next one (8 threads: 0.70 ms per C2 frame, 16: 0.43 ms)
+        ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 15));
     }
     const float* st_rgb = F.h_stage;
     const float* st_alpha = st_rgb + size_t(n) * 3;
     const float* st_depth = st_alpha + n;
     for (uint32_t b = 0; b < F.nb; ++b) {
         SVLF_CUDA(cudaEventSynchronize(F.band_copied[b]));
-        if (F.direct) continue;
+        if (F.sparse) frame_expand_band(ctx, F, b);
+        if (F.direct || F.sparse) continue;
         const size_t off = size_t(b) * F.band_rows * W;
         const size_t cnt = size_t(std::min(F.band_rows, H - b * F.band_rows)) * W;
         constexpr size_t kPart = 64 * 1024;  // pixels per host copy task
@@ -620,7 +728,7 @@ bool frame_complete(svlf_ctx* ctx, FrameSlot& F, svlf_render_stats* stats) {
         fallback += c[3];
         worst = std::max<uint64_t>(worst, c[0]);
     }
-    const uint32_t* snap = F.h_ctr + 4 * svlf_ctx::kMaxBands;
+    const uint32_t* snap = F.h_ctr + kCtrMisc;
     const int err = int(snap[0]);
     unsigned long long fg = 0;
     std::memcpy(&fg, snap + 2, 8);
@@ -742,7 +850,7 @@ svlf_status svlf_ctx_create(int device, svlf_ctx** out) {
                 SVLF_CUDA(cudaEventCreateWithFlags(&fs.band_done[b], cudaEventDisableTiming));
                 SVLF_CUDA(cudaEventCreateWithFlags(&fs.band_copied[b], cudaEventDisableTiming));
             }
-            SVLF_CUDA(cudaMallocHost(&fs.h_ctr, 4 * (4 * svlf_ctx::kMaxBands + 8)));
+            SVLF_CUDA(cudaMallocHost(&fs.h_ctr, 4 * kCtrWords));
         }
         for (auto& ts : ctx->tslot) SVLF_CUDA(cudaEventCreateWithFlags(&ts.copied, cudaEventDisableTiming));
         ctx->misc.ensure<unsigned long long>(8);
@@ -766,6 +874,7 @@ svlf_status svlf_ctx_destroy(svlf_ctx* ctx) {
                     cudaEventDestroy(fs.band_copied[b]);
                 }
                 if (fs.h_stage) cudaFreeHost(fs.h_stage);
+                if (fs.h_tab) cudaFreeHost(fs.h_tab);
                 if (fs.h_ctr) cudaFreeHost(fs.h_ctr);
             }
             for (auto& ts : ctx->tslot) {

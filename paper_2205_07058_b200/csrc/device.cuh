@@ -147,6 +147,16 @@ void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const do
                       const double* hit_tout, HitOut hits, uint32_t n_rays, const float* bg3, float* rgb,
                       float* alpha, float* depth, unsigned long long* fg_count, bool exact, cudaStream_t s);
 
+// Sparse host-frame transfer: pixel blocks of 256 (kPackBlock); block j of the
+// band writes its foreground mask (rays with hits, 8 words) and the base of its
+// foreground pixels in tab[9j .. 9j+8], and the foreground pixels' (r, g, b,
+// alpha, depth) to vals[5 (base + rank)] (base from an atomic on *count, so the
+// block order in vals varies; the table makes the expansion deterministic).
+// Background pixels are (bg, 0, 0) exactly and are filled on the host.
+constexpr uint32_t kPackBlock = 256;
+void launch_pack_fg(const uint32_t* ray_cnt, uint32_t n, const float* rgb, const float* alpha, const float* depth,
+                    float* vals, uint32_t* tab, uint32_t* count, cudaStream_t s);
+
 // ---- tcgen05 decoder (decode_tc.cu)
 void ensure_pack_tc(const DevModel& M, const DevOctree& T, DevBuf& pack, uint64_t& pack_version, uint64_t version,
                     bool bf16, cudaStream_t s);

@@ -249,6 +249,51 @@ void launch_decode_f32(const DevOctree& T, const DevModel& M, const DecPackF32& 
     note_launch();
 }
 
+namespace {
+__global__ void __launch_bounds__(kPackBlock) k_pack_fg(const uint32_t* __restrict__ ray_cnt, uint32_t n,
+                                                        const float* __restrict__ rgb,
+                                                        const float* __restrict__ alpha,
+                                                        const float* __restrict__ depth, float* __restrict__ vals,
+                                                        uint32_t* __restrict__ tab, uint32_t* count) {
+    __shared__ uint32_t wmask[kPackBlock / 32], wbase[kPackBlock / 32 + 1];
+    const uint32_t p = blockIdx.x * kPackBlock + threadIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const bool fg = p < n && ray_cnt[p] > 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, fg);
+    if (lane == 0) wmask[warp] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (uint32_t w = 0; w < kPackBlock / 32; ++w) {
+            wbase[w] = t;
+            t += __popc(wmask[w]);
+        }
+        wbase[kPackBlock / 32] = t ? atomicAdd(count, t) : 0u;
+    }
+    __syncthreads();
+    if (threadIdx.x <= kPackBlock / 32)
+        tab[9 * size_t(blockIdx.x) + threadIdx.x] =
+            threadIdx.x < kPackBlock / 32 ? wmask[threadIdx.x] : wbase[kPackBlock / 32];
+    if (fg) {
+        const uint32_t k = wbase[kPackBlock / 32] + wbase[warp] + __popc(m & ((1u << lane) - 1u));
+        float* v = vals + 5 * size_t(k);
+        v[0] = rgb[3 * size_t(p)];
+        v[1] = rgb[3 * size_t(p) + 1];
+        v[2] = rgb[3 * size_t(p) + 2];
+        v[3] = alpha[p];
+        v[4] = depth[p];
+    }
+}
+}  // namespace
+
+void launch_pack_fg(const uint32_t* ray_cnt, uint32_t n, const float* rgb, const float* alpha, const float* depth,
+                    float* vals, uint32_t* tab, uint32_t* count, cudaStream_t s) {
+    static_assert(kPackBlock == 256, "8 mask words + base per table row");
+    if (n == 0) return;
+    k_pack_fg<<<(n + kPackBlock - 1) / kPackBlock, kPackBlock, 0, s>>>(ray_cnt, n, rgb, alpha, depth, vals, tab,
+                                                                       count);
+    note_launch();
+}
+
 void launch_composite(const uint32_t* ray_off, const uint32_t* ray_cnt, const double* hit_tin,
                       const double* hit_tout, HitOut hits, uint32_t n_rays, const float* bg3, float* rgb,
                       float* alpha, float* depth, unsigned long long* fg_count, bool exact, cudaStream_t s) {

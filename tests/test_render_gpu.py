@@ -279,23 +279,41 @@ def test_device_frame_submit_finish(precision):
     c.close()
 
 
-def test_host_frame_paths_agree(ctx, oracle):
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+@pytest.mark.parametrize("background", [None, (0.25, 0.5, 0.75)])
+def test_host_frame_paths_agree(ctx, oracle, precision, background):
     """svlf_render_frame delivers the same bits through every host path: fresh pageable
-    arrays (pinned staging + parallel copies), reused pageable buffers, and page-locked
-    buffers (direct per-band copies); frame large enough for several bands."""
+    arrays, reused pageable buffers and page-locked buffers, synchronous (several bands)
+    and submitted (one band) — and they are the bits of the device-buffer frame: the
+    sparse transfer (foreground pixels + block table, background filled on the host)
+    reproduces the composite's output exactly."""
+    import torch
+
     sc, pts, res, dil, cam, W, H = S.rtmv_workload(n_objects=4, n_views=8, view_res=96, res=64, width=1280)
     tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
     model = P.Model(tree, seed=1, ctx=ctx)
     camera = P.Camera.from_record(cam, W, H)
-    ref = [x.reshape(-1).copy() for x in P.render_frame(model, camera, precision="fp16")]
-    reuse = (np.full(3 * W * H, -1, np.float32), np.full(W * H, -1, np.float32), np.full(W * H, -1, np.float32))
+    n = W * H
+    dev = (torch.full((3 * n,), -1.0, device="cuda"), torch.full((n,), -1.0, device="cuda"),
+           torch.full((n,), -1.0, device="cuda"))
+    P.render_frame_device(model, camera, *(x.data_ptr() for x in dev), background=background, precision=precision)
+    torch.cuda.synchronize()
+    ref = [x.cpu().numpy() for x in dev]
+    got = [x.reshape(-1).copy() for x in P.render_frame(model, camera, background=background, precision=precision)]
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+    reuse = (np.full(3 * n, -1, np.float32), np.full(n, -1, np.float32), np.full(n, -1, np.float32))
     pinned = P.pinned_frame(W, H)
     for out in (reuse, pinned):
         for _ in range(2):
-            P.render_frame(model, camera, precision="fp16", out=out)
+            P.render_frame(model, camera, background=background, precision=precision, out=out)
             for a, b in zip(out, ref):
                 assert np.array_equal(a, b)
+        P.render_frame_submit(model, camera, out, background=background, precision=precision).wait()
+        for a, b in zip(out, ref):
+            assert np.array_equal(a, b)
     assert ref[1].max() > 0.5  # the frame is not empty
+    assert (ref[1] == 0).mean() > 0.3  # and has background
 
 
 def test_pipelined_frames(ctx, oracle):
