@@ -156,7 +156,7 @@ def stage_rooflines(stage, hits, n, peaks, node_tests=None):
         gbs = (24 * hits + 8 * n) / (trav_ms * 1e-3) / 1e9
         out["traversal"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                             "frac": round(gbs / hbm, 5), "ms": round(trav_ms, 4),
-                            "note": "fp64 / latency-bound (see profiles/r2c_render.md)"}
+                            "note": "fp64 / latency-bound (see profiles/r2d_render.md)"}
         if node_tests:  # secondary figure: ray-box tests, the reference's ray_aabb calls
             out["traversal"]["node_tests_per_ray"] = round(node_tests / n, 2)
             out["traversal"]["node_tests_per_s"] = round(node_tests / (trav_ms * 1e-3) / 1e9, 2)
@@ -172,7 +172,7 @@ def stage_rooflines(stage, hits, n, peaks, node_tests=None):
     return out
 
 
-def ncu_traffic(prefix, path=os.path.join(ROOT, "profiles", "r2c_render.json")):
+def ncu_traffic(prefix, path=os.path.join(ROOT, "profiles", "r2d_render.json")):
     """DRAM bytes (read + write) per launch of the kernels named prefix*, from the
     committed ncu summary (profiles/summarize.py); None if absent."""
     try:
@@ -534,8 +534,8 @@ def bench_c2_dense(P, torch, device, stream, ctx, steps, precision, dist=None, w
             "foreground_fraction": round(st.rays_with_hits / steps / n, 4), "stages_ms": stage,
             "decode_roofline": {"bound": "tensor", "achieved": round(tf, 2), "peak": peak, "unit": "TFLOP/s",
                                 "frac": round(tf / peak, 4),
-                                "traffic": ncu_traffic("k_decode", os.path.join(ROOT, "profiles", "r2c_render20.json")),
-                                "traffic_source": "profiles/r2c_render20.json"}, "precision": precision}
+                                "traffic": ncu_traffic("k_decode", os.path.join(ROOT, "profiles", "r2d_render20.json")),
+                                "traffic_source": "profiles/r2d_render20.json"}, "precision": precision}
 
 
 def bench_c5(P, torch, device, stream, ctx, steps, dist=None, world=1, rank=0):
@@ -837,7 +837,7 @@ def main():
         "roofline": {"bound": "tensor", "kernel": f"decode_{precision}", "achieved": round(achieved_tflops, 3),
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved_tflops / peak, 5),
                      "traffic": ncu_traffic("k_decode"), "traffic_unit": "bytes per launch (decode_t + decode_c)",
-                     "traffic_source": "profiles/r2c_render.json (ncu --set full --clock-control none)",
+                     "traffic_source": "profiles/r2d_render.json (ncu --set full --clock-control none)",
                      "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)",
                      "algorithmic": f"{FLOP_PER_HIT} FLOP/hit x {int(hits)} hits per launch"},
         "stage_rooflines": stage_rooflines(stage, hits, n, peaks, node_tests),
