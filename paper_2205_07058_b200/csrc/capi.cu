@@ -645,6 +645,22 @@ void frame_submit(svlf_ctx* ctx, FrameSlot& F, uint32_t bands) {
     F.nb = nb;
 }
 
+// The context's host worker pool (sparse frame expansion, pageable-batch
+// staging): $SVLF_HOST_THREADS threads, else this process's share of the host
+// threads (hardware threads / $LOCAL_WORLD_SIZE, at most 16): the sparse
+// expansion writes the whole frame (51 MB on C2) while the GPU renders the
+// next one (8 threads: 0.70 ms per C2 frame, 16: 0.43 ms).
+std::unique_ptr<HostPool>& host_pool(std::unique_ptr<HostPool>& p) {
+    if (!p) {
+        const char* e = std::getenv("SVLF_HOST_THREADS");
+        const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+        const int hw = int(std::thread::hardware_concurrency());
+        const int share = hw / std::max(1, lw ? std::atoi(lw) : 1);
+        p = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(share - 1, 0, 15));
+    }
+    return p;
+}
+
 // Sparse transfer, host side, one band (as soon as its copies landed, while
 // later bands render): copies the foreground pixels the submit did not (more
 // than the estimate), then writes the band into the caller's buffers from the
@@ -693,13 +709,7 @@ void frame_expand_band(svlf_ctx* ctx, FrameSlot& F, uint32_t b) {
 // Returns false when the frame has to be redone (hit buffers overflowed).
 bool frame_complete(svlf_ctx* ctx, FrameSlot& F, svlf_render_stats* stats) {
     const uint32_t W = F.cam.width, H = F.cam.height, n = F.n;
-    if ((!F.direct || F.sparse) && !ctx->pool) {
-        const char* e = std::getenv("SVLF_COPY_THREADS");
-        const int hw = int(std::thread::hardware_concurrency());
-        // all host threads: the sparse expansion writes the whole frame (51 MB on C2) while the
-        // GPU renders the next one (8 threads: 0.70 ms per C2 frame, 16: 0.43 ms)
-        ctx->pool = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 15));
-    }
+    if (!F.direct || F.sparse) host_pool(ctx->pool);
     const float* st_rgb = F.h_stage;
     const float* st_alpha = st_rgb + size_t(n) * 3;
     const float* st_depth = st_alpha + n;
@@ -1844,14 +1854,6 @@ extern "C" {
 // ---- train --------------------------------------------------------------------
 namespace {
 
-std::unique_ptr<HostPool>& host_pool(std::unique_ptr<HostPool>& p) {
-    if (!p) {
-        const char* e = std::getenv("SVLF_HOST_THREADS");
-        const int hw = int(std::thread::hardware_concurrency());
-        p = std::make_unique<HostPool>(e ? std::max(0, std::atoi(e) - 1) : std::clamp(hw - 1, 0, 7));
-    }
-    return p;
-}
 
 // A host train batch (rays, c_gt, depth_gt, alpha_gt) and its device destinations.
 struct HostBatch {
