@@ -335,7 +335,7 @@ def bench_train(P, torch, device, stream, ctx, steps, warmup, cpu=True, dist=Non
         pipe.stage(*host)
         pipe.step(mode="volumetric", lr=2e-4)
     pipe.drain()
-    k_e2e = max(10, steps)
+    k_e2e = max(30, steps)  # steps per timed loop (the upload pipeline fills and drains once per loop)
     loops = []
     for _ in range(3):  # three timed loops of k_e2e steps; the median loop is reported
         barrier(dist)
@@ -747,7 +747,7 @@ def main():
     # is reported beside it.
     frames = [P.pinned_frame(W, H), P.pinned_frame(W, H)]
     P.render_frame_submit(model, camera, frames[0], precision=precision).wait()
-    k_e2e = max(10, args.steps)
+    k_e2e = max(30, args.steps)  # frames per timed loop (the pipeline fills and drains once per loop)
 
     def pipe_loops(with_flush):
         out = []
