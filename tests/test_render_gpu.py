@@ -316,6 +316,41 @@ def test_host_frame_paths_agree(ctx, oracle, precision, background):
     assert (ref[1] == 0).mean() > 0.3  # and has background
 
 
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+def test_sparse_frame_estimate_exceeded(ctx, precision):
+    """Sparse host frames copy as many foreground pixels as the previous frame of the band had
+    (+1/8); a frame with far more foreground (the camera moved closer) takes the completion's
+    extra copy. Every frame equals the device-buffer frame bit for bit, synchronous (several
+    bands) and submitted (one band)."""
+    import torch
+
+    pts = S.random_occupancy_points(32, 0.3, 5)
+    tree = P.SparseOctree.build(pts, P.GridConfig(32, dilation=0), ctx)
+    model = P.Model(tree, seed=2, ctx=ctx)
+    W = 1024  # several bands in the synchronous path
+    n = W * W
+    dev = (torch.empty(3 * n, device="cuda"), torch.empty(n, device="cuda"), torch.empty(n, device="cuda"))
+    fgs = []
+    for dist in (6.0, 1.8, 6.0, 1.5):  # far (little foreground), near (mostly foreground), ...
+        cam = S.lookat_camera((0.5 + dist * 0.6, 0.5 + dist * 0.3, 0.5 + dist * 0.7416), (0.5, 0.5, 0.5), W, W,
+                              1.2 * W)
+        camera = P.Camera.from_record(cam, W, W)
+        st = P.RenderStats()
+        P.render_frame_device(model, camera, *(x.data_ptr() for x in dev), stats=st, background=(0.1, 0.2, 0.3),
+                              precision=precision)
+        torch.cuda.synchronize()
+        ref = [x.cpu().numpy() for x in dev]
+        fgs.append(st.rays_with_hits)
+        got = P.render_frame(model, camera, background=(0.1, 0.2, 0.3), precision=precision)
+        for a, b in zip(got, ref):
+            assert np.array_equal(a.reshape(-1), b)
+        out = P.pinned_frame(W, W)
+        P.render_frame_submit(model, camera, out, background=(0.1, 0.2, 0.3), precision=precision).wait()
+        for a, b in zip(out, ref):
+            assert np.array_equal(a.reshape(-1), b)
+    assert fgs[1] > 2 * fgs[0] and fgs[1] > n // 4  # the near frames exceed the far frames' estimate
+
+
 def test_pipelined_frames(ctx, oracle):
     """render_frame_submit / wait: two frames in flight give the same bits and statistics as
     synchronous render_frame calls; a third submit is refused until a wait."""
