@@ -666,6 +666,16 @@ def main():
     t_gen = time.perf_counter()
     pts, res, dil, cam, W, H = workload(args.objects, ctx)
     t_gen = time.perf_counter() - t_gen
+    if world > 1 and rank > 0:  # each rank its own view: the C2 camera rotated 360 deg * rank / N about z
+        import math
+
+        import paper_2205_07058_b200.synthetic as S
+
+        a = 2.0 * math.pi * rank / world
+        d = S.C1_EYE_DIR
+        eye = (0.5 + 1.8 * (d[0] * math.cos(a) - d[1] * math.sin(a)),
+               0.5 + 1.8 * (d[0] * math.sin(a) + d[1] * math.cos(a)), 0.5 + 1.8 * d[2])
+        cam = S.lookat_camera(eye, (0.5, 0.5, 0.5), W, H, 1.5 * W)
     stream = torch.cuda.Stream(device)
     ctx.set_stream(stream.cuda_stream)
     tree = P.SparseOctree.build(pts, P.GridConfig(res, dilation=dil), ctx)
@@ -830,7 +840,8 @@ def main():
                    "leaves": int(tree.leaf_count), "vertices": int(tree.vertex_count),
                    "hits_per_ray": round(hits / n, 4),
                    "foreground_fraction": round(stats.rays_with_hits / args.steps / n, 4),
-                   "precision": precision, "parallelism": f"replicated octree, {world} rank(s), one frame each",
+                   "precision": precision, "parallelism": f"replicated octree, {world} rank(s), one frame each" +
+                                  (" (rank r: the C2 camera rotated 360 deg * r / N about z)" if world > 1 else ""),
                    "l2": f"flushed ({flush.numel() >> 20} MiB write, 1.25x L2) between timed steps",
                    "input_gen_seconds": round(t_gen, 1)},
         "stages_ms": stage,
