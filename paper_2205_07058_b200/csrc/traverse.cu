@@ -43,6 +43,9 @@ constexpr double kMinHitSpan = 1e-12;  // tie rule, src/octree.cpp:16
 #ifndef SVLF_BFS_PARTIAL
 #define SVLF_BFS_PARTIAL 1  // queue overflow hands only the rays reaching the overflowing chunk to the next pass
 #endif
+#ifndef SVLF_BFS_EMPTY_EXIT
+#define SVLF_BFS_EMPTY_EXIT 1  // tiles whose pairs all die before the leaf level skip the segment scan and sort
+#endif
 
 // Slab intervals of the two halves of a node along each axis.
 struct NodeSplit {
@@ -631,6 +634,16 @@ __device__ __forceinline__ void bfs_tile(const DevOctree& T, const DevCamera& ca
     // Pairs are grouped by ray in order, so the pair scan is also the per-ray
     // segment layout; each ray's segment is then sorted in place.
     const bool leaf_pass = level + 1 == T.L && n_cur > 0;
+#if SVLF_BFS_EMPTY_EXIT
+    if (!leaf_pass) {  // no (ray, node) pair reached the leaf level: every ray of the tile has no hits
+        if (tid < kR && S.gray[tid] != 0xffffffffu) {
+            A.ray_off[S.gray[tid]] = 0;  // (what the segment scan gives a tile without hits)
+            A.ray_cnt[S.gray[tid]] = 0;
+        }
+        if constexpr (kCount) tests_done += tests;
+        return;
+    }
+#endif
     uint32_t total = 0;
     if (leaf_pass) {
         for (uint32_t base = 0; base < n_cur; base += kT) {
