@@ -170,7 +170,10 @@ __global__ void __launch_bounds__(128) k_composite(const uint32_t* __restrict__ 
 // hit loads); the five sums of each ray land in a per-warp shared table (one
 // store by the five lanes holding them) and every lane writes its own ray's
 // pixel at the end. One foreground-count atomic per block.
-constexpr int kCompBlock = 256;
+#ifndef SVLF_COMP_BLOCK
+#define SVLF_COMP_BLOCK 128  // (64 / 128 / 256 / 512 measured: 128 best by ~1-2 %)
+#endif
+constexpr int kCompBlock = SVLF_COMP_BLOCK;
 __global__ void __launch_bounds__(kCompBlock) k_composite_warp(HitOut h, uint32_t n, PixelOut P,
                                                                unsigned long long* fg_count) {
     __shared__ float sums[kCompBlock / 32][32][5];
